@@ -1,0 +1,224 @@
+/*
+ * quadsim_b200 — C ABI of the B200-native quadsim hot path.
+ *
+ * The reference (DiffAero re-implemented as the numpy package `quadsim`,
+ * /root/reference/pkg/src/quadsim, cited below as q/) has NO native FFI: its
+ * boundary is the Python env API.  Each entry point below replaces the
+ * reference function named in its comment; the Python package
+ * `paper_2509_10247_b200` binds them with ctypes.
+ *
+ * Rules shared by every entry point:
+ *   - every pointer is a caller-owned, contiguous device buffer (fp32 unless
+ *     stated), laid out as documented in DESIGN.md §3;
+ *   - nothing allocates and nothing synchronises the host; work is enqueued
+ *     on `stream` (a cudaStream_t passed as void*), so every call is
+ *     CUDA-graph capturable;
+ *   - the return value is a launch status (QS_OK or QS_ERR_*); data-dependent
+ *     contract violations (non-finite action/state, failed reset sampling)
+ *     are reported through the device error word `err` (int32[2] = {code,
+ *     first offending row}, codes QS_ERR_*), read lazily by the host.
+ */
+#ifndef QUADSIM_B200_H
+#define QUADSIM_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QS_ABI_VERSION 1
+
+/* status / device error codes (map to the reference's exceptions) */
+#define QS_OK 0
+#define QS_ERR_NONFINITE_ACTION 1 /* tk.TaskContractError  q/tasks.py:555-558 */
+#define QS_ERR_NONFINITE_STATE 2  /* dyn.ContractError     q/dynamics.py:130-133 */
+#define QS_ERR_GENERATION 3       /* wd.GenerationError    q/world.py:251,340,448 */
+#define QS_ERR_BAD_ARGUMENT 4     /* shape / enum errors */
+#define QS_ERR_LAUNCH 5           /* cudaGetLastError after launch */
+
+/* dynamics models  (q/dynamics.py:34) */
+#define QS_MODEL_FULL 0
+#define QS_MODEL_PM_CONTINUOUS 1
+#define QS_MODEL_PM_DISCRETE 2
+
+/* tasks (q/tasks.py:30) */
+#define QS_TASK_POSITION 0
+#define QS_TASK_AVOIDANCE 1
+#define QS_TASK_RACING 2
+
+#define QS_MAX_AGENTS 8
+#define QS_MAX_GATES 16
+
+/* Reward weights, q/tasks.py:37-54 (RewardWeights). */
+typedef struct qs_weights {
+  float w_p, w_v, w_a, w_s, w_t, w_o, w_f, w_g;
+  float near_radius, near_width, track_gain, v_max, sdf_sharpness;
+  float gate_pass_bonus, gate_crash_penalty, goal_bonus;
+} qs_weights;
+
+/* Everything constant over a rollout: TaskConfig (q/tasks.py:67-106) +
+ * QuadParams (q/dynamics.py:42-82) + RandomizationSpec (q/world.py:114-127)
+ * + the IMU spec (q/sensors.py:508-530). */
+typedef struct qs_task_cfg {
+  int32_t model, task;
+  int32_t n_envs;      /* local envs on this rank */
+  int32_t n_agents;    /* rows per env; row = env * n_agents + agent */
+  int32_t episode_len, action_dim, proprio_dim, n_gates;
+  int64_t env_offset;  /* global id of local env 0 (sharding; RNG keys) */
+  uint64_t seed;
+  float dt, success_radius, hover_speed, collision_radius, d_min, d_safe;
+  float yaw_ema_alpha, obs_clip, goal_dist;
+  float g[3], drag_diag[3], rate_gains[3];
+  float drag_coeff, lag_decay;          /* scalar params (no randomization) */
+  float act_lo[4], act_hi[4];           /* model action box (q/dynamics.py:342-425) */
+  float formation[QS_MAX_AGENTS][3];    /* template (q/world.py:386-406) */
+  float form_ref[QS_MAX_AGENTS][QS_MAX_AGENTS]; /* |f_i - f_j| (q/tasks.py:188) */
+  qs_weights w, w_rl;
+  int32_t dr_enabled, dr_per_episode;
+  float dr_drag[2], dr_latency[2], dr_scale[2];
+  int32_t imu_enabled;
+  float imu_accel_std, imu_gyro_std, imu_accel_rw, imu_gyro_rw;
+  int32_t reset_mode;   /* 0: in-kernel Philox resets; 1: deferred (injected) */
+  int32_t want_cam;     /* write camera yaw (cos,sin) per row for rendering */
+} qs_task_cfg;
+
+/* Per-env scene data (read-only during a rollout).  Obstacles are packed
+ * valid-first per env: counts[e] = {n_sph, n_box, n_cyl, has_ground}. */
+typedef struct qs_scene {
+  const float* bounds;      /* (E,2,4) scene bounds lo, hi (without the 1e-6 shrink) */
+  const float* spawn_goal;  /* (E,2,4) scene.spawn, scene.goal */
+  const float* spheres;     /* (E,Sm,4)  cx cy cz r */
+  const float* boxes;       /* (E,Bm,8)  cx cy cz _ hx hy hz _ */
+  const float* cylinders;   /* (E,Cm,8)  cx cy cz r hh _ _ _ */
+  const int32_t* counts;    /* (E,4) */
+  const float* ground_z;    /* (E,)  */
+  const float* gates;       /* (E,G,8)  cx cy cz inner nx ny nz frame */
+  int32_t Sm, Bm, Cm;
+} qs_scene;
+
+/* Mutable per-env / per-row buffers.  `*_in` are read, `*_out` written
+ * (functional update: the *_in buffers are what the backward replays). */
+typedef struct qs_step_io {
+  /* differentiable state + v_ema in the pad lanes: (NP,N,4), NP = 3 (pm) or 4 (full) */
+  const float* S_in;  float* S_out;
+  const float* raw;                     /* (N,A) raw (pre-squash) action */
+  const float* goal_in; float* goal_out;  /* (N,4) */
+  const float* peff_in; float* peff_out;  /* (N,4) previous effort */
+  const float* dr_in;   float* dr_out;    /* (N,4) drag, lag_decay, action scale, latency | NULL */
+  int32_t* meta;        /* (E,4) steps_in_episode, episode index, tick, next_gate (in place) */
+  float* ep_return;     /* (E,) (in place) */
+  float* imu_bias;      /* (N,8) accel bias, gyro bias (in place) | NULL */
+  const float* imu_noise; /* (4,N,3) injected normals (ba, bg, na, ng) | NULL = Philox */
+  float* imu_out;       /* (N,6) accel xyz, gyro xyz | NULL */
+  float* obs;           /* (N,P) proprio */
+  float* r_ctrl; float* r_goal; float* r_rl;  /* (N,) */
+  int8_t* terminated; uint8_t* truncated;     /* (N,) */
+  int32_t* flags;       /* (N,) record for the backward: bit0 done, clamp masks, sdf argmin */
+  float* cam;           /* (N,2) cos/sin of camera yaw | NULL */
+  double* stats;        /* (4,) finished, successes, collisions, finished_return (atomic) */
+  int32_t* err;         /* (2,) code, first row */
+} qs_step_io;
+
+typedef struct qs_step_grad {
+  const float* S_in; const float* raw; const float* goal_in; const float* peff_in;
+  const float* dr_in; const int32_t* flags;
+  const float* g_S_out;   /* (NP,N,4) | NULL */
+  const float* g_obs;     /* (N,P) | NULL */
+  const float* g_rctrl;   /* (N,) | NULL */
+  float* g_S_in;          /* (NP,N,4) */
+  float* g_raw;           /* (N,A) */
+} qs_step_grad;
+
+/* Reset table for deferred/injected resets: rows of the done envs only need
+ * valid data; layout (N,4) each.  dr may be NULL. */
+typedef struct qs_reset_table {
+  const uint8_t* env_mask;  /* (E,) 1 = respawn this env */
+  const float* p; const float* v; const float* goal; const float* v_ema;
+  const float* dr;          /* (N,4) drag, lag_decay, scale, latency | NULL */
+  const int32_t* next_gate; /* (E,) | NULL */
+} qs_reset_table;
+
+int qs_abi_version(void);
+int qs_proprio_dim(int32_t model, int32_t task);
+int qs_state_planes(int32_t model);
+
+/* FlightTask.step (q/tasks.py:549-600): squash -> yaw frame -> dynamics ->
+ * EMA -> rewards -> termination -> auto-reset -> observe, fused per env. */
+int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
+                     void* stream);
+/* Analytic VJP of qs_task_step_fwd (replaces the tape backward of the ops
+ * recorded by FlightTask.step; subgradients per q/autodiff.py). */
+int qs_task_step_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_grad* g,
+                     void* stream);
+/* _spawn_all (q/tasks.py:687-721, 789-815, 873-902) + _redraw_randomization
+ * (:377-387) for masked envs, writing into io->S_out/goal_out/peff_out/dr_out
+ * in place; table==NULL -> in-kernel Philox sampling. */
+int qs_task_spawn(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
+                  const uint8_t* env_mask, const qs_reset_table* table, void* stream);
+/* FlightTask.observe proprio (q/tasks.py:415-442, racing :904-915) of io->S_out. */
+int qs_task_observe(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
+                    void* stream);
+
+/* ---- sensing (q/sensors.py) ---- */
+typedef struct qs_ray_cfg {
+  int32_t kind;        /* 0 camera (frustum cull), 1 lidar (range-ball cull), 2 generic rays */
+  int32_t n_rays;      /* rays per env */
+  int32_t cull;
+  float max_range;
+  float tan_h, tan_v;  /* camera half-FOV tangents (cull planes) */
+  float offset[3];     /* sensor offset in the body frame */
+  int32_t n_agents;    /* rows per env (obstacles are per env) */
+} qs_ray_cfg;
+
+/* render_depth / render_lidar / raycast (q/sensors.py:245-269, 377-410):
+ * rows (N), origin = pos + Rz(yaw) offset, dir = Rz(yaw) dirs_body[r]
+ * (or dirs_world (N,R,4) for kind 2).  out (N,R) fp32 distances, hit (N,R)
+ * u8 | NULL.  dT_dO (N,R,4) | NULL: analytic d t / d origin (opt-in depth VJP). */
+int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
+               int32_t pos_stride, const float* cam_cs, const float* dirs_body,
+               const float* dirs_world, float* out, uint8_t* hit, float* dT_dO, void* stream);
+/* d loss / d pos = sum_r g_depth[r] * dT_dO[r]  (N,3) accumulate into g_pos (N,4 stride pos_stride). */
+int qs_raycast_vjp(int32_t n_rows, int32_t n_rays, const float* g_depth, const float* dT_dO,
+                   float* g_pos, int32_t pos_stride, void* stream);
+
+/* sdf_np / sdf_var (q/sensors.py:417-501): points (N,4); out (N,); grad (N,4) | NULL */
+int qs_sdf(const qs_scene* scene, int32_t n_rows, int32_t n_agents, const float* pts, float* out,
+           float* grad, void* stream);
+
+/* ImuModel.read (q/sensors.py:540-555), batch rows: R (N,9) row-major body->world,
+ * w (N,4) | NULL, vdot (N,4).  noise (4,N,3) injected | NULL (Philox keyed by
+ * seed,row,tick).  bias (N,8) in place; out (N,6). */
+int qs_imu_read(int32_t n_rows, const float* R, const float* w, const float* vdot, const float* g,
+                float dt, float sa, float sg, float ra, float rg, uint64_t seed, int64_t tick,
+                const float* noise, float* bias, float* out, void* stream);
+
+/* DynamicsModel.step (q/dynamics.py:140-274) on squashed world-frame commands,
+ * state planes (NP,N,4) -> (NP,N,4); per-row drag/decay (N,4) | NULL. */
+int qs_dyn_step_fwd(int32_t model, int32_t n, const float* S_in, const float* act,
+                    const float* dr, const qs_task_cfg* cfg, float* S_out, int32_t* err,
+                    void* stream);
+int qs_dyn_step_bwd(int32_t model, int32_t n, const float* S_in, const float* act,
+                    const float* dr, const qs_task_cfg* cfg, const float* g_S_out, float* g_S_in,
+                    float* g_act, void* stream);
+
+/* reconstruct_attitude (q/sensors.py:569-606): a (N,4), v_ema (N,4) -> R (N,9). */
+int qs_reconstruct_attitude(int32_t n, const float* a, const float* v_ema, float* R, void* stream);
+
+/* In-kernel obstacle-course generation with BFS feasibility
+ * (q/world.py:207-340), Philox keyed by (seed, global env id, attempt). */
+typedef struct qs_gen_cfg {
+  float spawn[3], goal[3];
+  float density, r_quad, clearance, corridor_halfwidth;
+  int32_t indoor, max_attempts, Sm, Bm, Cm;
+  uint64_t seed;
+  int64_t env_offset;
+} qs_gen_cfg;
+int qs_gen_obstacle_course(const qs_gen_cfg* cfg, int32_t n_envs, float* bounds, float* spawn_goal,
+                           float* spheres, float* boxes, float* cylinders, int32_t* counts,
+                           float* ground_z, int32_t* err, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUADSIM_B200_H */

@@ -1,0 +1,161 @@
+"""ctypes binding of the C ABI in ``include/quadsim_b200.h``.
+
+There is no fallback: if ``libquadsim_b200.so`` is missing or CUDA is not
+available the calls raise.  Structures mirror the header field for field.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libquadsim_b200.so")
+
+QS_OK = 0
+QS_ERR_NONFINITE_ACTION = 1
+QS_ERR_NONFINITE_STATE = 2
+QS_ERR_GENERATION = 3
+QS_ERR_BAD_ARGUMENT = 4
+QS_ERR_LAUNCH = 5
+
+MODEL_IDS = {"full": 0, "pm_continuous": 1, "pm_discrete": 2}
+TASK_IDS = {"position": 0, "avoidance": 1, "racing": 2}
+MAX_AGENTS = 8
+MAX_GATES = 16
+
+f32, i32, i64, u64, vp = C.c_float, C.c_int32, C.c_int64, C.c_uint64, C.c_void_p
+
+
+class QsWeights(C.Structure):
+    _fields_ = [(n, f32) for n in (
+        "w_p", "w_v", "w_a", "w_s", "w_t", "w_o", "w_f", "w_g", "near_radius", "near_width",
+        "track_gain", "v_max", "sdf_sharpness", "gate_pass_bonus", "gate_crash_penalty", "goal_bonus")]
+
+
+class QsTaskCfg(C.Structure):
+    _fields_ = [
+        ("model", i32), ("task", i32), ("n_envs", i32), ("n_agents", i32),
+        ("episode_len", i32), ("action_dim", i32), ("proprio_dim", i32), ("n_gates", i32),
+        ("env_offset", i64), ("seed", u64),
+        ("dt", f32), ("success_radius", f32), ("hover_speed", f32), ("collision_radius", f32),
+        ("d_min", f32), ("d_safe", f32), ("yaw_ema_alpha", f32), ("obs_clip", f32), ("goal_dist", f32),
+        ("g", f32 * 3), ("drag_diag", f32 * 3), ("rate_gains", f32 * 3),
+        ("drag_coeff", f32), ("lag_decay", f32),
+        ("act_lo", f32 * 4), ("act_hi", f32 * 4),
+        ("formation", (f32 * 3) * MAX_AGENTS), ("form_ref", (f32 * MAX_AGENTS) * MAX_AGENTS),
+        ("w", QsWeights), ("w_rl", QsWeights),
+        ("dr_enabled", i32), ("dr_per_episode", i32),
+        ("dr_drag", f32 * 2), ("dr_latency", f32 * 2), ("dr_scale", f32 * 2),
+        ("imu_enabled", i32), ("imu_accel_std", f32), ("imu_gyro_std", f32), ("imu_accel_rw", f32),
+        ("imu_gyro_rw", f32),
+        ("reset_mode", i32), ("want_cam", i32),
+    ]
+
+
+class QsScene(C.Structure):
+    _fields_ = [("bounds", vp), ("spawn_goal", vp), ("spheres", vp), ("boxes", vp),
+                ("cylinders", vp), ("counts", vp), ("ground_z", vp), ("gates", vp),
+                ("Sm", i32), ("Bm", i32), ("Cm", i32)]
+
+
+class QsStepIo(C.Structure):
+    _fields_ = [(n, vp) for n in (
+        "S_in", "S_out", "raw", "goal_in", "goal_out", "peff_in", "peff_out", "dr_in", "dr_out",
+        "meta", "ep_return", "imu_bias", "imu_noise", "imu_out", "obs", "r_ctrl", "r_goal", "r_rl",
+        "terminated", "truncated", "flags", "cam", "stats", "err")]
+
+
+class QsStepGrad(C.Structure):
+    _fields_ = [(n, vp) for n in (
+        "S_in", "raw", "goal_in", "peff_in", "dr_in", "flags", "g_S_out", "g_obs", "g_rctrl",
+        "g_S_in", "g_raw")]
+
+
+class QsResetTable(C.Structure):
+    _fields_ = [(n, vp) for n in ("env_mask", "p", "v", "goal", "v_ema", "dr", "next_gate")]
+
+
+class QsRayCfg(C.Structure):
+    _fields_ = [("kind", i32), ("n_rays", i32), ("cull", i32), ("max_range", f32), ("tan_h", f32),
+                ("tan_v", f32), ("offset", f32 * 3), ("n_agents", i32)]
+
+
+class QsGenCfg(C.Structure):
+    _fields_ = [("spawn", f32 * 3), ("goal", f32 * 3), ("density", f32), ("r_quad", f32),
+                ("clearance", f32), ("corridor_halfwidth", f32), ("indoor", i32),
+                ("max_attempts", i32), ("Sm", i32), ("Bm", i32), ("Cm", i32), ("seed", u64),
+                ("env_offset", i64)]
+
+
+P = C.POINTER
+_SIGS = {
+    "qs_abi_version": ([], i32),
+    "qs_proprio_dim": ([i32, i32], i32),
+    "qs_state_planes": ([i32], i32),
+    "qs_task_step_fwd": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp], i32),
+    "qs_task_step_bwd": ([P(QsTaskCfg), P(QsScene), P(QsStepGrad), vp], i32),
+    "qs_task_spawn": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp, P(QsResetTable), vp], i32),
+    "qs_task_observe": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp], i32),
+    "qs_raycast": ([P(QsRayCfg), P(QsScene), i32, vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
+    "qs_raycast_vjp": ([i32, i32, vp, vp, vp, i32, vp], i32),
+    "qs_sdf": ([P(QsScene), i32, i32, vp, vp, vp, vp], i32),
+    "qs_imu_read": ([i32, vp, vp, vp, vp, f32, f32, f32, f32, f32, u64, i64, vp, vp, vp, vp], i32),
+    "qs_dyn_step_fwd": ([i32, i32, vp, vp, vp, P(QsTaskCfg), vp, vp, vp], i32),
+    "qs_dyn_step_bwd": ([i32, i32, vp, vp, vp, P(QsTaskCfg), vp, vp, vp, vp], i32),
+    "qs_reconstruct_attitude": ([i32, vp, vp, vp, vp], i32),
+    "qs_gen_obstacle_course": ([P(QsGenCfg), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+}
+
+_lib = None
+
+
+class QuadsimLibraryError(RuntimeError):
+    pass
+
+
+def lib():
+    """The loaded CUDA library (raises when it is missing: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise QuadsimLibraryError(
+                f"{LIB_PATH} is missing; build it with `python -m paper_2509_10247_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle(device=None):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def check(status: int, what: str):
+    if status != QS_OK:
+        raise QuadsimLibraryError(f"{what} failed with status {status}")
+
+
+def require_cuda(device) -> torch.device:
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device()) \
+        if torch.cuda.is_available() else None
+    if dev is None or dev.type != "cuda" or not torch.cuda.is_available():
+        raise QuadsimLibraryError("quadsim_b200 runs only on a CUDA device (B200, sm_100a); "
+                                  "no CPU fallback exists")
+    return dev

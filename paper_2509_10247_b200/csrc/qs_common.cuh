@@ -1,0 +1,148 @@
+// Shared device helpers: small-vector math, Philox4x32-10, error word.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/quadsim_b200.h"
+
+#define QS_HD __host__ __device__ __forceinline__
+#define QS_D __device__ __forceinline__
+
+struct V3 {
+  float x, y, z;
+};
+
+QS_HD V3 v3(float x, float y, float z) { return V3{x, y, z}; }
+QS_HD V3 operator+(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+QS_HD V3 operator-(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+QS_HD V3 operator-(V3 a) { return v3(-a.x, -a.y, -a.z); }
+QS_HD V3 operator*(V3 a, float s) { return v3(a.x * s, a.y * s, a.z * s); }
+QS_HD V3 operator*(float s, V3 a) { return v3(a.x * s, a.y * s, a.z * s); }
+QS_HD V3 hmul(V3 a, V3 b) { return v3(a.x * b.x, a.y * b.y, a.z * b.z); }
+QS_HD float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+QS_HD V3 cross(V3 a, V3 b) {
+  return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+QS_HD float norm3(V3 a) { return sqrtf(dot(a, a)); }
+QS_HD V3& operator+=(V3& a, V3 b) {
+  a.x += b.x; a.y += b.y; a.z += b.z;
+  return a;
+}
+QS_HD V3& operator-=(V3& a, V3 b) {
+  a.x -= b.x; a.y -= b.y; a.z -= b.z;
+  return a;
+}
+QS_HD V3 xyz(float4 f) { return v3(f.x, f.y, f.z); }
+QS_HD float4 f4(V3 a, float w) { return make_float4(a.x, a.y, a.z, w); }
+QS_HD bool finite3(V3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z); }
+
+// norm VJP with the reference's convention: zero vector -> zero gradient
+// (q/autodiff.py:580-591)
+QS_HD V3 norm_vjp(V3 a, float n, float g) {
+  return n > 0.f ? a * (g / n) : v3(0.f, 0.f, 0.f);
+}
+
+struct Q4 {
+  float w, x, y, z;
+};
+QS_HD Q4 q4(float w, float x, float y, float z) { return Q4{w, x, y, z}; }
+QS_HD Q4 qmul(Q4 q, Q4 r) {  // q/autodiff.py:689-701
+  return q4(q.w * r.w - q.x * r.x - q.y * r.y - q.z * r.z,
+            q.w * r.x + q.x * r.w + q.y * r.z - q.z * r.y,
+            q.w * r.y - q.x * r.z + q.y * r.w + q.z * r.x,
+            q.w * r.z + q.x * r.y - q.y * r.x + q.z * r.w);
+}
+QS_HD Q4 qconj(Q4 q) { return q4(q.w, -q.x, -q.y, -q.z); }
+QS_HD V3 qvec(Q4 q) { return v3(q.x, q.y, q.z); }
+// v + 2 (w (u x v) + u x (u x v))   (q/autodiff.py:737-750)
+QS_HD V3 qrot(Q4 q, V3 v) {
+  V3 u = qvec(q);
+  V3 uv = cross(u, v);
+  V3 uuv = cross(u, uv);
+  return v + (uv * q.w + uuv) * 2.f;
+}
+// VJP of qrot wrt v: exact transpose of the formula (== qrot(conj q, g))
+QS_HD V3 qrot_vjp_v(Q4 q, V3 g) { return qrot(qconj(q), g); }
+// VJP of qrot wrt q (w, u):  g_w = 2 g.(u x v);
+// g_u = 2w (v x g) + 2 (u.v) g + 2 (g.u) v - 4 (g.v) u
+QS_HD Q4 qrot_vjp_q(Q4 q, V3 v, V3 g) {
+  V3 u = qvec(q);
+  float gw = 2.f * dot(g, cross(u, v));
+  V3 gu = cross(v, g) * (2.f * q.w) + g * (2.f * dot(u, v)) + v * (2.f * dot(g, u)) -
+          u * (4.f * dot(g, v));
+  return q4(gw, gu.x, gu.y, gu.z);
+}
+
+QS_HD float sigmoid_stable(float x) {  // q/autodiff.py:446-456
+  if (x >= 0.f) return 1.f / (1.f + expf(-x));
+  float e = expf(x);
+  return e / (1.f + e);
+}
+QS_HD float softplus(float x) {  // logaddexp(0, x)
+  return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x)));
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 counter-based RNG (Salmon et al., SC'11).  Stateless: a draw
+// is a pure function of (key, counter), so resets and IMU noise are graph
+// capturable and independent of launch geometry / sharding.
+
+QS_D uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) {
+    uint32_t lo0 = c.x * 0xD2511F53u, hi0 = __umulhi(c.x, 0xD2511F53u);
+    uint32_t lo1 = c.z * 0xCD9E8D57u, hi1 = __umulhi(c.z, 0xCD9E8D57u);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// purposes (counter word 2, high byte)
+enum : uint32_t {
+  RNG_SPAWN = 1u,
+  RNG_DR = 2u,
+  RNG_IMU = 3u,
+  RNG_SCENE = 4u,
+};
+
+struct Rng {
+  uint4 ctr;
+  uint2 key;
+  QS_D Rng(uint64_t seed, uint64_t id, uint32_t sub, uint32_t purpose) {
+    key = make_uint2((uint32_t)seed, (uint32_t)(seed >> 32));
+    ctr = make_uint4((uint32_t)id, (uint32_t)(id >> 32), sub, purpose << 24);
+  }
+  // four uniforms in (0, 1)
+  QS_D float4 uniform4() {
+    uint4 r = philox4x32_10(ctr, key);
+    ctr.w++;
+    const float s = 1.f / 16777216.f;
+    return make_float4(((r.x >> 8) + 0.5f) * s, ((r.y >> 8) + 0.5f) * s, ((r.z >> 8) + 0.5f) * s,
+                       ((r.w >> 8) + 0.5f) * s);
+  }
+  // four standard normals (Box-Muller on two pairs)
+  QS_D float4 normal4() {
+    float4 u = uniform4();
+    float r0 = sqrtf(-2.f * logf(u.x)), r1 = sqrtf(-2.f * logf(u.z));
+    float s0, c0, s1, c1;
+    sincospif(2.f * u.y, &s0, &c0);
+    sincospif(2.f * u.w, &s1, &c1);
+    return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+  }
+};
+
+QS_D void report_err(int32_t* err, int code, int row) {
+  if (!err) return;
+  atomicCAS(err, 0, code);
+  atomicMin(err + 1, row);
+}
+
+template <typename T>
+QS_D T ldg(const T* p) {
+  return __ldg(p);
+}
+
+QS_D float4 ld4(const float* p, long i) { return __ldg(reinterpret_cast<const float4*>(p) + i); }
+QS_D void st4(float* p, long i, float4 v) { reinterpret_cast<float4*>(p)[i] = v; }

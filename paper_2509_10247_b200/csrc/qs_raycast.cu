@@ -1,0 +1,319 @@
+// Per-ray ray casting against analytic obstacles: depth camera, LiDAR and
+// generic rays (q/sensors.py:131-269, 276-410), plus the opt-in analytic
+// depth VJP (new; no reference counterpart, q/sensors.py:4-6).
+//
+// Layout: one CTA per (row, ray chunk).  The CTA stages its env's obstacles
+// in shared memory ONCE, hoisting every ray-invariant term (o - c, |o-c|^2 - r^2,
+// slab offsets, ...) and dropping obstacles the conservative frustum /
+// range-ball test proves unreachable (never changes the image, q/sensors.py:
+// 338-374); each thread then owns RPT rays and keeps its running min-t in
+// registers, reading obstacle records as shared-memory broadcasts.
+#include "qs_dynamics.cuh"
+#include "qs_geom.cuh"
+
+namespace {
+
+constexpr int RAY_BLOCK = 256;
+constexpr float INF = __builtin_huge_valf();
+
+// NaN-propagating min/max (PTX min.NaN/max.NaN, sm_80+): a NaN slab term makes
+// the whole box test fail exactly like the reference's nan_to_num dance
+// (q/sensors.py:157-159).
+QS_D float fmin_nan(float a, float b) {
+  float d;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+QS_D float fmax_nan(float a, float b) {
+  float d;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+QS_D float sqrt_approx(float x) {
+  float d;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(x));
+  return d;
+}
+
+// conservative keep tests (fp32 margins absorb rounding; the reference uses
+// 1e-9 in fp64)
+QS_D bool keep_camera(const qs_ray_cfg& rc, float2 cs, V3 o, V3 c, float rad) {
+  V3 l = unrotz(cs, c - o);  // camera-frame centre (yaw-only attitude)
+  const float m = 1e-3f * (1.f + fabsf(l.x) + fabsf(l.y) + fabsf(l.z));
+  const float nh = rsqrtf(rc.tan_h * rc.tan_h + 1.f), nv = rsqrtf(rc.tan_v * rc.tan_v + 1.f);
+  bool in = (rc.tan_h * l.x - l.y) * nh >= -rad - m;
+  in = in && (rc.tan_h * l.x + l.y) * nh >= -rad - m;
+  in = in && (rc.tan_v * l.x - l.z) * nv >= -rad - m;
+  in = in && (rc.tan_v * l.x + l.z) * nv >= -rad - m;
+  in = in && l.x >= -rad - m;
+  in = in && norm3(l) - rad <= rc.max_range + m;
+  return in;
+}
+QS_D bool keep_ball(const qs_ray_cfg& rc, V3 o, V3 c, float rad) {
+  V3 l = c - o;
+  const float m = 1e-3f * (1.f + fabsf(l.x) + fabsf(l.y) + fabsf(l.z));
+  return norm3(l) - rad <= rc.max_range + m;
+}
+
+// --- ray-primitive tests on hoisted records ---------------------------------
+
+// sphere record: (oc.xyz, r^2), oc = o - c.  Robust discriminant
+// r^2 - |oc - b d|^2 (== b^2 - (|oc|^2 - r^2) in exact arithmetic).
+QS_D float hit_sphere(float4 s, V3 d) {
+  float b = d.x * s.x + d.y * s.y + d.z * s.z;
+  float vx = fmaf(-b, d.x, s.x), vy = fmaf(-b, d.y, s.y), vz = fmaf(-b, d.z, s.z);
+  float disc = s.w - (vx * vx + vy * vy + vz * vz);
+  float sq = sqrt_approx(fmaxf(disc, 0.f));
+  float t1 = -b - sq, t2 = -b + sq;
+  float t = t1 >= 0.f ? t1 : (t2 >= 0.f ? t2 : INF);
+  return disc >= 0.f ? t : INF;
+}
+
+// box record: lo - o, hi - o
+QS_D float hit_box(float4 lo, float4 hi, V3 inv, int* axis) {
+  float t1x = lo.x * inv.x, t2x = hi.x * inv.x;
+  float t1y = lo.y * inv.y, t2y = hi.y * inv.y;
+  float t1z = lo.z * inv.z, t2z = hi.z * inv.z;
+  float nx = fmin_nan(t1x, t2x), fx = fmax_nan(t1x, t2x);
+  float ny = fmin_nan(t1y, t2y), fy = fmax_nan(t1y, t2y);
+  float nz = fmin_nan(t1z, t2z), fz = fmax_nan(t1z, t2z);
+  float tn = fmax_nan(fmax_nan(nx, ny), nz);
+  float tf = fmin_nan(fmin_nan(fx, fy), fz);
+  bool hit = (tn <= tf) && (tf >= 0.f);
+  float t = tn >= 0.f ? tn : tf;
+  if (axis) {  // face normal axis of the returned root (depth VJP)
+    if (tn >= 0.f)
+      *axis = (tn == nx) ? 0 : (tn == ny ? 1 : 2);
+    else
+      *axis = (tf == fx) ? 0 : (tf == fy ? 1 : 2);
+  }
+  return hit ? t : INF;
+}
+
+// cylinder record A: (ox, oy, oz, r^2), B: (hh, _, _, _)
+// robust side discriminant a r^2 - (ox dy - oy dx)^2 (Lagrange identity)
+QS_D float hit_cyl(float4 c, float hh, V3 d, float a, float inv_a, float inv_dz, int* part) {
+  float b = c.x * d.x + c.y * d.y;
+  float cr = c.x * d.y - c.y * d.x;
+  float disc = a * c.w - cr * cr;
+  float sq = sqrt_approx(fmaxf(disc, 0.f));
+  float ts1 = (-b - sq) * inv_a, ts2 = (-b + sq) * inv_a;
+  bool base = disc >= 0.f && a > 0.f;
+  bool ok1 = base && ts1 >= 0.f && fabsf(fmaf(ts1, d.z, c.z)) <= hh;
+  bool ok2 = base && ts2 >= 0.f && fabsf(fmaf(ts2, d.z, c.z)) <= hh;
+  float ts = ok1 ? ts1 : (ok2 ? ts2 : INF);
+  float tt = (hh - c.z) * inv_dz, tb = (-hh - c.z) * inv_dz;
+  float xt = fmaf(tt, d.x, c.x), yt = fmaf(tt, d.y, c.y);
+  float xb = fmaf(tb, d.x, c.x), yb = fmaf(tb, d.y, c.y);
+  bool okt = tt >= 0.f && tt < INF && xt * xt + yt * yt <= c.w;
+  bool okb = tb >= 0.f && tb < INF && xb * xb + yb * yb <= c.w;
+  float tc = fminf(okt ? tt : INF, okb ? tb : INF);
+  if (part) *part = (ts <= tc) ? 0 : 1;
+  return fminf(ts, tc);
+}
+
+template <int KIND, bool GRAD>
+__global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, const qs_scene sc,
+                                                       int n_rows, const float* __restrict__ pos,
+                                                       int pos_stride, const float* __restrict__ cam_cs,
+                                                       const float* __restrict__ dirs_body,
+                                                       const float* __restrict__ dirs_world,
+                                                       float* __restrict__ out, uint8_t* __restrict__ hitm,
+                                                       float* __restrict__ dT_dO, int rays_per_cta) {
+  extern __shared__ float4 sm[];
+  __shared__ int cnt[3];
+  const long row = blockIdx.y;
+  const long e = row / rc.n_agents;
+  const int r0 = blockIdx.x * rays_per_cta;
+  const int r1 = min(rc.n_rays, r0 + rays_per_cta);
+  float2 cs = make_float2(1.f, 0.f);
+  if (cam_cs) cs = reinterpret_cast<const float2*>(cam_cs)[row];
+  const float* pp = pos + row * pos_stride;
+  V3 off = rotz(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
+  V3 o = v3(pp[0], pp[1], pp[2]) + off;
+  SceneView sv = scene_view(sc, e);
+  float4* s_sph = sm;
+  float4* s_box = sm + sc.Sm;
+  float4* s_cyl = s_box + 2 * sc.Bm;
+  float* s_cyl_hh = reinterpret_cast<float*>(s_cyl + sc.Cm);
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  // stage + cull; compaction order is arbitrary, which is fine: min-t is
+  // order independent (fminf is exact), so the image is deterministic
+  const int tot = sv.ns + sv.nb + sv.nc;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    if (i < sv.ns) {
+      float4 s = ld4(sv.sph, i);
+      V3 c = xyz(s);
+      bool keep = !rc.cull || (KIND == 0 ? keep_camera(rc, cs, o, c, s.w) : keep_ball(rc, o, c, s.w));
+      if (keep) {
+        int k = atomicAdd(&cnt[0], 1);
+        V3 oc = o - c;
+        s_sph[k] = f4(oc, s.w * s.w);
+      }
+    } else if (i < sv.ns + sv.nb) {
+      int j = i - sv.ns;
+      float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
+      float rad = norm3(xyz(h));
+      bool keep = !rc.cull ||
+                  (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
+      if (keep) {
+        int k = atomicAdd(&cnt[1], 1);
+        s_box[2 * k] = f4(xyz(c) - xyz(h) - o, 0.f);
+        s_box[2 * k + 1] = f4(xyz(c) + xyz(h) - o, 0.f);
+      }
+    } else {
+      int j = i - sv.ns - sv.nb;
+      float4 c = ld4(sv.cyl, 2 * j);
+      float hh = __ldg(sv.cyl + 8 * j + 4);
+      float rad = sqrtf(c.w * c.w + hh * hh);
+      bool keep = !rc.cull ||
+                  (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
+      if (keep) {
+        int k = atomicAdd(&cnt[2], 1);
+        s_cyl[k] = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
+        s_cyl_hh[k] = hh;
+      }
+    }
+  }
+  __syncthreads();
+  const int ns = cnt[0], nb = cnt[1], nc = cnt[2];
+  const bool ground = sv.ground;
+  const float gdz = sv.gz - o.z;
+  for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+    V3 d;
+    if (KIND == 2) {
+      d = xyz(ld4(dirs_world, row * rc.n_rays + r));
+    } else {
+      d = rotz(cs, xyz(ld4(dirs_body, r)));
+    }
+    V3 inv = v3(1.f / d.x, 1.f / d.y, 1.f / d.z);
+    float a = d.x * d.x + d.y * d.y;
+    float inv_a = 1.f / a;
+    float best = INF;
+    int code = 0, bidx = 0;  // kind | detail, shared-memory index of the argmin
+    for (int i = 0; i < ns; ++i) {
+      float t = hit_sphere(s_sph[i], d);
+      if (GRAD) {
+        if (t < best) { best = t; code = 1; bidx = i; }
+      } else {
+        best = fminf(best, t);
+      }
+    }
+    for (int i = 0; i < nb; ++i) {
+      int ax = 0;
+      float t = hit_box(s_box[2 * i], s_box[2 * i + 1], inv, GRAD ? &ax : nullptr);
+      if (GRAD) {
+        if (t < best) { best = t; code = 2 | (ax << 4); bidx = i; }
+      } else {
+        best = fminf(best, t);
+      }
+    }
+    for (int i = 0; i < nc; ++i) {
+      int part = 0;
+      float t = hit_cyl(s_cyl[i], s_cyl_hh[i], d, a, inv_a, inv.z, GRAD ? &part : nullptr);
+      if (GRAD) {
+        if (t < best) { best = t; code = 3 | (part << 4); bidx = i; }
+      } else {
+        best = fminf(best, t);
+      }
+    }
+    if (ground) {
+      float t = gdz * inv.z;
+      bool ok = t >= 0.f && t < INF;  // isfinite(t) && t >= 0
+      if (ok && t < best) { best = t; code = 4; }
+    }
+    float tout = fminf(best, rc.max_range);
+    const long oi = row * rc.n_rays + r;
+    out[oi] = tout;
+    if (hitm) hitm[oi] = best < rc.max_range ? 1 : 0;
+    if (GRAD) {
+      // d t / d o = -n / (n . d) at the hit surface; 0 when clamped / missed
+      V3 n = v3(0.f, 0.f, 0.f);
+      if (best < rc.max_range) {
+        int kind = code & 15;
+        if (kind == 1) {
+          n = xyz(s_sph[bidx]) + d * best;  // x - c = oc + t d
+        } else if (kind == 2) {
+          int ax = code >> 4;
+          n = v3(ax == 0 ? 1.f : 0.f, ax == 1 ? 1.f : 0.f, ax == 2 ? 1.f : 0.f);
+        } else if (kind == 3) {
+          if ((code >> 4) == 0) {
+            float4 c = s_cyl[bidx];
+            n = v3(c.x + best * d.x, c.y + best * d.y, 0.f);
+          } else {
+            n = v3(0.f, 0.f, 1.f);
+          }
+        } else if (kind == 4) {
+          n = v3(0.f, 0.f, 1.f);
+        }
+      }
+      float nd = dot(n, d);
+      V3 g = nd != 0.f ? n * (-1.f / nd) : v3(0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(dT_dO)[oi] = f4(g, 0.f);
+    }
+  }
+}
+
+// g_pos[row] += sum_r g_depth[row, r] * dT_dO[row, r]   (one CTA per row)
+__global__ void __launch_bounds__(256) k_raycast_vjp(int n_rays, const float* __restrict__ g_depth,
+                                                     const float* __restrict__ dT_dO,
+                                                     float* __restrict__ g_pos, int pos_stride) {
+  const long row = blockIdx.x;
+  V3 acc = v3(0.f, 0.f, 0.f);
+  for (int r = threadIdx.x; r < n_rays; r += blockDim.x) {
+    long i = row * n_rays + r;
+    float g = g_depth[i];
+    acc += xyz(ld4(dT_dO, i)) * g;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    acc.z += __shfl_xor_sync(0xffffffffu, acc.z, o);
+  }
+  __shared__ V3 part[8];
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    V3 s = v3(0.f, 0.f, 0.f);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += part[w];
+    float* gp = g_pos + row * pos_stride;
+    gp[0] += s.x;
+    gp[1] += s.y;
+    gp[2] += s.z;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
+               int32_t pos_stride, const float* cam_cs, const float* dirs_body,
+               const float* dirs_world, float* out, uint8_t* hit, float* dT_dO, void* stream) {
+  if (n_rows <= 0 || cfg->n_rays <= 0) return QS_OK;
+  if (cfg->kind < 0 || cfg->kind > 2 || cfg->n_agents < 1) return QS_ERR_BAD_ARGUMENT;
+  const int rpc = cfg->n_rays <= 4096 ? cfg->n_rays : 4096;
+  dim3 grid((cfg->n_rays + rpc - 1) / rpc, n_rows);
+  size_t smem = (size_t)(scene->Sm + 2 * scene->Bm + scene->Cm) * 16 + scene->Cm * 4;
+  cudaStream_t s = (cudaStream_t)stream;
+  const bool g = dT_dO != nullptr;
+#define QS_RC(K, G)                                                                           \
+  k_raycast<K, G><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, \
+                                                dirs_body, dirs_world, out, hit, dT_dO, rpc)
+  if (cfg->kind == 0) { if (g) QS_RC(0, true); else QS_RC(0, false); }
+  else if (cfg->kind == 1) { if (g) QS_RC(1, true); else QS_RC(1, false); }
+  else { if (g) QS_RC(2, true); else QS_RC(2, false); }
+#undef QS_RC
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
+
+int qs_raycast_vjp(int32_t n_rows, int32_t n_rays, const float* g_depth, const float* dT_dO,
+                   float* g_pos, int32_t pos_stride, void* stream) {
+  if (n_rows <= 0) return QS_OK;
+  k_raycast_vjp<<<n_rows, 256, 0, (cudaStream_t)stream>>>(n_rays, g_depth, dT_dO, g_pos, pos_stride);
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
+
+}  // extern "C"

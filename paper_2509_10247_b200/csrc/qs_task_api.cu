@@ -1,0 +1,57 @@
+// C ABI for the fused task step (include/quadsim_b200.h).
+#include "qs_dynamics.cuh"
+
+namespace qs {
+template <int T>
+int task_dispatch(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
+                  const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
+}
+
+namespace {
+int task_call(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
+              const uint8_t* mask, const qs_reset_table* tab, void* stream) {
+  if (!cfg || !sc || !p) return QS_ERR_BAD_ARGUMENT;
+  if (cfg->n_agents < 1 || cfg->n_agents > QS_MAX_AGENTS) return QS_ERR_BAD_ARGUMENT;
+  if (cfg->n_envs <= 0) return QS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (cfg->task) {
+    case QS_TASK_POSITION: return qs::task_dispatch<QS_TASK_POSITION>(op, cfg, sc, p, mask, tab, s);
+    case QS_TASK_AVOIDANCE: return qs::task_dispatch<QS_TASK_AVOIDANCE>(op, cfg, sc, p, mask, tab, s);
+    case QS_TASK_RACING: return qs::task_dispatch<QS_TASK_RACING>(op, cfg, sc, p, mask, tab, s);
+  }
+  return QS_ERR_BAD_ARGUMENT;
+}
+}  // namespace
+
+extern "C" {
+
+int qs_abi_version(void) { return QS_ABI_VERSION; }
+
+int qs_proprio_dim(int32_t model, int32_t task) {
+  int base = model == QS_MODEL_FULL ? 12 : 9;
+  return base + (task == QS_TASK_RACING ? 9 : 0);
+}
+
+int qs_state_planes(int32_t model) { return model == QS_MODEL_FULL ? 4 : 3; }
+
+int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
+                     void* stream) {
+  return task_call(0, cfg, scene, io, nullptr, nullptr, stream);
+}
+
+int qs_task_step_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_grad* g,
+                     void* stream) {
+  return task_call(1, cfg, scene, g, nullptr, nullptr, stream);
+}
+
+int qs_task_spawn(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
+                  const uint8_t* env_mask, const qs_reset_table* table, void* stream) {
+  return task_call(2, cfg, scene, io, env_mask, table, stream);
+}
+
+int qs_task_observe(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
+                    void* stream) {
+  return task_call(3, cfg, scene, io, nullptr, nullptr, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,5 @@
+// Avoidance task instantiations (q/tasks.py:766-844).
+#include "qs_task_impl.cuh"
+namespace qs {
+QS_DEFINE_TASK_DISPATCH(QS_TASK_AVOIDANCE, true)
+}

@@ -1,0 +1,894 @@
+// Fused env step (forward + analytic VJP), spawn and observe kernels.
+//
+// One thread owns one ENV (all of its agent rows), so every per-env coupling
+// of the reference step -- success needs all agents, bounds/collision any
+// agent, the formation penalty, the shared reset -- stays in registers with no
+// inter-thread communication.  Reference: q/tasks.py:549-763, 817-844,
+// 925-972; q/dynamics.py; q/sensors.py:417-611; q/world.py:409-448.
+#pragma once
+#include "qs_dynamics.cuh"
+#include "qs_geom.cuh"
+
+namespace qs {
+
+constexpr int FLAG_DONE = 1;
+constexpr int FLAG_CLAMP_SHIFT = 1;  // 9 bits: goal(3) gate0(3) gate1(3)
+constexpr int FLAG_CLAMP_MASK = 0x1FF << FLAG_CLAMP_SHIFT;
+constexpr int FLAG_SDF_SHIFT = 10;
+
+template <int M, int TASK>
+struct TaskTraits {
+  static constexpr int A = ModelTraits<M>::A;
+  static constexpr int P = ModelTraits<M>::P + (TASK == QS_TASK_RACING ? 9 : 0);
+};
+
+struct GateV {
+  V3 c, n;
+  float inner, frame;
+};
+
+QS_D GateV load_gate(const qs_scene& sc, const qs_task_cfg& cfg, long e, int g) {
+  const float* p = sc.gates + (e * cfg.n_gates + g) * 8;
+  float4 a = ld4(p, 0), b = ld4(p, 1);
+  return GateV{xyz(a), xyz(b), a.w, b.w};
+}
+
+QS_D V3 load3(const float* p, long row) { return xyz(ld4(p, row)); }
+
+QS_D V3 head_xy(V3 d) {  // q/tasks.py:705-708
+  d.z = 0.f;
+  float n = norm3(d);
+  return d * (1.f / fmaxf(n, 1e-9f));
+}
+
+QS_D bool in_range(float x, float lo, float hi) { return x >= lo && x <= hi; }
+QS_D float clampf(float x, float lo, float hi) { return fminf(fmaxf(x, lo), hi); }
+
+// ---------------------------------------------------------------------------
+// observation (q/tasks.py:415-442, racing extras :904-915)
+
+template <int M, int TASK>
+QS_D int observe_row(const qs_task_cfg& cfg, const State& s, float2 cs, V3 goal, const GateV* g0,
+                     const GateV* g1, float* o) {
+  const float clip = cfg.obs_clip;
+  int bits = 0;
+  V3 off = unrotz(cs, goal - s.p);
+  o[0] = clampf(off.x, -clip, clip);
+  o[1] = clampf(off.y, -clip, clip);
+  o[2] = clampf(off.z, -clip, clip);
+  bits |= (in_range(off.x, -clip, clip) ? 1 : 0) | (in_range(off.y, -clip, clip) ? 2 : 0) |
+          (in_range(off.z, -clip, clip) ? 4 : 0);
+  V3 vl = unrotz(cs, s.v);
+  o[3] = vl.x;
+  o[4] = vl.y;
+  o[5] = vl.z;
+  int k = 6;
+  if (M == QS_MODEL_FULL) {
+    V3 zl = unrotz(cs, qrot(s.q, v3(0.f, 0.f, 1.f)));
+    o[6] = zl.x;
+    o[7] = zl.y;
+    o[8] = zl.z;
+    o[9] = s.w.x;
+    o[10] = s.w.y;
+    o[11] = s.w.z;
+    k = 12;
+  } else {
+    V3 xl = unrotz(cs, s.x);
+    o[6] = xl.x;
+    o[7] = xl.y;
+    o[8] = xl.z;
+    k = 9;
+  }
+  if (TASK == QS_TASK_RACING) {
+    V3 a = unrotz(cs, g0->c - s.p);
+    V3 nl = unrotz(cs, g0->n);
+    V3 b = unrotz(cs, g1->c - s.p);
+    o[k + 0] = clampf(a.x, -clip, clip);
+    o[k + 1] = clampf(a.y, -clip, clip);
+    o[k + 2] = clampf(a.z, -clip, clip);
+    o[k + 3] = nl.x;
+    o[k + 4] = nl.y;
+    o[k + 5] = nl.z;
+    o[k + 6] = clampf(b.x, -clip, clip);
+    o[k + 7] = clampf(b.y, -clip, clip);
+    o[k + 8] = clampf(b.z, -clip, clip);
+    bits |= (in_range(a.x, -clip, clip) ? 8 : 0) | (in_range(a.y, -clip, clip) ? 16 : 0) |
+            (in_range(a.z, -clip, clip) ? 32 : 0) | (in_range(b.x, -clip, clip) ? 64 : 0) |
+            (in_range(b.y, -clip, clip) ? 128 : 0) | (in_range(b.z, -clip, clip) ? 256 : 0);
+  }
+  return bits << FLAG_CLAMP_SHIFT;
+}
+
+template <int M, int TASK>
+QS_D void write_obs(const qs_task_cfg& cfg, const qs_step_io& io, long row, const float* o) {
+  constexpr int P = TaskTraits<M, TASK>::P;
+  float* dst = io.obs + row * P;
+#pragma unroll
+  for (int k = 0; k < P; ++k) dst[k] = o[k];
+}
+
+// ---------------------------------------------------------------------------
+// resets: in-kernel Philox sampling (q/tasks.py:676-710, 789-815, 873-902;
+// q/world.py:130-137, 409-448).  Keys: (seed, global env id, episode index).
+
+template <int M, int TASK, int NAMAX>
+QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int episode, int na,
+                       V3* p, V3* v, V3* goal, V3& head, int& next_gate) {
+  const uint64_t gid = (uint64_t)(e + cfg.env_offset);
+  Rng rng(cfg.seed, gid, (uint32_t)episode, RNG_SPAWN);
+  float4 blo = ld4(sc.bounds, 2 * e), bhi = ld4(sc.bounds, 2 * e + 1);
+  V3 lo = xyz(blo), hi = xyz(bhi);
+  bool ok = true;
+  next_gate = 0;
+  if (TASK == QS_TASK_POSITION) {
+    V3 l8 = lo + v3(0.8f, 0.8f, 0.8f), h8 = hi - v3(0.8f, 0.8f, 0.8f);
+    V3 sp = l8, gl = l8;
+    ok = false;
+    for (int t = 0; t < 100 && !ok; ++t) {
+      float4 u = rng.uniform4(), w = rng.uniform4();
+      sp = l8 + hmul(h8 - l8, v3(u.x, u.y, u.z));
+      gl = l8 + hmul(h8 - l8, v3(u.w, w.x, w.y));
+      float d = norm3(gl - sp);
+      ok = d >= 2.5f && d <= cfg.goal_dist;
+    }
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      V3 f = v3(cfg.formation[a][0], cfg.formation[a][1], cfg.formation[a][2]);
+      float4 n0 = rng.normal4(), n1 = rng.normal4();
+      p[a] = sp + f + v3(n0.x, n0.y, n0.z) * 0.1f;
+      v[a] = v3(n0.w, n1.x, n1.y) * 0.3f;
+      goal[a] = gl + f;
+    }
+    head = head_xy(gl - sp);
+  } else if (TASK == QS_TASK_AVOIDANCE) {
+    V3 ssp = load3(sc.spawn_goal, 2 * e), sgl = load3(sc.spawn_goal, 2 * e + 1);
+    SceneView sv = scene_view(sc, e);
+    ok = false;
+    for (int t = 0; t < 100 && !ok; ++t) {
+      bool good = true;
+#pragma unroll
+      for (int a = 0; a < NAMAX; ++a) {
+        if (a >= na) break;
+        V3 f = v3(cfg.formation[a][0], cfg.formation[a][1], cfg.formation[a][2]);
+        float4 n0 = rng.normal4();
+        V3 q = ssp + f + v3(n0.x, n0.y, n0.z) * 0.15f;
+        q.z = clampf(q.z, lo.z + 0.3f, hi.z - 0.3f);
+        p[a] = q;
+      }
+      if (na > 1) {
+        for (int i = 0; i < na; ++i)
+          for (int j = i + 1; j < na; ++j) good = good && norm3(p[i] - p[j]) >= cfg.d_min;
+      }
+#pragma unroll
+      for (int a = 0; a < NAMAX; ++a) {
+        if (a >= na) break;
+        int code;
+        good = good && sdf_eval(sv, p[a], code) > cfg.collision_radius + 0.3f;
+        V3 q = p[a];
+        good = good && q.x > lo.x + 0.2f && q.y > lo.y + 0.2f && q.z > lo.z + 0.2f &&
+               q.x < hi.x - 0.2f && q.y < hi.y - 0.2f && q.z < hi.z - 0.2f;
+      }
+      ok = good;
+    }
+    float4 nj = rng.normal4();
+    V3 jit = v3(nj.x, nj.y, nj.z) * 0.2f;
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      V3 f = v3(cfg.formation[a][0], cfg.formation[a][1], cfg.formation[a][2]);
+      float4 n1 = rng.normal4();
+      v[a] = v3(n1.x, n1.y, n1.z) * 0.2f;
+      goal[a] = sgl + f + jit;
+    }
+    head = head_xy(sgl - ssp);
+  } else {  // racing, single agent
+    V3 ssp = load3(sc.spawn_goal, 2 * e);
+    float4 n0 = rng.normal4(), n1 = rng.normal4();
+    p[0] = ssp + v3(n0.x, n0.y, n0.z) * 0.2f;
+    v[0] = v3(n0.w, n1.x, n1.y) * 0.2f;
+    GateV g0 = load_gate(sc, cfg, e, 0);
+    goal[0] = g0.c;
+    head = head_xy(g0.c - ssp);
+  }
+  return ok;
+}
+
+QS_D float4 dr_sample(const qs_task_cfg& cfg, long row, int episode) {
+  Rng rng(cfg.seed, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)episode, RNG_DR);
+  float4 u = rng.uniform4();
+  float drag = cfg.dr_drag[0] + (cfg.dr_drag[1] - cfg.dr_drag[0]) * u.x;
+  float lat = cfg.dr_latency[0] + (cfg.dr_latency[1] - cfg.dr_latency[0]) * u.y;
+  float scale = cfg.dr_scale[0] + (cfg.dr_scale[1] - cfg.dr_scale[0]) * u.z;
+  return make_float4(drag, expf(-lat * cfg.dt), scale, lat);
+}
+
+// ---------------------------------------------------------------------------
+// IMU read (q/sensors.py:540-555) on the post-dynamics state
+
+template <int M>
+QS_D void imu_row(const qs_task_cfg& cfg, const qs_step_io& io, long row, long N, int tick,
+                  const State& s2, V3 vdot, V3 g) {
+  float4 b0 = ld4(io.imu_bias, 2 * row), b1 = ld4(io.imu_bias, 2 * row + 1);
+  V3 ba = xyz(b0), bg = xyz(b1);
+  V3 nba, nbg, na, ng;
+  if (io.imu_noise) {
+    const float* z = io.imu_noise;
+    nba = v3(z[3 * row], z[3 * row + 1], z[3 * row + 2]);
+    nbg = v3(z[3 * (N + row)], z[3 * (N + row) + 1], z[3 * (N + row) + 2]);
+    na = v3(z[3 * (2 * N + row)], z[3 * (2 * N + row) + 1], z[3 * (2 * N + row) + 2]);
+    ng = v3(z[3 * (3 * N + row)], z[3 * (3 * N + row) + 1], z[3 * (3 * N + row) + 2]);
+  } else {
+    Rng rng(cfg.seed, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)tick, RNG_IMU);
+    float4 a = rng.normal4(), b = rng.normal4(), c = rng.normal4();
+    nba = v3(a.x, a.y, a.z);
+    nbg = v3(a.w, b.x, b.y);
+    na = v3(b.z, b.w, c.x);
+    ng = v3(c.y, c.z, c.w);
+  }
+  float sq = sqrtf(cfg.dt);
+  ba += nba * (cfg.imu_accel_rw * sq);
+  bg += nbg * (cfg.imu_gyro_rw * sq);
+  V3 xb, yb, zb;
+  V3 w = v3(0.f, 0.f, 0.f);
+  if (M == QS_MODEL_FULL) {
+    zb = qrot(s2.q, v3(0.f, 0.f, 1.f));
+    xb = qrot(s2.q, v3(1.f, 0.f, 0.f));
+    yb = qrot(s2.q, v3(0.f, 1.f, 0.f));
+    w = s2.w;
+  } else {
+    attitude_pm(thrust_of<M>(s2, g), s2.ve, xb, yb, zb);
+  }
+  V3 sp = vdot - g;
+  V3 acc = v3(dot(xb, sp), dot(yb, sp), dot(zb, sp)) + ba;
+  if (cfg.imu_accel_std != 0.f) acc += na * cfg.imu_accel_std;
+  V3 gy = w + bg;
+  if (cfg.imu_gyro_std != 0.f) gy += ng * cfg.imu_gyro_std;
+  st4(io.imu_bias, 2 * row, f4(ba, 0.f));
+  st4(io.imu_bias, 2 * row + 1, f4(bg, 0.f));
+  float* o = io.imu_out + 6 * row;
+  o[0] = acc.x; o[1] = acc.y; o[2] = acc.z;
+  o[3] = gy.x; o[4] = gy.y; o[5] = gy.z;
+}
+
+// ---------------------------------------------------------------------------
+// rewards (q/tasks.py:144-170, 625-637, 744-763, 817-844)
+
+struct RewardFwd {
+  float r, dist, speed;
+};
+
+QS_D RewardFwd reward_ctrl(const qs_weights& w, V3 off, V3 v, float effn, float deffn) {
+  float dist = norm3(off);
+  float speed = norm3(v);
+  float nearv = sigmoid_stable((w.near_radius - dist) * (1.f / w.near_width));
+  float sd = fminf(dist * w.track_gain, w.v_max);
+  V3 vdes = off * (sd / fmaxf(dist, 1e-9f));
+  float track = norm3(v - vdes);
+  float pen = dist * w.w_p;
+  pen = pen + (speed * nearv) * w.w_v;
+  pen = pen + effn * w.w_a;
+  pen = pen + deffn * w.w_s;
+  pen = pen + track * w.w_t;
+  return RewardFwd{-pen, dist, speed};
+}
+
+QS_D float reward_rl(const qs_weights& w, float clip, V3 off, V3 v, float effn, float deffn) {
+  float dist = norm3(off);
+  float speed = norm3(v);
+  float nearv = 1.f / (1.f + expf(-(w.near_radius - dist) / w.near_width));
+  float sd = fminf(dist * w.track_gain, w.v_max);
+  V3 vdes = off * (sd / fmaxf(dist, 1e-9f));
+  float track = norm3(v - vdes);
+  float dist_c = fminf(dist, clip);
+  return -(w.w_p * dist_c + w.w_v * speed * nearv + w.w_a * effn + w.w_s * deffn + w.w_t * track);
+}
+
+// VJP of reward_ctrl: returns grads wrt off, v, effort vec, d_effort vec
+QS_D void reward_ctrl_vjp(const qs_weights& w, V3 off, V3 v, float4 eff, float4 deff, int A, float g,
+                          V3& g_off, V3& g_v, float4& g_eff) {
+  float dist = norm3(off);
+  float speed = norm3(v);
+  float x = (w.near_radius - dist) * (1.f / w.near_width);
+  float nearv = sigmoid_stable(x);
+  float m = fmaxf(dist, 1e-9f);
+  float sd = fminf(dist * w.track_gain, w.v_max);
+  float kk = sd / m;
+  V3 vdes = off * kk;
+  V3 ev = v - vdes;
+  float track = norm3(ev);
+  float gp = -g;  // r = -pen
+  float g_dist = gp * w.w_p;
+  float g_speed = gp * w.w_v * nearv;
+  float g_near = gp * w.w_v * speed;
+  g_dist += g_near * nearv * (1.f - nearv) * (-1.f / w.near_width);
+  float g_track = gp * w.w_t;
+  // track = |v - off*k|
+  V3 gev = norm_vjp(ev, track, g_track);
+  g_v = gev + norm_vjp(v, speed, g_speed);
+  V3 g_vdes = -gev;
+  g_off = g_vdes * kk;
+  float g_k = dot(g_vdes, off);
+  float g_sd = g_k / m;
+  float g_m = -g_k * sd / (m * m);
+  if (dist * w.track_gain <= w.v_max) g_dist += g_sd * w.track_gain;  // minimum: tie -> first
+  if (dist >= 1e-9f) g_dist += g_m;                                   // maximum: tie -> first
+  g_off += norm_vjp(off, dist, g_dist);
+  // effort norms
+  float en = sqrtf(eff.x * eff.x + eff.y * eff.y + eff.z * eff.z + (A == 4 ? eff.w * eff.w : 0.f));
+  float dn = sqrtf(deff.x * deff.x + deff.y * deff.y + deff.z * deff.z +
+                   (A == 4 ? deff.w * deff.w : 0.f));
+  float ca = en > 0.f ? gp * w.w_a / en : 0.f;
+  float cs = dn > 0.f ? gp * w.w_s / dn : 0.f;
+  g_eff = make_float4(eff.x * ca + deff.x * cs, eff.y * ca + deff.y * cs, eff.z * ca + deff.z * cs,
+                      A == 4 ? eff.w * ca + deff.w * cs : 0.f);
+}
+
+QS_D float f4get(float4 v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+QS_D void f4set(float4& v, int k, float x) {
+  if (k == 0) v.x = x; else if (k == 1) v.y = x; else if (k == 2) v.z = x; else v.w = x;
+}
+
+template <int A>
+QS_D float4 load_act(const float* raw, long row) {
+  const float* p = raw + row * A;
+  return make_float4(p[0], p[1], p[2], A == 4 ? p[3] : 0.f);
+}
+
+template <int A>
+QS_D bool act_finite(float4 a) {
+  return isfinite(a.x) && isfinite(a.y) && isfinite(a.z) && (A < 4 || isfinite(a.w));
+}
+
+struct Squash {
+  float4 t, sq, eff;
+};
+
+template <int A>
+QS_D Squash squash(float4 raw, const RowPrm& rp) {  // q/dynamics.py:277-284
+  Squash s;
+  s.t = make_float4(tanhf(raw.x), tanhf(raw.y), tanhf(raw.z), A == 4 ? tanhf(raw.w) : 0.f);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < A) {
+      float sq = rp.center[k] + rp.half[k] * f4get(s.t, k);
+      f4set(s.sq, k, sq);
+      f4set(s.eff, k, sq - rp.center[k]);  // q/tasks.py:568
+    } else {
+      f4set(s.sq, k, 0.f);
+      f4set(s.eff, k, 0.f);
+    }
+  }
+  return s;
+}
+
+template <int M>
+QS_D float4 world_cmd(const State& s, float4 sq, V3 g, float2& cs) {  // q/tasks.py:613-618
+  if (M == QS_MODEL_FULL) {
+    cs = make_float2(1.f, 0.f);
+    return sq;
+  }
+  cs = yaw_cs<M>(s, g);
+  V3 c = rotz(cs, v3(sq.x, sq.y, sq.z));
+  return make_float4(c.x, c.y, c.z, 0.f);
+}
+
+QS_D float effnorm(float4 e, int A) {
+  return sqrtf(e.x * e.x + e.y * e.y + e.z * e.z + (A == 4 ? e.w * e.w : 0.f));
+}
+
+QS_D void warp_stats(bool active, bool done, int term, float ret, double* stats) {
+  unsigned m = __ballot_sync(0xffffffffu, active && done);
+  if (!m) return;
+  unsigned ms = __ballot_sync(0xffffffffu, active && done && term == 1);
+  unsigned mc = __ballot_sync(0xffffffffu, active && done && term == 2);
+  double r = (active && done) ? (double)ret : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+  if ((threadIdx.x & 31) == 0 && stats) {
+    atomicAdd(stats + 0, (double)__popc(m));
+    atomicAdd(stats + 1, (double)__popc(ms));
+    atomicAdd(stats + 2, (double)__popc(mc));
+    atomicAdd(stats + 3, r);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// forward
+
+template <int M, int TASK, int NAMAX, bool INLINE>
+__global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const qs_scene sc,
+                                                  const qs_step_io io) {
+  constexpr int A = ModelTraits<M>::A;
+  constexpr int P = TaskTraits<M, TASK>::P;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < cfg.n_envs;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  const DynK k = dyn_consts(cfg);
+  bool done = false;
+  int term_env = 0;
+  float ret_env = 0.f;
+  if (active) {
+    int4 meta = reinterpret_cast<int4*>(io.meta)[e];
+    State s2[NAMAX];
+    float rc[NAMAX], rl[NAMAX];
+    float4 eff[NAMAX];
+    int codes[NAMAX];
+    float4 drs[NAMAX];
+    bool all_goal = true, any_oob = false, any_coll = false;
+    V3 p0 = v3(0.f, 0.f, 0.f);
+    SceneView sv;
+    if (TASK == QS_TASK_AVOIDANCE) sv = scene_view(sc, e);
+    const V3 blo = xyz(ld4(sc.bounds, 2 * e)) + v3(1e-6f, 1e-6f, 1e-6f);
+    const V3 bhi = xyz(ld4(sc.bounds, 2 * e + 1)) - v3(1e-6f, 1e-6f, 1e-6f);
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      const long row = e * na + a;
+      State s = load_state<M>(io.S_in, N, row);
+      RowPrm rp = row_params<M>(cfg, io.dr_in, row);
+      drs[a] = io.dr_in ? ld4(io.dr_in, row) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 raw = load_act<A>(io.raw, row);
+      if (!act_finite<A>(raw)) report_err(io.err, QS_ERR_NONFINITE_ACTION, (int)row);
+      if (!state_finite<M>(s)) report_err(io.err, QS_ERR_NONFINITE_STATE, (int)row);
+      Squash q = squash<A>(raw, rp);
+      float2 cs;
+      float4 cmd = world_cmd<M>(s, q.sq, k.g, cs);
+      State n = model_step<M>(s, cmd, rp, k);
+      n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;  // q/sensors.py:566
+      if (io.imu_out) imu_row<M>(cfg, io, row, N, meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g);
+      float4 pe = ld4(io.peff_in, row);
+      float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
+      float en = effnorm(q.eff, A), dn = effnorm(de, A);
+      eff[a] = q.eff;
+      s2[a] = n;
+      codes[a] = 0;
+      p0 = s.p;
+      if (TASK != QS_TASK_RACING) {
+        V3 goal = load3(io.goal_in, row);
+        V3 off = goal - n.p;
+        RewardFwd rf = reward_ctrl(cfg.w, off, n.v, en, dn);
+        float extra = 0.f;
+        if (TASK == QS_TASK_AVOIDANCE) {
+          int code;
+          float sd = sdf_eval(sv, n.p, code);
+          codes[a] = code;
+          rf.r -= cfg.w.w_o * softplus((cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness));
+          any_coll = any_coll || sd <= cfg.collision_radius;
+          extra = -(cfg.w_rl.w_o * softplus((cfg.d_safe - sd) / cfg.w_rl.sdf_sharpness));
+        }
+        rc[a] = rf.r;
+        rl[a] = reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn) + extra;
+        all_goal = all_goal && (rf.dist < cfg.success_radius) && (rf.speed < cfg.hover_speed);
+      }
+      any_oob = any_oob || n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x ||
+                n.p.y > bhi.y || n.p.z > bhi.z;
+    }
+    // ---- per-env couplings
+    float r_goal = 0.f;
+    int next_gate = meta.w;
+    V3 goal_adv = v3(0.f, 0.f, 0.f);
+    bool advanced = false;
+    if (TASK == QS_TASK_RACING) {  // q/tasks.py:925-972
+      const qs_weights& w = cfg.w_rl;
+      GateV gt = load_gate(sc, cfg, e, next_gate);
+      V3 p1 = s2[0].p;
+      float r = w.w_g * (norm3(p0 - gt.c) - norm3(p1 - gt.c));
+      float sa = dot(p0 - gt.c, gt.n), sb = dot(p1 - gt.c, gt.n);
+      if (sa < 0.f && sb >= 0.f) {
+        float frac = -sa / fmaxf(sb - sa, 1e-12f);
+        V3 x = p0 + (p1 - p0) * frac;
+        V3 xc = x - gt.c;
+        float radial = norm3(xc - gt.n * dot(xc, gt.n));
+        bool passed = radial < gt.inner;
+        bool crashed = !passed && radial < gt.inner + gt.frame;
+        if (passed) r += w.gate_pass_bonus;
+        if (crashed) {
+          r -= w.gate_crash_penalty;
+          term_env = 2;
+          r_goal = -1.f;
+        }
+        bool finished = passed && next_gate == cfg.n_gates - 1;
+        if (finished) {
+          term_env = 1;
+          r_goal = 1.f;
+        }
+        if (passed && !finished) {
+          next_gate += 1;
+          advanced = true;
+          goal_adv = load_gate(sc, cfg, e, next_gate).c;
+        }
+      }
+      if (any_oob && term_env == 0) {
+        term_env = 3;
+        r_goal = -1.f;
+        r -= w.goal_bonus;
+      }
+      rc[0] = 0.f;
+      rl[0] = r;
+    } else {
+      if (na > 1) {  // q/tasks.py:173-192
+        float pen = 0.f;
+        for (int i = 0; i < na; ++i)
+          for (int j = i + 1; j < na; ++j) {
+            float dij = norm3(s2[i].p - s2[j].p);
+            float t = dij - cfg.form_ref[i][j];
+            pen = pen + t * t;
+            any_coll = any_coll || dij < cfg.d_min;
+          }
+        pen *= cfg.w.w_f;
+#pragma unroll
+        for (int a = 0; a < NAMAX; ++a)
+          if (a < na) rc[a] -= pen;
+      }
+      // precedence: success, then bounds, then collision overwrite (q/tasks.py:734-737)
+      if (all_goal) term_env = 1;
+      if (any_oob) term_env = 3;
+      if (any_coll) term_env = 2;
+      r_goal = term_env == 1 ? 1.f : (term_env != 0 ? -1.f : 0.f);
+#pragma unroll
+      for (int a = 0; a < NAMAX; ++a)
+        if (a < na) rl[a] = rl[a] + cfg.w_rl.goal_bonus * r_goal;
+    }
+    // ---- counters, truncation, stats (q/tasks.py:574-591, 606-611)
+    int steps = meta.x + 1;
+    bool trunc = steps >= cfg.episode_len && term_env == 0;
+    done = term_env != 0 || trunc;
+    float ret = io.ep_return[e] + rl[0];
+    ret_env = ret;
+    int episode = meta.y;
+    if (done) {
+      steps = 0;
+      episode += 1;
+      io.ep_return[e] = 0.f;
+      next_gate = 0;
+    } else {
+      io.ep_return[e] = ret;
+    }
+    reinterpret_cast<int4*>(io.meta)[e] = make_int4(steps, episode, meta.z + 1, next_gate);
+    // ---- spawn (inline) or keep
+    V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
+    int ng0 = 0;
+    if (INLINE && done) {
+      bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, episode, na, sp_p, sp_v, sp_g, head, ng0);
+      if (!ok) report_err(io.err, QS_ERR_GENERATION, (int)(e * na));
+    }
+    // racing gates for the observation
+    GateV g0, g1;
+    if (TASK == QS_TASK_RACING && INLINE) {
+      int ngate = done ? 0 : next_gate;
+      g0 = load_gate(sc, cfg, e, ngate);
+      g1 = load_gate(sc, cfg, e, min(ngate + 1, cfg.n_gates - 1));
+    }
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      const long row = e * na + a;
+      io.r_ctrl[row] = rc[a];
+      io.r_goal[row] = r_goal;
+      io.r_rl[row] = rl[a];
+      io.terminated[row] = (int8_t)term_env;
+      io.truncated[row] = trunc ? 1 : 0;
+      State so = s2[a];
+      V3 goal = (TASK == QS_TASK_RACING) ? (advanced ? goal_adv : load3(io.goal_in, row))
+                                         : load3(io.goal_in, row);
+      float4 pe = eff[a];
+      float4 dro = drs[a];
+      if (done) {
+        pe = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (io.imu_bias) {
+          st4(io.imu_bias, 2 * row, make_float4(0.f, 0.f, 0.f, 0.f));
+          st4(io.imu_bias, 2 * row + 1, make_float4(0.f, 0.f, 0.f, 0.f));
+        }
+        if (INLINE) {
+          so = init_state<M>(sp_p[a], sp_v[a], head, k.g);
+          goal = sp_g[a];
+          if (cfg.dr_enabled && cfg.dr_per_episode) dro = dr_sample(cfg, row, episode);
+        }
+      }
+      store_state<M>(io.S_out, N, row, so);
+      st4(io.goal_out, row, f4(goal, 0.f));
+      st4(io.peff_out, row, pe);
+      if (io.dr_out) st4(io.dr_out, row, dro);
+      int fl = (done ? FLAG_DONE : 0) | (codes[a] << FLAG_SDF_SHIFT);
+      if (INLINE) {
+        float o[P];
+        float2 cs = yaw_cs<M>(so, k.g);
+        fl |= observe_row<M, TASK>(cfg, so, cs, goal, &g0, &g1, o);
+        write_obs<M, TASK>(cfg, io, row, o);
+        if (io.cam) reinterpret_cast<float2*>(io.cam)[row] = cs;
+      }
+      io.flags[row] = fl;
+    }
+  }
+  warp_stats(active, done, term_env, ret_env, io.stats);
+}
+
+// ---------------------------------------------------------------------------
+// backward (analytic VJP of k_task_fwd; recomputes the forward from the
+// checkpoint (S_in, raw, goal_in, peff_in, dr_in) + the flags record)
+
+template <int M, int TASK, int NAMAX>
+__global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const qs_scene sc,
+                                                  const qs_step_grad gr) {
+  constexpr int A = ModelTraits<M>::A;
+  constexpr int P = TaskTraits<M, TASK>::P;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cfg.n_envs) return;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  const DynK k = dyn_consts(cfg);
+  State s1[NAMAX], s2[NAMAX], g2[NAMAX];
+  float4 cmd[NAMAX];
+  float2 csc[NAMAX];
+  float4 geff[NAMAX];
+  float gr_r[NAMAX];
+  SceneView sv;
+  if (TASK == QS_TASK_AVOIDANCE) sv = scene_view(sc, e);
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    State s = load_state<M>(gr.S_in, N, row);
+    RowPrm rp = row_params<M>(cfg, gr.dr_in, row);
+    float4 raw = load_act<A>(gr.raw, row);
+    Squash q = squash<A>(raw, rp);
+    float2 cs;
+    float4 c = world_cmd<M>(s, q.sq, k.g, cs);
+    State n = model_step<M>(s, c, rp, k);
+    n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;
+    const int fl = gr.flags[row];
+    const bool done = fl & FLAG_DONE;
+    State g = done ? zero_state() : load_grad<M>(gr.g_S_out, N, row);
+    // observation path (only rows that were not reset; q/tasks.py:584-594)
+    if (!done && gr.g_obs) {
+      const float* go = gr.g_obs + row * P;
+      float2 cs2 = yaw_cs<M>(n, k.g);
+      V3 gg = v3(go[0], go[1], go[2]);
+      int cb = fl >> FLAG_CLAMP_SHIFT;
+      gg = v3((cb & 1) ? gg.x : 0.f, (cb & 2) ? gg.y : 0.f, (cb & 4) ? gg.z : 0.f);
+      g.p -= rotz(cs2, gg);  // unrot^T = rot
+      g.v += rotz(cs2, v3(go[3], go[4], go[5]));
+      if (M == QS_MODEL_FULL) {
+        V3 gz = rotz(cs2, v3(go[6], go[7], go[8]));
+        Q4 gq = qrot_vjp_q(n.q, v3(0.f, 0.f, 1.f), gz);
+        g.q = q4(g.q.w + gq.w, g.q.x + gq.x, g.q.y + gq.y, g.q.z + gq.z);
+        g.w += v3(go[9], go[10], go[11]);
+      } else {
+        g.x += rotz(cs2, v3(go[6], go[7], go[8]));
+      }
+      if (TASK == QS_TASK_RACING) {
+        const int kk = ModelTraits<M>::P;
+        V3 ga = v3((cb & 8) ? go[kk] : 0.f, (cb & 16) ? go[kk + 1] : 0.f, (cb & 32) ? go[kk + 2] : 0.f);
+        V3 gb = v3((cb & 64) ? go[kk + 6] : 0.f, (cb & 128) ? go[kk + 7] : 0.f,
+                   (cb & 256) ? go[kk + 8] : 0.f);
+        g.p -= rotz(cs2, ga + gb);
+      }
+    }
+    float grr = gr.g_rctrl ? gr.g_rctrl[row] : 0.f;
+    float4 ge = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (TASK != QS_TASK_RACING && grr != 0.f) {
+      float4 pe = ld4(gr.peff_in, row);
+      float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
+      V3 goal = load3(gr.goal_in, row);
+      V3 off = goal - n.p;
+      V3 goff, gv;
+      reward_ctrl_vjp(cfg.w, off, n.v, q.eff, de, A, grr, goff, gv, ge);
+      g.p -= goff;
+      g.v += gv;
+      if (TASK == QS_TASK_AVOIDANCE) {
+        const int code = fl >> FLAG_SDF_SHIFT;  // argmin recorded by the forward
+        if (code != 0) {
+          float sd = sdf_prim(sv, n.p, code);
+          float arg = (cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness);
+          float gsd = grr * cfg.w.w_o * sigmoid_stable(arg) * (1.f / cfg.w.sdf_sharpness);
+          g.p += sdf_grad(sv, n.p, code) * gsd;
+        }
+      }
+    }
+    s1[a] = s;
+    s2[a] = n;
+    g2[a] = g;
+    cmd[a] = c;
+    csc[a] = cs;
+    geff[a] = ge;
+    gr_r[a] = grr;
+  }
+  if (TASK != QS_TASK_RACING && na > 1) {  // formation penalty VJP
+    float gpen = 0.f;
+    for (int a = 0; a < na; ++a) gpen -= gr_r[a];
+    gpen *= cfg.w.w_f;
+    for (int i = 0; i < na; ++i)
+      for (int j = i + 1; j < na; ++j) {
+        V3 d = s2[i].p - s2[j].p;
+        float dij = norm3(d);
+        float gd = gpen * 2.f * (dij - cfg.form_ref[i][j]);
+        V3 gv = norm_vjp(d, dij, gd);
+        g2[i].p += gv;
+        g2[j].p -= gv;
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    RowPrm rp = row_params<M>(cfg, gr.dr_in, row);
+    State gi;
+    float4 gc;
+    model_step_vjp<M>(s1[a], cmd[a], rp, k, g2[a], gi, gc);
+    float4 gsq;
+    if (M == QS_MODEL_FULL) {
+      gsq = gc;
+    } else {
+      V3 u = unrotz(csc[a], v3(gc.x, gc.y, gc.z));  // Rz^T g
+      gsq = make_float4(u.x, u.y, u.z, 0.f);
+    }
+    gsq = make_float4(gsq.x + geff[a].x, gsq.y + geff[a].y, gsq.z + geff[a].z, gsq.w + geff[a].w);
+    float4 raw = load_act<A>(gr.raw, row);
+    float* gout = gr.g_raw + row * A;
+#pragma unroll
+    for (int kk = 0; kk < A; ++kk) {
+      float t = tanhf(f4get(raw, kk));
+      gout[kk] = f4get(gsq, kk) * rp.half[kk] * (1.f - t * t);
+    }
+    store_state<M>(gr.g_S_in, N, row, gi);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// spawn (reset of masked envs), observe
+
+template <int M, int TASK, int NAMAX>
+__global__ void __launch_bounds__(128) k_task_spawn(const qs_task_cfg cfg, const qs_scene sc,
+                                                    const qs_step_io io, const uint8_t* mask,
+                                                    const qs_reset_table tab, bool use_tab) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cfg.n_envs) return;
+  if (mask && !mask[e]) return;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  const DynK k = dyn_consts(cfg);
+  int4 meta = reinterpret_cast<int4*>(io.meta)[e];
+  V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
+  int ng0 = 0;
+  if (!use_tab) {
+    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, meta.y, na, sp_p, sp_v, sp_g, head, ng0);
+    if (!ok) report_err(io.err, QS_ERR_GENERATION, (int)(e * na));
+  } else if (tab.next_gate) {
+    ng0 = tab.next_gate[e];
+  }
+  meta.w = ng0;
+  reinterpret_cast<int4*>(io.meta)[e] = meta;
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    V3 p, v, gl, ve;
+    if (use_tab) {
+      p = load3(tab.p, row);
+      v = load3(tab.v, row);
+      gl = load3(tab.goal, row);
+      ve = load3(tab.v_ema, row);
+    } else {
+      p = sp_p[a];
+      v = sp_v[a];
+      gl = sp_g[a];
+      ve = head;
+    }
+    store_state<M>(io.S_out, N, row, init_state<M>(p, v, ve, k.g));
+    st4(io.goal_out, row, f4(gl, 0.f));
+    st4(io.peff_out, row, make_float4(0.f, 0.f, 0.f, 0.f));
+    if (io.dr_out && cfg.dr_enabled) {
+      float4 d = use_tab && tab.dr ? ld4(tab.dr, row) : dr_sample(cfg, row, meta.y);
+      st4(io.dr_out, row, d);
+    }
+    if (io.imu_bias) {
+      st4(io.imu_bias, 2 * row, make_float4(0.f, 0.f, 0.f, 0.f));
+      st4(io.imu_bias, 2 * row + 1, make_float4(0.f, 0.f, 0.f, 0.f));
+    }
+  }
+}
+
+template <int M, int TASK, int NAMAX>
+__global__ void __launch_bounds__(128) k_task_observe(const qs_task_cfg cfg, const qs_scene sc,
+                                                      const qs_step_io io) {
+  constexpr int P = TaskTraits<M, TASK>::P;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cfg.n_envs) return;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  const DynK k = dyn_consts(cfg);
+  GateV g0, g1;
+  if (TASK == QS_TASK_RACING) {
+    int ng = io.meta[4 * e + 3];
+    g0 = load_gate(sc, cfg, e, ng);
+    g1 = load_gate(sc, cfg, e, min(ng + 1, cfg.n_gates - 1));
+  }
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    State s = load_state<M>(io.S_out, N, row);
+    V3 goal = load3(io.goal_out, row);
+    float o[P];
+    float2 cs = yaw_cs<M>(s, k.g);
+    int bits = observe_row<M, TASK>(cfg, s, cs, goal, &g0, &g1, o);
+    write_obs<M, TASK>(cfg, io, row, o);
+    if (io.cam) reinterpret_cast<float2*>(io.cam)[row] = cs;
+    if (io.flags) io.flags[row] = (io.flags[row] & ~FLAG_CLAMP_MASK) | bits;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// per-task launchers (one translation unit per task keeps builds parallel)
+
+inline int grid_for(int n, int block) { return (n + block - 1) / block; }
+inline int launch_status() { return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH; }
+
+template <int M, int T, int NA>
+int run_fwd(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, cudaStream_t s) {
+  if (cfg->reset_mode == 0)
+    k_task_fwd<M, T, NA, true><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io);
+  else
+    k_task_fwd<M, T, NA, false><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io);
+  return launch_status();
+}
+template <int M, int T, int NA>
+int run_bwd(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_grad* g, cudaStream_t s) {
+  k_task_bwd<M, T, NA><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *g);
+  return launch_status();
+}
+template <int M, int T, int NA>
+int run_spawn(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, const uint8_t* mask,
+              const qs_reset_table* tab, cudaStream_t s) {
+  qs_reset_table t{};
+  if (tab) t = *tab;
+  k_task_spawn<M, T, NA><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io, mask, t,
+                                                                    tab != nullptr);
+  return launch_status();
+}
+template <int M, int T, int NA>
+int run_observe(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, cudaStream_t s) {
+  k_task_observe<M, T, NA><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io);
+  return launch_status();
+}
+
+// op: 0 fwd, 1 bwd, 2 spawn, 3 observe
+template <int T>
+int task_dispatch(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
+                  const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
+
+template <int T, int M, int NA>
+int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, const uint8_t* mask,
+            const qs_reset_table* tab, cudaStream_t s) {
+  switch (op) {
+    case 0: return run_fwd<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), s);
+    case 1: return run_bwd<M, T, NA>(cfg, sc, static_cast<const qs_step_grad*>(p), s);
+    case 2: return run_spawn<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), mask, tab, s);
+    case 3: return run_observe<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), s);
+  }
+  return QS_ERR_BAD_ARGUMENT;
+}
+
+#define QS_DEFINE_TASK_DISPATCH(T, MULTI_OK)                                                   \
+  template <>                                                                                 \
+  int task_dispatch<T>(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,     \
+                       const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s) {      \
+    const bool multi = cfg->n_agents > 1;                                                     \
+    if (multi && !(MULTI_OK)) return QS_ERR_BAD_ARGUMENT;                                     \
+    switch (cfg->model) {                                                                     \
+      case QS_MODEL_FULL:                                                                     \
+        return multi ? task_op<T, QS_MODEL_FULL, QS_MAX_AGENTS>(op, cfg, sc, p, mask, tab, s) \
+                     : task_op<T, QS_MODEL_FULL, 1>(op, cfg, sc, p, mask, tab, s);            \
+      case QS_MODEL_PM_CONTINUOUS:                                                            \
+        return multi ? task_op<T, QS_MODEL_PM_CONTINUOUS, QS_MAX_AGENTS>(op, cfg, sc, p, mask, tab, s) \
+                     : task_op<T, QS_MODEL_PM_CONTINUOUS, 1>(op, cfg, sc, p, mask, tab, s);   \
+      case QS_MODEL_PM_DISCRETE:                                                              \
+        return multi ? task_op<T, QS_MODEL_PM_DISCRETE, QS_MAX_AGENTS>(op, cfg, sc, p, mask, tab, s) \
+                     : task_op<T, QS_MODEL_PM_DISCRETE, 1>(op, cfg, sc, p, mask, tab, s);     \
+    }                                                                                         \
+    return QS_ERR_BAD_ARGUMENT;                                                               \
+  }
+
+}  // namespace qs

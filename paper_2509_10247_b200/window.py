@@ -1,0 +1,135 @@
+"""Native BPTT window engine: T fused env steps forward, T analytic VJP steps
+backward, no autograd bookkeeping, optionally replayed from one CUDA graph.
+
+This is ``collect_window`` + ``Tape.backward`` of the reference BPTT learner
+(q/learners.py:201-230, 251-265) for an open-loop action sequence: the loss is
+L = -(1/T) sum_t gamma^t mean(r_ctrl_t) and the engine returns dL/d(raw
+actions).  It drives exactly the same kernels as ``FlightTask.step`` and its
+autograd node (``qs_task_step_fwd`` / ``qs_task_step_bwd``), with every
+per-step checkpoint preallocated so a whole window is graph-capturable.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from paper_2509_10247_b200 import _lib as L
+from paper_2509_10247_b200.tasks import FlightTask
+
+
+class BpttWindow:
+    def __init__(self, env: FlightTask, horizon: int, gamma: float = 0.99, want_obs: bool = True):
+        if env.reset_source is not None:
+            raise ValueError("BpttWindow needs in-kernel (Philox) resets; reset_source forces host syncs")
+        self.env, self.T, self.gamma = env, horizon, gamma
+        dev, N, T = env.device, env.N, horizon
+        f = dict(device=dev, dtype=torch.float32)
+        NP = env._S.shape[0]
+        A, P = env.action_dim, env.proprio_dim
+        self.S = torch.zeros(T + 1, NP, N, 4, **f)
+        self.goal = torch.zeros(T + 1, N, 4, **f)
+        self.peff = torch.zeros(T + 1, N, 4, **f)
+        self.dr = torch.zeros(T + 1, N, 4, **f) if env._dr is not None else None
+        self.flags = torch.zeros(T, N, dtype=torch.int32, device=dev)
+        self.obs = torch.zeros(T, N, P, **f) if want_obs else torch.zeros(1, N, P, **f)
+        self.r = torch.zeros(T, 3, N, **f)  # r_ctrl, r_goal, r_rl
+        self.term = torch.zeros(T, N, dtype=torch.int8, device=dev)
+        self.trunc = torch.zeros(T, N, dtype=torch.bool, device=dev)
+        self.imu = torch.zeros(T, N, 6, **f) if env._imu_bias is not None else None
+        self.actions = torch.zeros(T, N, A, **f)
+        self.g_actions = torch.zeros(T, N, A, **f)
+        self.gS = torch.zeros(2, NP, N, 4, **f)
+        # dL/dr_ctrl_t = -gamma^t / (T N)
+        w = torch.tensor([-(gamma ** t) / (T * N) for t in range(T)], **f)
+        self.g_r = w[:, None].expand(T, N).contiguous()
+        self.w_loss = w[:, None] * 1.0
+        self.loss = torch.zeros((), **f)
+        self.want_obs = want_obs
+        self.graph = None
+        self.launches_per_window = 2 * T
+        self._load_env_state()
+
+    def _load_env_state(self):
+        e = self.env
+        self.S[0].copy_(e._S.detach())
+        self.goal[0].copy_(e._goal)
+        self.peff[0].copy_(e._peff)
+        if self.dr is not None:
+            self.dr[0].copy_(e._dr)
+
+    def _store_env_state(self):
+        e = self.env
+        e._S = self.S[self.T].clone()
+        e._goal = self.goal[self.T].clone()
+        e._peff = self.peff[self.T].clone()
+        if self.dr is not None:
+            e._dr = self.dr[self.T].clone()
+
+    def _run(self):
+        e = self.env
+        lib = L.lib()
+        cfg, sc = e._cfg, e._scene.struct()
+        stream = L.stream_handle(e.device)
+        T = self.T
+        for t in range(T):
+            io = e._new_io()
+            io.S_in, io.S_out, io.raw = L.ptr(self.S[t]), L.ptr(self.S[t + 1]), L.ptr(self.actions[t])
+            io.goal_in, io.goal_out = L.ptr(self.goal[t]), L.ptr(self.goal[t + 1])
+            io.peff_in, io.peff_out = L.ptr(self.peff[t]), L.ptr(self.peff[t + 1])
+            if self.dr is not None:
+                io.dr_in, io.dr_out = L.ptr(self.dr[t]), L.ptr(self.dr[t + 1])
+            if self.imu is not None:
+                io.imu_out = L.ptr(self.imu[t])
+            io.obs = L.ptr(self.obs[t if self.want_obs else 0])
+            io.r_ctrl, io.r_goal, io.r_rl = L.ptr(self.r[t, 0]), L.ptr(self.r[t, 1]), L.ptr(self.r[t, 2])
+            io.terminated, io.truncated, io.flags = L.ptr(self.term[t]), L.ptr(self.trunc[t]), L.ptr(self.flags[t])
+            lib.qs_task_step_fwd(cfg, sc, io, stream)
+        for t in reversed(range(T)):
+            g = L.QsStepGrad()
+            g.S_in, g.raw, g.goal_in, g.peff_in = L.ptr(self.S[t]), L.ptr(self.actions[t]), L.ptr(self.goal[t]), L.ptr(self.peff[t])
+            g.dr_in = L.ptr(self.dr[t]) if self.dr is not None else None
+            g.flags = L.ptr(self.flags[t])
+            g.g_S_out = L.ptr(self.gS[(t + 1) % 2]) if t < T - 1 else None
+            g.g_rctrl = L.ptr(self.g_r[t])
+            g.g_S_in, g.g_raw = L.ptr(self.gS[t % 2]), L.ptr(self.g_actions[t])
+            lib.qs_task_step_bwd(cfg, sc, g, stream)
+        torch.sum(self.r[:, 0] * self.w_loss, out=self.loss)
+        # carry the final state into slot 0 for the next window
+        self.S[0].copy_(self.S[T])
+        self.goal[0].copy_(self.goal[T])
+        self.peff[0].copy_(self.peff[T])
+        if self.dr is not None:
+            self.dr[0].copy_(self.dr[T])
+
+    def capture(self):
+        """Record one window into a CUDA graph (replayed by ``run``)."""
+        s = torch.cuda.Stream(self.env.device)
+        s.wait_stream(torch.cuda.current_stream(self.env.device))
+        snap = [x.clone() for x in (self.S[0], self.goal[0], self.peff[0], self.env._meta, self.env._ep_ret,
+                                    self.env._stats)]
+        with torch.cuda.stream(s):
+            self._run()  # warm-up outside capture (lazy init)
+        torch.cuda.current_stream(self.env.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._run()
+        # capture launches nothing; warm-up did: restore the pre-warm-up state
+        for dst, src in zip((self.S[0], self.goal[0], self.peff[0], self.env._meta, self.env._ep_ret,
+                             self.env._stats), snap):
+            dst.copy_(src)
+        self.graph = g
+        return self
+
+    def run(self, actions: torch.Tensor | None = None):
+        """One window (fwd + bwd).  Returns (loss tensor, dL/d actions (T,N,A))."""
+        if actions is not None:
+            self.actions.copy_(actions, non_blocking=True)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._run()
+        return self.loss, self.g_actions
+
+    def sync_env(self):
+        """Write the window's final state back into the env object."""
+        self._store_env_state()
