@@ -1,0 +1,452 @@
+"""Benchmark: env-steps/s (fwd+bwd) of the quadsim hot path on B200.
+
+Headline workload (BASELINE.json configs[1], C2): full rigid-body quadrotor +
+IMU noise, position task, 65,536 envs per GPU, BPTT windows of T=32 steps
+(forward: fused env-step kernel; backward: analytic VJP kernel), open-loop
+synthetic actions N(0, 0.3^2).  One bench "step" = one window fwd+bwd.
+Secondary: depth rays/s for C3 (16,384 envs, 64x48 camera, 32 solids + ground).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU: one process per GPU under torchrun; envs shard across ranks with
+no communication inside the sim step (weak scaling); timing is the max over
+ranks of CUDA-event time.  ``--impl reference`` times the CPU oracle port of
+the same workload (numpy fp64, reference algorithm incl. its reverse pass) on
+all host cores, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/s (fwd+bwd)"
+UNIT = "env-steps/s"
+IMU = dict(accel_noise_std=0.1, gyro_noise_std=0.01, accel_bias_rw_std=0.01, gyro_bias_rw_std=0.001)
+
+# algorithmic bytes per env-step of the fused-window kernels,
+# full+IMU, open-loop BPTT, unpadded payload:
+#   fwd: raw 16 + checkpoint state 52 + goal 12 + prev effort 16 + obs 48
+#        + rewards 12 + term/trunc 2 + flags 4 + IMU 24          = 186
+#   bwd: checkpoint state 52 + raw 16 + goal 12 + prev effort 16 + flags 4
+#        + dL/draw 16                                            = 116
+FWD_BYTES = 186
+BWD_BYTES = 116
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--envs", type=int, default=65536)
+    ap.add_argument("--horizon", type=int, default=32)
+    ap.add_argument("--model", default="full")
+    ap.add_argument("--no-depth", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no cpu/clock sampling)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port (reference algorithm, numpy fp64)
+
+
+def _cpu_worker(args):
+    n_envs, T, model, seconds, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import quadsim_oracle as O
+
+    cfg = O.Config(task="position", dynamics=model, n_envs=n_envs, episode_len=128, dt=0.05)
+    env = O.OracleTask(cfg, imu=dict(IMU, seed=seed))
+    env.reset(seed)
+    rng = np.random.default_rng(seed)
+    A = O.MODEL_ACTION_DIM[model]
+    done_steps = 0
+    t0 = time.perf_counter()
+    while True:
+        acts = rng.normal(size=(T, n_envs, A)) * 0.3
+        O.window_value_and_grad(env, acts)
+        done_steps += n_envs * T
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return done_steps, el
+
+
+def cpu_baseline(seconds: float, model: str, T: int, n_sample: int = 4096):
+    cores = len(os.sched_getaffinity(0))
+    per = max(1, n_sample // cores)
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_worker, [(per, T, model, seconds, 1000 + i) for i in range(cores)])
+    steps = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": steps / wall, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{cores} procs x {per} envs, {model}+IMU position task, T={T} windows fwd+bwd "
+                      f"(numpy fp64 oracle incl. reverse pass) for {wall:.1f}s"}
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    """SM clock + throttle reasons sampled every 20 ms through NVML while the
+    timed region runs (the same counters nvidia-smi reports)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.result = None
+        self._stop = False
+
+    def _loop(self):
+        import pynvml as nv
+
+        h = nv.nvmlDeviceGetHandleByIndex(self.gpu)
+        self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop:
+            try:
+                self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                self.masks.append(nv.nvmlDeviceGetCurrentClocksEventReasons(h))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        import threading
+
+        self.sm, self.masks, self.max_mhz = [], [], None
+        try:
+            import pynvml as nv
+
+            nv.nvmlInit()
+            dev = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if dev and dev.split(",")[0].isdigit():
+                self.gpu = int(dev.split(",")[self.gpu]) if self.gpu < len(dev.split(",")) else self.gpu
+            self.th = threading.Thread(target=self._loop, daemon=True)
+            self.th.start()
+        except Exception as ex:  # pragma: no cover
+            self.th = None
+            self.result = {"error": str(ex)}
+        return self
+
+    def __exit__(self, *a):
+        if getattr(self, "th", None) is None:
+            return
+        self._stop = True
+        self.th.join(timeout=2)
+        if self.sm:
+            reasons = sorted({n for m in self.masks for n, b in self.REASONS.items() if m & b})
+            self.result = {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz,
+                           "reasons": reasons, "samples": len(self.sm), "source": "NVML during timed region"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_init():
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def time_graph(fn, iters: int) -> float:
+    import torch
+
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def bench_depth(dev, rank, frames=20):
+    """C3: 16,384 envs, 64x48 depth, 32 solids (10 sph, 9 box, 13 cyl) + ground."""
+    import torch
+
+    from paper_2509_10247_b200 import sensors as sn
+    from paper_2509_10247_b200 import world as wd
+
+    E = 16384
+    spawn, goal = np.array([0.0, 0.0, 1.2]), np.array([8.0, 0.0, 1.5])
+    sc = wd.gen_obstacle_courses(3 + rank, E, spawn, goal, density=32 / 48.0, device=dev,
+                                 env_offset=rank * E, check=False)
+    g = torch.Generator(device="cpu").manual_seed(7 + rank)
+    along = torch.rand(E, generator=g) * 8.0
+    lat = (torch.rand(E, generator=g) - 0.5) * 6.0
+    z = 0.5 + torch.rand(E, generator=g) * 3.0
+    yaw = torch.rand(E, generator=g) * 2 * np.pi
+    pos = torch.zeros(E, 4)
+    pos[:, 0], pos[:, 1], pos[:, 2] = along, lat, z
+    pos = pos.to(dev)
+    cs = torch.stack([torch.cos(yaw), torch.sin(yaw)], -1).to(dev).contiguous()
+    cam = sn.CameraIntrinsics(width=64, height=48, max_range=10.0)
+    R = cam.n_rays
+
+    def frame():
+        sn.cast_rays(sc, pos, 4, cs, cam, 0, True)
+
+    for _ in range(3):
+        frame()
+    ms = time_graph(frame, frames)
+    cnt = sc.counts.double().cpu().numpy()
+    # un-culled algorithmic flops per ray: 14 + 10 ns + 6 nb + 31 nc (+1 ground)
+    flops_frame = float(np.sum(14 + 10 * cnt[:, 0] + 6 * cnt[:, 1] + 31 * cnt[:, 2] + cnt[:, 3])) * R
+    return {"rays_per_s": E * R / (ms * 1e-3), "ms_per_frame": ms, "n_envs": E, "rays_per_env": R,
+            "mean_solids": float(cnt[:, :3].sum(1).mean()),
+            "tflops_uncull_equiv": flops_frame / (ms * 1e-3) / 1e12}
+
+
+def run_ours(a):
+    import torch
+
+    world, rank, local = dist_init()
+    dev = torch.device("cuda", local if world > 1 else 0)
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.window import BpttWindow
+
+    N, T = a.envs, a.horizon
+    cfg = qs.TaskConfig(task="position", dynamics=a.model, n_envs=N, episode_len=128,
+                        imu=qs.ImuSpec(**IMU) if a.model == "full" else None)
+    env = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
+    env.reset(seed=1)
+    win = BpttWindow(env, T)
+    g = torch.Generator(device="cpu").manual_seed(1234 + rank)
+    actions = (torch.randn(T, N, env.action_dim, generator=g) * 0.3).to(dev)
+    win.actions.copy_(actions)
+    win.capture()
+    if a.profile:
+        for _ in range(max(1, a.warmup)):
+            win.run()
+        torch.cuda.synchronize()
+        print(json.dumps({"profile_run": True, "loss": float(win.loss)}))
+        return
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(a.warmup):
+            win.run()
+        torch.cuda.synchronize()
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            win.run()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = e0.elapsed_time(e1) / a.steps
+    ms = max_over_ranks(ms, world)
+    value = world * N * T / (ms * 1e-3)
+    loss = float(win.loss)
+    assert np.isfinite(loss)
+
+    # per-kernel durations: one graph holding only the window-forward launch,
+    # one holding only the window-backward launch (same buffers as above)
+    from paper_2509_10247_b200 import _lib as L
+
+    lib = L.lib()
+
+    def fwd_only():
+        L.check(lib.qs_task_window_fwd(env._cfg, env._scene.struct(), win._window_io(), L.stream_handle(dev)), "fwd")
+
+    def bwd_only():
+        L.check(lib.qs_task_window_bwd(env._cfg, env._scene.struct(), win._window_io(), L.stream_handle(dev)), "bwd")
+
+    graphs = {}
+    for name, fn in (("fwd", fwd_only), ("bwd", bwd_only)):
+        fn()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            fn()
+        graphs[name] = gr
+    reps = max(5, a.steps // 2)
+    ms_fwd = time_graph(graphs["fwd"].replay, reps)
+    ms_bwd = time_graph(graphs["bwd"].replay, reps)
+    peak = 6553.3
+    try:
+        peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    gbs_fwd = FWD_BYTES * N * T / (ms_fwd * 1e-3) / 1e9
+    gbs_bwd = BWD_BYTES * N * T / (ms_bwd * 1e-3) / 1e9
+    dom = "fwd" if ms_fwd >= ms_bwd else "bwd"
+    achieved = gbs_fwd if dom == "fwd" else gbs_bwd
+    traffic = None
+    try:
+        traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"window_{dom}")
+    except Exception:
+        pass
+    # the per-step kernels behind FlightTask.step (closed-loop path), same workload
+    win_ps = BpttWindow(env, T, fused=False)
+    win_ps.actions.copy_(actions)
+    win_ps.capture()
+    ms_per_step_path = time_graph(lambda: win_ps.run(), reps)
+    del win_ps
+
+    # e2e through the public window API: pinned host actions in, loss out
+    host = actions.cpu().pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_iters = max(3, min(a.steps, 20))
+    for _ in range(e2e_iters):
+        loss_t, _ = win.run(host)
+        float(loss_t.item())
+    e2e_s = (time.perf_counter() - t0) / e2e_iters
+    e2e_s = max_over_ranks(e2e_s, world)
+    e2e = {"value": world * N * T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": host.numel() * 4,
+           "d2h_bytes_per_step": 4, "api": "paper_2509_10247_b200.window.BpttWindow.run(host actions)"}
+
+    # eager public API (env.step + torch.autograd) for reference, 1 window
+    eager = None
+    if rank == 0:
+        env2 = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
+        env2.reset(seed=1)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(2):
+            acts = host.to(dev, non_blocking=True).requires_grad_(True)
+            env2.detach_states()
+            tot = 0.0
+            for t in range(T):
+                tot = tot + env2.step(acts[t]).r_ctrl.mean() * 0.99 ** t
+            loss_e = -tot / T
+            loss_e.backward()
+            float(loss_e.item())
+        eager = {"value": N * T / ((time.perf_counter() - t0) / 2), "unit": UNIT,
+                 "api": "FlightTask.step + torch.autograd backward, per window"}
+        del env2
+
+    depth = None
+    if not a.no_depth:
+        depth = bench_depth(dev, rank)
+        depth["rays_per_s"] = depth["rays_per_s"] * world if world > 1 else depth["rays_per_s"]
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        depth["fp32_peak_tflops"] = round(fp32_peak, 1)
+        depth["fp32_peak_source"] = "computed 148 SM x 128 FMA lanes x 2 x 1.965 GHz (not in MEASURED_PEAKS.json)"
+        depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / fp32_peak
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_baseline(a.cpu_seconds, a.model, T)
+        cpu["host"] = cpu_model()
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (in-kernel Philox resets, actions N(0,0.3^2))",
+        "config": {"workload": f"C2: {a.model} quadrotor + IMU, position task, {N} envs/GPU, BPTT window T={T} "
+                               f"fwd+bwd (open-loop actions)", "envs_per_gpu": N, "horizon": T,
+                   "parallelism": f"env-sharded x{world}, no collective in the sim step",
+                   "l2": "window footprint ~%d MB > 126 MB L2 (no flush needed)" % int(
+                       (win.S.numel() + win.obs.numel() + win.goal.numel() * 2 + win.actions.numel() * 2) * 4 / 1e6)},
+        "roofline": {"bound": "hbm", "kernel": f"k_window_{dom} (qs_task_window_{dom})", "achieved": achieved,
+                     "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_env_step": {"fwd": FWD_BYTES, "bwd": BWD_BYTES},
+                     "units_per_launch": N * T, "ms_per_launch": {"fwd": ms_fwd, "bwd": ms_bwd},
+                     "gbs": {"fwd": gbs_fwd, "bwd": gbs_bwd}, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        "per_step_kernels": {"ms_per_window": ms_per_step_path,
+                             "env_steps_per_s": world * N * T / (ms_per_step_path * 1e-3),
+                             "note": "same window through the per-step kernels behind FlightTask.step"},
+        "e2e": e2e, "e2e_eager": eager,
+        "gpu_launches": a.steps * win.launches_per_window,
+        "clocks": getattr(clk, "result", None),
+        "cpu_baseline": cpu,
+        "depth": depth,
+        "loss": loss,
+    }
+    print(json.dumps(line))
+
+
+def run_reference(a):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    per_step_seconds = max(2.0, min(10.0, 60.0 / max(1, a.steps + a.warmup)))
+    for _ in range(a.warmup):
+        cpu_baseline(min(2.0, per_step_seconds), a.model, a.horizon, n_sample=1024)
+    vals = []
+    last = None
+    for _ in range(a.steps):
+        last = cpu_baseline(per_step_seconds, a.model, a.horizon)
+        vals.append(last["value"])
+    v = statistics.median(vals)
+    ms = a.envs * a.horizon / v * 1e3
+    last["value"] = v
+    last["host"] = cpu_model()
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "config": {
+            "workload": f"C2: {a.model} quadrotor + IMU, position task, BPTT window T={a.horizon} fwd+bwd; "
+                        f"CPU oracle port on a bounded env sample"},
+        "cpu_baseline": last, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)

@@ -139,6 +139,31 @@ typedef struct qs_reset_table {
   const int32_t* next_gate; /* (E,) | NULL */
 } qs_reset_table;
 
+/* A fused T-step window (open-loop actions, in-kernel resets): the env's
+ * state stays in registers across the T steps.  Checkpoint slot 0 holds the
+ * window's initial state; slot t+1 receives the state after step t (the
+ * backward's checkpoints).  Per-step outputs are stacked on a leading T axis. */
+typedef struct qs_window_io {
+  int32_t T;
+  float* S;          /* (T+1,NP,N,4) */
+  float* goal;       /* (T+1,N,4) */
+  float* peff;       /* (T+1,N,4) */
+  float* dr;         /* (T+1,N,4) | NULL */
+  const float* actions; /* (T,N,A) raw actions */
+  int32_t* meta; float* ep_return; float* imu_bias;  /* in place, as qs_step_io */
+  const float* imu_noise;  /* (T,4,N,3) | NULL */
+  float* imu_out;    /* (T,N,6) | NULL */
+  float* obs;        /* (T,N,P) | NULL (observation not materialised) */
+  float* r;          /* (T,3,N) r_ctrl, r_goal, r_rl */
+  int8_t* terminated; uint8_t* truncated; int32_t* flags;  /* (T,N) */
+  double* stats; int32_t* err;
+  /* backward: dL/dr_ctrl[t,row] = g_rctrl[t,row], or g_rctrl_scale * gamma^t when NULL */
+  const float* g_rctrl; float g_rctrl_scale, gamma;
+  const float* g_S_final;  /* (NP,N,4) | NULL */
+  float* g_actions;        /* (T,N,A) */
+  float* g_S0;             /* (NP,N,4) | NULL */
+} qs_window_io;
+
 int qs_abi_version(void);
 int qs_proprio_dim(int32_t model, int32_t task);
 int qs_state_planes(int32_t model);
@@ -151,6 +176,13 @@ int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_ste
  * recorded by FlightTask.step; subgradients per q/autodiff.py). */
 int qs_task_step_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_grad* g,
                      void* stream);
+/* collect_window + Tape.backward of the BPTT learner for open-loop actions
+ * (q/learners.py:201-265): T fused steps forward / T analytic VJPs backward in
+ * one launch each. */
+int qs_task_window_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_window_io* w,
+                       void* stream);
+int qs_task_window_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_window_io* w,
+                       void* stream);
 /* _spawn_all (q/tasks.py:687-721, 789-815, 873-902) + _redraw_randomization
  * (:377-387) for masked envs, writing into io->S_out/goal_out/peff_out/dr_out
  * in place; table==NULL -> in-kernel Philox sampling. */

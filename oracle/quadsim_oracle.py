@@ -1368,3 +1368,168 @@ def fd_grad_actions(env: OracleTask, actions, gamma=0.99, h_scale=1e-6):
                 g[t, rows, k] = (lp - lm) / (2.0 * h)
     env.restore(snap)
     return g
+
+
+# ---------------------------------------------------------------------------
+# reverse pass (restates the reference tape's backward for the position task,
+# q/autodiff.py:201-237 over the ops recorded by q/tasks.py:549-637).  Used as
+# the CPU baseline of the fwd+bwd benchmark and pinned to the golden tape
+# gradients in tests/test_oracle_golden.py.
+
+
+def _qconj(q):
+    return np.concatenate([q[:, :1], -q[:, 1:]], axis=-1)
+
+
+def _qrot_vjp_q(q, v, g):
+    u, w = q[:, 1:], q[:, :1]
+    v = np.broadcast_to(v, u.shape)
+    gw = 2.0 * np.sum(g * np.cross(u, v), axis=-1, keepdims=True)
+    gu = (2.0 * w * np.cross(v, g) + 2.0 * np.sum(u * v, -1, keepdims=True) * g
+          + 2.0 * np.sum(g * u, -1, keepdims=True) * v - 4.0 * np.sum(g * v, -1, keepdims=True) * u)
+    return np.concatenate([gw, gu], axis=-1)
+
+
+def _norm_vjp(a, n, g):
+    safe = np.maximum(n, np.finfo(np.float64).tiny)
+    return (g / safe)[:, None] * a
+
+
+def step_full_vjp(st, act, prm: Params, gs):
+    """VJP of step_full (q/dynamics.py:155-186)."""
+    p, v, q, w = st["p"], st["v"], st["q"], st["w"]
+    c = act[:, 0:1]
+    dt = prm.dt
+    zero = np.zeros((q.shape[0], 1))
+    r = np.concatenate([zero, w], axis=-1)
+    qd = quat_mul(q, r) * 0.5
+    qn = q + qd * dt
+    nn = np.sqrt(np.sum(qn * qn, -1, keepdims=True))
+    qo = qn / nn
+    gq_ = gs["q"]
+    gqn = (gq_ - qo * np.sum(qo * gq_, -1, keepdims=True)) / nn
+    gqd = gqn * dt * 0.5
+    gq = gqn + quat_mul(gqd, _qconj(r))
+    gw_q = quat_mul(_qconj(q), gqd)[:, 1:]
+    gwdot = gs["w"] * dt
+    K = prm.rate_gains
+    g_wc = K * gwdot
+    gw = gs["w"] - K * gwdot + gw_q
+    gvdot = gs["v"] * dt
+    gp = gs["p"].copy()
+    gv = gs["v"] + gs["p"] * dt
+    zb = quat_rotate(q, np.array([0.0, 0.0, 1.0]))
+    g_c = np.sum(gvdot * zb, -1, keepdims=True)
+    gq = gq + _qrot_vjp_q(q, np.array([0.0, 0.0, 1.0]), gvdot * c)
+    D = prm.drag_matrix_diag
+    if np.any(D != 0):
+        qc = _qconj(q)
+        vb = quat_rotate(qc, v)
+        dv = D * vb
+        gdrag = -gvdot
+        gq = gq + _qrot_vjp_q(q, dv, gdrag)
+        gdv = quat_rotate(qc, gdrag)
+        gvb = D * gdv
+        gv = gv + quat_rotate(q, gvb)
+        g2 = _qrot_vjp_q(qc, v, gvb)
+        gq = gq + np.concatenate([g2[:, :1], -g2[:, 1:]], -1)
+    return {"p": gp, "v": gv, "q": gq, "w": gw}, np.concatenate([g_c, g_wc], -1)
+
+
+def model_step_vjp(model, st, act, prm: Params, gs):
+    if model == "full":
+        return step_full_vjp(st, act, prm, gs)
+    dt = prm.dt
+    B = act.shape[0]
+    if model == "pm_continuous":
+        decay = _bcast(prm.lag_decay, B)
+        d = _bcast(prm.drag_coeff, B)
+        ga = gs["a_lat"] + gs["v"] * dt
+        return ({"p": gs["p"].copy(), "v": gs["v"] - gs["v"] * (d * dt) + gs["p"] * dt, "a_lat": ga * decay},
+                ga - ga * decay)
+    gu = gs["p"] * (0.5 * dt * dt) + gs["v"] * (0.5 * dt) + gs["u_prev"]
+    return ({"p": gs["p"].copy(), "v": gs["v"] + gs["p"] * dt, "u_prev": gs["v"] * (0.5 * dt)}, gu)
+
+
+def reward_ctrl_vjp(w: Weights, off, v, eff, deff, g):
+    """VJP of reward_position + velocity_field_error (q/tasks.py:144-165, 625-637)."""
+    dist = np.linalg.norm(off, axis=-1)
+    speed = np.linalg.norm(v, axis=-1)
+    x = (w.near_radius - dist) * (1.0 / w.near_width)
+    near = _stable_sigmoid(x)
+    m = np.maximum(dist, 1e-9)
+    sd = np.minimum(dist * w.track_gain, w.v_max)
+    k = sd / m
+    vdes = off * k[:, None]
+    ev = v - vdes
+    track = np.linalg.norm(ev, axis=-1)
+    gp = -g
+    g_dist = gp * w.w_p
+    g_speed = gp * w.w_v * near
+    g_near = gp * w.w_v * speed
+    g_dist = g_dist + g_near * near * (1 - near) * (-1.0 / w.near_width)
+    gev = _norm_vjp(ev, track, gp * w.w_t)
+    g_v = gev + _norm_vjp(v, speed, g_speed)
+    g_vdes = -gev
+    g_off = g_vdes * k[:, None]
+    g_k = np.sum(g_vdes * off, -1)
+    g_sd = g_k / m
+    g_m = -g_k * sd / (m * m)
+    g_dist = g_dist + np.where(dist * w.track_gain <= w.v_max, g_sd * w.track_gain, 0.0)
+    g_dist = g_dist + np.where(dist >= 1e-9, g_m, 0.0)
+    g_off = g_off + _norm_vjp(off, dist, g_dist)
+    en = np.linalg.norm(eff, axis=-1)
+    dn = np.linalg.norm(deff, axis=-1)
+    g_eff = _norm_vjp(eff, en, gp * w.w_a) + _norm_vjp(deff, dn, gp * w.w_s)
+    return g_off, g_v, g_eff
+
+
+def window_value_and_grad(env: OracleTask, actions, gamma=0.99):
+    """Position-task BPTT window: L and dL/d(raw actions) by the reverse pass.
+
+    Forward runs env.step (resets included); the backward replays the
+    recorded checkpoints in reverse with the tape's semantics: yaw frame and
+    prev_effort constant, gradient cut at resets (q/tasks.py:712-721).
+    """
+    cfg = env.cfg
+    assert cfg.task == "position" and env.n_agents == 1
+    T, N, A = actions.shape
+    recs = []
+    loss = 0.0
+    for t in range(T):
+        st = {k: v.copy() for k, v in env.state.items()}
+        yaw = env.yaw() if env.model.startswith("pm") else None
+        lo, hi = env.act_lo.copy(), env.act_hi.copy()
+        prm = copy.copy(env.params)
+        goals, peff = env.goals.copy(), env.prev_effort.copy()
+        out = env.step(actions[t])
+        loss += gamma ** t * out["r_ctrl"].mean()
+        recs.append((st, yaw, lo, hi, prm, goals, peff, out["state2"], out["done"]))
+    loss = -loss / T
+    g_act = np.zeros_like(actions)
+    gS_next = None
+    for t in reversed(range(T)):
+        st, yaw, lo, hi, prm, goals, peff, st2, done = recs[t]
+        raw = actions[t]
+        th = np.tanh(raw)
+        half = (hi - lo) * 0.5
+        center = (lo + hi) * 0.5
+        sq = center + half * th
+        eff = sq - center
+        deff = eff - peff
+        cmd = matvec(rotz(yaw), sq) if yaw is not None else sq
+        gs2 = {k: np.zeros_like(v) for k, v in st2.items()}
+        if gS_next is not None:
+            keep = (~done)[:, None]
+            for k in gs2:
+                gs2[k] = np.where(keep, gS_next[k], 0.0)
+        g_r = np.full(N, -(gamma ** t) / (T * N))
+        g_off, g_v, g_eff = reward_ctrl_vjp(cfg.weights, goals - st2["p"], st2["v"], eff, deff, g_r)
+        gs2["p"] = gs2["p"] - g_off
+        gs2["v"] = gs2["v"] + g_v
+        gS, g_cmd = model_step_vjp(env.model, st, cmd, prm, gs2)
+        g_sq = matvec(np.swapaxes(rotz(yaw), -1, -2), g_cmd) if yaw is not None else g_cmd
+        g_sq = g_sq + g_eff
+        g_act[t] = g_sq * half * (1.0 - th * th)
+        gS_next = gS
+    return loss, g_act

@@ -74,6 +74,13 @@ class QsStepGrad(C.Structure):
         "g_S_in", "g_raw")]
 
 
+class QsWindowIo(C.Structure):
+    _fields_ = [("T", i32)] + [(n, vp) for n in (
+        "S", "goal", "peff", "dr", "actions", "meta", "ep_return", "imu_bias", "imu_noise", "imu_out",
+        "obs", "r", "terminated", "truncated", "flags", "stats", "err", "g_rctrl")] + [
+        ("g_rctrl_scale", f32), ("gamma", f32)] + [(n, vp) for n in ("g_S_final", "g_actions", "g_S0")]
+
+
 class QsResetTable(C.Structure):
     _fields_ = [(n, vp) for n in ("env_mask", "p", "v", "goal", "v_ema", "dr", "next_gate")]
 
@@ -99,6 +106,8 @@ _SIGS = {
     "qs_task_step_bwd": ([P(QsTaskCfg), P(QsScene), P(QsStepGrad), vp], i32),
     "qs_task_spawn": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp, P(QsResetTable), vp], i32),
     "qs_task_observe": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp], i32),
+    "qs_task_window_fwd": ([P(QsTaskCfg), P(QsScene), P(QsWindowIo), vp], i32),
+    "qs_task_window_bwd": ([P(QsTaskCfg), P(QsScene), P(QsWindowIo), vp], i32),
     "qs_raycast": ([P(QsRayCfg), P(QsScene), i32, vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "qs_raycast_vjp": ([i32, i32, vp, vp, vp, i32, vp], i32),
     "qs_sdf": ([P(QsScene), i32, i32, vp, vp, vp, vp], i32),

@@ -122,14 +122,20 @@ struct Rng {
     return make_float4(((r.x >> 8) + 0.5f) * s, ((r.y >> 8) + 0.5f) * s, ((r.z >> 8) + 0.5f) * s,
                        ((r.w >> 8) + 0.5f) * s);
   }
-  // four standard normals (Box-Muller on two pairs)
+  // four standard normals (Box-Muller on two pairs).  MUFU intrinsics: the
+  // ~2-ulp error of lg2/sqrt/sin/cos is immaterial for sampling noise.
   QS_D float4 normal4() {
     float4 u = uniform4();
-    float r0 = sqrtf(-2.f * logf(u.x)), r1 = sqrtf(-2.f * logf(u.z));
+    float r0 = sqrt_fast(-2.f * __logf(u.x)), r1 = sqrt_fast(-2.f * __logf(u.z));
     float s0, c0, s1, c1;
-    sincospif(2.f * u.y, &s0, &c0);
-    sincospif(2.f * u.w, &s1, &c1);
+    __sincosf(6.28318530717958648f * u.y, &s0, &c0);
+    __sincosf(6.28318530717958648f * u.w, &s1, &c1);
     return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+  }
+  QS_D static float sqrt_fast(float x) {
+    float d;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(x));
+    return d;
   }
 };
 

@@ -54,4 +54,15 @@ int qs_task_observe(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step
   return task_call(3, cfg, scene, io, nullptr, nullptr, stream);
 }
 
+int qs_task_window_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_window_io* w,
+                       void* stream) {
+  if (cfg && cfg->reset_mode != 0) return QS_ERR_BAD_ARGUMENT;  // windows reset in-kernel
+  return task_call(4, cfg, scene, w, nullptr, nullptr, stream);
+}
+
+int qs_task_window_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_window_io* w,
+                       void* stream) {
+  return task_call(5, cfg, scene, w, nullptr, nullptr, stream);
+}
+
 }  // extern "C"

@@ -204,16 +204,16 @@ QS_D float4 dr_sample(const qs_task_cfg& cfg, long row, int episode) {
 }
 
 // ---------------------------------------------------------------------------
-// IMU read (q/sensors.py:540-555) on the post-dynamics state
+// IMU read (q/sensors.py:540-555) on the post-dynamics state.  Bias state lives
+// in registers (ba, bg); noise is injected (noise != NULL, (4,N,3)) or Philox.
 
 template <int M>
-QS_D void imu_row(const qs_task_cfg& cfg, const qs_step_io& io, long row, long N, int tick,
-                  const State& s2, V3 vdot, V3 g) {
-  float4 b0 = ld4(io.imu_bias, 2 * row), b1 = ld4(io.imu_bias, 2 * row + 1);
+QS_D void imu_apply(const qs_task_cfg& cfg, long row, long N, int tick, const State& s2, V3 vdot, V3 g,
+                    float4& b0, float4& b1, const float* noise, float* out) {
   V3 ba = xyz(b0), bg = xyz(b1);
   V3 nba, nbg, na, ng;
-  if (io.imu_noise) {
-    const float* z = io.imu_noise;
+  if (noise) {
+    const float* z = noise;
     nba = v3(z[3 * row], z[3 * row + 1], z[3 * row + 2]);
     nbg = v3(z[3 * (N + row)], z[3 * (N + row) + 1], z[3 * (N + row) + 2]);
     na = v3(z[3 * (2 * N + row)], z[3 * (2 * N + row) + 1], z[3 * (2 * N + row) + 2]);
@@ -244,12 +244,13 @@ QS_D void imu_row(const qs_task_cfg& cfg, const qs_step_io& io, long row, long N
   if (cfg.imu_accel_std != 0.f) acc += na * cfg.imu_accel_std;
   V3 gy = w + bg;
   if (cfg.imu_gyro_std != 0.f) gy += ng * cfg.imu_gyro_std;
-  st4(io.imu_bias, 2 * row, f4(ba, 0.f));
-  st4(io.imu_bias, 2 * row + 1, f4(bg, 0.f));
-  float* o = io.imu_out + 6 * row;
+  b0 = f4(ba, 0.f);
+  b1 = f4(bg, 0.f);
+  float* o = out + 6 * row;
   o[0] = acc.x; o[1] = acc.y; o[2] = acc.z;
   o[3] = gy.x; o[4] = gy.y; o[5] = gy.z;
 }
+
 
 // ---------------------------------------------------------------------------
 // rewards (q/tasks.py:144-170, 625-637, 744-763, 817-844)
@@ -331,8 +332,9 @@ QS_D void f4set(float4& v, int k, float x) {
 
 template <int A>
 QS_D float4 load_act(const float* raw, long row) {
+  if (A == 4) return ld4(raw, row);  // 16-byte rows: one vector load
   const float* p = raw + row * A;
-  return make_float4(p[0], p[1], p[2], A == 4 ? p[3] : 0.f);
+  return make_float4(__ldg(p), __ldg(p + 1), __ldg(p + 2), 0.f);
 }
 
 template <int A>
@@ -394,232 +396,325 @@ QS_D void warp_stats(bool active, bool done, int term, float ret, double* stats)
 }
 
 // ---------------------------------------------------------------------------
-// forward
+// per-env register file: everything one env carries from step to step
 
-template <int M, int TASK, int NAMAX, bool INLINE>
-__global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const qs_scene sc,
-                                                  const qs_step_io io) {
-  constexpr int A = ModelTraits<M>::A;
-  constexpr int P = TaskTraits<M, TASK>::P;
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = e < cfg.n_envs;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
-  const long N = (long)cfg.n_envs * na;
-  const DynK k = dyn_consts(cfg);
-  bool done = false;
-  int term_env = 0;
-  float ret_env = 0.f;
-  if (active) {
-    int4 meta = reinterpret_cast<int4*>(io.meta)[e];
-    State s2[NAMAX];
-    float rc[NAMAX], rl[NAMAX];
-    float4 eff[NAMAX];
-    int codes[NAMAX];
-    float4 drs[NAMAX];
-    bool all_goal = true, any_oob = false, any_coll = false;
-    V3 p0 = v3(0.f, 0.f, 0.f);
-    SceneView sv;
-    if (TASK == QS_TASK_AVOIDANCE) sv = scene_view(sc, e);
-    const V3 blo = xyz(ld4(sc.bounds, 2 * e)) + v3(1e-6f, 1e-6f, 1e-6f);
-    const V3 bhi = xyz(ld4(sc.bounds, 2 * e + 1)) - v3(1e-6f, 1e-6f, 1e-6f);
+template <int NAMAX>
+struct EnvRegs {
+  State s[NAMAX];
+  float4 goal[NAMAX], peff[NAMAX], dr[NAMAX];
+  float4 ba[NAMAX], bg[NAMAX];  // IMU bias (accel, gyro)
+  int4 meta;                    // steps_in_episode, episode, tick, next_gate
+  float ep_ret;
+  V3 blo, bhi;                  // bounds shrunk by 1e-6 (q/tasks.py:673-674)
+};
+
+// pointers of one step's outputs (rows are env-major, N = n_envs * n_agents)
+struct StepOut {
+  float* obs;
+  float* r_ctrl;
+  float* r_goal;
+  float* r_rl;
+  int8_t* term;
+  uint8_t* trunc;
+  int32_t* flags;
+  float* cam;
+  float* imu_out;
+  const float* imu_noise;
+};
+
+template <int M>
+QS_D RowPrm row_params_v(const qs_task_cfg& cfg, bool has_dr, float4 d) {
+  RowPrm r;
+  float scale = 1.f;
+  r.drag = cfg.drag_coeff;
+  r.decay = cfg.lag_decay;
+  if (has_dr) {
+    r.drag = d.x;
+    r.decay = d.y;
+    scale = d.z;
+  }
 #pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      const long row = e * na + a;
-      State s = load_state<M>(io.S_in, N, row);
-      RowPrm rp = row_params<M>(cfg, io.dr_in, row);
-      drs[a] = io.dr_in ? ld4(io.dr_in, row) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 raw = load_act<A>(io.raw, row);
-      if (!act_finite<A>(raw)) report_err(io.err, QS_ERR_NONFINITE_ACTION, (int)row);
-      if (!state_finite<M>(s)) report_err(io.err, QS_ERR_NONFINITE_STATE, (int)row);
-      Squash q = squash<A>(raw, rp);
-      float2 cs;
-      float4 cmd = world_cmd<M>(s, q.sq, k.g, cs);
-      State n = model_step<M>(s, cmd, rp, k);
-      n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;  // q/sensors.py:566
-      if (io.imu_out) imu_row<M>(cfg, io, row, N, meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g);
-      float4 pe = ld4(io.peff_in, row);
-      float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
-      float en = effnorm(q.eff, A), dn = effnorm(de, A);
-      eff[a] = q.eff;
-      s2[a] = n;
-      codes[a] = 0;
-      p0 = s.p;
-      if (TASK != QS_TASK_RACING) {
-        V3 goal = load3(io.goal_in, row);
-        V3 off = goal - n.p;
-        RewardFwd rf = reward_ctrl(cfg.w, off, n.v, en, dn);
-        float extra = 0.f;
-        if (TASK == QS_TASK_AVOIDANCE) {
-          int code;
-          float sd = sdf_eval(sv, n.p, code);
-          codes[a] = code;
-          rf.r -= cfg.w.w_o * softplus((cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness));
-          any_coll = any_coll || sd <= cfg.collision_radius;
-          extra = -(cfg.w_rl.w_o * softplus((cfg.d_safe - sd) / cfg.w_rl.sdf_sharpness));
-        }
-        rc[a] = rf.r;
-        rl[a] = reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn) + extra;
-        all_goal = all_goal && (rf.dist < cfg.success_radius) && (rf.speed < cfg.hover_speed);
-      }
-      any_oob = any_oob || n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x ||
-                n.p.y > bhi.y || n.p.z > bhi.z;
+  for (int k = 0; k < ModelTraits<M>::A; ++k) {
+    float lo = cfg.act_lo[k], hi = cfg.act_hi[k];
+    if (has_dr) {  // q/tasks.py:370-375
+      float c = (lo + hi) * 0.5f, h = (hi - lo) * 0.5f;
+      lo = c - h * scale;
+      hi = c + h * scale;
     }
-    // ---- per-env couplings
-    float r_goal = 0.f;
-    int next_gate = meta.w;
-    V3 goal_adv = v3(0.f, 0.f, 0.f);
-    bool advanced = false;
-    if (TASK == QS_TASK_RACING) {  // q/tasks.py:925-972
-      const qs_weights& w = cfg.w_rl;
-      GateV gt = load_gate(sc, cfg, e, next_gate);
-      V3 p1 = s2[0].p;
-      float r = w.w_g * (norm3(p0 - gt.c) - norm3(p1 - gt.c));
-      float sa = dot(p0 - gt.c, gt.n), sb = dot(p1 - gt.c, gt.n);
-      if (sa < 0.f && sb >= 0.f) {
-        float frac = -sa / fmaxf(sb - sa, 1e-12f);
-        V3 x = p0 + (p1 - p0) * frac;
-        V3 xc = x - gt.c;
-        float radial = norm3(xc - gt.n * dot(xc, gt.n));
-        bool passed = radial < gt.inner;
-        bool crashed = !passed && radial < gt.inner + gt.frame;
-        if (passed) r += w.gate_pass_bonus;
-        if (crashed) {
-          r -= w.gate_crash_penalty;
-          term_env = 2;
-          r_goal = -1.f;
-        }
-        bool finished = passed && next_gate == cfg.n_gates - 1;
-        if (finished) {
-          term_env = 1;
-          r_goal = 1.f;
-        }
-        if (passed && !finished) {
-          next_gate += 1;
-          advanced = true;
-          goal_adv = load_gate(sc, cfg, e, next_gate).c;
-        }
-      }
-      if (any_oob && term_env == 0) {
-        term_env = 3;
-        r_goal = -1.f;
-        r -= w.goal_bonus;
-      }
-      rc[0] = 0.f;
-      rl[0] = r;
-    } else {
-      if (na > 1) {  // q/tasks.py:173-192
-        float pen = 0.f;
-        for (int i = 0; i < na; ++i)
-          for (int j = i + 1; j < na; ++j) {
-            float dij = norm3(s2[i].p - s2[j].p);
-            float t = dij - cfg.form_ref[i][j];
-            pen = pen + t * t;
-            any_coll = any_coll || dij < cfg.d_min;
-          }
-        pen *= cfg.w.w_f;
+    r.center[k] = (lo + hi) * 0.5f;
+    r.half[k] = (hi - lo) * 0.5f;
+  }
+  return r;
+}
+
+template <int M, int NAMAX>
+QS_D void env_load(const qs_task_cfg& cfg, const float* sc_bounds, long e, int na, long N, EnvRegs<NAMAX>& R,
+                   const float* S,
+                   const float* goal, const float* peff, const float* dr, const int32_t* meta,
+                   const float* ep_ret, const float* bias) {
+  R.meta = reinterpret_cast<const int4*>(meta)[e];
+  R.ep_ret = ep_ret[e];
+  R.blo = xyz(ld4(sc_bounds, 2 * e)) + v3(1e-6f, 1e-6f, 1e-6f);
+  R.bhi = xyz(ld4(sc_bounds, 2 * e + 1)) - v3(1e-6f, 1e-6f, 1e-6f);
 #pragma unroll
-        for (int a = 0; a < NAMAX; ++a)
-          if (a < na) rc[a] -= pen;
-      }
-      // precedence: success, then bounds, then collision overwrite (q/tasks.py:734-737)
-      if (all_goal) term_env = 1;
-      if (any_oob) term_env = 3;
-      if (any_coll) term_env = 2;
-      r_goal = term_env == 1 ? 1.f : (term_env != 0 ? -1.f : 0.f);
-#pragma unroll
-      for (int a = 0; a < NAMAX; ++a)
-        if (a < na) rl[a] = rl[a] + cfg.w_rl.goal_bonus * r_goal;
-    }
-    // ---- counters, truncation, stats (q/tasks.py:574-591, 606-611)
-    int steps = meta.x + 1;
-    bool trunc = steps >= cfg.episode_len && term_env == 0;
-    done = term_env != 0 || trunc;
-    float ret = io.ep_return[e] + rl[0];
-    ret_env = ret;
-    int episode = meta.y;
-    if (done) {
-      steps = 0;
-      episode += 1;
-      io.ep_return[e] = 0.f;
-      next_gate = 0;
-    } else {
-      io.ep_return[e] = ret;
-    }
-    reinterpret_cast<int4*>(io.meta)[e] = make_int4(steps, episode, meta.z + 1, next_gate);
-    // ---- spawn (inline) or keep
-    V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
-    int ng0 = 0;
-    if (INLINE && done) {
-      bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, episode, na, sp_p, sp_v, sp_g, head, ng0);
-      if (!ok) report_err(io.err, QS_ERR_GENERATION, (int)(e * na));
-    }
-    // racing gates for the observation
-    GateV g0, g1;
-    if (TASK == QS_TASK_RACING && INLINE) {
-      int ngate = done ? 0 : next_gate;
-      g0 = load_gate(sc, cfg, e, ngate);
-      g1 = load_gate(sc, cfg, e, min(ngate + 1, cfg.n_gates - 1));
-    }
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      const long row = e * na + a;
-      io.r_ctrl[row] = rc[a];
-      io.r_goal[row] = r_goal;
-      io.r_rl[row] = rl[a];
-      io.terminated[row] = (int8_t)term_env;
-      io.truncated[row] = trunc ? 1 : 0;
-      State so = s2[a];
-      V3 goal = (TASK == QS_TASK_RACING) ? (advanced ? goal_adv : load3(io.goal_in, row))
-                                         : load3(io.goal_in, row);
-      float4 pe = eff[a];
-      float4 dro = drs[a];
-      if (done) {
-        pe = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (io.imu_bias) {
-          st4(io.imu_bias, 2 * row, make_float4(0.f, 0.f, 0.f, 0.f));
-          st4(io.imu_bias, 2 * row + 1, make_float4(0.f, 0.f, 0.f, 0.f));
-        }
-        if (INLINE) {
-          so = init_state<M>(sp_p[a], sp_v[a], head, k.g);
-          goal = sp_g[a];
-          if (cfg.dr_enabled && cfg.dr_per_episode) dro = dr_sample(cfg, row, episode);
-        }
-      }
-      store_state<M>(io.S_out, N, row, so);
-      st4(io.goal_out, row, f4(goal, 0.f));
-      st4(io.peff_out, row, pe);
-      if (io.dr_out) st4(io.dr_out, row, dro);
-      int fl = (done ? FLAG_DONE : 0) | (codes[a] << FLAG_SDF_SHIFT);
-      if (INLINE) {
-        float o[P];
-        float2 cs = yaw_cs<M>(so, k.g);
-        fl |= observe_row<M, TASK>(cfg, so, cs, goal, &g0, &g1, o);
-        write_obs<M, TASK>(cfg, io, row, o);
-        if (io.cam) reinterpret_cast<float2*>(io.cam)[row] = cs;
-      }
-      io.flags[row] = fl;
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    R.s[a] = load_state<M>(S, N, row);
+    R.goal[a] = ld4(goal, row);
+    R.peff[a] = ld4(peff, row);
+    R.dr[a] = dr ? ld4(dr, row) : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (bias) {
+      R.ba[a] = ld4(bias, 2 * row);
+      R.bg[a] = ld4(bias, 2 * row + 1);
     }
   }
-  warp_stats(active, done, term_env, ret_env, io.stats);
+}
+
+// the functional (checkpointed) part of the register file
+template <int M, int NAMAX>
+QS_D void env_store_ckpt(long e, int na, long N, const EnvRegs<NAMAX>& R, float* S, float* goal, float* peff,
+                         float* dr) {
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    store_state<M>(S, N, row, R.s[a]);
+    st4(goal, row, R.goal[a]);
+    st4(peff, row, R.peff[a]);
+    if (dr) st4(dr, row, R.dr[a]);
+  }
+}
+
+// the in-place part
+template <int NAMAX>
+QS_D void env_store_inplace(long e, int na, const EnvRegs<NAMAX>& R, int32_t* meta, float* ep_ret,
+                            float* bias) {
+  reinterpret_cast<int4*>(meta)[e] = R.meta;
+  ep_ret[e] = R.ep_ret;
+  if (bias) {
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      const long row = e * na + a;
+      st4(bias, 2 * row, R.ba[a]);
+      st4(bias, 2 * row + 1, R.bg[a]);
+    }
+  }
+}
+
+struct StepStat {
+  bool done;
+  int term;
+  float ret;
+};
+
+// ---------------------------------------------------------------------------
+// one fused env step on the register file (FlightTask.step, q/tasks.py:549-600)
+
+template <int M, int TASK, int NAMAX, bool INLINE>
+QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int na, long N,
+                           EnvRegs<NAMAX>& R, const float4* raw_in, const StepOut& out, int32_t* err,
+                           bool has_dr, bool has_imu) {
+  constexpr int A = ModelTraits<M>::A;
+  constexpr int P = TaskTraits<M, TASK>::P;
+  const DynK k = dyn_consts(cfg);
+  int term_env = 0;
+  State s2[NAMAX];
+  float rc[NAMAX], rl[NAMAX];
+  int codes[NAMAX];
+  bool all_goal = true, any_oob = false, any_coll = false;
+  V3 p0 = v3(0.f, 0.f, 0.f);
+  SceneView sv;
+  if (TASK == QS_TASK_AVOIDANCE) sv = scene_view(sc, e);
+  const V3 blo = R.blo, bhi = R.bhi;
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    const State& s = R.s[a];
+    RowPrm rp = row_params_v<M>(cfg, has_dr, R.dr[a]);
+    const float4 raw = raw_in[a];
+    if (!act_finite<A>(raw)) report_err(err, QS_ERR_NONFINITE_ACTION, (int)row);
+    if (!state_finite<M>(s)) report_err(err, QS_ERR_NONFINITE_STATE, (int)row);
+    Squash q = squash<A>(raw, rp);
+    float2 cs;
+    float4 cmd = world_cmd<M>(s, q.sq, k.g, cs);
+    State n = model_step<M>(s, cmd, rp, k);
+    n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;  // q/sensors.py:566
+    if (has_imu)
+      imu_apply<M>(cfg, row, N, R.meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g, R.ba[a], R.bg[a], out.imu_noise,
+                   out.imu_out);
+    const float4 pe = R.peff[a];
+    float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
+    float en = effnorm(q.eff, A), dn = effnorm(de, A);
+    R.peff[a] = q.eff;  // q/tasks.py:570
+    s2[a] = n;
+    codes[a] = 0;
+    p0 = s.p;
+    if (TASK != QS_TASK_RACING) {
+      V3 off = xyz(R.goal[a]) - n.p;
+      RewardFwd rf = reward_ctrl(cfg.w, off, n.v, en, dn);
+      float extra = 0.f;
+      if (TASK == QS_TASK_AVOIDANCE) {
+        int code;
+        float sd = sdf_eval(sv, n.p, code);
+        codes[a] = code;
+        rf.r -= cfg.w.w_o * softplus((cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness));
+        any_coll = any_coll || sd <= cfg.collision_radius;
+        extra = -(cfg.w_rl.w_o * softplus((cfg.d_safe - sd) / cfg.w_rl.sdf_sharpness));
+      }
+      rc[a] = rf.r;
+      rl[a] = reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn) + extra;
+      all_goal = all_goal && (rf.dist < cfg.success_radius) && (rf.speed < cfg.hover_speed);
+    }
+    any_oob = any_oob || n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x ||
+              n.p.y > bhi.y || n.p.z > bhi.z;
+  }
+  // ---- per-env couplings
+  float r_goal = 0.f;
+  int next_gate = R.meta.w;
+  if (TASK == QS_TASK_RACING) {  // q/tasks.py:925-972
+    const qs_weights& w = cfg.w_rl;
+    GateV gt = load_gate(sc, cfg, e, next_gate);
+    V3 p1 = s2[0].p;
+    float r = w.w_g * (norm3(p0 - gt.c) - norm3(p1 - gt.c));
+    float sa = dot(p0 - gt.c, gt.n), sb = dot(p1 - gt.c, gt.n);
+    if (sa < 0.f && sb >= 0.f) {
+      float frac = -sa / fmaxf(sb - sa, 1e-12f);
+      V3 x = p0 + (p1 - p0) * frac;
+      V3 xc = x - gt.c;
+      float radial = norm3(xc - gt.n * dot(xc, gt.n));
+      bool passed = radial < gt.inner;
+      bool crashed = !passed && radial < gt.inner + gt.frame;
+      if (passed) r += w.gate_pass_bonus;
+      if (crashed) {
+        r -= w.gate_crash_penalty;
+        term_env = 2;
+        r_goal = -1.f;
+      }
+      bool finished = passed && next_gate == cfg.n_gates - 1;
+      if (finished) {
+        term_env = 1;
+        r_goal = 1.f;
+      }
+      if (passed && !finished) {
+        next_gate += 1;
+        R.goal[0] = f4(load_gate(sc, cfg, e, next_gate).c, 0.f);
+      }
+    }
+    if (any_oob && term_env == 0) {
+      term_env = 3;
+      r_goal = -1.f;
+      r -= w.goal_bonus;
+    }
+    rc[0] = 0.f;
+    rl[0] = r;
+  } else {
+    if (na > 1) {  // q/tasks.py:173-192
+      float pen = 0.f;
+      for (int i = 0; i < na; ++i)
+        for (int j = i + 1; j < na; ++j) {
+          float dij = norm3(s2[i].p - s2[j].p);
+          float t = dij - cfg.form_ref[i][j];
+          pen = pen + t * t;
+          any_coll = any_coll || dij < cfg.d_min;
+        }
+      pen *= cfg.w.w_f;
+#pragma unroll
+      for (int a = 0; a < NAMAX; ++a)
+        if (a < na) rc[a] -= pen;
+    }
+    // precedence: success, then bounds, then collision overwrite (q/tasks.py:734-737)
+    if (all_goal) term_env = 1;
+    if (any_oob) term_env = 3;
+    if (any_coll) term_env = 2;
+    r_goal = term_env == 1 ? 1.f : (term_env != 0 ? -1.f : 0.f);
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a)
+      if (a < na) rl[a] = rl[a] + cfg.w_rl.goal_bonus * r_goal;
+  }
+  // ---- counters, truncation (q/tasks.py:574-591, 606-611)
+  int steps = R.meta.x + 1;
+  const bool trunc = steps >= cfg.episode_len && term_env == 0;
+  const bool done = term_env != 0 || trunc;
+  const float ret = R.ep_ret + rl[0];
+  int episode = R.meta.y;
+  if (done) {
+    steps = 0;
+    episode += 1;
+    R.ep_ret = 0.f;
+    next_gate = 0;
+  } else {
+    R.ep_ret = ret;
+  }
+  R.meta = make_int4(steps, episode, R.meta.z + 1, next_gate);
+  // ---- auto-reset (inline Philox) or keep
+  V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
+  int ng0 = 0;
+  if (INLINE && done) {
+    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, episode, na, sp_p, sp_v, sp_g, head, ng0);
+    if (!ok) report_err(err, QS_ERR_GENERATION, (int)(e * na));
+  }
+  GateV g0, g1;
+  if (TASK == QS_TASK_RACING && INLINE) {
+    int ngate = done ? 0 : next_gate;
+    g0 = load_gate(sc, cfg, e, ngate);
+    g1 = load_gate(sc, cfg, e, min(ngate + 1, cfg.n_gates - 1));
+  }
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    out.r_ctrl[row] = rc[a];
+    out.r_goal[row] = r_goal;
+    out.r_rl[row] = rl[a];
+    out.term[row] = (int8_t)term_env;
+    out.trunc[row] = trunc ? 1 : 0;
+    State so = s2[a];
+    if (done) {
+      R.peff[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (has_imu) {
+        R.ba[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+        R.bg[a] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (INLINE) {
+        so = init_state<M>(sp_p[a], sp_v[a], head, k.g);
+        R.goal[a] = f4(sp_g[a], 0.f);
+        if (cfg.dr_enabled && cfg.dr_per_episode) R.dr[a] = dr_sample(cfg, row, episode);
+      }
+    }
+    R.s[a] = so;
+    int fl = (done ? FLAG_DONE : 0) | (codes[a] << FLAG_SDF_SHIFT);
+    if (INLINE && out.obs) {
+      float o[P];
+      float2 cs = yaw_cs<M>(so, k.g);
+      fl |= observe_row<M, TASK>(cfg, so, cs, xyz(R.goal[a]), &g0, &g1, o);
+      float* dst = out.obs + row * P;
+#pragma unroll
+      for (int kk = 0; kk < P; ++kk) dst[kk] = o[kk];
+      if (out.cam) reinterpret_cast<float2*>(out.cam)[row] = cs;
+    }
+    out.flags[row] = fl;
+  }
+  return StepStat{done, term_env, ret};
 }
 
 // ---------------------------------------------------------------------------
-// backward (analytic VJP of k_task_fwd; recomputes the forward from the
-// checkpoint (S_in, raw, goal_in, peff_in, dr_in) + the flags record)
+// analytic VJP of one step.  Inputs: the step's checkpoint (pre-step state s_in,
+// raw action, goal, previous effort, per-row params, flags), upstream grads of
+// the post-step state (gS, in/out: replaced by the grad of s_in), of the
+// observation (g_obs, may be NULL) and of r_ctrl (per row or a scalar).
 
 template <int M, int TASK, int NAMAX>
-__global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const qs_scene sc,
-                                                  const qs_step_grad gr) {
+QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int na, long N,
+                       const State* s_in, const float4* raw_in, const float4* goal, const float4* peff,
+                       const float4* dr, bool has_dr, const int* flags_in, const float* g_obs,
+                       const float* g_r_rows, float g_r_scalar, State* gS, float* g_raw_t) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= cfg.n_envs) return;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
-  const long N = (long)cfg.n_envs * na;
   const DynK k = dyn_consts(cfg);
-  State s1[NAMAX], s2[NAMAX], g2[NAMAX];
+  State s2[NAMAX], g2[NAMAX];
   float4 cmd[NAMAX];
   float2 csc[NAMAX];
   float4 geff[NAMAX];
@@ -630,20 +725,21 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
   for (int a = 0; a < NAMAX; ++a) {
     if (a >= na) break;
     const long row = e * na + a;
-    State s = load_state<M>(gr.S_in, N, row);
-    RowPrm rp = row_params<M>(cfg, gr.dr_in, row);
-    float4 raw = load_act<A>(gr.raw, row);
+    const State& s = s_in[a];
+    RowPrm rp = row_params_v<M>(cfg, has_dr, dr[a]);
+    const float4 raw = raw_in[a];
     Squash q = squash<A>(raw, rp);
     float2 cs;
     float4 c = world_cmd<M>(s, q.sq, k.g, cs);
     State n = model_step<M>(s, c, rp, k);
     n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;
-    const int fl = gr.flags[row];
+    const int fl = flags_in[a];
     const bool done = fl & FLAG_DONE;
-    State g = done ? zero_state() : load_grad<M>(gr.g_S_out, N, row);
+    State g = done ? zero_state() : gS[a];
+    g.ve = v3(0.f, 0.f, 0.f);
     // observation path (only rows that were not reset; q/tasks.py:584-594)
-    if (!done && gr.g_obs) {
-      const float* go = gr.g_obs + row * P;
+    if (!done && g_obs) {
+      const float* go = g_obs + row * P;
       float2 cs2 = yaw_cs<M>(n, k.g);
       V3 gg = v3(go[0], go[1], go[2]);
       int cb = fl >> FLAG_CLAMP_SHIFT;
@@ -666,13 +762,12 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
         g.p -= rotz(cs2, ga + gb);
       }
     }
-    float grr = gr.g_rctrl ? gr.g_rctrl[row] : 0.f;
+    float grr = g_r_rows ? g_r_rows[row] : g_r_scalar;
     float4 ge = make_float4(0.f, 0.f, 0.f, 0.f);
     if (TASK != QS_TASK_RACING && grr != 0.f) {
-      float4 pe = ld4(gr.peff_in, row);
+      float4 pe = peff[a];
       float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
-      V3 goal = load3(gr.goal_in, row);
-      V3 off = goal - n.p;
+      V3 off = xyz(goal[a]) - n.p;
       V3 goff, gv;
       reward_ctrl_vjp(cfg.w, off, n.v, q.eff, de, A, grr, goff, gv, ge);
       g.p -= goff;
@@ -687,7 +782,6 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
         }
       }
     }
-    s1[a] = s;
     s2[a] = n;
     g2[a] = g;
     cmd[a] = c;
@@ -713,10 +807,10 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
   for (int a = 0; a < NAMAX; ++a) {
     if (a >= na) break;
     const long row = e * na + a;
-    RowPrm rp = row_params<M>(cfg, gr.dr_in, row);
+    RowPrm rp = row_params_v<M>(cfg, has_dr, dr[a]);
     State gi;
     float4 gc;
-    model_step_vjp<M>(s1[a], cmd[a], rp, k, g2[a], gi, gc);
+    model_step_vjp<M>(s_in[a], cmd[a], rp, k, g2[a], gi, gc);
     float4 gsq;
     if (M == QS_MODEL_FULL) {
       gsq = gc;
@@ -725,16 +819,221 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
       gsq = make_float4(u.x, u.y, u.z, 0.f);
     }
     gsq = make_float4(gsq.x + geff[a].x, gsq.y + geff[a].y, gsq.z + geff[a].z, gsq.w + geff[a].w);
-    float4 raw = load_act<A>(gr.raw, row);
-    float* gout = gr.g_raw + row * A;
+    const float4 raw = raw_in[a];
+    float* gout = g_raw_t + row * A;
 #pragma unroll
     for (int kk = 0; kk < A; ++kk) {
       float t = tanhf(f4get(raw, kk));
       gout[kk] = f4get(gsq, kk) * rp.half[kk] * (1.f - t * t);
     }
-    store_state<M>(gr.g_S_in, N, row, gi);
+    gS[a] = gi;
   }
 }
+
+// ---------------------------------------------------------------------------
+// per-step kernels (FlightTask.step and its autograd node)
+
+template <int M, int TASK, int NAMAX, bool INLINE>
+__global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const qs_scene sc,
+                                                  const qs_step_io io) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < cfg.n_envs;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  StepStat st{false, 0, 0.f};
+  if (active) {
+    EnvRegs<NAMAX> R;
+    float4 raw[NAMAX];
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a)
+      if (a < na) raw[a] = load_act<ModelTraits<M>::A>(io.raw, e * na + a);
+    env_load<M, NAMAX>(cfg, sc.bounds, e, na, N, R, io.S_in, io.goal_in, io.peff_in, io.dr_in, io.meta,
+                       io.ep_return, io.imu_bias);
+    StepOut o{io.obs, io.r_ctrl, io.r_goal, io.r_rl, io.terminated, io.truncated, io.flags, io.cam,
+              io.imu_out, io.imu_noise};
+    st = env_step_fwd<M, TASK, NAMAX, INLINE>(cfg, sc, e, na, N, R, raw, o, io.err, io.dr_in != nullptr,
+                                             io.imu_out != nullptr);
+    env_store_ckpt<M, NAMAX>(e, na, N, R, io.S_out, io.goal_out, io.peff_out, io.dr_out);
+    env_store_inplace<NAMAX>(e, na, R, io.meta, io.ep_return, io.imu_out ? io.imu_bias : nullptr);
+  }
+  warp_stats(active, st.done, st.term, st.ret, io.stats);
+}
+
+template <int M, int TASK, int NAMAX>
+__global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const qs_scene sc,
+                                                  const qs_step_grad gr) {
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cfg.n_envs) return;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  State s_in[NAMAX], gS[NAMAX];
+  float4 goal[NAMAX], peff[NAMAX], dr[NAMAX], raw[NAMAX];
+  int fl[NAMAX];
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    const long row = e * na + a;
+    s_in[a] = load_state<M>(gr.S_in, N, row);
+    goal[a] = ld4(gr.goal_in, row);
+    peff[a] = ld4(gr.peff_in, row);
+    dr[a] = gr.dr_in ? ld4(gr.dr_in, row) : make_float4(0.f, 0.f, 0.f, 0.f);
+    raw[a] = load_act<ModelTraits<M>::A>(gr.raw, row);
+    fl[a] = __ldg(gr.flags + row);
+    gS[a] = load_grad<M>(gr.g_S_out, N, row);
+  }
+  env_step_bwd<M, TASK, NAMAX>(cfg, sc, e, na, N, s_in, raw, goal, peff, dr, gr.dr_in != nullptr, fl, gr.g_obs,
+                               gr.g_rctrl, 0.f, gS, gr.g_raw);
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    store_state<M>(gr.g_S_in, N, e * na + a, gS[a]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused T-step windows (open-loop actions): the env's register file stays on
+// chip for the whole window; only the per-step outputs and the backward's
+// checkpoints go to HBM, and the backward carries dL/dS in registers.
+
+// 64-thread CTAs, >= 7 resident per SM: 65,536 envs = 1,024 CTAs = one wave
+// on 148 SMs with <= 144 registers per thread
+constexpr int WIN_BLOCK = 64;
+
+template <int M, int TASK, int NAMAX>
+__global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg cfg, const qs_scene sc,
+                                                    const qs_window_io w) {
+  constexpr int A = ModelTraits<M>::A;
+  constexpr int P = TaskTraits<M, TASK>::P;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool active = e < cfg.n_envs;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  const int NP = ModelTraits<M>::NP;
+  const bool has_dr = w.dr != nullptr, has_imu = w.imu_out != nullptr;
+  EnvRegs<NAMAX> R;
+  int n_done = 0, n_succ = 0, n_coll = 0;
+  float ret_sum = 0.f;
+  float4 raw[NAMAX], raw_next[NAMAX];
+  if (active) {
+    env_load<M, NAMAX>(cfg, sc.bounds, e, na, N, R, w.S, w.goal, w.peff, w.dr, w.meta, w.ep_return,
+                       w.imu_bias);
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a)
+      if (a < na) raw[a] = load_act<A>(w.actions, e * na + a);
+  }
+  for (int t = 0; t < w.T; ++t) {
+    if (active) {
+      // prefetch the next step's actions: their latency hides under this step
+      if (t + 1 < w.T) {
+#pragma unroll
+        for (int a = 0; a < NAMAX; ++a)
+          if (a < na) raw_next[a] = load_act<A>(w.actions + (long)(t + 1) * N * A, e * na + a);
+      }
+      StepOut o{w.obs ? w.obs + (long)t * N * P : nullptr, w.r + (long)t * 3 * N, w.r + (long)t * 3 * N + N,
+                w.r + (long)t * 3 * N + 2 * N, w.terminated + (long)t * N, w.truncated + (long)t * N,
+                w.flags + (long)t * N, nullptr, has_imu ? w.imu_out + (long)t * N * 6 : nullptr,
+                w.imu_noise ? w.imu_noise + (long)t * 4 * N * 3 : nullptr};
+      StepStat st = env_step_fwd<M, TASK, NAMAX, true>(cfg, sc, e, na, N, R, raw, o, w.err, has_dr, has_imu);
+#pragma unroll
+      for (int a = 0; a < NAMAX; ++a) raw[a] = raw_next[a];
+      if (st.done) {
+        n_done++;
+        n_succ += st.term == 1;
+        n_coll += st.term == 2;
+        ret_sum += st.ret;
+      }
+      env_store_ckpt<M, NAMAX>(e, na, N, R, w.S + (long)(t + 1) * NP * N * 4, w.goal + (long)(t + 1) * N * 4,
+                               w.peff + (long)(t + 1) * N * 4, has_dr ? w.dr + (long)(t + 1) * N * 4 : nullptr);
+    }
+  }
+  if (active) env_store_inplace<NAMAX>(e, na, R, w.meta, w.ep_return, has_imu ? w.imu_bias : nullptr);
+  // episode statistics: one warp reduction for the whole window
+  double r = ret_sum;
+  int c0 = n_done, c1 = n_succ, c2 = n_coll;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r += __shfl_xor_sync(0xffffffffu, r, o);
+    c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+    c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+  }
+  if ((threadIdx.x & 31) == 0 && w.stats && c0) {
+    atomicAdd(w.stats + 0, (double)c0);
+    atomicAdd(w.stats + 1, (double)c1);
+    atomicAdd(w.stats + 2, (double)c2);
+    atomicAdd(w.stats + 3, r);
+  }
+}
+
+template <int M, int TASK, int NAMAX>
+__global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg cfg, const qs_scene sc,
+                                                    const qs_window_io w) {
+  constexpr int A = ModelTraits<M>::A;
+  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cfg.n_envs) return;
+  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const long N = (long)cfg.n_envs * na;
+  const int NP = ModelTraits<M>::NP;
+  const bool has_dr = w.dr != nullptr;
+  State gS[NAMAX];
+  // double-buffered checkpoint of step t (cur) and t-1 (nxt): loads of the
+  // previous step are independent of the dL/dS chain, so they are issued a
+  // whole step ahead
+  struct Ck {
+    State s;
+    float4 goal, peff, dr, raw;
+    int fl;
+  };
+  Ck cur[NAMAX], nxt[NAMAX];
+  auto load_ck = [&](int t, Ck* c) {
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      const long row = e * na + a;
+      c[a].s = load_state<M>(w.S + (long)t * NP * N * 4, N, row);
+      c[a].goal = ld4(w.goal + (long)t * N * 4, row);
+      c[a].peff = ld4(w.peff + (long)t * N * 4, row);
+      c[a].dr = has_dr ? ld4(w.dr + (long)t * N * 4, row) : make_float4(0.f, 0.f, 0.f, 0.f);
+      c[a].raw = load_act<A>(w.actions + (long)t * N * A, row);
+      c[a].fl = __ldg(w.flags + (long)t * N + row);
+    }
+  };
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    gS[a] = load_grad<M>(w.g_S_final, N, e * na + a);
+  }
+  load_ck(w.T - 1, cur);
+  for (int t = w.T - 1; t >= 0; --t) {
+    if (t > 0) load_ck(t - 1, nxt);
+    const float gscale = w.g_rctrl_scale * powf(w.gamma, (float)t);
+    State s_in[NAMAX];
+    float4 goal[NAMAX], peff[NAMAX], dr[NAMAX], raw[NAMAX];
+    int fl[NAMAX];
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      s_in[a] = cur[a].s;
+      goal[a] = cur[a].goal;
+      peff[a] = cur[a].peff;
+      dr[a] = cur[a].dr;
+      raw[a] = cur[a].raw;
+      fl[a] = cur[a].fl;
+    }
+    env_step_bwd<M, TASK, NAMAX>(cfg, sc, e, na, N, s_in, raw, goal, peff, dr, has_dr, fl, nullptr,
+                                 w.g_rctrl ? w.g_rctrl + (long)t * N : nullptr, gscale, gS,
+                                 w.g_actions + (long)t * N * A);
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) cur[a] = nxt[a];
+  }
+  if (w.g_S0) {
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      store_state<M>(w.g_S0, N, e * na + a, gS[a]);
+    }
+  }
+}
+
 
 // ---------------------------------------------------------------------------
 // spawn (reset of masked envs), observe
@@ -854,7 +1153,17 @@ int run_observe(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io
   return launch_status();
 }
 
-// op: 0 fwd, 1 bwd, 2 spawn, 3 observe
+template <int M, int T, int NA>
+int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_window_io* w, cudaStream_t s) {
+  if (w->T <= 0) return QS_OK;
+  if (op == 4)
+    k_window_fwd<M, T, NA><<<grid_for(cfg->n_envs, WIN_BLOCK), WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+  else
+    k_window_bwd<M, T, NA><<<grid_for(cfg->n_envs, WIN_BLOCK), WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+  return launch_status();
+}
+
+// op: 0 fwd, 1 bwd, 2 spawn, 3 observe, 4 window fwd, 5 window bwd
 template <int T>
 int task_dispatch(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
                   const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
@@ -867,6 +1176,8 @@ int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, c
     case 1: return run_bwd<M, T, NA>(cfg, sc, static_cast<const qs_step_grad*>(p), s);
     case 2: return run_spawn<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), mask, tab, s);
     case 3: return run_observe<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), s);
+    case 4:
+    case 5: return run_window<M, T, NA>(op, cfg, sc, static_cast<const qs_window_io*>(p), s);
   }
   return QS_ERR_BAD_ARGUMENT;
 }

@@ -18,7 +18,8 @@ from paper_2509_10247_b200.tasks import FlightTask
 
 
 class BpttWindow:
-    def __init__(self, env: FlightTask, horizon: int, gamma: float = 0.99, want_obs: bool = True):
+    def __init__(self, env: FlightTask, horizon: int, gamma: float = 0.99, want_obs: bool = True,
+                 fused: bool = True):
         if env.reset_source is not None:
             raise ValueError("BpttWindow needs in-kernel (Philox) resets; reset_source forces host syncs")
         self.env, self.T, self.gamma = env, horizon, gamma
@@ -45,8 +46,9 @@ class BpttWindow:
         self.w_loss = w[:, None] * 1.0
         self.loss = torch.zeros((), **f)
         self.want_obs = want_obs
+        self.fused = fused
         self.graph = None
-        self.launches_per_window = 2 * T
+        self.launches_per_window = 2 if fused else 2 * T
         self._load_env_state()
 
     def _load_env_state(self):
@@ -65,12 +67,36 @@ class BpttWindow:
         if self.dr is not None:
             e._dr = self.dr[self.T].clone()
 
+    def _window_io(self) -> L.QsWindowIo:
+        e = self.env
+        w = L.QsWindowIo()
+        w.T = self.T
+        w.S, w.goal, w.peff = L.ptr(self.S), L.ptr(self.goal), L.ptr(self.peff)
+        w.dr = L.ptr(self.dr)
+        w.actions = L.ptr(self.actions)
+        w.meta, w.ep_return, w.imu_bias = L.ptr(e._meta), L.ptr(e._ep_ret), L.ptr(e._imu_bias)
+        w.imu_out = L.ptr(self.imu)
+        w.obs = L.ptr(self.obs) if self.want_obs else None
+        w.r, w.terminated, w.truncated, w.flags = L.ptr(self.r), L.ptr(self.term), L.ptr(self.trunc), L.ptr(self.flags)
+        w.stats, w.err = L.ptr(e._stats), L.ptr(e._err)
+        w.g_rctrl = None
+        w.g_rctrl_scale = -1.0 / (self.T * e.N)
+        w.gamma = self.gamma
+        w.g_actions = L.ptr(self.g_actions)
+        return w
+
     def _run(self):
         e = self.env
         lib = L.lib()
         cfg, sc = e._cfg, e._scene.struct()
         stream = L.stream_handle(e.device)
         T = self.T
+        if self.fused:
+            w = self._window_io()
+            L.check(lib.qs_task_window_fwd(cfg, sc, w, stream), "qs_task_window_fwd")
+            L.check(lib.qs_task_window_bwd(cfg, sc, w, stream), "qs_task_window_bwd")
+            self._finish()
+            return
         for t in range(T):
             io = e._new_io()
             io.S_in, io.S_out, io.raw = L.ptr(self.S[t]), L.ptr(self.S[t + 1]), L.ptr(self.actions[t])
@@ -93,7 +119,11 @@ class BpttWindow:
             g.g_rctrl = L.ptr(self.g_r[t])
             g.g_S_in, g.g_raw = L.ptr(self.gS[t % 2]), L.ptr(self.g_actions[t])
             lib.qs_task_step_bwd(cfg, sc, g, stream)
-        torch.sum(self.r[:, 0] * self.w_loss, out=self.loss)
+        self._finish()
+
+    def _finish(self):
+        T = self.T
+        torch.sum(self.r[:, 0] * self.w_loss, dim=(0, 1), out=self.loss)
         # carry the final state into slot 0 for the next window
         self.S[0].copy_(self.S[T])
         self.goal[0].copy_(self.goal[T])
@@ -105,8 +135,10 @@ class BpttWindow:
         """Record one window into a CUDA graph (replayed by ``run``)."""
         s = torch.cuda.Stream(self.env.device)
         s.wait_stream(torch.cuda.current_stream(self.env.device))
-        snap = [x.clone() for x in (self.S[0], self.goal[0], self.peff[0], self.env._meta, self.env._ep_ret,
-                                    self.env._stats)]
+        e = self.env
+        live = [x for x in (self.S[0], self.goal[0], self.peff[0], e._meta, e._ep_ret, e._stats, e._imu_bias,
+                            self.dr[0] if self.dr is not None else None) if x is not None]
+        snap = [x.clone() for x in live]
         with torch.cuda.stream(s):
             self._run()  # warm-up outside capture (lazy init)
         torch.cuda.current_stream(self.env.device).wait_stream(s)
@@ -114,8 +146,7 @@ class BpttWindow:
         with torch.cuda.graph(g):
             self._run()
         # capture launches nothing; warm-up did: restore the pre-warm-up state
-        for dst, src in zip((self.S[0], self.goal[0], self.peff[0], self.env._meta, self.env._ep_ret,
-                             self.env._stats), snap):
+        for dst, src in zip(live, snap):
             dst.copy_(src)
         self.graph = g
         return self

@@ -192,3 +192,100 @@ def test_imu_philox_statistics(qs):
     imu2 = qs.sensors.ImuModel(B, accel_noise_std=0.2, gyro_noise_std=0.05, seed=3)
     a2, _ = imu2.read(R, z3, z3, np.array([0.0, 0.0, -9.81]), 0.01)
     assert np.array_equal(a2.cpu().numpy() - np.array([0, 0, 9.81]), a)
+
+
+# ---------------------------------------------------------------------------
+# native window engine == autograd path; Philox resets; in-kernel scenes
+
+
+@pytest.mark.parametrize("fused", [True, False])
+@pytest.mark.parametrize("model", ["full", "pm_continuous", "pm_discrete"])
+def test_window_engine_matches_autograd_path(qs, model, fused):
+    from paper_2509_10247_b200.window import BpttWindow
+
+    cfg = qs.TaskConfig(task="position", dynamics=model, n_envs=512, episode_len=9,
+                        imu=qs.ImuSpec(0.1, 0.01, 0.01, 0.001))
+    T = 12
+    g = torch.Generator(device="cpu").manual_seed(0)
+    acts = (torch.randn(T, 512, 4 if model == "full" else 3, generator=g) * 0.4).cuda()
+    e1 = qs.make_task(cfg, strict=False)
+    e1.reset(seed=5)
+    e2 = qs.make_task(cfg, strict=False)
+    e2.reset(seed=5)
+    win = BpttWindow(e1, T, fused=fused)
+    win.actions.copy_(acts)
+    win.capture()
+    loss_w, g_w = win.run()
+    a = acts.clone().requires_grad_(True)
+    tot = 0.0
+    for t in range(T):
+        tot = tot + e2.step(a[t]).r_ctrl.mean() * 0.99 ** t
+    loss = -tot / T
+    (ga,) = torch.autograd.grad(loss, a)
+    assert abs(float(loss_w) - float(loss.detach())) < 1e-6 * max(1, abs(float(loss.detach())))
+    assert grad_err(g_w.cpu().numpy(), ga.cpu().numpy()) < 1e-5
+    win.sync_env()
+    assert torch.allclose(e1._S, e2._S.detach(), rtol=1e-6, atol=1e-6)
+    assert torch.equal(e1._meta, e2._meta)
+    # resets happened (episode_len 9 < T) and stats agree
+    assert e1.finished_episodes == e2.finished_episodes > 0
+
+
+def test_philox_resets_are_valid_and_deterministic(qs):
+    cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=4096, episode_len=3)
+    env = qs.make_task(cfg, strict=True)
+    env.reset(seed=11)
+    ext = cfg.goal_dist
+    lo = np.array([-2.0, -ext - 2.0, 0.0]) + 0.8
+    hi = np.array([ext + 2.0, ext + 2.0, 4.0]) - 0.8
+    g = env.goals.cpu().numpy()
+    assert np.all(g >= lo - 1e-5) and np.all(g <= hi + 1e-5)
+    p = env.state.p.detach().cpu().numpy()
+    d = np.linalg.norm(g - p, axis=-1)
+    assert d.min() > 2.5 - 1.0 and d.max() < ext + 1.0  # spawn jitter N(0, 0.1^2) around the pair
+    env2 = qs.make_task(cfg, strict=True)
+    env2.reset(seed=11)
+    assert torch.equal(env.goals, env2.goals) and torch.equal(env._S, env2._S)
+    for _ in range(3):
+        env.step(torch.zeros(env.N, 3, device="cuda"))
+    assert env.finished_episodes == 4096  # truncation at episode_len
+    assert bool((env.steps_in_episode == 0).all())
+    assert not torch.equal(env.goals, env2.goals)  # re-spawned with the next episode key
+
+
+def test_in_kernel_scene_generation_is_feasible(qs):
+    from oracle import quadsim_oracle as O
+
+    sc = qs.world.gen_obstacle_courses(7, 64, [0.0, 0.0, 1.2], [8.0, 0.0, 1.5], 0.25, style="indoor",
+                                       device="cuda")
+    scenes = qs.world.device_scene_to_scenes(sc, style="indoor")
+    keep_min = 0.15 + 0.5
+    for s in scenes:
+        osc = O.Scene(prims={"spheres": s.prims.spheres, "boxes": s.prims.boxes,
+                             "cylinders": s.prims.cylinders, "ground_z": 0.0},
+                      bounds_lo=s.bounds_lo, bounds_hi=s.bounds_hi, spawn=s.spawn, goal=s.goal)
+        assert O.grid_path_exists(osc)  # the oracle's own BFS agrees
+        rand_boxes = s.prims.boxes[:-5]  # shell walls always kept
+        pk = O.pack_primitives([{"spheres": s.prims.spheres, "boxes": rand_boxes,
+                                 "cylinders": s.prims.cylinders}])
+        ends = np.stack([s.spawn, s.goal])
+        assert O.sdf_single_scene(ends, pk).min() > keep_min - 1e-4
+        if len(s.prims.spheres):
+            r = s.prims.spheres[:, 3]
+            assert r.min() >= 0.3 - 1e-6 and r.max() <= 1.0 + 1e-6
+        if len(s.prims.cylinders):
+            assert np.allclose(s.prims.cylinders[:, 2], s.prims.cylinders[:, 4])  # trunks on the ground
+    assert len(scenes[0].prims.boxes) >= 5  # indoor shell incl. ceiling
+
+
+def test_avoidance_with_generated_scenes_and_depth_steps(qs):
+    cfg = qs.TaskConfig(task="avoidance", dynamics="pm_continuous", n_envs=256, episode_len=20,
+                        sensor="depth", depth_width=64, depth_height=48, density=0.3)
+    env = qs.make_task(cfg)
+    out = env.reset(seed=2)
+    assert out.obs.visual.shape == (256, 48, 64)
+    a = torch.zeros(256, 3, device="cuda", requires_grad=True)
+    out = env.step(a)
+    assert torch.isfinite(out.r_ctrl).all()
+    out.r_ctrl.sum().backward()
+    assert torch.isfinite(a.grad).all() and a.grad.abs().sum() > 0

@@ -191,3 +191,13 @@ def test_oracle_fd_gradient_long_window(name):
     g = O.fd_grad_actions(env, z["raw"])
     g_ref = z["grad"]
     assert np.abs(g - g_ref).max() / np.abs(g_ref).max() < 1e-6
+
+
+@pytest.mark.parametrize("name", ["pos_pmc", "pos_pmd", "pos_full", "pos_pmc_dr", "pos_events",
+                                  "pos_full_events"])
+def test_oracle_reverse_pass_matches_reference_tape(name):
+    env, z = build_oracle_task(name)
+    loss, g = O.window_value_and_grad(env, z["raw"])
+    g_ref = z["grad_unaliased"] if "grad_unaliased" in z else z["grad"]
+    assert abs(loss - float(z["loss"])) < 1e-12
+    assert np.abs(g - g_ref).max() / np.abs(g_ref).max() < 1e-10
