@@ -153,13 +153,18 @@ QS_D void attitude_pm(V3 a, V3 ve, V3& xb, V3& yb, V3& zb) {
 // atan2 signed-zero semantics (q/sensors.py:609-611).
 QS_D float2 yaw_cs_from(float x, float y) {
   float m = fmaxf(fabsf(x), fabsf(y));
+  if (m > 1e-18f && m < 1e18f) {  // no under/overflow in x^2 + y^2
+    float r = rsqrtf(x * x + y * y);
+    return make_float2(x * r, y * r);
+  }
   if (m == 0.f) {
     float yaw = atan2f(y, x), s, c;
     sincosf(yaw, &s, &c);
     return make_float2(c, s);
   }
-  x /= m;
-  y /= m;
+  float im = 1.f / m;
+  x *= im;
+  y *= im;
   float r = rsqrtf(x * x + y * y);
   return make_float2(x * r, y * r);
 }
@@ -221,7 +226,8 @@ QS_D State step_full(const State& s, float4 cmd, const DynK& k) {
   Q4 qd = qmul(q, q4(0.f, s.w.x, s.w.y, s.w.z));
   Q4 qn = q4(q.w + qd.w * 0.5f * dt, q.x + qd.x * 0.5f * dt, q.y + qd.y * 0.5f * dt,
              q.z + qd.z * 0.5f * dt);
-  float inv = 1.f / sqrtf(qn.w * qn.w + qn.x * qn.x + qn.y * qn.y + qn.z * qn.z);
+  // |qn| ~ 1: rsqrt (<= 2 ulp) instead of IEEE sqrt + divide
+  float inv = rsqrtf(qn.w * qn.w + qn.x * qn.x + qn.y * qn.y + qn.z * qn.z);
   State o;
   o.p = s.p + s.v * dt;
   o.v = s.v + vdot * dt;
@@ -242,8 +248,7 @@ QS_D void step_full_vjp(const State& s, float4 cmd, const DynK& k, const State& 
   Q4 qd = qmul(q, q4(0.f, s.w.x, s.w.y, s.w.z));
   Q4 qn = q4(q.w + qd.w * 0.5f * dt, q.x + qd.x * 0.5f * dt, q.y + qd.y * 0.5f * dt,
              q.z + qd.z * 0.5f * dt);
-  float nn = sqrtf(qn.w * qn.w + qn.x * qn.x + qn.y * qn.y + qn.z * qn.z);
-  float inv = 1.f / nn;
+  float inv = rsqrtf(qn.w * qn.w + qn.x * qn.x + qn.y * qn.y + qn.z * qn.z);
   Q4 qo = q4(qn.w * inv, qn.x * inv, qn.y * inv, qn.z * inv);
   // normalize VJP: (g - q'(q'.g)) / |qn|
   const Q4 gq = gs.q;

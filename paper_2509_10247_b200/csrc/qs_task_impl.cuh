@@ -231,10 +231,14 @@ QS_D void imu_apply(const qs_task_cfg& cfg, long row, long N, int tick, const St
   bg += nbg * (cfg.imu_gyro_rw * sq);
   V3 xb, yb, zb;
   V3 w = v3(0.f, 0.f, 0.f);
-  if (M == QS_MODEL_FULL) {
-    zb = qrot(s2.q, v3(0.f, 0.f, 1.f));
-    xb = qrot(s2.q, v3(1.f, 0.f, 0.f));
-    yb = qrot(s2.q, v3(0.f, 1.f, 0.f));
+  if (M == QS_MODEL_FULL) {  // columns of quat_to_matrix (q/dynamics.py:448-460)
+    const Q4 q = s2.q;
+    const float xx = q.x * q.x, yy = q.y * q.y, zz = q.z * q.z;
+    const float xy = q.x * q.y, xz = q.x * q.z, yz = q.y * q.z;
+    const float wx = q.w * q.x, wy = q.w * q.y, wz = q.w * q.z;
+    xb = v3(1.f - 2.f * (yy + zz), 2.f * (xy + wz), 2.f * (xz - wy));
+    yb = v3(2.f * (xy - wz), 1.f - 2.f * (xx + zz), 2.f * (yz + wx));
+    zb = v3(2.f * (xz + wy), 2.f * (yz - wx), 1.f - 2.f * (xx + yy));
     w = s2.w;
   } else {
     attitude_pm(thrust_of<M>(s2, g), s2.ve, xb, yb, zb);
@@ -274,12 +278,15 @@ QS_D RewardFwd reward_ctrl(const qs_weights& w, V3 off, V3 v, float effn, float 
   return RewardFwd{-pen, dist, speed};
 }
 
+// RL scalar (q/tasks.py:744-763): never differentiated, so the divisions use
+// the 2-ulp fast path
 QS_D float reward_rl(const qs_weights& w, float clip, V3 off, V3 v, float effn, float deffn) {
   float dist = norm3(off);
   float speed = norm3(v);
-  float nearv = 1.f / (1.f + expf(-(w.near_radius - dist) / w.near_width));
+  float nearv = __fdividef(1.f, 1.f + __expf(__fdividef(-(w.near_radius - dist), w.near_width)));
+  if (!(nearv == nearv)) nearv = 0.f;  // exp overflow -> 1/inf = 0 (matches the reference)
   float sd = fminf(dist * w.track_gain, w.v_max);
-  V3 vdes = off * (sd / fmaxf(dist, 1e-9f));
+  V3 vdes = off * __fdividef(sd, fmaxf(dist, 1e-9f));
   float track = norm3(v - vdes);
   float dist_c = fminf(dist, clip);
   return -(w.w_p * dist_c + w.w_v * speed * nearv + w.w_a * effn + w.w_s * deffn + w.w_t * track);
