@@ -244,15 +244,32 @@ def bench_depth(dev, rank, frames=20):
     def frame():
         sn.cast_rays(sc, pos, 4, cs, cam, 0, True)
 
-    for _ in range(3):
-        frame()
-    ms = time_graph(frame, frames)
+    def timed(tiled, sensor, kind):
+        sn.TILED = tiled
+
+        def f():
+            sn.cast_rays(sc, pos, 4, cs, sensor, kind, True)
+
+        for _ in range(3):
+            f()
+        out = time_graph(f, frames)
+        sn.TILED = True
+        return out
+
+    ms = timed(True, cam, 0)
+    ms_untiled = timed(False, cam, 0)
+    lidar = sn.LidarPattern(n_azimuth=360, n_elevation=16, max_range=20.0)
+    ms_lidar = timed(True, lidar, 1)
     cnt = sc.counts.double().cpu().numpy()
     # un-culled algorithmic flops per ray: 14 + 10 ns + 6 nb + 31 nc (+1 ground)
     flops_frame = float(np.sum(14 + 10 * cnt[:, 0] + 6 * cnt[:, 1] + 31 * cnt[:, 2] + cnt[:, 3])) * R
     return {"rays_per_s": E * R / (ms * 1e-3), "ms_per_frame": ms, "n_envs": E, "rays_per_env": R,
             "mean_solids": float(cnt[:, :3].sum(1).mean()),
-            "tflops_uncull_equiv": flops_frame / (ms * 1e-3) / 1e12}
+            "tflops_uncull_equiv": flops_frame / (ms * 1e-3) / 1e12,
+            "kernel": "k_raycast_tiled<0> (per-warp cone culling)",
+            "untiled": {"rays_per_s": E * R / (ms_untiled * 1e-3), "ms_per_frame": ms_untiled,
+                        "tflops_uncull_equiv": flops_frame / (ms_untiled * 1e-3) / 1e12},
+            "lidar_360x16": {"rays_per_s": E * lidar.n_rays / (ms_lidar * 1e-3), "ms_per_frame": ms_lidar}}
 
 
 def run_ours(a):

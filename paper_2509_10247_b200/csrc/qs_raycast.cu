@@ -255,6 +255,143 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
   }
 }
 
+// ---------------------------------------------------------------------------
+// tiled variant: rays are grouped host-side into tiles of 32 angularly compact
+// rays (8x4 pixel blocks for cameras, 2 azimuths x 16 elevations for LiDAR);
+// each tile carries a bounding cone (axis, cos/sin of its half-angle, body
+// frame).  A warp owns a tile: lane j tests staged obstacle j's bounding
+// sphere against the cone, one ballot per 32 obstacles gives the warp-uniform
+// candidate mask, and every lane intersects its ray with the candidates only.
+// The surviving set is a superset of the obstacles any ray of the tile can
+// hit, so the image is identical to the untiled kernel's.
+
+QS_D bool cone_keeps(float4 b, V3 ax, float cth, float sth) {
+  V3 u = xyz(b);
+  float L2 = dot(u, u);
+  float r = b.w;
+  if (L2 <= r * r) return true;
+  float d = dot(u, ax);
+  float L = sqrtf(L2);
+  float m = 1e-4f * (1.f + L);
+  return d >= cth * sqrtf(L2 - r * r) - sth * r - m;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
+    const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
+    const float* __restrict__ cam_cs, const float* __restrict__ dirs_body, const int* __restrict__ tile_rays,
+    const float* __restrict__ tile_cones, int n_tiles, int tiles_per_cta, float* __restrict__ out,
+    uint8_t* __restrict__ hitm) {
+  extern __shared__ float4 sm[];
+  __shared__ int cnt[3];
+  const long row = blockIdx.y;
+  const long e = row / rc.n_agents;
+  float2 cs = make_float2(1.f, 0.f);
+  if (cam_cs) cs = reinterpret_cast<const float2*>(cam_cs)[row];
+  const float* pp = pos + row * pos_stride;
+  V3 o = v3(pp[0], pp[1], pp[2]) + rotz(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
+  SceneView sv = scene_view(sc, e);
+  // layout: records then bounding spheres (centre relative to o, radius)
+  float4* s_sph = sm;
+  float4* s_box = s_sph + sc.Sm;
+  float4* s_cyl = s_box + 2 * sc.Bm;
+  float* s_cyl_hh = reinterpret_cast<float*>(s_cyl + sc.Cm);
+  float4* b_sph = reinterpret_cast<float4*>(s_cyl_hh + ((sc.Cm + 3) & ~3));
+  float4* b_box = b_sph + sc.Sm;
+  float4* b_cyl = b_box + sc.Bm;
+  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const int tot = sv.ns + sv.nb + sv.nc;
+  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+    if (i < sv.ns) {
+      float4 s = ld4(sv.sph, i);
+      V3 c = xyz(s);
+      bool keep = !rc.cull || (KIND == 0 ? keep_camera(rc, cs, o, c, s.w) : keep_ball(rc, o, c, s.w));
+      if (keep) {
+        int k = atomicAdd(&cnt[0], 1);
+        s_sph[k] = f4(o - c, s.w * s.w);
+        b_sph[k] = f4(c - o, s.w);
+      }
+    } else if (i < sv.ns + sv.nb) {
+      int j = i - sv.ns;
+      float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
+      float rad = norm3(xyz(h));
+      bool keep = !rc.cull ||
+                  (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
+      if (keep) {
+        int k = atomicAdd(&cnt[1], 1);
+        s_box[2 * k] = f4(xyz(c) - xyz(h) - o, 0.f);
+        s_box[2 * k + 1] = f4(xyz(c) + xyz(h) - o, 0.f);
+        b_box[k] = f4(xyz(c) - o, rad);
+      }
+    } else {
+      int j = i - sv.ns - sv.nb;
+      float4 c = ld4(sv.cyl, 2 * j);
+      float hh = __ldg(sv.cyl + 8 * j + 4);
+      float rad = sqrtf(c.w * c.w + hh * hh);
+      bool keep = !rc.cull ||
+                  (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
+      if (keep) {
+        int k = atomicAdd(&cnt[2], 1);
+        s_cyl[k] = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
+        s_cyl_hh[k] = hh;
+        b_cyl[k] = f4(xyz(c) - o, rad);
+      }
+    }
+  }
+  __syncthreads();
+  const int ns = cnt[0], nb = cnt[1], nc = cnt[2];
+  const bool ground = sv.ground;
+  const float gdz = sv.gz - o.z;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+  for (int tile = t0 + warp; tile < t1; tile += nwarps) {
+    const float4 cone = ld4(tile_cones, tile);  // axis (body), cos(half-angle)
+    const V3 ax = rotz(cs, xyz(cone));
+    const float cth = cone.w, sth = sqrtf(fmaxf(0.f, 1.f - cone.w * cone.w));
+    const int ray = __ldg(tile_rays + tile * 32 + lane);
+    V3 d = v3(1.f, 0.f, 0.f);
+    if (ray >= 0) d = rotz(cs, xyz(ld4(dirs_body, ray)));
+    const V3 inv = v3(1.f / d.x, 1.f / d.y, 1.f / d.z);
+    const float a = d.x * d.x + d.y * d.y;
+    const float inv_a = 1.f / a;
+    float best = INF;
+    for (int base = 0; base < ns; base += 32) {
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < ns && cone_keeps(b_sph[base + lane], ax, cth, sth));
+      while (m) {
+        int i = base + __ffs(m) - 1;
+        m &= m - 1;
+        best = fminf(best, hit_sphere(s_sph[i], d));
+      }
+    }
+    for (int base = 0; base < nb; base += 32) {
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < nb && cone_keeps(b_box[base + lane], ax, cth, sth));
+      while (m) {
+        int i = base + __ffs(m) - 1;
+        m &= m - 1;
+        best = fminf(best, hit_box(s_box[2 * i], s_box[2 * i + 1], inv, nullptr));
+      }
+    }
+    for (int base = 0; base < nc; base += 32) {
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < nc && cone_keeps(b_cyl[base + lane], ax, cth, sth));
+      while (m) {
+        int i = base + __ffs(m) - 1;
+        m &= m - 1;
+        best = fminf(best, hit_cyl(s_cyl[i], s_cyl_hh[i], d, a, inv_a, inv.z, nullptr));
+      }
+    }
+    if (ground) {
+      float t = gdz * inv.z;
+      if (t >= 0.f && t < INF) best = fminf(best, t);
+    }
+    if (ray >= 0) {
+      const long oi = row * rc.n_rays + ray;
+      out[oi] = fminf(best, rc.max_range);
+      if (hitm) hitm[oi] = best < rc.max_range ? 1 : 0;
+    }
+  }
+}
+
 // g_pos[row] += sum_r g_depth[row, r] * dT_dO[row, r]   (one CTA per row)
 __global__ void __launch_bounds__(256) k_raycast_vjp(int n_rays, const float* __restrict__ g_depth,
                                                      const float* __restrict__ dT_dO,
@@ -306,6 +443,26 @@ int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, con
   else if (cfg->kind == 1) { if (g) QS_RC(1, true); else QS_RC(1, false); }
   else { if (g) QS_RC(2, true); else QS_RC(2, false); }
 #undef QS_RC
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
+
+int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
+                     int32_t pos_stride, const float* cam_cs, const float* dirs_body,
+                     const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, float* out,
+                     uint8_t* hit, void* stream) {
+  if (n_rows <= 0 || cfg->n_rays <= 0) return QS_OK;
+  if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0) return QS_ERR_BAD_ARGUMENT;
+  const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
+  dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
+  size_t smem = (size_t)(scene->Sm + 2 * scene->Bm + scene->Cm) * 16 + ((scene->Cm + 3) & ~3) * 4 +
+                (size_t)(scene->Sm + scene->Bm + scene->Cm) * 16;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cfg->kind == 0)
+    k_raycast_tiled<0><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
+                                                     tile_rays, tile_cones, n_tiles, tpc, out, hit);
+  else
+    k_raycast_tiled<1><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
+                                                     tile_rays, tile_cones, n_tiles, tpc, out, hit);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 

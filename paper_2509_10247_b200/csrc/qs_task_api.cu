@@ -2,9 +2,20 @@
 #include "qs_dynamics.cuh"
 
 namespace qs {
+template <int T, int NA>
+int task_dispatch_na(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
+                     const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
+
 template <int T>
 int task_dispatch(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
-                  const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
+                  const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s) {
+  if (cfg->n_agents > 1) {
+    if (T == QS_TASK_RACING) return QS_ERR_BAD_ARGUMENT;  // racing is single-agent (q/tasks.py:859)
+    return task_dispatch_na<T == QS_TASK_RACING ? QS_TASK_POSITION : T, QS_MAX_AGENTS>(op, cfg, sc, p, mask,
+                                                                                       tab, s);
+  }
+  return task_dispatch_na<T, 1>(op, cfg, sc, p, mask, tab, s);
+}
 }
 
 namespace {

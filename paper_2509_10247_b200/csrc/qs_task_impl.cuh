@@ -1170,10 +1170,11 @@ int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_wind
   return launch_status();
 }
 
-// op: 0 fwd, 1 bwd, 2 spawn, 3 observe, 4 window fwd, 5 window bwd
-template <int T>
-int task_dispatch(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
-                  const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
+// op: 0 fwd, 1 bwd, 2 spawn, 3 observe, 4 window fwd, 5 window bwd.
+// One translation unit per (task, agent capacity) keeps the build parallel.
+template <int T, int NA>
+int task_dispatch_na(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
+                     const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
 
 template <int T, int M, int NA>
 int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, const uint8_t* mask,
@@ -1189,24 +1190,18 @@ int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, c
   return QS_ERR_BAD_ARGUMENT;
 }
 
-#define QS_DEFINE_TASK_DISPATCH(T, MULTI_OK)                                                   \
-  template <>                                                                                 \
-  int task_dispatch<T>(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,     \
-                       const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s) {      \
-    const bool multi = cfg->n_agents > 1;                                                     \
-    if (multi && !(MULTI_OK)) return QS_ERR_BAD_ARGUMENT;                                     \
-    switch (cfg->model) {                                                                     \
-      case QS_MODEL_FULL:                                                                     \
-        return multi ? task_op<T, QS_MODEL_FULL, QS_MAX_AGENTS>(op, cfg, sc, p, mask, tab, s) \
-                     : task_op<T, QS_MODEL_FULL, 1>(op, cfg, sc, p, mask, tab, s);            \
-      case QS_MODEL_PM_CONTINUOUS:                                                            \
-        return multi ? task_op<T, QS_MODEL_PM_CONTINUOUS, QS_MAX_AGENTS>(op, cfg, sc, p, mask, tab, s) \
-                     : task_op<T, QS_MODEL_PM_CONTINUOUS, 1>(op, cfg, sc, p, mask, tab, s);   \
-      case QS_MODEL_PM_DISCRETE:                                                              \
-        return multi ? task_op<T, QS_MODEL_PM_DISCRETE, QS_MAX_AGENTS>(op, cfg, sc, p, mask, tab, s) \
-                     : task_op<T, QS_MODEL_PM_DISCRETE, 1>(op, cfg, sc, p, mask, tab, s);     \
-    }                                                                                         \
-    return QS_ERR_BAD_ARGUMENT;                                                               \
+#define QS_DEFINE_TASK_DISPATCH(T, NA)                                                          \
+  template <>                                                                                  \
+  int task_dispatch_na<T, NA>(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, \
+                              const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s) { \
+    switch (cfg->model) {                                                                      \
+      case QS_MODEL_FULL: return task_op<T, QS_MODEL_FULL, NA>(op, cfg, sc, p, mask, tab, s);  \
+      case QS_MODEL_PM_CONTINUOUS:                                                             \
+        return task_op<T, QS_MODEL_PM_CONTINUOUS, NA>(op, cfg, sc, p, mask, tab, s);           \
+      case QS_MODEL_PM_DISCRETE:                                                               \
+        return task_op<T, QS_MODEL_PM_DISCRETE, NA>(op, cfg, sc, p, mask, tab, s);             \
+    }                                                                                          \
+    return QS_ERR_BAD_ARGUMENT;                                                                \
   }
 
 }  // namespace qs

@@ -1,5 +1,5 @@
-// Position task instantiations (q/tasks.py:658-763).
+// Position task, single agent (q/tasks.py:658-763) instantiations.
 #include "qs_task_impl.cuh"
 namespace qs {
-QS_DEFINE_TASK_DISPATCH(QS_TASK_POSITION, true)
+QS_DEFINE_TASK_DISPATCH(QS_TASK_POSITION, 1)
 }

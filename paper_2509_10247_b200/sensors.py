@@ -261,6 +261,43 @@ def _dir_table(sensor, device) -> torch.Tensor:
     return t
 
 
+_TILE_CACHE: dict = {}
+
+
+def _tile_table(sensor, device):
+    """Group the sensor's rays into angularly compact tiles of 32 with a bounding
+    cone each (fp64 host geometry, once per sensor): 8x4 pixel blocks for a
+    camera, consecutive azimuth-major runs for a LiDAR."""
+    key = (type(sensor).__name__, repr(sensor), str(device))
+    hit = _TILE_CACHE.get(key)
+    if hit is not None:
+        return hit
+    if isinstance(sensor, CameraIntrinsics):
+        d = sensor.pixel_dirs()
+        W, H = sensor.width, sensor.height
+        tiles = []
+        for ty in range(0, H, 4):
+            for tx in range(0, W, 8):
+                tiles.append([r * W + c for r in range(ty, min(H, ty + 4)) for c in range(tx, min(W, tx + 8))])
+    else:
+        d = sensor.ray_dirs()
+        tiles = [list(range(s, min(len(d), s + 32))) for s in range(0, len(d), 32)]
+    rays = np.full((len(tiles), 32), -1, dtype=np.int32)
+    cones = np.zeros((len(tiles), 4))
+    for k, t in enumerate(tiles):
+        rays[k, :len(t)] = t
+        v = d[t]
+        ax = v.sum(0)
+        n = np.linalg.norm(ax)
+        ax = ax / n if n > 1e-12 else np.array([1.0, 0.0, 0.0])
+        c = float(np.min(v @ ax)) if n > 1e-12 else -1.0
+        cones[k, :3] = ax
+        cones[k, 3] = max(-1.0, c - 1e-6)  # widen by ~1e-6 rad for round-off
+    out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device))
+    _TILE_CACHE[key] = out
+    return out
+
+
 def _ray_cfg(sensor, kind, cull, n_agents=1) -> L.QsRayCfg:
     rc = L.QsRayCfg()
     rc.kind = kind
@@ -302,10 +339,19 @@ def cast_rays(scene: DeviceScene, pos: torch.Tensor, pos_stride: int, cam_cs, se
     hit = torch.empty(N, rc.n_rays, dtype=torch.uint8, device=dev) if want_hit else None
     dT = torch.empty(N, rc.n_rays, 4, dtype=torch.float32, device=dev) if want_grad else None
     dirs = _dir_table(sensor, dev)
+    if not want_grad and kind in (0, 1) and TILED:
+        tr, tc = _tile_table(sensor, dev)
+        L.check(L.lib().qs_raycast_tiled(rc, scene.struct(), N, L.ptr(pos), pos_stride, L.ptr(cam_cs),
+                                         L.ptr(dirs), L.ptr(tr), L.ptr(tc), tr.shape[0], L.ptr(out),
+                                         L.ptr(hit), L.stream_handle(dev)), "qs_raycast_tiled")
+        return out, hit, dT
     L.check(L.lib().qs_raycast(rc, scene.struct(), N, L.ptr(pos), pos_stride, L.ptr(cam_cs),
                                L.ptr(dirs), None, L.ptr(out), L.ptr(hit), L.ptr(dT),
                                L.stream_handle(dev)), "qs_raycast")
     return out, hit, dT
+
+
+TILED = True  # per-warp cone culling (k_raycast_tiled); False selects the untiled kernel
 
 
 def raycast(prims, origins, dirs, max_range: float, chunk_elems: int = 0, device=None):
