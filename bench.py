@@ -294,7 +294,7 @@ def run_ours(a):
         for _ in range(max(1, a.warmup)):
             win.run()
         torch.cuda.synchronize()
-        print(json.dumps({"profile_run": True, "loss": float(win.loss)}))
+        print(json.dumps({"profile_run": True, "loss": float(win.loss64 if win.fused else win.loss)}))
         return
     for _ in range(a.warmup):
         win.run()
@@ -320,7 +320,7 @@ def run_ours(a):
         ms = e0.elapsed_time(e1) / a.steps
     ms = max_over_ranks(ms, world)
     value = world * N * T / (ms * 1e-3)
-    loss = float(win.loss)
+    loss = float(win.loss64 if win.fused else win.loss)
     assert np.isfinite(loss)
 
     # per-kernel durations: one graph holding only the window-forward launch,

@@ -162,6 +162,12 @@ typedef struct qs_window_io {
   const float* g_S_final;  /* (NP,N,4) | NULL */
   float* g_actions;        /* (T,N,A) */
   float* g_S0;             /* (NP,N,4) | NULL */
+  /* fwd: loss += -(1/(T N)) sum_t gamma^t sum_rows r_ctrl[t]  (the BPTT loss,
+   * q/learners.py:222,254); zeroed by qs_task_window_fwd.  NULL = skip */
+  double* loss;
+  /* bwd: after the reverse sweep copy checkpoint slot T into slot 0 (the next
+   * window starts where this one ended) */
+  int32_t carry;
 } qs_window_io;
 
 int qs_abi_version(void);
@@ -212,8 +218,8 @@ int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, con
                const float* dirs_world, float* out, uint8_t* hit, float* dT_dO, void* stream);
 /* Same images as qs_raycast (kinds 0/1) with per-warp cone culling: rays are
  * grouped into n_tiles tiles of 32 (tile_rays (n_tiles,32) ray indices, -1 =
- * empty slot), each with a body-frame bounding cone tile_cones (n_tiles,4) =
- * unit axis xyz, cos(half-angle). */
+ * empty slot), each with a body-frame bounding cone tile_cones (n_tiles,8) =
+ * unit axis xyz, cos(half-angle), sin(half-angle), 3 pad. */
 int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
                      int32_t pos_stride, const float* cam_cs, const float* dirs_body,
                      const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, float* out,

@@ -78,7 +78,8 @@ class QsWindowIo(C.Structure):
     _fields_ = [("T", i32)] + [(n, vp) for n in (
         "S", "goal", "peff", "dr", "actions", "meta", "ep_return", "imu_bias", "imu_noise", "imu_out",
         "obs", "r", "terminated", "truncated", "flags", "stats", "err", "g_rctrl")] + [
-        ("g_rctrl_scale", f32), ("gamma", f32)] + [(n, vp) for n in ("g_S_final", "g_actions", "g_S0")]
+        ("g_rctrl_scale", f32), ("gamma", f32)] + [(n, vp) for n in ("g_S_final", "g_actions", "g_S0", "loss")] + [
+        ("carry", i32)]
 
 
 class QsResetTable(C.Structure):

@@ -23,7 +23,18 @@ QS_HD float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 QS_HD V3 cross(V3 a, V3 b) {
   return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
 }
-QS_HD float norm3(V3 a) { return sqrtf(dot(a, a)); }
+// Euclidean norm.  On device: MUFU sqrt (sqrt.approx, ~1 ulp) instead of the
+// IEEE-rounded sequence; norms feed rewards, SDF and attitude, all checked
+// against the fp64 oracle at 1e-5 relative.
+QS_HD float norm3(V3 a) {
+#ifdef __CUDA_ARCH__
+  float d;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(d) : "f"(dot(a, a)));
+  return d;
+#else
+  return sqrtf(dot(a, a));
+#endif
+}
 QS_HD V3& operator+=(V3& a, V3 b) {
   a.x += b.x; a.y += b.y; a.z += b.z;
   return a;
@@ -138,6 +149,42 @@ struct Rng {
     return d;
   }
 };
+
+// ---------------------------------------------------------------------------
+// TMA bulk copy (cp.async.bulk, sm_90+) global -> shared with mbarrier
+// completion; used to stage the next step's action block one step ahead.
+
+QS_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+QS_D void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+QS_D void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+QS_D void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// one thread: arm the barrier with the byte count and launch the bulk copy
+QS_D void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+QS_D void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
 
 QS_D void report_err(int32_t* err, int code, int row) {
   if (!err) return;

@@ -265,16 +265,22 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
 // The surviving set is a superset of the obstacles any ray of the tile can
 // hit, so the image is identical to the untiled kernel's.
 
-QS_D bool cone_keeps(float4 b, V3 ax, float cth, float sth) {
-  V3 u = xyz(b);
+// bounding-sphere record, hoisted once per (env, obstacle):
+//   b = (u = c - o, Q)  with Q = sqrt(|u|^2 - r^2) the tangent length (-1: o inside)
+//   e = (r, slack)      slack = 1e-4 (1 + |u|) absorbs fp32 round-off
+// keep iff angle(u, axis) <= half-angle + asin(r/|u|)
+//      <=> u . axis >= cos(th) Q - sin(th) r           (times |u| on both sides)
+QS_D float4 bsphere(V3 u, float r, float2& e) {
   float L2 = dot(u, u);
-  float r = b.w;
-  if (L2 <= r * r) return true;
-  float d = dot(u, ax);
   float L = sqrtf(L2);
-  float m = 1e-4f * (1.f + L);
-  return d >= cth * sqrtf(L2 - r * r) - sth * r - m;
+  e = make_float2(r, 1e-4f * (1.f + L));
+  return f4(u, L2 <= r * r ? -1.f : sqrtf(L2 - r * r));
 }
+QS_D bool cone_keeps(float4 b, float2 e, V3 ax, float cth, float sth) {
+  if (b.w < 0.f) return true;
+  return dot(xyz(b), ax) >= cth * b.w - sth * e.x - e.y;
+}
+QS_D float rcp_fast(float x) { return __fdividef(1.f, x); }  // MUFU.RCP; 1/(+-0) = +-inf
 
 template <int KIND>
 __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
@@ -299,6 +305,9 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
   float4* b_sph = reinterpret_cast<float4*>(s_cyl_hh + ((sc.Cm + 3) & ~3));
   float4* b_box = b_sph + sc.Sm;
   float4* b_cyl = b_box + sc.Bm;
+  float2* e_sph = reinterpret_cast<float2*>(b_cyl + sc.Cm);
+  float2* e_box = e_sph + sc.Sm;
+  float2* e_cyl = e_box + sc.Bm;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   __syncthreads();
   const int tot = sv.ns + sv.nb + sv.nc;
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
       if (keep) {
         int k = atomicAdd(&cnt[0], 1);
         s_sph[k] = f4(o - c, s.w * s.w);
-        b_sph[k] = f4(c - o, s.w);
+        b_sph[k] = bsphere(c - o, s.w, e_sph[k]);
       }
     } else if (i < sv.ns + sv.nb) {
       int j = i - sv.ns;
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
         int k = atomicAdd(&cnt[1], 1);
         s_box[2 * k] = f4(xyz(c) - xyz(h) - o, 0.f);
         s_box[2 * k + 1] = f4(xyz(c) + xyz(h) - o, 0.f);
-        b_box[k] = f4(xyz(c) - o, rad);
+        b_box[k] = bsphere(xyz(c) - o, rad, e_box[k]);
       }
     } else {
       int j = i - sv.ns - sv.nb;
@@ -335,7 +344,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
         int k = atomicAdd(&cnt[2], 1);
         s_cyl[k] = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
         s_cyl_hh[k] = hh;
-        b_cyl[k] = f4(xyz(c) - o, rad);
+        b_cyl[k] = bsphere(xyz(c) - o, rad, e_cyl[k]);
       }
     }
   }
@@ -346,18 +355,20 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
-    const float4 cone = ld4(tile_cones, tile);  // axis (body), cos(half-angle)
+    const float4 cone = ld4(tile_cones, 2 * tile);  // axis (body), cos(half-angle)
+    const float sth = __ldg(tile_cones + 8 * tile + 4);
     const V3 ax = rotz(cs, xyz(cone));
-    const float cth = cone.w, sth = sqrtf(fmaxf(0.f, 1.f - cone.w * cone.w));
+    const float cth = cone.w;
     const int ray = __ldg(tile_rays + tile * 32 + lane);
     V3 d = v3(1.f, 0.f, 0.f);
     if (ray >= 0) d = rotz(cs, xyz(ld4(dirs_body, ray)));
-    const V3 inv = v3(1.f / d.x, 1.f / d.y, 1.f / d.z);
+    const V3 inv = v3(rcp_fast(d.x), rcp_fast(d.y), rcp_fast(d.z));
     const float a = d.x * d.x + d.y * d.y;
-    const float inv_a = 1.f / a;
+    const float inv_a = rcp_fast(a);
     float best = INF;
     for (int base = 0; base < ns; base += 32) {
-      unsigned m = __ballot_sync(0xffffffffu, base + lane < ns && cone_keeps(b_sph[base + lane], ax, cth, sth));
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < ns &&
+                                                  cone_keeps(b_sph[base + lane], e_sph[base + lane], ax, cth, sth));
       while (m) {
         int i = base + __ffs(m) - 1;
         m &= m - 1;
@@ -365,7 +376,8 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
       }
     }
     for (int base = 0; base < nb; base += 32) {
-      unsigned m = __ballot_sync(0xffffffffu, base + lane < nb && cone_keeps(b_box[base + lane], ax, cth, sth));
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < nb &&
+                                                  cone_keeps(b_box[base + lane], e_box[base + lane], ax, cth, sth));
       while (m) {
         int i = base + __ffs(m) - 1;
         m &= m - 1;
@@ -373,7 +385,8 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
       }
     }
     for (int base = 0; base < nc; base += 32) {
-      unsigned m = __ballot_sync(0xffffffffu, base + lane < nc && cone_keeps(b_cyl[base + lane], ax, cth, sth));
+      unsigned m = __ballot_sync(0xffffffffu, base + lane < nc &&
+                                                  cone_keeps(b_cyl[base + lane], e_cyl[base + lane], ax, cth, sth));
       while (m) {
         int i = base + __ffs(m) - 1;
         m &= m - 1;
@@ -455,7 +468,7 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
   size_t smem = (size_t)(scene->Sm + 2 * scene->Bm + scene->Cm) * 16 + ((scene->Cm + 3) & ~3) * 4 +
-                (size_t)(scene->Sm + scene->Bm + scene->Cm) * 16;
+                (size_t)(scene->Sm + scene->Bm + scene->Cm) * (16 + 8);
   cudaStream_t s = (cudaStream_t)stream;
   if (cfg->kind == 0)
     k_raycast_tiled<0><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,

@@ -514,6 +514,7 @@ struct StepStat {
   bool done;
   int term;
   float ret;
+  float rc_sum;  // sum of r_ctrl over the env's rows
 };
 
 // ---------------------------------------------------------------------------
@@ -704,7 +705,11 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, i
     }
     out.flags[row] = fl;
   }
-  return StepStat{done, term_env, ret};
+  float rc_sum = 0.f;
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a)
+    if (a < na) rc_sum += rc[a];
+  return StepStat{done, term_env, ret, rc_sum};
 }
 
 // ---------------------------------------------------------------------------
@@ -920,50 +925,84 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   EnvRegs<NAMAX> R;
   int n_done = 0, n_succ = 0, n_coll = 0;
   float ret_sum = 0.f;
-  float4 raw[NAMAX], raw_next[NAMAX];
-  if (active) {
+  double loss_sum = 0.0;
+  float gpow = 1.f;
+  // The CTA's action block of a step (blockDim * na rows x A floats, contiguous)
+  // is staged in shared memory by a TMA bulk copy issued one step ahead into a
+  // double buffer, so the action latency never sits on the step's critical path
+  // and costs no registers.  Partial tail CTAs load directly.
+  __shared__ __align__(128) float s_raw[2][WIN_BLOCK * NAMAX * 4];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  const long e0 = (long)blockIdx.x * blockDim.x;
+  const uint32_t blk_bytes = (uint32_t)(blockDim.x * na * A * 4);
+  const bool use_tma = (e0 + blockDim.x <= cfg.n_envs) && (blk_bytes % 16 == 0) && ((N * A) % 4 == 0) &&
+                       ((reinterpret_cast<uintptr_t>(w.actions) & 15) == 0);
+  if (use_tma && threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (use_tma && threadIdx.x == 0) {
+    tma_load_1d(s_raw[0], w.actions + e0 * na * A, blk_bytes, &s_bar[0]);
+    if (w.T > 1) tma_load_1d(s_raw[1], w.actions + (N + e0 * na) * A, blk_bytes, &s_bar[1]);
+  }
+  if (active)
     env_load<M, NAMAX>(cfg, sc.bounds, e, na, N, R, w.S, w.goal, w.peff, w.dr, w.meta, w.ep_return,
                        w.imu_bias);
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a)
-      if (a < na) raw[a] = load_act<A>(w.actions, e * na + a);
-  }
   for (int t = 0; t < w.T; ++t) {
-    if (active) {
-      // prefetch the next step's actions: their latency hides under this step
-      if (t + 1 < w.T) {
+    float4 raw[NAMAX];
+    if (use_tma) {
+      mbar_wait(&s_bar[t & 1], (t >> 1) & 1);
+      const float* sr = s_raw[t & 1];
 #pragma unroll
-        for (int a = 0; a < NAMAX; ++a)
-          if (a < na) raw_next[a] = load_act<A>(w.actions + (long)(t + 1) * N * A, e * na + a);
+      for (int a = 0; a < NAMAX; ++a) {
+        if (a >= na) break;
+        const float* p = sr + (threadIdx.x * na + a) * A;
+        raw[a] = make_float4(p[0], p[1], p[2], A == 4 ? p[3] : 0.f);
       }
+    } else if (active) {
+#pragma unroll
+      for (int a = 0; a < NAMAX; ++a)
+        if (a < na) raw[a] = load_act<A>(w.actions + (long)t * N * A, e * na + a);
+    }
+    if (active) {
       StepOut o{w.obs ? w.obs + (long)t * N * P : nullptr, w.r + (long)t * 3 * N, w.r + (long)t * 3 * N + N,
                 w.r + (long)t * 3 * N + 2 * N, w.terminated + (long)t * N, w.truncated + (long)t * N,
                 w.flags + (long)t * N, nullptr, has_imu ? w.imu_out + (long)t * N * 6 : nullptr,
                 w.imu_noise ? w.imu_noise + (long)t * 4 * N * 3 : nullptr};
       StepStat st = env_step_fwd<M, TASK, NAMAX, true>(cfg, sc, e, na, N, R, raw, o, w.err, has_dr, has_imu);
-#pragma unroll
-      for (int a = 0; a < NAMAX; ++a) raw[a] = raw_next[a];
       if (st.done) {
         n_done++;
         n_succ += st.term == 1;
         n_coll += st.term == 2;
         ret_sum += st.ret;
       }
+      loss_sum += (double)(gpow * st.rc_sum);
+      gpow *= w.gamma;
       env_store_ckpt<M, NAMAX>(e, na, N, R, w.S + (long)(t + 1) * NP * N * 4, w.goal + (long)(t + 1) * N * 4,
                                w.peff + (long)(t + 1) * N * 4, has_dr ? w.dr + (long)(t + 1) * N * 4 : nullptr);
     }
+    if (use_tma) {
+      __syncthreads();  // every thread has consumed buffer t&1: refill it with step t+2
+      if (threadIdx.x == 0 && t + 2 < w.T)
+        tma_load_1d(s_raw[t & 1], w.actions + ((long)(t + 2) * N + e0 * na) * A, blk_bytes, &s_bar[t & 1]);
+    }
   }
   if (active) env_store_inplace<NAMAX>(e, na, R, w.meta, w.ep_return, has_imu ? w.imu_bias : nullptr);
-  // episode statistics: one warp reduction for the whole window
+  // episode statistics and the BPTT loss: one warp reduction for the window
   double r = ret_sum;
+  double ls = loss_sum;
   int c0 = n_done, c1 = n_succ, c2 = n_coll;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     r += __shfl_xor_sync(0xffffffffu, r, o);
+    ls += __shfl_xor_sync(0xffffffffu, ls, o);
     c0 += __shfl_xor_sync(0xffffffffu, c0, o);
     c1 += __shfl_xor_sync(0xffffffffu, c1, o);
     c2 += __shfl_xor_sync(0xffffffffu, c2, o);
   }
+  if ((threadIdx.x & 31) == 0 && w.loss) atomicAdd(w.loss, ls * (double)w.g_rctrl_scale);
   if ((threadIdx.x & 31) == 0 && w.stats && c0) {
     atomicAdd(w.stats + 0, (double)c0);
     atomicAdd(w.stats + 1, (double)c1);
@@ -1037,6 +1076,19 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
     for (int a = 0; a < NAMAX; ++a) {
       if (a >= na) break;
       store_state<M>(w.g_S0, N, e * na + a, gS[a]);
+    }
+  }
+  if (w.carry) {  // this thread's rows only: slot 0 was its last checkpoint read
+    const long T = w.T;
+#pragma unroll
+    for (int a = 0; a < NAMAX; ++a) {
+      if (a >= na) break;
+      const long row = e * na + a;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) st4(w.S, (long)k * N + row, ld4(w.S + T * NP * N * 4, (long)k * N + row));
+      st4(w.goal, row, ld4(w.goal + T * N * 4, row));
+      st4(w.peff, row, ld4(w.peff + T * N * 4, row));
+      if (has_dr) st4(w.dr, row, ld4(w.dr + T * N * 4, row));
     }
   }
 }
@@ -1163,6 +1215,7 @@ int run_observe(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io
 template <int M, int T, int NA>
 int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_window_io* w, cudaStream_t s) {
   if (w->T <= 0) return QS_OK;
+  if (op == 4 && w->loss) cudaMemsetAsync(w->loss, 0, sizeof(double), s);
   if (op == 4)
     k_window_fwd<M, T, NA><<<grid_for(cfg->n_envs, WIN_BLOCK), WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
   else

@@ -283,7 +283,7 @@ def _tile_table(sensor, device):
         d = sensor.ray_dirs()
         tiles = [list(range(s, min(len(d), s + 32))) for s in range(0, len(d), 32)]
     rays = np.full((len(tiles), 32), -1, dtype=np.int32)
-    cones = np.zeros((len(tiles), 4))
+    cones = np.zeros((len(tiles), 8))  # axis xyz, cos(half-angle), sin(half-angle), pad
     for k, t in enumerate(tiles):
         rays[k, :len(t)] = t
         v = d[t]
@@ -291,8 +291,10 @@ def _tile_table(sensor, device):
         n = np.linalg.norm(ax)
         ax = ax / n if n > 1e-12 else np.array([1.0, 0.0, 0.0])
         c = float(np.min(v @ ax)) if n > 1e-12 else -1.0
+        th = min(np.pi, np.arccos(np.clip(c, -1.0, 1.0)) + 1e-6)  # widen for round-off
         cones[k, :3] = ax
-        cones[k, 3] = max(-1.0, c - 1e-6)  # widen by ~1e-6 rad for round-off
+        cones[k, 3] = np.cos(th)
+        cones[k, 4] = np.sin(th)
     out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device))
     _TILE_CACHE[key] = out
     return out

@@ -45,6 +45,7 @@ class BpttWindow:
         self.g_r = w[:, None].expand(T, N).contiguous()
         self.w_loss = w[:, None] * 1.0
         self.loss = torch.zeros((), **f)
+        self.loss64 = torch.zeros((), dtype=torch.float64, device=dev)
         self.want_obs = want_obs
         self.fused = fused
         self.graph = None
@@ -83,6 +84,8 @@ class BpttWindow:
         w.g_rctrl_scale = -1.0 / (self.T * e.N)
         w.gamma = self.gamma
         w.g_actions = L.ptr(self.g_actions)
+        w.loss = L.ptr(self.loss64)  # accumulated by the forward kernel
+        w.carry = 1  # the backward moves slot T into slot 0 for the next window
         return w
 
     def _run(self):
@@ -95,7 +98,6 @@ class BpttWindow:
             w = self._window_io()
             L.check(lib.qs_task_window_fwd(cfg, sc, w, stream), "qs_task_window_fwd")
             L.check(lib.qs_task_window_bwd(cfg, sc, w, stream), "qs_task_window_bwd")
-            self._finish()
             return
         for t in range(T):
             io = e._new_io()
@@ -159,7 +161,7 @@ class BpttWindow:
             self.graph.replay()
         else:
             self._run()
-        return self.loss, self.g_actions
+        return (self.loss64 if self.fused else self.loss), self.g_actions
 
     def sync_env(self):
         """Write the window's final state back into the env object."""
