@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no cpu/clock sampling)")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="c2: headline BPTT windows; c5: SHAC training with NCCL gradient all-reduce")
     return ap.parse_args()
 
 
@@ -474,9 +476,49 @@ def run_reference(a):
     }))
 
 
+def run_c5(a):
+    """C5: SHAC-style differentiable training, pm_continuous position task,
+    131,072 envs per GPU, horizon 16, GRU-64 + MLP-128^2 policy, privileged
+    critic; policy/critic gradients averaged by NCCL all-reduce across ranks.
+    Reports training env-steps/s and the all-reduce time separately."""
+    import torch
+
+    world, rank, local = dist_init()
+    dev = torch.device("cuda", local if world > 1 else 0)
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.train import LearnerOptions, ShortHorizonTrainer
+
+    N = 131072 if a.envs == 65536 else a.envs
+    cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=N, episode_len=128)
+    env = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
+    env.reset(seed=1)
+    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0))
+    for _ in range(a.warmup):
+        tr.update()
+    torch.cuda.synchronize()
+    barrier(world)
+    tr.timing = {"sim_fwd_bwd_s": 0.0, "allreduce_s": 0.0}
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        out = tr.update()
+    torch.cuda.synchronize()
+    el = max_over_ranks(time.perf_counter() - t0, world)
+    ar = max_over_ranks(tr.timing["allreduce_s"], world)
+    if rank == 0:
+        print(json.dumps({
+            "metric": "env-steps/s (SHAC train: policy + sim fwd+bwd + critic)", "value": world * N * 16 * a.steps / el,
+            "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "dtype": "f32",
+            "config": {"workload": f"C5: SHAC, pm_continuous position, {N} envs/GPU x {world}, horizon 16",
+                       "parallelism": f"env-sharded x{world}; NCCL all-reduce of policy+critic grads"},
+            "allreduce_ms_per_update": ar / a.steps * 1e3, "last": out}))
+
+
 if __name__ == "__main__":
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.workload == "c5":
+        run_c5(args)
     else:
         run_ours(args)

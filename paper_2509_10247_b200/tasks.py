@@ -773,6 +773,51 @@ class FlightTask:
     def state_records(self):
         return {k: v.detach().cpu().tolist() for k, v in self.state.fields().items()}
 
+    # -- critic features (q/tasks.py:292-297, 465-545)
+
+    def privileged_dim(self) -> int:
+        return 14
+
+    def privileged_scale(self) -> tuple:
+        return (0.2,) * 3 + (1 / 3.0,) * 3 + (0.1,) * 3 + (0.2,) + (1.0,) * 3 + (0.2,)
+
+    def _thrust(self, st: dyn.QuadState) -> torch.Tensor:
+        """q/tasks.py:479-498."""
+        name = self.config.dynamics
+        g = torch.as_tensor(self.base_params.g_vec, dtype=torch.float32, device=self.device)
+        if name == "pm_continuous":
+            return st.a_lat
+        if name == "pm_discrete":
+            return st.u_prev - g
+        w, x, y, z = st.q.unbind(-1)
+        zb = torch.stack([2 * (x * z + w * y), 2 * (y * z - w * x), 1 - 2 * (x * x + y * y)], -1)
+        return zb * 9.81
+
+    def privileged_var(self) -> torch.Tensor:
+        """(N,14) critic features, differentiable through the state (q/tasks.py:500-523):
+        yaw-local goal offset, velocity, thrust; sdf clamped to +-5; yaw-local
+        clearance direction (constant); goal distance.  The clearance direction
+        is the sdf kernel's analytic gradient of the nearest primitive, which is
+        what the reference's 6-probe central difference (h=1e-4, :465-477)
+        approximates; in fp32 that difference quotient would be noise-limited."""
+        st = self.state
+        cam = _cam_of(self)
+        c, s = cam[:, 0:1], cam[:, 1:2]
+
+        def unrot(v):
+            return torch.cat([c * v[:, 0:1] + s * v[:, 1:2], -s * v[:, 0:1] + c * v[:, 1:2], v[:, 2:3]], -1)
+
+        off = self.goals - st.p
+        sd = sn.sdf_var(st.p, self._scene, self.n_agents)
+        _, grad = sn._sdf_launch(self._scene, st.p.detach(), self.n_agents, True)
+        return torch.cat([unrot(off), unrot(st.v), unrot(self._thrust(st)), torch.clamp(sd, -5.0, 5.0)[:, None],
+                          unrot(grad[:, 0:3]), torch.linalg.norm(off, dim=-1, keepdim=True)], -1)
+
+    def privileged_state(self) -> torch.Tensor:
+        """No-grad twin of privileged_var (q/tasks.py:525-545)."""
+        with torch.no_grad():
+            return self.privileged_var().detach()
+
 
 class _ObserveFn(torch.autograd.Function):
     """observe() on a grad-carrying state: value from qs_task_observe, VJP from

@@ -388,8 +388,26 @@ def gen_world():
     save("world", **rec)
 
 
+def gen_learners():
+    """TD-lambda targets (q/learners.py:78-113), the critic side of configs C5."""
+    from quadsim import learners as ln
+
+    rng = np.random.default_rng(400)
+    T, N = 16, 32
+    r = rng.normal(size=(T, N))
+    values = rng.normal(size=(T, N))
+    boot = rng.normal(size=N)
+    done = rng.uniform(size=(T, N)) < 0.1
+    rec = {"r": r, "values": values, "boot": boot, "done": done}
+    rec["td"] = ln.td_lambda_targets(r, values, boot, done, 0.99, 0.95)
+    rec["td_k4"] = ln.td_lambda_targets(r, values, boot, done, 0.99, 0.95, k=4)
+    save("learners", **rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks"]
+    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners"]
+    if "learners" in which:
+        gen_learners()
     if "dynamics" in which:
         gen_dynamics()
     if "sensors" in which:

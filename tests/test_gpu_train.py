@@ -1,0 +1,70 @@
+"""Short-horizon trainers (BPTT / SHAC / SHA2C) on the kernel env, and the
+critic's privileged features against the oracle."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("algo", ["bptt", "shac", "sha2c"])
+def test_trainer_updates(algo):
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.train import LearnerOptions, ShortHorizonTrainer
+
+    cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=512, episode_len=64)
+    env = qs.make_task(cfg, strict=False)
+    env.reset(seed=0)
+    tr = ShortHorizonTrainer(env, LearnerOptions(algo=algo, horizon=8, critic_iters=2, seed=1))
+    hist = [tr.update() for _ in range(12)]
+    for h in hist:
+        assert np.isfinite(h["loss"]) and h["grad_norm"] > 0
+        if algo != "bptt":
+            assert np.isfinite(h["critic_loss"])
+    env.check_errors()
+
+
+def test_bptt_training_reduces_loss():
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.train import LearnerOptions, ShortHorizonTrainer
+
+    cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=2048, episode_len=200)
+    env = qs.make_task(cfg, strict=False)
+    env.reset(seed=3)
+    tr = ShortHorizonTrainer(env, LearnerOptions(algo="bptt", horizon=16, explore=False, recurrent=False,
+                                                 actor_lr=3e-3, seed=2))
+    losses = [tr.update()["loss"] for _ in range(40)]
+    assert np.mean(losses[-8:]) < np.mean(losses[:8])
+
+
+def test_privileged_features_match_oracle():
+    import paper_2509_10247_b200 as qs
+    from oracle import quadsim_oracle as O
+
+    cfg = qs.TaskConfig(task="avoidance", dynamics="pm_continuous", n_envs=64, density=0.2)
+    env = qs.make_task(cfg)
+    env.reset(seed=4)
+    feats = env.privileged_state().cpu().numpy()
+    assert feats.shape == (64, 14)
+    # oracle: same formulas (q/tasks.py:525-545) on the env's state
+    p = env.state.p.detach().double().cpu().numpy()
+    goals = env.goals.double().cpu().numpy()
+    scenes = qs.world.device_scene_to_scenes(env._scene)
+    prims = O.pack_primitives([{"spheres": s.prims.spheres, "boxes": s.prims.boxes,
+                                "cylinders": s.prims.cylinders, "ground_z": s.prims.ground_z} for s in scenes])
+    R = O.reconstruct_attitude(env.state.a_lat.detach().double().cpu().numpy(), env.v_ema.double().cpu().numpy())
+    unrot = O.rotz(-O.yaw_of(R))
+    off = goals - p
+    np.testing.assert_allclose(feats[:, 0:3], O.matvec(unrot, off), atol=2e-5)
+    np.testing.assert_allclose(feats[:, 9], np.clip(O.sdf(p, prims), -5, 5), atol=2e-5)
+    np.testing.assert_allclose(feats[:, 13], np.linalg.norm(off, axis=-1), atol=2e-5)
+    # clearance direction: analytic gradient == the reference's central difference
+    h = 1e-4
+    fd = np.stack([(O.sdf(p + np.eye(3)[k] * h, prims) - O.sdf(p - np.eye(3)[k] * h, prims)) / (2 * h)
+                   for k in range(3)], -1)
+    np.testing.assert_allclose(feats[:, 10:13], O.matvec(unrot, fd), atol=1e-3)
+    # differentiable twin carries gradient into the state
+    env.state = env.model.init_state(env.state.p.detach().requires_grad_(True), env.state.v.detach())
+    v = env.privileged_var()
+    v[:, 9].sum().backward()

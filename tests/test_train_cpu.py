@@ -1,0 +1,68 @@
+"""Trainer host logic on CPU: TD-lambda against the reference's values and the
+multi-rank gradient all-reduce over gloo (world_size 2)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from golden_utils import load
+
+
+def test_td_lambda_matches_reference():
+    from paper_2509_10247_b200.train import td_lambda_targets
+
+    z = load("learners")
+    G = td_lambda_targets(torch.as_tensor(z["r"]), torch.as_tensor(z["values"]), torch.as_tensor(z["boot"]),
+                          torch.as_tensor(z["done"]), 0.99, 0.95)
+    np.testing.assert_allclose(G.numpy(), z["td"], rtol=1e-12, atol=1e-12)
+
+
+def test_shard_envs_partitions_global_ids():
+    from paper_2509_10247_b200.train import shard_envs
+
+    for n, w in ((1048576, 8), (100, 3), (5, 8)):
+        spans = [shard_envs(n, r, w) for r in range(w)]
+        ids = np.concatenate([np.arange(a, b) for a, b in spans])
+        assert np.array_equal(ids, np.arange(n))
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_10247_b200.train import allreduce_mean_
+
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(5, 7), torch.nn.Tanh(), torch.nn.Linear(7, 3))
+    x = torch.randn(16, 5, generator=torch.Generator().manual_seed(100 + rank))  # rank-local data
+    net(x).pow(2).mean().backward()
+    local = [p.grad.clone() for p in net.parameters()]
+    allreduce_mean_(list(net.parameters()))
+    q.put((rank, [g.numpy() for g in local], [p.grad.numpy() for p in net.parameters()]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gradient_allreduce_two_ranks_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict((r, (loc, red)) for r, loc, red in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    mean = [(a + b) / 2 for a, b in zip(res[0][0], res[1][0])]
+    for r in (0, 1):
+        for got, want in zip(res[r][1], mean):
+            np.testing.assert_allclose(got, want, rtol=1e-6, atol=1e-7)
+    # the two ranks had different local gradients and now agree exactly
+    assert not np.allclose(res[0][0][0], res[1][0][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        assert np.array_equal(a, b)
