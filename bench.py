@@ -180,12 +180,17 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; BENCH_DIST_BACKEND=gloo lets the multi-rank control
+    # flow be exercised with several ranks on fewer GPUs (no NCCL)
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
     if world > 1:
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -195,7 +200,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -220,7 +226,7 @@ def time_graph(fn, iters: int) -> float:
     return e0.elapsed_time(e1) / iters
 
 
-def bench_depth(dev, rank, frames=20):
+def bench_depth(dev, rank, world=1, frames=20):
     """C3: 16,384 envs, 64x48 depth, 32 solids (10 sph, 9 box, 13 cyl) + ground."""
     import torch
 
@@ -258,13 +264,14 @@ def bench_depth(dev, rank, frames=20):
         sn.TILED = True
         return out
 
-    ms = timed(True, cam, 0)
-    ms_untiled = timed(False, cam, 0)
+    ms = max_over_ranks(timed(True, cam, 0), world)
+    ms_untiled = max_over_ranks(timed(False, cam, 0), world)
     lidar = sn.LidarPattern(n_azimuth=360, n_elevation=16, max_range=20.0)
-    ms_lidar = timed(True, lidar, 1)
+    ms_lidar = max_over_ranks(timed(True, lidar, 1), world)
+    E *= world  # rays of all ranks in the max-over-ranks frame time
     cnt = sc.counts.double().cpu().numpy()
     # un-culled algorithmic flops per ray: 14 + 10 ns + 6 nb + 31 nc (+1 ground)
-    flops_frame = float(np.sum(14 + 10 * cnt[:, 0] + 6 * cnt[:, 1] + 31 * cnt[:, 2] + cnt[:, 3])) * R
+    flops_frame = float(np.sum(14 + 10 * cnt[:, 0] + 6 * cnt[:, 1] + 31 * cnt[:, 2] + cnt[:, 3])) * R * world
     return {"rays_per_s": E * R / (ms * 1e-3), "ms_per_frame": ms, "n_envs": E, "rays_per_env": R,
             "mean_solids": float(cnt[:, :3].sum(1).mean()),
             "tflops_uncull_equiv": flops_frame / (ms * 1e-3) / 1e12,
@@ -408,12 +415,11 @@ def run_ours(a):
 
     depth = None
     if not a.no_depth:
-        depth = bench_depth(dev, rank)
-        depth["rays_per_s"] = depth["rays_per_s"] * world if world > 1 else depth["rays_per_s"]
+        depth = bench_depth(dev, rank, world)
         fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
         depth["fp32_peak_tflops"] = round(fp32_peak, 1)
         depth["fp32_peak_source"] = "computed 148 SM x 128 FMA lanes x 2 x 1.965 GHz (not in MEASURED_PEAKS.json)"
-        depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / fp32_peak
+        depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / (fp32_peak * world)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
