@@ -1,0 +1,94 @@
+"""Opt-in depth VJP against fp64 central differences, in-kernel domain
+randomisation statistics, and the differentiable-depth env path."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def test_depth_vjp_matches_central_differences():
+    """d depth / d position: analytic -n/(n.d) vs the oracle's fp64 central
+    difference (h = 1e-6 (1+|x|), pkg/tests/oracles.py:15-30), away from
+    silhouettes (rays whose FD stencil changes the hit primitive are excluded)."""
+    import paper_2509_10247_b200 as qs
+    from oracle import quadsim_oracle as O
+
+    sn = qs.sensors
+    rng = np.random.default_rng(0)
+    E = 16
+    sets = []
+    for _ in range(E):
+        sph = np.column_stack([rng.uniform(2, 7, 3), rng.uniform(-3, 3, 3), rng.uniform(0.5, 2.5, 3),
+                               rng.uniform(0.4, 1.0, 3)])
+        box = np.column_stack([rng.uniform(2, 7, 2), rng.uniform(-3, 3, 2), rng.uniform(0.5, 2.5, 2),
+                               rng.uniform(0.3, 0.8, (2, 3))])
+        cyl = np.column_stack([rng.uniform(2, 7, 2), rng.uniform(-3, 3, 2), rng.uniform(0.8, 1.5, 2),
+                               rng.uniform(0.2, 0.5, 2), rng.uniform(0.8, 1.5, 2)])
+        sets.append(sn.PrimitiveSet(spheres=sph, boxes=box, cylinders=cyl, ground_z=0.0))
+    bp = sn.pack_primitives(sets)
+    sc = sn.DeviceScene.from_batched(bp, "cuda")
+    pos = np.column_stack([np.zeros(E), rng.uniform(-0.5, 0.5, E), rng.uniform(1.0, 2.0, E)])
+    cam = sn.CameraIntrinsics(width=16, height=12, max_range=10.0)
+    cs = torch.tensor([[1.0, 0.0]] * E, device="cuda")
+    p4 = torch.zeros(E, 4, device="cuda")
+    p4[:, :3] = torch.as_tensor(pos)
+    depth, _, dT = sn.cast_rays(sc, p4, 4, cs, cam, 0, True, want_grad=True)
+    dT = dT[..., :3].cpu().numpy()
+    prims = O.pack_primitives([{"spheres": s.spheres, "boxes": s.boxes, "cylinders": s.cylinders,
+                                "ground_z": 0.0} for s in sets])
+    dirs = np.broadcast_to(cam.pixel_dirs(), (E, cam.n_rays, 3))
+    base = O.raycast(prims, pos, dirs, 10.0)
+    ok_total, bad = 0, 0
+    for k in range(3):
+        h = 1e-6 * (1 + np.abs(pos[:, k]))
+        pp, pm = pos.copy(), pos.copy()
+        pp[:, k] += h
+        pm[:, k] -= h
+        fp = O.raycast(prims, pp, dirs, 10.0)
+        fm = O.raycast(prims, pm, dirs, 10.0)
+        fd = (fp - fm) / (2 * h[:, None])
+        smooth = (np.abs(fp - base) < 1e-3) & (np.abs(fm - base) < 1e-3) & (base < 10.0)
+        err = np.abs(dT[..., k] - fd)[smooth]
+        ok_total += smooth.sum()
+        bad += int((err > 1e-3 * (1 + np.abs(fd[smooth]))).sum())
+    assert ok_total > 1000
+    assert bad / ok_total < 2e-3, (bad, ok_total)
+
+
+def test_differentiable_depth_env_backprop():
+    import paper_2509_10247_b200 as qs
+
+    cfg = qs.TaskConfig(task="avoidance", dynamics="pm_continuous", n_envs=64, sensor="depth", depth_width=16,
+                        depth_height=12, density=0.3, differentiable_depth=True)
+    env = qs.make_task(cfg)
+    env.reset(seed=1)
+    a = torch.zeros(64, 3, device="cuda", requires_grad=True)
+    env.step(a)  # explicit Euler: p_{t+1} = p_t + v_t dt, so a_t reaches depth at t+2
+    out = env.step(torch.zeros(64, 3, device="cuda"))
+    assert out.obs.visual.requires_grad
+    (g,) = torch.autograd.grad(out.obs.visual.sum(), a)
+    assert torch.isfinite(g).all() and g.abs().sum() > 0
+
+
+def test_in_kernel_domain_randomisation_statistics():
+    import paper_2509_10247_b200 as qs
+
+    spec = qs.world.RandomizationSpec(drag_coeff=(0.1, 0.5), latency=(2.0, 8.0), action_scale=(0.5, 1.0))
+    cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=20000, episode_len=2,
+                        randomization=spec)
+    env = qs.make_task(cfg)
+    env.reset(seed=7)
+    dr = env._dr.double().cpu().numpy()
+    for col, (lo, hi) in ((0, spec.drag_coeff), (3, spec.latency), (2, spec.action_scale)):
+        x = dr[:, col]
+        assert x.min() >= lo - 1e-6 and x.max() <= hi + 1e-6
+        assert abs(x.mean() - (lo + hi) / 2) < 0.01 * (hi - lo) + 1e-6
+        assert abs(x.std() - (hi - lo) / np.sqrt(12)) < 0.02 * (hi - lo)
+    np.testing.assert_allclose(dr[:, 1], np.exp(-dr[:, 3] * cfg.dt), rtol=1e-5)
+    before = dr.copy()
+    for _ in range(2):  # episode_len 2: every env resets and redraws (per_episode)
+        env.step(torch.zeros(env.N, 3, device="cuda"))
+    after = env._dr.double().cpu().numpy()
+    assert (np.abs(after - before).max(axis=1) > 0).mean() > 0.99
