@@ -41,6 +41,7 @@ extern "C" {
 #define QS_MODEL_FULL 0
 #define QS_MODEL_PM_CONTINUOUS 1
 #define QS_MODEL_PM_DISCRETE 2
+#define QS_MODEL_SIMPLIFIED 3
 
 /* tasks (q/tasks.py:30) */
 #define QS_TASK_POSITION 0

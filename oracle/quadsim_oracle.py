@@ -58,9 +58,10 @@ class Params:
         return np.exp(-np.asarray(self.latency, dtype=np.float64) * self.dt)
 
 
-MODEL_ACTION_DIM = {"full": 4, "pm_continuous": 3, "pm_discrete": 3}
+MODEL_ACTION_DIM = {"full": 4, "simplified": 4, "pm_continuous": 3, "pm_discrete": 3}
 STATE_FIELDS = {
     "full": ("p", "v", "q", "w"),
+    "simplified": ("p", "v", "R"),
     "pm_continuous": ("p", "v", "a_lat"),
     "pm_discrete": ("p", "v", "u_prev"),
 }
@@ -69,7 +70,7 @@ STATE_FIELDS = {
 def action_box(model: str, g_vec=GRAVITY):
     """q/dynamics.py:342-346 (full), :398-402 (pm_cont), :424-425 (pm_disc)."""
     gz = -g_vec[2]
-    if model == "full":
+    if model in ("full", "simplified"):  # :342-346, :373-376
         return np.array([0.0, -6.0, -6.0, -3.0]), np.array([2.0 * gz, 6.0, 6.0, 3.0])
     if model == "pm_continuous":
         return np.array([-6.0, -6.0, gz - 6.0]), np.array([6.0, 6.0, gz + 6.0])
@@ -87,6 +88,8 @@ def init_state(model: str, p, v, g_vec=GRAVITY):
         q[:, 0] = 1.0
         st["q"] = q
         st["w"] = np.zeros((B, 3))
+    elif model == "simplified":  # q/dynamics.py:356-360
+        st["R"] = np.broadcast_to(np.eye(3), (B, 3, 3)).copy()
     elif model == "pm_continuous":
         st["a_lat"] = np.broadcast_to(-g_vec, (B, 3)).copy()
     else:
@@ -192,9 +195,30 @@ def step_full(st, act, prm: Params):
     return {"p": p + v * dt, "v": v + v_dot * dt, "q": qn, "w": w + w_dot * dt}
 
 
+def step_simplified(st, act, prm: Params):
+    """q/dynamics.py:189-234 (Gram-Schmidt columns :189-198)."""
+    p, v, R = st["p"], st["v"], st["R"]
+    c = act[:, 0:1]
+    wx, wy, wz = act[:, 1], act[:, 2], act[:, 3]
+    zero = np.zeros_like(wx)
+    skew = np.stack([np.stack([zero, -wz, wy], -1), np.stack([wz, zero, -wx], -1),
+                     np.stack([-wy, wx, zero], -1)], -2)
+    R_dot = R @ skew
+    M = R + R_dot * prm.dt
+    x, y = M[..., 0], M[..., 1]
+    xn = x / np.linalg.norm(x, axis=-1, keepdims=True)
+    y_orth = y - xn * np.sum(y * xn, -1, keepdims=True)
+    yn = y_orth / np.linalg.norm(y_orth, axis=-1, keepdims=True)
+    zn = np.cross(xn, yn)
+    v_dot = R[..., 2] * c + prm.g_vec
+    return {"p": p + v * prm.dt, "v": v + v_dot * prm.dt, "R": np.stack([xn, yn, zn], -1)}
+
+
 def model_step(model: str, st, act, prm: Params):
     if model == "full":
         return step_full(st, act, prm)
+    if model == "simplified":
+        return step_simplified(st, act, prm)
     if model == "pm_continuous":
         return step_pm_continuous(st, act, prm)
     return step_pm_discrete(st, act, prm)
@@ -267,6 +291,8 @@ def attitude(model: str, st, v_ema, g_vec=GRAVITY):
     """q/tasks.py:400-410."""
     if model == "full":
         return quat_to_matrix(st["q"])
+    if model == "simplified":
+        return st["R"]
     return reconstruct_attitude(thrust_accel(model, st, g_vec), v_ema)
 
 
@@ -1045,7 +1071,8 @@ class OracleTask:
         self.episode_counter += 1
         fresh = init_state(self.model, p_new, v_new)
         for k in self.state:
-            self.state[k] = np.where(rows_mask[:, None], fresh[k], self.state[k])
+            m = rows_mask.reshape((-1,) + (1,) * (fresh[k].ndim - 1))
+            self.state[k] = np.where(m, fresh[k], self.state[k])
         self.prev_effort[rows_mask] = 0.0
 
     def _sample_pair(self, rng):
@@ -1077,6 +1104,8 @@ class OracleTask:
             parts.append(matvec(unrot, st["a_lat"]))
         elif self.model == "pm_discrete":
             parts.append(matvec(unrot, st["u_prev"]))
+        elif self.model == "simplified":
+            parts.append(matvec(unrot, st["R"][..., 2]))
         else:
             parts.append(matvec(unrot, quat_rotate(st["q"], np.array([0.0, 0.0, 1.0]))))
             parts.append(st["w"])
@@ -1144,6 +1173,8 @@ class OracleTask:
         if self.imu_cfg is not None:
             if self.model == "full":
                 Rb, wb = quat_to_matrix(st2["q"]), st2["w"]
+            elif self.model == "simplified":
+                Rb, wb = st2["R"], None
             else:
                 Rb = reconstruct_attitude(thrust_accel(self.model, st2), self.v_ema)
                 wb = None

@@ -21,7 +21,7 @@ QS_ERR_GENERATION = 3
 QS_ERR_BAD_ARGUMENT = 4
 QS_ERR_LAUNCH = 5
 
-MODEL_IDS = {"full": 0, "pm_continuous": 1, "pm_discrete": 2}
+MODEL_IDS = {"full": 0, "pm_continuous": 1, "pm_discrete": 2, "simplified": 3}
 TASK_IDS = {"position": 0, "avoidance": 1, "racing": 2}
 MAX_AGENTS = 8
 MAX_GATES = 16

@@ -9,12 +9,23 @@
 //   full: P0 = (p, vema.x)  P1 = (v, vema.y)  P2 = q (w,x,y,z)  P3 = (w, vema.z)
 // so every row is 3 or 4 coalesced 16-byte loads and v_ema (non-differentiable,
 // q/tasks.py:566) rides in the pad lanes for free.
+//   simplified (NP = 5): P0 = (p, vema.x)  P1 = (v, vema.y)  P2 = (R col0, vema.z)
+//                        P3 = (R col1, _)  P4 = (R col2, _)
 struct State {
   V3 p, v, x;  // x: a_lat (pm_continuous) / u_prev (pm_discrete)
   Q4 q;        // full
   V3 w;        // full: body rates
   V3 ve;       // velocity EMA (not differentiated)
+  V3 r0, r1, r2;  // simplified: rotation-matrix columns (body x, y, z in world)
 };
+
+QS_D State zero_state() {
+  State z;
+  z.p = z.v = z.x = z.w = z.ve = z.r0 = z.r1 = z.r2 = v3(0.f, 0.f, 0.f);
+  z.q = q4(0.f, 0.f, 0.f, 0.f);
+  return z;
+}
+QS_D State zero_state_like() { return zero_state(); }
 
 template <int M>
 struct ModelTraits;
@@ -30,6 +41,10 @@ template <>
 struct ModelTraits<QS_MODEL_PM_DISCRETE> {
   static constexpr int NP = 3, A = 3, P = 9;
 };
+template <>
+struct ModelTraits<QS_MODEL_SIMPLIFIED> {
+  static constexpr int NP = 5, A = 4, P = 9;
+};
 
 template <int M>
 QS_D State load_state(const float* S, long N, long row) {
@@ -37,7 +52,16 @@ QS_D State load_state(const float* S, long N, long row) {
   float4 a = ld4(S, row), b = ld4(S, N + row), c = ld4(S, 2 * N + row);
   s.p = xyz(a);
   s.v = xyz(b);
-  if (M == QS_MODEL_FULL) {
+  s.r0 = s.r1 = s.r2 = v3(0.f, 0.f, 0.f);
+  if (M == QS_MODEL_SIMPLIFIED) {
+    s.r0 = xyz(c);
+    s.r1 = xyz(ld4(S, 3 * N + row));
+    s.r2 = xyz(ld4(S, 4 * N + row));
+    s.ve = v3(a.w, b.w, c.w);
+    s.x = v3(0.f, 0.f, 0.f);
+    s.q = q4(1.f, 0.f, 0.f, 0.f);
+    s.w = v3(0.f, 0.f, 0.f);
+  } else if (M == QS_MODEL_FULL) {
     float4 d = ld4(S, 3 * N + row);
     s.q = q4(c.x, c.y, c.z, c.w);
     s.w = xyz(d);
@@ -56,7 +80,11 @@ template <int M>
 QS_D void store_state(float* S, long N, long row, const State& s) {
   st4(S, row, f4(s.p, s.ve.x));
   st4(S, N + row, f4(s.v, s.ve.y));
-  if (M == QS_MODEL_FULL) {
+  if (M == QS_MODEL_SIMPLIFIED) {
+    st4(S, 2 * N + row, f4(s.r0, s.ve.z));
+    st4(S, 3 * N + row, f4(s.r1, 0.f));
+    st4(S, 4 * N + row, f4(s.r2, 0.f));
+  } else if (M == QS_MODEL_FULL) {
     st4(S, 2 * N + row, make_float4(s.q.w, s.q.x, s.q.y, s.q.z));
     st4(S, 3 * N + row, f4(s.w, s.ve.z));
   } else {
@@ -67,7 +95,9 @@ QS_D void store_state(float* S, long N, long row, const State& s) {
 template <int M>
 QS_D bool state_finite(const State& s) {
   bool ok = finite3(s.p) && finite3(s.v);
-  if (M == QS_MODEL_FULL)
+  if (M == QS_MODEL_SIMPLIFIED)
+    ok = ok && finite3(s.r0) && finite3(s.r1) && finite3(s.r2);
+  else if (M == QS_MODEL_FULL)
     ok = ok && isfinite(s.q.w) && isfinite(s.q.x) && isfinite(s.q.y) && isfinite(s.q.z) &&
          finite3(s.w);
   else
@@ -85,6 +115,9 @@ QS_D State init_state(V3 p, V3 v, V3 ve, V3 g) {
   s.q = q4(1.f, 0.f, 0.f, 0.f);
   s.w = v3(0.f, 0.f, 0.f);
   s.x = (M == QS_MODEL_PM_CONTINUOUS) ? -g : v3(0.f, 0.f, 0.f);
+  s.r0 = v3(1.f, 0.f, 0.f);  // q/dynamics.py:356-360 (R = I)
+  s.r1 = v3(0.f, 1.f, 0.f);
+  s.r2 = v3(0.f, 0.f, 1.f);
   return s;
 }
 
@@ -176,6 +209,7 @@ QS_D V3 thrust_of(const State& s, V3 g) {  // q/dynamics.py:406, 430
 
 template <int M>
 QS_D float2 yaw_cs(const State& s, V3 g) {  // q/tasks.py:400-413
+  if (M == QS_MODEL_SIMPLIFIED) return yaw_cs_from(s.r0.x, s.r0.y);  // R00, R10
   if (M == QS_MODEL_FULL) {
     const Q4 q = s.q;  // R00, R10 of q/dynamics.py:448-460
     return yaw_cs_from(1.f - 2.f * (q.y * q.y + q.z * q.z), 2.f * (q.x * q.y + q.w * q.z));
@@ -332,8 +366,73 @@ QS_D void step_pmd_vjp(const State& gs, const DynK& k, State& gi, V3& gu) {
   gi.w = gi.ve = v3(0.f, 0.f, 0.f);
 }
 
+// step_simplified (q/dynamics.py:189-234): v' = v + (R e_z c + g) dt,
+// R' = GramSchmidt(R + R [w]x dt) on columns 0,1 (z = x cross y), body rates
+// are the command (cmd = (c, wx, wy, wz)).
+struct GsFwd {
+  V3 m0, m1, xn, yn, yo;
+  float n0, n1, s;
+};
+QS_D GsFwd simplified_gs(const State& s, float4 cmd, float dt) {
+  GsFwd f;
+  const float wx = cmd.y, wy = cmd.z, wz = cmd.w;
+  f.m0 = s.r0 + (s.r1 * wz - s.r2 * wy) * dt;  // column 0 of R + R S dt
+  f.m1 = s.r1 + (s.r2 * wx - s.r0 * wz) * dt;  // column 1
+  f.n0 = norm3(f.m0);
+  f.xn = f.m0 * (1.f / f.n0);
+  f.s = dot(f.m1, f.xn);
+  f.yo = f.m1 - f.xn * f.s;
+  f.n1 = norm3(f.yo);
+  f.yn = f.yo * (1.f / f.n1);
+  return f;
+}
+
+QS_D State step_simplified(const State& s, float4 cmd, const DynK& k) {
+  const float dt = k.dt;
+  GsFwd f = simplified_gs(s, cmd, dt);
+  State o = s;
+  V3 vdot = s.r2 * cmd.x + k.g;
+  o.p = s.p + s.v * dt;
+  o.v = s.v + vdot * dt;
+  o.r0 = f.xn;
+  o.r1 = f.yn;
+  o.r2 = cross(f.xn, f.yn);
+  return o;
+}
+
+QS_D void step_simplified_vjp(const State& s, float4 cmd, const DynK& k, const State& gs, State& gi,
+                              float4& gc) {
+  const float dt = k.dt;
+  GsFwd f = simplified_gs(s, cmd, dt);
+  gi = zero_state_like();
+  gi.p = gs.p;
+  gi.v = gs.v + gs.p * dt;
+  V3 gvdot = gs.v * dt;
+  float g_c = dot(gvdot, s.r2);
+  V3 g_r2 = gvdot * cmd.x;
+  // z' = xn x yn
+  V3 g_xn = gs.r0 + cross(f.yn, gs.r2);
+  V3 g_yn = gs.r1 + cross(gs.r2, f.xn);
+  // yn = yo / |yo|
+  V3 g_yo = (g_yn - f.yn * dot(f.yn, g_yn)) * (1.f / f.n1);
+  // yo = m1 - xn (m1 . xn)
+  V3 g_m1 = g_yo;
+  g_xn -= g_yo * f.s;
+  float g_s = -dot(f.xn, g_yo);
+  g_m1 += f.xn * g_s;
+  g_xn += f.m1 * g_s;
+  // xn = m0 / |m0|
+  V3 g_m0 = (g_xn - f.xn * dot(f.xn, g_xn)) * (1.f / f.n0);
+  const float wx = cmd.y, wy = cmd.z, wz = cmd.w;
+  gi.r0 = g_m0 - g_m1 * (dt * wz);
+  gi.r1 = g_m1 + g_m0 * (dt * wz);
+  gi.r2 = g_r2 + (g_m1 * wx - g_m0 * wy) * dt;
+  gc = make_float4(g_c, dt * dot(s.r2, g_m1), -dt * dot(s.r2, g_m0), dt * (dot(s.r1, g_m0) - dot(s.r0, g_m1)));
+}
+
 template <int M>
 QS_D State model_step(const State& s, float4 cmd, const RowPrm& rp, const DynK& k) {
+  if (M == QS_MODEL_SIMPLIFIED) return step_simplified(s, cmd, k);
   if (M == QS_MODEL_FULL) return step_full(s, cmd, k);
   V3 u = v3(cmd.x, cmd.y, cmd.z);
   if (M == QS_MODEL_PM_CONTINUOUS) return step_pmc(s, u, rp.drag, rp.decay, k);
@@ -343,7 +442,9 @@ QS_D State model_step(const State& s, float4 cmd, const RowPrm& rp, const DynK& 
 template <int M>
 QS_D void model_step_vjp(const State& s, float4 cmd, const RowPrm& rp, const DynK& k,
                          const State& gs, State& gi, float4& gc) {
-  if (M == QS_MODEL_FULL) {
+  if (M == QS_MODEL_SIMPLIFIED) {
+    step_simplified_vjp(s, cmd, k, gs, gi, gc);
+  } else if (M == QS_MODEL_FULL) {
     step_full_vjp(s, cmd, k, gs, gi, gc);
   } else {
     V3 gu;
@@ -355,12 +456,6 @@ QS_D void model_step_vjp(const State& s, float4 cmd, const RowPrm& rp, const Dyn
   }
 }
 
-QS_D State zero_state() {
-  State z;
-  z.p = z.v = z.x = z.w = z.ve = v3(0.f, 0.f, 0.f);
-  z.q = q4(0.f, 0.f, 0.f, 0.f);
-  return z;
-}
 
 template <int M>
 QS_D State load_grad(const float* G, long N, long row) {

@@ -139,6 +139,8 @@ int qs_dyn_step_fwd(int32_t model, int32_t n, const float* S_in, const float* ac
     k_dyn_fwd<QS_MODEL_PM_CONTINUOUS><<<g, 128, 0, s>>>(n, S_in, act, dr, *cfg, S_out, err);
   else if (model == QS_MODEL_PM_DISCRETE)
     k_dyn_fwd<QS_MODEL_PM_DISCRETE><<<g, 128, 0, s>>>(n, S_in, act, dr, *cfg, S_out, err);
+  else if (model == QS_MODEL_SIMPLIFIED)
+    k_dyn_fwd<QS_MODEL_SIMPLIFIED><<<g, 128, 0, s>>>(n, S_in, act, dr, *cfg, S_out, err);
   else return QS_ERR_BAD_ARGUMENT;
   return status();
 }
@@ -155,6 +157,8 @@ int qs_dyn_step_bwd(int32_t model, int32_t n, const float* S_in, const float* ac
     k_dyn_bwd<QS_MODEL_PM_CONTINUOUS><<<g, 128, 0, s>>>(n, S_in, act, dr, *cfg, g_S_out, g_S_in, g_act);
   else if (model == QS_MODEL_PM_DISCRETE)
     k_dyn_bwd<QS_MODEL_PM_DISCRETE><<<g, 128, 0, s>>>(n, S_in, act, dr, *cfg, g_S_out, g_S_in, g_act);
+  else if (model == QS_MODEL_SIMPLIFIED)
+    k_dyn_bwd<QS_MODEL_SIMPLIFIED><<<g, 128, 0, s>>>(n, S_in, act, dr, *cfg, g_S_out, g_S_in, g_act);
   else return QS_ERR_BAD_ARGUMENT;
   return status();
 }

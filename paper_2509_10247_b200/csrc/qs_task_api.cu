@@ -43,7 +43,9 @@ int qs_proprio_dim(int32_t model, int32_t task) {
   return base + (task == QS_TASK_RACING ? 9 : 0);
 }
 
-int qs_state_planes(int32_t model) { return model == QS_MODEL_FULL ? 4 : 3; }
+int qs_state_planes(int32_t model) {
+  return model == QS_MODEL_FULL ? 4 : (model == QS_MODEL_SIMPLIFIED ? 5 : 3);
+}
 
 int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
                      void* stream) {

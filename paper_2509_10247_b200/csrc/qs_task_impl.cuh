@@ -63,7 +63,13 @@ QS_D int observe_row(const qs_task_cfg& cfg, const State& s, float2 cs, V3 goal,
   o[4] = vl.y;
   o[5] = vl.z;
   int k = 6;
-  if (M == QS_MODEL_FULL) {
+  if (M == QS_MODEL_SIMPLIFIED) {  // body z axis = third column of R (q/tasks.py:431-432)
+    V3 zl = unrotz(cs, s.r2);
+    o[6] = zl.x;
+    o[7] = zl.y;
+    o[8] = zl.z;
+    k = 9;
+  } else if (M == QS_MODEL_FULL) {
     V3 zl = unrotz(cs, qrot(s.q, v3(0.f, 0.f, 1.f)));
     o[6] = zl.x;
     o[7] = zl.y;
@@ -240,6 +246,10 @@ QS_D void imu_apply(const qs_task_cfg& cfg, long row, long N, int tick, const St
     yb = v3(2.f * (xy - wz), 1.f - 2.f * (xx + zz), 2.f * (yz + wx));
     zb = v3(2.f * (xz + wy), 2.f * (yz - wx), 1.f - 2.f * (xx + yy));
     w = s2.w;
+  } else if (M == QS_MODEL_SIMPLIFIED) {  // no rate state: gyro reads bias + noise
+    xb = s2.r0;
+    yb = s2.r1;
+    zb = s2.r2;
   } else {
     attitude_pm(thrust_of<M>(s2, g), s2.ve, xb, yb, zb);
   }
@@ -373,7 +383,7 @@ QS_D Squash squash(float4 raw, const RowPrm& rp) {  // q/dynamics.py:277-284
 
 template <int M>
 QS_D float4 world_cmd(const State& s, float4 sq, V3 g, float2& cs) {  // q/tasks.py:613-618
-  if (M == QS_MODEL_FULL) {
+  if (M == QS_MODEL_FULL || M == QS_MODEL_SIMPLIFIED) {  // only point-mass commands are yaw-local
     cs = make_float2(1.f, 0.f);
     return sq;
   }
@@ -758,7 +768,9 @@ QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int n
       gg = v3((cb & 1) ? gg.x : 0.f, (cb & 2) ? gg.y : 0.f, (cb & 4) ? gg.z : 0.f);
       g.p -= rotz(cs2, gg);  // unrot^T = rot
       g.v += rotz(cs2, v3(go[3], go[4], go[5]));
-      if (M == QS_MODEL_FULL) {
+      if (M == QS_MODEL_SIMPLIFIED) {
+        g.r2 += rotz(cs2, v3(go[6], go[7], go[8]));
+      } else if (M == QS_MODEL_FULL) {
         V3 gz = rotz(cs2, v3(go[6], go[7], go[8]));
         Q4 gq = qrot_vjp_q(n.q, v3(0.f, 0.f, 1.f), gz);
         g.q = q4(g.q.w + gq.w, g.q.x + gq.x, g.q.y + gq.y, g.q.z + gq.z);
@@ -824,7 +836,7 @@ QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int n
     float4 gc;
     model_step_vjp<M>(s_in[a], cmd[a], rp, k, g2[a], gi, gc);
     float4 gsq;
-    if (M == QS_MODEL_FULL) {
+    if (M == QS_MODEL_FULL || M == QS_MODEL_SIMPLIFIED) {
       gsq = gc;
     } else {
       V3 u = unrotz(csc[a], v3(gc.x, gc.y, gc.z));  // Rz^T g
@@ -1253,6 +1265,8 @@ int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, c
         return task_op<T, QS_MODEL_PM_CONTINUOUS, NA>(op, cfg, sc, p, mask, tab, s);           \
       case QS_MODEL_PM_DISCRETE:                                                               \
         return task_op<T, QS_MODEL_PM_DISCRETE, NA>(op, cfg, sc, p, mask, tab, s);             \
+      case QS_MODEL_SIMPLIFIED:                                                                \
+        return task_op<T, QS_MODEL_SIMPLIFIED, NA>(op, cfg, sc, p, mask, tab, s);              \
     }                                                                                          \
     return QS_ERR_BAD_ARGUMENT;                                                                \
   }

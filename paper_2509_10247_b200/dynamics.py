@@ -69,6 +69,7 @@ class QuadParams:
 
 FIELDS = {
     "full": ("p", "v", "q", "w"),
+    "simplified": ("p", "v", "R"),
     "pm_continuous": ("p", "v", "a_lat"),
     "pm_discrete": ("p", "v", "u_prev"),
 }
@@ -108,6 +109,8 @@ class QuadState:
 def model_of_state(st: QuadState) -> str:
     if st.q is not None:
         return "full"
+    if st.R is not None:
+        return "simplified"
     if st.a_lat is not None:
         return "pm_continuous"
     return "pm_discrete"
@@ -123,6 +126,11 @@ def pack_state(model: str, st: QuadState, v_ema: torch.Tensor | None = None) -> 
     planes = [torch.cat([f(st.p), ve[:, 0:1]], -1), torch.cat([f(st.v), ve[:, 1:2]], -1)]
     if model == "full":
         planes += [f(st.q), torch.cat([f(st.w), ve[:, 2:3]], -1)]
+    elif model == "simplified":
+        R = f(st.R)
+        z = torch.zeros(B, 1, dtype=torch.float32, device=dev)
+        planes += [torch.cat([R[:, :, 0], ve[:, 2:3]], -1), torch.cat([R[:, :, 1], z], -1),
+                   torch.cat([R[:, :, 2], z], -1)]
     else:
         x = st.a_lat if model == "pm_continuous" else st.u_prev
         planes.append(torch.cat([f(x), ve[:, 2:3]], -1))
@@ -133,14 +141,22 @@ def unpack_state(model: str, S: torch.Tensor) -> QuadState:
     """(NP,B,4) planes -> QuadState of views (autograd flows through them)."""
     if model == "full":
         return QuadState(p=S[0, :, 0:3], v=S[1, :, 0:3], q=S[2], w=S[3, :, 0:3])
+    if model == "simplified":
+        return QuadState(p=S[0, :, 0:3], v=S[1, :, 0:3], R=torch.stack([S[2, :, 0:3], S[3, :, 0:3], S[4, :, 0:3]], -1))
     x = S[2, :, 0:3]
     if model == "pm_continuous":
         return QuadState(p=S[0, :, 0:3], v=S[1, :, 0:3], a_lat=x)
     return QuadState(p=S[0, :, 0:3], v=S[1, :, 0:3], u_prev=x)
 
 
+def vema_plane(S: torch.Tensor) -> int:
+    """Plane whose pad lane holds v_ema.z: the last plane, except for the
+    simplified model whose R columns 1 and 2 have no spare lane meaning."""
+    return 2 if S.shape[0] == 5 else S.shape[0] - 1
+
+
 def v_ema_of(S: torch.Tensor) -> torch.Tensor:
-    return torch.stack([S[0, :, 3], S[1, :, 3], S[-1, :, 3]], -1)
+    return torch.stack([S[0, :, 3], S[1, :, 3], S[vema_plane(S), :, 3]], -1)
 
 
 def fill_dyn_cfg(cfg: L.QsTaskCfg, model: str, params: QuadParams, action_box=None):
@@ -276,6 +292,30 @@ class FullQuadrotor(DynamicsModel):
         return quat_to_matrix(state.q)
 
 
+class SimplifiedQuadrotor(DynamicsModel):
+    """q/dynamics.py:352-379: v' = v + (R e_z c + g) dt, R' = GS(R + R[w]x dt)."""
+
+    name = "simplified"
+    action_dim = 4
+
+    def init_state(self, p, v):
+        p, v = self._t(p), self._t(v)
+        R = torch.eye(3, dtype=torch.float32, device=self.device).expand(p.shape[0], 3, 3).contiguous()
+        return QuadState(p=p, v=v, R=R)
+
+    def hover_action(self, batch):
+        a = torch.zeros(batch, 4, dtype=torch.float32, device=self.device)
+        a[:, 0] = float(-self.params.g_vec[2])
+        return a
+
+    def action_box(self):
+        gz = -self.params.g_vec[2]
+        return np.array([0.0, -6.0, -6.0, -3.0]), np.array([2.0 * gz, 6.0, 6.0, 3.0])
+
+    def attitude(self, state):
+        return state.R
+
+
 class PointMassContinuous(DynamicsModel):
     name = "pm_continuous"
     action_dim = 3
@@ -314,11 +354,11 @@ class PointMassDiscrete(DynamicsModel):
         return state.u_prev - self._t(self.params.g_vec)
 
 
-_MODELS = {c.name: c for c in (FullQuadrotor, PointMassContinuous, PointMassDiscrete)}
+_MODELS = {c.name: c for c in (FullQuadrotor, SimplifiedQuadrotor, PointMassContinuous, PointMassDiscrete)}
 
 
 def make_model(name: str, params: QuadParams | None = None, device=None) -> DynamicsModel:
-    """q/dynamics.py:437-441.  ('simplified' is a SURVEY §8(f1) next item.)"""
+    """q/dynamics.py:437-441."""
     try:
         cls = _MODELS[name]
     except KeyError:

@@ -316,6 +316,8 @@ class FlightTask:
             out = [{"name": "latent_accel", "size": 3, "frame": "yaw-local", "units": "m/s^2"}]
         elif name == "pm_discrete":
             out = [{"name": "prev_accel_cmd", "size": 3, "frame": "yaw-local", "units": "m/s^2"}]
+        elif name == "simplified":
+            out = [{"name": "body_z_axis", "size": 3, "frame": "yaw-local", "units": "1"}]
         else:
             out = [{"name": "body_z_axis", "size": 3, "frame": "yaw-local", "units": "1"},
                    {"name": "body_rates", "size": 3, "frame": "body", "units": "rad/s"}]
@@ -488,7 +490,7 @@ class FlightTask:
         self._alloc_persistent()
         self._cfg = self._build_cfg()
         dev, N = self.device, self.N
-        NP = 4 if self.config.dynamics == "full" else 3
+        NP = L.lib().qs_state_planes(L.MODEL_IDS[self.config.dynamics])
         f = dict(device=dev, dtype=torch.float32)
         S = torch.zeros(NP, N, 4, **f)
         goal = torch.zeros(N, 4, **f)
@@ -585,7 +587,7 @@ class FlightTask:
         ve = torch.as_tensor(np.asarray(ve) if not isinstance(ve, torch.Tensor) else ve,
                              dtype=torch.float32, device=self.device)
         S = self._S.clone()
-        S[0, :, 3], S[1, :, 3], S[-1, :, 3] = ve[:, 0], ve[:, 1], ve[:, 2]
+        S[0, :, 3], S[1, :, 3], S[dyn.vema_plane(S), :, 3] = ve[:, 0], ve[:, 1], ve[:, 2]
         self._S = S
 
     @property
@@ -789,6 +791,8 @@ class FlightTask:
             return st.a_lat
         if name == "pm_discrete":
             return st.u_prev - g
+        if name == "simplified":
+            return st.R[:, :, 2] * 9.81
         w, x, y, z = st.q.unbind(-1)
         zb = torch.stack([2 * (x * z + w * y), 2 * (y * z - w * x), 1 - 2 * (x * x + y * y)], -1)
         return zb * 9.81
@@ -854,6 +858,8 @@ class _ObserveFn(torch.autograd.Function):
                 w, x, y, z = st.q.unbind(-1)
                 zb = torch.stack([2 * (x * z + w * y), 2 * (y * z - w * x), 1 - 2 * (x * x + y * y)], -1)
                 parts += [unrot(zb), st.w]
+            elif model == "simplified":
+                parts.append(unrot(st.R[:, :, 2]))
             else:
                 parts.append(unrot(st.a_lat if model == "pm_continuous" else st.u_prev))
             lin = torch.cat(parts, -1)

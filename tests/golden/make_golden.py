@@ -44,9 +44,9 @@ def gen_dynamics():
     out = {}
     rng = np.random.default_rng(100)
     B, T = 16, 8
-    for name in ("full", "pm_continuous", "pm_discrete"):
+    for name in ("full", "pm_continuous", "pm_discrete", "simplified"):
         for variant in ("default", "drag"):
-            if variant == "drag" and name == "pm_discrete":
+            if variant == "drag" and name in ("pm_discrete", "simplified"):
                 continue
             kw = {}
             if variant == "drag":
@@ -64,6 +64,10 @@ def gen_dynamics():
                 st = dyn.QuadState(p=st.p, v=st.v, q=Var(q), w=Var(rng.normal(size=(B, 3))))
             elif name == "pm_continuous":
                 st = dyn.QuadState(p=st.p, v=st.v, a_lat=Var(rng.normal(size=(B, 3)) * 3))
+            elif name == "simplified":
+                q = rng.normal(size=(B, 4))
+                q /= np.linalg.norm(q, axis=-1, keepdims=True)
+                st = dyn.QuadState(p=st.p, v=st.v, R=Var(dyn.quat_to_matrix_np(q)))
             else:
                 st = dyn.QuadState(p=st.p, v=st.v, u_prev=Var(rng.normal(size=(B, 3))))
             raw = rng.normal(size=(T, B, model.action_dim)) * 0.7
@@ -131,6 +135,9 @@ TASK_CASES = {
     "avoid_collide": dict(cfg=dict(task="avoidance", dynamics="pm_continuous", n_envs=6, episode_len=20,
                                    density=0.2),
                           T=10, scale=0.1, seed=11, teleport="obstacle"),
+    # simplified quadrotor, with resets and success/bounds events
+    "pos_simp": dict(cfg=dict(task="position", dynamics="simplified", n_envs=24, episode_len=7),
+                     T=16, scale=0.3, seed=12, teleport="goal_bounds"),
 }
 
 

@@ -55,10 +55,11 @@ TASK_CASES = {
     "pos_full_events": dict(cfg=dict(task="position", dynamics="full", n_envs=16, episode_len=20)),
     "avoid_collide": dict(cfg=dict(task="avoidance", dynamics="pm_continuous", n_envs=6, episode_len=20,
                                    density=0.2)),
+    "pos_simp": dict(cfg=dict(task="position", dynamics="simplified", n_envs=24, episode_len=7)),
 }
 
 STATE_KEYS = {"full": ("p", "v", "q", "w"), "pm_continuous": ("p", "v", "a_lat"),
-              "pm_discrete": ("p", "v", "u_prev")}
+              "pm_discrete": ("p", "v", "u_prev"), "simplified": ("p", "v", "R")}
 
 
 def oracle_config(name) -> O.Config:

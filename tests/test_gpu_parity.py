@@ -27,7 +27,7 @@ def qs():
 
 
 @pytest.mark.parametrize("key", ["full_default", "full_drag", "pm_continuous_default",
-                                 "pm_continuous_drag", "pm_discrete_default"])
+                                 "pm_continuous_drag", "pm_discrete_default", "simplified_default"])
 def test_dynamics_kernels_match_reference(qs, key):
     z = load("dynamics")
     model_name = key.rsplit("_", 1)[0]

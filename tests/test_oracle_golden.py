@@ -27,7 +27,7 @@ def close(a, b, tol=1e-10):
 
 
 @pytest.mark.parametrize("key", ["full_default", "full_drag", "pm_continuous_default",
-                                 "pm_continuous_drag", "pm_discrete_default"])
+                                 "pm_continuous_drag", "pm_discrete_default", "simplified_default"])
 def test_dynamics_rollout_matches_reference(key):
     z = load("dynamics")
     model = key.rsplit("_", 1)[0]
@@ -169,7 +169,7 @@ def test_task_trajectory_matches_reference(name):
 
 
 @pytest.mark.parametrize("name", ["pos_full", "pos_form", "avoid_form", "pos_pmc_dr", "avoid_collide",
-                                  "pos_events"])
+                                  "pos_events", "pos_simp"])
 def test_oracle_fd_gradient_matches_reference_tape(name):
     """Central-difference BPTT gradient of the oracle == the reference's tape gradient."""
     env, z = build_oracle_task(name)
