@@ -166,3 +166,57 @@ class BpttWindow:
     def sync_env(self):
         """Write the window's final state back into the env object."""
         self._store_env_state()
+
+    # -- host-fed streaming: the next window's action upload overlaps this
+    #    window's kernels (double-buffered device actions, one graph each)
+
+    def _ensure_pipeline(self):
+        if getattr(self, "_pipe", None) is not None:
+            return
+        dev = self.env.device
+        bufs = [self.actions, torch.zeros_like(self.actions)]
+        graphs = []
+        keep = self.actions
+        for b in bufs:
+            self.actions = b
+            self.graph = None
+            self.capture()
+            graphs.append(self.graph)
+        self.actions = keep
+        self.graph = graphs[0]
+        self._pipe = {"bufs": bufs, "graphs": graphs, "copy": torch.cuda.Stream(dev),
+                      "loss_host": torch.zeros(2, dtype=torch.float64).pin_memory()}
+
+    def run_pipelined(self, host_batches):
+        """Run one window per pinned host action batch (T,N,A); returns the
+        host losses.  H2D of batch k+1 runs on a copy stream while window k
+        computes; each window's loss is read back with an async D2H copy."""
+        self._ensure_pipeline()
+        P = self._pipe
+        comp = torch.cuda.current_stream(self.env.device)
+        cp = P["copy"]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in free:
+            e.record(comp)
+        losses = torch.zeros(len(host_batches), dtype=torch.float64).pin_memory()
+
+        def upload(k):
+            b = k % 2
+            with torch.cuda.stream(cp):
+                cp.wait_event(free[b])
+                P["bufs"][b].copy_(host_batches[k], non_blocking=True)
+                ready[b].record(cp)
+
+        if host_batches:
+            upload(0)
+        for k in range(len(host_batches)):
+            b = k % 2
+            if k + 1 < len(host_batches):
+                upload(k + 1)
+            comp.wait_event(ready[b])
+            P["graphs"][b].replay()
+            free[b].record(comp)
+            losses[k].copy_(self.loss64, non_blocking=True)
+        comp.synchronize()
+        return losses.tolist()

@@ -231,6 +231,28 @@ def test_window_engine_matches_autograd_path(qs, model, fused):
     assert e1.finished_episodes == e2.finished_episodes > 0
 
 
+def test_pipelined_windows_match_sequential(qs):
+    from paper_2509_10247_b200.window import BpttWindow
+
+    cfg = qs.TaskConfig(task="position", dynamics="full", n_envs=1024, episode_len=20,
+                        imu=qs.ImuSpec(0.1, 0.01, 0.01, 0.001))
+    g = torch.Generator(device="cpu").manual_seed(3)
+    batches = [(torch.randn(16, 1024, 4, generator=g) * 0.3).pin_memory() for _ in range(4)]
+    e1 = qs.make_task(cfg, strict=False)
+    e1.reset(seed=2)
+    w1 = BpttWindow(e1, 16).capture()
+    seq = []
+    for b in batches:
+        loss, _ = w1.run(b)
+        seq.append(float(loss))
+    e2 = qs.make_task(cfg, strict=False)
+    e2.reset(seed=2)
+    w2 = BpttWindow(e2, 16)
+    pip = w2.run_pipelined(batches)
+    np.testing.assert_allclose(pip, seq, rtol=1e-9)
+    assert torch.equal(w1.S[0], w2.S[0])
+
+
 def test_philox_resets_are_valid_and_deterministic(qs):
     cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=4096, episode_len=3)
     env = qs.make_task(cfg, strict=True)
