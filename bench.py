@@ -35,14 +35,20 @@ METRIC = "env-steps/s (fwd+bwd)"
 UNIT = "env-steps/s"
 IMU = dict(accel_noise_std=0.1, gyro_noise_std=0.01, accel_bias_rw_std=0.01, gyro_bias_rw_std=0.001)
 
-# algorithmic bytes per env-step of the fused-window kernels,
-# full+IMU, open-loop BPTT, unpadded payload:
-#   fwd: raw 16 + checkpoint state 52 + goal 12 + prev effort 16 + obs 48
-#        + rewards 12 + term/trunc 2 + flags 4 + IMU 24          = 186
-#   bwd: checkpoint state 52 + raw 16 + goal 12 + prev effort 16 + flags 4
-#        + dL/draw 16                                            = 116
-FWD_BYTES = 186
-BWD_BYTES = 116
+# Algorithmic bytes per env-step, SURVEY.md §8(d) (the fused env.step boundary,
+# fp32 unpadded), full quadrotor + IMU, open-loop BPTT:
+#   fwd 234 B (reads S 52, v_ema 12, raw 16, goal 12, prev effort 16, counter 4;
+#       writes S 52, v_ema 12, obs 48, rewards 12, effort 16, flags 2, counter 4)
+#       + IMU 72 B (bias read+write 48, readings 24)                     = 306
+#   bwd 265 B - 48 B (open loop: no dL/dobs)                 = 217
+FWD_BYTES = 306
+BWD_BYTES = 217
+# the fused-window kernels keep state/effort/counters/IMU bias on chip across
+# the T steps; the payload they MUST move per env-step is smaller:
+#   fwd: raw 16 + checkpoint state 52 + goal 12 + effort 16 + obs 48 + rewards 12
+#        + term/trunc 2 + flags 4 + IMU 24 = 186;  bwd: 52 + 16 + 12 + 16 + 4 + 16 = 116
+FWD_BYTES_FUSED = 186
+BWD_BYTES_FUSED = 116
 
 
 def parse():
@@ -450,7 +456,13 @@ def run_ours(a):
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_env_step": {"fwd": FWD_BYTES, "bwd": BWD_BYTES},
                      "units_per_launch": N * T, "ms_per_launch": {"fwd": ms_fwd, "bwd": ms_bwd},
-                     "gbs": {"fwd": gbs_fwd, "bwd": gbs_bwd}, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+                     "gbs": {"fwd": gbs_fwd, "bwd": gbs_bwd}, "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)",
+                     "bytes_source": "SURVEY.md §8(d) per env-step boundary bytes (full+IMU; open-loop bwd)",
+                     "fused_payload": {
+                         "bytes_per_env_step": {"fwd": FWD_BYTES_FUSED, "bwd": BWD_BYTES_FUSED},
+                         "gbs": {"fwd": FWD_BYTES_FUSED * N * T / (ms_fwd * 1e-3) / 1e9,
+                                 "bwd": BWD_BYTES_FUSED * N * T / (ms_bwd * 1e-3) / 1e9},
+                         "note": "bytes the fused-window kernels must move; they are issue-bound (profiles/README.md)"}},
         "per_step_kernels": {"ms_per_window": ms_per_step_path,
                              "env_steps_per_s": world * N * T / (ms_per_step_path * 1e-3),
                              "note": "same window through the per-step kernels behind FlightTask.step"},

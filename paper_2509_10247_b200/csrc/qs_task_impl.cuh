@@ -732,7 +732,8 @@ template <int M, int TASK, int NAMAX>
 QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int na, long N,
                        const State* s_in, const float4* raw_in, const float4* goal, const float4* peff,
                        const float4* dr, bool has_dr, const int* flags_in, const float* g_obs,
-                       const float* g_r_rows, float g_r_scalar, State* gS, float* g_raw_t) {
+                       const float* g_r_rows, float g_r_scalar, State* gS, float* g_raw_t,
+                       const State* s2_known = nullptr) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
   const DynK k = dyn_consts(cfg);
@@ -753,10 +754,15 @@ QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int n
     Squash q = squash<A>(raw, rp);
     float2 cs;
     float4 c = world_cmd<M>(s, q.sq, k.g, cs);
-    State n = model_step<M>(s, c, rp, k);
-    n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;
     const int fl = flags_in[a];
     const bool done = fl & FLAG_DONE;
+    State n;
+    if (s2_known && !done) {
+      n = s2_known[a];  // the next checkpoint is this step's post-dynamics state
+    } else {  // reset rows: the checkpoint holds the respawned state, recompute
+      n = model_step<M>(s, c, rp, k);
+      n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;
+    }
     State g = done ? zero_state() : gS[a];
     g.ve = v3(0.f, 0.f, 0.f);
     // observation path (only rows that were not reset; q/tasks.py:584-594)
@@ -1062,6 +1068,12 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
     gS[a] = load_grad<M>(w.g_S_final, N, e * na + a);
   }
   load_ck(w.T - 1, cur);
+  State s2[NAMAX];  // checkpoint t+1 = post-dynamics state of step t (non-reset rows)
+#pragma unroll
+  for (int a = 0; a < NAMAX; ++a) {
+    if (a >= na) break;
+    s2[a] = load_state<M>(w.S + (long)w.T * NP * N * 4, N, e * na + a);
+  }
   for (int t = w.T - 1; t >= 0; --t) {
     if (t > 0) load_ck(t - 1, nxt);
     const float gscale = w.g_rctrl_scale * powf(w.gamma, (float)t);
@@ -1079,9 +1091,12 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
     }
     env_step_bwd<M, TASK, NAMAX>(cfg, sc, e, na, N, s_in, raw, goal, peff, dr, has_dr, fl, nullptr,
                                  w.g_rctrl ? w.g_rctrl + (long)t * N : nullptr, gscale, gS,
-                                 w.g_actions + (long)t * N * A);
+                                 w.g_actions + (long)t * N * A, s2);
 #pragma unroll
-    for (int a = 0; a < NAMAX; ++a) cur[a] = nxt[a];
+    for (int a = 0; a < NAMAX; ++a) {
+      s2[a] = cur[a].s;
+      cur[a] = nxt[a];
+    }
   }
   if (w.g_S0) {
 #pragma unroll
