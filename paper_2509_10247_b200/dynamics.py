@@ -366,6 +366,15 @@ def make_model(name: str, params: QuadParams | None = None, device=None) -> Dyna
     return cls(params or QuadParams(), device=device)
 
 
+def rate_loop(w: torch.Tensor, w_cmd: torch.Tensor, params: QuadParams) -> torch.Tensor:
+    """Body-rate P controller with gyroscopic feedforward (q/dynamics.py:140-152):
+    tau = J (K (w_cmd - w)) + w x (J w).  The step kernels use the algebraically
+    equal w_dot = K (w_cmd - w); this is the torque for API parity."""
+    J = torch.as_tensor(params.inertia, dtype=w.dtype, device=w.device)
+    K = torch.as_tensor(params.rate_gains, dtype=w.dtype, device=w.device)
+    return (K * (w_cmd - w)) @ J.T + torch.cross(w, w @ J.T, dim=-1)
+
+
 def action_squash(raw: torch.Tensor, lo, hi) -> torch.Tensor:
     """tanh squash into [lo, hi] (q/dynamics.py:277-284)."""
     lo = torch.as_tensor(np.asarray(lo), dtype=torch.float32, device=raw.device)

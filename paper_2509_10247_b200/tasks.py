@@ -638,6 +638,18 @@ class FlightTask:
     def bounds_hi_per_row(self) -> torch.Tensor:
         return torch.repeat_interleave(self._scene.bounds[:, 1, :3] - 1e-6, self.n_agents, dim=0)
 
+    @bounds_lo_per_row.setter
+    def bounds_lo_per_row(self, lo):
+        lo = torch.as_tensor(np.asarray(lo) if not isinstance(lo, torch.Tensor) else lo, dtype=torch.float32,
+                             device=self.device).reshape(self.N, 3)
+        self._scene.bounds[:, 0, :3] = lo[::self.n_agents] - 1e-6
+
+    @bounds_hi_per_row.setter
+    def bounds_hi_per_row(self, hi):
+        hi = torch.as_tensor(np.asarray(hi) if not isinstance(hi, torch.Tensor) else hi, dtype=torch.float32,
+                             device=self.device).reshape(self.N, 3)
+        self._scene.bounds[:, 1, :3] = hi[::self.n_agents] + 1e-6
+
     # -- observation (q/tasks.py:415-463)
 
     def observe(self) -> Obs:
