@@ -82,6 +82,8 @@ typedef struct qs_task_cfg {
   float imu_accel_std, imu_gyro_std, imu_accel_rw, imu_gyro_rw;
   int32_t reset_mode;   /* 0: in-kernel Philox resets; 1: deferred (injected) */
   int32_t want_cam;     /* write camera yaw (cos,sin) per row for rendering */
+  float act_center[4], act_half[4];  /* (lo+hi)/2, (hi-lo)/2 of act_lo/hi (host-computed) */
+  float imu_sqrt_dt;                 /* sqrt(dt) */
 } qs_task_cfg;
 
 /* Per-env scene data (read-only during a rollout).  Obstacles are packed

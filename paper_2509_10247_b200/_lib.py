@@ -52,6 +52,7 @@ class QsTaskCfg(C.Structure):
         ("imu_enabled", i32), ("imu_accel_std", f32), ("imu_gyro_std", f32), ("imu_accel_rw", f32),
         ("imu_gyro_rw", f32),
         ("reset_mode", i32), ("want_cam", i32),
+        ("act_center", f32 * 4), ("act_half", f32 * 4), ("imu_sqrt_dt", f32),
     ]
 
 

@@ -232,7 +232,7 @@ QS_D void imu_apply(const qs_task_cfg& cfg, long row, long N, int tick, const St
     na = v3(b.z, b.w, c.x);
     ng = v3(c.y, c.z, c.w);
   }
-  float sq = sqrtf(cfg.dt);
+  const float sq = cfg.imu_sqrt_dt;
   ba += nba * (cfg.imu_accel_rw * sq);
   bg += nbg * (cfg.imu_gyro_rw * sq);
   V3 xb, yb, zb;
@@ -452,14 +452,15 @@ QS_D RowPrm row_params_v(const qs_task_cfg& cfg, bool has_dr, float4 d) {
   }
 #pragma unroll
   for (int k = 0; k < ModelTraits<M>::A; ++k) {
-    float lo = cfg.act_lo[k], hi = cfg.act_hi[k];
     if (has_dr) {  // q/tasks.py:370-375
-      float c = (lo + hi) * 0.5f, h = (hi - lo) * 0.5f;
-      lo = c - h * scale;
-      hi = c + h * scale;
+      const float c = cfg.act_center[k], h = cfg.act_half[k];
+      const float lo = c - h * scale, hi = c + h * scale;
+      r.center[k] = (lo + hi) * 0.5f;
+      r.half[k] = (hi - lo) * 0.5f;
+    } else {  // host-precomputed: no per-step arithmetic
+      r.center[k] = cfg.act_center[k];
+      r.half[k] = cfg.act_half[k];
     }
-    r.center[k] = (lo + hi) * 0.5f;
-    r.half[k] = (hi - lo) * 0.5f;
   }
   return r;
 }

@@ -174,6 +174,11 @@ def fill_dyn_cfg(cfg: L.QsTaskCfg, model: str, params: QuadParams, action_box=No
         lo, hi = action_box
         for i in range(len(lo)):
             cfg.act_lo[i], cfg.act_hi[i] = float(lo[i]), float(hi[i])
+            # the kernels' fp32 (lo+hi)*0.5 and (hi-lo)*0.5, precomputed once
+            l32, h32 = np.float32(lo[i]), np.float32(hi[i])
+            cfg.act_center[i] = float((l32 + h32) * np.float32(0.5))
+            cfg.act_half[i] = float((h32 - l32) * np.float32(0.5))
+    cfg.imu_sqrt_dt = float(np.sqrt(np.float32(params.dt)))
     return cfg
 
 
