@@ -262,6 +262,12 @@ typedef struct qs_gen_cfg {
   int32_t indoor, max_attempts, Sm, Bm, Cm;
   uint64_t seed;
   int64_t env_offset;
+  /* re-randomisation on reset: only envs with env_mask[e] != 0 are
+   * regenerated (NULL = all), keyed additionally by episode[e * episode_stride]
+   * (NULL = episode 0).  Lets a reset regenerate its obstacles on device. */
+  const uint8_t* env_mask;
+  const int32_t* episode;
+  int32_t episode_stride;
 } qs_gen_cfg;
 int qs_gen_obstacle_course(const qs_gen_cfg* cfg, int32_t n_envs, float* bounds, float* spawn_goal,
                            float* spheres, float* boxes, float* cylinders, int32_t* counts,

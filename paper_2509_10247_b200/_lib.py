@@ -96,7 +96,7 @@ class QsGenCfg(C.Structure):
     _fields_ = [("spawn", f32 * 3), ("goal", f32 * 3), ("density", f32), ("r_quad", f32),
                 ("clearance", f32), ("corridor_halfwidth", f32), ("indoor", i32),
                 ("max_attempts", i32), ("Sm", i32), ("Bm", i32), ("Cm", i32), ("seed", u64),
-                ("env_offset", i64)]
+                ("env_offset", i64), ("env_mask", vp), ("episode", vp), ("episode_stride", i32)]
 
 
 P = C.POINTER

@@ -89,6 +89,8 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
   __shared__ int s_done;
   const long e = blockIdx.x;
   if (e >= n_envs) return;
+  if (cfg.env_mask && !cfg.env_mask[e]) return;  // re-randomise only the masked envs
+  const uint32_t episode = cfg.episode ? (uint32_t)cfg.episode[e * cfg.episode_stride] : 0u;
   const Frame F = make_frame(cfg);
   const long cells = (long)F.dims[0] * F.dims[1] * F.dims[2];
   const long nw = (cells + 31) >> 5;
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
     for (int i = threadIdx.x; i < n_total; i += blockDim.x) {
       Rng rng(cfg.seed, gid, (uint32_t)attempt, RNG_SCENE);
       rng.ctr.z = (uint32_t)attempt * 4096u + (uint32_t)i;
+      rng.ctr.w |= (episode & 0xFFFFu) << 8;  // purpose byte stays on top
       float4 u = rng.uniform4(), w = rng.uniform4();
       float along = u.x * F.dist;
       float lat = -cfg.corridor_halfwidth + 2.f * cfg.corridor_halfwidth * u.y;

@@ -291,6 +291,7 @@ class FlightTask:
         self.lidar = (config.lidar or sn.LidarPattern()) if config.sensor == "lidar" else None
         self.imu_noise_source = None  # test hook: callable(step_index) -> (4,N,3)
         self._episode_counter = 0
+        self._regen = False
         self._S = None
         self._pending = None
 
@@ -416,7 +417,9 @@ class FlightTask:
             cfg.imu_enabled = 1
             cfg.imu_accel_std, cfg.imu_gyro_std = c.imu.accel_noise_std, c.imu.gyro_noise_std
             cfg.imu_accel_rw, cfg.imu_gyro_rw = c.imu.accel_bias_rw_std, c.imu.gyro_bias_rw_std
-        cfg.reset_mode = 1 if self.reset_source is not None else 0
+        # deferred resets: host-injected draws, or a scene regeneration that must
+        # precede the spawn draw (spawn/goal come from the regenerated course)
+        cfg.reset_mode = 1 if (self.reset_source is not None or self._regen) else 0
         cfg.want_cam = 1 if c.sensor != "none" else 0
         return cfg
 
@@ -450,9 +453,9 @@ class FlightTask:
             self._scene = sc
             self.scenes = None
         elif c.task == "avoidance":
-            self._scene = wd.gen_obstacle_courses(
-                self.seed, E, [0.0, 0.0, 1.2], [c.goal_dist, 0.0, 1.5], c.density, c.style,
-                r_quad=c.collision_radius, device=dev, env_offset=self.env_offset, check=self.strict)
+            self._gen_args = dict(spawn=[0.0, 0.0, 1.2], goal=[c.goal_dist, 0.0, 1.5], density=c.density,
+                                  style=c.style, r_quad=c.collision_radius, env_offset=self.env_offset)
+            self._scene = wd.gen_obstacle_courses(self.seed, E, device=dev, check=self.strict, **self._gen_args)
             self.scenes = None
         else:
             self.scenes = [wd.gen_race_track((self.seed * 99_991 + e + self.env_offset) & 0x7FFFFFFF,
@@ -486,6 +489,11 @@ class FlightTask:
         self._episode_counter = 0
         self._steps_total = 0
         self._frame_cache = None
+        c = self.config
+        if c.regen_scene_on_reset and (c.task != "avoidance" or self.scene_source is not None):
+            raise TaskContractError("regen_scene_on_reset needs the avoidance task with generated scenes "
+                                    "(no scene_source)")
+        self._regen = bool(c.regen_scene_on_reset)
         self._build_scenes()
         self._alloc_persistent()
         self._cfg = self._build_cfg()
@@ -752,17 +760,35 @@ class FlightTask:
         io.terminated, io.truncated, io.flags, io.cam = L.ptr(b.term), L.ptr(b.trunc), L.ptr(b.flags), L.ptr(b.cam)
         stream = L.stream_handle(dev)
         L.check(L.lib().qs_task_step_fwd(self._cfg, self._scene.struct(), io, stream), "qs_task_step_fwd")
-        if self.reset_source is not None:  # deferred, host-injected resets
-            done_env = (b.flags.view(self.n_envs, self.n_agents)[:, 0] & 1).cpu().numpy().astype(bool)
-            if done_env.any():
-                ids = np.flatnonzero(done_env)
-                tab, keep = self._reset_table(ids)
-                L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, tab.env_mask, tab, stream),
+        if self._cfg.reset_mode == 1:  # deferred resets
+            if self.reset_source is not None:  # host-injected draws (syncs on the done mask)
+                done_env = (b.flags.view(self.n_envs, self.n_agents)[:, 0] & 1).cpu().numpy().astype(bool)
+                if done_env.any():
+                    ids = np.flatnonzero(done_env)
+                    tab, keep = self._reset_table(ids)
+                    self._regen_scenes(keep["mask"])
+                    L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, tab.env_mask, tab,
+                                                  stream), "qs_task_spawn")
+                    self._episode_counter += 1
+                    del keep
+            else:  # device-only: done mask -> new course -> Philox spawn, no host sync
+                mask = (b.flags.view(self.n_envs, self.n_agents)[:, 0] & 1).to(torch.uint8)
+                self._regen_scenes(mask)
+                L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, L.ptr(mask), None, stream),
                         "qs_task_spawn")
-                self._episode_counter += 1
-                del keep
             L.check(L.lib().qs_task_observe(self._cfg, self._scene.struct(), io, stream), "qs_task_observe")
+            self._frame_cache = None
         return b
+
+    def _regen_scenes(self, mask):
+        """Re-randomise the obstacle course of every env in ``mask`` (uint8, device),
+        keyed by (seed, env, episode) — ``meta[:, 1]`` already holds the new
+        episode index.  The reference declares ``regen_scene_on_reset`` without
+        wiring it (q/tasks.py:98); the course distribution is q/world.py:207-340."""
+        if not self._regen:
+            return
+        wd.gen_obstacle_courses(self.seed, self.n_envs, check=False, out=self._scene, env_mask=mask,
+                                episode=self._meta[:, 1], episode_stride=4, err=self._err, **self._gen_args)
 
     def step(self, raw_action) -> StepOutput:
         raw = raw_action if isinstance(raw_action, torch.Tensor) else torch.as_tensor(np.asarray(raw_action))

@@ -22,6 +22,8 @@ class BpttWindow:
                  fused: bool = True):
         if env.reset_source is not None:
             raise ValueError("BpttWindow needs in-kernel (Philox) resets; reset_source forces host syncs")
+        if env._cfg.reset_mode != 0:
+            raise ValueError("BpttWindow resets inline; regen_scene_on_reset needs the per-step env.step path")
         self.env, self.T, self.gamma = env, horizon, gamma
         dev, N, T = env.device, env.N, horizon
         f = dict(device=dev, dtype=torch.float32)

@@ -143,9 +143,14 @@ def course_counts(spawn, goal, density, corridor_halfwidth=3.0):
 def gen_obstacle_courses(seed: int, n_envs: int, spawn, goal, density: float, style: str = "outdoor",
                          r_quad: float = 0.15, clearance: float = 0.5, corridor_halfwidth: float = 3.0,
                          max_attempts: int = 100, device=None, env_offset: int = 0,
-                         check: bool = True) -> DeviceScene:
-    """Batch of feasible obstacle courses generated on the GPU (q/world.py:207-340)."""
-    dev = L.require_cuda(device)
+                         check: bool = True, out: DeviceScene | None = None, env_mask=None, episode=None,
+                         episode_stride: int = 1, err=None) -> DeviceScene:
+    """Batch of feasible obstacle courses generated on the GPU (q/world.py:207-340).
+
+    With ``out``/``env_mask``/``episode`` (device tensors) it regenerates, in
+    place and without a host sync, only the masked envs' courses keyed by their
+    episode index: obstacle re-randomisation on reset."""
+    dev = L.require_cuda(device if out is None else out.device)
     spawn = np.asarray(spawn, dtype=np.float64)
     goal = np.asarray(goal, dtype=np.float64)
     if np.linalg.norm(goal - spawn) <= 2.0:
@@ -154,8 +159,9 @@ def gen_obstacle_courses(seed: int, n_envs: int, spawn, goal, density: float, st
         raise GenerationError("density must be >= 0", seed)
     ns, nb, nc = course_counts(spawn, goal, density, corridor_halfwidth)
     nb_tot = nb + (5 if style == "indoor" else 0)
-    sc = DeviceScene(n_envs, dev, max(ns, 1), max(nb_tot, 1), max(nc, 1))
+    sc = out if out is not None else DeviceScene(n_envs, dev, max(ns, 1), max(nb_tot, 1), max(nc, 1))
     cfg = L.QsGenCfg()
+    cfg.env_mask, cfg.episode, cfg.episode_stride = L.ptr(env_mask), L.ptr(episode), int(episode_stride)
     for i in range(3):
         cfg.spawn[i], cfg.goal[i] = float(spawn[i]), float(goal[i])
     cfg.density, cfg.r_quad, cfg.clearance = float(density), float(r_quad), float(clearance)
@@ -165,7 +171,8 @@ def gen_obstacle_courses(seed: int, n_envs: int, spawn, goal, density: float, st
     cfg.Sm, cfg.Bm, cfg.Cm = sc.spheres.shape[1], sc.boxes.shape[1], sc.cylinders.shape[1]
     cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
     cfg.env_offset = int(env_offset)
-    err = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
+    if err is None:
+        err = torch.tensor([0, 2**31 - 1], dtype=torch.int32, device=dev)
     L.check(L.lib().qs_gen_obstacle_course(
         cfg, n_envs, L.ptr(sc.bounds), L.ptr(sc.spawn_goal), L.ptr(sc.spheres), L.ptr(sc.boxes),
         L.ptr(sc.cylinders), L.ptr(sc.counts), L.ptr(sc.ground_z), L.ptr(err),

@@ -92,3 +92,55 @@ def test_in_kernel_domain_randomisation_statistics():
         env.step(torch.zeros(env.N, 3, device="cuda"))
     after = env._dr.double().cpu().numpy()
     assert (np.abs(after - before).max(axis=1) > 0).mean() > 0.99
+
+
+def test_obstacle_rerandomisation_on_reset():
+    """regen_scene_on_reset (declared, unwired at q/tasks.py:98): a done env gets
+    a fresh course keyed by (seed, env, episode) on the device, then a Philox
+    spawn on that course; envs that did not finish keep theirs."""
+    import paper_2509_10247_b200 as qs
+    from oracle import quadsim_oracle as O
+
+    E = 96
+    cfg = qs.TaskConfig(task="avoidance", dynamics="pm_continuous", n_envs=E, episode_len=3, density=0.3,
+                        regen_scene_on_reset=True)
+    env = qs.make_task(cfg)
+    env.reset(seed=5)
+    sc = env._scene
+    snap = lambda: [t.clone() for t in (sc.spheres, sc.boxes, sc.cylinders, sc.counts)]
+    before = snap()
+    ever_done = np.zeros(E, bool)
+    for step in range(3):
+        prev = snap()
+        out = env.step(torch.zeros(E, 3, device="cuda"))
+        done = (env._last_flags.cpu().numpy() & 1).astype(bool)
+        now = snap()
+        changed = np.zeros(E, bool)
+        for a, b in zip(prev, now):
+            changed |= (a != b).reshape(E, -1).any(1).cpu().numpy()
+        assert not changed[~done].any(), step  # untouched unless reset
+        assert changed[done].all(), step
+        ever_done |= done
+        p = env.state.p.detach().cpu().numpy()
+        spawn = sc.spawn_goal[:, 0, :3].cpu().numpy()
+        if done.any():
+            assert np.linalg.norm(p[done] - spawn[done], axis=-1).max() < 1.0  # spawned on the new course
+        assert torch.isfinite(out.obs.proprio).all()
+    assert ever_done.all()  # episode_len 3 truncates everything
+    after = snap()
+    moved = torch.zeros(E, dtype=torch.bool, device="cuda")
+    for a, b in zip(before, after):
+        moved |= (a != b).reshape(E, -1).any(1)
+    assert moved.all()
+    # deterministic: regenerating every env at its current episode reproduces the live scenes
+    ref = qs.world.gen_obstacle_courses(5, E, [0.0, 0.0, 1.2], [cfg.goal_dist, 0.0, 1.5], cfg.density,
+                                        cfg.style, r_quad=cfg.collision_radius, device="cuda",
+                                        episode=env._meta[:, 1], episode_stride=4)
+    for a, b in zip((ref.spheres, ref.boxes, ref.cylinders, ref.counts), after):
+        assert torch.equal(a, b)
+    env.check_errors()
+    for s in qs.world.device_scene_to_scenes(sc, style=cfg.style):
+        osc = O.Scene(prims={"spheres": s.prims.spheres, "boxes": s.prims.boxes,
+                             "cylinders": s.prims.cylinders, "ground_z": 0.0},
+                      bounds_lo=s.bounds_lo, bounds_hi=s.bounds_hi, spawn=s.spawn, goal=s.goal)
+        assert O.grid_path_exists(osc)
