@@ -84,6 +84,8 @@ typedef struct qs_task_cfg {
   int32_t want_cam;     /* write camera yaw (cos,sin) per row for rendering */
   float act_center[4], act_half[4];  /* (lo+hi)/2, (hi-lo)/2 of act_lo/hi (host-computed) */
   float imu_sqrt_dt;                 /* sqrt(dt) */
+  uint32_t rng_round_keys[20];       /* Philox round keys of `seed`: written by the library
+                                        on its private copy, ignored on input */
 } qs_task_cfg;
 
 /* Per-env scene data (read-only during a rollout).  Obstacles are packed
@@ -253,6 +255,12 @@ int qs_dyn_step_bwd(int32_t model, int32_t n, const float* S_in, const float* ac
 
 /* reconstruct_attitude (q/sensors.py:569-606): a (N,4), v_ema (N,4) -> R (N,9). */
 int qs_reconstruct_attitude(int32_t n, const float* a, const float* v_ema, float* R, void* stream);
+
+/* Philox4x32-10 (Salmon et al., SC'11), the counter-based generator behind every
+ * in-kernel draw (resets, DR, IMU, scenes), exposed for known-answer tests:
+ * items (n,6) = ctr[4], key[2] -> out (n,8) = the block computed with the key
+ * schedule on the fly, then with precomputed round keys (the two must agree). */
+int qs_philox4x32_10(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream);
 
 /* In-kernel obstacle-course generation with BFS feasibility
  * (q/world.py:207-340), Philox keyed by (seed, global env id, attempt). */

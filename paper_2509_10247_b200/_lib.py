@@ -53,6 +53,7 @@ class QsTaskCfg(C.Structure):
         ("imu_gyro_rw", f32),
         ("reset_mode", i32), ("want_cam", i32),
         ("act_center", f32 * 4), ("act_half", f32 * 4), ("imu_sqrt_dt", f32),
+        ("rng_round_keys", C.c_uint32 * 20),
     ]
 
 
@@ -118,6 +119,7 @@ _SIGS = {
     "qs_dyn_step_fwd": ([i32, i32, vp, vp, vp, P(QsTaskCfg), vp, vp, vp], i32),
     "qs_dyn_step_bwd": ([i32, i32, vp, vp, vp, P(QsTaskCfg), vp, vp, vp, vp], i32),
     "qs_reconstruct_attitude": ([i32, vp, vp, vp, vp], i32),
+    "qs_philox4x32_10": ([i32, vp, vp, vp], i32),
     "qs_gen_obstacle_course": ([P(QsGenCfg), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
 }
 

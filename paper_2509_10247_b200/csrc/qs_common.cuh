@@ -98,16 +98,62 @@ QS_HD float softplus(float x) {  // logaddexp(0, x)
 // is a pure function of (key, counter), so resets and IMU noise are graph
 // capturable and independent of launch geometry / sharding.
 
+QS_HD uint4 philox_round(uint4 c, uint32_t k0, uint32_t k1) {
+#ifdef __CUDA_ARCH__
+  uint32_t lo0 = c.x * 0xD2511F53u, hi0 = __umulhi(c.x, 0xD2511F53u);
+  uint32_t lo1 = c.z * 0xCD9E8D57u, hi1 = __umulhi(c.z, 0xCD9E8D57u);
+#else
+  uint64_t p0 = (uint64_t)c.x * 0xD2511F53u, p1 = (uint64_t)c.z * 0xCD9E8D57u;
+  uint32_t lo0 = (uint32_t)p0, hi0 = (uint32_t)(p0 >> 32), lo1 = (uint32_t)p1, hi1 = (uint32_t)(p1 >> 32);
+#endif
+  return make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+}
+
 QS_D uint4 philox4x32_10(uint4 c, uint2 k) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
-    uint32_t lo0 = c.x * 0xD2511F53u, hi0 = __umulhi(c.x, 0xD2511F53u);
-    uint32_t lo1 = c.z * 0xCD9E8D57u, hi1 = __umulhi(c.z, 0xCD9E8D57u);
-    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    c = philox_round(c, k.x, k.y);
     k.x += 0x9E3779B9u;
     k.y += 0xBB67AE85u;
   }
   return c;
+}
+
+// the same permutation with the key schedule precomputed on the host
+// (qs_task_cfg::rng_round_keys): inside a kernel the round keys are
+// kernel-parameter operands, so each round is 2 IMAD.WIDE + 2 LOP3
+QS_D uint4 philox4x32_10_rk(uint4 c, const uint32_t* rk) {
+#pragma unroll
+  for (int i = 0; i < 10; ++i) c = philox_round(c, rk[2 * i], rk[2 * i + 1]);
+  return c;
+}
+
+inline void philox_round_keys(uint64_t seed, uint32_t* rk) {
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  for (int i = 0; i < 10; ++i) {
+    rk[2 * i] = k0;
+    rk[2 * i + 1] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+}
+
+// 32 random bits -> uniform in (0, 1): 23 mantissa bits in [1, 2), shifted by
+// 1 - 2^-24 (exact by Sterbenz), so the result lies in [2^-24, 1 - 2^-24]
+QS_D float u01(uint32_t r) { return __uint_as_float((r >> 9) | 0x3f800000u) - 0.99999994f; }
+
+QS_D float4 u01x4(uint4 r) { return make_float4(u01(r.x), u01(r.y), u01(r.z), u01(r.w)); }
+
+// four standard normals (Box-Muller on two pairs).  MUFU intrinsics: the
+// ~2-ulp error of lg2/sqrt/sin/cos is immaterial for sampling noise.
+QS_D float4 box_muller4(float4 u) {
+  float d0, d1;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(-2.f * __logf(u.x)));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(-2.f * __logf(u.z)));
+  float s0, c0, s1, c1;
+  __sincosf(6.28318530717958648f * u.y, &s0, &c0);
+  __sincosf(6.28318530717958648f * u.w, &s1, &c1);
+  return make_float4(d0 * c0, d0 * s0, d1 * c1, d1 * s1);
 }
 
 // purposes (counter word 2, high byte)
@@ -129,25 +175,25 @@ struct Rng {
   QS_D float4 uniform4() {
     uint4 r = philox4x32_10(ctr, key);
     ctr.w++;
-    const float s = 1.f / 16777216.f;
-    return make_float4(((r.x >> 8) + 0.5f) * s, ((r.y >> 8) + 0.5f) * s, ((r.z >> 8) + 0.5f) * s,
-                       ((r.w >> 8) + 0.5f) * s);
+    return u01x4(r);
   }
-  // four standard normals (Box-Muller on two pairs).  MUFU intrinsics: the
-  // ~2-ulp error of lg2/sqrt/sin/cos is immaterial for sampling noise.
-  QS_D float4 normal4() {
-    float4 u = uniform4();
-    float r0 = sqrt_fast(-2.f * __logf(u.x)), r1 = sqrt_fast(-2.f * __logf(u.z));
-    float s0, c0, s1, c1;
-    __sincosf(6.28318530717958648f * u.y, &s0, &c0);
-    __sincosf(6.28318530717958648f * u.w, &s1, &c1);
-    return make_float4(r0 * c0, r0 * s0, r1 * c1, r1 * s1);
+  QS_D float4 normal4() { return box_muller4(uniform4()); }
+};
+
+// Rng with the round keys precomputed (the task kernels: cfg.rng_round_keys);
+// draws are identical to Rng's for the same seed
+struct RngK {
+  uint4 ctr;
+  const uint32_t* rk;
+  QS_D RngK(const uint32_t* rk_, uint64_t id, uint32_t sub, uint32_t purpose) : rk(rk_) {
+    ctr = make_uint4((uint32_t)id, (uint32_t)(id >> 32), sub, purpose << 24);
   }
-  QS_D static float sqrt_fast(float x) {
-    float d;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(x));
-    return d;
+  QS_D float4 uniform4() {
+    uint4 r = philox4x32_10_rk(ctr, rk);
+    ctr.w++;
+    return u01x4(r);
   }
+  QS_D float4 normal4() { return box_muller4(uniform4()); }
 };
 
 // ---------------------------------------------------------------------------

@@ -25,6 +25,9 @@ int task_call(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
   if (cfg->n_agents < 1 || cfg->n_agents > QS_MAX_AGENTS) return QS_ERR_BAD_ARGUMENT;
   if (cfg->n_envs <= 0) return QS_OK;
   cudaStream_t s = (cudaStream_t)stream;
+  qs_task_cfg c = *cfg;  // private copy carrying the derived Philox round keys
+  philox_round_keys(c.seed, c.rng_round_keys);
+  cfg = &c;
   switch (cfg->task) {
     case QS_TASK_POSITION: return qs::task_dispatch<QS_TASK_POSITION>(op, cfg, sc, p, mask, tab, s);
     case QS_TASK_AVOIDANCE: return qs::task_dispatch<QS_TASK_AVOIDANCE>(op, cfg, sc, p, mask, tab, s);

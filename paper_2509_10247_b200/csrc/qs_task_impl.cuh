@@ -121,7 +121,7 @@ template <int M, int TASK, int NAMAX>
 QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int episode, int na,
                        V3* p, V3* v, V3* goal, V3& head, int& next_gate) {
   const uint64_t gid = (uint64_t)(e + cfg.env_offset);
-  Rng rng(cfg.seed, gid, (uint32_t)episode, RNG_SPAWN);
+  RngK rng(cfg.rng_round_keys, gid, (uint32_t)episode, RNG_SPAWN);
   float4 blo = ld4(sc.bounds, 2 * e), bhi = ld4(sc.bounds, 2 * e + 1);
   V3 lo = xyz(blo), hi = xyz(bhi);
   bool ok = true;
@@ -201,7 +201,7 @@ QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int e
 }
 
 QS_D float4 dr_sample(const qs_task_cfg& cfg, long row, int episode) {
-  Rng rng(cfg.seed, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)episode, RNG_DR);
+  RngK rng(cfg.rng_round_keys, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)episode, RNG_DR);
   float4 u = rng.uniform4();
   float drag = cfg.dr_drag[0] + (cfg.dr_drag[1] - cfg.dr_drag[0]) * u.x;
   float lat = cfg.dr_latency[0] + (cfg.dr_latency[1] - cfg.dr_latency[0]) * u.y;
@@ -213,10 +213,28 @@ QS_D float4 dr_sample(const qs_task_cfg& cfg, long row, int episode) {
 // IMU read (q/sensors.py:540-555) on the post-dynamics state.  Bias state lives
 // in registers (ba, bg); noise is injected (noise != NULL, (4,N,3)) or Philox.
 
+// the 12 Philox normals of one row-step: bias walks (accel, gyro), then white
+// noise (accel, gyro).  Independent of the state, so the window kernel draws
+// them at the top of the step where they fill the dynamics' dependency stalls.
+struct ImuNoise {
+  float4 a, b, c;
+};
+QS_D ImuNoise imu_draw(const qs_task_cfg& cfg, long row, int tick) {
+  RngK rng(cfg.rng_round_keys, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)tick, RNG_IMU);
+  ImuNoise z;
+  z.a = rng.normal4();
+  z.b = rng.normal4();
+  z.c = rng.normal4();
+  return z;
+}
+
+template <int M>
+QS_D void imu_apply_z(const qs_task_cfg& cfg, long row, const State& s2, V3 vdot, V3 g, float4& b0, float4& b1,
+                      V3 nba, V3 nbg, V3 na, V3 ng, float* out);
+
 template <int M>
 QS_D void imu_apply(const qs_task_cfg& cfg, long row, long N, int tick, const State& s2, V3 vdot, V3 g,
                     float4& b0, float4& b1, const float* noise, float* out) {
-  V3 ba = xyz(b0), bg = xyz(b1);
   V3 nba, nbg, na, ng;
   if (noise) {
     const float* z = noise;
@@ -225,13 +243,19 @@ QS_D void imu_apply(const qs_task_cfg& cfg, long row, long N, int tick, const St
     na = v3(z[3 * (2 * N + row)], z[3 * (2 * N + row) + 1], z[3 * (2 * N + row) + 2]);
     ng = v3(z[3 * (3 * N + row)], z[3 * (3 * N + row) + 1], z[3 * (3 * N + row) + 2]);
   } else {
-    Rng rng(cfg.seed, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)tick, RNG_IMU);
-    float4 a = rng.normal4(), b = rng.normal4(), c = rng.normal4();
-    nba = v3(a.x, a.y, a.z);
-    nbg = v3(a.w, b.x, b.y);
-    na = v3(b.z, b.w, c.x);
-    ng = v3(c.y, c.z, c.w);
+    ImuNoise z = imu_draw(cfg, row, tick);
+    nba = v3(z.a.x, z.a.y, z.a.z);
+    nbg = v3(z.a.w, z.b.x, z.b.y);
+    na = v3(z.b.z, z.b.w, z.c.x);
+    ng = v3(z.c.y, z.c.z, z.c.w);
   }
+  imu_apply_z<M>(cfg, row, s2, vdot, g, b0, b1, nba, nbg, na, ng, out);
+}
+
+template <int M>
+QS_D void imu_apply_z(const qs_task_cfg& cfg, long row, const State& s2, V3 vdot, V3 g, float4& b0, float4& b1,
+                      V3 nba, V3 nbg, V3 na, V3 ng, float* out) {
+  V3 ba = xyz(b0), bg = xyz(b1);
   const float sq = cfg.imu_sqrt_dt;
   ba += nba * (cfg.imu_accel_rw * sq);
   bg += nbg * (cfg.imu_gyro_rw * sq);
@@ -531,13 +555,17 @@ struct StepStat {
 // ---------------------------------------------------------------------------
 // one fused env step on the register file (FlightTask.step, q/tasks.py:549-600)
 
-template <int M, int TASK, int NAMAX, bool INLINE>
+// IMU: 0 = decided at run time by has_imu / out.imu_noise; 1 = Philox IMU on
+// (compile time), its normals drawn at the top of the row's step
+template <int M, int TASK, int NAMAX, bool INLINE, int IMU = 0>
 QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int na, long N,
                            EnvRegs<NAMAX>& R, const float4* raw_in, const StepOut& out, int32_t* err,
                            bool has_dr, bool has_imu) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
   const DynK k = dyn_consts(cfg);
+  if (IMU == 1) has_imu = true;
+  int errc = 0, err_row = 0;  // first contract error of the env, reported once after the rows
   int term_env = 0;
   State s2[NAMAX];
   float rc[NAMAX], rl[NAMAX];
@@ -554,14 +582,23 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, i
     const State& s = R.s[a];
     RowPrm rp = row_params_v<M>(cfg, has_dr, R.dr[a]);
     const float4 raw = raw_in[a];
-    if (!act_finite<A>(raw)) report_err(err, QS_ERR_NONFINITE_ACTION, (int)row);
-    if (!state_finite<M>(s)) report_err(err, QS_ERR_NONFINITE_STATE, (int)row);
+    ImuNoise z;
+    if (IMU == 1) z = imu_draw(cfg, row, R.meta.z);
+    {
+      const int c = !act_finite<A>(raw) ? QS_ERR_NONFINITE_ACTION
+                                        : (!state_finite<M>(s) ? QS_ERR_NONFINITE_STATE : 0);
+      err_row = (errc == 0 && c != 0) ? (int)row : err_row;
+      errc = errc != 0 ? errc : c;
+    }
     Squash q = squash<A>(raw, rp);
     float2 cs;
     float4 cmd = world_cmd<M>(s, q.sq, k.g, cs);
     State n = model_step<M>(s, cmd, rp, k);
     n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;  // q/sensors.py:566
-    if (has_imu)
+    if (IMU == 1)
+      imu_apply_z<M>(cfg, row, n, (n.v - s.v) * (1.f / cfg.dt), k.g, R.ba[a], R.bg[a], v3(z.a.x, z.a.y, z.a.z),
+                     v3(z.a.w, z.b.x, z.b.y), v3(z.b.z, z.b.w, z.c.x), v3(z.c.y, z.c.z, z.c.w), out.imu_out);
+    else if (has_imu)
       imu_apply<M>(cfg, row, N, R.meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g, R.ba[a], R.bg[a], out.imu_noise,
                    out.imu_out);
     const float4 pe = R.peff[a];
@@ -590,6 +627,7 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, i
     any_oob = any_oob || n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x ||
               n.p.y > bhi.y || n.p.z > bhi.z;
   }
+  if (errc != 0) report_err(err, errc, err_row);
   // ---- per-env couplings
   float r_goal = 0.f;
   int next_gate = R.meta.w;
@@ -930,7 +968,7 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
 // on 148 SMs with <= 144 registers per thread
 constexpr int WIN_BLOCK = 64;
 
-template <int M, int TASK, int NAMAX>
+template <int M, int TASK, int NAMAX, int IMU>
 __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg cfg, const qs_scene sc,
                                                     const qs_window_io w) {
   constexpr int A = ModelTraits<M>::A;
@@ -940,7 +978,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   const int na = NAMAX == 1 ? 1 : cfg.n_agents;
   const long N = (long)cfg.n_envs * na;
   const int NP = ModelTraits<M>::NP;
-  const bool has_dr = w.dr != nullptr, has_imu = w.imu_out != nullptr;
+  const bool has_dr = w.dr != nullptr, has_imu = IMU == 1 || w.imu_out != nullptr;
   EnvRegs<NAMAX> R;
   int n_done = 0, n_succ = 0, n_coll = 0;
   float ret_sum = 0.f;
@@ -990,7 +1028,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
                 w.r + (long)t * 3 * N + 2 * N, w.terminated + (long)t * N, w.truncated + (long)t * N,
                 w.flags + (long)t * N, nullptr, has_imu ? w.imu_out + (long)t * N * 6 : nullptr,
                 w.imu_noise ? w.imu_noise + (long)t * 4 * N * 3 : nullptr};
-      StepStat st = env_step_fwd<M, TASK, NAMAX, true>(cfg, sc, e, na, N, R, raw, o, w.err, has_dr, has_imu);
+      StepStat st = env_step_fwd<M, TASK, NAMAX, true, IMU>(cfg, sc, e, na, N, R, raw, o, w.err, has_dr, has_imu);
       if (st.done) {
         n_done++;
         n_succ += st.term == 1;
@@ -1244,8 +1282,11 @@ template <int M, int T, int NA>
 int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_window_io* w, cudaStream_t s) {
   if (w->T <= 0) return QS_OK;
   if (op == 4 && w->loss) cudaMemsetAsync(w->loss, 0, sizeof(double), s);
-  if (op == 4)
-    k_window_fwd<M, T, NA><<<grid_for(cfg->n_envs, WIN_BLOCK), WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+  const dim3 grid(grid_for(cfg->n_envs, WIN_BLOCK));
+  if (op == 4 && NA == 1 && w->imu_out && !w->imu_noise)  // Philox IMU specialisation
+    k_window_fwd<M, T, NA, NA == 1 ? 1 : 0><<<grid, WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+  else if (op == 4)
+    k_window_fwd<M, T, NA, 0><<<grid, WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
   else
     k_window_bwd<M, T, NA><<<grid_for(cfg->n_envs, WIN_BLOCK), WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
   return launch_status();

@@ -311,3 +311,40 @@ def test_avoidance_with_generated_scenes_and_depth_steps(qs):
     assert torch.isfinite(out.r_ctrl).all()
     out.r_ctrl.sum().backward()
     assert torch.isfinite(a.grad).all() and a.grad.abs().sum() > 0
+
+
+PHILOX_KAT = [  # Random123 kat_vectors, philox4x32 10 rounds: ctr[4], key[2] -> out[4]
+    ([0, 0, 0, 0], [0, 0], [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]),
+    ([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2, [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+     [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]),
+]
+
+
+def _philox_py(c, k):
+    M = 0xFFFFFFFF
+    c, k = list(c), list(k)
+    for _ in range(10):
+        p0, p1 = c[0] * 0xD2511F53, c[2] * 0xCD9E8D57
+        c = [(p1 >> 32) ^ c[1] ^ k[0], p1 & M, (p0 >> 32) ^ c[3] ^ k[1], p0 & M]
+        k = [(k[0] + 0x9E3779B9) & M, (k[1] + 0xBB67AE85) & M]
+    return c
+
+
+def test_philox_known_answers(qs):
+    """The generator behind every in-kernel draw, both key-schedule forms,
+    against the published Philox4x32-10 known-answer vectors."""
+    from paper_2509_10247_b200 import _lib as L
+
+    rng = np.random.default_rng(0)
+    items = [c + k for c, k, _ in PHILOX_KAT]
+    items += rng.integers(0, 2**32, size=(61, 6), dtype=np.uint64).tolist()
+    ck = torch.tensor(np.array(items, dtype=np.uint32).view(np.int32), device="cuda")
+    out = torch.empty(len(items), 8, dtype=torch.int32, device="cuda")
+    L.check(L.lib().qs_philox4x32_10(len(items), L.ptr(ck), L.ptr(out), L.stream_handle()), "philox")
+    got = out.cpu().numpy().view(np.uint32)
+    for i, (c, k, want) in enumerate(PHILOX_KAT):
+        assert got[i, :4].tolist() == want and got[i, 4:].tolist() == want
+    for i, it in enumerate(items):
+        want = _philox_py(it[:4], it[4:])
+        assert got[i, :4].tolist() == want and got[i, 4:].tolist() == want
