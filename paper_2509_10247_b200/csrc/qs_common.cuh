@@ -26,15 +26,16 @@ QS_HD V3 cross(V3 a, V3 b) {
 // Euclidean norm.  On device: MUFU sqrt (sqrt.approx, ~1 ulp) instead of the
 // IEEE-rounded sequence; norms feed rewards, SDF and attitude, all checked
 // against the fp64 oracle at 1e-5 relative.
-QS_HD float norm3(V3 a) {
+QS_HD float sqrt_mufu(float x) {
 #ifdef __CUDA_ARCH__
   float d;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(d) : "f"(dot(a, a)));
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(d) : "f"(x));
   return d;
 #else
-  return sqrtf(dot(a, a));
+  return sqrtf(x);
 #endif
 }
+QS_HD float norm3(V3 a) { return sqrt_mufu(dot(a, a)); }
 QS_HD V3& operator+=(V3& a, V3 b) {
   a.x += b.x; a.y += b.y; a.z += b.z;
   return a;
@@ -84,13 +85,31 @@ QS_HD Q4 qrot_vjp_q(Q4 q, V3 v, V3 g) {
   return q4(gw, gu.x, gu.y, gu.z);
 }
 
+// sigmoid / softplus / tanh on the MUFU ex2/lg2/rcp units.  Absolute error
+// <= ~2e-7 (what the 1e-5 state/reward bars see); the saturated tails are
+// exact: sigmoid -> 0/1, tanh -> +-1 (ex2 -> inf/0, fast division of 2/inf -> 0).
 QS_HD float sigmoid_stable(float x) {  // q/autodiff.py:446-456
+#ifdef __CUDA_ARCH__
+  return __fdividef(1.f, 1.f + __expf(-x));
+#else
   if (x >= 0.f) return 1.f / (1.f + expf(-x));
   float e = expf(x);
   return e / (1.f + e);
+#endif
 }
 QS_HD float softplus(float x) {  // logaddexp(0, x)
+#ifdef __CUDA_ARCH__
+  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x)));
+#else
   return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x)));
+#endif
+}
+QS_HD float tanh_fast(float x) {  // 1 - 2 / (e^{2x} + 1)
+#ifdef __CUDA_ARCH__
+  return 1.f - __fdividef(2.f, __expf(2.f * x) + 1.f);
+#else
+  return tanhf(x);
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -357,9 +357,9 @@ QS_D void reward_ctrl_vjp(const qs_weights& w, V3 off, V3 v, float4 eff, float4 
   if (dist >= 1e-9f) g_dist += g_m;                                   // maximum: tie -> first
   g_off += norm_vjp(off, dist, g_dist);
   // effort norms
-  float en = sqrtf(eff.x * eff.x + eff.y * eff.y + eff.z * eff.z + (A == 4 ? eff.w * eff.w : 0.f));
-  float dn = sqrtf(deff.x * deff.x + deff.y * deff.y + deff.z * deff.z +
-                   (A == 4 ? deff.w * deff.w : 0.f));
+  float en = sqrt_mufu(eff.x * eff.x + eff.y * eff.y + eff.z * eff.z + (A == 4 ? eff.w * eff.w : 0.f));
+  float dn = sqrt_mufu(deff.x * deff.x + deff.y * deff.y + deff.z * deff.z +
+                       (A == 4 ? deff.w * deff.w : 0.f));
   float ca = en > 0.f ? gp * w.w_a / en : 0.f;
   float cs = dn > 0.f ? gp * w.w_s / dn : 0.f;
   g_eff = make_float4(eff.x * ca + deff.x * cs, eff.y * ca + deff.y * cs, eff.z * ca + deff.z * cs,
@@ -390,7 +390,7 @@ struct Squash {
 template <int A>
 QS_D Squash squash(float4 raw, const RowPrm& rp) {  // q/dynamics.py:277-284
   Squash s;
-  s.t = make_float4(tanhf(raw.x), tanhf(raw.y), tanhf(raw.z), A == 4 ? tanhf(raw.w) : 0.f);
+  s.t = make_float4(tanh_fast(raw.x), tanh_fast(raw.y), tanh_fast(raw.z), A == 4 ? tanh_fast(raw.w) : 0.f);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (k < A) {
@@ -417,7 +417,7 @@ QS_D float4 world_cmd(const State& s, float4 sq, V3 g, float2& cs) {  // q/tasks
 }
 
 QS_D float effnorm(float4 e, int A) {
-  return sqrtf(e.x * e.x + e.y * e.y + e.z * e.z + (A == 4 ? e.w * e.w : 0.f));
+  return sqrt_mufu(e.x * e.x + e.y * e.y + e.z * e.z + (A == 4 ? e.w * e.w : 0.f));
 }
 
 QS_D void warp_stats(bool active, bool done, int term, float ret, double* stats) {
@@ -892,7 +892,7 @@ QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int n
     float* gout = g_raw_t + row * A;
 #pragma unroll
     for (int kk = 0; kk < A; ++kk) {
-      float t = tanhf(f4get(raw, kk));
+      float t = tanh_fast(f4get(raw, kk));
       gout[kk] = f4get(gsq, kk) * rp.half[kk] * (1.f - t * t);
     }
     gS[a] = gi;
