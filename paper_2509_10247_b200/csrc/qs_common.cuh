@@ -51,7 +51,11 @@ QS_HD bool finite3(V3 a) { return isfinite(a.x) && isfinite(a.y) && isfinite(a.z
 // norm VJP with the reference's convention: zero vector -> zero gradient
 // (q/autodiff.py:580-591)
 QS_HD V3 norm_vjp(V3 a, float n, float g) {
+#ifdef __CUDA_ARCH__
+  return n > 0.f ? a * __fdividef(g, n) : v3(0.f, 0.f, 0.f);  // n is a norm: far below 2^126
+#else
   return n > 0.f ? a * (g / n) : v3(0.f, 0.f, 0.f);
+#endif
 }
 
 struct Q4 {

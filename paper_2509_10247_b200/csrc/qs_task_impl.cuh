@@ -302,7 +302,7 @@ QS_D RewardFwd reward_ctrl(const qs_weights& w, V3 off, V3 v, float effn, float 
   float speed = norm3(v);
   float nearv = sigmoid_stable((w.near_radius - dist) * (1.f / w.near_width));
   float sd = fminf(dist * w.track_gain, w.v_max);
-  V3 vdes = off * (sd / fmaxf(dist, 1e-9f));
+  V3 vdes = off * __fdividef(sd, fmaxf(dist, 1e-9f));
   float track = norm3(v - vdes);
   float pen = dist * w.w_p;
   pen = pen + (speed * nearv) * w.w_v;
@@ -335,7 +335,8 @@ QS_D void reward_ctrl_vjp(const qs_weights& w, V3 off, V3 v, float4 eff, float4 
   float nearv = sigmoid_stable(x);
   float m = fmaxf(dist, 1e-9f);
   float sd = fminf(dist * w.track_gain, w.v_max);
-  float kk = sd / m;
+  const float im = __fdividef(1.f, m);
+  float kk = sd * im;
   V3 vdes = off * kk;
   V3 ev = v - vdes;
   float track = norm3(ev);
@@ -351,8 +352,8 @@ QS_D void reward_ctrl_vjp(const qs_weights& w, V3 off, V3 v, float4 eff, float4 
   V3 g_vdes = -gev;
   g_off = g_vdes * kk;
   float g_k = dot(g_vdes, off);
-  float g_sd = g_k / m;
-  float g_m = -g_k * sd / (m * m);
+  float g_sd = g_k * im;
+  float g_m = -g_k * kk * im;
   if (dist * w.track_gain <= w.v_max) g_dist += g_sd * w.track_gain;  // minimum: tie -> first
   if (dist >= 1e-9f) g_dist += g_m;                                   // maximum: tie -> first
   g_off += norm_vjp(off, dist, g_dist);
@@ -360,8 +361,8 @@ QS_D void reward_ctrl_vjp(const qs_weights& w, V3 off, V3 v, float4 eff, float4 
   float en = sqrt_mufu(eff.x * eff.x + eff.y * eff.y + eff.z * eff.z + (A == 4 ? eff.w * eff.w : 0.f));
   float dn = sqrt_mufu(deff.x * deff.x + deff.y * deff.y + deff.z * deff.z +
                        (A == 4 ? deff.w * deff.w : 0.f));
-  float ca = en > 0.f ? gp * w.w_a / en : 0.f;
-  float cs = dn > 0.f ? gp * w.w_s / dn : 0.f;
+  float ca = en > 0.f ? __fdividef(gp * w.w_a, en) : 0.f;
+  float cs = dn > 0.f ? __fdividef(gp * w.w_s, dn) : 0.f;
   g_eff = make_float4(eff.x * ca + deff.x * cs, eff.y * ca + deff.y * cs, eff.z * ca + deff.z * cs,
                       A == 4 ? eff.w * ca + deff.w * cs : 0.f);
 }
@@ -1113,9 +1114,10 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
     if (a >= na) break;
     s2[a] = load_state<M>(w.S + (long)w.T * NP * N * 4, N, e * na + a);
   }
+  const float lg_gamma = log2f(w.gamma);  // gamma^t = 2^(t lg): one MUFU.EX2 per step
   for (int t = w.T - 1; t >= 0; --t) {
     if (t > 0) load_ck(t - 1, nxt);
-    const float gscale = w.g_rctrl_scale * powf(w.gamma, (float)t);
+    const float gscale = w.g_rctrl_scale * (t == 0 ? 1.f : exp2f((float)t * lg_gamma));
     State s_in[NAMAX];
     float4 goal[NAMAX], peff[NAMAX], dr[NAMAX], raw[NAMAX];
     int fl[NAMAX];
