@@ -89,12 +89,29 @@ QS_HD Q4 qrot_vjp_q(Q4 q, V3 v, V3 g) {
   return q4(gw, gu.x, gu.y, gu.z);
 }
 
+// MUFU ex2 / lg2 / rcp with flush-to-zero: no denormal fix-up sequences
+QS_D float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+QS_D float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+QS_D float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // sigmoid / softplus / tanh on the MUFU ex2/lg2/rcp units.  Absolute error
 // <= ~2e-7 (what the 1e-5 state/reward bars see); the saturated tails are
-// exact: sigmoid -> 0/1, tanh -> +-1 (ex2 -> inf/0, fast division of 2/inf -> 0).
+// exact: sigmoid -> 0/1, tanh -> +-1 (ex2 -> inf/0, rcp(inf) = 0).
 QS_HD float sigmoid_stable(float x) {  // q/autodiff.py:446-456
 #ifdef __CUDA_ARCH__
-  return __fdividef(1.f, 1.f + __expf(-x));
+  return rcp_ftz(1.f + ex2_ftz(-1.44269504f * x));
 #else
   if (x >= 0.f) return 1.f / (1.f + expf(-x));
   float e = expf(x);
@@ -103,14 +120,14 @@ QS_HD float sigmoid_stable(float x) {  // q/autodiff.py:446-456
 }
 QS_HD float softplus(float x) {  // logaddexp(0, x)
 #ifdef __CUDA_ARCH__
-  return fmaxf(x, 0.f) + __logf(1.f + __expf(-fabsf(x)));
+  return fmaxf(x, 0.f) + 0.693147181f * lg2_ftz(1.f + ex2_ftz(-1.44269504f * fabsf(x)));
 #else
   return fmaxf(x, 0.f) + log1pf(expf(-fabsf(x)));
 #endif
 }
 QS_HD float tanh_fast(float x) {  // 1 - 2 / (e^{2x} + 1)
 #ifdef __CUDA_ARCH__
-  return 1.f - __fdividef(2.f, __expf(2.f * x) + 1.f);
+  return 1.f - 2.f * rcp_ftz(ex2_ftz(2.88539008f * x) + 1.f);
 #else
   return tanhf(x);
 #endif
@@ -161,25 +178,29 @@ inline void philox_round_keys(uint64_t seed, uint32_t* rk) {
   }
 }
 
-// 32 random bits -> uniform in (0, 1): 23 mantissa bits in [1, 2), shifted by
-// 1 - 2^-24 (exact by Sterbenz), so the result lies in [2^-24, 1 - 2^-24]
-QS_D float u01(uint32_t r) { return __uint_as_float((r >> 9) | 0x3f800000u) - 0.99999994f; }
+// 32 random bits -> uniform in (0, 1): the low 23 bits as the mantissa of
+// v in [1, 2) (one LOP3), shifted by 1 - 2^-24 (exact by Sterbenz), so the
+// result lies in [2^-24, 1 - 2^-24]
+QS_D float u12(uint32_t r) { return __uint_as_float((r & 0x007fffffu) | 0x3f800000u); }
+QS_D float u01(uint32_t r) { return u12(r) - 0.99999994f; }
 
 QS_D float4 u01x4(uint4 r) { return make_float4(u01(r.x), u01(r.y), u01(r.z), u01(r.w)); }
 
-// four standard normals (Box-Muller on two pairs).  MUFU intrinsics: the
-// ~2-ulp error of lg2/sqrt/sin/cos is immaterial for sampling noise.
-QS_D float4 box_muller4(float4 u) {
+// four standard normals from 128 random bits (Box-Muller on two pairs):
+// radius from 2 - v in (0, 1] (|z| <= 5.6), angle from v in [1, 2) directly
+// (sin/cos of 2 pi v are 1-periodic).  MUFU lg2/sqrt/sin/cos: their ~2-ulp
+// error is immaterial for sampling noise.
+QS_D float4 box_muller4(uint4 r) {
   float d0, d1;
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(-2.f * __logf(u.x)));
-  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(-2.f * __logf(u.z)));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d0) : "f"(-1.38629436f * lg2_ftz(2.f - u12(r.x))));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d1) : "f"(-1.38629436f * lg2_ftz(2.f - u12(r.z))));
   float s0, c0, s1, c1;
-  __sincosf(6.28318530717958648f * u.y, &s0, &c0);
-  __sincosf(6.28318530717958648f * u.w, &s1, &c1);
+  __sincosf(6.28318530717958648f * u12(r.y), &s0, &c0);
+  __sincosf(6.28318530717958648f * u12(r.w), &s1, &c1);
   return make_float4(d0 * c0, d0 * s0, d1 * c1, d1 * s1);
 }
 
-// purposes (counter word 2, high byte)
+// purposes (counter word 3, high byte)
 enum : uint32_t {
   RNG_SPAWN = 1u,
   RNG_DR = 2u,
@@ -200,7 +221,11 @@ struct Rng {
     ctr.w++;
     return u01x4(r);
   }
-  QS_D float4 normal4() { return box_muller4(uniform4()); }
+  QS_D float4 normal4() {
+    uint4 r = philox4x32_10(ctr, key);
+    ctr.w++;
+    return box_muller4(r);
+  }
 };
 
 // Rng with the round keys precomputed (the task kernels: cfg.rng_round_keys);
@@ -216,7 +241,11 @@ struct RngK {
     ctr.w++;
     return u01x4(r);
   }
-  QS_D float4 normal4() { return box_muller4(uniform4()); }
+  QS_D float4 normal4() {
+    uint4 r = philox4x32_10_rk(ctr, rk);
+    ctr.w++;
+    return box_muller4(r);
+  }
 };
 
 // ---------------------------------------------------------------------------

@@ -317,8 +317,7 @@ QS_D RewardFwd reward_ctrl(const qs_weights& w, V3 off, V3 v, float effn, float 
 QS_D float reward_rl(const qs_weights& w, float clip, V3 off, V3 v, float effn, float deffn) {
   float dist = norm3(off);
   float speed = norm3(v);
-  float nearv = __fdividef(1.f, 1.f + __expf(__fdividef(-(w.near_radius - dist), w.near_width)));
-  if (!(nearv == nearv)) nearv = 0.f;  // exp overflow -> 1/inf = 0 (matches the reference)
+  float nearv = sigmoid_stable((w.near_radius - dist) * (1.f / w.near_width));  // exp overflow -> 0
   float sd = fminf(dist * w.track_gain, w.v_max);
   V3 vdes = off * __fdividef(sd, fmaxf(dist, 1e-9f));
   float track = norm3(v - vdes);
@@ -991,6 +990,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   // and costs no registers.  Partial tail CTAs load directly.
   __shared__ __align__(128) float s_raw[2][WIN_BLOCK * NAMAX * 4];
   __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ int s_free[2];  // warps done with each buffer this round
   const long e0 = (long)blockIdx.x * blockDim.x;
   const uint32_t blk_bytes = (uint32_t)(blockDim.x * na * A * 4);
   const bool use_tma = (e0 + blockDim.x <= cfg.n_envs) && (blk_bytes % 16 == 0) && ((N * A) % 4 == 0) &&
@@ -998,6 +998,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   if (use_tma && threadIdx.x == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
+    s_free[0] = s_free[1] = 0;
     fence_barrier_init();
   }
   __syncthreads();
@@ -1042,9 +1043,20 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
                                w.peff + (long)(t + 1) * N * 4, has_dr ? w.dr + (long)(t + 1) * N * 4 : nullptr);
     }
     if (use_tma) {
-      __syncthreads();  // every thread has consumed buffer t&1: refill it with step t+2
-      if (threadIdx.x == 0 && t + 2 < w.T)
-        tma_load_1d(s_raw[t & 1], w.actions + ((long)(t + 2) * N + e0 * na) * A, blk_bytes, &s_bar[t & 1]);
+      // No CTA barrier: the last warp to finish with buffer t&1 (its lanes'
+      // actions have fed this step) refills it with step t+2, so warps drift
+      // freely by up to a step instead of meeting every step.
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();
+        if (atomicAdd(&s_free[t & 1], 1) == (int)(blockDim.x >> 5) - 1) {
+          atomicExch(&s_free[t & 1], 0);
+          if (t + 2 < w.T) {
+            fence_proxy_async();
+            tma_load_1d(s_raw[t & 1], w.actions + ((long)(t + 2) * N + e0 * na) * A, blk_bytes, &s_bar[t & 1]);
+          }
+        }
+      }
     }
   }
   if (active) env_store_inplace<NAMAX>(e, na, R, w.meta, w.ep_return, has_imu ? w.imu_bias : nullptr);
