@@ -29,7 +29,7 @@ QS_HD V3 cross(V3 a, V3 b) {
 QS_HD float sqrt_mufu(float x) {
 #ifdef __CUDA_ARCH__
   float d;
-  asm("sqrt.approx.f32 %0, %1;" : "=f"(d) : "f"(x));
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(x));  // denormal inputs flush to 0
   return d;
 #else
   return sqrtf(x);

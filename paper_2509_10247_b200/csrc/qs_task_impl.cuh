@@ -988,23 +988,25 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   // is staged in shared memory by a TMA bulk copy issued one step ahead into a
   // double buffer, so the action latency never sits on the step's critical path
   // and costs no registers.  Partial tail CTAs load directly.
-  __shared__ __align__(128) float s_raw[2][WIN_BLOCK * NAMAX * 4];
-  __shared__ __align__(8) uint64_t s_bar[2];
-  __shared__ int s_free[2];  // warps done with each buffer this round
+  constexpr int NB = NAMAX == 1 ? 4 : 2;  // ring depth: step t+NB is in flight during step t
+  __shared__ __align__(128) float s_raw[NB][WIN_BLOCK * NAMAX * 4];
+  __shared__ __align__(8) uint64_t s_bar[NB];
+  __shared__ int s_free[NB];  // warps done with each buffer this round
   const long e0 = (long)blockIdx.x * blockDim.x;
   const uint32_t blk_bytes = (uint32_t)(blockDim.x * na * A * 4);
   const bool use_tma = (e0 + blockDim.x <= cfg.n_envs) && (blk_bytes % 16 == 0) && ((N * A) % 4 == 0) &&
                        ((reinterpret_cast<uintptr_t>(w.actions) & 15) == 0);
   if (use_tma && threadIdx.x == 0) {
-    mbar_init(&s_bar[0], 1);
-    mbar_init(&s_bar[1], 1);
-    s_free[0] = s_free[1] = 0;
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(&s_bar[b], 1);
+      s_free[b] = 0;
+    }
     fence_barrier_init();
   }
   __syncthreads();
   if (use_tma && threadIdx.x == 0) {
-    tma_load_1d(s_raw[0], w.actions + e0 * na * A, blk_bytes, &s_bar[0]);
-    if (w.T > 1) tma_load_1d(s_raw[1], w.actions + (N + e0 * na) * A, blk_bytes, &s_bar[1]);
+    for (int b = 0; b < NB && b < w.T; ++b)
+      tma_load_1d(s_raw[b], w.actions + ((long)b * N + e0 * na) * A, blk_bytes, &s_bar[b]);
   }
   if (active)
     env_load<M, NAMAX>(cfg, sc.bounds, e, na, N, R, w.S, w.goal, w.peff, w.dr, w.meta, w.ep_return,
@@ -1012,8 +1014,8 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   for (int t = 0; t < w.T; ++t) {
     float4 raw[NAMAX];
     if (use_tma) {
-      mbar_wait(&s_bar[t & 1], (t >> 1) & 1);
-      const float* sr = s_raw[t & 1];
+      mbar_wait(&s_bar[t % NB], (t / NB) & 1);
+      const float* sr = s_raw[t % NB];
 #pragma unroll
       for (int a = 0; a < NAMAX; ++a) {
         if (a >= na) break;
@@ -1049,11 +1051,12 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
       __syncwarp();
       if ((threadIdx.x & 31) == 0) {
         __threadfence_block();
-        if (atomicAdd(&s_free[t & 1], 1) == (int)(blockDim.x >> 5) - 1) {
-          atomicExch(&s_free[t & 1], 0);
-          if (t + 2 < w.T) {
+        if (atomicAdd(&s_free[t % NB], 1) == (int)(blockDim.x >> 5) - 1) {
+          atomicExch(&s_free[t % NB], 0);
+          if (t + NB < w.T) {
             fence_proxy_async();
-            tma_load_1d(s_raw[t & 1], w.actions + ((long)(t + 2) * N + e0 * na) * A, blk_bytes, &s_bar[t & 1]);
+            tma_load_1d(s_raw[t % NB], w.actions + ((long)(t + NB) * N + e0 * na) * A, blk_bytes,
+                        &s_bar[t % NB]);
           }
         }
       }
