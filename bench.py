@@ -287,6 +287,98 @@ def bench_depth(dev, rank, world=1, frames=20):
             "lidar_360x16": {"rays_per_s": E * lidar.n_rays / (ms_lidar * 1e-3), "ms_per_frame": ms_lidar}}
 
 
+def measure_fp32_peak(dev):
+    """FFMA and FFMA2 throughput on this GPU (qs_probe_fp32): the measured FP32
+    denominator BASELINE.md §3 asks for.  Full occupancy (8 x 256 threads per
+    SM), 8 independent chains per thread, best of 5 launches."""
+    import torch
+
+    from paper_2509_10247_b200 import _lib as L
+
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    blocks, iters = sms * 8, 4096
+    out = torch.zeros(blocks, device=dev)
+    res = {}
+    for mode, name in ((0, "ffma"), (1, "ffma2")):
+        best = None
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            L.check(L.lib().qs_probe_fp32(mode, blocks, iters, L.ptr(out), L.stream_handle(dev)), "probe")
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        flops = blocks * 256 * iters * 16 * 8 * 2 * (2 if mode else 1)
+        res[name + "_tflops"] = flops / (best * 1e-3) / 1e12
+    return res
+
+
+def bench_c1(dev):
+    """C1: pm_continuous / pm_discrete position task, 1,024 envs.
+    The 0.4 MB working set makes it latency-bound, so it reports microseconds:
+    (i) one `env.step` forward through the public API, (ii) the T=32 open-loop
+    BPTT window L = -(1/32) sum_t 0.99^t mean(r_ctrl_t) fwd+bwd as one graph
+    replay, (iii) the same loss through `env.step` + torch.autograd."""
+    import torch
+
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.window import BpttWindow
+
+    out = {}
+    raw = np.random.default_rng(0).normal(size=(32, 1024, 3)) * 0.3
+    for model in ("pm_continuous", "pm_discrete"):
+        cfg = qs.TaskConfig(task="position", dynamics=model, n_envs=1024, episode_len=10 ** 6)
+        env = qs.make_task(cfg, device=dev, strict=False)
+        env.reset(seed=1)
+        acts = torch.as_tensor(raw, dtype=torch.float32, device=dev)
+        for t in range(8):
+            env.step(acts[t])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(200):
+            env.step(acts[t % 32])
+        e1.record()
+        torch.cuda.synchronize()
+        step_us = e0.elapsed_time(e1) / 200 * 1e3
+        env.reset(seed=1)
+        win = BpttWindow(env, 32)
+        win.actions.copy_(acts)
+        win.capture()
+        for _ in range(5):
+            win.run()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(100):
+            win.run()
+        e1.record()
+        torch.cuda.synchronize()
+        win_us = e0.elapsed_time(e1) / 100 * 1e3
+        env.reset(seed=1)
+
+        def autograd_window():
+            a_ = acts.clone().requires_grad_(True)
+            env.detach_states()
+            tot = 0.0
+            for t in range(32):
+                tot = tot + env.step(a_[t]).r_ctrl.mean() * 0.99 ** t
+            (-tot / 32).backward()
+            return a_.grad
+
+        autograd_window()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            autograd_window()
+        e1.record()
+        torch.cuda.synchronize()
+        ag_us = e0.elapsed_time(e1) / 5 * 1e3
+        out[model] = {"env_step_fwd_us": step_us, "bptt_window_fwd_bwd_us": win_us,
+                      "bptt_window_autograd_us": ag_us}
+    return out
+
+
 def run_ours(a):
     import torch
 
@@ -431,10 +523,15 @@ def run_ours(a):
     depth = None
     if not a.no_depth:
         depth = bench_depth(dev, rank, world)
-        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
-        depth["fp32_peak_tflops"] = round(fp32_peak, 1)
-        depth["fp32_peak_source"] = "computed 148 SM x 128 FMA lanes x 2 x 1.965 GHz (not in MEASURED_PEAKS.json)"
+        probe = measure_fp32_peak(dev)
+        fp32_peak = probe["ffma_tflops"]
+        depth["fp32_peak_tflops"] = fp32_peak
+        depth["fp32_peak_source"] = ("measured here: FFMA probe (qs_probe_fp32), full occupancy; nominal "
+                                     "148 SM x 128 x 2 x 1.965 GHz = 74.4")
+        depth["ffma2_tflops_measured"] = probe["ffma2_tflops"]
         depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / (fp32_peak * world)
+
+    c1 = bench_c1(dev) if rank == 0 and not a.no_depth else None
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -471,6 +568,7 @@ def run_ours(a):
         "clocks": getattr(clk, "result", None),
         "cpu_baseline": cpu,
         "depth": depth,
+        "c1_latency": c1,
         "loss": loss,
     }
     print(json.dumps(line))

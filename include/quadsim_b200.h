@@ -262,6 +262,12 @@ int qs_reconstruct_attitude(int32_t n, const float* a, const float* v_ema, float
  * schedule on the fly, then with precomputed round keys (the two must agree). */
 int qs_philox4x32_10(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream);
 
+/* Measurement aid (not part of the reference API): FP32 peak probe for the
+ * ray-casting roofline.  n_blocks CTAs of 256 threads, each thread 8 independent
+ * FMA chains x 16 x iters; mode 0 = FFMA, mode 1 = packed fma.rn.f32x2 (FFMA2).
+ * FLOPs per launch = n_blocks * 256 * iters * 256 (mode 0), twice that (mode 1). */
+int qs_probe_fp32(int32_t mode, int32_t n_blocks, int32_t iters, float* out, void* stream);
+
 /* In-kernel obstacle-course generation with BFS feasibility
  * (q/world.py:207-340), Philox keyed by (seed, global env id, attempt). */
 typedef struct qs_gen_cfg {
