@@ -221,10 +221,12 @@ typedef struct qs_ray_cfg {
 int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
                int32_t pos_stride, const float* cam_cs, const float* dirs_body,
                const float* dirs_world, float* out, uint8_t* hit, float* dT_dO, void* stream);
-/* Same images as qs_raycast (kinds 0/1) with per-warp cone culling: rays are
+/* Same images as qs_raycast (kinds 0/1) with per-warp culling: rays are
  * grouped into n_tiles tiles of 32 (tile_rays (n_tiles,32) ray indices, -1 =
- * empty slot), each with a body-frame bounding cone tile_cones (n_tiles,8) =
- * unit axis xyz, cos(half-angle), sin(half-angle), 3 pad. */
+ * empty slot), each with a body-frame bounding cone and azimuth sector,
+ * tile_cones (n_tiles,12) = unit axis xyz, cos(half-angle), sin(half-angle),
+ * unit horizontal sector centre xy, cos(sector half-width) (< -1.5: no sector
+ * test), sin(sector half-width), 3 pad. */
 int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
                      int32_t pos_stride, const float* cam_cs, const float* dirs_body,
                      const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, float* out,

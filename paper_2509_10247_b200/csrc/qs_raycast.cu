@@ -280,7 +280,24 @@ QS_D bool cone_keeps(float4 b, float2 e, V3 ax, float cth, float sth) {
   if (b.w < 0.f) return true;
   return dot(xyz(b), ax) >= cth * b.w - sth * e.x - e.y;
 }
-QS_D float rcp_fast(float x) { return __fdividef(1.f, x); }  // MUFU.RCP; 1/(+-0) = +-inf
+QS_D float rcp_fast(float x) {  // one MUFU.RCP; 1/(+-0) = +-inf, 1/(+-inf) = +-0
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// horizontal footprint record (u2 = (c - o).xy, Q2 = tangent length, r2 = the
+// footprint circle's radius; Q2 = -1: o is inside it) and its keep test against
+// the tile's azimuth sector (world centre az, cos/sin of the half-width; cw < -1.5
+// keeps everything).  Every ray that hits the obstacle passes through its
+// footprint, so the sector test only drops obstacles no ray of the tile can hit.
+QS_D float4 footprint(V3 u, float r2) {
+  float L2 = u.x * u.x + u.y * u.y;
+  return make_float4(u.x, u.y, L2 <= r2 * r2 ? -1.f : sqrtf(L2 - r2 * r2), r2);
+}
+QS_D bool sector_keeps(float4 h, float slack, float2 az, float cw, float sw) {
+  if (h.z < 0.f || cw < -1.5f) return true;
+  return h.x * az.x + h.y * az.y >= cw * h.z - sw * h.w - slack;
+}
 
 template <int KIND>
 __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
@@ -297,21 +314,24 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
   const float* pp = pos + row * pos_stride;
   V3 o = v3(pp[0], pp[1], pp[2]) + rotz(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
   SceneView sv = scene_view(sc, e);
-  // layout: records then bounding spheres (centre relative to o, radius)
+  // layout: intersection records per kind; bounding records staged per kind
+  // (fixed offsets), then compacted into one list (spheres, boxes, cylinders)
+  // so a single ballot per 32 obstacles culls all kinds at once
+  const int cap = sc.Sm + sc.Bm + sc.Cm;
   float4* s_sph = sm;
   float4* s_box = s_sph + sc.Sm;
   float4* s_cyl = s_box + 2 * sc.Bm;
   float* s_cyl_hh = reinterpret_cast<float*>(s_cyl + sc.Cm);
-  float4* b_sph = reinterpret_cast<float4*>(s_cyl_hh + ((sc.Cm + 3) & ~3));
-  float4* b_box = b_sph + sc.Sm;
-  float4* b_cyl = b_box + sc.Bm;
-  float2* e_sph = reinterpret_cast<float2*>(b_cyl + sc.Cm);
-  float2* e_box = e_sph + sc.Sm;
-  float2* e_cyl = e_box + sc.Bm;
+  float4* b_fix = reinterpret_cast<float4*>(s_cyl_hh + ((sc.Cm + 3) & ~3));
+  float4* h_fix = b_fix + cap;
+  float4* b_all = h_fix + cap;
+  float4* h_all = b_all + cap;
+  float2* e_fix = reinterpret_cast<float2*>(h_all + cap);
+  float2* e_all = e_fix + cap;
   if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
   __syncthreads();
-  const int tot = sv.ns + sv.nb + sv.nc;
-  for (int i = threadIdx.x; i < tot; i += blockDim.x) {
+  const int tot_in = sv.ns + sv.nb + sv.nc;
+  for (int i = threadIdx.x; i < tot_in; i += blockDim.x) {
     if (i < sv.ns) {
       float4 s = ld4(sv.sph, i);
       V3 c = xyz(s);
@@ -319,7 +339,8 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
       if (keep) {
         int k = atomicAdd(&cnt[0], 1);
         s_sph[k] = f4(o - c, s.w * s.w);
-        b_sph[k] = bsphere(c - o, s.w, e_sph[k]);
+        b_fix[k] = bsphere(c - o, s.w, e_fix[k]);
+        h_fix[k] = footprint(c - o, s.w);
       }
     } else if (i < sv.ns + sv.nb) {
       int j = i - sv.ns;
@@ -331,7 +352,8 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
         int k = atomicAdd(&cnt[1], 1);
         s_box[2 * k] = f4(xyz(c) - xyz(h) - o, 0.f);
         s_box[2 * k + 1] = f4(xyz(c) + xyz(h) - o, 0.f);
-        b_box[k] = bsphere(xyz(c) - o, rad, e_box[k]);
+        b_fix[sc.Sm + k] = bsphere(xyz(c) - o, rad, e_fix[sc.Sm + k]);
+        h_fix[sc.Sm + k] = footprint(xyz(c) - o, sqrtf(h.x * h.x + h.y * h.y));
       }
     } else {
       int j = i - sv.ns - sv.nb;
@@ -344,21 +366,33 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
         int k = atomicAdd(&cnt[2], 1);
         s_cyl[k] = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
         s_cyl_hh[k] = hh;
-        b_cyl[k] = bsphere(xyz(c) - o, rad, e_cyl[k]);
+        b_fix[sc.Sm + sc.Bm + k] = bsphere(xyz(c) - o, rad, e_fix[sc.Sm + sc.Bm + k]);
+        h_fix[sc.Sm + sc.Bm + k] = footprint(xyz(c) - o, c.w);
       }
     }
   }
   __syncthreads();
   const int ns = cnt[0], nb = cnt[1], nc = cnt[2];
+  const int tot = ns + nb + nc;
+  for (int j = threadIdx.x; j < tot; j += blockDim.x) {
+    const int src = j < ns ? j : (j < ns + nb ? sc.Sm + (j - ns) : sc.Sm + sc.Bm + (j - ns - nb));
+    b_all[j] = b_fix[src];
+    h_all[j] = h_fix[src];
+    e_all[j] = e_fix[src];
+  }
+  __syncthreads();
   const bool ground = sv.ground;
   const float gdz = sv.gz - o.z;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
-    const float4 cone = ld4(tile_cones, 2 * tile);  // axis (body), cos(half-angle)
-    const float sth = __ldg(tile_cones + 8 * tile + 4);
-    const V3 ax = rotz(cs, xyz(cone));
-    const float cth = cone.w;
+    // tile record (12 floats): cone axis xyz, cos, sin | azimuth centre xy, cos, sin of the sector
+    const float4 c0 = ld4(tile_cones, 3 * tile), c1 = ld4(tile_cones, 3 * tile + 1);
+    const float sw = __ldg(tile_cones + 12 * tile + 8);
+    const V3 ax = rotz(cs, xyz(c0));
+    const float cth = c0.w, sth = c1.x;
+    const float2 azw = make_float2(cs.x * c1.y - cs.y * c1.z, cs.y * c1.y + cs.x * c1.z);
+    const float cw = c1.w;
     const int ray = __ldg(tile_rays + tile * 32 + lane);
     V3 d = v3(1.f, 0.f, 0.f);
     if (ray >= 0) d = rotz(cs, xyz(ld4(dirs_body, ray)));
@@ -366,31 +400,26 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
     const float a = d.x * d.x + d.y * d.y;
     const float inv_a = rcp_fast(a);
     float best = INF;
-    for (int base = 0; base < ns; base += 32) {
-      unsigned m = __ballot_sync(0xffffffffu, base + lane < ns &&
-                                                  cone_keeps(b_sph[base + lane], e_sph[base + lane], ax, cth, sth));
-      while (m) {
-        int i = base + __ffs(m) - 1;
-        m &= m - 1;
-        best = fminf(best, hit_sphere(s_sph[i], d));
+    for (int base = 0; base < tot; base += 32) {
+      const int j = base + lane;
+      bool keep = false;
+      if (j < tot) {
+        const float2 ej = e_all[j];
+        keep = cone_keeps(b_all[j], ej, ax, cth, sth) && sector_keeps(h_all[j], ej.y, azw, cw, sw);
       }
-    }
-    for (int base = 0; base < nb; base += 32) {
-      unsigned m = __ballot_sync(0xffffffffu, base + lane < nb &&
-                                                  cone_keeps(b_box[base + lane], e_box[base + lane], ax, cth, sth));
-      while (m) {
-        int i = base + __ffs(m) - 1;
+      unsigned m = __ballot_sync(0xffffffffu, keep);
+      while (m) {  // warp-uniform candidate kinds: no divergence
+        const int i = base + __ffs(m) - 1;
         m &= m - 1;
-        best = fminf(best, hit_box(s_box[2 * i], s_box[2 * i + 1], inv, nullptr));
-      }
-    }
-    for (int base = 0; base < nc; base += 32) {
-      unsigned m = __ballot_sync(0xffffffffu, base + lane < nc &&
-                                                  cone_keeps(b_cyl[base + lane], e_cyl[base + lane], ax, cth, sth));
-      while (m) {
-        int i = base + __ffs(m) - 1;
-        m &= m - 1;
-        best = fminf(best, hit_cyl(s_cyl[i], s_cyl_hh[i], d, a, inv_a, inv.z, nullptr));
+        if (i < ns) {
+          best = fminf(best, hit_sphere(s_sph[i], d));
+        } else if (i < ns + nb) {
+          const int k = i - ns;
+          best = fminf(best, hit_box(s_box[2 * k], s_box[2 * k + 1], inv, nullptr));
+        } else {
+          const int k = i - ns - nb;
+          best = fminf(best, hit_cyl(s_cyl[k], s_cyl_hh[k], d, a, inv_a, inv.z, nullptr));
+        }
       }
     }
     if (ground) {
@@ -468,7 +497,7 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
   size_t smem = (size_t)(scene->Sm + 2 * scene->Bm + scene->Cm) * 16 + ((scene->Cm + 3) & ~3) * 4 +
-                (size_t)(scene->Sm + scene->Bm + scene->Cm) * (16 + 8);
+                (size_t)(scene->Sm + scene->Bm + scene->Cm) * (4 * 16 + 2 * 8);
   cudaStream_t s = (cudaStream_t)stream;
   if (cfg->kind == 0)
     k_raycast_tiled<0><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,

@@ -283,7 +283,8 @@ def _tile_table(sensor, device):
         d = sensor.ray_dirs()
         tiles = [list(range(s, min(len(d), s + 32))) for s in range(0, len(d), 32)]
     rays = np.full((len(tiles), 32), -1, dtype=np.int32)
-    cones = np.zeros((len(tiles), 8))  # axis xyz, cos(half-angle), sin(half-angle), pad
+    # axis xyz, cos/sin(half-angle) | sector centre xy, cos/sin(sector half-width) | pad
+    cones = np.zeros((len(tiles), 12))
     for k, t in enumerate(tiles):
         rays[k, :len(t)] = t
         v = d[t]
@@ -295,6 +296,24 @@ def _tile_table(sensor, device):
         cones[k, :3] = ax
         cones[k, 3] = np.cos(th)
         cones[k, 4] = np.sin(th)
+        # azimuth sector of the tile's rays (a yaw-only camera keeps it a
+        # sector in the world frame); exactly vertical rays have no azimuth and
+        # can only hit footprints containing the origin, which are always kept
+        hxy = v[:, :2]
+        hn = np.linalg.norm(hxy, axis=1)
+        hxy = hxy[hn > 1e-12] / hn[hn > 1e-12, None]
+        cen = hxy.sum(0) if len(hxy) else np.array([1.0, 0.0])
+        cn = np.linalg.norm(cen)
+        w = np.pi
+        if cn > 1e-9:
+            cen = cen / cn
+            w = float(np.arccos(np.clip(np.min(hxy @ cen), -1.0, 1.0))) + 1e-6 if len(hxy) else 0.0
+        cones[k, 5:7] = cen
+        if w <= np.pi / 2:  # the tangent-sector test needs half-width + footprint angle <= pi
+            cones[k, 7] = np.cos(w)
+            cones[k, 8] = np.sin(w)
+        else:
+            cones[k, 7] = -2.0
     out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device))
     _TILE_CACHE[key] = out
     return out
