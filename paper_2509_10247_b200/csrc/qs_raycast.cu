@@ -299,8 +299,10 @@ QS_D bool sector_keeps(float4 h, float slack, float2 az, float cw, float sw) {
   return h.x * az.x + h.y * az.y >= cw * h.z - sw * h.w - slack;
 }
 
+constexpr int TILED_BLOCK = 128;
+
 template <int KIND>
-__global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
+__global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
     const float* __restrict__ cam_cs, const float* __restrict__ dirs_body, const int* __restrict__ tile_rays,
     const float* __restrict__ tile_cones, int n_tiles, int tiles_per_cta, float* __restrict__ out,
@@ -314,76 +316,79 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
   const float* pp = pos + row * pos_stride;
   V3 o = v3(pp[0], pp[1], pp[2]) + rotz(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
   SceneView sv = scene_view(sc, e);
-  // layout: intersection records per kind; bounding records staged per kind
-  // (fixed offsets), then compacted into one list (spheres, boxes, cylinders)
-  // so a single ballot per 32 obstacles culls all kinds at once
+  // One list of kept obstacles in input order (spheres, boxes, cylinders, so
+  // the list stays kind-sorted), each with two intersection records
+  //   sphere (o - c, r^2) | box (lo - o), (hi - o) | cylinder (o - c, r^2), (hh)
+  // plus its bounding sphere, horizontal footprint and slack.  Warp 0 builds it
+  // with ballot compaction (no atomics, one CTA barrier); a single ballot per 32
+  // entries then culls every kind at once for a tile.
   const int cap = sc.Sm + sc.Bm + sc.Cm;
-  float4* s_sph = sm;
-  float4* s_box = s_sph + sc.Sm;
-  float4* s_cyl = s_box + 2 * sc.Bm;
-  float* s_cyl_hh = reinterpret_cast<float*>(s_cyl + sc.Cm);
-  float4* b_fix = reinterpret_cast<float4*>(s_cyl_hh + ((sc.Cm + 3) & ~3));
-  float4* h_fix = b_fix + cap;
-  float4* b_all = h_fix + cap;
+  float4* r0 = sm;
+  float4* r1 = r0 + cap;
+  float4* b_all = r1 + cap;
   float4* h_all = b_all + cap;
-  float2* e_fix = reinterpret_cast<float2*>(h_all + cap);
-  float2* e_all = e_fix + cap;
-  if (threadIdx.x < 3) cnt[threadIdx.x] = 0;
-  __syncthreads();
-  const int tot_in = sv.ns + sv.nb + sv.nc;
-  for (int i = threadIdx.x; i < tot_in; i += blockDim.x) {
-    if (i < sv.ns) {
-      float4 s = ld4(sv.sph, i);
-      V3 c = xyz(s);
-      bool keep = !rc.cull || (KIND == 0 ? keep_camera(rc, cs, o, c, s.w) : keep_ball(rc, o, c, s.w));
-      if (keep) {
-        int k = atomicAdd(&cnt[0], 1);
-        s_sph[k] = f4(o - c, s.w * s.w);
-        b_fix[k] = bsphere(c - o, s.w, e_fix[k]);
-        h_fix[k] = footprint(c - o, s.w);
+  float2* e_all = reinterpret_cast<float2*>(h_all + cap);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (warp == 0) {
+    const int tot_in = sv.ns + sv.nb + sv.nc;
+    int run = 0, ks = 0, kb = 0;
+    for (int c0 = 0; c0 < tot_in; c0 += 32) {
+      const int i = c0 + lane;
+      bool keep = false;
+      float4 q0, q1, bs, fp;
+      float2 ee;
+      if (i < sv.ns) {
+        float4 sp = ld4(sv.sph, i);
+        V3 c = xyz(sp);
+        keep = !rc.cull || keep_ball(rc, o, c, sp.w);
+        q0 = f4(o - c, sp.w * sp.w);
+        q1 = make_float4(0.f, 0.f, 0.f, 0.f);
+        bs = bsphere(c - o, sp.w, ee);
+        fp = footprint(c - o, sp.w);
+      } else if (i < sv.ns + sv.nb) {
+        int j = i - sv.ns;
+        float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
+        float rad = norm3(xyz(h));
+        keep = !rc.cull || keep_ball(rc, o, xyz(c), rad);
+        q0 = f4(xyz(c) - xyz(h) - o, 0.f);
+        q1 = f4(xyz(c) + xyz(h) - o, 0.f);
+        bs = bsphere(xyz(c) - o, rad, ee);
+        fp = footprint(xyz(c) - o, sqrtf(h.x * h.x + h.y * h.y));
+      } else if (i < tot_in) {
+        int j = i - sv.ns - sv.nb;
+        float4 c = ld4(sv.cyl, 2 * j);
+        float hh = __ldg(sv.cyl + 8 * j + 4);
+        float rad = sqrtf(c.w * c.w + hh * hh);
+        keep = !rc.cull || keep_ball(rc, o, xyz(c), rad);
+        q0 = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
+        q1 = make_float4(hh, 0.f, 0.f, 0.f);
+        bs = bsphere(xyz(c) - o, rad, ee);
+        fp = footprint(xyz(c) - o, c.w);
       }
-    } else if (i < sv.ns + sv.nb) {
-      int j = i - sv.ns;
-      float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
-      float rad = norm3(xyz(h));
-      bool keep = !rc.cull ||
-                  (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
-        int k = atomicAdd(&cnt[1], 1);
-        s_box[2 * k] = f4(xyz(c) - xyz(h) - o, 0.f);
-        s_box[2 * k + 1] = f4(xyz(c) + xyz(h) - o, 0.f);
-        b_fix[sc.Sm + k] = bsphere(xyz(c) - o, rad, e_fix[sc.Sm + k]);
-        h_fix[sc.Sm + k] = footprint(xyz(c) - o, sqrtf(h.x * h.x + h.y * h.y));
+        const int p = run + __popc(m & ((1u << lane) - 1u));
+        r0[p] = q0;
+        r1[p] = q1;
+        b_all[p] = bs;
+        h_all[p] = fp;
+        e_all[p] = ee;
       }
-    } else {
-      int j = i - sv.ns - sv.nb;
-      float4 c = ld4(sv.cyl, 2 * j);
-      float hh = __ldg(sv.cyl + 8 * j + 4);
-      float rad = sqrtf(c.w * c.w + hh * hh);
-      bool keep = !rc.cull ||
-                  (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
-      if (keep) {
-        int k = atomicAdd(&cnt[2], 1);
-        s_cyl[k] = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
-        s_cyl_hh[k] = hh;
-        b_fix[sc.Sm + sc.Bm + k] = bsphere(xyz(c) - o, rad, e_fix[sc.Sm + sc.Bm + k]);
-        h_fix[sc.Sm + sc.Bm + k] = footprint(xyz(c) - o, c.w);
-      }
+      run += __popc(m);
+      ks += __popc(__ballot_sync(0xffffffffu, keep && i < sv.ns));
+      kb += __popc(__ballot_sync(0xffffffffu, keep && i >= sv.ns && i < sv.ns + sv.nb));
+    }
+    if (lane == 0) {
+      cnt[0] = ks;
+      cnt[1] = kb;
+      cnt[2] = run - ks - kb;
     }
   }
   __syncthreads();
   const int ns = cnt[0], nb = cnt[1], nc = cnt[2];
   const int tot = ns + nb + nc;
-  for (int j = threadIdx.x; j < tot; j += blockDim.x) {
-    const int src = j < ns ? j : (j < ns + nb ? sc.Sm + (j - ns) : sc.Sm + sc.Bm + (j - ns - nb));
-    b_all[j] = b_fix[src];
-    h_all[j] = h_fix[src];
-    e_all[j] = e_fix[src];
-  }
-  __syncthreads();
   const bool ground = sv.ground;
   const float gdz = sv.gz - o.z;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
     // tile record (12 floats): cone axis xyz, cos, sin | azimuth centre xy, cos, sin of the sector
@@ -412,13 +417,11 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast_tiled(
         const int i = base + __ffs(m) - 1;
         m &= m - 1;
         if (i < ns) {
-          best = fminf(best, hit_sphere(s_sph[i], d));
+          best = fminf(best, hit_sphere(r0[i], d));
         } else if (i < ns + nb) {
-          const int k = i - ns;
-          best = fminf(best, hit_box(s_box[2 * k], s_box[2 * k + 1], inv, nullptr));
+          best = fminf(best, hit_box(r0[i], r1[i], inv, nullptr));
         } else {
-          const int k = i - ns - nb;
-          best = fminf(best, hit_cyl(s_cyl[k], s_cyl_hh[k], d, a, inv_a, inv.z, nullptr));
+          best = fminf(best, hit_cyl(r0[i], r1[i].x, d, a, inv_a, inv.z, nullptr));
         }
       }
     }
@@ -496,14 +499,13 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0) return QS_ERR_BAD_ARGUMENT;
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
-  size_t smem = (size_t)(scene->Sm + 2 * scene->Bm + scene->Cm) * 16 + ((scene->Cm + 3) & ~3) * 4 +
-                (size_t)(scene->Sm + scene->Bm + scene->Cm) * (4 * 16 + 2 * 8);
+  size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * (4 * 16 + 8);
   cudaStream_t s = (cudaStream_t)stream;
   if (cfg->kind == 0)
-    k_raycast_tiled<0><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
+    k_raycast_tiled<0><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
                                                      tile_rays, tile_cones, n_tiles, tpc, out, hit);
   else
-    k_raycast_tiled<1><<<grid, RAY_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
+    k_raycast_tiled<1><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
                                                      tile_rays, tile_cones, n_tiles, tpc, out, hit);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
