@@ -232,6 +232,38 @@ def time_graph(fn, iters: int) -> float:
     return e0.elapsed_time(e1) / iters
 
 
+def fov_kept_counts(sc, pos, cs, cam):
+    """Per-env counts of the solids the reference's own fov_cull keeps
+    (q/sensors.py:338-374: bounding sphere vs the 4 frustum planes + behind
+    plane, and the range ball), for the culled flops/ray figure SURVEY §8d
+    asks to headline.  Yaw-only camera at pos (no offset)."""
+    import torch
+
+    th, tv = float(np.tan(cam.fov_h / 2)), float(np.tan(cam.fov_v / 2))
+    nrm = torch.tensor([[th, -1.0, 0.0], [th, 1.0, 0.0], [tv, 0.0, -1.0], [tv, 0.0, 1.0], [1.0, 0.0, 0.0]],
+                       dtype=torch.float64, device=pos.device)
+    nrm = nrm / nrm.norm(dim=-1, keepdim=True)
+    p = pos[:, :3].double()
+    c, s_ = cs[:, 0].double(), cs[:, 1].double()
+
+    def keep(cen, rad, valid):
+        rel = cen.double() - p[:, None, :]
+        loc = torch.stack([c[:, None] * rel[..., 0] + s_[:, None] * rel[..., 1],
+                           -s_[:, None] * rel[..., 0] + c[:, None] * rel[..., 1], rel[..., 2]], -1)
+        sd = loc @ nrm.T
+        inside = (sd >= -rad.double()[..., None] - 1e-9).all(-1)
+        rng = loc.norm(dim=-1) - rad.double() <= cam.max_range + 1e-9
+        return (inside & rng & valid).sum(1)
+
+    cnt = sc.counts
+    ar = lambda m: torch.arange(m, device=pos.device)[None, :]
+    ks = keep(sc.spheres[..., :3], sc.spheres[..., 3], ar(sc.spheres.shape[1]) < cnt[:, 0:1])
+    kb = keep(sc.boxes[..., :3], sc.boxes[..., 4:7].norm(dim=-1), ar(sc.boxes.shape[1]) < cnt[:, 1:2])
+    kc = keep(sc.cylinders[..., :3], torch.sqrt(sc.cylinders[..., 3] ** 2 + sc.cylinders[..., 4] ** 2),
+              ar(sc.cylinders.shape[1]) < cnt[:, 2:3])
+    return ks, kb, kc
+
+
 def bench_depth(dev, rank, world=1, frames=20):
     """C3: 16,384 envs, 64x48 depth, 32 solids (10 sph, 9 box, 13 cyl) + ground."""
     import torch
@@ -278,9 +310,13 @@ def bench_depth(dev, rank, world=1, frames=20):
     cnt = sc.counts.double().cpu().numpy()
     # un-culled algorithmic flops per ray: 14 + 10 ns + 6 nb + 31 nc (+1 ground)
     flops_frame = float(np.sum(14 + 10 * cnt[:, 0] + 6 * cnt[:, 1] + 31 * cnt[:, 2] + cnt[:, 3])) * R * world
+    ks, kb, kc = fov_kept_counts(sc, pos, cs, cam)
+    flops_culled = float((14 + 10 * ks + 6 * kb + 31 * kc).sum().item() + cnt[:, 3].sum()) * R * world
     return {"rays_per_s": E * R / (ms * 1e-3), "ms_per_frame": ms, "n_envs": E, "rays_per_env": R,
             "mean_solids": float(cnt[:, :3].sum(1).mean()),
             "tflops_uncull_equiv": flops_frame / (ms * 1e-3) / 1e12,
+            "flops_per_ray": {"uncull": flops_frame / (E * R), "fov_culled": flops_culled / (E * R)},
+            "tflops_culled_equiv": flops_culled / (ms * 1e-3) / 1e12,
             "kernel": "k_raycast_tiled<0> (per-warp cone culling)",
             "untiled": {"rays_per_s": E * R / (ms_untiled * 1e-3), "ms_per_frame": ms_untiled,
                         "tflops_uncull_equiv": flops_frame / (ms_untiled * 1e-3) / 1e12},
@@ -530,6 +566,7 @@ def run_ours(a):
                                      "148 SM x 128 x 2 x 1.965 GHz = 74.4")
         depth["ffma2_tflops_measured"] = probe["ffma2_tflops"]
         depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / (fp32_peak * world)
+        depth["frac_culled_equiv"] = depth["tflops_culled_equiv"] / (fp32_peak * world)
 
     c1 = bench_c1(dev) if rank == 0 and not a.no_depth else None
 
