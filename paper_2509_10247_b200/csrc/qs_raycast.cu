@@ -325,9 +325,8 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
   const int cap = sc.Sm + sc.Bm + sc.Cm;
   float4* r0 = sm;
   float4* r1 = r0 + cap;
-  float4* b_all = r1 + cap;
-  float4* h_all = b_all + cap;
-  float2* e_all = reinterpret_cast<float2*>(h_all + cap);
+  float4* b_all = r1 + cap;  // bounding sphere (u = c - o, Q)
+  float4* f_all = b_all + cap;  // (r, slack, Q2, r2): bounding radius, slack, footprint
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   if (warp == 0) {
     const int tot_in = sv.ns + sv.nb + sv.nc;
@@ -337,6 +336,7 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       bool keep = false;
       float4 q0, q1, bs, fp;
       float2 ee;
+      float4 ff;
       if (i < sv.ns) {
         float4 sp = ld4(sv.sph, i);
         V3 c = xyz(sp);
@@ -371,8 +371,8 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
         r0[p] = q0;
         r1[p] = q1;
         b_all[p] = bs;
-        h_all[p] = fp;
-        e_all[p] = ee;
+        ff = make_float4(ee.x, ee.y, fp.z, fp.w);
+        f_all[p] = ff;
       }
       run += __popc(m);
       ks += __popc(__ballot_sync(0xffffffffu, keep && i < sv.ns));
@@ -409,8 +409,9 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       const int j = base + lane;
       bool keep = false;
       if (j < tot) {
-        const float2 ej = e_all[j];
-        keep = cone_keeps(b_all[j], ej, ax, cth, sth) && sector_keeps(h_all[j], ej.y, azw, cw, sw);
+        const float4 bj = b_all[j], fj = f_all[j];
+        keep = cone_keeps(bj, make_float2(fj.x, fj.y), ax, cth, sth) &&
+               sector_keeps(make_float4(bj.x, bj.y, fj.z, fj.w), fj.y, azw, cw, sw);
       }
       unsigned m = __ballot_sync(0xffffffffu, keep);
       while (m) {  // warp-uniform candidate kinds: no divergence
@@ -499,7 +500,7 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0) return QS_ERR_BAD_ARGUMENT;
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
-  size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * (4 * 16 + 8);
+  size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * (4 * 16);
   cudaStream_t s = (cudaStream_t)stream;
   if (cfg->kind == 0)
     k_raycast_tiled<0><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
