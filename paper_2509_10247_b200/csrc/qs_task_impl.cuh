@@ -117,13 +117,15 @@ QS_D void write_obs(const qs_task_cfg& cfg, const qs_step_io& io, long row, cons
 // resets: in-kernel Philox sampling (q/tasks.py:676-710, 789-815, 873-902;
 // q/world.py:130-137, 409-448).  Keys: (seed, global env id, episode index).
 
+// blo/bhi: the env's bounds shrunk by 1e-6 (EnvRegs keeps them in registers;
+// the spawn margins below are taken from the shrunk bounds, so every caller
+// draws identical spawns without a global load on the reset path)
 template <int M, int TASK, int NAMAX>
-QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int episode, int na,
-                       V3* p, V3* v, V3* goal, V3& head, int& next_gate) {
+QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int episode, int na, V3 blo,
+                       V3 bhi, V3* p, V3* v, V3* goal, V3& head, int& next_gate) {
   const uint64_t gid = (uint64_t)(e + cfg.env_offset);
   RngK rng(cfg.rng_round_keys, gid, (uint32_t)episode, RNG_SPAWN);
-  float4 blo = ld4(sc.bounds, 2 * e), bhi = ld4(sc.bounds, 2 * e + 1);
-  V3 lo = xyz(blo), hi = xyz(bhi);
+  const V3 lo = blo, hi = bhi;
   bool ok = true;
   next_gate = 0;
   if (TASK == QS_TASK_POSITION) {
@@ -710,7 +712,7 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, i
   V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
   int ng0 = 0;
   if (INLINE && done) {
-    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, episode, na, sp_p, sp_v, sp_g, head, ng0);
+    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, episode, na, R.blo, R.bhi, sp_p, sp_v, sp_g, head, ng0);
     if (!ok) report_err(err, QS_ERR_GENERATION, (int)(e * na));
   }
   GateV g0, g1;
@@ -1194,7 +1196,9 @@ __global__ void __launch_bounds__(128) k_task_spawn(const qs_task_cfg cfg, const
   V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
   int ng0 = 0;
   if (!use_tab) {
-    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, meta.y, na, sp_p, sp_v, sp_g, head, ng0);
+    const V3 blo = xyz(ld4(sc.bounds, 2 * e)) + v3(1e-6f, 1e-6f, 1e-6f);  // as env_load
+    const V3 bhi = xyz(ld4(sc.bounds, 2 * e + 1)) - v3(1e-6f, 1e-6f, 1e-6f);
+    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, meta.y, na, blo, bhi, sp_p, sp_v, sp_g, head, ng0);
     if (!ok) report_err(io.err, QS_ERR_GENERATION, (int)(e * na));
   } else if (tab.next_gate) {
     ng0 = tab.next_gate[e];
