@@ -670,7 +670,7 @@ def run_c5(a):
         print(json.dumps({
             "metric": "env-steps/s (SHAC train: policy + sim fwd+bwd + critic)", "value": world * N * 16 * a.steps / el,
             "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "dtype": "f32",
+            "higher_is_better": True, "scaling": "weak", "dtype": "f32 sim, bf16 policy/critic matmuls",
             "config": {"workload": f"C5: SHAC, pm_continuous position, {N} envs/GPU x {world}, horizon 16",
                        "parallelism": f"env-sharded x{world}; NCCL all-reduce of policy+critic grads"},
             "allreduce_ms_per_update": ar / a.steps * 1e3, "last": out}))

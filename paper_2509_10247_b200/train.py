@@ -43,6 +43,10 @@ class LearnerOptions:
     log_sigma_init: float = -1.2
     log_sigma_max: float = 2.0
     seed: int = 0
+    # matmul precision of the policy/critic on CUDA: "bf16" runs them on the
+    # tensor cores under torch.autocast (fp32 master weights, fp32 sim
+    # gradients); "fp32" keeps the reference's all-fp32 arithmetic (SIMT GEMMs)
+    net_dtype: str = "bf16"
 
 
 class PolicyNet(torch.nn.Module):
@@ -71,11 +75,12 @@ class PolicyNet(torch.nn.Module):
     def forward(self, proprio, h=None):
         x = proprio * self.input_scale
         if self.gru is not None:
-            h = self.gru(x, h)
+            h = self.gru(x, h).float()
             x = h
         for layer in self.trunk:
             x = torch.tanh(layer(x))
-        return self.mu(x), torch.clamp(self.sig(x), LOG_SIGMA_MIN, self.log_sigma_max), h
+        mu, ls = self.mu(x).float(), self.sig(x).float()
+        return mu, torch.clamp(ls, LOG_SIGMA_MIN, self.log_sigma_max), h
 
 
 class ValueNet(torch.nn.Module):
@@ -94,7 +99,7 @@ class ValueNet(torch.nn.Module):
             x = layer(x)
             if i < len(self.layers) - 1:
                 x = torch.tanh(x)
-        return x[..., 0]
+        return x[..., 0].float()
 
 
 def td_lambda_targets(r, values, bootstrap, done, gamma, lam):
@@ -154,6 +159,13 @@ class ShortHorizonTrainer:
         self._gen = torch.Generator(device=dev)
         self._gen.manual_seed(opts.seed * 1_000_003 + env.env_offset)
         self.timing = {"sim_fwd_bwd_s": 0.0, "allreduce_s": 0.0}
+        if opts.net_dtype not in ("bf16", "fp32"):
+            raise ValueError("net_dtype must be 'bf16' or 'fp32'")
+        self._amp = opts.net_dtype == "bf16" and dev.type == "cuda"
+
+    def _nets(self):
+        """autocast scope for policy/critic evaluations (no-op for fp32 / CPU)."""
+        return torch.autocast("cuda", dtype=torch.bfloat16, enabled=self._amp)
 
     def collect_window(self, record_privileged: bool):
         """q/learners.py:201-230."""
@@ -167,7 +179,8 @@ class ShortHorizonTrainer:
         for t in range(T):
             if record_privileged:
                 priv.append(env.privileged_state())
-            mu, log_sigma, h = self.policy(obs.proprio, h)
+            with self._nets():
+                mu, log_sigma, h = self.policy(obs.proprio, h)
             a = mu
             if opts.explore:
                 eps = torch.randn(mu.shape, generator=self._gen, device=mu.device)
@@ -193,7 +206,8 @@ class ShortHorizonTrainer:
         if self.needs_critic:
             for p in self.value.parameters():
                 p.requires_grad_(False)
-            v_term = self.value(self.env.privileged_var())  # grad flows through the state
+            with self._nets():
+                v_term = self.value(self.env.privileged_var())  # grad flows through the state
             for p in self.value.parameters():
                 p.requires_grad_(True)
             body = body + v_term.mean() * (opts.gamma ** opts.horizon)
@@ -222,15 +236,18 @@ class ShortHorizonTrainer:
         opts = self.opts
         with torch.no_grad():
             T, N, K = priv.shape
-            values = self.value(priv.reshape(T * N, K)).reshape(T, N)
-            boot = self.value(self.env.privileged_state())
+            with self._nets():
+                values = self.value(priv.reshape(T * N, K)).reshape(T, N)
+                boot = self.value(self.env.privileged_state())
             targets = td_lambda_targets(r, values, boot, dones, opts.gamma, opts.td_lambda)
         X = priv.reshape(-1, priv.shape[-1])
         y = targets.reshape(-1)
         loss_val = 0.0
         for _ in range(opts.critic_iters):
             self.critic_opt.zero_grad(set_to_none=True)
-            loss = ((self.value(X) - y) ** 2).mean()
+            with self._nets():
+                pred = self.value(X)
+            loss = ((pred - y) ** 2).mean()
             loss.backward()
             allreduce_mean_(list(self.value.parameters()), self.group)
             torch.nn.utils.clip_grad_norm_(self.value.parameters(), opts.grad_clip)
