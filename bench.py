@@ -62,6 +62,7 @@ def parse():
     ap.add_argument("--model", default="full")
     ap.add_argument("--no-depth", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-imu", action="store_true", help="diagnostic: full model without the IMU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no cpu/clock sampling)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
@@ -425,7 +426,7 @@ def run_ours(a):
 
     N, T = a.envs, a.horizon
     cfg = qs.TaskConfig(task="position", dynamics=a.model, n_envs=N, episode_len=128,
-                        imu=qs.ImuSpec(**IMU) if a.model == "full" else None)
+                        imu=qs.ImuSpec(**IMU) if a.model == "full" and not a.no_imu else None)
     env = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
     env.reset(seed=1)
     win = BpttWindow(env, T)
