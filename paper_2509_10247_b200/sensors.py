@@ -91,7 +91,10 @@ def pack_primitives(sets) -> BatchedPrimitives:
 def _t(x, device, dtype=torch.float32):
     if isinstance(x, torch.Tensor):
         return x.to(device=device, dtype=dtype)
-    return torch.as_tensor(np.asarray(x), dtype=dtype, device=device)
+    a = np.asarray(x)
+    if not a.flags.writeable:  # read-only views (e.g. broadcast) cannot back a tensor
+        a = a.copy()
+    return torch.as_tensor(a, dtype=dtype, device=device)
 
 
 def _valid_first(data, valid):

@@ -606,6 +606,29 @@ class FlightTask:
     def next_gate(self) -> torch.Tensor:
         return self._meta[:, 3]
 
+    # racing gate arrays (q/tasks.py:864-867), views of the device gate table
+    # (E, G, 8) = centre xyz, inner radius, normal xyz, frame width
+    def _gate_table(self) -> torch.Tensor:
+        if self.config.task != "racing" or self._scene.gates is None:
+            raise AttributeError("gate arrays exist only for the racing task")
+        return self._scene.gates
+
+    @property
+    def gate_centers(self) -> torch.Tensor:
+        return self._gate_table()[..., 0:3]
+
+    @property
+    def gate_normals(self) -> torch.Tensor:
+        return self._gate_table()[..., 4:7]
+
+    @property
+    def gate_inner(self) -> torch.Tensor:
+        return self._gate_table()[..., 3]
+
+    @property
+    def gate_frame(self) -> torch.Tensor:
+        return self._gate_table()[..., 7]
+
     @property
     def params(self) -> dyn.QuadParams:
         if self._dr is None:

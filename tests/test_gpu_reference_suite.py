@@ -381,3 +381,55 @@ def test_dual_reward_contract_and_detach(qs):  # :565-589
     g0, g1 = torch.autograd.grad(out.r_ctrl.sum(), [a0, a1], allow_unused=True)
     assert g0 is None or float(g0.abs().sum()) == 0.0
     assert float(g1.abs().sum()) > 0
+
+
+# ---------------------------------------------------------------------------
+# racing (pkg/tests/test_tasks.py:402-480): gate arrays + pass / crash through env.step
+
+
+def race_cfg(qs, **kw):
+    base = dict(task="racing", dynamics="pm_continuous", n_envs=1, episode_len=256, n_gates=3, gate_spread=6.0)
+    base.update(kw)
+    return qs.TaskConfig(**base)
+
+
+def _through_gate(qs, env, offset):
+    """Place the drone 0.5 m before gate 0 (+ offset) moving 1 m per step along
+    its normal (pm_continuous integrates p with the pre-step velocity)."""
+    c = env.gate_centers[0, 0].double()
+    n = env.gate_normals[0, 0].double()
+    p = (c - 0.5 * n + offset)[None].float()
+    v = (n / env.config.dt)[None].float()
+    env.state = env.model.init_state(p, v)
+    return env.step(torch.zeros(1, 3, device="cuda"))
+
+
+def test_racing_gate_arrays_and_initial_goal(qs):  # :864-867, 887-891
+    env = qs.make_task(race_cfg(qs))
+    env.reset(seed=31)
+    g = env.scenes[0].gates
+    assert env.gate_centers.shape == (1, 3, 3)
+    np.testing.assert_allclose(np_(env.gate_centers[0]), np.stack([x.center for x in g]), atol=1e-6)
+    np.testing.assert_allclose(np_(env.gate_normals[0]), np.stack([x.normal for x in g]), atol=1e-6)
+    np.testing.assert_allclose(np_(env.gate_inner[0]), [x.inner_radius for x in g], atol=1e-6)
+    np.testing.assert_allclose(np_(env.gate_frame[0]), [x.frame_width for x in g], atol=1e-6)
+    assert torch.equal(env.goals[0], env.gate_centers[0, 0])
+    assert int(env.next_gate[0]) == 0
+
+
+def test_racing_gate_pass_and_crash(qs):  # :427-458
+    env = qs.make_task(race_cfg(qs))
+    env.reset(seed=32)
+    out = _through_gate(qs, env, torch.zeros(3, dtype=torch.float64, device="cuda"))
+    assert int(out.terminated[0]) == 0  # a clean pass through a non-final gate
+    assert int(env.next_gate[0]) == 1
+    assert torch.equal(env.goals[0], env.gate_centers[0, 1])
+    env.reset(seed=32)
+    n = env.gate_normals[0, 0].double()
+    up = torch.tensor([0.0, 0.0, 1.0], dtype=torch.float64, device="cuda")
+    radial = up - torch.dot(up, n) * n
+    radial = radial / radial.norm()
+    r_hit = float(env.gate_inner[0, 0]) + 0.5 * float(env.gate_frame[0, 0])
+    out = _through_gate(qs, env, radial * r_hit)
+    assert int(out.terminated[0]) == qs.tasks.TERM_COLLISION
+    assert float(out.r_goal[0]) == -1.0
