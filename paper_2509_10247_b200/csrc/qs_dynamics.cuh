@@ -46,23 +46,24 @@ struct ModelTraits<QS_MODEL_SIMPLIFIED> {
   static constexpr int NP = 5, A = 4, P = 9;
 };
 
-template <int M>
+template <int M, bool GENERIC = false>  // GENERIC: plain loads (shared-memory staging)
 QS_D State load_state(const float* S, long N, long row) {
+  auto ld = [](const float* p, long i) { return GENERIC ? reinterpret_cast<const float4*>(p)[i] : ld4(p, i); };
   State s;
-  float4 a = ld4(S, row), b = ld4(S, N + row), c = ld4(S, 2 * N + row);
+  float4 a = ld(S, row), b = ld(S, N + row), c = ld(S, 2 * N + row);
   s.p = xyz(a);
   s.v = xyz(b);
   s.r0 = s.r1 = s.r2 = v3(0.f, 0.f, 0.f);
   if (M == QS_MODEL_SIMPLIFIED) {
     s.r0 = xyz(c);
-    s.r1 = xyz(ld4(S, 3 * N + row));
-    s.r2 = xyz(ld4(S, 4 * N + row));
+    s.r1 = xyz(ld(S, 3 * N + row));
+    s.r2 = xyz(ld(S, 4 * N + row));
     s.ve = v3(a.w, b.w, c.w);
     s.x = v3(0.f, 0.f, 0.f);
     s.q = q4(1.f, 0.f, 0.f, 0.f);
     s.w = v3(0.f, 0.f, 0.f);
   } else if (M == QS_MODEL_FULL) {
-    float4 d = ld4(S, 3 * N + row);
+    float4 d = ld(S, 3 * N + row);
     s.q = q4(c.x, c.y, c.z, c.w);
     s.w = xyz(d);
     s.ve = v3(a.w, b.w, d.w);

@@ -1124,7 +1124,47 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
     if (a >= na) break;
     gS[a] = load_grad<M>(w.g_S_final, N, e * na + a);
   }
-  load_ck(w.T - 1, cur);
+  // Single-agent rows stream their checkpoints through a per-thread cp.async
+  // ring in shared memory, NST steps ahead: the loads hold no registers while
+  // in flight and each thread waits only for its own copies (no barrier).
+  // Multi-agent rows load one step ahead into registers.
+  constexpr int NST = 3;
+  constexpr int NPL = ModelTraits<M>::NP;
+  constexpr int NREC = NPL + 4;  // state planes, goal, peff, dr, raw
+  __shared__ __align__(16) float4 ring[NAMAX == 1 ? NST : 1][NREC][WIN_BLOCK];
+  __shared__ int ring_fl[NAMAX == 1 ? NST : 1][WIN_BLOCK];
+  const int tx = threadIdx.x;
+  const bool use_ring = NAMAX == 1 && blockDim.x == WIN_BLOCK;
+  auto issue = [&](int t, int b) {  // this thread's rows of step t -> stage b
+    if (t >= 0) {
+      const long row = e;
+#pragma unroll
+      for (int k = 0; k < NPL; ++k) cp_async16(&ring[b][k][tx], w.S + (((long)t * NP + k) * N + row) * 4);
+      cp_async16(&ring[b][NPL][tx], w.goal + ((long)t * N + row) * 4);
+      cp_async16(&ring[b][NPL + 1][tx], w.peff + ((long)t * N + row) * 4);
+      if (has_dr) cp_async16(&ring[b][NPL + 2][tx], w.dr + ((long)t * N + row) * 4);
+      const float* ra = w.actions + ((long)t * N + row) * A;
+      float* rd = &ring[b][NPL + 3][tx].x;
+#pragma unroll
+      for (int k = 0; k < A; ++k) cp_async4(rd + k, ra + k);
+      cp_async4(&ring_fl[b][tx], w.flags + (long)t * N + row);
+    }
+    cp_async_commit();  // one group per step, possibly empty, keeps the count uniform
+  };
+  auto read_stage = [&](int b, Ck* c) {
+    c[0].s = load_state<M, true>(&ring[b][0][0].x, WIN_BLOCK, tx);
+    c[0].goal = ring[b][NPL][tx];
+    c[0].peff = ring[b][NPL + 1][tx];
+    c[0].dr = has_dr ? ring[b][NPL + 2][tx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 r = ring[b][NPL + 3][tx];
+    c[0].raw = make_float4(r.x, r.y, r.z, A == 4 ? r.w : 0.f);
+    c[0].fl = ring_fl[b][tx];
+  };
+  if (use_ring) {
+    for (int k = 0; k < NST; ++k) issue(w.T - 1 - k, k);
+  } else {
+    load_ck(w.T - 1, cur);
+  }
   State s2[NAMAX];  // checkpoint t+1 = post-dynamics state of step t (non-reset rows)
 #pragma unroll
   for (int a = 0; a < NAMAX; ++a) {
@@ -1133,8 +1173,14 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
   }
   const float lg_gamma = log2f(w.gamma);  // gamma^t = 2^(t lg): one MUFU.EX2 per step
   for (int t = w.T - 1; t >= 0; --t) {
-    if (t > 0) load_ck(t - 1, nxt);
     const float gscale = w.g_rctrl_scale * (t == 0 ? 1.f : exp2f((float)t * lg_gamma));
+    const int kk = w.T - 1 - t;
+    if (use_ring) {
+      cp_async_wait<NST - 1>();  // this thread's copies of step t have landed
+      read_stage(kk % NST, cur);
+    } else if (t > 0) {
+      load_ck(t - 1, nxt);
+    }
     State s_in[NAMAX];
     float4 goal[NAMAX], peff[NAMAX], dr[NAMAX], raw[NAMAX];
     int fl[NAMAX];
@@ -1153,8 +1199,9 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
 #pragma unroll
     for (int a = 0; a < NAMAX; ++a) {
       s2[a] = cur[a].s;
-      cur[a] = nxt[a];
+      if (!use_ring) cur[a] = nxt[a];
     }
+    if (use_ring) issue(t - NST, kk % NST);  // the stage just consumed takes step t - NST
   }
   if (w.g_S0) {
 #pragma unroll
