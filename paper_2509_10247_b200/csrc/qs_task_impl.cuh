@@ -1134,7 +1134,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
   __shared__ __align__(16) float4 ring[NAMAX == 1 ? NST : 1][NREC][WIN_BLOCK];
   __shared__ int ring_fl[NAMAX == 1 ? NST : 1][WIN_BLOCK];
   const int tx = threadIdx.x;
-  const bool use_ring = NAMAX == 1 && blockDim.x == WIN_BLOCK;
+  const bool use_ring = NAMAX == 1 && blockDim.x <= WIN_BLOCK;
   auto issue = [&](int t, int b) {  // this thread's rows of step t -> stage b
     if (t >= 0) {
       const long row = e;
@@ -1318,17 +1318,22 @@ __global__ void __launch_bounds__(128) k_task_observe(const qs_task_cfg cfg, con
 inline int grid_for(int n, int block) { return (n + block - 1) / block; }
 inline int launch_status() { return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH; }
 
+// per-step kernels: 128-thread CTAs, or 32 when too few envs to fill the SMs
+inline int step_block(int n_envs) { return n_envs >= 148 * 2 * 128 ? 128 : 32; }
+
 template <int M, int T, int NA>
 int run_fwd(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, cudaStream_t s) {
+  const int b = step_block(cfg->n_envs);
   if (cfg->reset_mode == 0)
-    k_task_fwd<M, T, NA, true><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io);
+    k_task_fwd<M, T, NA, true><<<grid_for(cfg->n_envs, b), b, 0, s>>>(*cfg, *sc, *io);
   else
-    k_task_fwd<M, T, NA, false><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io);
+    k_task_fwd<M, T, NA, false><<<grid_for(cfg->n_envs, b), b, 0, s>>>(*cfg, *sc, *io);
   return launch_status();
 }
 template <int M, int T, int NA>
 int run_bwd(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_grad* g, cudaStream_t s) {
-  k_task_bwd<M, T, NA><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *g);
+  const int b = step_block(cfg->n_envs);
+  k_task_bwd<M, T, NA><<<grid_for(cfg->n_envs, b), b, 0, s>>>(*cfg, *sc, *g);
   return launch_status();
 }
 template <int M, int T, int NA>
@@ -1350,13 +1355,16 @@ template <int M, int T, int NA>
 int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_window_io* w, cudaStream_t s) {
   if (w->T <= 0) return QS_OK;
   if (op == 4 && w->loss) cudaMemsetAsync(w->loss, 0, sizeof(double), s);
-  const dim3 grid(grid_for(cfg->n_envs, WIN_BLOCK));
+  // 64-thread CTAs when there are enough envs for >= 4 CTAs per SM; otherwise
+  // 32-thread CTAs spread the (few, latency-bound) envs over twice the SMs
+  const int blk = cfg->n_envs >= 148 * 4 * WIN_BLOCK ? WIN_BLOCK : 32;
+  const dim3 grid(grid_for(cfg->n_envs, blk));
   if (op == 4 && NA == 1 && w->imu_out && !w->imu_noise)  // Philox IMU specialisation
-    k_window_fwd<M, T, NA, NA == 1 ? 1 : 0><<<grid, WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+    k_window_fwd<M, T, NA, NA == 1 ? 1 : 0><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
   else if (op == 4)
-    k_window_fwd<M, T, NA, 0><<<grid, WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+    k_window_fwd<M, T, NA, 0><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
   else
-    k_window_bwd<M, T, NA><<<grid_for(cfg->n_envs, WIN_BLOCK), WIN_BLOCK, 0, s>>>(*cfg, *sc, *w);
+    k_window_bwd<M, T, NA><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
   return launch_status();
 }
 
