@@ -1,9 +1,9 @@
 // Fused env step (forward + analytic VJP), spawn and observe kernels.
 //
-// One thread owns one ENV (all of its agent rows), so every per-env coupling
-// of the reference step -- success needs all agents, bounds/collision any
-// agent, the formation penalty, the shared reset -- stays in registers with no
-// inter-thread communication.  Reference: q/tasks.py:549-763, 817-844,
+// One thread owns one agent ROW; an env's rows sit in adjacent lanes (a lane
+// group), so every per-env coupling of the reference step -- success needs all
+// agents, bounds/collision any agent, the formation penalty, the shared reset
+// -- is a shuffle within the group, and single-agent envs need none.  Reference: q/tasks.py:549-763, 817-844,
 // 925-972; q/dynamics.py; q/sensors.py:417-611; q/world.py:409-448.
 #pragma once
 #include "qs_dynamics.cuh"
@@ -114,21 +114,70 @@ QS_D void write_obs(const qs_task_cfg& cfg, const qs_step_io& io, long row, cons
 }
 
 // ---------------------------------------------------------------------------
+// lane groups.  An env's agent rows live in G adjacent lanes (G = 1, 2, 4, 8,
+// the power of two >= n_agents); lane g of a group owns agent row g, so each
+// thread carries ONE row's registers.  Per-env couplings (all-agent success,
+// any-agent bounds/collision, the formation penalty and its VJP, the shared
+// reset) are group shuffles.  Lanes g >= n_agents (padding, when n_agents is
+// not a power of two) mirror agent 0, contribute neutral values and write
+// nothing.  G = 1 compiles every group operation away.
+
+template <int G>
+struct Grp {
+  unsigned mask;  // this group's lanes in the warp
+  int g;          // agent index of this lane
+  bool real;      // g < n_agents
+  QS_D static Grp make(int na) {
+    Grp r;
+    const int lane = threadIdx.x & 31;
+    r.g = G == 1 ? 0 : (lane & (G - 1));
+    r.mask = G == 1 ? 0u : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    r.real = r.g < na;
+    return r;
+  }
+  QS_D float sum(float v) const {
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(mask, v, o, G);
+    return v;
+  }
+  QS_D bool any(bool b) const {
+    int v = b;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v |= __shfl_xor_sync(mask, v, o, G);
+    return v != 0;
+  }
+  QS_D bool all(bool b) const {
+    int v = b;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) v &= __shfl_xor_sync(mask, v, o, G);
+    return v != 0;
+  }
+  QS_D float bcast(float v, int src) const { return G == 1 ? v : __shfl_sync(mask, v, src, G); }
+  QS_D V3 bcast(V3 v, int src) const { return v3(bcast(v.x, src), bcast(v.y, src), bcast(v.z, src)); }
+};
+
+// ---------------------------------------------------------------------------
 // resets: in-kernel Philox sampling (q/tasks.py:676-710, 789-815, 873-902;
 // q/world.py:130-137, 409-448).  Keys: (seed, global env id, episode index).
+// One stream per env; the agents' draws sit at fixed counter offsets, so each
+// lane computes exactly the draws its agent takes in the reference's order.
 
 // blo/bhi: the env's bounds shrunk by 1e-6 (EnvRegs keeps them in registers;
 // the spawn margins below are taken from the shrunk bounds, so every caller
 // draws identical spawns without a global load on the reset path)
-template <int M, int TASK, int NAMAX>
+template <int M, int TASK, int G>
 QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int episode, int na, V3 blo,
-                       V3 bhi, V3* p, V3* v, V3* goal, V3& head, int& next_gate) {
+                       V3 bhi, const Grp<G>& grp, V3& p, V3& v, V3& goal, V3& head, int& next_gate) {
   const uint64_t gid = (uint64_t)(e + cfg.env_offset);
   RngK rng(cfg.rng_round_keys, gid, (uint32_t)episode, RNG_SPAWN);
+  const uint32_t c0 = rng.ctr.w;
   const V3 lo = blo, hi = bhi;
+  const int ag = grp.real ? grp.g : 0;
+  const V3 f = v3(cfg.formation[ag][0], cfg.formation[ag][1], cfg.formation[ag][2]);
   bool ok = true;
   next_gate = 0;
   if (TASK == QS_TASK_POSITION) {
+    // the shared spawn/goal pair: every lane runs the same rejection loop
     V3 l8 = lo + v3(0.8f, 0.8f, 0.8f), h8 = hi - v3(0.8f, 0.8f, 0.8f);
     V3 sp = l8, gl = l8;
     ok = false;
@@ -139,64 +188,52 @@ QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int e
       float d = norm3(gl - sp);
       ok = d >= 2.5f && d <= cfg.goal_dist;
     }
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      V3 f = v3(cfg.formation[a][0], cfg.formation[a][1], cfg.formation[a][2]);
-      float4 n0 = rng.normal4(), n1 = rng.normal4();
-      p[a] = sp + f + v3(n0.x, n0.y, n0.z) * 0.1f;
-      v[a] = v3(n0.w, n1.x, n1.y) * 0.3f;
-      goal[a] = gl + f;
-    }
+    rng.ctr.w += 2u * (uint32_t)ag;  // agent a draws normals 2a, 2a+1 after the pair
+    float4 n0 = rng.normal4(), n1 = rng.normal4();
+    p = sp + f + v3(n0.x, n0.y, n0.z) * 0.1f;
+    v = v3(n0.w, n1.x, n1.y) * 0.3f;
+    goal = gl + f;
     head = head_xy(gl - sp);
   } else if (TASK == QS_TASK_AVOIDANCE) {
     V3 ssp = load3(sc.spawn_goal, 2 * e), sgl = load3(sc.spawn_goal, 2 * e + 1);
     SceneView sv = scene_view(sc, e);
     ok = false;
-    for (int t = 0; t < 100 && !ok; ++t) {
+    int t = 0;
+    for (; t < 100 && !ok; ++t) {
+      rng.ctr.w = c0 + (uint32_t)(t * na + ag);  // try t: one normal4 per agent, in agent order
+      float4 n0 = rng.normal4();
+      V3 q = ssp + f + v3(n0.x, n0.y, n0.z) * 0.15f;
+      q.z = clampf(q.z, lo.z + 0.3f, hi.z - 0.3f);
+      p = q;
       bool good = true;
+      if (G > 1) {  // pairwise separation (q/world.py:433-437)
 #pragma unroll
-      for (int a = 0; a < NAMAX; ++a) {
-        if (a >= na) break;
-        V3 f = v3(cfg.formation[a][0], cfg.formation[a][1], cfg.formation[a][2]);
-        float4 n0 = rng.normal4();
-        V3 q = ssp + f + v3(n0.x, n0.y, n0.z) * 0.15f;
-        q.z = clampf(q.z, lo.z + 0.3f, hi.z - 0.3f);
-        p[a] = q;
+        for (int j = 0; j < G; ++j) {
+          V3 pj = grp.bcast(q, j);
+          if (j > grp.g && j < na) good = good && norm3(q - pj) >= cfg.d_min;
+        }
       }
-      if (na > 1) {
-        for (int i = 0; i < na; ++i)
-          for (int j = i + 1; j < na; ++j) good = good && norm3(p[i] - p[j]) >= cfg.d_min;
-      }
-#pragma unroll
-      for (int a = 0; a < NAMAX; ++a) {
-        if (a >= na) break;
-        int code;
-        good = good && sdf_eval(sv, p[a], code) > cfg.collision_radius + 0.3f;
-        V3 q = p[a];
-        good = good && q.x > lo.x + 0.2f && q.y > lo.y + 0.2f && q.z > lo.z + 0.2f &&
-               q.x < hi.x - 0.2f && q.y < hi.y - 0.2f && q.z < hi.z - 0.2f;
-      }
-      ok = good;
+      int code;
+      good = good && sdf_eval(sv, q, code) > cfg.collision_radius + 0.3f;
+      good = good && q.x > lo.x + 0.2f && q.y > lo.y + 0.2f && q.z > lo.z + 0.2f && q.x < hi.x - 0.2f &&
+             q.y < hi.y - 0.2f && q.z < hi.z - 0.2f;
+      ok = grp.all(good || !grp.real);
     }
-    float4 nj = rng.normal4();
+    rng.ctr.w = c0 + (uint32_t)(t * na);
+    float4 nj = rng.normal4();  // shared goal jitter
     V3 jit = v3(nj.x, nj.y, nj.z) * 0.2f;
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      V3 f = v3(cfg.formation[a][0], cfg.formation[a][1], cfg.formation[a][2]);
-      float4 n1 = rng.normal4();
-      v[a] = v3(n1.x, n1.y, n1.z) * 0.2f;
-      goal[a] = sgl + f + jit;
-    }
+    rng.ctr.w = c0 + (uint32_t)(t * na + 1 + ag);
+    float4 n1 = rng.normal4();
+    v = v3(n1.x, n1.y, n1.z) * 0.2f;
+    goal = sgl + f + jit;
     head = head_xy(sgl - ssp);
   } else {  // racing, single agent
     V3 ssp = load3(sc.spawn_goal, 2 * e);
     float4 n0 = rng.normal4(), n1 = rng.normal4();
-    p[0] = ssp + v3(n0.x, n0.y, n0.z) * 0.2f;
-    v[0] = v3(n0.w, n1.x, n1.y) * 0.2f;
+    p = ssp + v3(n0.x, n0.y, n0.z) * 0.2f;
+    v = v3(n0.w, n1.x, n1.y) * 0.2f;
     GateV g0 = load_gate(sc, cfg, e, 0);
-    goal[0] = g0.c;
+    goal = g0.c;
     head = head_xy(g0.c - ssp);
   }
   return ok;
@@ -286,7 +323,7 @@ QS_D void imu_apply_z(const qs_task_cfg& cfg, long row, const State& s2, V3 vdot
   if (cfg.imu_gyro_std != 0.f) gy += ng * cfg.imu_gyro_std;
   b0 = f4(ba, 0.f);
   b1 = f4(bg, 0.f);
-  float* o = out + 6 * row;
+  float* o = out;  // 6 floats: accel xyz, gyro xyz
   o[0] = acc.x; o[1] = acc.y; o[2] = acc.z;
   o[3] = gy.x; o[4] = gy.y; o[5] = gy.z;
 }
@@ -439,16 +476,16 @@ QS_D void warp_stats(bool active, bool done, int term, float ret, double* stats)
 }
 
 // ---------------------------------------------------------------------------
-// per-env register file: everything one env carries from step to step
+// per-row register file: everything one agent row carries from step to step
+// (meta / ep_ret / bounds are the env's, replicated across its group)
 
-template <int NAMAX>
 struct EnvRegs {
-  State s[NAMAX];
-  float4 goal[NAMAX], peff[NAMAX], dr[NAMAX];
-  float4 ba[NAMAX], bg[NAMAX];  // IMU bias (accel, gyro)
-  int4 meta;                    // steps_in_episode, episode, tick, next_gate
+  State s;
+  float4 goal, peff, dr;
+  float4 ba, bg;  // IMU bias (accel, gyro)
+  int4 meta;      // steps_in_episode, episode, tick, next_gate
   float ep_ret;
-  V3 blo, bhi;                  // bounds shrunk by 1e-6 (q/tasks.py:673-674)
+  V3 blo, bhi;    // bounds shrunk by 1e-6 (q/tasks.py:673-674)
 };
 
 // pointers of one step's outputs (rows are env-major, N = n_envs * n_agents)
@@ -491,59 +528,43 @@ QS_D RowPrm row_params_v(const qs_task_cfg& cfg, bool has_dr, float4 d) {
   return r;
 }
 
-template <int M, int NAMAX>
-QS_D void env_load(const qs_task_cfg& cfg, const float* sc_bounds, long e, int na, long N, EnvRegs<NAMAX>& R,
-                   const float* S,
+template <int M>
+QS_D void env_load(const float* sc_bounds, long e, long row, long N, EnvRegs& R, const float* S,
                    const float* goal, const float* peff, const float* dr, const int32_t* meta,
                    const float* ep_ret, const float* bias) {
   R.meta = reinterpret_cast<const int4*>(meta)[e];
   R.ep_ret = ep_ret[e];
   R.blo = xyz(ld4(sc_bounds, 2 * e)) + v3(1e-6f, 1e-6f, 1e-6f);
   R.bhi = xyz(ld4(sc_bounds, 2 * e + 1)) - v3(1e-6f, 1e-6f, 1e-6f);
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    R.s[a] = load_state<M>(S, N, row);
-    R.goal[a] = ld4(goal, row);
-    R.peff[a] = ld4(peff, row);
-    R.dr[a] = dr ? ld4(dr, row) : make_float4(0.f, 0.f, 0.f, 0.f);
-    if (bias) {
-      R.ba[a] = ld4(bias, 2 * row);
-      R.bg[a] = ld4(bias, 2 * row + 1);
-    }
+  R.s = load_state<M>(S, N, row);
+  R.goal = ld4(goal, row);
+  R.peff = ld4(peff, row);
+  R.dr = dr ? ld4(dr, row) : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (bias) {
+    R.ba = ld4(bias, 2 * row);
+    R.bg = ld4(bias, 2 * row + 1);
   }
 }
 
 // the functional (checkpointed) part of the register file
-template <int M, int NAMAX>
-QS_D void env_store_ckpt(long e, int na, long N, const EnvRegs<NAMAX>& R, float* S, float* goal, float* peff,
-                         float* dr) {
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    store_state<M>(S, N, row, R.s[a]);
-    st4(goal, row, R.goal[a]);
-    st4(peff, row, R.peff[a]);
-    if (dr) st4(dr, row, R.dr[a]);
-  }
+template <int M>
+QS_D void env_store_ckpt(long row, long N, const EnvRegs& R, float* S, float* goal, float* peff, float* dr) {
+  store_state<M>(S, N, row, R.s);
+  st4(goal, row, R.goal);
+  st4(peff, row, R.peff);
+  if (dr) st4(dr, row, R.dr);
 }
 
-// the in-place part
-template <int NAMAX>
-QS_D void env_store_inplace(long e, int na, const EnvRegs<NAMAX>& R, int32_t* meta, float* ep_ret,
+// the in-place part (env counters by the group's lane 0)
+QS_D void env_store_inplace(long e, long row, bool lead, const EnvRegs& R, int32_t* meta, float* ep_ret,
                             float* bias) {
-  reinterpret_cast<int4*>(meta)[e] = R.meta;
-  ep_ret[e] = R.ep_ret;
+  if (lead) {
+    reinterpret_cast<int4*>(meta)[e] = R.meta;
+    ep_ret[e] = R.ep_ret;
+  }
   if (bias) {
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      const long row = e * na + a;
-      st4(bias, 2 * row, R.ba[a]);
-      st4(bias, 2 * row + 1, R.bg[a]);
-    }
+    st4(bias, 2 * row, R.ba);
+    st4(bias, 2 * row + 1, R.bg);
   }
 }
 
@@ -551,92 +572,86 @@ struct StepStat {
   bool done;
   int term;
   float ret;
-  float rc_sum;  // sum of r_ctrl over the env's rows
+  float rc;  // this row's r_ctrl (0 for padding lanes)
 };
 
 // ---------------------------------------------------------------------------
-// one fused env step on the register file (FlightTask.step, q/tasks.py:549-600)
-
+// one fused env step of one agent row (FlightTask.step, q/tasks.py:549-600);
 // IMU: 0 = decided at run time by has_imu / out.imu_noise; 1 = Philox IMU on
-// (compile time), its normals drawn at the top of the row's step
-template <int M, int TASK, int NAMAX, bool INLINE, int IMU = 0>
-QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int na, long N,
-                           EnvRegs<NAMAX>& R, const float4* raw_in, const StepOut& out, int32_t* err,
+// (compile time), its normals drawn at the top of the step
+
+template <int M, int TASK, int G, bool INLINE, int IMU = 0>
+QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, long row, int na, long N,
+                           const Grp<G>& grp, EnvRegs& R, float4 raw, const StepOut& out, int32_t* err,
                            bool has_dr, bool has_imu) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
   const DynK k = dyn_consts(cfg);
   if (IMU == 1) has_imu = true;
-  int errc = 0, err_row = 0;  // first contract error of the env, reported once after the rows
-  int term_env = 0;
-  State s2[NAMAX];
-  float rc[NAMAX], rl[NAMAX];
-  int codes[NAMAX];
-  bool all_goal = true, any_oob = false, any_coll = false;
-  V3 p0 = v3(0.f, 0.f, 0.f);
+  const bool real = grp.real;
   SceneView sv;
   if (TASK == QS_TASK_AVOIDANCE) sv = scene_view(sc, e);
   const V3 blo = R.blo, bhi = R.bhi;
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    const State& s = R.s[a];
-    RowPrm rp = row_params_v<M>(cfg, has_dr, R.dr[a]);
-    const float4 raw = raw_in[a];
-    ImuNoise z;
-    if (IMU == 1) z = imu_draw(cfg, row, R.meta.z);
-    {
-      const int c = !act_finite<A>(raw) ? QS_ERR_NONFINITE_ACTION
-                                        : (!state_finite<M>(s) ? QS_ERR_NONFINITE_STATE : 0);
-      err_row = (errc == 0 && c != 0) ? (int)row : err_row;
-      errc = errc != 0 ? errc : c;
-    }
-    Squash q = squash<A>(raw, rp);
-    float2 cs;
-    float4 cmd = world_cmd<M>(s, q.sq, k.g, cs);
-    State n = model_step<M>(s, cmd, rp, k);
-    n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;  // q/sensors.py:566
-    if (IMU == 1)
-      imu_apply_z<M>(cfg, row, n, (n.v - s.v) * (1.f / cfg.dt), k.g, R.ba[a], R.bg[a], v3(z.a.x, z.a.y, z.a.z),
-                     v3(z.a.w, z.b.x, z.b.y), v3(z.b.z, z.b.w, z.c.x), v3(z.c.y, z.c.z, z.c.w), out.imu_out);
-    else if (has_imu)
-      imu_apply<M>(cfg, row, N, R.meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g, R.ba[a], R.bg[a], out.imu_noise,
-                   out.imu_out);
-    const float4 pe = R.peff[a];
-    float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
-    float en = effnorm(q.eff, A), dn = effnorm(de, A);
-    R.peff[a] = q.eff;  // q/tasks.py:570
-    s2[a] = n;
-    codes[a] = 0;
-    p0 = s.p;
-    if (TASK != QS_TASK_RACING) {
-      V3 off = xyz(R.goal[a]) - n.p;
-      RewardFwd rf = reward_ctrl(cfg.w, off, n.v, en, dn);
-      float extra = 0.f;
-      if (TASK == QS_TASK_AVOIDANCE) {
-        int code;
-        float sd = sdf_eval(sv, n.p, code);
-        codes[a] = code;
-        rf.r -= cfg.w.w_o * softplus((cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness));
-        any_coll = any_coll || sd <= cfg.collision_radius;
-        extra = -(cfg.w_rl.w_o * softplus((cfg.d_safe - sd) / cfg.w_rl.sdf_sharpness));
-      }
-      rc[a] = rf.r;
-      rl[a] = reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn) + extra;
-      all_goal = all_goal && (rf.dist < cfg.success_radius) && (rf.speed < cfg.hover_speed);
-    }
-    any_oob = any_oob || n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x ||
-              n.p.y > bhi.y || n.p.z > bhi.z;
+  const State& s = R.s;
+  RowPrm rp = row_params_v<M>(cfg, has_dr, R.dr);
+  ImuNoise z;
+  if (IMU == 1) z = imu_draw(cfg, row, R.meta.z);
+  {
+    const int c = !act_finite<A>(raw) ? QS_ERR_NONFINITE_ACTION
+                                      : (!state_finite<M>(s) ? QS_ERR_NONFINITE_STATE : 0);
+    if (c != 0 && real) report_err(err, c, (int)row);
   }
-  if (errc != 0) report_err(err, errc, err_row);
+  Squash q = squash<A>(raw, rp);
+  float2 cs;
+  float4 cmd = world_cmd<M>(s, q.sq, k.g, cs);
+  State n = model_step<M>(s, cmd, rp, k);
+  n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;  // q/sensors.py:566
+  float4 ba = R.ba, bg = R.bg;
+  float imu[6];
+  if (IMU == 1)
+    imu_apply_z<M>(cfg, row, n, (n.v - s.v) * (1.f / cfg.dt), k.g, ba, bg, v3(z.a.x, z.a.y, z.a.z),
+                   v3(z.a.w, z.b.x, z.b.y), v3(z.b.z, z.b.w, z.c.x), v3(z.c.y, z.c.z, z.c.w), imu);
+  else if (has_imu)
+    imu_apply<M>(cfg, row, N, R.meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g, ba, bg, out.imu_noise, imu);
+  if (has_imu && real) {
+    float* o = out.imu_out + 6 * row;
+    o[0] = imu[0]; o[1] = imu[1]; o[2] = imu[2];
+    o[3] = imu[3]; o[4] = imu[4]; o[5] = imu[5];
+  }
+  R.ba = ba;
+  R.bg = bg;
+  const float4 pe = R.peff;
+  float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
+  float en = effnorm(q.eff, A), dn = effnorm(de, A);
+  R.peff = q.eff;  // q/tasks.py:570
+  int code = 0;
+  float rc = 0.f, rl = 0.f;
+  bool goal_ok = true, coll = false;
+  if (TASK != QS_TASK_RACING) {
+    V3 off = xyz(R.goal) - n.p;
+    RewardFwd rf = reward_ctrl(cfg.w, off, n.v, en, dn);
+    float extra = 0.f;
+    if (TASK == QS_TASK_AVOIDANCE) {
+      float sd = sdf_eval(sv, n.p, code);
+      rf.r -= cfg.w.w_o * softplus((cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness));
+      coll = sd <= cfg.collision_radius;
+      extra = -(cfg.w_rl.w_o * softplus((cfg.d_safe - sd) / cfg.w_rl.sdf_sharpness));
+    }
+    rc = rf.r;
+    rl = reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn) + extra;
+    goal_ok = (rf.dist < cfg.success_radius) && (rf.speed < cfg.hover_speed);
+  }
+  const bool oob = n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x || n.p.y > bhi.y ||
+                   n.p.z > bhi.z;
   // ---- per-env couplings
+  int term_env = 0;
   float r_goal = 0.f;
   int next_gate = R.meta.w;
-  if (TASK == QS_TASK_RACING) {  // q/tasks.py:925-972
+  if (TASK == QS_TASK_RACING) {  // q/tasks.py:925-972 (single agent)
     const qs_weights& w = cfg.w_rl;
+    const V3 p0 = s.p;
     GateV gt = load_gate(sc, cfg, e, next_gate);
-    V3 p1 = s2[0].p;
+    V3 p1 = n.p;
     float r = w.w_g * (norm3(p0 - gt.c) - norm3(p1 - gt.c));
     float sa = dot(p0 - gt.c, gt.n), sb = dot(p1 - gt.c, gt.n);
     if (sa < 0.f && sb >= 0.f) {
@@ -659,45 +674,49 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, i
       }
       if (passed && !finished) {
         next_gate += 1;
-        R.goal[0] = f4(load_gate(sc, cfg, e, next_gate).c, 0.f);
+        R.goal = f4(load_gate(sc, cfg, e, next_gate).c, 0.f);
       }
     }
-    if (any_oob && term_env == 0) {
+    if (oob && term_env == 0) {
       term_env = 3;
       r_goal = -1.f;
       r -= w.goal_bonus;
     }
-    rc[0] = 0.f;
-    rl[0] = r;
+    rc = 0.f;
+    rl = r;
   } else {
-    if (na > 1) {  // q/tasks.py:173-192
-      float pen = 0.f;
-      for (int i = 0; i < na; ++i)
-        for (int j = i + 1; j < na; ++j) {
-          float dij = norm3(s2[i].p - s2[j].p);
-          float t = dij - cfg.form_ref[i][j];
-          pen = pen + t * t;
-          any_coll = any_coll || dij < cfg.d_min;
-        }
-      pen *= cfg.w.w_f;
+    bool all_goal = grp.all(goal_ok || !real);
+    bool any_oob = grp.any(oob && real);
+    bool any_coll = grp.any(coll && real);
+    if (G > 1 && na > 1) {  // formation penalty + inter-agent collision (q/tasks.py:173-192)
+      float part = 0.f;
+      bool close = false;
 #pragma unroll
-      for (int a = 0; a < NAMAX; ++a)
-        if (a < na) rc[a] -= pen;
+      for (int j = 0; j < G; ++j) {
+        const V3 pj = grp.bcast(n.p, j);
+        if (real && j > grp.g && j < na) {
+          float dij = norm3(n.p - pj);
+          float t = dij - cfg.form_ref[grp.g][j];
+          part = part + t * t;
+          close = close || dij < cfg.d_min;
+        }
+      }
+      const float pen = grp.sum(part) * cfg.w.w_f;
+      any_coll = any_coll || grp.any(close);
+      rc -= pen;
     }
     // precedence: success, then bounds, then collision overwrite (q/tasks.py:734-737)
     if (all_goal) term_env = 1;
     if (any_oob) term_env = 3;
     if (any_coll) term_env = 2;
     r_goal = term_env == 1 ? 1.f : (term_env != 0 ? -1.f : 0.f);
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a)
-      if (a < na) rl[a] = rl[a] + cfg.w_rl.goal_bonus * r_goal;
+    rl = rl + cfg.w_rl.goal_bonus * r_goal;
   }
-  // ---- counters, truncation (q/tasks.py:574-591, 606-611)
+  // ---- counters, truncation (q/tasks.py:574-591, 606-611); the return is agent 0's
   int steps = R.meta.x + 1;
   const bool trunc = steps >= cfg.episode_len && term_env == 0;
   const bool done = term_env != 0 || trunc;
-  const float ret = R.ep_ret + rl[0];
+  const float ret = R.ep_ret + grp.bcast(rl, 0);
   int episode = R.meta.y;
   if (done) {
     steps = 0;
@@ -709,260 +728,234 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, i
   }
   R.meta = make_int4(steps, episode, R.meta.z + 1, next_gate);
   // ---- auto-reset (inline Philox) or keep
-  V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
-  int ng0 = 0;
-  if (INLINE && done) {
-    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, episode, na, R.blo, R.bhi, sp_p, sp_v, sp_g, head, ng0);
-    if (!ok) report_err(err, QS_ERR_GENERATION, (int)(e * na));
-  }
-  GateV g0, g1;
-  if (TASK == QS_TASK_RACING && INLINE) {
-    int ngate = done ? 0 : next_gate;
-    g0 = load_gate(sc, cfg, e, ngate);
-    g1 = load_gate(sc, cfg, e, min(ngate + 1, cfg.n_gates - 1));
-  }
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    out.r_ctrl[row] = rc[a];
-    out.r_goal[row] = r_goal;
-    out.r_rl[row] = rl[a];
-    out.term[row] = (int8_t)term_env;
-    out.trunc[row] = trunc ? 1 : 0;
-    State so = s2[a];
-    if (done) {
-      R.peff[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (has_imu) {
-        R.ba[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-        R.bg[a] = make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      if (INLINE) {
-        so = init_state<M>(sp_p[a], sp_v[a], head, k.g);
-        R.goal[a] = f4(sp_g[a], 0.f);
-        if (cfg.dr_enabled && cfg.dr_per_episode) R.dr[a] = dr_sample(cfg, row, episode);
-      }
+  State so = n;
+  if (done) {
+    R.peff = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (has_imu) {
+      R.ba = make_float4(0.f, 0.f, 0.f, 0.f);
+      R.bg = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    R.s[a] = so;
-    int fl = (done ? FLAG_DONE : 0) | (codes[a] << FLAG_SDF_SHIFT);
-    if (INLINE && out.obs) {
-      float o[P];
-      float2 cs = yaw_cs<M>(so, k.g);
-      fl |= observe_row<M, TASK>(cfg, so, cs, xyz(R.goal[a]), &g0, &g1, o);
+    if (INLINE) {
+      V3 sp, sv_, sg, head;
+      int ng0;
+      bool ok = spawn_sample<M, TASK, G>(cfg, sc, e, episode, na, R.blo, R.bhi, grp, sp, sv_, sg, head, ng0);
+      if (!ok && grp.g == 0) report_err(err, QS_ERR_GENERATION, (int)(e * na));
+      so = init_state<M>(sp, sv_, head, k.g);
+      R.goal = f4(sg, 0.f);
+      if (cfg.dr_enabled && cfg.dr_per_episode) R.dr = dr_sample(cfg, row, episode);
+    }
+  }
+  R.s = so;
+  int fl = (done ? FLAG_DONE : 0) | (code << FLAG_SDF_SHIFT);
+  if (INLINE && out.obs) {
+    GateV g0, g1;
+    if (TASK == QS_TASK_RACING) {
+      int ngate = done ? 0 : next_gate;
+      g0 = load_gate(sc, cfg, e, ngate);
+      g1 = load_gate(sc, cfg, e, min(ngate + 1, cfg.n_gates - 1));
+    }
+    float o[P];
+    float2 cs2 = yaw_cs<M>(so, k.g);
+    fl |= observe_row<M, TASK>(cfg, so, cs2, xyz(R.goal), &g0, &g1, o);
+    if (real) {
       float* dst = out.obs + row * P;
 #pragma unroll
       for (int kk = 0; kk < P; ++kk) dst[kk] = o[kk];
-      if (out.cam) reinterpret_cast<float2*>(out.cam)[row] = cs;
+      if (out.cam) reinterpret_cast<float2*>(out.cam)[row] = cs2;
     }
+  }
+  if (real) {
+    out.r_ctrl[row] = rc;
+    out.r_goal[row] = r_goal;
+    out.r_rl[row] = rl;
+    out.term[row] = (int8_t)term_env;
+    out.trunc[row] = trunc ? 1 : 0;
     out.flags[row] = fl;
   }
-  float rc_sum = 0.f;
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a)
-    if (a < na) rc_sum += rc[a];
-  return StepStat{done, term_env, ret, rc_sum};
+  return StepStat{done, term_env, ret, real ? rc : 0.f};
 }
 
 // ---------------------------------------------------------------------------
-// analytic VJP of one step.  Inputs: the step's checkpoint (pre-step state s_in,
-// raw action, goal, previous effort, per-row params, flags), upstream grads of
-// the post-step state (gS, in/out: replaced by the grad of s_in), of the
-// observation (g_obs, may be NULL) and of r_ctrl (per row or a scalar).
+// analytic VJP of one agent row's step.  Inputs: the step's checkpoint
+// (pre-step state s, raw action, goal, previous effort, per-row params,
+// flags), the upstream grad of the post-step state (gS, in/out: replaced by
+// the grad of s), of the observation (g_obs, may be NULL) and of r_ctrl (per
+// row or a scalar).  The formation penalty's VJP is the group's only coupling.
 
-template <int M, int TASK, int NAMAX>
-QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, int na, long N,
-                       const State* s_in, const float4* raw_in, const float4* goal, const float4* peff,
-                       const float4* dr, bool has_dr, const int* flags_in, const float* g_obs,
-                       const float* g_r_rows, float g_r_scalar, State* gS, float* g_raw_t,
-                       const State* s2_known = nullptr) {
+template <int M, int TASK, int G>
+QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, long row, int na, long N,
+                       const Grp<G>& grp, const State& s, float4 raw, float4 goal, float4 peff, float4 dr,
+                       bool has_dr, int fl, const float* g_obs, const float* g_r_rows, float g_r_scalar, State& gS,
+                       float* g_raw_t, const State* s2_known = nullptr) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
   const DynK k = dyn_consts(cfg);
-  State s2[NAMAX], g2[NAMAX];
-  float4 cmd[NAMAX];
-  float2 csc[NAMAX];
-  float4 geff[NAMAX];
-  float gr_r[NAMAX];
+  const bool real = grp.real;
   SceneView sv;
   if (TASK == QS_TASK_AVOIDANCE) sv = scene_view(sc, e);
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    const State& s = s_in[a];
-    RowPrm rp = row_params_v<M>(cfg, has_dr, dr[a]);
-    const float4 raw = raw_in[a];
-    Squash q = squash<A>(raw, rp);
-    float2 cs;
-    float4 c = world_cmd<M>(s, q.sq, k.g, cs);
-    const int fl = flags_in[a];
-    const bool done = fl & FLAG_DONE;
-    State n;
-    if (s2_known && !done) {
-      n = s2_known[a];  // the next checkpoint is this step's post-dynamics state
-    } else {  // reset rows: the checkpoint holds the respawned state, recompute
-      n = model_step<M>(s, c, rp, k);
-      n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;
-    }
-    State g = done ? zero_state() : gS[a];
-    g.ve = v3(0.f, 0.f, 0.f);
-    // observation path (only rows that were not reset; q/tasks.py:584-594)
-    if (!done && g_obs) {
-      const float* go = g_obs + row * P;
-      float2 cs2 = yaw_cs<M>(n, k.g);
-      V3 gg = v3(go[0], go[1], go[2]);
-      int cb = fl >> FLAG_CLAMP_SHIFT;
-      gg = v3((cb & 1) ? gg.x : 0.f, (cb & 2) ? gg.y : 0.f, (cb & 4) ? gg.z : 0.f);
-      g.p -= rotz(cs2, gg);  // unrot^T = rot
-      g.v += rotz(cs2, v3(go[3], go[4], go[5]));
-      if (M == QS_MODEL_SIMPLIFIED) {
-        g.r2 += rotz(cs2, v3(go[6], go[7], go[8]));
-      } else if (M == QS_MODEL_FULL) {
-        V3 gz = rotz(cs2, v3(go[6], go[7], go[8]));
-        Q4 gq = qrot_vjp_q(n.q, v3(0.f, 0.f, 1.f), gz);
-        g.q = q4(g.q.w + gq.w, g.q.x + gq.x, g.q.y + gq.y, g.q.z + gq.z);
-        g.w += v3(go[9], go[10], go[11]);
-      } else {
-        g.x += rotz(cs2, v3(go[6], go[7], go[8]));
-      }
-      if (TASK == QS_TASK_RACING) {
-        const int kk = ModelTraits<M>::P;
-        V3 ga = v3((cb & 8) ? go[kk] : 0.f, (cb & 16) ? go[kk + 1] : 0.f, (cb & 32) ? go[kk + 2] : 0.f);
-        V3 gb = v3((cb & 64) ? go[kk + 6] : 0.f, (cb & 128) ? go[kk + 7] : 0.f,
-                   (cb & 256) ? go[kk + 8] : 0.f);
-        g.p -= rotz(cs2, ga + gb);
-      }
-    }
-    float grr = g_r_rows ? g_r_rows[row] : g_r_scalar;
-    float4 ge = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (TASK != QS_TASK_RACING && grr != 0.f) {
-      float4 pe = peff[a];
-      float4 de = make_float4(q.eff.x - pe.x, q.eff.y - pe.y, q.eff.z - pe.z, q.eff.w - pe.w);
-      V3 off = xyz(goal[a]) - n.p;
-      V3 goff, gv;
-      reward_ctrl_vjp(cfg.w, off, n.v, q.eff, de, A, grr, goff, gv, ge);
-      g.p -= goff;
-      g.v += gv;
-      if (TASK == QS_TASK_AVOIDANCE) {
-        const int code = fl >> FLAG_SDF_SHIFT;  // argmin recorded by the forward
-        if (code != 0) {
-          float sd = sdf_prim(sv, n.p, code);
-          float arg = (cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness);
-          float gsd = grr * cfg.w.w_o * sigmoid_stable(arg) * (1.f / cfg.w.sdf_sharpness);
-          g.p += sdf_grad(sv, n.p, code) * gsd;
-        }
-      }
-    }
-    s2[a] = n;
-    g2[a] = g;
-    cmd[a] = c;
-    csc[a] = cs;
-    geff[a] = ge;
-    gr_r[a] = grr;
+  RowPrm rp = row_params_v<M>(cfg, has_dr, dr);
+  Squash q = squash<A>(raw, rp);
+  float2 cs;
+  float4 c = world_cmd<M>(s, q.sq, k.g, cs);
+  const bool done = fl & FLAG_DONE;
+  State n;
+  if (s2_known && !done) {
+    n = *s2_known;  // the next checkpoint is this step's post-dynamics state
+  } else {  // reset rows: the checkpoint holds the respawned state, recompute
+    n = model_step<M>(s, c, rp, k);
+    n.ve = s.ve * (1.f - cfg.yaw_ema_alpha) + n.v * cfg.yaw_ema_alpha;
   }
-  if (TASK != QS_TASK_RACING && na > 1) {  // formation penalty VJP
-    float gpen = 0.f;
-    for (int a = 0; a < na; ++a) gpen -= gr_r[a];
-    gpen *= cfg.w.w_f;
-    for (int i = 0; i < na; ++i)
-      for (int j = i + 1; j < na; ++j) {
-        V3 d = s2[i].p - s2[j].p;
-        float dij = norm3(d);
-        float gd = gpen * 2.f * (dij - cfg.form_ref[i][j]);
-        V3 gv = norm_vjp(d, dij, gd);
-        g2[i].p += gv;
-        g2[j].p -= gv;
-      }
-  }
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    RowPrm rp = row_params_v<M>(cfg, has_dr, dr[a]);
-    State gi;
-    float4 gc;
-    model_step_vjp<M>(s_in[a], cmd[a], rp, k, g2[a], gi, gc);
-    float4 gsq;
-    if (M == QS_MODEL_FULL || M == QS_MODEL_SIMPLIFIED) {
-      gsq = gc;
+  State g = done ? zero_state() : gS;
+  g.ve = v3(0.f, 0.f, 0.f);
+  // observation path (only rows that were not reset; q/tasks.py:584-594)
+  if (!done && g_obs) {
+    const float* go = g_obs + row * P;
+    float2 cs2 = yaw_cs<M>(n, k.g);
+    V3 gg = v3(go[0], go[1], go[2]);
+    int cb = fl >> FLAG_CLAMP_SHIFT;
+    gg = v3((cb & 1) ? gg.x : 0.f, (cb & 2) ? gg.y : 0.f, (cb & 4) ? gg.z : 0.f);
+    g.p -= rotz(cs2, gg);  // unrot^T = rot
+    g.v += rotz(cs2, v3(go[3], go[4], go[5]));
+    if (M == QS_MODEL_SIMPLIFIED) {
+      g.r2 += rotz(cs2, v3(go[6], go[7], go[8]));
+    } else if (M == QS_MODEL_FULL) {
+      V3 gz = rotz(cs2, v3(go[6], go[7], go[8]));
+      Q4 gq = qrot_vjp_q(n.q, v3(0.f, 0.f, 1.f), gz);
+      g.q = q4(g.q.w + gq.w, g.q.x + gq.x, g.q.y + gq.y, g.q.z + gq.z);
+      g.w += v3(go[9], go[10], go[11]);
     } else {
-      V3 u = unrotz(csc[a], v3(gc.x, gc.y, gc.z));  // Rz^T g
-      gsq = make_float4(u.x, u.y, u.z, 0.f);
+      g.x += rotz(cs2, v3(go[6], go[7], go[8]));
     }
-    gsq = make_float4(gsq.x + geff[a].x, gsq.y + geff[a].y, gsq.z + geff[a].z, gsq.w + geff[a].w);
-    const float4 raw = raw_in[a];
+    if (TASK == QS_TASK_RACING) {
+      const int kk = ModelTraits<M>::P;
+      V3 ga = v3((cb & 8) ? go[kk] : 0.f, (cb & 16) ? go[kk + 1] : 0.f, (cb & 32) ? go[kk + 2] : 0.f);
+      V3 gb = v3((cb & 64) ? go[kk + 6] : 0.f, (cb & 128) ? go[kk + 7] : 0.f, (cb & 256) ? go[kk + 8] : 0.f);
+      g.p -= rotz(cs2, ga + gb);
+    }
+  }
+  const float grr = g_r_rows ? g_r_rows[row] : g_r_scalar;
+  float4 ge = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (TASK != QS_TASK_RACING && grr != 0.f) {
+    float4 de = make_float4(q.eff.x - peff.x, q.eff.y - peff.y, q.eff.z - peff.z, q.eff.w - peff.w);
+    V3 off = xyz(goal) - n.p;
+    V3 goff, gv;
+    reward_ctrl_vjp(cfg.w, off, n.v, q.eff, de, A, grr, goff, gv, ge);
+    g.p -= goff;
+    g.v += gv;
+    if (TASK == QS_TASK_AVOIDANCE) {
+      const int code = fl >> FLAG_SDF_SHIFT;  // argmin recorded by the forward
+      if (code != 0) {
+        float sd = sdf_prim(sv, n.p, code);
+        float arg = (cfg.d_safe - sd) * (1.f / cfg.w.sdf_sharpness);
+        float gsd = grr * cfg.w.w_o * sigmoid_stable(arg) * (1.f / cfg.w.sdf_sharpness);
+        g.p += sdf_grad(sv, n.p, code) * gsd;
+      }
+    }
+  }
+  if (TASK != QS_TASK_RACING && G > 1 && na > 1) {  // formation penalty VJP
+    // pen is subtracted from every agent's r_ctrl: dL/dpen = -sum_a dL/dr_a
+    const float gpen = -grp.sum(real ? grr : 0.f) * cfg.w.w_f;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const V3 pj = grp.bcast(n.p, j);
+      if (real && j != grp.g && j < na) {
+        V3 d = n.p - pj;
+        float dij = norm3(d);
+        const int a0 = min(grp.g, j), a1 = max(grp.g, j);
+        float gd = gpen * 2.f * (dij - cfg.form_ref[a0][a1]);
+        g.p += norm_vjp(d, dij, gd);
+      }
+    }
+  }
+  State gi;
+  float4 gc;
+  model_step_vjp<M>(s, c, rp, k, g, gi, gc);
+  float4 gsq;
+  if (M == QS_MODEL_FULL || M == QS_MODEL_SIMPLIFIED) {
+    gsq = gc;
+  } else {
+    V3 u = unrotz(cs, v3(gc.x, gc.y, gc.z));  // Rz^T g
+    gsq = make_float4(u.x, u.y, u.z, 0.f);
+  }
+  gsq = make_float4(gsq.x + ge.x, gsq.y + ge.y, gsq.z + ge.z, gsq.w + ge.w);
+  if (real) {
     float* gout = g_raw_t + row * A;
 #pragma unroll
     for (int kk = 0; kk < A; ++kk) {
       float t = tanh_fast(f4get(raw, kk));
       gout[kk] = f4get(gsq, kk) * rp.half[kk] * (1.f - t * t);
     }
-    gS[a] = gi;
   }
+  gS = gi;
 }
+
+// ---------------------------------------------------------------------------
+// thread -> (env, agent row): G lanes per env, padding lanes read agent 0
+
+template <int G>
+struct RowMap {
+  long e, row;
+  bool active;  // e < n_envs (group-uniform)
+  QS_D static RowMap make(long t, int n_envs, int na) {
+    RowMap m;
+    m.e = G == 1 ? t : t / G;
+    const int g = G == 1 ? 0 : (int)(t & (G - 1));
+    m.row = m.e * na + (g < na ? g : 0);
+    m.active = m.e < n_envs;
+    return m;
+  }
+};
 
 // ---------------------------------------------------------------------------
 // per-step kernels (FlightTask.step and its autograd node)
 
-template <int M, int TASK, int NAMAX, bool INLINE>
+template <int M, int TASK, int G, bool INLINE>
 __global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const qs_scene sc,
                                                   const qs_step_io io) {
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = e < cfg.n_envs;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  const Grp<G> grp = Grp<G>::make(na);
   const long N = (long)cfg.n_envs * na;
-  StepStat st{false, 0, 0.f};
-  if (active) {
-    EnvRegs<NAMAX> R;
-    float4 raw[NAMAX];
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a)
-      if (a < na) raw[a] = load_act<ModelTraits<M>::A>(io.raw, e * na + a);
-    env_load<M, NAMAX>(cfg, sc.bounds, e, na, N, R, io.S_in, io.goal_in, io.peff_in, io.dr_in, io.meta,
-                       io.ep_return, io.imu_bias);
+  StepStat st{false, 0, 0.f, 0.f};
+  if (rm.active) {
+    EnvRegs R;
+    const float4 raw = load_act<ModelTraits<M>::A>(io.raw, rm.row);
+    env_load<M>(sc.bounds, rm.e, rm.row, N, R, io.S_in, io.goal_in, io.peff_in, io.dr_in, io.meta,
+                io.ep_return, io.imu_bias);
     StepOut o{io.obs, io.r_ctrl, io.r_goal, io.r_rl, io.terminated, io.truncated, io.flags, io.cam,
               io.imu_out, io.imu_noise};
-    st = env_step_fwd<M, TASK, NAMAX, INLINE>(cfg, sc, e, na, N, R, raw, o, io.err, io.dr_in != nullptr,
-                                             io.imu_out != nullptr);
-    env_store_ckpt<M, NAMAX>(e, na, N, R, io.S_out, io.goal_out, io.peff_out, io.dr_out);
-    env_store_inplace<NAMAX>(e, na, R, io.meta, io.ep_return, io.imu_out ? io.imu_bias : nullptr);
+    st = env_step_fwd<M, TASK, G, INLINE>(cfg, sc, rm.e, rm.row, na, N, grp, R, raw, o, io.err,
+                                          io.dr_in != nullptr, io.imu_out != nullptr);
+    if (grp.real) {
+      env_store_ckpt<M>(rm.row, N, R, io.S_out, io.goal_out, io.peff_out, io.dr_out);
+      env_store_inplace(rm.e, rm.row, grp.g == 0, R, io.meta, io.ep_return, io.imu_out ? io.imu_bias : nullptr);
+    }
   }
-  warp_stats(active, st.done, st.term, st.ret, io.stats);
+  warp_stats(rm.active && grp.g == 0, st.done, st.term, st.ret, io.stats);
 }
 
-template <int M, int TASK, int NAMAX>
+template <int M, int TASK, int G>
 __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const qs_scene sc,
                                                   const qs_step_grad gr) {
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= cfg.n_envs) return;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  if (!rm.active) return;
+  const Grp<G> grp = Grp<G>::make(na);
   const long N = (long)cfg.n_envs * na;
-  State s_in[NAMAX], gS[NAMAX];
-  float4 goal[NAMAX], peff[NAMAX], dr[NAMAX], raw[NAMAX];
-  int fl[NAMAX];
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    s_in[a] = load_state<M>(gr.S_in, N, row);
-    goal[a] = ld4(gr.goal_in, row);
-    peff[a] = ld4(gr.peff_in, row);
-    dr[a] = gr.dr_in ? ld4(gr.dr_in, row) : make_float4(0.f, 0.f, 0.f, 0.f);
-    raw[a] = load_act<ModelTraits<M>::A>(gr.raw, row);
-    fl[a] = __ldg(gr.flags + row);
-    gS[a] = load_grad<M>(gr.g_S_out, N, row);
-  }
-  env_step_bwd<M, TASK, NAMAX>(cfg, sc, e, na, N, s_in, raw, goal, peff, dr, gr.dr_in != nullptr, fl, gr.g_obs,
-                               gr.g_rctrl, 0.f, gS, gr.g_raw);
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    store_state<M>(gr.g_S_in, N, e * na + a, gS[a]);
-  }
+  const long row = rm.row;
+  const State s_in = load_state<M>(gr.S_in, N, row);
+  const float4 goal = ld4(gr.goal_in, row), peff = ld4(gr.peff_in, row);
+  const float4 dr = gr.dr_in ? ld4(gr.dr_in, row) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 raw = load_act<ModelTraits<M>::A>(gr.raw, row);
+  const int fl = __ldg(gr.flags + row);
+  State gS = load_grad<M>(gr.g_S_out, N, row);
+  env_step_bwd<M, TASK, G>(cfg, sc, rm.e, row, na, N, grp, s_in, raw, goal, peff, dr, gr.dr_in != nullptr, fl,
+                           gr.g_obs, gr.g_rctrl, 0.f, gS, gr.g_raw);
+  if (grp.real) store_state<M>(gr.g_S_in, N, row, gS);
 }
 
 // ---------------------------------------------------------------------------
-// fused T-step windows (open-loop actions): the env's register file stays on
+// fused T-step windows (open-loop actions): each row's register file stays on
 // chip for the whole window; only the per-step outputs and the backward's
 // checkpoints go to HBM, and the backward carries dL/dS in registers.
 
@@ -970,33 +963,36 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
 // on 148 SMs with <= 144 registers per thread
 constexpr int WIN_BLOCK = 64;
 
-template <int M, int TASK, int NAMAX, int IMU>
+template <int M, int TASK, int G, int IMU>
 __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg cfg, const qs_scene sc,
                                                     const qs_window_io w) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const bool active = e < cfg.n_envs;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  const Grp<G> grp = Grp<G>::make(na);
+  const bool active = rm.active;
+  const long e = rm.e, row = rm.row;
   const long N = (long)cfg.n_envs * na;
   const int NP = ModelTraits<M>::NP;
   const bool has_dr = w.dr != nullptr, has_imu = IMU == 1 || w.imu_out != nullptr;
-  EnvRegs<NAMAX> R;
+  EnvRegs R;
   int n_done = 0, n_succ = 0, n_coll = 0;
   float ret_sum = 0.f;
   double loss_sum = 0.0;
   float gpow = 1.f;
-  // The CTA's action block of a step (blockDim * na rows x A floats, contiguous)
-  // is staged in shared memory by a TMA bulk copy issued one step ahead into a
-  // double buffer, so the action latency never sits on the step's critical path
-  // and costs no registers.  Partial tail CTAs load directly.
-  constexpr int NB = NAMAX == 1 ? 4 : 2;  // ring depth: step t+NB is in flight during step t
-  __shared__ __align__(128) float s_raw[NB][WIN_BLOCK * NAMAX * 4];
+  // The CTA's action block of a step (its envs' rows x A floats, contiguous) is
+  // staged in shared memory by a TMA bulk copy into a 4-deep ring, 4 steps
+  // ahead, so the action latency never sits on the step's critical path and
+  // costs no registers.  Partial tail CTAs load directly.
+  constexpr int NB = 4;  // ring depth: step t+NB is in flight during step t
+  __shared__ __align__(128) float s_raw[NB][WIN_BLOCK * 4];
   __shared__ __align__(8) uint64_t s_bar[NB];
   __shared__ int s_free[NB];  // warps done with each buffer this round
-  const long e0 = (long)blockIdx.x * blockDim.x;
-  const uint32_t blk_bytes = (uint32_t)(blockDim.x * na * A * 4);
-  const bool use_tma = (e0 + blockDim.x <= cfg.n_envs) && (blk_bytes % 16 == 0) && ((N * A) % 4 == 0) &&
+  const int epc = blockDim.x / G;  // envs per CTA
+  const long e0 = (long)blockIdx.x * epc;
+  const uint32_t blk_bytes = (uint32_t)(epc * na * A * 4);
+  const bool use_tma = (e0 + epc <= cfg.n_envs) && (blk_bytes % 16 == 0) && ((N * A) % 4 == 0) &&
                        ((reinterpret_cast<uintptr_t>(w.actions) & 15) == 0);
   if (use_tma && threadIdx.x == 0) {
     for (int b = 0; b < NB; ++b) {
@@ -1011,45 +1007,40 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
       tma_load_1d(s_raw[b], w.actions + ((long)b * N + e0 * na) * A, blk_bytes, &s_bar[b]);
   }
   if (active)
-    env_load<M, NAMAX>(cfg, sc.bounds, e, na, N, R, w.S, w.goal, w.peff, w.dr, w.meta, w.ep_return,
-                       w.imu_bias);
+    env_load<M>(sc.bounds, e, row, N, R, w.S, w.goal, w.peff, w.dr, w.meta, w.ep_return, w.imu_bias);
+  const int lrow = (int)(row - e0 * na);  // this row's slot in the CTA's action block
   for (int t = 0; t < w.T; ++t) {
-    float4 raw[NAMAX];
+    float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
     if (use_tma) {
       mbar_wait(&s_bar[t % NB], (t / NB) & 1);
-      const float* sr = s_raw[t % NB];
-#pragma unroll
-      for (int a = 0; a < NAMAX; ++a) {
-        if (a >= na) break;
-        const float* p = sr + (threadIdx.x * na + a) * A;
-        raw[a] = make_float4(p[0], p[1], p[2], A == 4 ? p[3] : 0.f);
-      }
+      const float* p = s_raw[t % NB] + lrow * A;
+      raw = make_float4(p[0], p[1], p[2], A == 4 ? p[3] : 0.f);
     } else if (active) {
-#pragma unroll
-      for (int a = 0; a < NAMAX; ++a)
-        if (a < na) raw[a] = load_act<A>(w.actions + (long)t * N * A, e * na + a);
+      raw = load_act<A>(w.actions + (long)t * N * A, row);
     }
     if (active) {
       StepOut o{w.obs ? w.obs + (long)t * N * P : nullptr, w.r + (long)t * 3 * N, w.r + (long)t * 3 * N + N,
                 w.r + (long)t * 3 * N + 2 * N, w.terminated + (long)t * N, w.truncated + (long)t * N,
                 w.flags + (long)t * N, nullptr, has_imu ? w.imu_out + (long)t * N * 6 : nullptr,
                 w.imu_noise ? w.imu_noise + (long)t * 4 * N * 3 : nullptr};
-      StepStat st = env_step_fwd<M, TASK, NAMAX, true, IMU>(cfg, sc, e, na, N, R, raw, o, w.err, has_dr, has_imu);
-      if (st.done) {
+      StepStat st = env_step_fwd<M, TASK, G, true, IMU>(cfg, sc, e, row, na, N, grp, R, raw, o, w.err, has_dr,
+                                                        has_imu);
+      if (st.done && grp.g == 0) {
         n_done++;
         n_succ += st.term == 1;
         n_coll += st.term == 2;
         ret_sum += st.ret;
       }
-      loss_sum += (double)(gpow * st.rc_sum);
+      loss_sum += (double)(gpow * st.rc);
       gpow *= w.gamma;
-      env_store_ckpt<M, NAMAX>(e, na, N, R, w.S + (long)(t + 1) * NP * N * 4, w.goal + (long)(t + 1) * N * 4,
-                               w.peff + (long)(t + 1) * N * 4, has_dr ? w.dr + (long)(t + 1) * N * 4 : nullptr);
+      if (grp.real)
+        env_store_ckpt<M>(row, N, R, w.S + (long)(t + 1) * NP * N * 4, w.goal + (long)(t + 1) * N * 4,
+                          w.peff + (long)(t + 1) * N * 4, has_dr ? w.dr + (long)(t + 1) * N * 4 : nullptr);
     }
     if (use_tma) {
-      // No CTA barrier: the last warp to finish with buffer t&1 (its lanes'
-      // actions have fed this step) refills it with step t+2, so warps drift
-      // freely by up to a step instead of meeting every step.
+      // No CTA barrier: the last warp to finish with buffer t%NB (its lanes'
+      // actions have fed this step) refills it with step t+NB, so warps drift
+      // freely by up to a few steps instead of meeting every step.
       __syncwarp();
       if ((threadIdx.x & 31) == 0) {
         __threadfence_block();
@@ -1064,7 +1055,8 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
       }
     }
   }
-  if (active) env_store_inplace<NAMAX>(e, na, R, w.meta, w.ep_return, has_imu ? w.imu_bias : nullptr);
+  if (active && grp.real)
+    env_store_inplace(e, row, grp.g == 0, R, w.meta, w.ep_return, has_imu ? w.imu_bias : nullptr);
   // episode statistics and the BPTT loss: one warp reduction for the window
   double r = ret_sum;
   double ls = loss_sum;
@@ -1086,58 +1078,30 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
   }
 }
 
-template <int M, int TASK, int NAMAX>
+template <int M, int TASK, int G>
 __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg cfg, const qs_scene sc,
                                                     const qs_window_io w) {
   constexpr int A = ModelTraits<M>::A;
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= cfg.n_envs) return;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  if (!rm.active) return;  // group-uniform
+  const Grp<G> grp = Grp<G>::make(na);
+  const long e = rm.e, row = rm.row;
   const long N = (long)cfg.n_envs * na;
   const int NP = ModelTraits<M>::NP;
   const bool has_dr = w.dr != nullptr;
-  State gS[NAMAX];
-  // double-buffered checkpoint of step t (cur) and t-1 (nxt): loads of the
-  // previous step are independent of the dL/dS chain, so they are issued a
-  // whole step ahead
-  struct Ck {
-    State s;
-    float4 goal, peff, dr, raw;
-    int fl;
-  };
-  Ck cur[NAMAX], nxt[NAMAX];
-  auto load_ck = [&](int t, Ck* c) {
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      const long row = e * na + a;
-      c[a].s = load_state<M>(w.S + (long)t * NP * N * 4, N, row);
-      c[a].goal = ld4(w.goal + (long)t * N * 4, row);
-      c[a].peff = ld4(w.peff + (long)t * N * 4, row);
-      c[a].dr = has_dr ? ld4(w.dr + (long)t * N * 4, row) : make_float4(0.f, 0.f, 0.f, 0.f);
-      c[a].raw = load_act<A>(w.actions + (long)t * N * A, row);
-      c[a].fl = __ldg(w.flags + (long)t * N + row);
-    }
-  };
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    gS[a] = load_grad<M>(w.g_S_final, N, e * na + a);
-  }
-  // Single-agent rows stream their checkpoints through a per-thread cp.async
-  // ring in shared memory, NST steps ahead: the loads hold no registers while
-  // in flight and each thread waits only for its own copies (no barrier).
-  // Multi-agent rows load one step ahead into registers.
+  State gS = load_grad<M>(w.g_S_final, N, row);
+  // Each thread streams its row's checkpoints through a private cp.async ring
+  // in shared memory, NST steps ahead: the loads hold no registers while in
+  // flight and each thread waits only for its own copies (no barrier).
   constexpr int NST = 3;
   constexpr int NPL = ModelTraits<M>::NP;
   constexpr int NREC = NPL + 4;  // state planes, goal, peff, dr, raw
-  __shared__ __align__(16) float4 ring[NAMAX == 1 ? NST : 1][NREC][WIN_BLOCK];
-  __shared__ int ring_fl[NAMAX == 1 ? NST : 1][WIN_BLOCK];
+  __shared__ __align__(16) float4 ring[NST][NREC][WIN_BLOCK];
+  __shared__ int ring_fl[NST][WIN_BLOCK];
   const int tx = threadIdx.x;
-  const bool use_ring = NAMAX == 1 && blockDim.x <= WIN_BLOCK;
-  auto issue = [&](int t, int b) {  // this thread's rows of step t -> stage b
+  auto issue = [&](int t, int b) {  // this thread's row of step t -> stage b
     if (t >= 0) {
-      const long row = e;
 #pragma unroll
       for (int k = 0; k < NPL; ++k) cp_async16(&ring[b][k][tx], w.S + (((long)t * NP + k) * N + row) * 4);
       cp_async16(&ring[b][NPL][tx], w.goal + ((long)t * N + row) * 4);
@@ -1151,144 +1115,96 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
     }
     cp_async_commit();  // one group per step, possibly empty, keeps the count uniform
   };
-  auto read_stage = [&](int b, Ck* c) {
-    c[0].s = load_state<M, true>(&ring[b][0][0].x, WIN_BLOCK, tx);
-    c[0].goal = ring[b][NPL][tx];
-    c[0].peff = ring[b][NPL + 1][tx];
-    c[0].dr = has_dr ? ring[b][NPL + 2][tx] : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 r = ring[b][NPL + 3][tx];
-    c[0].raw = make_float4(r.x, r.y, r.z, A == 4 ? r.w : 0.f);
-    c[0].fl = ring_fl[b][tx];
-  };
-  if (use_ring) {
-    for (int k = 0; k < NST; ++k) issue(w.T - 1 - k, k);
-  } else {
-    load_ck(w.T - 1, cur);
-  }
-  State s2[NAMAX];  // checkpoint t+1 = post-dynamics state of step t (non-reset rows)
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    s2[a] = load_state<M>(w.S + (long)w.T * NP * N * 4, N, e * na + a);
-  }
+  for (int k = 0; k < NST; ++k) issue(w.T - 1 - k, k);
+  // checkpoint t+1 = post-dynamics state of step t (non-reset rows)
+  State s2 = load_state<M>(w.S + (long)w.T * NP * N * 4, N, row);
   const float lg_gamma = log2f(w.gamma);  // gamma^t = 2^(t lg): one MUFU.EX2 per step
   for (int t = w.T - 1; t >= 0; --t) {
     const float gscale = w.g_rctrl_scale * (t == 0 ? 1.f : exp2f((float)t * lg_gamma));
     const int kk = w.T - 1 - t;
-    if (use_ring) {
-      cp_async_wait<NST - 1>();  // this thread's copies of step t have landed
-      read_stage(kk % NST, cur);
-    } else if (t > 0) {
-      load_ck(t - 1, nxt);
-    }
-    State s_in[NAMAX];
-    float4 goal[NAMAX], peff[NAMAX], dr[NAMAX], raw[NAMAX];
-    int fl[NAMAX];
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      s_in[a] = cur[a].s;
-      goal[a] = cur[a].goal;
-      peff[a] = cur[a].peff;
-      dr[a] = cur[a].dr;
-      raw[a] = cur[a].raw;
-      fl[a] = cur[a].fl;
-    }
-    env_step_bwd<M, TASK, NAMAX>(cfg, sc, e, na, N, s_in, raw, goal, peff, dr, has_dr, fl, nullptr,
-                                 w.g_rctrl ? w.g_rctrl + (long)t * N : nullptr, gscale, gS,
-                                 w.g_actions + (long)t * N * A, s2);
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      s2[a] = cur[a].s;
-      if (!use_ring) cur[a] = nxt[a];
-    }
-    if (use_ring) issue(t - NST, kk % NST);  // the stage just consumed takes step t - NST
+    const int b = kk % NST;
+    cp_async_wait<NST - 1>();  // this thread's copies of step t have landed
+    const State s_in = load_state<M, true>(&ring[b][0][0].x, WIN_BLOCK, tx);
+    const float4 goal = ring[b][NPL][tx], peff = ring[b][NPL + 1][tx];
+    const float4 dr = has_dr ? ring[b][NPL + 2][tx] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 rr = ring[b][NPL + 3][tx];
+    const float4 raw = make_float4(rr.x, rr.y, rr.z, A == 4 ? rr.w : 0.f);
+    const int fl = ring_fl[b][tx];
+    env_step_bwd<M, TASK, G>(cfg, sc, e, row, na, N, grp, s_in, raw, goal, peff, dr, has_dr, fl, nullptr,
+                             w.g_rctrl ? w.g_rctrl + (long)t * N : nullptr, gscale, gS,
+                             w.g_actions + (long)t * N * A, &s2);
+    s2 = s_in;
+    issue(t - NST, b);  // the stage just consumed takes step t - NST
   }
-  if (w.g_S0) {
-#pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      store_state<M>(w.g_S0, N, e * na + a, gS[a]);
-    }
-  }
-  if (w.carry) {  // this thread's rows only: slot 0 was its last checkpoint read
+  if (!grp.real) return;
+  if (w.g_S0) store_state<M>(w.g_S0, N, row, gS);
+  if (w.carry) {  // this thread's row only: slot 0 was its last checkpoint read
     const long T = w.T;
 #pragma unroll
-    for (int a = 0; a < NAMAX; ++a) {
-      if (a >= na) break;
-      const long row = e * na + a;
-#pragma unroll
-      for (int k = 0; k < NP; ++k) st4(w.S, (long)k * N + row, ld4(w.S + T * NP * N * 4, (long)k * N + row));
-      st4(w.goal, row, ld4(w.goal + T * N * 4, row));
-      st4(w.peff, row, ld4(w.peff + T * N * 4, row));
-      if (has_dr) st4(w.dr, row, ld4(w.dr + T * N * 4, row));
-    }
+    for (int k = 0; k < NP; ++k) st4(w.S, (long)k * N + row, ld4(w.S + T * NP * N * 4, (long)k * N + row));
+    st4(w.goal, row, ld4(w.goal + T * N * 4, row));
+    st4(w.peff, row, ld4(w.peff + T * N * 4, row));
+    if (has_dr) st4(w.dr, row, ld4(w.dr + T * N * 4, row));
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // spawn (reset of masked envs), observe
 
-template <int M, int TASK, int NAMAX>
+template <int M, int TASK, int G>
 __global__ void __launch_bounds__(128) k_task_spawn(const qs_task_cfg cfg, const qs_scene sc,
                                                     const qs_step_io io, const uint8_t* mask,
                                                     const qs_reset_table tab, bool use_tab) {
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= cfg.n_envs) return;
-  if (mask && !mask[e]) return;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  if (!rm.active) return;
+  const long e = rm.e, row = rm.row;
+  if (mask && !mask[e]) return;  // env-uniform
+  const Grp<G> grp = Grp<G>::make(na);
   const long N = (long)cfg.n_envs * na;
   const DynK k = dyn_consts(cfg);
   int4 meta = reinterpret_cast<int4*>(io.meta)[e];
-  V3 sp_p[NAMAX], sp_v[NAMAX], sp_g[NAMAX], head = v3(0.f, 0.f, 0.f);
+  V3 p, v, gl, ve = v3(0.f, 0.f, 0.f);
   int ng0 = 0;
   if (!use_tab) {
     const V3 blo = xyz(ld4(sc.bounds, 2 * e)) + v3(1e-6f, 1e-6f, 1e-6f);  // as env_load
     const V3 bhi = xyz(ld4(sc.bounds, 2 * e + 1)) - v3(1e-6f, 1e-6f, 1e-6f);
-    bool ok = spawn_sample<M, TASK, NAMAX>(cfg, sc, e, meta.y, na, blo, bhi, sp_p, sp_v, sp_g, head, ng0);
-    if (!ok) report_err(io.err, QS_ERR_GENERATION, (int)(e * na));
-  } else if (tab.next_gate) {
-    ng0 = tab.next_gate[e];
+    bool ok = spawn_sample<M, TASK, G>(cfg, sc, e, meta.y, na, blo, bhi, grp, p, v, gl, ve, ng0);
+    if (!ok && grp.g == 0) report_err(io.err, QS_ERR_GENERATION, (int)(e * na));
+  } else {
+    if (tab.next_gate) ng0 = tab.next_gate[e];
+    p = load3(tab.p, row);
+    v = load3(tab.v, row);
+    gl = load3(tab.goal, row);
+    ve = load3(tab.v_ema, row);
   }
-  meta.w = ng0;
-  reinterpret_cast<int4*>(io.meta)[e] = meta;
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    V3 p, v, gl, ve;
-    if (use_tab) {
-      p = load3(tab.p, row);
-      v = load3(tab.v, row);
-      gl = load3(tab.goal, row);
-      ve = load3(tab.v_ema, row);
-    } else {
-      p = sp_p[a];
-      v = sp_v[a];
-      gl = sp_g[a];
-      ve = head;
-    }
-    store_state<M>(io.S_out, N, row, init_state<M>(p, v, ve, k.g));
-    st4(io.goal_out, row, f4(gl, 0.f));
-    st4(io.peff_out, row, make_float4(0.f, 0.f, 0.f, 0.f));
-    if (io.dr_out && cfg.dr_enabled) {
-      float4 d = use_tab && tab.dr ? ld4(tab.dr, row) : dr_sample(cfg, row, meta.y);
-      st4(io.dr_out, row, d);
-    }
-    if (io.imu_bias) {
-      st4(io.imu_bias, 2 * row, make_float4(0.f, 0.f, 0.f, 0.f));
-      st4(io.imu_bias, 2 * row + 1, make_float4(0.f, 0.f, 0.f, 0.f));
-    }
+  if (!grp.real) return;
+  if (grp.g == 0) {
+    meta.w = ng0;
+    reinterpret_cast<int4*>(io.meta)[e] = meta;
+  }
+  store_state<M>(io.S_out, N, row, init_state<M>(p, v, ve, k.g));
+  st4(io.goal_out, row, f4(gl, 0.f));
+  st4(io.peff_out, row, make_float4(0.f, 0.f, 0.f, 0.f));
+  if (io.dr_out && cfg.dr_enabled) {
+    float4 d = use_tab && tab.dr ? ld4(tab.dr, row) : dr_sample(cfg, row, meta.y);
+    st4(io.dr_out, row, d);
+  }
+  if (io.imu_bias) {
+    st4(io.imu_bias, 2 * row, make_float4(0.f, 0.f, 0.f, 0.f));
+    st4(io.imu_bias, 2 * row + 1, make_float4(0.f, 0.f, 0.f, 0.f));
   }
 }
 
-template <int M, int TASK, int NAMAX>
+template <int M, int TASK, int G>
 __global__ void __launch_bounds__(128) k_task_observe(const qs_task_cfg cfg, const qs_scene sc,
                                                       const qs_step_io io) {
   constexpr int P = TaskTraits<M, TASK>::P;
-  const long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= cfg.n_envs) return;
-  const int na = NAMAX == 1 ? 1 : cfg.n_agents;
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  const Grp<G> grp = Grp<G>::make(na);
+  if (!rm.active || !grp.real) return;
+  const long e = rm.e, row = rm.row;
   const long N = (long)cfg.n_envs * na;
   const DynK k = dyn_consts(cfg);
   GateV g0, g1;
@@ -1297,95 +1213,108 @@ __global__ void __launch_bounds__(128) k_task_observe(const qs_task_cfg cfg, con
     g0 = load_gate(sc, cfg, e, ng);
     g1 = load_gate(sc, cfg, e, min(ng + 1, cfg.n_gates - 1));
   }
-#pragma unroll
-  for (int a = 0; a < NAMAX; ++a) {
-    if (a >= na) break;
-    const long row = e * na + a;
-    State s = load_state<M>(io.S_out, N, row);
-    V3 goal = load3(io.goal_out, row);
-    float o[P];
-    float2 cs = yaw_cs<M>(s, k.g);
-    int bits = observe_row<M, TASK>(cfg, s, cs, goal, &g0, &g1, o);
-    write_obs<M, TASK>(cfg, io, row, o);
-    if (io.cam) reinterpret_cast<float2*>(io.cam)[row] = cs;
-    if (io.flags) io.flags[row] = (io.flags[row] & ~FLAG_CLAMP_MASK) | bits;
-  }
+  State s = load_state<M>(io.S_out, N, row);
+  V3 goal = load3(io.goal_out, row);
+  float o[P];
+  float2 cs = yaw_cs<M>(s, k.g);
+  int bits = observe_row<M, TASK>(cfg, s, cs, goal, &g0, &g1, o);
+  write_obs<M, TASK>(cfg, io, row, o);
+  if (io.cam) reinterpret_cast<float2*>(io.cam)[row] = cs;
+  if (io.flags) io.flags[row] = (io.flags[row] & ~FLAG_CLAMP_MASK) | bits;
 }
 
 // ---------------------------------------------------------------------------
 // per-task launchers (one translation unit per task keeps builds parallel)
 
-inline int grid_for(int n, int block) { return (n + block - 1) / block; }
+inline int grid_for(long n, int block) { return (int)((n + block - 1) / block); }
 inline int launch_status() { return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH; }
 
-// per-step kernels: 128-thread CTAs, or 32 when too few envs to fill the SMs
-inline int step_block(int n_envs) { return n_envs >= 148 * 2 * 128 ? 128 : 32; }
+// per-step kernels: 128-thread CTAs, or 32 when too few rows to fill the SMs
+inline int step_block(long threads) { return threads >= 148 * 2 * 128 ? 128 : 32; }
 
-template <int M, int T, int NA>
+template <int M, int T, int G>
 int run_fwd(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, cudaStream_t s) {
-  const int b = step_block(cfg->n_envs);
+  const long th = (long)cfg->n_envs * G;
+  const int b = step_block(th);
   if (cfg->reset_mode == 0)
-    k_task_fwd<M, T, NA, true><<<grid_for(cfg->n_envs, b), b, 0, s>>>(*cfg, *sc, *io);
+    k_task_fwd<M, T, G, true><<<grid_for(th, b), b, 0, s>>>(*cfg, *sc, *io);
   else
-    k_task_fwd<M, T, NA, false><<<grid_for(cfg->n_envs, b), b, 0, s>>>(*cfg, *sc, *io);
+    k_task_fwd<M, T, G, false><<<grid_for(th, b), b, 0, s>>>(*cfg, *sc, *io);
   return launch_status();
 }
-template <int M, int T, int NA>
+template <int M, int T, int G>
 int run_bwd(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_grad* g, cudaStream_t s) {
-  const int b = step_block(cfg->n_envs);
-  k_task_bwd<M, T, NA><<<grid_for(cfg->n_envs, b), b, 0, s>>>(*cfg, *sc, *g);
+  const long th = (long)cfg->n_envs * G;
+  const int b = step_block(th);
+  k_task_bwd<M, T, G><<<grid_for(th, b), b, 0, s>>>(*cfg, *sc, *g);
   return launch_status();
 }
-template <int M, int T, int NA>
+template <int M, int T, int G>
 int run_spawn(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, const uint8_t* mask,
               const qs_reset_table* tab, cudaStream_t s) {
   qs_reset_table t{};
   if (tab) t = *tab;
-  k_task_spawn<M, T, NA><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io, mask, t,
-                                                                    tab != nullptr);
+  const long th = (long)cfg->n_envs * G;
+  k_task_spawn<M, T, G><<<grid_for(th, 128), 128, 0, s>>>(*cfg, *sc, *io, mask, t, tab != nullptr);
   return launch_status();
 }
-template <int M, int T, int NA>
+template <int M, int T, int G>
 int run_observe(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, cudaStream_t s) {
-  k_task_observe<M, T, NA><<<grid_for(cfg->n_envs, 128), 128, 0, s>>>(*cfg, *sc, *io);
+  const long th = (long)cfg->n_envs * G;
+  k_task_observe<M, T, G><<<grid_for(th, 128), 128, 0, s>>>(*cfg, *sc, *io);
   return launch_status();
 }
 
-template <int M, int T, int NA>
+template <int M, int T, int G>
 int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_window_io* w, cudaStream_t s) {
   if (w->T <= 0) return QS_OK;
   if (op == 4 && w->loss) cudaMemsetAsync(w->loss, 0, sizeof(double), s);
-  // 64-thread CTAs when there are enough envs for >= 4 CTAs per SM; otherwise
-  // 32-thread CTAs spread the (few, latency-bound) envs over twice the SMs
-  const int blk = cfg->n_envs >= 148 * 4 * WIN_BLOCK ? WIN_BLOCK : 32;
-  const dim3 grid(grid_for(cfg->n_envs, blk));
-  if (op == 4 && NA == 1 && w->imu_out && !w->imu_noise)  // Philox IMU specialisation
-    k_window_fwd<M, T, NA, NA == 1 ? 1 : 0><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
+  // 64-thread CTAs when there are enough rows for >= 4 CTAs per SM; otherwise
+  // 32-thread CTAs spread the (few, latency-bound) rows over twice the SMs
+  const long th = (long)cfg->n_envs * G;
+  const int blk = th >= 148 * 4 * WIN_BLOCK ? WIN_BLOCK : 32;
+  const dim3 grid(grid_for(th, blk));
+  if (op == 4 && G == 1 && w->imu_out && !w->imu_noise)  // Philox IMU specialisation
+    k_window_fwd<M, T, G, G == 1 ? 1 : 0><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
   else if (op == 4)
-    k_window_fwd<M, T, NA, 0><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
+    k_window_fwd<M, T, G, 0><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
   else
-    k_window_bwd<M, T, NA><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
+    k_window_bwd<M, T, G><<<grid, blk, 0, s>>>(*cfg, *sc, *w);
   return launch_status();
 }
 
 // op: 0 fwd, 1 bwd, 2 spawn, 3 observe, 4 window fwd, 5 window bwd.
-// One translation unit per (task, agent capacity) keeps the build parallel.
+// One translation unit per (task, single / multi agent) keeps the build
+// parallel; multi-agent picks the lane-group width G from n_agents.
 template <int T, int NA>
 int task_dispatch_na(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
                      const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s);
 
-template <int T, int M, int NA>
+template <int T, int M, int G>
 int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, const uint8_t* mask,
             const qs_reset_table* tab, cudaStream_t s) {
   switch (op) {
-    case 0: return run_fwd<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), s);
-    case 1: return run_bwd<M, T, NA>(cfg, sc, static_cast<const qs_step_grad*>(p), s);
-    case 2: return run_spawn<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), mask, tab, s);
-    case 3: return run_observe<M, T, NA>(cfg, sc, static_cast<const qs_step_io*>(p), s);
+    case 0: return run_fwd<M, T, G>(cfg, sc, static_cast<const qs_step_io*>(p), s);
+    case 1: return run_bwd<M, T, G>(cfg, sc, static_cast<const qs_step_grad*>(p), s);
+    case 2: return run_spawn<M, T, G>(cfg, sc, static_cast<const qs_step_io*>(p), mask, tab, s);
+    case 3: return run_observe<M, T, G>(cfg, sc, static_cast<const qs_step_io*>(p), s);
     case 4:
-    case 5: return run_window<M, T, NA>(op, cfg, sc, static_cast<const qs_window_io*>(p), s);
+    case 5: return run_window<M, T, G>(op, cfg, sc, static_cast<const qs_window_io*>(p), s);
   }
   return QS_ERR_BAD_ARGUMENT;
+}
+
+template <int T, int M, int NA>
+int task_op_groups(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, const uint8_t* mask,
+                   const qs_reset_table* tab, cudaStream_t s) {
+  if constexpr (NA == 1) {
+    return task_op<T, M, 1>(op, cfg, sc, p, mask, tab, s);
+  } else {
+    const int na = cfg->n_agents;
+    if (na <= 2) return task_op<T, M, 2>(op, cfg, sc, p, mask, tab, s);
+    if (na <= 4) return task_op<T, M, 4>(op, cfg, sc, p, mask, tab, s);
+    return task_op<T, M, 8>(op, cfg, sc, p, mask, tab, s);
+  }
 }
 
 #define QS_DEFINE_TASK_DISPATCH(T, NA)                                                          \
@@ -1393,13 +1322,13 @@ int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, c
   int task_dispatch_na<T, NA>(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, \
                               const uint8_t* mask, const qs_reset_table* tab, cudaStream_t s) { \
     switch (cfg->model) {                                                                      \
-      case QS_MODEL_FULL: return task_op<T, QS_MODEL_FULL, NA>(op, cfg, sc, p, mask, tab, s);  \
+      case QS_MODEL_FULL: return task_op_groups<T, QS_MODEL_FULL, NA>(op, cfg, sc, p, mask, tab, s); \
       case QS_MODEL_PM_CONTINUOUS:                                                             \
-        return task_op<T, QS_MODEL_PM_CONTINUOUS, NA>(op, cfg, sc, p, mask, tab, s);           \
+        return task_op_groups<T, QS_MODEL_PM_CONTINUOUS, NA>(op, cfg, sc, p, mask, tab, s);    \
       case QS_MODEL_PM_DISCRETE:                                                               \
-        return task_op<T, QS_MODEL_PM_DISCRETE, NA>(op, cfg, sc, p, mask, tab, s);             \
+        return task_op_groups<T, QS_MODEL_PM_DISCRETE, NA>(op, cfg, sc, p, mask, tab, s);      \
       case QS_MODEL_SIMPLIFIED:                                                                \
-        return task_op<T, QS_MODEL_SIMPLIFIED, NA>(op, cfg, sc, p, mask, tab, s);              \
+        return task_op_groups<T, QS_MODEL_SIMPLIFIED, NA>(op, cfg, sc, p, mask, tab, s);       \
     }                                                                                          \
     return QS_ERR_BAD_ARGUMENT;                                                                \
   }
