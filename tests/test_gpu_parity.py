@@ -348,3 +348,64 @@ def test_philox_known_answers(qs):
     for i, it in enumerate(items):
         want = _philox_py(it[:4], it[4:])
         assert got[i, :4].tolist() == want and got[i, 4:].tolist() == want
+
+
+@pytest.mark.parametrize("task,n_agents", [("position", 2), ("position", 3), ("avoidance", 4)])
+def test_multi_agent_window_matches_autograd_path(qs, task, n_agents):
+    """Lane groups (one thread per agent row, env couplings as shuffles; 3 agents
+    run in 4-lane groups with a padding lane): the fused window equals the
+    per-step kernels + autograd, Philox resets included."""
+    from paper_2509_10247_b200.window import BpttWindow
+
+    cfg = qs.TaskConfig(task=task, dynamics="pm_continuous", n_envs=256, n_agents=n_agents, episode_len=7,
+                        formation="line", formation_side=1.0, density=0.0)
+    T = 10
+    g = torch.Generator(device="cpu").manual_seed(1)
+    acts = (torch.randn(T, 256 * n_agents, 3, generator=g) * 0.4).cuda()
+    e1 = qs.make_task(cfg, strict=False)
+    e1.reset(seed=3)
+    e2 = qs.make_task(cfg, strict=False)
+    e2.reset(seed=3)
+    assert torch.equal(e1._S, e2._S)
+    win = BpttWindow(e1, T)
+    win.actions.copy_(acts)
+    win.capture()
+    loss_w, g_w = win.run()
+    a = acts.clone().requires_grad_(True)
+    tot = 0.0
+    for t in range(T):
+        tot = tot + e2.step(a[t]).r_ctrl.mean() * 0.99 ** t
+    loss = -tot / T
+    (ga,) = torch.autograd.grad(loss, a)
+    assert abs(float(loss_w) - float(loss.detach())) < 1e-6 * max(1, abs(float(loss.detach())))
+    assert grad_err(g_w.cpu().numpy(), ga.cpu().numpy()) < 1e-5
+    win.sync_env()
+    assert torch.allclose(e1._S, e2._S.detach(), rtol=1e-6, atol=1e-6)
+    assert torch.equal(e1._meta, e2._meta)
+    assert e1.finished_episodes == e2.finished_episodes > 0
+
+
+@pytest.mark.parametrize("task", ["position", "avoidance"])
+def test_multi_agent_philox_spawns_are_valid(qs, task):
+    """Each lane draws its own agent's reset from the env's stream: formation
+    offsets + jitter around one shared spawn, pairwise separation >= d_min
+    (avoidance), deterministic per seed."""
+    na, E = 4, 512
+    cfg = qs.TaskConfig(task=task, dynamics="pm_continuous", n_envs=E, n_agents=na, formation="line",
+                        formation_side=1.0, density=0.0)
+    env = qs.make_task(cfg)
+    env.reset(seed=9)
+    p = env.state.p.detach().double().cpu().numpy().reshape(E, na, 3)
+    gl = env.goals.double().cpu().numpy().reshape(E, na, 3)
+    tmpl = env._template
+    # goals are one shared goal + the formation template (exact up to fp32)
+    np.testing.assert_allclose(gl - gl[:, :1], (tmpl - tmpl[0])[None].repeat(E, 0), atol=1e-5)
+    # spawns: template + small jitter around one shared spawn point
+    dev = p - (tmpl - tmpl[0])[None]
+    assert np.abs(dev - dev[:, :1]).max() < 2.0
+    if task == "avoidance":
+        d = np.linalg.norm(p[:, :, None] - p[:, None, :], axis=-1) + np.eye(na)[None] * 1e9
+        assert d.min() >= cfg.d_min - 1e-5
+    env2 = qs.make_task(cfg)
+    env2.reset(seed=9)
+    assert torch.equal(env._S, env2._S) and torch.equal(env.goals, env2.goals)
