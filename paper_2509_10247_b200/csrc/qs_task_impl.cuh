@@ -615,8 +615,15 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, l
     imu_apply<M>(cfg, row, N, R.meta.z, n, (n.v - s.v) * (1.f / cfg.dt), k.g, ba, bg, out.imu_noise, imu);
   if (has_imu && real) {
     float* o = out.imu_out + 6 * row;
-    o[0] = imu[0]; o[1] = imu[1]; o[2] = imu[2];
-    o[3] = imu[3]; o[4] = imu[4]; o[5] = imu[5];
+    if ((reinterpret_cast<uintptr_t>(o) & 7) == 0) {  // 3 x 8-byte stores
+      float2* o2 = reinterpret_cast<float2*>(o);
+      o2[0] = make_float2(imu[0], imu[1]);
+      o2[1] = make_float2(imu[2], imu[3]);
+      o2[2] = make_float2(imu[4], imu[5]);
+    } else {
+      o[0] = imu[0]; o[1] = imu[1]; o[2] = imu[2];
+      o[3] = imu[3]; o[4] = imu[4]; o[5] = imu[5];
+    }
   }
   R.ba = ba;
   R.bg = bg;
@@ -759,8 +766,14 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, l
     fl |= observe_row<M, TASK>(cfg, so, cs2, xyz(R.goal), &g0, &g1, o);
     if (real) {
       float* dst = out.obs + row * P;
+      if (P % 4 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // 16-byte stores
+        float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
-      for (int kk = 0; kk < P; ++kk) dst[kk] = o[kk];
+        for (int kk = 0; kk < P / 4; ++kk) d4[kk] = make_float4(o[4 * kk], o[4 * kk + 1], o[4 * kk + 2], o[4 * kk + 3]);
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < P; ++kk) dst[kk] = o[kk];
+      }
       if (out.cam) reinterpret_cast<float2*>(out.cam)[row] = cs2;
     }
   }
