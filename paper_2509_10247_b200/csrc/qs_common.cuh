@@ -200,6 +200,32 @@ QS_D float4 box_muller4(uint4 r) {
   return make_float4(d0 * c0, d0 * s0, d1 * c1, d1 * s1);
 }
 
+// twelve standard normals from 256 random bits (two Philox blocks): six
+// Box-Muller pairs.  Radii take 23 bits (bits 8-30) of a word each, so
+// |z| <= 5.6 as before; angles take 16 bits each (a 2^-16-turn grid, far
+// below anything a sensor-noise model resolves): the low bytes of the four
+// radius words of block a, and the two halves of b.z and b.w.
+QS_D float bm_radius(uint32_t r) {  // sqrt(-2 ln u), u = 2 - v in (0, 1]
+  float d;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(d) : "f"(-1.38629436f * lg2_ftz(2.f - u12(r >> 8))));
+  return d;
+}
+QS_D float2 bm_pair(uint32_t rbits, uint32_t abits) {
+  const float d = bm_radius(rbits);
+  const float v = __uint_as_float(((abits & 0xffffu) << 7) | 0x3f800000u);  // [1, 2), 16 bits
+  float s, c;
+  __sincosf(6.28318530717958648f * v, &s, &c);
+  return make_float2(d * c, d * s);
+}
+QS_D void normals12(uint4 a, uint4 b, float4& n0, float4& n1, float4& n2) {
+  const uint32_t h0 = (a.x & 255u) | ((a.y & 255u) << 8), h1 = (a.z & 255u) | ((a.w & 255u) << 8);
+  const float2 p0 = bm_pair(a.x, h0), p1 = bm_pair(a.y, h1), p2 = bm_pair(a.z, b.z),
+               p3 = bm_pair(a.w, b.z >> 16), p4 = bm_pair(b.x, b.w), p5 = bm_pair(b.y, b.w >> 16);
+  n0 = make_float4(p0.x, p0.y, p1.x, p1.y);
+  n1 = make_float4(p2.x, p2.y, p3.x, p3.y);
+  n2 = make_float4(p4.x, p4.y, p5.x, p5.y);
+}
+
 // purposes (counter word 3, high byte)
 enum : uint32_t {
   RNG_SPAWN = 1u,
@@ -226,6 +252,11 @@ struct Rng {
     ctr.w++;
     return box_muller4(r);
   }
+  QS_D uint4 bits4() {
+    uint4 r = philox4x32_10(ctr, key);
+    ctr.w++;
+    return r;
+  }
 };
 
 // Rng with the round keys precomputed (the task kernels: cfg.rng_round_keys);
@@ -245,6 +276,11 @@ struct RngK {
     uint4 r = philox4x32_10_rk(ctr, rk);
     ctr.w++;
     return box_muller4(r);
+  }
+  QS_D uint4 bits4() {
+    uint4 r = philox4x32_10_rk(ctr, rk);
+    ctr.w++;
+    return r;
   }
 };
 

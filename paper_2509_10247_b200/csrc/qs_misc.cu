@@ -36,7 +36,9 @@ __global__ void k_imu(int n, const float* __restrict__ R, const float* __restric
     ng = v3(noise[3 * (3 * N + row)], noise[3 * (3 * N + row) + 1], noise[3 * (3 * N + row) + 2]);
   } else {
     Rng rng(seed, (uint64_t)row, (uint32_t)tick, RNG_IMU);
-    float4 a = rng.normal4(), b = rng.normal4(), c = rng.normal4();
+    const uint4 ua = rng.bits4(), ub = rng.bits4();
+    float4 a, b, c;
+    normals12(ua, ub, a, b, c);  // the same 12 normals as the fused step's IMU
     nba = v3(a.x, a.y, a.z);
     nbg = v3(a.w, b.x, b.y);
     na = v3(b.z, b.w, c.x);

@@ -261,9 +261,8 @@ struct ImuNoise {
 QS_D ImuNoise imu_draw(const qs_task_cfg& cfg, long row, int tick) {
   RngK rng(cfg.rng_round_keys, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)tick, RNG_IMU);
   ImuNoise z;
-  z.a = rng.normal4();
-  z.b = rng.normal4();
-  z.c = rng.normal4();
+  const uint4 a = rng.bits4(), b = rng.bits4();
+  normals12(a, b, z.a, z.b, z.c);
   return z;
 }
 

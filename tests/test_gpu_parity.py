@@ -188,6 +188,19 @@ def test_imu_philox_statistics(qs):
     w = w.cpu().numpy()
     assert abs(a.std() - 0.2) / 0.2 < 0.02 and abs(a.mean()) < 0.01
     assert abs(w.std() - 0.05) / 0.05 < 0.02
+    # the 6 white-noise channels are uncorrelated, Gaussian-tailed (Box-Muller
+    # pairs share a radius: cos/sin of one pair must still be uncorrelated)
+    x = np.concatenate([a / 0.2, w / 0.05], axis=1)
+    c = np.corrcoef(x.T)
+    assert np.abs(c - np.eye(6)).max() < 0.015
+    kurt = ((x - x.mean(0)) ** 4).mean(0) / x.var(0) ** 2
+    assert np.all(np.abs(kurt - 3.0) < 0.1)
+    assert (np.abs(x) > 3.0).mean() == pytest.approx(2.7e-3, rel=0.15)
+    # bias random walks (the other 6 normals of the row-step)
+    rw = qs.sensors.ImuModel(B, accel_bias_rw_std=1.0, gyro_bias_rw_std=1.0, seed=4)
+    a_rw, w_rw = rw.read(R, z3, z3, np.array([0.0, 0.0, -9.81]), 0.01)
+    y = np.concatenate([a_rw.cpu().numpy() - np.array([0, 0, 9.81]), w_rw.cpu().numpy()], axis=1) / 0.1
+    assert np.all(np.abs(y.std(0) - 1.0) < 0.02) and np.abs(np.corrcoef(y.T) - np.eye(6)).max() < 0.015
     # deterministic given (seed, read index)
     imu2 = qs.sensors.ImuModel(B, accel_noise_std=0.2, gyro_noise_std=0.05, seed=3)
     a2, _ = imu2.read(R, z3, z3, np.array([0.0, 0.0, -9.81]), 0.01)
