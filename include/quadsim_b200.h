@@ -207,7 +207,9 @@ int qs_task_observe(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step
 typedef struct qs_ray_cfg {
   int32_t kind;        /* 0 camera (frustum cull), 1 lidar (range-ball cull), 2 generic rays */
   int32_t n_rays;      /* rays per env */
-  int32_t cull;
+  int32_t cull;         /* bit 0: conservative frustum / range cull (never changes an image);
+                          bit 1 (qs_raycast_tiled): extended per-tile culling (exact box
+                          azimuth intervals + vertical flags), for scenes with large boxes */
   float max_range;
   float tan_h, tan_v;  /* camera half-FOV tangents (cull planes) */
   float offset[3];     /* sensor offset in the body frame */
@@ -226,7 +228,7 @@ int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, con
  * empty slot), each with a body-frame bounding cone and azimuth sector,
  * tile_cones (n_tiles,12) = unit axis xyz, cos(half-angle), sin(half-angle),
  * unit horizontal sector centre xy, cos(sector half-width) (< -1.5: no sector
- * test), sin(sector half-width), 3 pad. */
+ * test), sin(sector half-width), min and max direction z, 1 pad. */
 int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
                      int32_t pos_stride, const float* cam_cs, const float* dirs_body,
                      const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, float* out,

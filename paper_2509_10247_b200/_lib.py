@@ -12,7 +12,8 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libquadsim_b200.so")
+# QS_LIB_PATH: load another build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("QS_LIB_PATH") or os.path.join(_PKG, "libquadsim_b200.so")
 
 QS_OK = 0
 QS_ERR_NONFINITE_ACTION = 1

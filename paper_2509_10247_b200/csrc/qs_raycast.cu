@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
     if (i < sv.ns) {
       float4 s = ld4(sv.sph, i);
       V3 c = xyz(s);
-      bool keep = !rc.cull || (KIND == 0 ? keep_camera(rc, cs, o, c, s.w) : keep_ball(rc, o, c, s.w));
+      bool keep = !(rc.cull & 1) || (KIND == 0 ? keep_camera(rc, cs, o, c, s.w) : keep_ball(rc, o, c, s.w));
       if (keep) {
         int k = atomicAdd(&cnt[0], 1);
         V3 oc = o - c;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
       int j = i - sv.ns;
       float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
       float rad = norm3(xyz(h));
-      bool keep = !rc.cull ||
+      bool keep = !(rc.cull & 1) ||
                   (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
       if (keep) {
         int k = atomicAdd(&cnt[1], 1);
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
       float4 c = ld4(sv.cyl, 2 * j);
       float hh = __ldg(sv.cyl + 8 * j + 4);
       float rad = sqrtf(c.w * c.w + hh * hh);
-      bool keep = !rc.cull ||
+      bool keep = !(rc.cull & 1) ||
                   (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
       if (keep) {
         int k = atomicAdd(&cnt[2], 1);
@@ -285,23 +285,71 @@ QS_D float rcp_fast(float x) {  // one MUFU.RCP; 1/(+-0) = +-inf, 1/(+-inf) = +-
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// horizontal footprint record (u2 = (c - o).xy, Q2 = tangent length, r2 = the
-// footprint circle's radius; Q2 = -1: o is inside it) and its keep test against
-// the tile's azimuth sector (world centre az, cos/sin of the half-width; cw < -1.5
-// keeps everything).  Every ray that hits the obstacle passes through its
-// footprint, so the sector test only drops obstacles no ray of the tile can hit.
+// azimuth record of an obstacle's horizontal footprint seen from o: the unit
+// centre direction and cos/sin of the half-width of the angular interval it
+// covers (ch < -1.5: o is inside the footprint, keep for every azimuth).
+// Circles (spheres, cylinders) are exact; a box's footprint rectangle uses the
+// extreme corners.  Every ray that hits the obstacle crosses its footprint, so
+// its azimuth lies in that interval; a tile whose azimuth sector misses the
+// interval cannot hit it.
+QS_D float4 az_circle(V3 u, float r2) {
+  const float L2 = u.x * u.x + u.y * u.y;
+  if (L2 <= r2 * r2 * (1.f + 1e-4f) + 1e-8f) return make_float4(1.f, 0.f, -2.f, 0.f);
+  const float il = rsqrtf(L2), sh = fminf(r2 * il, 1.f);
+  return make_float4(u.x * il, u.y * il, sqrtf(fmaxf(1.f - sh * sh, 0.f)), sh);
+}
+// horizontal footprint circle record (u2 = (c - o).xy, Q2 = tangent length, r2 =
+// radius; Q2 = -1: o is inside) and its sector test in distance units
 QS_D float4 footprint(V3 u, float r2) {
   float L2 = u.x * u.x + u.y * u.y;
   return make_float4(u.x, u.y, L2 <= r2 * r2 ? -1.f : sqrtf(L2 - r2 * r2), r2);
 }
-QS_D bool sector_keeps(float4 h, float slack, float2 az, float cw, float sw) {
+QS_D bool circle_sector_keeps(float4 h, float slack, float2 az, float cw, float sw) {
   if (h.z < 0.f || cw < -1.5f) return true;
   return h.x * az.x + h.y * az.y >= cw * h.z - sw * h.w - slack;
 }
+// pseudo-angle of (x, y): strictly increasing in atan2(y, x) over (-pi, pi]
+QS_D float pseudo_angle(float x, float y) {
+  const float q = __fdividef(y, fabsf(x) + fabsf(y));
+  return x >= 0.f ? q : (y >= 0.f ? 2.f - q : -2.f - q);
+}
+QS_D float4 az_rect(V3 u, float hx, float hy) {
+  const float m = 1e-4f * (1.f + fabsf(u.x) + fabsf(u.y));
+  if (fabsf(u.x) <= hx + m && fabsf(u.y) <= hy + m) return make_float4(1.f, 0.f, -2.f, 0.f);
+  const float il = rsqrtf(u.x * u.x + u.y * u.y);
+  const float cx = u.x * il, cy = u.y * il;  // frame: c along +x
+  float plo = 3.f, phi = -3.f;
+  float2 e1 = make_float2(cx, cy), e2 = e1;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {  // the corners with the extreme angles about c
+    const float kx = u.x + ((k & 1) ? hx : -hx), ky = u.y + ((k & 2) ? hy : -hy);
+    const float pa = pseudo_angle(cx * kx + cy * ky, cx * ky - cy * kx);
+    const float ik = rsqrtf(kx * kx + ky * ky);
+    if (pa < plo) { plo = pa; e1 = make_float2(kx * ik, ky * ik); }
+    if (pa > phi) { phi = pa; e2 = make_float2(kx * ik, ky * ik); }
+  }
+  const float sx = e1.x + e2.x, sy = e1.y + e2.y, s2 = sx * sx + sy * sy;
+  if (s2 < 0.05f) return make_float4(1.f, 0.f, -2.f, 0.f);  // interval close to a half-turn
+  const float is = rsqrtf(s2);
+  const float ax = sx * is, ay = sy * is;
+  const float ch = fmaxf(ax * e1.x + ay * e1.y - 1e-4f, 0.f);  // widened by ~1e-4 for round-off
+  return make_float4(ax, ay, ch, sqrtf(fmaxf(1.f - ch * ch, 0.f)));
+}
+// angle(az, centre) <= w + h  <=>  az . centre >= cos(w + h)   (w, h <= pi/2)
+QS_D bool sector_keeps(float4 h, float2 az, float cw, float sw) {
+  if (h.z < -1.5f || cw < -1.5f) return true;
+  return h.x * az.x + h.y * az.y >= cw * h.z - sw * h.w - 1e-4f;
+}
+// vertical flags: a ray that never rises (d.z <= 0) cannot reach an obstacle
+// entirely above o, nor one that never falls an obstacle entirely below it
 
 constexpr int TILED_BLOCK = 128;
 
-template <int KIND>
+// EXT (qs_ray_cfg.cull bit 1): box footprints use their exact azimuth interval
+// and every obstacle carries vertical flags.  That costs a third record load
+// per (tile, obstacle) and pays off when large boxes (indoor shells: walls,
+// ceiling) would otherwise be candidates for every tile.
+template <int KIND, bool EXT>
 __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
     const float* __restrict__ cam_cs, const float* __restrict__ dirs_body, const int* __restrict__ tile_rays,
@@ -326,7 +374,12 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
   float4* r0 = sm;
   float4* r1 = r0 + cap;
   float4* b_all = r1 + cap;  // bounding sphere (u = c - o, Q)
-  float4* f_all = b_all + cap;  // (r, slack, Q2, r2): bounding radius, slack, footprint
+  // EXT: a_all = azimuth interval of the footprint; f_all.xy = (r, slack) with
+  // the sign bits as vertical flags (r < 0: entirely above o, slack < 0:
+  // entirely below).  Otherwise f_all = (r, slack, Q2, r2): the footprint
+  // circle's tangent length and radius for the sector test, a_all unused.
+  float4* a_all = b_all + cap;
+  float4* f_all = a_all + (EXT ? cap : 0);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   if (warp == 0) {
     const int tot_in = sv.ns + sv.nb + sv.nc;
@@ -334,36 +387,42 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     for (int c0 = 0; c0 < tot_in; c0 += 32) {
       const int i = c0 + lane;
       bool keep = false;
-      float4 q0, q1, bs, fp;
+      float4 q0, q1, bs, az;
       float2 ee;
-      float4 ff;
+      float zl, zh;
       if (i < sv.ns) {
         float4 sp = ld4(sv.sph, i);
         V3 c = xyz(sp);
-        keep = !rc.cull || keep_ball(rc, o, c, sp.w);
+        keep = !(rc.cull & 1) || keep_ball(rc, o, c, sp.w);
         q0 = f4(o - c, sp.w * sp.w);
         q1 = make_float4(0.f, 0.f, 0.f, 0.f);
         bs = bsphere(c - o, sp.w, ee);
-        fp = footprint(c - o, sp.w);
+        az = EXT ? az_circle(c - o, sp.w) : footprint(c - o, sp.w);
+        zl = c.z - sp.w - o.z;
+        zh = c.z + sp.w - o.z;
       } else if (i < sv.ns + sv.nb) {
         int j = i - sv.ns;
         float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
         float rad = norm3(xyz(h));
-        keep = !rc.cull || keep_ball(rc, o, xyz(c), rad);
+        keep = !(rc.cull & 1) || keep_ball(rc, o, xyz(c), rad);
         q0 = f4(xyz(c) - xyz(h) - o, 0.f);
         q1 = f4(xyz(c) + xyz(h) - o, 0.f);
         bs = bsphere(xyz(c) - o, rad, ee);
-        fp = footprint(xyz(c) - o, sqrtf(h.x * h.x + h.y * h.y));
+        az = EXT ? az_rect(xyz(c) - o, h.x, h.y) : footprint(xyz(c) - o, sqrtf(h.x * h.x + h.y * h.y));
+        zl = c.z - h.z - o.z;
+        zh = c.z + h.z - o.z;
       } else if (i < tot_in) {
         int j = i - sv.ns - sv.nb;
         float4 c = ld4(sv.cyl, 2 * j);
         float hh = __ldg(sv.cyl + 8 * j + 4);
         float rad = sqrtf(c.w * c.w + hh * hh);
-        keep = !rc.cull || keep_ball(rc, o, xyz(c), rad);
+        keep = !(rc.cull & 1) || keep_ball(rc, o, xyz(c), rad);
         q0 = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
         q1 = make_float4(hh, 0.f, 0.f, 0.f);
         bs = bsphere(xyz(c) - o, rad, ee);
-        fp = footprint(xyz(c) - o, c.w);
+        az = EXT ? az_circle(xyz(c) - o, c.w) : footprint(xyz(c) - o, c.w);
+        zl = c.z - hh - o.z;
+        zh = c.z + hh - o.z;
       }
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (keep) {
@@ -371,8 +430,13 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
         r0[p] = q0;
         r1[p] = q1;
         b_all[p] = bs;
-        ff = make_float4(ee.x, ee.y, fp.z, fp.w);
-        f_all[p] = ff;
+        if (EXT) {
+          const float zs = 1e-4f * (1.f + fabsf(zl) + fabsf(zh));  // fp32 slack
+          f_all[p] = make_float4(zl - zs > 0.f ? -ee.x : ee.x, zh + zs < 0.f ? -ee.y : ee.y, 0.f, 0.f);
+          a_all[p] = az;
+        } else {
+          f_all[p] = make_float4(ee.x, ee.y, az.z, az.w);
+        }
       }
       run += __popc(m);
       ks += __popc(__ballot_sync(0xffffffffu, keep && i < sv.ns));
@@ -393,7 +457,9 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
     // tile record (12 floats): cone axis xyz, cos, sin | azimuth centre xy, cos, sin of the sector
     const float4 c0 = ld4(tile_cones, 3 * tile), c1 = ld4(tile_cones, 3 * tile + 1);
-    const float sw = __ldg(tile_cones + 12 * tile + 8);
+    const float4 c2 = ld4(tile_cones, 3 * tile + 2);  // sin(sector half-width), dz range
+    const float sw = c2.x;
+    const bool down = c2.z <= 0.f, up = c2.y >= 0.f;  // the tile never rises / never falls
     const V3 ax = rotz(cs, xyz(c0));
     const float cth = c0.w, sth = c1.x;
     const float2 azw = make_float2(cs.x * c1.y - cs.y * c1.z, cs.y * c1.y + cs.x * c1.z);
@@ -410,8 +476,15 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       bool keep = false;
       if (j < tot) {
         const float4 bj = b_all[j], fj = f_all[j];
-        keep = cone_keeps(bj, make_float2(fj.x, fj.y), ax, cth, sth) &&
-               sector_keeps(make_float4(bj.x, bj.y, fj.z, fj.w), fj.y, azw, cw, sw);
+        if (EXT) {
+          const bool above = __float_as_int(fj.x) < 0, below = __float_as_int(fj.y) < 0;
+          keep = !((above && down) || (below && up)) &&
+                 cone_keeps(bj, make_float2(fabsf(fj.x), fabsf(fj.y)), ax, cth, sth) &&
+                 sector_keeps(a_all[j], azw, cw, sw);
+        } else {
+          keep = cone_keeps(bj, make_float2(fj.x, fj.y), ax, cth, sth) &&
+                 circle_sector_keeps(make_float4(bj.x, bj.y, fj.z, fj.w), fj.y, azw, cw, sw);
+        }
       }
       unsigned m = __ballot_sync(0xffffffffu, keep);
       while (m) {  // warp-uniform candidate kinds: no divergence
@@ -500,14 +573,15 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0) return QS_ERR_BAD_ARGUMENT;
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
-  size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * (4 * 16);
+  const bool ext = (cfg->cull & 2) != 0;
+  size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * ((ext ? 5 : 4) * 16);
   cudaStream_t s = (cudaStream_t)stream;
-  if (cfg->kind == 0)
-    k_raycast_tiled<0><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
-                                                     tile_rays, tile_cones, n_tiles, tpc, out, hit);
-  else
-    k_raycast_tiled<1><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, dirs_body,
-                                                     tile_rays, tile_cones, n_tiles, tpc, out, hit);
+#define QS_RT(K, X)                                                                                \
+  k_raycast_tiled<K, X><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, \
+                                                        dirs_body, tile_rays, tile_cones, n_tiles, tpc, out, hit)
+  if (cfg->kind == 0) { if (ext) QS_RT(0, true); else QS_RT(0, false); }
+  else { if (ext) QS_RT(1, true); else QS_RT(1, false); }
+#undef QS_RT
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 

@@ -125,6 +125,9 @@ class DeviceScene:
         self.spawn_goal = torch.zeros(n_envs, 2, 4, **f)
         self.gates = torch.zeros(n_envs, max(n_gates, 1), 8, **f)
         self._struct = None
+        # scenes with large boxes (indoor shells) take the tiled ray caster's
+        # extended per-tile culling (qs_ray_cfg.cull bit 1)
+        self.ext_cull = False
 
     @classmethod
     def from_batched(cls, bp: BatchedPrimitives, device, n_gates=0) -> "DeviceScene":
@@ -317,6 +320,8 @@ def _tile_table(sensor, device):
             cones[k, 8] = np.sin(w)
         else:
             cones[k, 7] = -2.0
+        cones[k, 9] = float(v[:, 2].min())  # vertical range of the tile's directions
+        cones[k, 10] = float(v[:, 2].max())
     out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device))
     _TILE_CACHE[key] = out
     return out
@@ -358,6 +363,8 @@ def cast_rays(scene: DeviceScene, pos: torch.Tensor, pos_stride: int, cam_cs, se
     """Launch the ray-cast kernel.  pos: (N, pos_stride) fp32 device rows."""
     N = pos.shape[0] if pos.dim() == 2 else pos.numel() // pos_stride
     rc = _ray_cfg(sensor, kind, cull, n_agents)
+    if getattr(scene, "ext_cull", False):
+        rc.cull |= 2
     dev = scene.device
     out = torch.empty(N, rc.n_rays, dtype=torch.float32, device=dev)
     hit = torch.empty(N, rc.n_rays, dtype=torch.uint8, device=dev) if want_hit else None

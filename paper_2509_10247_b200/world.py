@@ -160,6 +160,7 @@ def gen_obstacle_courses(seed: int, n_envs: int, spawn, goal, density: float, st
     ns, nb, nc = course_counts(spawn, goal, density, corridor_halfwidth)
     nb_tot = nb + (5 if style == "indoor" else 0)
     sc = out if out is not None else DeviceScene(n_envs, dev, max(ns, 1), max(nb_tot, 1), max(nc, 1))
+    sc.ext_cull = style == "indoor"  # the 5-box shell spans the whole course
     cfg = L.QsGenCfg()
     cfg.env_mask, cfg.episode, cfg.episode_stride = L.ptr(env_mask), L.ptr(episode), int(episode_stride)
     for i in range(3):
@@ -244,6 +245,8 @@ def scenes_to_device(scenes: list, device, n_gates: int = 0) -> DeviceScene:
     from paper_2509_10247_b200.sensors import pack_primitives
 
     sc = DeviceScene.from_batched(pack_primitives([s.prims for s in scenes]), device, n_gates=n_gates)
+    sc.ext_cull = any(len(s.prims.boxes) and float(np.hypot(s.prims.boxes[:, 3], s.prims.boxes[:, 4]).max()) > 2.0
+                      for s in scenes)
     E = len(scenes)
     bd = np.zeros((E, 2, 4))
     sg = np.zeros((E, 2, 4))
