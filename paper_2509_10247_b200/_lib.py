@@ -160,7 +160,16 @@ def ptr(t):
 
 
 def stream_handle(device=None):
-    return torch.cuda.current_stream(device).cuda_stream
+    """The raw cudaStream_t of the current stream on ``device`` (fast path: no
+    Stream object is built on every kernel launch)."""
+    if device is None:
+        idx = torch.cuda.current_device()
+    elif isinstance(device, int):
+        idx = device
+    else:
+        idx = device.index if isinstance(device, torch.device) and device.index is not None \
+            else torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)
 
 
 def check(status: int, what: str):
