@@ -105,7 +105,8 @@ typedef struct qs_scene {
 /* Mutable per-env / per-row buffers.  `*_in` are read, `*_out` written
  * (functional update: the *_in buffers are what the backward replays). */
 typedef struct qs_step_io {
-  /* differentiable state + v_ema in the pad lanes: (NP,N,4), NP = 3 (pm) or 4 (full) */
+  /* differentiable state + v_ema in the pad lanes: (NP,N,4), NP = qs_state_planes(model):
+     3 (pm), 4 (full), 5 (simplified) */
   const float* S_in;  float* S_out;
   const float* raw;                     /* (N,A) raw (pre-squash) action */
   const float* goal_in; float* goal_out;  /* (N,4) */
