@@ -363,7 +363,7 @@ def test_philox_known_answers(qs):
         assert got[i, :4].tolist() == want and got[i, 4:].tolist() == want
 
 
-@pytest.mark.parametrize("task,n_agents", [("position", 2), ("position", 3), ("avoidance", 4)])
+@pytest.mark.parametrize("task,n_agents", [("position", 2), ("position", 3), ("avoidance", 4), ("position", 8)])
 def test_multi_agent_window_matches_autograd_path(qs, task, n_agents):
     """Lane groups (one thread per agent row, env couplings as shuffles; 3 agents
     run in 4-lane groups with a padding lane): the fused window equals the
@@ -422,3 +422,35 @@ def test_multi_agent_philox_spawns_are_valid(qs, task):
     env2 = qs.make_task(cfg)
     env2.reset(seed=9)
     assert torch.equal(env._S, env2._S) and torch.equal(env.goals, env2.goals)
+
+
+@pytest.mark.parametrize("n_envs", [1, 77])
+def test_window_ragged_batch_matches_autograd_path(qs, n_envs):
+    """Batches that fill neither a warp nor a CTA: the tail CTA loads its
+    actions without TMA, and tiny batches launch 32-thread CTAs."""
+    from paper_2509_10247_b200.window import BpttWindow
+
+    cfg = qs.TaskConfig(task="position", dynamics="full", n_envs=n_envs, episode_len=5,
+                        imu=qs.ImuSpec(0.1, 0.01, 0.01, 0.001))
+    T = 9
+    g = torch.Generator(device="cpu").manual_seed(2)
+    acts = (torch.randn(T, n_envs, 4, generator=g) * 0.4).cuda()
+    e1 = qs.make_task(cfg, strict=False)
+    e1.reset(seed=6)
+    e2 = qs.make_task(cfg, strict=False)
+    e2.reset(seed=6)
+    win = BpttWindow(e1, T)
+    win.actions.copy_(acts)
+    win.capture()
+    loss_w, g_w = win.run()
+    a = acts.clone().requires_grad_(True)
+    tot = 0.0
+    for t in range(T):
+        tot = tot + e2.step(a[t]).r_ctrl.mean() * 0.99 ** t
+    loss = -tot / T
+    (ga,) = torch.autograd.grad(loss, a)
+    assert abs(float(loss_w) - float(loss.detach())) < 1e-6 * max(1, abs(float(loss.detach())))
+    assert grad_err(g_w.cpu().numpy(), ga.cpu().numpy()) < 1e-5
+    win.sync_env()
+    assert torch.allclose(e1._S, e2._S.detach(), rtol=1e-6, atol=1e-6)
+    assert torch.equal(e1._meta, e2._meta)
