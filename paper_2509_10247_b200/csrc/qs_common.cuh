@@ -226,6 +226,17 @@ QS_D void normals12(uint4 a, uint4 b, float4& n0, float4& n1, float4& n2) {
   n2 = make_float4(p4.x, p4.y, p5.x, p5.y);
 }
 
+// six standard normals from one block: three Box-Muller pairs, radii from
+// bits 8-30 of x, y, z, angles from the halves of w and the low bytes of x, y
+QS_D void normals6(uint4 r, float4& n0, float4& n1) {
+  const float2 p0 = bm_pair(r.x, r.w), p1 = bm_pair(r.y, r.w >> 16),
+               p2 = bm_pair(r.z, (r.x & 255u) | ((r.y & 255u) << 8));
+  n0 = make_float4(p0.x, p0.y, p1.x, p1.y);
+  n1 = make_float4(p2.x, p2.y, 0.f, 0.f);
+}
+// a uniform in (0, 1) on a 2^-16 grid from the low 16 bits
+QS_D float u16(uint32_t h) { return __uint_as_float(((h & 0xffffu) << 7) | 0x3f800000u) - 0.99999237f; }
+
 // purposes (counter word 3, high byte)
 enum : uint32_t {
   RNG_SPAWN = 1u,

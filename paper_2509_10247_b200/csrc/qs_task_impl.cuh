@@ -181,15 +181,18 @@ QS_D bool spawn_sample(const qs_task_cfg& cfg, const qs_scene& sc, long e, int e
     V3 l8 = lo + v3(0.8f, 0.8f, 0.8f), h8 = hi - v3(0.8f, 0.8f, 0.8f);
     V3 sp = l8, gl = l8;
     ok = false;
+    // one Philox block per candidate pair: six 16-bit uniforms (a 2^-16 grid,
+    // ~0.2 mm over these courses), so a rejection try costs one block
     for (int t = 0; t < 100 && !ok; ++t) {
-      float4 u = rng.uniform4(), w = rng.uniform4();
-      sp = l8 + hmul(h8 - l8, v3(u.x, u.y, u.z));
-      gl = l8 + hmul(h8 - l8, v3(u.w, w.x, w.y));
+      const uint4 r = rng.bits4();
+      sp = l8 + hmul(h8 - l8, v3(u16(r.x), u16(r.x >> 16), u16(r.y)));
+      gl = l8 + hmul(h8 - l8, v3(u16(r.y >> 16), u16(r.z), u16(r.z >> 16)));
       float d = norm3(gl - sp);
       ok = d >= 2.5f && d <= cfg.goal_dist;
     }
-    rng.ctr.w += 2u * (uint32_t)ag;  // agent a draws normals 2a, 2a+1 after the pair
-    float4 n0 = rng.normal4(), n1 = rng.normal4();
+    rng.ctr.w += (uint32_t)ag;  // agent a's six spawn normals: block a after the pair
+    float4 n0, n1;
+    normals6(rng.bits4(), n0, n1);
     p = sp + f + v3(n0.x, n0.y, n0.z) * 0.1f;
     v = v3(n0.w, n1.x, n1.y) * 0.3f;
     goal = gl + f;

@@ -4,7 +4,7 @@ import paper_2509_10247_b200 as qs
 from paper_2509_10247_b200.window import BpttWindow
 from paper_2509_10247_b200 import _lib as L
 import bench
-for scale, elen in ((0.3, 128), (0.3, 10**6), (0.05, 10**6)):
+for scale, elen in ((0.3, 128), (0.0, 10**6), (0.05, 10**6)):
     cfg = qs.TaskConfig(task="position", dynamics="full", n_envs=65536, episode_len=elen, imu=qs.ImuSpec(**bench.IMU))
     env = qs.make_task(cfg, device="cuda", strict=False); env.reset(seed=1)
     win = BpttWindow(env, 32)
