@@ -56,58 +56,87 @@ QS_D bool keep_ball(const qs_ray_cfg& rc, V3 o, V3 c, float rad) {
 }
 
 // --- ray-primitive tests on hoisted records ---------------------------------
+// One arithmetic core per primitive, shared by the untiled kernel (float
+// min-t, argmin for the depth VJP) and the tiled one (min-t in IEEE bit
+// order, below), so both kernels produce identical images.
+
+QS_D float rcp_fast(float x) {  // one MUFU.RCP; 1/(+-0) = +-inf, 1/(+-inf) = +-0
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+QS_D float pos0(float x) { return __fadd_rn(x, 0.f); }  // -0 -> +0, else x
 
 // sphere record: (oc.xyz, r^2), oc = o - c.  Robust discriminant
-// r^2 - |oc - b d|^2 (== b^2 - (|oc|^2 - r^2) in exact arithmetic).
+// r^2 - |oc - b d|^2 (== b^2 - (|oc|^2 - r^2) in exact arithmetic); its sqrt is
+// NaN when it is negative (a miss), so both roots are NaN then.  t1 <= t2.
+QS_D float2 sphere_roots(float4 s, V3 d) {
+  const float b = fmaf(d.x, s.x, fmaf(d.y, s.y, d.z * s.z));
+  const float vx = fmaf(-b, d.x, s.x), vy = fmaf(-b, d.y, s.y), vz = fmaf(-b, d.z, s.z);
+  const float disc = fmaf(-vx, vx, fmaf(-vy, vy, fmaf(-vz, vz, s.w)));
+  const float sq = sqrt_approx(disc);
+  return make_float2(-b - sq, sq - b);
+}
 QS_D float hit_sphere(float4 s, V3 d) {
-  float b = d.x * s.x + d.y * s.y + d.z * s.z;
-  float vx = fmaf(-b, d.x, s.x), vy = fmaf(-b, d.y, s.y), vz = fmaf(-b, d.z, s.z);
-  float disc = s.w - (vx * vx + vy * vy + vz * vz);
-  float sq = sqrt_approx(fmaxf(disc, 0.f));
-  float t1 = -b - sq, t2 = -b + sq;
-  float t = t1 >= 0.f ? t1 : (t2 >= 0.f ? t2 : INF);
-  return disc >= 0.f ? t : INF;
+  const float2 r = sphere_roots(s, d);
+  return r.x >= 0.f ? r.x : (r.y >= 0.f ? r.y : INF);  // NaN compares false
 }
 
-// box record: lo - o, hi - o
-QS_D float hit_box(float4 lo, float4 hi, V3 inv, int* axis) {
-  float t1x = lo.x * inv.x, t2x = hi.x * inv.x;
-  float t1y = lo.y * inv.y, t2y = hi.y * inv.y;
-  float t1z = lo.z * inv.z, t2z = hi.z * inv.z;
-  float nx = fmin_nan(t1x, t2x), fx = fmax_nan(t1x, t2x);
-  float ny = fmin_nan(t1y, t2y), fy = fmax_nan(t1y, t2y);
-  float nz = fmin_nan(t1z, t2z), fz = fmax_nan(t1z, t2z);
-  float tn = fmax_nan(fmax_nan(nx, ny), nz);
-  float tf = fmin_nan(fmin_nan(fx, fy), fz);
-  bool hit = (tn <= tf) && (tf >= 0.f);
-  float t = tn >= 0.f ? tn : tf;
+// box record: lo - o, hi - o.  Slab entry/exit with NaN-propagating min/max.
+QS_D void box_slab(float4 lo, float4 hi, V3 inv, float& tn, float& tf, int* axis) {
+  const float t1x = lo.x * inv.x, t2x = hi.x * inv.x;
+  const float t1y = lo.y * inv.y, t2y = hi.y * inv.y;
+  const float t1z = lo.z * inv.z, t2z = hi.z * inv.z;
+  const float nx = fmin_nan(t1x, t2x), fx = fmax_nan(t1x, t2x);
+  const float ny = fmin_nan(t1y, t2y), fy = fmax_nan(t1y, t2y);
+  const float nz = fmin_nan(t1z, t2z), fz = fmax_nan(t1z, t2z);
+  tn = fmax_nan(fmax_nan(nx, ny), nz);
+  tf = fmin_nan(fmin_nan(fx, fy), fz);
   if (axis) {  // face normal axis of the returned root (depth VJP)
     if (tn >= 0.f)
       *axis = (tn == nx) ? 0 : (tn == ny ? 1 : 2);
     else
       *axis = (tf == fx) ? 0 : (tf == fy ? 1 : 2);
   }
-  return hit ? t : INF;
+}
+QS_D float hit_box(float4 lo, float4 hi, V3 inv, int* axis) {
+  float tn, tf;
+  box_slab(lo, hi, inv, tn, tf, axis);
+  const bool hit = (tn <= tf) && (tf >= 0.f);
+  return hit ? (tn >= 0.f ? tn : tf) : INF;
 }
 
-// cylinder record A: (ox, oy, oz, r^2), B: (hh, _, _, _)
-// robust side discriminant a r^2 - (ox dy - oy dx)^2 (Lagrange identity)
-QS_D float hit_cyl(float4 c, float hh, V3 d, float a, float inv_a, float inv_dz, int* part) {
-  float b = c.x * d.x + c.y * d.y;
-  float cr = c.x * d.y - c.y * d.x;
-  float disc = a * c.w - cr * cr;
-  float sq = sqrt_approx(fmaxf(disc, 0.f));
-  float ts1 = (-b - sq) * inv_a, ts2 = (-b + sq) * inv_a;
-  bool base = disc >= 0.f && a > 0.f;
-  bool ok1 = base && ts1 >= 0.f && fabsf(fmaf(ts1, d.z, c.z)) <= hh;
-  bool ok2 = base && ts2 >= 0.f && fabsf(fmaf(ts2, d.z, c.z)) <= hh;
-  float ts = ok1 ? ts1 : (ok2 ? ts2 : INF);
-  float tt = (hh - c.z) * inv_dz, tb = (-hh - c.z) * inv_dz;
-  float xt = fmaf(tt, d.x, c.x), yt = fmaf(tt, d.y, c.y);
-  float xb = fmaf(tb, d.x, c.x), yb = fmaf(tb, d.y, c.y);
-  bool okt = tt >= 0.f && tt < INF && xt * xt + yt * yt <= c.w;
-  bool okb = tb >= 0.f && tb < INF && xb * xb + yb * yb <= c.w;
-  float tc = fminf(okt ? tt : INF, okb ? tb : INF);
+// capped z-cylinder: record (o - c, r^2) and the cap planes relative to o
+// (ztop = hh - (o-c).z, zbot = -hh - (o-c).z).  Robust side discriminant
+// a r^2 - (ox dy - oy dx)^2 (Lagrange identity).  Side roots count within
+// |z| <= hh, cap roots within the disc; degenerate rays give NaN roots
+// (a = 0: 0 * inf; dz = 0: inf - inf in the cap point) that fail every test.
+struct CylRoots {
+  float ts1, ts2, tt, tb;
+  bool z1, z2, ct, cb;
+};
+QS_D CylRoots cyl_roots(float4 c, float hh, float ztop, float zbot, V3 d, float a, float inv_a, float inv_dz) {
+  CylRoots r;
+  const float b = fmaf(c.x, d.x, c.y * d.y);
+  const float cr = fmaf(c.x, d.y, -c.y * d.x);
+  const float disc = fmaf(a, c.w, -cr * cr);
+  const float sq = sqrt_approx(disc);
+  r.ts1 = (-b - sq) * inv_a;  // -0 only together with ts2 = +0
+  r.ts2 = (sq - b) * inv_a;
+  r.z1 = fabsf(fmaf(r.ts1, d.z, c.z)) <= hh;
+  r.z2 = fabsf(fmaf(r.ts2, d.z, c.z)) <= hh;
+  r.tt = pos0(ztop * inv_dz);
+  r.tb = pos0(zbot * inv_dz);
+  const float xt = fmaf(r.tt, d.x, c.x), yt = fmaf(r.tt, d.y, c.y);
+  const float xb = fmaf(r.tb, d.x, c.x), yb = fmaf(r.tb, d.y, c.y);
+  r.ct = fmaf(xt, xt, yt * yt) <= c.w;  // false for inf / NaN cap points
+  r.cb = fmaf(xb, xb, yb * yb) <= c.w;
+  return r;
+}
+QS_D float hit_cyl(float4 c, float hh, float ztop, float zbot, V3 d, float a, float inv_a, float inv_dz, int* part) {
+  const CylRoots r = cyl_roots(c, hh, ztop, zbot, d, a, inv_a, inv_dz);
+  const float ts = (r.z1 && r.ts1 >= 0.f) ? r.ts1 : ((r.z2 && r.ts2 >= 0.f) ? r.ts2 : INF);
+  const float tc = fminf((r.ct && r.tt >= 0.f) ? r.tt : INF, (r.cb && r.tb >= 0.f) ? r.tb : INF);
   if (part) *part = (ts <= tc) ? 0 : 1;
   return fminf(ts, tc);
 }
@@ -187,9 +216,9 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
     } else {
       d = rotz(cs, xyz(ld4(dirs_body, r)));
     }
-    V3 inv = v3(1.f / d.x, 1.f / d.y, 1.f / d.z);
-    float a = d.x * d.x + d.y * d.y;
-    float inv_a = 1.f / a;
+    const V3 inv = v3(rcp_fast(d.x), rcp_fast(d.y), rcp_fast(d.z));
+    const float a = d.x * d.x + d.y * d.y;
+    const float inv_a = rcp_fast(a);
     float best = INF;
     int code = 0, bidx = 0;  // kind | detail, shared-memory index of the argmin
     for (int i = 0; i < ns; ++i) {
@@ -211,7 +240,9 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
     }
     for (int i = 0; i < nc; ++i) {
       int part = 0;
-      float t = hit_cyl(s_cyl[i], s_cyl_hh[i], d, a, inv_a, inv.z, GRAD ? &part : nullptr);
+      const float4 c = s_cyl[i];
+      const float hh = s_cyl_hh[i];
+      float t = hit_cyl(c, hh, hh - c.z, -hh - c.z, d, a, inv_a, inv.z, GRAD ? &part : nullptr);
       if (GRAD) {
         if (t < best) { best = t; code = 3 | (part << 4); bidx = i; }
       } else {
@@ -280,11 +311,6 @@ QS_D bool cone_keeps(float4 b, float2 e, V3 ax, float cth, float sth) {
   if (b.w < 0.f) return true;
   return dot(xyz(b), ax) >= cth * b.w - sth * e.x - e.y;
 }
-QS_D float rcp_fast(float x) {  // one MUFU.RCP; 1/(+-0) = +-inf, 1/(+-inf) = +-0
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 // azimuth record of an obstacle's horizontal footprint seen from o: the unit
 // centre direction and cos/sin of the half-width of the angular interval it
 // covers (ch < -1.5: o is inside the footprint, keep for every azimuth).
@@ -342,6 +368,41 @@ QS_D bool sector_keeps(float4 h, float2 az, float cw, float sw) {
 }
 // vertical flags: a ray that never rises (d.z <= 0) cannot reach an obstacle
 // entirely above o, nor one that never falls an obstacle entirely below it
+
+// --- min-t in IEEE bit order (tiled kernel) ----------------------------------
+// Non-negative floats order as their bit patterns read as unsigned ints, and
+// every negative float and every NaN reads as a larger unsigned than +inf.  So
+// one integer min over the candidate roots keeps exactly the roots the
+// reference accepts (finite or +inf, t >= 0; q/sensors.py:139-216) and drops
+// roots behind the origin and NaN roots (missed discriminant -> sqrt of a
+// negative; 0 * inf slab terms) with no compares or selects.  A -0 root (the
+// origin exactly on a surface plane) is canonicalised to +0 where one can
+// arise, because the reference counts t = -0.0 as t >= 0.
+constexpr unsigned INF_BITS = 0x7f800000u;
+QS_D unsigned fbits(float x) { return __float_as_uint(x); }
+QS_D unsigned umin3(unsigned a, unsigned b, unsigned c) { return min(a, min(b, c)); }
+
+QS_D unsigned hit_sphere_u(unsigned best, float4 s, V3 d) {
+  const float2 r = sphere_roots(s, d);  // t1 <= t2: the min non-negative root is the reference's
+  return umin3(best, fbits(r.x), fbits(r.y));  // -0 t1 comes with +0 t2
+}
+QS_D unsigned hit_box_u(unsigned best, float4 lo, float4 hi, V3 inv) {
+  float tn, tf;  // hit iff tn <= tf and tf >= 0, at tn if tn >= 0 else tf
+  box_slab(lo, hi, inv, tn, tf, nullptr);
+  const unsigned c = min(fbits(pos0(tn)), fbits(pos0(tf)));
+  return tn <= tf ? min(best, c) : best;
+}
+QS_D unsigned hit_cyl_u(unsigned best, float4 c, float4 h, V3 d, float a, float inv_a, float inv_dz) {
+  const CylRoots r = cyl_roots(c, h.x, h.y, h.z, d, a, inv_a, inv_dz);
+  unsigned m = best;
+  m = r.z1 ? min(m, fbits(r.ts1)) : m;
+  m = r.z2 ? min(m, fbits(r.ts2)) : m;
+  m = r.ct ? min(m, fbits(r.tt)) : m;
+  m = r.cb ? min(m, fbits(r.tb)) : m;
+  return m;
+}
+// lanes [0, k) of a warp, k clamped to [0, 32]
+QS_D unsigned lanes_below(int k) { return k >= 32 ? 0xffffffffu : (k <= 0 ? 0u : (1u << k) - 1u); }
 
 constexpr int TILED_BLOCK = 128;
 
@@ -418,7 +479,7 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
         float rad = sqrtf(c.w * c.w + hh * hh);
         keep = !(rc.cull & 1) || keep_ball(rc, o, xyz(c), rad);
         q0 = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
-        q1 = make_float4(hh, 0.f, 0.f, 0.f);
+        q1 = make_float4(hh, hh - (o.z - c.z), -hh - (o.z - c.z), 0.f);  // cap planes relative to o
         bs = bsphere(xyz(c) - o, rad, ee);
         az = EXT ? az_circle(xyz(c) - o, c.w) : footprint(xyz(c) - o, c.w);
         zl = c.z - hh - o.z;
@@ -470,7 +531,7 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const V3 inv = v3(rcp_fast(d.x), rcp_fast(d.y), rcp_fast(d.z));
     const float a = d.x * d.x + d.y * d.y;
     const float inv_a = rcp_fast(a);
-    float best = INF;
+    unsigned best = INF_BITS;
     for (int base = 0; base < tot; base += 32) {
       const int j = base + lane;
       bool keep = false;
@@ -486,27 +547,33 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
                  circle_sector_keeps(make_float4(bj.x, bj.y, fj.z, fj.w), fj.y, azw, cw, sw);
         }
       }
-      unsigned m = __ballot_sync(0xffffffffu, keep);
-      while (m) {  // warp-uniform candidate kinds: no divergence
-        const int i = base + __ffs(m) - 1;
-        m &= m - 1;
-        if (i < ns) {
-          best = fminf(best, hit_sphere(r0[i], d));
-        } else if (i < ns + nb) {
-          best = fminf(best, hit_box(r0[i], r1[i], inv, nullptr));
-        } else {
-          best = fminf(best, hit_cyl(r0[i], r1[i].x, d, a, inv_a, inv.z, nullptr));
-        }
+      // warp-uniform candidate masks, split by kind (the list is kind-sorted:
+      // spheres, boxes, cylinders), so each loop runs one test with no dispatch
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      const unsigned lt_s = lanes_below(ns - base), lt_b = lanes_below(ns + nb - base);
+      unsigned ms = m & lt_s, mb = m & lt_b & ~lt_s, mc = m & ~lt_b;
+      while (ms) {
+        const int i = base + __ffs(ms) - 1;
+        ms &= ms - 1;
+        best = hit_sphere_u(best, r0[i], d);
+      }
+      while (mb) {
+        const int i = base + __ffs(mb) - 1;
+        mb &= mb - 1;
+        best = hit_box_u(best, r0[i], r1[i], inv);
+      }
+      while (mc) {
+        const int i = base + __ffs(mc) - 1;
+        mc &= mc - 1;
+        best = hit_cyl_u(best, r0[i], r1[i], d, a, inv_a, inv.z);
       }
     }
-    if (ground) {
-      float t = gdz * inv.z;
-      if (t >= 0.f && t < INF) best = fminf(best, t);
-    }
+    if (ground) best = min(best, fbits(pos0(gdz * inv.z)));  // +inf / NaN / t < 0 drop out
     if (ray >= 0) {
+      const float t = __uint_as_float(best);
       const long oi = row * rc.n_rays + ray;
-      out[oi] = fminf(best, rc.max_range);
-      if (hitm) hitm[oi] = best < rc.max_range ? 1 : 0;
+      out[oi] = fminf(t, rc.max_range);
+      if (hitm) hitm[oi] = t < rc.max_range ? 1 : 0;
     }
   }
 }
