@@ -305,6 +305,19 @@ def bench_depth(dev, rank, world=1, frames=20):
 
     ms = max_over_ranks(timed(True, cam, 0), world)
     ms_untiled = max_over_ranks(timed(False, cam, 0), world)
+    # spawn-facing-goal poses (SURVEY §8d's other C3 pose set): near the spawn,
+    # looking down the corridor through the course, yaw jitter 0.1 rad
+    pos_rand, cs_rand = pos, cs
+    g2 = torch.Generator(device="cpu").manual_seed(17 + rank)
+    pos_sf = torch.zeros(E, 4)
+    pos_sf[:, 0] = torch.rand(E, generator=g2)
+    pos_sf[:, 1] = (torch.rand(E, generator=g2) - 0.5) * 2.0
+    pos_sf[:, 2] = 0.8 + torch.rand(E, generator=g2) * 0.8
+    yaw_sf = torch.atan2(float(goal[1]) - pos_sf[:, 1], float(goal[0]) - pos_sf[:, 0]) + 0.1 * torch.randn(E, generator=g2)
+    pos, cs = pos_sf.to(dev), torch.stack([torch.cos(yaw_sf), torch.sin(yaw_sf)], -1).to(dev).contiguous()
+    ms_sf = max_over_ranks(timed(True, cam, 0), world)
+    ks2, kb2, kc2 = fov_kept_counts(sc, pos, cs, cam)
+    pos, cs = pos_rand, cs_rand
     lidar = sn.LidarPattern(n_azimuth=360, n_elevation=16, max_range=20.0)
     ms_lidar = max_over_ranks(timed(True, lidar, 1), world)
     E *= world  # rays of all ranks in the max-over-ranks frame time
@@ -313,12 +326,16 @@ def bench_depth(dev, rank, world=1, frames=20):
     flops_frame = float(np.sum(14 + 10 * cnt[:, 0] + 6 * cnt[:, 1] + 31 * cnt[:, 2] + cnt[:, 3])) * R * world
     ks, kb, kc = fov_kept_counts(sc, pos, cs, cam)
     flops_culled = float((14 + 10 * ks + 6 * kb + 31 * kc).sum().item() + cnt[:, 3].sum()) * R * world
+    flops_sf = float((14 + 10 * ks2 + 6 * kb2 + 31 * kc2).sum().item() + cnt[:, 3].sum()) * R * world
     return {"rays_per_s": E * R / (ms * 1e-3), "ms_per_frame": ms, "n_envs": E, "rays_per_env": R,
             "mean_solids": float(cnt[:, :3].sum(1).mean()),
             "tflops_uncull_equiv": flops_frame / (ms * 1e-3) / 1e12,
             "flops_per_ray": {"uncull": flops_frame / (E * R), "fov_culled": flops_culled / (E * R)},
             "tflops_culled_equiv": flops_culled / (ms * 1e-3) / 1e12,
-            "kernel": "k_raycast_tiled<0> (per-warp cone culling)",
+            "kernel": "k_raycast_tiled<0> (per-warp cone culling, 64-ray tiles, 2 rays per lane)",
+            "spawn_facing": {"ms_per_frame": ms_sf, "rays_per_s": E * R / (ms_sf * 1e-3),
+                             "flops_per_ray_fov_culled": flops_sf / (E * R),
+                             "tflops_culled_equiv": flops_sf / (ms_sf * 1e-3) / 1e12},
             "untiled": {"rays_per_s": E * R / (ms_untiled * 1e-3), "ms_per_frame": ms_untiled,
                         "tflops_uncull_equiv": flops_frame / (ms_untiled * 1e-3) / 1e12},
             "lidar_360x16": {"rays_per_s": E * lidar.n_rays / (ms_lidar * 1e-3), "ms_per_frame": ms_lidar}}
@@ -632,6 +649,7 @@ def run_ours(a):
         depth["ffma2_tflops_measured"] = probe["ffma2_tflops"]
         depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / (fp32_peak * world)
         depth["frac_culled_equiv"] = depth["tflops_culled_equiv"] / (fp32_peak * world)
+        depth["spawn_facing"]["frac_culled_equiv"] = depth["spawn_facing"]["tflops_culled_equiv"] / (fp32_peak * world)
 
     c1 = bench_c1(dev) if rank == 0 and not a.no_depth else None
     c4 = bench_c4(dev) if rank == 0 and not a.no_depth else None

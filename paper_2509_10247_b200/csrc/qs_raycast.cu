@@ -410,7 +410,10 @@ constexpr int TILED_BLOCK = 128;
 // and every obstacle carries vertical flags.  That costs a third record load
 // per (tile, obstacle) and pays off when large boxes (indoor shells: walls,
 // ceiling) would otherwise be candidates for every tile.
-template <int KIND, bool EXT>
+// RPL rays per lane: a tile holds 32 * RPL rays (lane j owns rays j, j + 32,
+// ...), so the tile's cone test, ballot, candidate loop and obstacle-record
+// loads are shared by RPL rays, and each candidate runs RPL independent tests.
+template <int KIND, bool EXT, int RPL>
 __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
     const float* __restrict__ cam_cs, const float* __restrict__ dirs_body, const int* __restrict__ tile_rays,
@@ -525,13 +528,20 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const float cth = c0.w, sth = c1.x;
     const float2 azw = make_float2(cs.x * c1.y - cs.y * c1.z, cs.y * c1.y + cs.x * c1.z);
     const float cw = c1.w;
-    const int ray = __ldg(tile_rays + tile * 32 + lane);
-    V3 d = v3(1.f, 0.f, 0.f);
-    if (ray >= 0) d = rotz(cs, xyz(ld4(dirs_body, ray)));
-    const V3 inv = v3(rcp_fast(d.x), rcp_fast(d.y), rcp_fast(d.z));
-    const float a = d.x * d.x + d.y * d.y;
-    const float inv_a = rcp_fast(a);
-    unsigned best = INF_BITS;
+    int ray[RPL];
+    V3 d[RPL], inv[RPL];
+    float a[RPL], inv_a[RPL];
+    unsigned best[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      ray[k] = __ldg(tile_rays + (tile * RPL + k) * 32 + lane);
+      d[k] = v3(1.f, 0.f, 0.f);
+      if (ray[k] >= 0) d[k] = rotz(cs, xyz(ld4(dirs_body, ray[k])));
+      inv[k] = v3(rcp_fast(d[k].x), rcp_fast(d[k].y), rcp_fast(d[k].z));
+      a[k] = d[k].x * d[k].x + d[k].y * d[k].y;
+      inv_a[k] = rcp_fast(a[k]);
+      best[k] = INF_BITS;
+    }
     for (int base = 0; base < tot; base += 32) {
       const int j = base + lane;
       bool keep = false;
@@ -555,25 +565,34 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       while (ms) {
         const int i = base + __ffs(ms) - 1;
         ms &= ms - 1;
-        best = hit_sphere_u(best, r0[i], d);
+        const float4 q = r0[i];
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) best[k] = hit_sphere_u(best[k], q, d[k]);
       }
       while (mb) {
         const int i = base + __ffs(mb) - 1;
         mb &= mb - 1;
-        best = hit_box_u(best, r0[i], r1[i], inv);
+        const float4 lo = r0[i], hi = r1[i];
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) best[k] = hit_box_u(best[k], lo, hi, inv[k]);
       }
       while (mc) {
         const int i = base + __ffs(mc) - 1;
         mc &= mc - 1;
-        best = hit_cyl_u(best, r0[i], r1[i], d, a, inv_a, inv.z);
+        const float4 q = r0[i], h = r1[i];
+#pragma unroll
+        for (int k = 0; k < RPL; ++k) best[k] = hit_cyl_u(best[k], q, h, d[k], a[k], inv_a[k], inv[k].z);
       }
     }
-    if (ground) best = min(best, fbits(pos0(gdz * inv.z)));  // +inf / NaN / t < 0 drop out
-    if (ray >= 0) {
-      const float t = __uint_as_float(best);
-      const long oi = row * rc.n_rays + ray;
-      out[oi] = fminf(t, rc.max_range);
-      if (hitm) hitm[oi] = t < rc.max_range ? 1 : 0;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      if (ground) best[k] = min(best[k], fbits(pos0(gdz * inv[k].z)));  // +inf / NaN / t < 0 drop out
+      if (ray[k] >= 0) {
+        const float t = __uint_as_float(best[k]);
+        const long oi = row * rc.n_rays + ray[k];
+        out[oi] = fminf(t, rc.max_range);
+        if (hitm) hitm[oi] = t < rc.max_range ? 1 : 0;
+      }
     }
   }
 }
@@ -634,20 +653,26 @@ int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, con
 
 int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
                      int32_t pos_stride, const float* cam_cs, const float* dirs_body,
-                     const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, float* out,
-                     uint8_t* hit, void* stream) {
+                     const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, int32_t tile_width,
+                     float* out, uint8_t* hit, void* stream) {
   if (n_rows <= 0 || cfg->n_rays <= 0) return QS_OK;
   if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0) return QS_ERR_BAD_ARGUMENT;
+  if (tile_width != 32 && tile_width != 64 && tile_width != 128) return QS_ERR_BAD_ARGUMENT;
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
   const bool ext = (cfg->cull & 2) != 0;
   size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * ((ext ? 5 : 4) * 16);
   cudaStream_t s = (cudaStream_t)stream;
-#define QS_RT(K, X)                                                                                \
-  k_raycast_tiled<K, X><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, \
-                                                        dirs_body, tile_rays, tile_cones, n_tiles, tpc, out, hit)
-  if (cfg->kind == 0) { if (ext) QS_RT(0, true); else QS_RT(0, false); }
-  else { if (ext) QS_RT(1, true); else QS_RT(1, false); }
+#define QS_RT(K, X, R)                                                                                  \
+  k_raycast_tiled<K, X, R><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, \
+                                                           dirs_body, tile_rays, tile_cones, n_tiles, tpc, out, hit)
+#define QS_RT_W(K, X)                 \
+  if (tile_width == 32) QS_RT(K, X, 1); \
+  else if (tile_width == 64) QS_RT(K, X, 2); \
+  else QS_RT(K, X, 4)
+  if (cfg->kind == 0) { if (ext) { QS_RT_W(0, true); } else { QS_RT_W(0, false); } }
+  else { if (ext) { QS_RT_W(1, true); } else { QS_RT_W(1, false); } }
+#undef QS_RT_W
 #undef QS_RT
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }

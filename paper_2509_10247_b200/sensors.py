@@ -9,6 +9,7 @@ once per sensor (fp64, as the reference does) and the DAIM dump format.
 
 from __future__ import annotations
 
+import os
 import struct
 from dataclasses import dataclass, field
 
@@ -270,25 +271,29 @@ def _dir_table(sensor, device) -> torch.Tensor:
 _TILE_CACHE: dict = {}
 
 
-def _tile_table(sensor, device):
-    """Group the sensor's rays into angularly compact tiles of 32 with a bounding
-    cone each (fp64 host geometry, once per sensor): 8x4 pixel blocks for a
-    camera, consecutive azimuth-major runs for a LiDAR."""
-    key = (type(sensor).__name__, repr(sensor), str(device))
+def _tile_table(sensor, device, width=None):
+    """Group the sensor's rays into angularly compact tiles of ``width`` (32, 64
+    or 128) with a bounding cone each (fp64 host geometry, once per sensor):
+    8 x (width/8) pixel blocks for a camera, consecutive azimuth-major runs for
+    a LiDAR."""
+    if width is None:
+        width = TILE_WIDTH or (64 if isinstance(sensor, CameraIntrinsics) else 128)
+    key = (type(sensor).__name__, repr(sensor), str(device), width)
     hit = _TILE_CACHE.get(key)
     if hit is not None:
         return hit
     if isinstance(sensor, CameraIntrinsics):
         d = sensor.pixel_dirs()
         W, H = sensor.width, sensor.height
+        bw, bh = (8, width // 8) if width <= 64 else (16, width // 16)
         tiles = []
-        for ty in range(0, H, 4):
-            for tx in range(0, W, 8):
-                tiles.append([r * W + c for r in range(ty, min(H, ty + 4)) for c in range(tx, min(W, tx + 8))])
+        for ty in range(0, H, bh):
+            for tx in range(0, W, bw):
+                tiles.append([r * W + c for r in range(ty, min(H, ty + bh)) for c in range(tx, min(W, tx + bw))])
     else:
         d = sensor.ray_dirs()
-        tiles = [list(range(s, min(len(d), s + 32))) for s in range(0, len(d), 32)]
-    rays = np.full((len(tiles), 32), -1, dtype=np.int32)
+        tiles = [list(range(s, min(len(d), s + width))) for s in range(0, len(d), width)]
+    rays = np.full((len(tiles), width), -1, dtype=np.int32)
     # axis xyz, cos/sin(half-angle) | sector centre xy, cos/sin(sector half-width) | pad
     cones = np.zeros((len(tiles), 12))
     for k, t in enumerate(tiles):
@@ -373,7 +378,7 @@ def cast_rays(scene: DeviceScene, pos: torch.Tensor, pos_stride: int, cam_cs, se
     if not want_grad and kind in (0, 1) and TILED:
         tr, tc = _tile_table(sensor, dev)
         L.check(L.lib().qs_raycast_tiled(rc, scene.struct(), N, L.ptr(pos), pos_stride, L.ptr(cam_cs),
-                                         L.ptr(dirs), L.ptr(tr), L.ptr(tc), tr.shape[0], L.ptr(out),
+                                         L.ptr(dirs), L.ptr(tr), L.ptr(tc), tr.shape[0], tr.shape[1], L.ptr(out),
                                          L.ptr(hit), L.stream_handle(dev)), "qs_raycast_tiled")
         return out, hit, dT
     L.check(L.lib().qs_raycast(rc, scene.struct(), N, L.ptr(pos), pos_stride, L.ptr(cam_cs),
@@ -383,6 +388,10 @@ def cast_rays(scene: DeviceScene, pos: torch.Tensor, pos_stride: int, cam_cs, se
 
 
 TILED = True  # per-warp cone culling (k_raycast_tiled); False selects the untiled kernel
+# rays per tile of the tiled kernel (32 x rays per lane): 0 = per sensor (8x8
+# pixel blocks for cameras, 8 azimuths x 16 elevations for LiDARs, the fastest
+# measured, profiles/README.md); QS_TILE_WIDTH overrides it for A/B runs
+TILE_WIDTH = int(os.environ.get("QS_TILE_WIDTH", "0"))
 
 
 def raycast(prims, origins, dirs, max_range: float, chunk_elems: int = 0, device=None):
