@@ -225,16 +225,17 @@ int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, con
                int32_t pos_stride, const float* cam_cs, const float* dirs_body,
                const float* dirs_world, float* out, uint8_t* hit, float* dT_dO, void* stream);
 /* Same images as qs_raycast (kinds 0/1) with per-warp culling: rays are
- * grouped into n_tiles tiles of tile_width = 32, 64 or 128 rays (tile_rays
- * (n_tiles,tile_width) ray indices, -1 = empty slot; lane j of the tile's warp
- * casts rays j, j+32, ...), each with a body-frame bounding cone and azimuth sector,
+ * grouped into n_tiles tiles of tile_width = 32, 64 or 128 rays; tile_dirs
+ * (n_tiles,tile_width,4) = body-frame unit direction xyz + ray index (as a
+ * float; < 0 = empty slot), lane j of the tile's warp casting slots j, j+32,
+ * ...  Each tile has a body-frame bounding cone and azimuth sector,
  * tile_cones (n_tiles,12) = unit axis xyz, cos(half-angle), sin(half-angle),
  * unit horizontal sector centre xy, cos(sector half-width) (< -1.5: no sector
  * test), sin(sector half-width), min and max direction z, 1 pad. */
 int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
-                     int32_t pos_stride, const float* cam_cs, const float* dirs_body,
-                     const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles,
-                     int32_t tile_width, float* out, uint8_t* hit, void* stream);
+                     int32_t pos_stride, const float* cam_cs, const float* tile_dirs,
+                     const float* tile_cones, int32_t n_tiles, int32_t tile_width, float* out,
+                     uint8_t* hit, void* stream);
 /* d loss / d pos = sum_r g_depth[r] * dT_dO[r]  (N,3) accumulate into g_pos (N,4 stride pos_stride). */
 int qs_raycast_vjp(int32_t n_rows, int32_t n_rays, const float* g_depth, const float* dT_dO,
                    float* g_pos, int32_t pos_stride, void* stream);

@@ -401,10 +401,74 @@ QS_D unsigned hit_cyl_u(unsigned best, float4 c, float4 h, V3 d, float a, float 
   m = r.cb ? min(m, fbits(r.tb)) : m;
   return m;
 }
+// --- packed ray pairs (FFMA2/FMUL2/FADD2, sm_100) -----------------------------
+// Two rays of a lane run each test as f32x2 instructions with the obstacle
+// record as a broadcast scalar operand.  Every packed op is the same IEEE
+// rn op the scalar cores above perform, in the same order, so a pair's depths
+// are bit-identical to the scalar (and untiled) kernels'.
+struct RayPair {
+  float2 dx, dy, dz;  // directions
+  float2 ix, iy, iz;  // reciprocal components
+  float2 a, ia;       // dx^2 + dy^2 and its reciprocal
+};
+QS_D float2 bc(float x) { return make_float2(x, x); }
+QS_D float2 neg2(float2 v) { return make_float2(-v.x, -v.y); }
+QS_D void hit_sphere_p(unsigned& b0, unsigned& b1, float4 s, const RayPair& r) {
+  const float2 b = __ffma2_rn(r.dx, bc(s.x), __ffma2_rn(r.dy, bc(s.y), __fmul2_rn(r.dz, bc(s.z))));
+  const float2 nb = neg2(b);
+  const float2 vx = __ffma2_rn(nb, r.dx, bc(s.x)), vy = __ffma2_rn(nb, r.dy, bc(s.y)),
+               vz = __ffma2_rn(nb, r.dz, bc(s.z));
+  const float2 disc = __ffma2_rn(neg2(vx), vx, __ffma2_rn(neg2(vy), vy, __ffma2_rn(neg2(vz), vz, bc(s.w))));
+  const float2 sq = make_float2(sqrt_approx(disc.x), sqrt_approx(disc.y));
+  const float2 t1 = __fadd2_rn(nb, neg2(sq)), t2 = __fadd2_rn(sq, nb);
+  b0 = umin3(b0, fbits(t1.x), fbits(t2.x));
+  b1 = umin3(b1, fbits(t1.y), fbits(t2.y));
+}
+QS_D unsigned box_u(unsigned best, float t1x, float t2x, float t1y, float t2y, float t1z, float t2z) {
+  const float tn = fmax_nan(fmax_nan(fmin_nan(t1x, t2x), fmin_nan(t1y, t2y)), fmin_nan(t1z, t2z));
+  const float tf = fmin_nan(fmin_nan(fmax_nan(t1x, t2x), fmax_nan(t1y, t2y)), fmax_nan(t1z, t2z));
+  const unsigned c = min(fbits(pos0(tn)), fbits(pos0(tf)));
+  return tn <= tf ? min(best, c) : best;
+}
+QS_D void hit_box_p(unsigned& b0, unsigned& b1, float4 lo, float4 hi, const RayPair& r) {
+  const float2 t1x = __fmul2_rn(bc(lo.x), r.ix), t2x = __fmul2_rn(bc(hi.x), r.ix);
+  const float2 t1y = __fmul2_rn(bc(lo.y), r.iy), t2y = __fmul2_rn(bc(hi.y), r.iy);
+  const float2 t1z = __fmul2_rn(bc(lo.z), r.iz), t2z = __fmul2_rn(bc(hi.z), r.iz);
+  b0 = box_u(b0, t1x.x, t2x.x, t1y.x, t2y.x, t1z.x, t2z.x);
+  b1 = box_u(b1, t1x.y, t2x.y, t1y.y, t2y.y, t1z.y, t2z.y);
+}
+QS_D unsigned cyl_u(unsigned m, float ts1, float ts2, float zs1, float zs2, float tt, float tb, float rt2,
+                    float rb2, float hh, float r2) {
+  m = fabsf(zs1) <= hh ? min(m, fbits(ts1)) : m;
+  m = fabsf(zs2) <= hh ? min(m, fbits(ts2)) : m;
+  m = rt2 <= r2 ? min(m, fbits(tt)) : m;
+  m = rb2 <= r2 ? min(m, fbits(tb)) : m;
+  return m;
+}
+QS_D void hit_cyl_p(unsigned& b0, unsigned& b1, float4 c, float4 h, const RayPair& r) {
+  const float2 b = __ffma2_rn(bc(c.x), r.dx, __fmul2_rn(bc(c.y), r.dy));
+  const float2 cr = __ffma2_rn(bc(c.x), r.dy, neg2(__fmul2_rn(bc(c.y), r.dx)));
+  const float2 disc = __ffma2_rn(r.a, bc(c.w), neg2(__fmul2_rn(cr, cr)));
+  const float2 sq = make_float2(sqrt_approx(disc.x), sqrt_approx(disc.y));
+  const float2 nb = neg2(b);
+  const float2 ts1 = __fmul2_rn(__fadd2_rn(nb, neg2(sq)), r.ia), ts2 = __fmul2_rn(__fadd2_rn(sq, nb), r.ia);
+  const float2 zs1 = __ffma2_rn(ts1, r.dz, bc(c.z)), zs2 = __ffma2_rn(ts2, r.dz, bc(c.z));
+  const float2 tt = __fadd2_rn(__fmul2_rn(bc(h.y), r.iz), bc(0.f));  // pos0
+  const float2 tb = __fadd2_rn(__fmul2_rn(bc(h.z), r.iz), bc(0.f));
+  const float2 xt = __ffma2_rn(tt, r.dx, bc(c.x)), yt = __ffma2_rn(tt, r.dy, bc(c.y));
+  const float2 xb = __ffma2_rn(tb, r.dx, bc(c.x)), yb = __ffma2_rn(tb, r.dy, bc(c.y));
+  const float2 rt2 = __ffma2_rn(xt, xt, __fmul2_rn(yt, yt)), rb2 = __ffma2_rn(xb, xb, __fmul2_rn(yb, yb));
+  b0 = cyl_u(b0, ts1.x, ts2.x, zs1.x, zs2.x, tt.x, tb.x, rt2.x, rb2.x, h.x, c.w);
+  b1 = cyl_u(b1, ts1.y, ts2.y, zs1.y, zs2.y, tt.y, tb.y, rt2.y, rb2.y, h.x, c.w);
+}
+
 // lanes [0, k) of a warp, k clamped to [0, 32]
 QS_D unsigned lanes_below(int k) { return k >= 32 ? 0xffffffffu : (k <= 0 ? 0u : (1u << k) - 1u); }
 
-constexpr int TILED_BLOCK = 128;
+#ifndef QS_TILED_BLOCK
+#define QS_TILED_BLOCK 128
+#endif
+constexpr int TILED_BLOCK = QS_TILED_BLOCK;
 
 // EXT (qs_ray_cfg.cull bit 1): box footprints use their exact azimuth interval
 // and every obstacle carries vertical flags.  That costs a third record load
@@ -416,9 +480,8 @@ constexpr int TILED_BLOCK = 128;
 template <int KIND, bool EXT, int RPL>
 __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
-    const float* __restrict__ cam_cs, const float* __restrict__ dirs_body, const int* __restrict__ tile_rays,
-    const float* __restrict__ tile_cones, int n_tiles, int tiles_per_cta, float* __restrict__ out,
-    uint8_t* __restrict__ hitm) {
+    const float* __restrict__ cam_cs, const float* __restrict__ tile_dirs, const float* __restrict__ tile_cones,
+    int n_tiles, int tiles_per_cta, float* __restrict__ out, uint8_t* __restrict__ hitm) {
   extern __shared__ float4 sm[];
   __shared__ int cnt[3];
   const long row = blockIdx.y;
@@ -444,6 +507,7 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
   // circle's tangent length and radius for the sector test, a_all unused.
   float4* a_all = b_all + cap;
   float4* f_all = a_all + (EXT ? cap : 0);
+  uint2* kmask = reinterpret_cast<uint2*>(f_all + cap);  // per 32-chunk: (sphere lanes, sphere|box lanes)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   if (warp == 0) {
     const int tot_in = sv.ns + sv.nb + sv.nc;
@@ -511,6 +575,8 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       cnt[1] = kb;
       cnt[2] = run - ks - kb;
     }
+    for (int c = lane; c * 32 < run; c += 32)
+      kmask[c] = make_uint2(lanes_below(ks - 32 * c), lanes_below(ks + kb - 32 * c));
   }
   __syncthreads();
   const int ns = cnt[0], nb = cnt[1], nc = cnt[2];
@@ -518,6 +584,8 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
   const bool ground = sv.ground;
   const float gdz = sv.gz - o.z;
   const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
+  float* out_row = out + row * rc.n_rays;
+  uint8_t* hitm_row = hitm ? hitm + row * rc.n_rays : nullptr;
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
     // tile record (12 floats): cone axis xyz, cos, sin | azimuth centre xy, cos, sin of the sector
     const float4 c0 = ld4(tile_cones, 3 * tile), c1 = ld4(tile_cones, 3 * tile + 1);
@@ -528,19 +596,38 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
     const float cth = c0.w, sth = c1.x;
     const float2 azw = make_float2(cs.x * c1.y - cs.y * c1.z, cs.y * c1.y + cs.x * c1.z);
     const float cw = c1.w;
+    // lane's rays: body-frame direction + ray index from the tile-ordered table
+    constexpr int NP = RPL / 2;  // packed pairs (RPL >= 2)
     int ray[RPL];
-    V3 d[RPL], inv[RPL];
-    float a[RPL], inv_a[RPL];
+    V3 d[RPL];
     unsigned best[RPL];
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
-      ray[k] = __ldg(tile_rays + (tile * RPL + k) * 32 + lane);
-      d[k] = v3(1.f, 0.f, 0.f);
-      if (ray[k] >= 0) d[k] = rotz(cs, xyz(ld4(dirs_body, ray[k])));
+      const float4 td = ld4(tile_dirs, (tile * RPL + k) * 32 + lane);
+      ray[k] = (int)td.w;
+      d[k] = rotz(cs, xyz(td));
+      best[k] = INF_BITS;
+    }
+    V3 inv[RPL];
+    float a[RPL], inv_a[RPL];
+    RayPair rp[NP > 0 ? NP : 1];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
       inv[k] = v3(rcp_fast(d[k].x), rcp_fast(d[k].y), rcp_fast(d[k].z));
       a[k] = d[k].x * d[k].x + d[k].y * d[k].y;
       inv_a[k] = rcp_fast(a[k]);
-      best[k] = INF_BITS;
+    }
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+      const int k0 = 2 * p, k1 = 2 * p + 1;
+      rp[p].dx = make_float2(d[k0].x, d[k1].x);
+      rp[p].dy = make_float2(d[k0].y, d[k1].y);
+      rp[p].dz = make_float2(d[k0].z, d[k1].z);
+      rp[p].ix = make_float2(inv[k0].x, inv[k1].x);
+      rp[p].iy = make_float2(inv[k0].y, inv[k1].y);
+      rp[p].iz = make_float2(inv[k0].z, inv[k1].z);
+      rp[p].a = make_float2(a[k0], a[k1]);
+      rp[p].ia = make_float2(inv_a[k0], inv_a[k1]);
     }
     for (int base = 0; base < tot; base += 32) {
       const int j = base + lane;
@@ -560,28 +647,40 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       // warp-uniform candidate masks, split by kind (the list is kind-sorted:
       // spheres, boxes, cylinders), so each loop runs one test with no dispatch
       const unsigned m = __ballot_sync(0xffffffffu, keep);
-      const unsigned lt_s = lanes_below(ns - base), lt_b = lanes_below(ns + nb - base);
-      unsigned ms = m & lt_s, mb = m & lt_b & ~lt_s, mc = m & ~lt_b;
+      const uint2 km = kmask[base >> 5];
+      unsigned ms = m & km.x, mb = m & km.y & ~km.x, mc = m & ~km.y;
       while (ms) {
         const int i = base + __ffs(ms) - 1;
         ms &= ms - 1;
         const float4 q = r0[i];
+        if constexpr (NP > 0) {
 #pragma unroll
-        for (int k = 0; k < RPL; ++k) best[k] = hit_sphere_u(best[k], q, d[k]);
+          for (int p = 0; p < NP; ++p) hit_sphere_p(best[2 * p], best[2 * p + 1], q, rp[p]);
+        } else {
+          best[0] = hit_sphere_u(best[0], q, d[0]);
+        }
       }
       while (mb) {
         const int i = base + __ffs(mb) - 1;
         mb &= mb - 1;
         const float4 lo = r0[i], hi = r1[i];
+        if constexpr (NP > 0) {
 #pragma unroll
-        for (int k = 0; k < RPL; ++k) best[k] = hit_box_u(best[k], lo, hi, inv[k]);
+          for (int p = 0; p < NP; ++p) hit_box_p(best[2 * p], best[2 * p + 1], lo, hi, rp[p]);
+        } else {
+          best[0] = hit_box_u(best[0], lo, hi, inv[0]);
+        }
       }
       while (mc) {
         const int i = base + __ffs(mc) - 1;
         mc &= mc - 1;
         const float4 q = r0[i], h = r1[i];
+        if constexpr (NP > 0) {
 #pragma unroll
-        for (int k = 0; k < RPL; ++k) best[k] = hit_cyl_u(best[k], q, h, d[k], a[k], inv_a[k], inv[k].z);
+          for (int p = 0; p < NP; ++p) hit_cyl_p(best[2 * p], best[2 * p + 1], q, h, rp[p]);
+        } else {
+          best[0] = hit_cyl_u(best[0], q, h, d[0], a[0], inv_a[0], inv[0].z);
+        }
       }
     }
 #pragma unroll
@@ -589,9 +688,8 @@ __global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
       if (ground) best[k] = min(best[k], fbits(pos0(gdz * inv[k].z)));  // +inf / NaN / t < 0 drop out
       if (ray[k] >= 0) {
         const float t = __uint_as_float(best[k]);
-        const long oi = row * rc.n_rays + ray[k];
-        out[oi] = fminf(t, rc.max_range);
-        if (hitm) hitm[oi] = t < rc.max_range ? 1 : 0;
+        out_row[ray[k]] = fminf(t, rc.max_range);
+        if (hitm) hitm_row[ray[k]] = t < rc.max_range ? 1 : 0;
       }
     }
   }
@@ -652,8 +750,8 @@ int qs_raycast(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, con
 }
 
 int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
-                     int32_t pos_stride, const float* cam_cs, const float* dirs_body,
-                     const int32_t* tile_rays, const float* tile_cones, int32_t n_tiles, int32_t tile_width,
+                     int32_t pos_stride, const float* cam_cs, const float* tile_dirs,
+                     const float* tile_cones, int32_t n_tiles, int32_t tile_width,
                      float* out, uint8_t* hit, void* stream) {
   if (n_rows <= 0 || cfg->n_rays <= 0) return QS_OK;
   if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0) return QS_ERR_BAD_ARGUMENT;
@@ -661,11 +759,12 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   const int tpc = n_tiles;  // one CTA per row: the staged obstacles serve every tile
   dim3 grid((n_tiles + tpc - 1) / tpc, n_rows);
   const bool ext = (cfg->cull & 2) != 0;
-  size_t smem = (size_t)(scene->Sm + scene->Bm + scene->Cm) * ((ext ? 5 : 4) * 16);
+  const int cap = scene->Sm + scene->Bm + scene->Cm;
+  size_t smem = (size_t)cap * ((ext ? 5 : 4) * 16) + (size_t)((cap + 31) / 32 + 1) * 8;
   cudaStream_t s = (cudaStream_t)stream;
 #define QS_RT(K, X, R)                                                                                  \
   k_raycast_tiled<K, X, R><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, \
-                                                           dirs_body, tile_rays, tile_cones, n_tiles, tpc, out, hit)
+                                                           tile_dirs, tile_cones, n_tiles, tpc, out, hit)
 #define QS_RT_W(K, X)                 \
   if (tile_width == 32) QS_RT(K, X, 1); \
   else if (tile_width == 64) QS_RT(K, X, 2); \

@@ -327,7 +327,16 @@ def _tile_table(sensor, device, width=None):
             cones[k, 7] = -2.0
         cones[k, 9] = float(v[:, 2].min())  # vertical range of the tile's directions
         cones[k, 10] = float(v[:, 2].max())
-    out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device))
+    # tile-ordered direction table for the kernel: (dir xyz as the fp32 values
+    # of the sensor's ray table, ray index; -1 = empty slot)
+    dirs32 = d.astype(np.float32)
+    td = np.zeros((len(tiles), width, 4), dtype=np.float32)
+    td[..., 3] = -1.0
+    ok = rays >= 0
+    td[ok, :3] = dirs32[rays[ok]]
+    td[ok, 3] = rays[ok]
+    out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device),
+           torch.as_tensor(td, device=device))
     _TILE_CACHE[key] = out
     return out
 
@@ -376,9 +385,9 @@ def cast_rays(scene: DeviceScene, pos: torch.Tensor, pos_stride: int, cam_cs, se
     dT = torch.empty(N, rc.n_rays, 4, dtype=torch.float32, device=dev) if want_grad else None
     dirs = _dir_table(sensor, dev)
     if not want_grad and kind in (0, 1) and TILED:
-        tr, tc = _tile_table(sensor, dev)
+        tr, tc, td = _tile_table(sensor, dev)
         L.check(L.lib().qs_raycast_tiled(rc, scene.struct(), N, L.ptr(pos), pos_stride, L.ptr(cam_cs),
-                                         L.ptr(dirs), L.ptr(tr), L.ptr(tc), tr.shape[0], tr.shape[1], L.ptr(out),
+                                         L.ptr(td), L.ptr(tc), tr.shape[0], tr.shape[1], L.ptr(out),
                                          L.ptr(hit), L.stream_handle(dev)), "qs_raycast_tiled")
         return out, hit, dT
     L.check(L.lib().qs_raycast(rc, scene.struct(), N, L.ptr(pos), pos_stride, L.ptr(cam_cs),

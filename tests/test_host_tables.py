@@ -7,17 +7,24 @@ import pytest
 import torch
 
 
+@pytest.mark.parametrize("width", [32, 64, 128])
 @pytest.mark.parametrize("kind", ["camera", "lidar", "lidar_full"])
-def test_tile_tables_bound_their_rays(kind):
+def test_tile_tables_bound_their_rays(kind, width):
     from paper_2509_10247_b200 import sensors as sn
 
     sensor = {"camera": sn.CameraIntrinsics(width=64, height=48, max_range=10.0),
               "lidar": sn.LidarPattern(n_azimuth=360, n_elevation=16, max_range=20.0),
               "lidar_full": sn.LidarPattern(n_azimuth=90, n_elevation=4, max_range=20.0)}[kind]
     sn._TILE_CACHE.clear()
-    rays, cones = sn._tile_table(sensor, torch.device("cpu"))
-    rays, cones = rays.numpy(), cones.double().numpy()
+    rays, cones, tdirs = sn._tile_table(sensor, torch.device("cpu"), width)
+    rays, cones, tdirs = rays.numpy(), cones.double().numpy(), tdirs.numpy()
     d = sensor.pixel_dirs() if kind == "camera" else sensor.ray_dirs()
+    assert rays.shape[1] == width and tdirs.shape == (rays.shape[0], width, 4)
+    # the kernel's tile-ordered direction table repeats the ray table's fp32 values
+    dir32 = sn._dir_table(sensor, torch.device("cpu")).numpy()
+    ok = rays >= 0
+    assert np.array_equal(tdirs[ok][:, :3], dir32[rays[ok], :3])
+    assert np.array_equal(tdirs[..., 3], rays.astype(np.float32))
     got = np.sort(rays[rays >= 0])
     assert np.array_equal(got, np.arange(len(d)))  # a partition of the rays
     for t in range(len(rays)):
