@@ -466,7 +466,7 @@ QS_D void hit_cyl_p(unsigned& b0, unsigned& b1, float4 c, float4 h, const RayPai
 QS_D unsigned lanes_below(int k) { return k >= 32 ? 0xffffffffu : (k <= 0 ? 0u : (1u << k) - 1u); }
 
 #ifndef QS_TILED_BLOCK
-#define QS_TILED_BLOCK 128
+#define QS_TILED_BLOCK 64  // two warps per env: the staging barrier idles one warp, not three
 #endif
 constexpr int TILED_BLOCK = QS_TILED_BLOCK;
 
