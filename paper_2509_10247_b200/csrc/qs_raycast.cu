@@ -466,7 +466,13 @@ QS_D void hit_cyl_p(unsigned& b0, unsigned& b1, float4 c, float4 h, const RayPai
 QS_D unsigned lanes_below(int k) { return k >= 32 ? 0xffffffffu : (k <= 0 ? 0u : (1u << k) - 1u); }
 
 #ifndef QS_TILED_BLOCK
-#define QS_TILED_BLOCK 64  // two warps per env: the staging barrier idles one warp, not three
+// one warp per env: staging needs no CTA barrier and its latency is spread
+// over all of the env's tiles; 24+ resident CTAs per SM cap the registers so
+// that ~32 warps fit (measured best: profiles/README.md)
+#define QS_TILED_BLOCK 32
+#endif
+#ifndef QS_TILED_MINB
+#define QS_TILED_MINB 24
 #endif
 constexpr int TILED_BLOCK = QS_TILED_BLOCK;
 
@@ -478,7 +484,7 @@ constexpr int TILED_BLOCK = QS_TILED_BLOCK;
 // ...), so the tile's cone test, ballot, candidate loop and obstacle-record
 // loads are shared by RPL rays, and each candidate runs RPL independent tests.
 template <int KIND, bool EXT, int RPL>
-__global__ void __launch_bounds__(TILED_BLOCK) k_raycast_tiled(
+__global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
     const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
     const float* __restrict__ cam_cs, const float* __restrict__ tile_dirs, const float* __restrict__ tile_cones,
     int n_tiles, int tiles_per_cta, float* __restrict__ out, uint8_t* __restrict__ hitm) {
