@@ -335,7 +335,7 @@ QS_D void imu_apply_z(const qs_task_cfg& cfg, long row, const State& s2, V3 vdot
 // rewards (q/tasks.py:144-170, 625-637, 744-763, 817-844)
 
 struct RewardFwd {
-  float r, dist, speed;
+  float r, dist, speed, nearv, track;
 };
 
 QS_D RewardFwd reward_ctrl(const qs_weights& w, V3 off, V3 v, float effn, float deffn) {
@@ -350,7 +350,7 @@ QS_D RewardFwd reward_ctrl(const qs_weights& w, V3 off, V3 v, float effn, float 
   pen = pen + effn * w.w_a;
   pen = pen + deffn * w.w_s;
   pen = pen + track * w.w_t;
-  return RewardFwd{-pen, dist, speed};
+  return RewardFwd{-pen, dist, speed, nearv, track};
 }
 
 // RL scalar (q/tasks.py:744-763): never differentiated, so the divisions use
@@ -364,6 +364,19 @@ QS_D float reward_rl(const qs_weights& w, float clip, V3 off, V3 v, float effn, 
   float track = norm3(v - vdes);
   float dist_c = fminf(dist, clip);
   return -(w.w_p * dist_c + w.w_v * speed * nearv + w.w_a * effn + w.w_s * deffn + w.w_t * track);
+}
+
+// the same RL scalar from reward_ctrl's terms: when the RL weights share the
+// control weights' shape parameters (near radius/width, tracking gain, v_max
+// -- the reference's defaults), dist, speed, near and track are the identical
+// fp32 values, so only the weighted sum is recomputed
+QS_D bool rl_shares_shape(const qs_weights& w, const qs_weights& wr) {
+  return w.near_radius == wr.near_radius && w.near_width == wr.near_width && w.track_gain == wr.track_gain &&
+         w.v_max == wr.v_max;
+}
+QS_D float reward_rl_from(const qs_weights& w, float clip, const RewardFwd& rf, float effn, float deffn) {
+  const float dist_c = fminf(rf.dist, clip);
+  return -(w.w_p * dist_c + w.w_v * rf.speed * rf.nearv + w.w_a * effn + w.w_s * deffn + w.w_t * rf.track);
 }
 
 // VJP of reward_ctrl: returns grads wrt off, v, effort vec, d_effort vec
@@ -647,7 +660,9 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, l
       extra = -(cfg.w_rl.w_o * softplus((cfg.d_safe - sd) / cfg.w_rl.sdf_sharpness));
     }
     rc = rf.r;
-    rl = reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn) + extra;
+    rl = (rl_shares_shape(cfg.w, cfg.w_rl) ? reward_rl_from(cfg.w_rl, cfg.obs_clip, rf, en, dn)
+                                           : reward_rl(cfg.w_rl, cfg.obs_clip, off, n.v, en, dn)) +
+         extra;
     goal_ok = (rf.dist < cfg.success_radius) && (rf.speed < cfg.hover_speed);
   }
   const bool oob = n.p.x < blo.x || n.p.y < blo.y || n.p.z < blo.z || n.p.x > bhi.x || n.p.y > bhi.y ||
