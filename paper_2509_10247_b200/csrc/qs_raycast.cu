@@ -66,6 +66,10 @@ QS_D float rcp_fast(float x) {  // one MUFU.RCP; 1/(+-0) = +-inf, 1/(+-inf) = +-
   return y;
 }
 QS_D float pos0(float x) { return __fadd_rn(x, 0.f); }  // -0 -> +0, else x
+// yaw rotation and |d_xy|^2 with explicit FMAs, so every kernel (and every
+// tile width) rounds them identically
+QS_D V3 rotz_f(float2 cs, V3 v) { return v3(fmaf(cs.x, v.x, -cs.y * v.y), fmaf(cs.y, v.x, cs.x * v.y), v.z); }
+QS_D float dxy2(V3 d) { return fmaf(d.x, d.x, d.y * d.y); }
 
 // sphere record: (oc.xyz, r^2), oc = o - c.  Robust discriminant
 // r^2 - |oc - b d|^2 (== b^2 - (|oc|^2 - r^2) in exact arithmetic); its sqrt is
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
   float2 cs = make_float2(1.f, 0.f);
   if (cam_cs) cs = reinterpret_cast<const float2*>(cam_cs)[row];
   const float* pp = pos + row * pos_stride;
-  V3 off = rotz(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
+  V3 off = rotz_f(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
   V3 o = v3(pp[0], pp[1], pp[2]) + off;
   SceneView sv = scene_view(sc, e);
   float4* s_sph = sm;
@@ -214,10 +218,10 @@ __global__ void __launch_bounds__(RAY_BLOCK) k_raycast(const qs_ray_cfg rc, cons
     if (KIND == 2) {
       d = xyz(ld4(dirs_world, row * rc.n_rays + r));
     } else {
-      d = rotz(cs, xyz(ld4(dirs_body, r)));
+      d = rotz_f(cs, xyz(ld4(dirs_body, r)));
     }
     const V3 inv = v3(rcp_fast(d.x), rcp_fast(d.y), rcp_fast(d.z));
-    const float a = d.x * d.x + d.y * d.y;
+    const float a = dxy2(d);
     const float inv_a = rcp_fast(a);
     float best = INF;
     int code = 0, bidx = 0;  // kind | detail, shared-memory index of the argmin
@@ -495,7 +499,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
   float2 cs = make_float2(1.f, 0.f);
   if (cam_cs) cs = reinterpret_cast<const float2*>(cam_cs)[row];
   const float* pp = pos + row * pos_stride;
-  V3 o = v3(pp[0], pp[1], pp[2]) + rotz(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
+  V3 o = v3(pp[0], pp[1], pp[2]) + rotz_f(cs, v3(rc.offset[0], rc.offset[1], rc.offset[2]));
   SceneView sv = scene_view(sc, e);
   // One list of kept obstacles in input order (spheres, boxes, cylinders, so
   // the list stays kind-sorted), each with two intersection records
@@ -611,7 +615,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
     for (int k = 0; k < RPL; ++k) {
       const float4 td = ld4(tile_dirs, (tile * RPL + k) * 32 + lane);
       ray[k] = (int)td.w;
-      d[k] = rotz(cs, xyz(td));
+      d[k] = rotz_f(cs, xyz(td));
       best[k] = INF_BITS;
     }
     V3 inv[RPL];
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
       inv[k] = v3(rcp_fast(d[k].x), rcp_fast(d[k].y), rcp_fast(d[k].z));
-      a[k] = d[k].x * d[k].x + d[k].y * d[k].y;
+      a[k] = dxy2(d[k]);
       inv_a[k] = rcp_fast(a[k]);
     }
 #pragma unroll
