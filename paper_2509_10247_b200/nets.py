@@ -1,0 +1,325 @@
+"""Policy / value networks of the learners, as torch modules (q/nets.py).
+
+The caller side of the simulation core: the only dense
+contractions of the reference, so on the GPU they are plain torch layers whose
+matmuls and convolutions run on the tensor cores through cuBLAS/cuDNN (library
+code, not the hot path).  What is mirrored exactly:
+
+- architecture and parameter names of ``q/nets.py:85-274`` -- ``Linear`` (x W +
+  b, W stored (n_in, n_out)), the tanh ``MLP`` with a linear last layer, the
+  GRU cell (gate order r, z, n), the two-conv ``ConvEncoder`` (3x3 stride 2,
+  im2col channel-major patches, position-major flatten), the LiDAR linear
+  encoder, the Gaussian policy heads with log_sigma clamped to [-5, max];
+- initialisation: built with a numpy Generator, every array is drawn from it
+  in the reference's order with the same Xavier scales, so a learner seeded
+  like the reference starts from the reference's weights;
+- the weight container (``q/nets.py:316-377``): ``manifest.json`` +
+  little-endian float32 ``weights.bin``, readable by the reference and vice
+  versa, with the same integrity errors.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+CONTAINER_VERSION = 1  # q/nets.py:21
+LOG_SIGMA_MIN = -5.0
+LOG_SIGMA_MAX = 2.0
+
+
+class IntegrityError(RuntimeError):
+    """q/nets.py:26-27."""
+
+
+def _xavier(rng, n_in, n_out, scale=1.0):  # q/nets.py:64-66
+    s = scale * np.sqrt(2.0 / (n_in + n_out))
+    return rng.normal(scale=s, size=(n_in, n_out))
+
+
+class Linear(torch.nn.Module):
+    """y = x W + b with W (n_in, n_out) (q/nets.py:73-82); ``tag`` is the
+    container's activation tag."""
+
+    def __init__(self, n_in, n_out, rng=None, scale=1.0, tag="linear"):
+        super().__init__()
+        w = _xavier(rng, n_in, n_out, scale) if rng is not None else np.zeros((n_in, n_out))
+        self.W = torch.nn.Parameter(torch.as_tensor(w, dtype=torch.float32))
+        self.b = torch.nn.Parameter(torch.zeros(n_out))
+        self.tag = tag
+
+    def forward(self, x):
+        return torch.addmm(self.b.to(x.dtype), x, self.W.to(x.dtype)) if x.dim() == 2 else x @ self.W + self.b
+
+
+class MLP(torch.nn.Module):
+    """tanh MLP, linear last layer; layers l0, l1, ... (q/nets.py:85-104)."""
+
+    def __init__(self, n_in, hidden, n_out, rng=None, out_scale=1.0):
+        super().__init__()
+        sizes = [n_in] + list(hidden) + [n_out]
+        self.layers = torch.nn.ModuleList()
+        for i in range(len(sizes) - 1):
+            last = i == len(sizes) - 2
+            self.layers.append(Linear(sizes[i], sizes[i + 1], rng, out_scale if last else 1.0,
+                                      "linear" if last else "tanh"))
+
+    def forward(self, x):
+        for i, layer in enumerate(self.layers):
+            x = layer(x)
+            if i < len(self.layers) - 1:
+                x = torch.tanh(x)
+        return x
+
+
+class GRUCell(torch.nn.Module):
+    """Standard GRU equations with the reference's layout (q/nets.py:107-132):
+    Wi (n_in, 3H), Wh (H, 3H), gates (r, z, n)."""
+
+    def __init__(self, n_in, n_hidden, rng=None):
+        super().__init__()
+        H = n_hidden
+        wi = _xavier(rng, n_in, 3 * H) if rng is not None else np.zeros((n_in, 3 * H))
+        wh = _xavier(rng, H, 3 * H) if rng is not None else np.zeros((H, 3 * H))
+        self.Wi = torch.nn.Parameter(torch.as_tensor(wi, dtype=torch.float32))
+        self.Wh = torch.nn.Parameter(torch.as_tensor(wh, dtype=torch.float32))
+        self.bi = torch.nn.Parameter(torch.zeros(3 * H))
+        self.bh = torch.nn.Parameter(torch.zeros(3 * H))
+        self.n_hidden = H
+
+    def forward(self, x, h):
+        # torch's fused GRU cell takes (3H, n_in) weights with the same gate order
+        if x.is_cuda or x.dtype == torch.float32:
+            return torch._VF.gru_cell(x, h, self.Wi.t().to(x.dtype), self.Wh.t().to(x.dtype),
+                                      self.bi.to(x.dtype), self.bh.to(x.dtype))
+        H = self.n_hidden
+        gi = x @ self.Wi + self.bi
+        gh = h @ self.Wh + self.bh
+        r = torch.sigmoid(gi[:, :H] + gh[:, :H])
+        z = torch.sigmoid(gi[:, H:2 * H] + gh[:, H:2 * H])
+        n = torch.tanh(gi[:, 2 * H:] + r * gh[:, 2 * H:])
+        return (1.0 - z) * n + z * h
+
+
+class ConvEncoder(torch.nn.Module):
+    """Two 3x3 stride-2 tanh convs (1 -> c1 -> c2), position-major flatten,
+    tanh linear (q/nets.py:135-180).  k1 (9, c1), k2 (9 c1, c2) in the
+    reference's im2col layout (row = c_in * 9 + 3 di + dj)."""
+
+    def __init__(self, height, width, n_out, rng=None, c1=8, c2=16):
+        super().__init__()
+        self.c1, self.c2 = c1, c2
+        self.h1, self.w1 = (height - 3) // 2 + 1, (width - 3) // 2 + 1
+        self.h2, self.w2 = (self.h1 - 3) // 2 + 1, (self.w1 - 3) // 2 + 1
+        if self.h2 < 1 or self.w2 < 1:
+            raise ValueError(f"image {height}x{width} too small for the 2-conv encoder")
+        z = lambda *s: np.zeros(s)  # noqa: E731
+        self.k1 = torch.nn.Parameter(torch.as_tensor(_xavier(rng, 9, c1) if rng is not None else z(9, c1),
+                                                     dtype=torch.float32))
+        self.b1 = torch.nn.Parameter(torch.zeros(c1))
+        self.k2 = torch.nn.Parameter(torch.as_tensor(_xavier(rng, 9 * c1, c2) if rng is not None
+                                                     else z(9 * c1, c2), dtype=torch.float32))
+        self.b2 = torch.nn.Parameter(torch.zeros(c2))
+        self.flat = c2 * self.h2 * self.w2
+        self.out = Linear(self.flat, n_out, rng, tag="tanh")
+
+    @staticmethod
+    def _kernel(k, c_in):  # (c_in * 9, c_out) -> (c_out, c_in, 3, 3)
+        return k.t().reshape(k.shape[1], c_in, 3, 3)
+
+    def forward(self, img):
+        B = img.shape[0]
+        x = img.reshape(B, 1, img.shape[-2], img.shape[-1])
+        k1, k2 = self._kernel(self.k1, 1).to(x.dtype), self._kernel(self.k2, self.c1).to(x.dtype)
+        y = torch.tanh(torch.nn.functional.conv2d(x, k1, self.b1.to(x.dtype), stride=2))
+        y = torch.tanh(torch.nn.functional.conv2d(y, k2, self.b2.to(x.dtype), stride=2))
+        feat = y.permute(0, 2, 3, 1).reshape(B, self.flat)  # position-major, as the im2col rows
+        return torch.tanh(self.out(feat))
+
+
+@dataclass
+class PolicyArch:
+    """q/nets.py:183-195."""
+
+    proprio_dim: int
+    action_dim: int
+    visual: dict | None = None  # {"kind": "depth", "height", "width", "max_range"} | {"kind": "lidar", "rays", ...}
+    recurrent: bool = True
+    hidden: int = 64
+    mlp: tuple = (128, 128)
+    conv_feat: int = 32
+    log_sigma_init: float = -1.2
+    log_sigma_max: float = LOG_SIGMA_MAX
+    input_scale: tuple | None = None
+
+
+class PolicyNet(torch.nn.Module):
+    """Optionally recurrent, optionally convolutional Gaussian policy
+    (q/nets.py:198-256): forward -> (mu, log_sigma, next_hidden)."""
+
+    def __init__(self, arch: PolicyArch, rng=None):
+        super().__init__()
+        self.arch = arch
+        # fp64 like the reference's conditioning; cast to the input's dtype per call
+        scale = torch.ones(arch.proprio_dim, dtype=torch.float64) if arch.input_scale is None else \
+            torch.as_tensor(arch.input_scale, dtype=torch.float64)
+        self.register_buffer("input_scale", scale)
+        feat = arch.proprio_dim
+        self.enc = None
+        if arch.visual is not None:
+            if arch.visual["kind"] == "depth":
+                self.enc = ConvEncoder(arch.visual["height"], arch.visual["width"], arch.conv_feat, rng)
+            else:  # lidar ranges enter as a flat vector
+                self.enc = Linear(arch.visual["rays"], arch.conv_feat, rng, tag="tanh")
+            feat += arch.conv_feat
+        self.gru = GRUCell(feat, arch.hidden, rng) if arch.recurrent else None
+        self.trunk = MLP(arch.hidden if arch.recurrent else feat, arch.mlp, arch.mlp[-1], rng)
+        self.mu = Linear(arch.mlp[-1], arch.action_dim, rng, scale=0.01)
+        self.sig = Linear(arch.mlp[-1], arch.action_dim, rng, scale=0.01)
+        with torch.no_grad():
+            self.sig.b.fill_(arch.log_sigma_init)
+        self.hidden = arch.hidden
+
+    def initial_hidden(self, batch, device=None):
+        return torch.zeros(batch, self.hidden, device=device) if self.gru is not None else None
+
+    def forward(self, proprio, visual=None, h=None):
+        x = proprio * self.input_scale.to(proprio.dtype)
+        if self.enc is not None:
+            if visual is None:
+                raise ValueError("policy expects a visual observation")
+            img = visual.to(x.dtype) * (1.0 / float(self.arch.visual.get("max_range", 1.0)))
+            f = self.enc(img) if self.arch.visual["kind"] == "depth" else torch.tanh(self.enc(img))
+            x = torch.cat([x, f.to(x.dtype)], -1)
+        if self.gru is not None:
+            if h is None:
+                h = torch.zeros(x.shape[0], self.hidden, device=x.device, dtype=x.dtype)
+            h = self.gru(x, h.to(x.dtype)).float() if x.dtype != torch.float64 else self.gru(x, h)
+            x = h.to(x.dtype)
+        z = torch.tanh(self.trunk(x))
+        mu, ls = self.mu(z), self.sig(z)
+        out_t = torch.float64 if z.dtype == torch.float64 else torch.float32
+        return mu.to(out_t), torch.clamp(ls.to(out_t), LOG_SIGMA_MIN, self.arch.log_sigma_max), h
+
+    def n_params(self) -> int:
+        return sum(p.numel() for p in self.parameters())
+
+
+class ValueNet(torch.nn.Module):
+    """Privileged-state MLP critic (q/nets.py:259-274): (B, K) -> (B,);
+    parameters value.l0, value.l1, ..."""
+
+    def __init__(self, n_in, rng=None, hidden=(128, 128), input_scale=None):
+        super().__init__()
+        scale = torch.ones(n_in, dtype=torch.float64) if input_scale is None else \
+            torch.as_tensor(input_scale, dtype=torch.float64)
+        self.register_buffer("input_scale", scale)
+        self.value = MLP(n_in, hidden, 1, rng)
+
+    def forward(self, x):
+        x = x * self.input_scale.to(x.dtype)
+        y = self.value(x)[..., 0]
+        return y if y.dtype == torch.float64 else y.float()
+
+    def n_params(self) -> int:
+        return sum(p.numel() for p in self.parameters())
+
+
+# ---------------------------------------------------------------------------
+# the reference's parameter names <-> module parameters
+
+
+def ref_params(module: torch.nn.Module) -> dict:
+    """Ordered {reference name: (parameter, activation tag)}, in the order the
+    reference's ParamSet holds them (its construction order)."""
+    out = {}
+    if isinstance(module, PolicyNet):
+        if module.enc is not None:
+            if isinstance(module.enc, ConvEncoder):
+                e = module.enc
+                out.update({"enc.k1": (e.k1, "conv"), "enc.b1": (e.b1, "conv"), "enc.k2": (e.k2, "conv"),
+                            "enc.b2": (e.b2, "conv"), "enc.out.W": (e.out.W, "tanh"),
+                            "enc.out.b": (e.out.b, "tanh")})
+            else:
+                out.update({"enc.lidar.W": (module.enc.W, "tanh"), "enc.lidar.b": (module.enc.b, "tanh")})
+        if module.gru is not None:
+            g = module.gru
+            out.update({"gru.Wi": (g.Wi, "gru"), "gru.Wh": (g.Wh, "gru"), "gru.bi": (g.bi, "gru"),
+                        "gru.bh": (g.bh, "gru")})
+        for i, layer in enumerate(module.trunk.layers):
+            out[f"trunk.l{i}.W"] = (layer.W, layer.tag)
+            out[f"trunk.l{i}.b"] = (layer.b, layer.tag)
+        out.update({"mu.W": (module.mu.W, "linear"), "mu.b": (module.mu.b, "linear"),
+                    "sig.W": (module.sig.W, "linear"), "sig.b": (module.sig.b, "linear")})
+    elif isinstance(module, ValueNet):
+        for i, layer in enumerate(module.value.layers):
+            out[f"value.l{i}.W"] = (layer.W, layer.tag)
+            out[f"value.l{i}.b"] = (layer.b, layer.tag)
+    else:
+        raise TypeError("ref_params expects a PolicyNet or ValueNet")
+    return out
+
+
+def save_container(dirpath: str, modules: dict, meta: dict) -> None:
+    """manifest.json + weights.bin, little-endian float32 (q/nets.py:316-345);
+    ``modules`` maps set names ("policy", "value") to PolicyNet / ValueNet."""
+    os.makedirs(dirpath, exist_ok=True)
+    layers, blobs, offset = [], [], 0
+    for set_name, mod in modules.items():
+        for name, (p, tag) in ref_params(mod).items():
+            a32 = p.detach().double().cpu().numpy().astype("<f4")
+            layers.append({"set": set_name, "name": name, "shape": list(a32.shape), "activation": tag,
+                           "offset": offset})
+            blobs.append(a32.tobytes(order="C"))
+            offset += a32.size
+    manifest = {"format_version": CONTAINER_VERSION, "total_floats": offset, "layers": layers, **meta}
+    with open(os.path.join(dirpath, "manifest.json"), "w") as f:
+        json.dump(manifest, f, indent=2)
+    with open(os.path.join(dirpath, "weights.bin"), "wb") as f:
+        f.write(b"".join(blobs))
+
+
+def read_container(dirpath: str):
+    """(arrays {set: {name: float64 ndarray}}, manifest) with the reference's
+    integrity checks (q/nets.py:348-377)."""
+    try:
+        with open(os.path.join(dirpath, "manifest.json")) as f:
+            manifest = json.load(f)
+    except (OSError, json.JSONDecodeError) as e:
+        raise IntegrityError(f"unreadable manifest: {e}")
+    if manifest.get("format_version") != CONTAINER_VERSION:
+        raise IntegrityError(f"unsupported container version {manifest.get('format_version')}")
+    try:
+        blob = np.fromfile(os.path.join(dirpath, "weights.bin"), dtype="<f4")
+    except OSError as e:
+        raise IntegrityError(f"unreadable weight blob: {e}")
+    if blob.size != manifest["total_floats"]:
+        raise IntegrityError(f"weight blob holds {blob.size} floats, manifest expects {manifest['total_floats']}")
+    sets: dict = {}
+    for layer in manifest["layers"]:
+        n = int(np.prod(layer["shape"])) if layer["shape"] else 1
+        vals = blob[layer["offset"]:layer["offset"] + n]
+        if vals.size != n:
+            raise IntegrityError(f"layer '{layer['name']}' truncated")
+        sets.setdefault(layer["set"], {})[layer["name"]] = vals.astype(np.float64).reshape(layer["shape"])
+    return sets, manifest
+
+
+def load_into(module: torch.nn.Module, arrays: dict) -> None:
+    """Copy one container set into a PolicyNet / ValueNet (names and shapes
+    must match the module's architecture)."""
+    want = ref_params(module)
+    missing = set(want) - set(arrays)
+    extra = set(arrays) - set(want)
+    if missing or extra:
+        raise IntegrityError(f"container/architecture mismatch: missing {sorted(missing)}, extra {sorted(extra)}")
+    with torch.no_grad():
+        for name, (p, _tag) in want.items():
+            a = torch.as_tensor(arrays[name])
+            if tuple(a.shape) != tuple(p.shape):
+                raise IntegrityError(f"layer '{name}': shape {tuple(a.shape)} != {tuple(p.shape)}")
+            p.copy_(a.to(p.dtype))

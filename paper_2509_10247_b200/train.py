@@ -18,10 +18,11 @@ from __future__ import annotations
 import time
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
-LOG_SIGMA_MIN = -5.0  # q/nets.py:22
+from paper_2509_10247_b200.nets import LOG_SIGMA_MIN, PolicyArch, PolicyNet, ValueNet  # noqa: F401
 
 
 @dataclass
@@ -40,66 +41,22 @@ class LearnerOptions:
     recurrent: bool = True
     hidden: int = 64
     mlp: tuple = (128, 128)
+    conv_feat: int = 32
     log_sigma_init: float = -1.2
     log_sigma_max: float = 2.0
+    # PPO specifics (q/learners.py:52-59)
+    ppo_horizon: int = 32
+    clip_eps: float = 0.2
+    ppo_epochs: int = 4
+    ppo_minibatch: int = 512
+    entropy_coef: float = 1e-3
+    value_coef: float = 0.5
+    reward_norm: bool = True
     seed: int = 0
     # matmul precision of the policy/critic on CUDA: "bf16" runs them on the
     # tensor cores under torch.autocast (fp32 master weights, fp32 sim
     # gradients); "fp32" keeps the reference's all-fp32 arithmetic (SIMT GEMMs)
     net_dtype: str = "bf16"
-
-
-class PolicyNet(torch.nn.Module):
-    """GRU-64 + tanh MLP trunk + (mu, log_sigma) heads (q/nets.py:183-256)."""
-
-    def __init__(self, proprio_dim, action_dim, input_scale=None, recurrent=True, hidden=64, mlp=(128, 128),
-                 log_sigma_init=-1.2, log_sigma_max=2.0):
-        super().__init__()
-        scale = torch.ones(proprio_dim) if input_scale is None else torch.as_tensor(input_scale, dtype=torch.float32)
-        self.register_buffer("input_scale", scale)
-        self.gru = torch.nn.GRUCell(proprio_dim, hidden) if recurrent else None
-        sizes = [hidden if recurrent else proprio_dim] + list(mlp)
-        self.trunk = torch.nn.ModuleList(torch.nn.Linear(a, b) for a, b in zip(sizes[:-1], sizes[1:]))
-        self.mu = torch.nn.Linear(mlp[-1], action_dim)
-        self.sig = torch.nn.Linear(mlp[-1], action_dim)
-        for head in (self.mu, self.sig):
-            torch.nn.init.normal_(head.weight, std=0.01 * (2.0 / (mlp[-1] + action_dim)) ** 0.5)
-            torch.nn.init.zeros_(head.bias)
-        torch.nn.init.constant_(self.sig.bias, log_sigma_init)
-        self.hidden = hidden
-        self.log_sigma_max = log_sigma_max
-
-    def initial_hidden(self, batch, device):
-        return torch.zeros(batch, self.hidden, device=device) if self.gru is not None else None
-
-    def forward(self, proprio, h=None):
-        x = proprio * self.input_scale
-        if self.gru is not None:
-            h = self.gru(x, h).float()
-            x = h
-        for layer in self.trunk:
-            x = torch.tanh(layer(x))
-        mu, ls = self.mu(x).float(), self.sig(x).float()
-        return mu, torch.clamp(ls, LOG_SIGMA_MIN, self.log_sigma_max), h
-
-
-class ValueNet(torch.nn.Module):
-    """Privileged-state MLP critic (q/nets.py:259-274)."""
-
-    def __init__(self, n_in, hidden=(128, 128), input_scale=None):
-        super().__init__()
-        scale = torch.ones(n_in) if input_scale is None else torch.as_tensor(input_scale, dtype=torch.float32)
-        self.register_buffer("input_scale", scale)
-        sizes = [n_in] + list(hidden) + [1]
-        self.layers = torch.nn.ModuleList(torch.nn.Linear(a, b) for a, b in zip(sizes[:-1], sizes[1:]))
-
-    def forward(self, x):
-        x = x * self.input_scale
-        for i, layer in enumerate(self.layers):
-            x = layer(x)
-            if i < len(self.layers) - 1:
-                x = torch.tanh(x)
-        return x[..., 0].float()
 
 
 def td_lambda_targets(r, values, bootstrap, done, gamma, lam):
@@ -113,6 +70,73 @@ def td_lambda_targets(r, values, bootstrap, done, gamma, lam):
         G[t] = r[t] + gamma * cont[t] * ((1.0 - lam) * v_next + lam * nxt)
         nxt = G[t]
     return G
+
+
+def gae_advantages(r, values, bootstrap, done, gamma, lam):
+    """Standard GAE with cuts at done (q/learners.py:116-127): (adv, targets)."""
+    T = r.shape[0]
+    cont = 1.0 - done.to(r.dtype)
+    adv = torch.empty_like(r)
+    acc = torch.zeros_like(bootstrap)
+    for t in reversed(range(T)):
+        v_next = values[t + 1] if t + 1 < T else bootstrap
+        delta = r[t] + gamma * cont[t] * v_next - values[t]
+        acc = delta + gamma * lam * cont[t] * acc
+        adv[t] = acc
+    return adv, adv + values
+
+
+def normalize(adv, eps: float = 1e-8):
+    """q/learners.py:130-131 (population std, as numpy's)."""
+    return (adv - adv.mean()) / (adv.std(unbiased=False) + eps)
+
+
+class ReturnScaler:
+    """PPO reward scaling by a running estimate of the discounted-return std
+    (q/learners.py:345-366): per step, the return trace of every env is merged
+    into running moments (parallel Welford), traces reset at done; the window's
+    rewards are divided by the std after the window.  The moments live on the
+    device; ``group`` merges every rank's batch (the global batch of the
+    sharded envs), which with one rank is exactly the reference's update."""
+
+    def __init__(self, n_envs, gamma, device, group=None):
+        self.gamma = gamma
+        self.trace = torch.zeros(n_envs, dtype=torch.float64, device=device)
+        # count, mean, m2 -- the reference's initial state
+        self.mom = torch.tensor([1e-4, 0.0, 1.0], dtype=torch.float64, device=device)
+        self.group = group
+
+    def __call__(self, rewards, dones):
+        T = rewards.shape[0]
+        distributed = dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+        for t in range(T):
+            self.trace = rewards[t].double() + self.gamma * self.trace
+            b = self.trace
+            n_b = torch.tensor(float(b.numel()), dtype=torch.float64, device=b.device)
+            s1, s2 = b.sum(), (b * b).sum()
+            if distributed:
+                st = torch.stack([n_b, s1, s2])
+                dist.all_reduce(st, group=self.group)
+                n_b, s1, s2 = st[0], st[1], st[2]
+            mean_b = s1 / n_b
+            var_b = torch.clamp(s2 / n_b - mean_b * mean_b, min=0.0) if distributed else b.var(unbiased=False)
+            cnt, mean, m2 = self.mom[0], self.mom[1], self.mom[2]
+            delta = mean_b - mean
+            tot = cnt + n_b
+            self.mom = torch.stack([tot, mean + delta * n_b / tot, m2 + var_b * n_b + delta * delta * cnt * n_b / tot])
+            self.trace = torch.where(dones[t], torch.zeros_like(self.trace), self.trace)
+        std = torch.sqrt(self.mom[2] / self.mom[0])
+        return (rewards.double() / torch.clamp(std, min=1e-8)).to(rewards.dtype)
+
+
+def ppo_log_prob(mu, log_sigma, a_raw, half):
+    """Gaussian log-density of the raw action with the tanh-squash correction
+    (q/learners.py:368-385): log|da/draw| = log(half) + 2 (log 2 - x - softplus(-2x))."""
+    z = (a_raw - mu) / torch.exp(log_sigma)
+    A = mu.shape[-1]
+    base = -(0.5 * (z * z).sum(-1) + log_sigma.sum(-1) + 0.5 * np.log(2 * np.pi) * A)
+    corr = 2.0 * (np.log(2.0) - a_raw - torch.nn.functional.softplus(-2.0 * a_raw)) + torch.log(half)
+    return base - corr.sum(-1)
 
 
 def allreduce_mean_(params, group=None):
@@ -132,6 +156,22 @@ def allreduce_mean_(params, group=None):
         off += n
 
 
+def make_nets(env, opts, critic: bool):
+    """Policy (and critic) with the reference's architecture, parameter names
+    and initial weights for ``opts.seed`` (q/learners.py:141-169)."""
+    rng = np.random.default_rng([opts.seed & 0x7FFFFFFF, 0x11])
+    spec = env.obs_spec()
+    recurrent = opts.recurrent and opts.algo != "ppo"  # recurrent PPO is out of the reference's scope (:335-337)
+    policy = PolicyNet(PolicyArch(proprio_dim=spec["proprio_dim"], action_dim=spec["action_dim"],
+                                  visual=spec["visual"], recurrent=recurrent, hidden=opts.hidden,
+                                  mlp=tuple(opts.mlp), conv_feat=opts.conv_feat,
+                                  log_sigma_init=opts.log_sigma_init, log_sigma_max=opts.log_sigma_max,
+                                  input_scale=env.proprio_scale()), rng)
+    value = ValueNet(env.privileged_dim(), rng, hidden=tuple(opts.mlp),
+                     input_scale=env.privileged_scale()) if critic else None
+    return policy, value
+
+
 def shard_envs(n_total: int, rank: int, world: int):
     """Contiguous global env range of ``rank`` (sharding is by global env id)."""
     per = (n_total + world - 1) // world
@@ -145,14 +185,14 @@ class ShortHorizonTrainer:
     def __init__(self, env, opts: LearnerOptions = LearnerOptions(), group=None):
         self.env, self.opts, self.group = env, opts, group
         dev = env.device
-        g = torch.Generator(device="cpu").manual_seed(opts.seed)
-        torch.manual_seed(opts.seed)  # identical initial weights on every rank
-        self.policy = PolicyNet(env.proprio_dim, env.action_dim, env.proprio_scale(), opts.recurrent, opts.hidden,
-                                opts.mlp, opts.log_sigma_init, opts.log_sigma_max).to(dev)
+        # the reference's init stream and order (q/learners.py:141-169): the
+        # same seed gives the reference's initial weights, on every rank
+        self.policy, self.value = make_nets(env, opts, critic=opts.algo in ("shac", "sha2c", "ppo"))
+        self.policy.to(dev)
         self.actor_opt = torch.optim.Adam(self.policy.parameters(), lr=opts.actor_lr)
-        self.needs_critic = opts.algo in ("shac", "sha2c")
+        self.needs_critic = self.value is not None
         if self.needs_critic:
-            self.value = ValueNet(env.privileged_dim(), opts.mlp, env.privileged_scale()).to(dev)
+            self.value.to(dev)
             self.critic_opt = torch.optim.Adam(self.value.parameters(), lr=opts.critic_lr)
         self.hidden = self.policy.initial_hidden(env.N, dev)
         self.update_count = 0
@@ -180,7 +220,7 @@ class ShortHorizonTrainer:
             if record_privileged:
                 priv.append(env.privileged_state())
             with self._nets():
-                mu, log_sigma, h = self.policy(obs.proprio, h)
+                mu, log_sigma, h = self.policy(obs.proprio, obs.visual, h)
             a = mu
             if opts.explore:
                 eps = torch.randn(mu.shape, generator=self._gen, device=mu.device)
@@ -254,3 +294,130 @@ class ShortHorizonTrainer:
             self.critic_opt.step()
             loss_val = float(loss.detach())
         return loss_val
+
+
+class PPOTrainer:
+    """Clipped surrogate + GAE on the RL reward scalar (q/learners.py:327-487).
+
+    Rollouts run the forward-only env step (no autograd graph: one fused
+    kernel per step); the policy is the reference's non-recurrent MLP (with its
+    conv / LiDAR encoder when the task has a visual observation).  Rewards are
+    scaled by the running discounted-return std; advantages are GAE with cuts
+    at done, normalised over the window.  Each epoch visits the window's rows
+    in a fresh permutation, in minibatches; the actor and critic each take one
+    Adam step per minibatch (global-norm clip ``grad_clip``), their gradients
+    averaged across ranks first (NCCL; gloo in the CPU tests).  Deviation: the
+    exploration noise and the permutations come from torch's Philox
+    generators, not numpy's (values are not pinned by the reference's tests,
+    only their statistics and determinism)."""
+
+    def __init__(self, env, opts: LearnerOptions, group=None):
+        self.env, self.opts, self.group = env, opts, group
+        dev = env.device
+        self.policy, self.value = make_nets(env, opts, critic=True)
+        self.policy.to(dev)
+        self.value.to(dev)
+        self.actor_opt = torch.optim.Adam(self.policy.parameters(), lr=opts.actor_lr)
+        self.critic_opt = torch.optim.Adam(self.value.parameters(), lr=opts.critic_lr)
+        self.scaler = ReturnScaler(env.N, opts.gamma, dev, group)
+        self.update_count = 0
+        self._gen = torch.Generator(device=dev)
+        self._gen.manual_seed(opts.seed * 1_000_003 + env.env_offset + 0xB)
+        self._amp = opts.net_dtype == "bf16" and dev.type == "cuda"
+
+    def _nets(self):
+        return torch.autocast("cuda", dtype=torch.bfloat16, enabled=self._amp)
+
+    def _half(self):
+        env = self.env
+        half = (torch.as_tensor(env.action_hi, dtype=torch.float32, device=env.device) -
+                torch.as_tensor(env.action_lo, dtype=torch.float32, device=env.device)) / 2.0
+        return half.expand(env.N, env.action_dim) if half.dim() == 1 else half
+
+    def collect(self):
+        env, opts = self.env, self.opts
+        T = opts.ppo_horizon
+        half = self._half()
+        env.detach_states()
+        obs = env.observe()
+        pro, vis, acts, logps, vals, rews, dones, priv = [], [], [], [], [], [], [], []
+        with torch.no_grad():
+            for t in range(T):
+                p = env.privileged_state()
+                with self._nets():
+                    mu, log_sigma, _ = self.policy(obs.proprio, obs.visual, None)
+                    v = self.value(p)
+                eps = torch.randn(mu.shape, generator=self._gen, device=mu.device)
+                a = mu + torch.exp(log_sigma) * eps
+                logps.append(ppo_log_prob(mu, log_sigma, a, half))
+                pro.append(obs.proprio.detach())
+                if obs.visual is not None:
+                    vis.append(obs.visual)
+                priv.append(p)
+                vals.append(v.float())
+                out = env.step(a)
+                acts.append(a)
+                rews.append(out.r_rl.float())
+                dones.append(out.done)
+                obs = out.obs
+            with self._nets():
+                boot = self.value(env.privileged_state()).float()
+        st = lambda xs: torch.stack(xs) if xs else None  # noqa: E731
+        return st(pro), st(vis), st(acts), st(logps), st(vals), st(rews), st(dones), st(priv), boot, half
+
+    def update(self) -> dict:
+        env, opts = self.env, self.opts
+        t0 = time.perf_counter()
+        pro, vis, acts, logps, vals, rews, dones, priv, boot, half = self.collect()
+        T, N = rews.shape
+        scaled = self.scaler(rews, dones) if opts.reward_norm else rews
+        adv, rets = gae_advantages(scaled, vals, boot, dones, opts.gamma, opts.td_lambda)
+        adv_n = normalize(adv)
+        n_rows = T * N
+        flat = lambda x: x.reshape(n_rows, *x.shape[2:]) if x is not None else None  # noqa: E731
+        pro_f, vis_f, a_f, old_f, adv_f, ret_f, priv_f = (flat(pro), flat(vis), flat(acts), logps.reshape(-1),
+                                                           adv_n.reshape(-1), rets.reshape(-1), flat(priv))
+        half_f = half.repeat(T, 1)
+        mb = min(opts.ppo_minibatch, n_rows)
+        pi_loss = v_loss = ent = torch.zeros((), device=env.device)
+        pgen = torch.Generator(device=env.device)
+        for epoch in range(opts.ppo_epochs):
+            pgen.manual_seed(((opts.seed & 0xFFFFFFFF) << 20) ^ (self.update_count << 8) ^ epoch)
+            order = torch.randperm(n_rows, generator=pgen, device=env.device)
+            for s0 in range(0, n_rows, mb):
+                rows = order[s0:s0 + mb]
+                with self._nets():
+                    mu, log_sigma, _ = self.policy(pro_f[rows], vis_f[rows] if vis_f is not None else None, None)
+                logp = ppo_log_prob(mu, log_sigma, a_f[rows], half_f[rows])
+                ratio = torch.exp(logp - old_f[rows])
+                r_clip = torch.clamp(ratio, 1.0 - opts.clip_eps, 1.0 + opts.clip_eps)
+                adv_rows = adv_f[rows]
+                surr = torch.minimum(ratio * adv_rows, r_clip * adv_rows).mean()
+                entropy = (log_sigma.sum(-1) + 0.5 * mu.shape[-1] * np.log(2 * np.pi * np.e)).mean()
+                actor_loss = -(surr + opts.entropy_coef * entropy)
+                self.actor_opt.zero_grad(set_to_none=True)
+                actor_loss.backward()
+                allreduce_mean_(list(self.policy.parameters()), self.group)
+                torch.nn.utils.clip_grad_norm_(self.policy.parameters(), opts.grad_clip)
+                self.actor_opt.step()
+                with self._nets():
+                    pred = self.value(priv_f[rows]).float()
+                value_loss = ((pred - ret_f[rows]) ** 2).mean()
+                self.critic_opt.zero_grad(set_to_none=True)
+                (value_loss * opts.value_coef).backward()
+                allreduce_mean_(list(self.value.parameters()), self.group)
+                torch.nn.utils.clip_grad_norm_(self.value.parameters(), opts.grad_clip)
+                self.critic_opt.step()
+                pi_loss, v_loss, ent = actor_loss.detach(), value_loss.detach(), entropy.detach()
+        self.update_count += 1
+        return {"loss": float(pi_loss), "critic_loss": float(v_loss), "entropy": float(ent),
+                "reward_mean": float(rews.mean()), "steps_per_sec": T * N / (time.perf_counter() - t0)}
+
+
+def make_learner(env, opts: LearnerOptions, group=None):
+    """q/learners.py:66-71."""
+    if opts.algo in ("bptt", "shac", "sha2c"):
+        return ShortHorizonTrainer(env, opts, group)
+    if opts.algo == "ppo":
+        return PPOTrainer(env, opts, group)
+    raise ValueError(f"unknown algorithm '{opts.algo}'; choose from ('bptt', 'shac', 'sha2c', 'ppo')")

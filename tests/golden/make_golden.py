@@ -411,8 +411,85 @@ def gen_learners():
     save("learners", **rec)
 
 
+def gen_nets_ppo():
+    """Networks (q/nets.py:85-274) through the weight container (:316-377), and
+    the PPO pieces (q/learners.py:116-131, 345-385): GAE with cuts, advantage
+    normalisation, running return-std reward scaling, tanh-squashed log-prob."""
+    from quadsim import learners as ln
+    from quadsim import nets
+
+    rec = {}
+    cdir = os.path.join(OUT, "nets_container")
+    rng = np.random.default_rng([5 & 0x7FFFFFFF, 0x11])  # the learners' init stream
+    arch_d = nets.PolicyArch(proprio_dim=9, action_dim=3,
+                             visual={"kind": "depth", "height": 12, "width": 16, "max_range": 10.0},
+                             recurrent=True, hidden=16, mlp=(32, 32), conv_feat=8,
+                             input_scale=tuple(np.linspace(0.2, 1.0, 9)))
+    pol_d = nets.PolicyNet(arch_d, rng)
+    val = nets.ValueNet(13, rng, hidden=(32, 32), input_scale=tuple(np.linspace(0.5, 1.5, 13)))
+    for k, v in pol_d.ps.arrays.items():
+        rec["init_depth/" + k] = v.copy()
+    for k, v in val.ps.arrays.items():
+        rec["init_value/" + k] = v.copy()
+    rng2 = np.random.default_rng(77)
+    for ps in (pol_d.ps, val.ps):  # trained-looking weights (biases nonzero), then f32
+        for k in ps.arrays:
+            ps.arrays[k] = ps.arrays[k] + 0.1 * rng2.normal(size=ps.arrays[k].shape)
+        ps.round_to_f32()
+    arch_l = nets.PolicyArch(proprio_dim=12, action_dim=4, visual={"kind": "lidar", "rays": 24, "max_range": 20.0},
+                             recurrent=False, hidden=16, mlp=(32, 32), conv_feat=8)
+    pol_l = nets.PolicyNet(arch_l, np.random.default_rng(9))
+    for k in pol_l.ps.arrays:
+        pol_l.ps.arrays[k] = pol_l.ps.arrays[k] + 0.1 * rng2.normal(size=pol_l.ps.arrays[k].shape)
+    pol_l.ps.round_to_f32()
+    nets.save_container(cdir, {"policy": pol_d.ps, "value": val.ps, "policy_lidar": pol_l.ps},
+                        {"note": "tests/golden/make_golden.py gen_nets_ppo"})
+    B = 5
+    pro = rng2.normal(size=(B, 9))
+    img = rng2.uniform(0.0, 12.0, size=(B, 12, 16))
+    h0 = rng2.normal(size=(B, 16)) * 0.5
+    mu, ls, h1 = pol_d.forward(pol_d.ps.bind(None), Var(pro), img, Var(h0))
+    rec.update({"d_pro": pro, "d_img": img, "d_h0": h0, "d_mu": mu.value, "d_ls": ls.value, "d_h1": h1.value})
+    pro_l = rng2.normal(size=(B, 12))
+    scan = rng2.uniform(0.0, 25.0, size=(B, 24))
+    mu, ls, _ = pol_l.forward(pol_l.ps.bind(None), Var(pro_l), scan, None)
+    rec.update({"l_pro": pro_l, "l_scan": scan, "l_mu": mu.value, "l_ls": ls.value})
+    priv = rng2.normal(size=(B, 13))
+    rec.update({"v_in": priv, "v_out": val.forward(val.ps.bind(None), priv).value})
+    # PPO pieces
+    T, N = 12, 16
+    r = rng2.normal(size=(T, N))
+    values = rng2.normal(size=(T, N))
+    boot = rng2.normal(size=N)
+    done = rng2.uniform(size=(T, N)) < 0.15
+    adv, rets = ln.gae_advantages(r, values, boot, done, 0.99, 0.95)
+    rec.update({"g_r": r, "g_values": values, "g_boot": boot, "g_done": done, "g_adv": adv, "g_rets": rets,
+                "g_norm": ln.normalize(adv)})
+
+    class _Stub:  # just the running return-std state of a PPO learner
+        pass
+
+    st = _Stub()
+    st.opts = ln.LearnerOptions(algo="ppo", gamma=0.99)
+    st._ret_trace, st._ret_count, st._ret_mean, st._ret_m2 = np.zeros(N), 1e-4, 0.0, 1.0
+    for u in range(3):
+        rw = rng2.normal(size=(T, N)) * (1.0 + u)
+        dn = rng2.uniform(size=(T, N)) < 0.1
+        rec[f"s_r{u}"], rec[f"s_done{u}"] = rw, dn
+        rec[f"s_scaled{u}"] = ln.PPO._scale_rewards(st, rw, dn)
+    mu = rng2.normal(size=(N, 3))
+    logs = rng2.normal(size=(N, 3)) * 0.3 - 1.0
+    a = mu + np.exp(logs) * rng2.normal(size=(N, 3))
+    half = np.abs(rng2.normal(size=(N, 3))) + 1.0
+    rec.update({"lp_mu": mu, "lp_logs": logs, "lp_a": a, "lp_half": half,
+                "lp": ln.PPO._log_prob(st, Var(mu), Var(logs), Var(a), half).value})
+    save("nets_ppo", **rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners"]
+    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners", "nets_ppo"]
+    if "nets_ppo" in which:
+        gen_nets_ppo()
     if "learners" in which:
         gen_learners()
     if "dynamics" in which:

@@ -68,3 +68,62 @@ def test_privileged_features_match_oracle():
     env.state = env.model.init_state(env.state.p.detach().requires_grad_(True), env.state.v.detach())
     v = env.privileged_var()
     v[:, 9].sum().backward()
+
+
+def test_ppo_ratio_starts_at_one():
+    """lr = 0 and no entropy bonus: the normalised-advantage clipped surrogate
+    is ~0 (pkg/tests/test_learners.py:224-233)."""
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.train import LearnerOptions, make_learner
+
+    env = qs.make_task(qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=8), strict=False)
+    env.reset(seed=37)
+    lr = make_learner(env, LearnerOptions(algo="ppo", ppo_horizon=8, ppo_epochs=1, entropy_coef=0.0,
+                                          net_dtype="fp32"))
+    for g in lr.actor_opt.param_groups + lr.critic_opt.param_groups:
+        g["lr"] = 0.0
+    m = lr.update()
+    assert abs(m["loss"]) < 1e-6
+
+
+def test_ppo_improves_reward_on_position_task():
+    """pkg/tests/test_learners.py:236-252, on the kernel env."""
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.train import LearnerOptions, make_learner
+
+    env = qs.make_task(qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=64, episode_len=48,
+                                     goal_dist=5.0), strict=False)
+    env.reset(seed=41)
+    lr = make_learner(env, LearnerOptions(algo="ppo", ppo_horizon=32, ppo_epochs=10, ppo_minibatch=512,
+                                          gamma=0.95, td_lambda=0.9, actor_lr=3e-4, critic_lr=1e-3,
+                                          entropy_coef=1e-3, log_sigma_init=-0.5, log_sigma_max=0.0,
+                                          mlp=(64, 64), seed=41))
+    early = np.mean([lr.update()["reward_mean"] for _ in range(5)])
+    for _ in range(60):
+        lr.update()
+    late = np.mean([lr.update()["reward_mean"] for _ in range(5)])
+    assert late > early
+    env.check_errors()
+
+
+@pytest.mark.parametrize("task", ["avoidance", "avoidance_lidar"])
+def test_ppo_with_visual_encoders(task):
+    """The conv (depth) and linear (LiDAR) encoders train end to end on the
+    rendered observations."""
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.train import LearnerOptions, make_learner
+
+    kw = dict(task="avoidance", dynamics="pm_continuous", n_envs=64, density=0.3)
+    if task == "avoidance":
+        kw["sensor"] = "depth"
+    else:
+        kw["sensor"] = "lidar"
+    env = qs.make_task(qs.TaskConfig(**kw), strict=False)
+    env.reset(seed=5)
+    lr = make_learner(env, LearnerOptions(algo="ppo", ppo_horizon=8, ppo_epochs=2, ppo_minibatch=256, seed=3))
+    before = {k: p.detach().clone() for k, p in lr.policy.named_parameters()}
+    for _ in range(2):
+        m = lr.update()
+        assert np.isfinite(m["loss"]) and np.isfinite(m["critic_loss"])
+    enc = [k for k in before if k.startswith("enc.")]
+    assert enc and all(not torch.equal(before[k], dict(lr.policy.named_parameters())[k]) for k in enc)

@@ -66,3 +66,39 @@ def test_gradient_allreduce_two_ranks_gloo():
     assert not np.allclose(res[0][0][0], res[1][0][0])
     for a, b in zip(res[0][1], res[1][1]):
         assert np.array_equal(a, b)
+
+
+def _scaler_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2509_10247_b200.train import ReturnScaler
+
+    z = load("nets_ppo")
+    N = z["s_r0"].shape[1]
+    lo, hi = rank * N // world, (rank + 1) * N // world  # this rank's env shard
+    sc = ReturnScaler(hi - lo, 0.99, torch.device("cpu"))
+    outs = [sc(torch.as_tensor(z[f"s_r{u}"][:, lo:hi]), torch.as_tensor(z[f"s_done{u}"][:, lo:hi])).numpy()
+            for u in range(3)]
+    q.put((rank, lo, hi, outs))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_return_scaler_sharded_two_ranks_gloo():
+    """PPO reward scaling over env shards on 2 ranks equals the reference's
+    single-process scaling of the whole batch (moments merged by all-reduce)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + (os.getpid() + 7) % 1000
+    procs = [ctx.Process(target=_scaler_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    z = load("nets_ppo")
+    for rank, lo, hi, outs in res:
+        for u in range(3):
+            np.testing.assert_allclose(outs[u], z[f"s_scaled{u}"][:, lo:hi], rtol=1e-10, atol=1e-12)
