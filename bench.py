@@ -650,6 +650,9 @@ def run_ours(a):
         depth["frac_uncull_equiv"] = depth["tflops_uncull_equiv"] / (fp32_peak * world)
         depth["frac_culled_equiv"] = depth["tflops_culled_equiv"] / (fp32_peak * world)
         depth["spawn_facing"]["frac_culled_equiv"] = depth["spawn_facing"]["tflops_culled_equiv"] / (fp32_peak * world)
+        depth["frac_note"] = ("flops are the reference algorithm's (SURVEY §8d: per ray, every solid its fov_cull "
+                              "keeps); the per-tile cone/sector cull tests far fewer solids per ray, so a "
+                              "fraction above 1 means less arithmetic than that algorithm, not more than peak")
 
     c1 = bench_c1(dev) if rank == 0 and not a.no_depth else None
     c4 = bench_c4(dev) if rank == 0 and not a.no_depth else None

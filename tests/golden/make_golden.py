@@ -484,6 +484,27 @@ def gen_nets_ppo():
     rec.update({"lp_mu": mu, "lp_logs": logs, "lp_a": a, "lp_half": half,
                 "lp": ln.PPO._log_prob(st, Var(mu), Var(logs), Var(a), half).value})
     save("nets_ppo", **rec)
+    # run artefacts (q/io.py): a trajectory dump and a metrics CSV of the same data
+    from quadsim import io as qio
+
+    N, S = 3, 2
+    tw = qio.TrajectoryWriter(os.path.join(OUT, "trajectory.jsonl"), env_limit=2)
+    io_rec = {}
+    for step in range(S):
+        states = {"p": rng2.normal(size=(N, 3)), "v": rng2.normal(size=(N, 3))}
+        acts = rng2.normal(size=(N, 3))
+        rc, rg = rng2.normal(size=N), np.array([0.0, 1.0, -1.0])
+        term, trunc = np.array([0, 1, 2], dtype=np.int8), np.array([False, True, False])
+        tw.write_step(step, states, acts, rc, rg, term, trunc)
+        io_rec.update({f"t{step}_p": states["p"], f"t{step}_v": states["v"], f"t{step}_a": acts,
+                       f"t{step}_rc": rc, f"t{step}_rg": rg, f"t{step}_term": term, f"t{step}_trunc": trunc})
+    tw.close()
+    mw = qio.MetricsWriter(os.path.join(OUT, "metrics.csv"))
+    for u in range(3):
+        mw.write({"update": u, "loss": float(rng2.normal()), "steps_per_sec": float(rng2.uniform() * 1e6)})
+        io_rec[f"m{u}"] = np.array([u])
+    mw.close()
+    save("io_inputs", **io_rec)
 
 
 if __name__ == "__main__":
