@@ -341,6 +341,38 @@ def bench_depth(dev, rank, world=1, frames=20):
             "lidar_360x16": {"rays_per_s": E * lidar.n_rays / (ms_lidar * 1e-3), "ms_per_frame": ms_lidar}}
 
 
+def bench_c3_env(dev, steps=20):
+    """C3 as a closed-loop env: the avoidance task (32-solid courses, SDF
+    penalty, collisions) with the 64x48 depth camera rendered every step,
+    16,384 envs, through the public ``FlightTask.step`` (fused step kernel +
+    tiled ray caster per step), forward only as a policy rollout sees it."""
+    import torch
+
+    import paper_2509_10247_b200 as qs
+
+    E = 16384
+    cfg = qs.TaskConfig(task="avoidance", dynamics="pm_continuous", n_envs=E, sensor="depth", depth_width=64,
+                        depth_height=48, density=32 / 48.0, episode_len=128)
+    env = qs.make_task(cfg, device=dev, strict=False)
+    env.reset(seed=2)
+    g = torch.Generator(device="cpu").manual_seed(21)
+    acts = (torch.randn(steps, E, env.action_dim, generator=g) * 0.3).to(dev)
+    with torch.no_grad():
+        for t in range(3):
+            env.step(acts[t])
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(steps):
+            out = env.step(acts[t])
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    assert out.obs.visual is not None and tuple(out.obs.visual.shape) == (E, 48, 64)
+    return {"ms_per_env_step": ms, "env_steps_per_s": E / (ms * 1e-3), "rays_per_s": E * 3072 / (ms * 1e-3),
+            "n_envs": E, "api": "FlightTask.step (no grad): fused step kernel + depth render per step"}
+
+
 def measure_fp32_peak(dev):
     """FFMA and FFMA2 throughput on this GPU (qs_probe_fp32): the measured FP32
     denominator BASELINE.md §3 asks for.  Full occupancy (8 x 256 threads per
@@ -656,6 +688,7 @@ def run_ours(a):
 
     c1 = bench_c1(dev) if rank == 0 and not a.no_depth else None
     c4 = bench_c4(dev) if rank == 0 and not a.no_depth else None
+    c3_env = bench_c3_env(dev) if rank == 0 and not a.no_depth else None
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -694,6 +727,7 @@ def run_ours(a):
         "depth": depth,
         "c1_latency": c1,
         "c4": c4,
+        "c3_env": c3_env,
         "loss": loss,
     }
     print(json.dumps(line))
