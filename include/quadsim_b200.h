@@ -236,6 +236,14 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
                      int32_t pos_stride, const float* cam_cs, const float* tile_dirs,
                      const float* tile_cones, int32_t n_tiles, int32_t tile_width, float* out,
                      uint8_t* hit, void* stream);
+/* The depth VJP without dT_dO in memory: recasts the tiled rays, finds each
+ * ray's hit surface and accumulates g_pos[row] += sum_r g_depth[row,r] *
+ * (-n/(n.d)) (rays clamped at max_range contribute 0), one atomic per row.
+ * Same tile tables and conventions as qs_raycast_tiled. */
+int qs_raycast_tiled_vjp(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
+                         int32_t pos_stride, const float* cam_cs, const float* tile_dirs,
+                         const float* tile_cones, int32_t n_tiles, int32_t tile_width, const float* g_depth,
+                         float* g_pos, int32_t gpos_stride, void* stream);
 /* d loss / d pos = sum_r g_depth[r] * dT_dO[r]  (N,3) accumulate into g_pos (N,4 stride pos_stride). */
 int qs_raycast_vjp(int32_t n_rows, int32_t n_rays, const float* g_depth, const float* dT_dO,
                    float* g_pos, int32_t pos_stride, void* stream);

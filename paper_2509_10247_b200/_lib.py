@@ -115,6 +115,7 @@ _SIGS = {
     "qs_raycast": ([P(QsRayCfg), P(QsScene), i32, vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "qs_raycast_vjp": ([i32, i32, vp, vp, vp, i32, vp], i32),
     "qs_raycast_tiled": ([P(QsRayCfg), P(QsScene), i32, vp, i32, vp, vp, vp, i32, i32, vp, vp, vp], i32),
+    "qs_raycast_tiled_vjp": ([P(QsRayCfg), P(QsScene), i32, vp, i32, vp, vp, vp, i32, i32, vp, vp, i32, vp], i32),
     "qs_sdf": ([P(QsScene), i32, i32, vp, vp, vp, vp], i32),
     "qs_imu_read": ([i32, vp, vp, vp, vp, f32, f32, f32, f32, f32, u64, i64, vp, vp, vp, vp], i32),
     "qs_dyn_step_fwd": ([i32, i32, vp, vp, vp, P(QsTaskCfg), vp, vp, vp], i32),

@@ -487,11 +487,18 @@ constexpr int TILED_BLOCK = QS_TILED_BLOCK;
 // RPL rays per lane: a tile holds 32 * RPL rays (lane j owns rays j, j + 32,
 // ...), so the tile's cone test, ballot, candidate loop and obstacle-record
 // loads are shared by RPL rays, and each candidate runs RPL independent tests.
-template <int KIND, bool EXT, int RPL>
+//
+// GRAD: the depth VJP by recasting (no per-ray dT/dO in HBM).  The same tiles
+// and culls, but each lane tracks the argmin primitive of its rays with the
+// untiled kernel's float tests (same cores, same first-wins tie rule within the
+// kind order), then accumulates g_depth[ray] * dt/do = -n/(n.d) of the hit
+// surface; one warp reduction per row adds the sum into g_pos.
+template <int KIND, bool EXT, int RPL, bool GRAD = false>
 __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
     const qs_ray_cfg rc, const qs_scene sc, int n_rows, const float* __restrict__ pos, int pos_stride,
     const float* __restrict__ cam_cs, const float* __restrict__ tile_dirs, const float* __restrict__ tile_cones,
-    int n_tiles, int tiles_per_cta, float* __restrict__ out, uint8_t* __restrict__ hitm) {
+    int n_tiles, int tiles_per_cta, float* __restrict__ out, uint8_t* __restrict__ hitm,
+    const float* __restrict__ g_depth = nullptr, float* __restrict__ g_pos = nullptr, int gpos_stride = 4) {
   extern __shared__ float4 sm[];
   __shared__ int cnt[3];
   const long row = blockIdx.y;
@@ -594,8 +601,10 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
   const bool ground = sv.ground;
   const float gdz = sv.gz - o.z;
   const int t0 = blockIdx.x * tiles_per_cta, t1 = min(n_tiles, t0 + tiles_per_cta);
-  float* out_row = out + row * rc.n_rays;
-  uint8_t* hitm_row = hitm ? hitm + row * rc.n_rays : nullptr;
+  float* out_row = GRAD ? nullptr : out + row * rc.n_rays;
+  uint8_t* hitm_row = hitm && !GRAD ? hitm + row * rc.n_rays : nullptr;
+  const float* g_row = GRAD ? g_depth + row * rc.n_rays : nullptr;
+  V3 gacc = v3(0.f, 0.f, 0.f);  // GRAD: this lane's share of d loss / d origin
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
     // tile record (12 floats): cone axis xyz, cos, sin | azimuth centre xy, cos, sin of the sector
     const float4 c0 = ld4(tile_cones, 3 * tile), c1 = ld4(tile_cones, 3 * tile + 1);
@@ -607,16 +616,21 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
     const float2 azw = make_float2(cs.x * c1.y - cs.y * c1.z, cs.y * c1.y + cs.x * c1.z);
     const float cw = c1.w;
     // lane's rays: body-frame direction + ray index from the tile-ordered table
-    constexpr int NP = RPL / 2;  // packed pairs (RPL >= 2)
+    constexpr int NP = GRAD ? 0 : RPL / 2;  // packed pairs (RPL >= 2; GRAD tracks argmins per ray)
     int ray[RPL];
     V3 d[RPL];
     unsigned best[RPL];
+    float bestf[RPL];  // GRAD: float min-t, argmin code (kind | detail << 4) and list index
+    int code[RPL], bidx[RPL];
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
       const float4 td = ld4(tile_dirs, (tile * RPL + k) * 32 + lane);
       ray[k] = (int)td.w;
       d[k] = rotz_f(cs, xyz(td));
       best[k] = INF_BITS;
+      bestf[k] = INF;
+      code[k] = 0;
+      bidx[k] = 0;
     }
     V3 inv[RPL];
     float a[RPL], inv_a[RPL];
@@ -663,7 +677,13 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
         const int i = base + __ffs(ms) - 1;
         ms &= ms - 1;
         const float4 q = r0[i];
-        if constexpr (NP > 0) {
+        if constexpr (GRAD) {
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) {
+            const float t = hit_sphere(q, d[k]);
+            if (t < bestf[k]) { bestf[k] = t; code[k] = 1; bidx[k] = i; }
+          }
+        } else if constexpr (NP > 0) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) hit_sphere_p(best[2 * p], best[2 * p + 1], q, rp[p]);
         } else {
@@ -674,7 +694,14 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
         const int i = base + __ffs(mb) - 1;
         mb &= mb - 1;
         const float4 lo = r0[i], hi = r1[i];
-        if constexpr (NP > 0) {
+        if constexpr (GRAD) {
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) {
+            int axk = 0;
+            const float t = hit_box(lo, hi, inv[k], &axk);
+            if (t < bestf[k]) { bestf[k] = t; code[k] = 2 | (axk << 4); bidx[k] = i; }
+          }
+        } else if constexpr (NP > 0) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) hit_box_p(best[2 * p], best[2 * p + 1], lo, hi, rp[p]);
         } else {
@@ -685,13 +712,51 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
         const int i = base + __ffs(mc) - 1;
         mc &= mc - 1;
         const float4 q = r0[i], h = r1[i];
-        if constexpr (NP > 0) {
+        if constexpr (GRAD) {
+#pragma unroll
+          for (int k = 0; k < RPL; ++k) {
+            int part = 0;
+            const float t = hit_cyl(q, h.x, h.y, h.z, d[k], a[k], inv_a[k], inv[k].z, &part);
+            if (t < bestf[k]) { bestf[k] = t; code[k] = 3 | (part << 4); bidx[k] = i; }
+          }
+        } else if constexpr (NP > 0) {
 #pragma unroll
           for (int p = 0; p < NP; ++p) hit_cyl_p(best[2 * p], best[2 * p + 1], q, h, rp[p]);
         } else {
           best[0] = hit_cyl_u(best[0], q, h, d[0], a[0], inv_a[0], inv[0].z);
         }
       }
+    }
+    if constexpr (GRAD) {
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        if (ground) {
+          const float t = gdz * inv[k].z;
+          if (t >= 0.f && t < INF && t < bestf[k]) { bestf[k] = t; code[k] = 4; }
+        }
+        if (ray[k] < 0 || !(bestf[k] < rc.max_range)) continue;  // clamped / missed: zero gradient
+        V3 n = v3(0.f, 0.f, 0.f);
+        const int kind = code[k] & 15;
+        if (kind == 1) {
+          n = xyz(r0[bidx[k]]) + d[k] * bestf[k];  // x - c = oc + t d
+        } else if (kind == 2) {
+          const int axk = code[k] >> 4;
+          n = v3(axk == 0 ? 1.f : 0.f, axk == 1 ? 1.f : 0.f, axk == 2 ? 1.f : 0.f);
+        } else if (kind == 3) {
+          if ((code[k] >> 4) == 0) {
+            const float4 c = r0[bidx[k]];
+            n = v3(c.x + bestf[k] * d[k].x, c.y + bestf[k] * d[k].y, 0.f);
+          } else {
+            n = v3(0.f, 0.f, 1.f);
+          }
+        } else if (kind == 4) {
+          n = v3(0.f, 0.f, 1.f);
+        }
+        const float nd = dot(n, d[k]);
+        const V3 gv = nd != 0.f ? n * (-1.f / nd) : v3(0.f, 0.f, 0.f);
+        gacc += gv * g_row[ray[k]];
+      }
+      continue;
     }
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
@@ -701,6 +766,20 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
         out_row[ray[k]] = fminf(t, rc.max_range);
         if (hitm) hitm_row[ray[k]] = t < rc.max_range ? 1 : 0;
       }
+    }
+  }
+  if constexpr (GRAD) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      gacc.x += __shfl_xor_sync(0xffffffffu, gacc.x, off);
+      gacc.y += __shfl_xor_sync(0xffffffffu, gacc.y, off);
+      gacc.z += __shfl_xor_sync(0xffffffffu, gacc.z, off);
+    }
+    if (lane == 0) {
+      float* gp = g_pos + row * gpos_stride;
+      atomicAdd(gp + 0, gacc.x);
+      atomicAdd(gp + 1, gacc.y);
+      atomicAdd(gp + 2, gacc.z);
     }
   }
 }
@@ -783,6 +862,34 @@ int qs_raycast_tiled(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_row
   else { if (ext) { QS_RT_W(1, true); } else { QS_RT_W(1, false); } }
 #undef QS_RT_W
 #undef QS_RT
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
+
+int qs_raycast_tiled_vjp(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n_rows, const float* pos,
+                         int32_t pos_stride, const float* cam_cs, const float* tile_dirs, const float* tile_cones,
+                         int32_t n_tiles, int32_t tile_width, const float* g_depth, float* g_pos,
+                         int32_t gpos_stride, void* stream) {
+  if (n_rows <= 0 || cfg->n_rays <= 0) return QS_OK;
+  if (cfg->kind < 0 || cfg->kind > 1 || cfg->n_agents < 1 || n_tiles <= 0 || !g_depth || !g_pos)
+    return QS_ERR_BAD_ARGUMENT;
+  if (tile_width != 32 && tile_width != 64 && tile_width != 128) return QS_ERR_BAD_ARGUMENT;
+  dim3 grid(1, n_rows);
+  const bool ext = (cfg->cull & 2) != 0;
+  const int cap = scene->Sm + scene->Bm + scene->Cm;
+  size_t smem = (size_t)cap * ((ext ? 5 : 4) * 16) + (size_t)((cap + 31) / 32 + 1) * 8;
+  cudaStream_t s = (cudaStream_t)stream;
+#define QS_RV(K, X, R)                                                                                     \
+  k_raycast_tiled<K, X, R, true><<<grid, TILED_BLOCK, smem, s>>>(*cfg, *scene, n_rows, pos, pos_stride, cam_cs, \
+                                                                 tile_dirs, tile_cones, n_tiles, n_tiles, nullptr, \
+                                                                 nullptr, g_depth, g_pos, gpos_stride)
+#define QS_RV_W(K, X)                 \
+  if (tile_width == 32) QS_RV(K, X, 1); \
+  else if (tile_width == 64) QS_RV(K, X, 2); \
+  else QS_RV(K, X, 4)
+  if (cfg->kind == 0) { if (ext) { QS_RV_W(0, true); } else { QS_RV_W(0, false); } }
+  else { if (ext) { QS_RV_W(1, true); } else { QS_RV_W(1, false); } }
+#undef QS_RV_W
+#undef QS_RV
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 

@@ -474,22 +474,42 @@ def fov_cull(prims, cam_pos, cam_R, intrinsics: CameraIntrinsics):
 
 class _RenderDepthFn(torch.autograd.Function):
     """Opt-in differentiable depth: d depth / d body position via the analytic
-    d t / d o = -n / (n . d) of the hit surface (new capability; no reference)."""
+    d t / d o = -n / (n . d) of the hit surface (new capability; no reference).
+
+    Cameras and LiDARs take the tiled ray caster both ways: the forward renders
+    with no per-ray gradient output, and the backward recasts the same tiles to
+    find each ray's hit surface (``qs_raycast_tiled_vjp``), so no (N, R, 4)
+    dt/do tensor goes through HBM.  Generic rays (kind 2) keep the untiled
+    kernel's stored dt/do + ``qs_raycast_vjp``."""
 
     @staticmethod
     def forward(ctx, pos3, scene, cam_cs, sensor, kind, n_agents):
         pos = _pos4(pos3.detach())
-        out, _, dT = cast_rays(scene, pos, 4, cam_cs, sensor, kind, True, n_agents, want_grad=True)
-        ctx.save_for_backward(dT)
+        recast = kind in (0, 1) and TILED
+        out, _, dT = cast_rays(scene, pos, 4, cam_cs, sensor, kind, True, n_agents, want_grad=not recast)
+        ctx.recast, ctx.scene, ctx.sensor, ctx.kind, ctx.n_agents = recast, scene, sensor, kind, n_agents
+        ctx.save_for_backward(pos, cam_cs if cam_cs is not None else pos.new_zeros(0), dT if dT is not None
+                              else pos.new_zeros(0))
+        ctx.has_cs = cam_cs is not None
         return out
 
     @staticmethod
     def backward(ctx, g):
-        (dT,) = ctx.saved_tensors
+        pos, cs, dT = ctx.saved_tensors
         N, R = g.shape
         gp = torch.zeros(N, 4, dtype=torch.float32, device=g.device)
-        L.check(L.lib().qs_raycast_vjp(N, R, L.ptr(g.contiguous()), L.ptr(dT), L.ptr(gp), 4,
-                                       L.stream_handle(g.device)), "qs_raycast_vjp")
+        if ctx.recast:
+            rc = _ray_cfg(ctx.sensor, ctx.kind, True, ctx.n_agents)
+            if getattr(ctx.scene, "ext_cull", False):
+                rc.cull |= 2
+            tr, tc, td = _tile_table(ctx.sensor, g.device)
+            L.check(L.lib().qs_raycast_tiled_vjp(rc, ctx.scene.struct(), N, L.ptr(pos), 4,
+                                                 L.ptr(cs) if ctx.has_cs else None, L.ptr(td), L.ptr(tc),
+                                                 tr.shape[0], tr.shape[1], L.ptr(g.contiguous()), L.ptr(gp), 4,
+                                                 L.stream_handle(g.device)), "qs_raycast_tiled_vjp")
+        else:
+            L.check(L.lib().qs_raycast_vjp(N, R, L.ptr(g.contiguous()), L.ptr(dT), L.ptr(gp), 4,
+                                           L.stream_handle(g.device)), "qs_raycast_vjp")
         return gp[:, :3], None, None, None, None, None
 
 

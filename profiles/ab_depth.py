@@ -78,6 +78,19 @@ def main():
         res[name] = run(sc, pos.to(dev), cs.to(dev), cam, 0)
     pos, cs = poses(E, False)
     res["lidar"] = run(sc, pos.to(dev), cs.to(dev), lidar, 1)
+    # differentiable depth (forward + VJP): tiled recast vs untiled stored dt/do
+    pos_d, cs_d = pos.to(dev), cs.to(dev)
+    gdep = torch.randn(E, cam.n_rays, device=dev)
+    for name, tiled in (("diff_depth_tiled_recast", True), ("diff_depth_untiled_stored", False)):
+        sn.TILED = tiled
+
+        def fb():
+            p = pos_d[:, :3].clone().requires_grad_(True)
+            d = sn.render_depth_differentiable(sc, p, cs_d, cam, 0)
+            d.backward(gdep)
+
+        res[name] = {"ms_fwd_bwd": timed(fb, 10)}
+        sn.TILED = True
     sci = wd.gen_obstacle_courses(11, E, [0.0, 0.0, 1.2], [8.0, 0.0, 1.5], density=32 / 48.0, style="indoor",
                                   device=dev, check=False)
     pos, cs = poses(E, False, seed=9)

@@ -141,3 +141,29 @@ def test_depth_matches_oracle_on_generated_scenes():
     mask_ref = ref < 10.0
     flips = (hit.cpu().numpy().astype(bool) != mask_ref)
     assert flips.mean() < 1e-4, flips.sum()
+
+
+@pytest.mark.parametrize("kind,style", [("depth", "outdoor"), ("depth", "indoor"), ("lidar", "outdoor")])
+def test_depth_vjp_recast_equals_stored(kind, style):
+    """The tiled recast VJP (no dt/do in HBM) gives the untiled kernel's
+    stored-dt/do gradient: same hit surfaces, fp32 summation order only."""
+    import paper_2509_10247_b200 as qs
+    sn = qs.sensors
+
+    sc, pos, cs, _ = _scene_and_poses(qs, 512, 13, style=style)
+    sensor = sn.CameraIntrinsics(width=64, height=48, max_range=10.0) if kind == "depth" else \
+        sn.LidarPattern(n_azimuth=360, n_elevation=16, max_range=20.0)
+    k = 0 if kind == "depth" else 1
+    g = torch.randn(512, sensor.n_rays, generator=torch.Generator().manual_seed(3)).cuda()
+    grads = []
+    for tiled in (True, False):
+        sn.TILED = tiled
+        p = pos[:, :3].clone().requires_grad_(True)
+        d = sn.render_depth_differentiable(sc, p, cs, sensor, k)
+        (d * g).sum().backward()
+        grads.append(p.grad.clone())
+        sn.TILED = True
+    a, b = grads
+    assert float(b.abs().max()) > 0
+    err = (a - b).abs() / (b.abs() + 1e-3 * float(b.abs().max()))
+    assert float(err.max()) < 1e-4, float(err.max())
