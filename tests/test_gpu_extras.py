@@ -144,3 +144,18 @@ def test_obstacle_rerandomisation_on_reset():
                              "cylinders": s.prims.cylinders, "ground_z": 0.0},
                       bounds_lo=s.bounds_lo, bounds_hi=s.bounds_hi, spawn=s.spawn, goal=s.goal)
         assert O.grid_path_exists(osc)
+
+
+def test_every_kernel_family_at_small_odd_sizes():
+    """profiles/sanitize_workload.py: partial CTAs and tiny batches through the
+    windows (TMA / cp.async rings), per-step path, scene gen, tiled/untiled
+    ray casting at every tile width and both depth VJPs; no device error."""
+    import importlib.util
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                        "sanitize_workload.py")
+    spec = importlib.util.spec_from_file_location("sanitize_workload", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    mod.main()
