@@ -991,10 +991,19 @@ __global__ void __launch_bounds__(128) k_task_bwd(const qs_task_cfg cfg, const q
 
 // 64-thread CTAs, >= 7 resident per SM: 65,536 envs = 1,024 CTAs = one wave
 // on 148 SMs with <= 144 registers per thread
-constexpr int WIN_BLOCK = 64;
+#ifndef QS_WIN_BLOCK
+#define QS_WIN_BLOCK 64
+#endif
+#ifndef QS_WIN_MINB
+#define QS_WIN_MINB 7
+#endif
+#ifndef QS_BWD_NST
+#define QS_BWD_NST 2  // ring depth of the bwd checkpoint stream: 2 beats 3 (52.5 vs 54.6 us at C2) and 4 (70 us)
+#endif
+constexpr int WIN_BLOCK = QS_WIN_BLOCK;
 
 template <int M, int TASK, int G, int IMU>
-__global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg cfg, const qs_scene sc,
+__global__ void __launch_bounds__(WIN_BLOCK, QS_WIN_MINB) k_window_fwd(const qs_task_cfg cfg, const qs_scene sc,
                                                     const qs_window_io w) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
@@ -1109,7 +1118,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_fwd(const qs_task_cfg c
 }
 
 template <int M, int TASK, int G>
-__global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg cfg, const qs_scene sc,
+__global__ void __launch_bounds__(WIN_BLOCK, QS_WIN_MINB) k_window_bwd(const qs_task_cfg cfg, const qs_scene sc,
                                                     const qs_window_io w) {
   constexpr int A = ModelTraits<M>::A;
   const int na = G == 1 ? 1 : cfg.n_agents;
@@ -1124,7 +1133,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, 7) k_window_bwd(const qs_task_cfg c
   // Each thread streams its row's checkpoints through a private cp.async ring
   // in shared memory, NST steps ahead: the loads hold no registers while in
   // flight and each thread waits only for its own copies (no barrier).
-  constexpr int NST = 3;
+  constexpr int NST = QS_BWD_NST;
   constexpr int NPL = ModelTraits<M>::NP;
   constexpr int NREC = NPL + 4;  // state planes, goal, peff, dr, raw
   __shared__ __align__(16) float4 ring[NST][NREC][WIN_BLOCK];
