@@ -139,6 +139,19 @@ def ppo_log_prob(mu, log_sigma, a_raw, half):
     return base - corr.sum(-1)
 
 
+def clip_grads_(params, clip: float):
+    """Global-norm clip with the reference Adam's rule (q/nets.py:293-298):
+    scale by clip / (norm + 1e-12) when norm > clip.  Returns the pre-clip
+    norm as a device tensor (no host sync)."""
+    grads = [p.grad for p in params if p.grad is not None]
+    if not grads:
+        return torch.zeros(())
+    norm = torch.linalg.vector_norm(torch.stack(torch._foreach_norm(grads)).double())
+    scale = torch.where(norm > clip, clip / (norm + 1e-12), torch.ones_like(norm))
+    torch._foreach_mul_(grads, scale.to(grads[0].dtype))
+    return norm
+
+
 def allreduce_mean_(params, group=None):
     """Average .grad of ``params`` over ranks with one flattened all-reduce."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
@@ -260,7 +273,7 @@ class ShortHorizonTrainer:
         t1 = time.perf_counter()
         allreduce_mean_(list(self.policy.parameters()), self.group)
         t2 = time.perf_counter()
-        gnorm = torch.nn.utils.clip_grad_norm_(self.policy.parameters(), opts.grad_clip)
+        gnorm = clip_grads_(list(self.policy.parameters()), opts.grad_clip)
         self.actor_opt.step()
         out = {"loss": float(loss.detach()), "grad_norm": float(gnorm)}
         if self.needs_critic:
@@ -290,7 +303,7 @@ class ShortHorizonTrainer:
             loss = ((pred - y) ** 2).mean()
             loss.backward()
             allreduce_mean_(list(self.value.parameters()), self.group)
-            torch.nn.utils.clip_grad_norm_(self.value.parameters(), opts.grad_clip)
+            clip_grads_(list(self.value.parameters()), opts.grad_clip)
             self.critic_opt.step()
             loss_val = float(loss.detach())
         return loss_val
@@ -398,7 +411,7 @@ class PPOTrainer:
                 self.actor_opt.zero_grad(set_to_none=True)
                 actor_loss.backward()
                 allreduce_mean_(list(self.policy.parameters()), self.group)
-                torch.nn.utils.clip_grad_norm_(self.policy.parameters(), opts.grad_clip)
+                clip_grads_(list(self.policy.parameters()), opts.grad_clip)
                 self.actor_opt.step()
                 with self._nets():
                     pred = self.value(priv_f[rows]).float()
@@ -406,7 +419,7 @@ class PPOTrainer:
                 self.critic_opt.zero_grad(set_to_none=True)
                 (value_loss * opts.value_coef).backward()
                 allreduce_mean_(list(self.value.parameters()), self.group)
-                torch.nn.utils.clip_grad_norm_(self.value.parameters(), opts.grad_clip)
+                clip_grads_(list(self.value.parameters()), opts.grad_clip)
                 self.critic_opt.step()
                 pi_loss, v_loss, ent = actor_loss.detach(), value_loss.detach(), entropy.detach()
         self.update_count += 1
