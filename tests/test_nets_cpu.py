@@ -140,6 +140,6 @@ def test_c5_policy_has_the_reference_parameter_count():
     rng = np.random.default_rng([0, 0x11])
     pol = nets.PolicyNet(nets.PolicyArch(proprio_dim=9, action_dim=3), rng)
     assert pol.n_params() == 56518
-    # privileged state of the pm position task: 13 features (q/tasks.py:465-545)
-    val = nets.ValueNet(13, rng)
-    assert val.n_params() == 13 * 128 + 128 + 128 * 128 + 128 + 128 + 1
+    # privileged state: 14 features (q/tasks.py:465-545)
+    val = nets.ValueNet(14, rng)
+    assert val.n_params() == 18561
