@@ -95,17 +95,56 @@ def _cpu_worker(args):
             return done_steps, el
 
 
-def cpu_baseline(seconds: float, model: str, T: int, n_sample: int = 4096):
+def _cpu_depth_worker(args):
+    """C3 depth on the host: the oracle's render_depth (the reference's
+    algorithm: fov cull, then every kept solid per ray, fp64) over a few
+    in-corridor courses of the C3 distribution, random poses and yaws."""
+    n_envs, seconds, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import quadsim_oracle as O
+
+    spawn, goal = np.array([0.0, 0.0, 1.2]), np.array([8.0, 0.0, 1.5])
+    scenes = [O.gen_obstacle_course(seed * 1000 + i, spawn, goal, 32 / 48.0) for i in range(n_envs)]
+    prims = O.pack_primitives([sc.prims for sc in scenes])
+    rng = np.random.default_rng(seed)
+    rays = 0
+    t0 = time.perf_counter()
+    while True:
+        pos = np.stack([rng.uniform(0, 8, n_envs), rng.uniform(-3, 3, n_envs), rng.uniform(0.5, 3.5, n_envs)], -1)
+        O.render_depth(prims, pos, O.rotz(rng.uniform(0, 2 * np.pi, n_envs)), 64, 48, 10.0)
+        rays += n_envs * 64 * 48
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return rays, el
+
+
+def cpu_baseline(seconds: float, model: str, T: int, n_sample: int = 4096, extras: bool = True):
     cores = len(os.sched_getaffinity(0))
     per = max(1, n_sample // cores)
     ctx = mp.get_context("fork")
     with ctx.Pool(cores) as pool:
         res = pool.map(_cpu_worker, [(per, T, model, seconds, 1000 + i) for i in range(cores)])
+        # depth (the metric's second half): 16 courses per process, 64x48
+        dres = pool.map(_cpu_depth_worker, [(16, max(2.0, seconds / 3), 7 + i) for i in range(cores)]) \
+            if extras else None
     steps = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
+    out = {"value": steps / wall, "unit": UNIT, "cores": cores, "kind": "port",
+           "sample": f"{cores} procs x {per} envs, {model}+IMU position task, T={T} windows fwd+bwd "
+                     f"(numpy fp64 oracle incl. reverse pass) for {wall:.1f}s"}
+    if not extras:
+        return out
+    # one process, same per-process sample (SURVEY §8d: report both)
+    one = _cpu_worker((per, T, model, max(2.0, seconds / 3), 999))
     return {"value": steps / wall, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{cores} procs x {per} envs, {model}+IMU position task, T={T} windows fwd+bwd "
-                      f"(numpy fp64 oracle incl. reverse pass) for {wall:.1f}s"}
+                      f"(numpy fp64 oracle incl. reverse pass) for {wall:.1f}s",
+            "single_process": {"value": one[0] / one[1], "unit": UNIT, "cores": 1,
+                               "sample": f"1 proc x {per} envs for {one[1]:.1f}s"},
+            "depth": {"value": sum(r[0] for r in dres) / max(r[1] for r in dres), "unit": "rays/s",
+                      "cores": cores, "kind": "port",
+                      "sample": f"{cores} procs x 16 C3 courses (32/48 density), 64x48 depth, random corridor "
+                                f"poses, oracle render_depth with the reference's fov_cull (fp64)"}}
 
 
 def cpu_model():
@@ -740,11 +779,11 @@ def run_reference(a):
         return
     per_step_seconds = max(2.0, min(10.0, 60.0 / max(1, a.steps + a.warmup)))
     for _ in range(a.warmup):
-        cpu_baseline(min(2.0, per_step_seconds), a.model, a.horizon, n_sample=1024)
+        cpu_baseline(min(2.0, per_step_seconds), a.model, a.horizon, n_sample=1024, extras=False)
     vals = []
     last = None
     for _ in range(a.steps):
-        last = cpu_baseline(per_step_seconds, a.model, a.horizon)
+        last = cpu_baseline(per_step_seconds, a.model, a.horizon, extras=False)
         vals.append(last["value"])
     v = statistics.median(vals)
     ms = a.envs * a.horizon / v * 1e3
