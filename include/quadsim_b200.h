@@ -248,6 +248,18 @@ int qs_raycast_tiled_vjp(const qs_ray_cfg* cfg, const qs_scene* scene, int32_t n
 int qs_raycast_vjp(int32_t n_rows, int32_t n_rays, const float* g_depth, const float* dT_dO,
                    float* g_pos, int32_t pos_stride, void* stream);
 
+/* Learner side (config C5): one full-batch gradient of the privileged-state
+ * value MLP pred = tanh(tanh((x*scale) W0 + b0) W1 + b1) w2 + b2 with hidden
+ * width 128 (q/nets.py:259-274) for L = mean((pred - y)^2) (q/learners.py:
+ * 232-245), forward and backward fused on the tensor cores (bf16 operands,
+ * fp32 accumulation).  x (m,k) fp32 rows (k <= 16), y (m,); W0 (k,128), W1
+ * (128,128), w2 (128,) fp32.  The gradients (caller-zeroed, same shapes) and
+ * loss are ACCUMULATED.  n_sm: persistent CTAs (the SM count). */
+int qs_mlp3_fit_grad(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
+                     const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
+                     float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
+                     int32_t n_sm, void* stream);
+
 /* sdf_np / sdf_var (q/sensors.py:417-501): points (N,4); out (N,); grad (N,4) | NULL */
 int qs_sdf(const qs_scene* scene, int32_t n_rows, int32_t n_agents, const float* pts, float* out,
            float* grad, void* stream);

@@ -1,0 +1,362 @@
+// Fused critic fit step (the caller side of config C5): one
+// full-batch gradient of the privileged-state value MLP of q/nets.py:259-274
+//
+//     pred = tanh(tanh(x W0 + b0) W1 + b1) w2 + b2,   L = mean((pred - y)^2)
+//
+// (q/learners.py:232-245) over all M = T x N rows in ONE launch, on the
+// tensor cores (mma.sync m16n8k16 bf16 -> fp32).  The torch version writes and
+// re-reads every 128-wide activation of 2.1M rows (GBs per iteration); here a
+// persistent CTA per SM keeps a 128-row tile's activations in shared memory,
+// runs forward and backward on it, and accumulates the weight gradients in
+// registers across all its tiles -- HBM sees only x, y and the parameters.
+//
+// Per tile (8 warps, warp w owns rows 16w..16w+15 for the row-parallel GEMMs):
+//   G1  H1 = tanh(X W0 + b0)            (128x16 @ 16x128)
+//   G2  H2 = tanh(H1 W1 + b1)           (128x128 @ 128x128), pred = H2 w2 + b2
+//       dZ2 = (2/M)(pred - y) w2 (1 - H2^2)
+//   G3  dZ1 = (dZ2 W1^T)(1 - H1^2)      (128x128 @ 128x128)
+//   G4  dW1 += H1^T dZ2                 (warp w owns dW1 rows 16w..: 16x128, K = 128 rows)
+//   G5  dW0 += X^T dZ1                  (warp w owns dW0 cols 16w..: 16x16)
+// and the bias / w2 gradients as column sums.  Operands are bf16 in shared
+// memory (row stride padded by 8 elements: conflict-free ldmatrix); the
+// accumulators, biases and all gradients are fp32.
+#include <cuda_bf16.h>
+
+#include "qs_common.cuh"
+
+namespace {
+
+constexpr int HID = 128;       // hidden width (the reference's (128, 128))
+constexpr int KIN = 16;        // input features, zero-padded (privileged state: 14)
+constexpr int TILE = 128;      // rows per tile
+constexpr int NWARP = 8;
+constexpr int LDH = HID + 8;   // padded row strides (bf16 elements)
+constexpr int LDX = KIN + 8;
+
+struct MlpSmem {
+  __nv_bfloat16 X[TILE][LDX];
+  __nv_bfloat16 W0[KIN][LDH];
+  __nv_bfloat16 W1[HID][LDH];
+  __nv_bfloat16 H1[TILE][LDH];
+  __nv_bfloat16 D2[TILE][LDH];
+  __nv_bfloat16 D1[TILE][LDH];
+  float b0[HID], b1[HID], w2[HID];
+  float gb0[HID], gb1[HID], gw2[HID];
+  float red[4];  // gb2, loss
+};
+
+QS_D uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+QS_D void ldsm4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr(p)));
+}
+QS_D void ldsm4t(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(saddr(p)));
+}
+QS_D void mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+QS_D float tanh_mufu(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+QS_D uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+QS_D float2 unpack_bf16(uint32_t u) {
+  __nv_bfloat162 v = *reinterpret_cast<__nv_bfloat162*>(&u);
+  return __bfloat1622float2(v);
+}
+// ldmatrix lane addresses: lane l feeds row (l % 8) of 8x8 matrix (l / 8)
+// A (16x16) from [m][k] storage: matrices (m0,k0) (m0+8,k0) (m0,k0+8) (m0+8,k0+8)
+template <int LD>
+QS_D const __nv_bfloat16* a_addr(const __nv_bfloat16* S, int m0, int k0, int lane) {
+  const int i = lane & 7, j = lane >> 3;
+  return S + (m0 + i + (j & 1) * 8) * LD + k0 + (j >> 1) * 8;
+}
+// A (16x16) from [k][m] storage with .trans: matrices (k0,m0) (k0,m0+8) (k0+8,m0) (k0+8,m0+8)
+template <int LD>
+QS_D const __nv_bfloat16* at_addr(const __nv_bfloat16* S, int m0, int k0, int lane) {
+  const int i = lane & 7, j = lane >> 3;
+  return S + (k0 + i + (j >> 1) * 8) * LD + m0 + (j & 1) * 8;
+}
+// two B (16x8) tiles n0, n0+8 from [k][n] storage with .trans:
+// matrices (k0,n0) (k0+8,n0) (k0,n0+8) (k0+8,n0+8) -> b0,b1 of tile 0, b0,b1 of tile 1
+template <int LD>
+QS_D const __nv_bfloat16* bt_addr(const __nv_bfloat16* S, int k0, int n0, int lane) {
+  const int i = lane & 7, j = lane >> 3;
+  return S + (k0 + i + (j & 1) * 8) * LD + n0 + (j >> 1) * 8;
+}
+// two B tiles from [n][k] storage (no trans): matrices (n0,k0) (n0,k0+8) (n0+8,k0) (n0+8,k0+8)
+template <int LD>
+QS_D const __nv_bfloat16* bn_addr(const __nv_bfloat16* S, int k0, int n0, int lane) {
+  const int i = lane & 7, j = lane >> 3;
+  return S + (n0 + i + (j >> 1) * 8) * LD + k0 + (j & 1) * 8;
+}
+
+__global__ void __launch_bounds__(NWARP * 32, 1)
+    k_mlp3_fit_grad(int64_t M, int K, float inv_m, const float* __restrict__ x, const float* __restrict__ scale,
+                    const float* __restrict__ y, const float* __restrict__ W0, const float* __restrict__ b0,
+                    const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ w2,
+                    const float* __restrict__ b2, float* __restrict__ gW0, float* __restrict__ gb0,
+                    float* __restrict__ gW1, float* __restrict__ gb1, float* __restrict__ gw2,
+                    float* __restrict__ gb2, float* __restrict__ loss) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  MlpSmem& S = *reinterpret_cast<MlpSmem*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  // ---- stage the parameters (bf16 operands, fp32 vectors)
+  for (int i = tid; i < KIN * HID; i += blockDim.x) {
+    const int r = i / HID, c = i % HID;
+    S.W0[r][c] = __float2bfloat16_rn(r < K ? W0[r * HID + c] : 0.f);
+  }
+  for (int i = tid; i < HID * HID; i += blockDim.x) S.W1[i / HID][i % HID] = __float2bfloat16_rn(W1[i]);
+  for (int i = tid; i < HID; i += blockDim.x) {
+    S.b0[i] = b0[i];
+    S.b1[i] = b1[i];
+    S.w2[i] = w2[i];
+    S.gb0[i] = S.gb1[i] = S.gw2[i] = 0.f;
+  }
+  if (tid < 4) S.red[tid] = 0.f;
+  const float bias2 = b2[0];
+  float acc4[16][4];  // dW1 rows 16w.. x 128 cols, persistent over tiles
+  float acc5[2][4];   // dW0 16 rows x cols 16w..16w+15
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc4[j][0] = acc4[j][1] = acc4[j][2] = acc4[j][3] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 2; ++j) acc5[j][0] = acc5[j][1] = acc5[j][2] = acc5[j][3] = 0.f;
+  __syncthreads();
+  const int r0 = warp * 16;  // this warp's rows within a tile
+  const int64_t ntiles = (M + TILE - 1) / TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * TILE;
+    // ---- X tile (scaled, zero-padded to 16 features; rows past M are zero)
+    for (int i = tid; i < TILE * KIN; i += blockDim.x) {
+      const int r = i / KIN, c = i % KIN;
+      const int64_t gr = row0 + r;
+      float v = 0.f;
+      if (c < K && gr < M) v = x[gr * K + c] * scale[c];
+      S.X[r][c] = __float2bfloat16_rn(v);
+    }
+    __syncthreads();
+    // ---- G1: H1 = tanh(X W0 + b0), this warp's 16 rows
+    float acc[16][4];
+    {
+      uint32_t a[4];
+      ldsm4(a, a_addr<LDX>(&S.X[0][0], r0, 0, lane));
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        uint32_t b[4];
+        ldsm4t(b, bt_addr<LDH>(&S.W0[0][0], 0, j * 8, lane));
+        acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+        acc[j + 1][0] = acc[j + 1][1] = acc[j + 1][2] = acc[j + 1][3] = 0.f;
+        mma(acc[j], a, b[0], b[1]);
+        mma(acc[j + 1], a, b[2], b[3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = j * 8 + 2 * t4;
+        const float h00 = tanh_mufu(acc[j][0] + S.b0[c]), h01 = tanh_mufu(acc[j][1] + S.b0[c + 1]);
+        const float h10 = tanh_mufu(acc[j][2] + S.b0[c]), h11 = tanh_mufu(acc[j][3] + S.b0[c + 1]);
+        *reinterpret_cast<uint32_t*>(&S.H1[r0 + g][c]) = pack_bf16(h00, h01);
+        *reinterpret_cast<uint32_t*>(&S.H1[r0 + g + 8][c]) = pack_bf16(h10, h11);
+      }
+    }
+    __syncwarp();
+    // ---- G2: H2 = tanh(H1 W1 + b1); pred; dZ2
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+    for (int k0 = 0; k0 < HID; k0 += 16) {
+      uint32_t a[4];
+      ldsm4(a, a_addr<LDH>(&S.H1[0][0], r0, k0, lane));
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        uint32_t b[4];
+        ldsm4t(b, bt_addr<LDH>(&S.W1[0][0], k0, j * 8, lane));
+        mma(acc[j], a, b[0], b[1]);
+        mma(acc[j + 1], a, b[2], b[3]);
+      }
+    }
+    float p0 = 0.f, p1 = 0.f;  // pred partials, rows g and g+8
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = j * 8 + 2 * t4;
+      acc[j][0] = tanh_mufu(acc[j][0] + S.b1[c]);
+      acc[j][1] = tanh_mufu(acc[j][1] + S.b1[c + 1]);
+      acc[j][2] = tanh_mufu(acc[j][2] + S.b1[c]);
+      acc[j][3] = tanh_mufu(acc[j][3] + S.b1[c + 1]);
+      p0 = fmaf(acc[j][0], S.w2[c], fmaf(acc[j][1], S.w2[c + 1], p0));
+      p1 = fmaf(acc[j][2], S.w2[c], fmaf(acc[j][3], S.w2[c + 1], p1));
+    }
+    p0 += __shfl_xor_sync(0xffffffffu, p0, 1);
+    p0 += __shfl_xor_sync(0xffffffffu, p0, 2);
+    p1 += __shfl_xor_sync(0xffffffffu, p1, 1);
+    p1 += __shfl_xor_sync(0xffffffffu, p1, 2);
+    const int64_t ra = row0 + r0 + g, rb = ra + 8;
+    const float e0 = ra < M ? p0 + bias2 - y[ra] : 0.f;
+    const float e1 = rb < M ? p1 + bias2 - y[rb] : 0.f;
+    const float d0 = 2.f * inv_m * e0, d1 = 2.f * inv_m * e1;  // dL/dpred
+    float lsum = t4 == 0 ? e0 * e0 + e1 * e1 : 0.f, gb2s = t4 == 0 ? d0 + d1 : 0.f;
+    // dw2, db1 column partials over this thread's two rows; dZ2 -> D2
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = j * 8 + 2 * t4;
+      float gw_a = acc[j][0] * d0 + acc[j][2] * d1, gw_b = acc[j][1] * d0 + acc[j][3] * d1;
+      const float z00 = d0 * S.w2[c] * (1.f - acc[j][0] * acc[j][0]);
+      const float z01 = d0 * S.w2[c + 1] * (1.f - acc[j][1] * acc[j][1]);
+      const float z10 = d1 * S.w2[c] * (1.f - acc[j][2] * acc[j][2]);
+      const float z11 = d1 * S.w2[c + 1] * (1.f - acc[j][3] * acc[j][3]);
+      *reinterpret_cast<uint32_t*>(&S.D2[r0 + g][c]) = pack_bf16(z00, z01);
+      *reinterpret_cast<uint32_t*>(&S.D2[r0 + g + 8][c]) = pack_bf16(z10, z11);
+      float gbs_a = z00 + z10, gbs_b = z01 + z11;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {  // sum over the 8 row groups (lanes with the same t4)
+        gw_a += __shfl_xor_sync(0xffffffffu, gw_a, o);
+        gw_b += __shfl_xor_sync(0xffffffffu, gw_b, o);
+        gbs_a += __shfl_xor_sync(0xffffffffu, gbs_a, o);
+        gbs_b += __shfl_xor_sync(0xffffffffu, gbs_b, o);
+      }
+      if (g == 0) {
+        atomicAdd(&S.gw2[c], gw_a);
+        atomicAdd(&S.gw2[c + 1], gw_b);
+        atomicAdd(&S.gb1[c], gbs_a);
+        atomicAdd(&S.gb1[c + 1], gbs_b);
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+      gb2s += __shfl_xor_sync(0xffffffffu, gb2s, o);
+    }
+    if (lane == 0) {
+      atomicAdd(&S.red[0], gb2s);
+      atomicAdd(&S.red[1], lsum);
+    }
+    __syncwarp();
+    // ---- G3: dZ1 = (dZ2 W1^T)(1 - H1^2) -> D1; db0 partials
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+#pragma unroll
+    for (int k0 = 0; k0 < HID; k0 += 16) {
+      uint32_t a[4];
+      ldsm4(a, a_addr<LDH>(&S.D2[0][0], r0, k0, lane));
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        uint32_t b[4];
+        ldsm4(b, bn_addr<LDH>(&S.W1[0][0], k0, j * 8, lane));  // W1^T: B(k=o, n=i) = W1[i][o]
+        mma(acc[j], a, b[0], b[1]);
+        mma(acc[j + 1], a, b[2], b[3]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int c = j * 8 + 2 * t4;
+      const float2 h0 = unpack_bf16(*reinterpret_cast<const uint32_t*>(&S.H1[r0 + g][c]));
+      const float2 h1 = unpack_bf16(*reinterpret_cast<const uint32_t*>(&S.H1[r0 + g + 8][c]));
+      const float z00 = acc[j][0] * (1.f - h0.x * h0.x), z01 = acc[j][1] * (1.f - h0.y * h0.y);
+      const float z10 = acc[j][2] * (1.f - h1.x * h1.x), z11 = acc[j][3] * (1.f - h1.y * h1.y);
+      *reinterpret_cast<uint32_t*>(&S.D1[r0 + g][c]) = pack_bf16(z00, z01);
+      *reinterpret_cast<uint32_t*>(&S.D1[r0 + g + 8][c]) = pack_bf16(z10, z11);
+      float ga = z00 + z10, gb = z01 + z11;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        gb += __shfl_xor_sync(0xffffffffu, gb, o);
+      }
+      if (g == 0) {
+        atomicAdd(&S.gb0[c], ga);
+        atomicAdd(&S.gb0[c + 1], gb);
+      }
+    }
+    __syncthreads();  // H1, D2, D1, X of every row are in shared memory
+    // ---- G4: dW1[16w.., :] += H1^T dZ2 (K = the tile's 128 rows)
+#pragma unroll
+    for (int k0 = 0; k0 < TILE; k0 += 16) {
+      uint32_t a[4];
+      ldsm4t(a, at_addr<LDH>(&S.H1[0][0], r0, k0, lane));
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        uint32_t b[4];
+        ldsm4t(b, bt_addr<LDH>(&S.D2[0][0], k0, j * 8, lane));
+        mma(acc4[j], a, b[0], b[1]);
+        mma(acc4[j + 1], a, b[2], b[3]);
+      }
+    }
+    // ---- G5: dW0[:, 16w..16w+15] += X^T dZ1
+#pragma unroll
+    for (int k0 = 0; k0 < TILE; k0 += 16) {
+      uint32_t a[4], b[4];
+      ldsm4t(a, at_addr<LDX>(&S.X[0][0], 0, k0, lane));
+      ldsm4t(b, bt_addr<LDH>(&S.D1[0][0], k0, r0, lane));
+      mma(acc5[0], a, b[0], b[1]);
+      mma(acc5[1], a, b[2], b[3]);
+    }
+    __syncthreads();  // the next tile overwrites X, H1, D2, D1
+  }
+  // ---- flush: register / shared partials into the global fp32 gradients
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int c = j * 8 + 2 * t4;
+    atomicAdd(&gW1[(r0 + g) * HID + c], acc4[j][0]);
+    atomicAdd(&gW1[(r0 + g) * HID + c + 1], acc4[j][1]);
+    atomicAdd(&gW1[(r0 + g + 8) * HID + c], acc4[j][2]);
+    atomicAdd(&gW1[(r0 + g + 8) * HID + c + 1], acc4[j][3]);
+  }
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int c = r0 + j * 8 + 2 * t4;
+    if (g < K) {
+      atomicAdd(&gW0[g * HID + c], acc5[j][0]);
+      atomicAdd(&gW0[g * HID + c + 1], acc5[j][1]);
+    }
+    if (g + 8 < K) {
+      atomicAdd(&gW0[(g + 8) * HID + c], acc5[j][2]);
+      atomicAdd(&gW0[(g + 8) * HID + c + 1], acc5[j][3]);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < HID; i += blockDim.x) {
+    atomicAdd(&gb0[i], S.gb0[i]);
+    atomicAdd(&gb1[i], S.gb1[i]);
+    atomicAdd(&gw2[i], S.gw2[i]);
+  }
+  if (tid == 0) {
+    atomicAdd(gb2, S.red[0]);
+    atomicAdd(loss, S.red[1] * inv_m);
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int qs_mlp3_fit_grad(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
+                     const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
+                     float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
+                     int32_t n_sm, void* stream) {
+  if (m <= 0) return QS_OK;
+  if (k < 1 || k > KIN || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
+  const size_t smem = sizeof(MlpSmem);
+  static_assert(sizeof(MlpSmem) <= 227 * 1024, "shared memory");
+  if (cudaFuncSetAttribute(k_mlp3_fit_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return QS_ERR_LAUNCH;
+  const int64_t ntiles = (m + TILE - 1) / TILE;
+  const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
+  k_mlp3_fit_grad<<<grid, NWARP * 32, smem, (cudaStream_t)stream>>>(m, k, 1.f / (float)m, x, scale, y, W0, b0, W1,
+                                                                     b1, w2, b2, gW0, gb0, gW1, gb1, gw2, gb2,
+                                                                     loss);
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
+
+}  // extern "C"

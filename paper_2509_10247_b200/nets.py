@@ -229,6 +229,42 @@ class ValueNet(torch.nn.Module):
         return sum(p.numel() for p in self.parameters())
 
 
+def value_fit_grad(value: "ValueNet", x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
+    """Full-batch gradient of L = mean((value(x) - y)^2) written into the
+    ``.grad`` of every ValueNet parameter by ONE fused kernel (forward and
+    backward on the tensor cores, activations never leave shared memory;
+    ``qs_mlp3_fit_grad``).  Returns L (a device scalar, no host sync).  For the
+    reference critic shape: two tanh layers of width 128, at most 16 inputs,
+    fp32 CUDA tensors x (M, K), y (M,)."""
+    from paper_2509_10247_b200 import _lib as L
+
+    layers = value.value.layers
+    if len(layers) != 3 or layers[0].W.shape[1] != 128 or layers[1].W.shape != (128, 128) or \
+            layers[2].W.shape != (128, 1) or x.shape[1] > 16:
+        raise ValueError("value_fit_grad: needs the (128, 128) critic with <= 16 inputs")
+    dev = x.device
+    x = x.contiguous().float()
+    y = y.contiguous().float()
+    M, K = x.shape
+    params = [layers[0].W, layers[0].b, layers[1].W, layers[1].b, layers[2].W, layers[2].b]
+    flat = torch.zeros(sum(p.numel() for p in params) + 1, dtype=torch.float32, device=dev)
+    grads, off = [], 0
+    for p in params:
+        grads.append(flat[off:off + p.numel()].view_as(p))
+        off += p.numel()
+    loss = flat[off:]
+    scale = value.input_scale.to(device=dev, dtype=torch.float32).contiguous()
+    w = [p.detach().float().contiguous() for p in params]
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    L.check(L.lib().qs_mlp3_fit_grad(M, K, L.ptr(x), L.ptr(scale), L.ptr(y), L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]),
+                                     L.ptr(w[3]), L.ptr(w[4]), L.ptr(w[5]), L.ptr(grads[0]), L.ptr(grads[1]),
+                                     L.ptr(grads[2]), L.ptr(grads[3]), L.ptr(grads[4]), L.ptr(grads[5]),
+                                     L.ptr(loss), n_sm, L.stream_handle(dev)), "qs_mlp3_fit_grad")
+    for p, gr in zip(params, grads):
+        p.grad = gr
+    return loss[0]
+
+
 # ---------------------------------------------------------------------------
 # the reference's parameter names <-> module parameters
 

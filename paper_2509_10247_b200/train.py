@@ -22,7 +22,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from paper_2509_10247_b200.nets import LOG_SIGMA_MIN, PolicyArch, PolicyNet, ValueNet  # noqa: F401
+from paper_2509_10247_b200.nets import LOG_SIGMA_MIN, PolicyArch, PolicyNet, ValueNet, value_fit_grad  # noqa: F401
 
 
 @dataclass
@@ -57,6 +57,8 @@ class LearnerOptions:
     # tensor cores under torch.autocast (fp32 master weights, fp32 sim
     # gradients); "fp32" keeps the reference's all-fp32 arithmetic (SIMT GEMMs)
     net_dtype: str = "bf16"
+    # bf16 critic fit through the fused forward+backward kernel (nets.value_fit_grad)
+    fused_critic: bool = True
 
 
 def td_lambda_targets(r, values, bootstrap, done, gamma, lam):
@@ -295,18 +297,20 @@ class ShortHorizonTrainer:
             targets = td_lambda_targets(r, values, boot, dones, opts.gamma, opts.td_lambda)
         X = priv.reshape(-1, priv.shape[-1])
         y = targets.reshape(-1)
-        loss_val = 0.0
+        fused = opts.fused_critic and self._amp and X.shape[1] <= 16 and tuple(opts.mlp) == (128, 128)
         for _ in range(opts.critic_iters):
             self.critic_opt.zero_grad(set_to_none=True)
-            with self._nets():
-                pred = self.value(X)
-            loss = ((pred - y) ** 2).mean()
-            loss.backward()
+            if fused:  # one kernel: forward + backward of the whole batch, grads into .grad
+                loss = value_fit_grad(self.value, X, y)
+            else:
+                with self._nets():
+                    pred = self.value(X)
+                loss = ((pred - y) ** 2).mean()
+                loss.backward()
             allreduce_mean_(list(self.value.parameters()), self.group)
             clip_grads_(list(self.value.parameters()), opts.grad_clip)
             self.critic_opt.step()
-            loss_val = float(loss.detach())
-        return loss_val
+        return float(loss.detach())  # the last iteration's loss; one host sync per fit
 
 
 class PPOTrainer:
