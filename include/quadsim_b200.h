@@ -188,6 +188,11 @@ int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_ste
  * recorded by FlightTask.step; subgradients per q/autodiff.py). */
 int qs_task_step_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_grad* g,
                      void* stream);
+/* privileged_state (q/tasks.py:500-545) of the state in io->S_out / io->goal_out:
+ * out (N,14) = yaw-local goal offset, velocity, thrust; sdf clamped to +-5;
+ * yaw-local clearance direction; goal distance (critic features). */
+int qs_task_privileged(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io, float* out,
+                       void* stream);
 /* collect_window + Tape.backward of the BPTT learner for open-loop actions
  * (q/learners.py:201-265): T fused steps forward / T analytic VJPs backward in
  * one launch each. */

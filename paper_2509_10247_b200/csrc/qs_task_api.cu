@@ -70,6 +70,14 @@ int qs_task_observe(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step
   return task_call(3, cfg, scene, io, nullptr, nullptr, stream);
 }
 
+int qs_task_privileged(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io, float* out,
+                       void* stream) {
+  if (!io || !out) return QS_ERR_BAD_ARGUMENT;
+  qs_step_io o = *io;
+  o.obs = out;
+  return task_call(7, cfg, scene, &o, nullptr, nullptr, stream);
+}
+
 int qs_task_window_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_window_io* w,
                        void* stream) {
   if (cfg && cfg->reset_mode != 0) return QS_ERR_BAD_ARGUMENT;  // windows reset in-kernel

@@ -1262,6 +1262,48 @@ __global__ void __launch_bounds__(128) k_task_observe(const qs_task_cfg cfg, con
   if (io.flags) io.flags[row] = (io.flags[row] & ~FLAG_CLAMP_MASK) | bits;
 }
 
+// critic features of the current state (q/tasks.py:500-545, the no-grad
+// FlightTask.privileged_state): yaw-local goal offset, velocity and thrust,
+// sdf clamped to +-5, yaw-local clearance direction (the sdf's analytic
+// gradient at its first argmin), goal distance -- 14 floats per row, written
+// to io.obs (stride 14).  One launch instead of the ~30 torch ops + 2 sdf
+// launches of the differentiable twin (privileged_var), which stays in torch.
+template <int M, int TASK, int G>
+__global__ void __launch_bounds__(128) k_task_privileged(const qs_task_cfg cfg, const qs_scene sc,
+                                                         const qs_step_io io) {
+  const int na = G == 1 ? 1 : cfg.n_agents;
+  const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
+  const Grp<G> grp = Grp<G>::make(na);
+  if (!rm.active || !grp.real) return;
+  const long e = rm.e, row = rm.row;
+  const long N = (long)cfg.n_envs * na;
+  const DynK k = dyn_consts(cfg);
+  const State s = load_state<M>(io.S_out, N, row);
+  const V3 off = load3(io.goal_out, row) - s.p;
+  const float2 cs = yaw_cs<M>(s, k.g);
+  V3 th;  // FlightTask._thrust (q/tasks.py:479-498)
+  if (M == QS_MODEL_FULL) {
+    const Q4 q = s.q;
+    th = v3(2.f * (q.x * q.z + q.w * q.y), 2.f * (q.y * q.z - q.w * q.x), 1.f - 2.f * (q.x * q.x + q.y * q.y)) * 9.81f;
+  } else if (M == QS_MODEL_SIMPLIFIED) {
+    th = s.r2 * 9.81f;
+  } else {
+    th = thrust_of<M>(s, k.g);
+  }
+  const SceneView sv = scene_view(sc, e);
+  int code;
+  const float sd = sdf_eval(sv, s.p, code);
+  const V3 gd = code ? sdf_grad(sv, s.p, code) : v3(0.f, 0.f, 0.f);
+  const V3 a = unrotz(cs, off), b = unrotz(cs, s.v), c = unrotz(cs, th), d = unrotz(cs, gd);
+  float* o = io.obs + row * 14;
+  o[0] = a.x; o[1] = a.y; o[2] = a.z;
+  o[3] = b.x; o[4] = b.y; o[5] = b.z;
+  o[6] = c.x; o[7] = c.y; o[8] = c.z;
+  o[9] = clampf(sd, -5.f, 5.f);
+  o[10] = d.x; o[11] = d.y; o[12] = d.z;
+  o[13] = sqrtf(dot(off, off));
+}
+
 // ---------------------------------------------------------------------------
 // per-task launchers (one translation unit per task keeps builds parallel)
 
@@ -1305,6 +1347,13 @@ int run_observe(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io
 }
 
 template <int M, int T, int G>
+int run_privileged(const qs_task_cfg* cfg, const qs_scene* sc, const qs_step_io* io, cudaStream_t s) {
+  const long th = (long)cfg->n_envs * G;
+  k_task_privileged<M, T, G><<<grid_for(th, 128), 128, 0, s>>>(*cfg, *sc, *io);
+  return launch_status();
+}
+
+template <int M, int T, int G>
 int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_window_io* w, cudaStream_t s) {
   if (w->T <= 0) return QS_OK;
   if (op == 4 && w->loss) cudaMemsetAsync(w->loss, 0, sizeof(double), s);
@@ -1322,7 +1371,7 @@ int run_window(int op, const qs_task_cfg* cfg, const qs_scene* sc, const qs_wind
   return launch_status();
 }
 
-// op: 0 fwd, 1 bwd, 2 spawn, 3 observe, 4 window fwd, 5 window bwd.
+// op: 0 fwd, 1 bwd, 2 spawn, 3 observe, 4 window fwd, 5 window bwd, 7 critic features.
 // One translation unit per (task, single / multi agent) keeps the build
 // parallel; multi-agent picks the lane-group width G from n_agents.
 template <int T, int NA>
@@ -1339,6 +1388,7 @@ int task_op(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p, c
     case 3: return run_observe<M, T, G>(cfg, sc, static_cast<const qs_step_io*>(p), s);
     case 4:
     case 5: return run_window<M, T, G>(op, cfg, sc, static_cast<const qs_window_io*>(p), s);
+    case 7: return run_privileged<M, T, G>(cfg, sc, static_cast<const qs_step_io*>(p), s);
   }
   return QS_ERR_BAD_ARGUMENT;
 }

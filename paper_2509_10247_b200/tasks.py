@@ -879,9 +879,14 @@ class FlightTask:
                           unrot(grad[:, 0:3]), torch.linalg.norm(off, dim=-1, keepdim=True)], -1)
 
     def privileged_state(self) -> torch.Tensor:
-        """No-grad twin of privileged_var (q/tasks.py:525-545)."""
-        with torch.no_grad():
-            return self.privileged_var().detach()
+        """No-grad twin of privileged_var (q/tasks.py:525-545), one kernel
+        (qs_task_privileged) on the current state."""
+        out = torch.empty(self.N, 14, dtype=torch.float32, device=self.device)
+        io = self._new_io()
+        io.S_out, io.goal_out = L.ptr(self._S.detach()), L.ptr(self._goal)
+        L.check(L.lib().qs_task_privileged(self._cfg, self._scene.struct(), io, L.ptr(out),
+                                           L.stream_handle(self.device)), "qs_task_privileged")
+        return out
 
 
 class _ObserveFn(torch.autograd.Function):

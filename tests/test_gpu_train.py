@@ -167,3 +167,21 @@ def test_shac_with_fused_critic_fits_values():
     losses = [tr.update()["critic_loss"] for _ in range(15)]
     assert all(np.isfinite(losses))
     assert np.mean(losses[-4:]) < np.mean(losses[:4])
+
+
+@pytest.mark.parametrize("task,model", [("position", "full"), ("position", "simplified"),
+                                        ("avoidance", "pm_discrete"), ("avoidance", "pm_continuous")])
+def test_privileged_state_kernel_equals_torch_twin(task, model):
+    """qs_task_privileged (one kernel) == privileged_var (torch ops), the
+    differentiable twin the terminal critic value backpropagates through."""
+    import paper_2509_10247_b200 as qs
+
+    env = qs.make_task(qs.TaskConfig(task=task, dynamics=model, n_envs=300, density=0.3), strict=False)
+    env.reset(seed=6)
+    for t in range(5):
+        env.step(torch.randn(env.N, env.action_dim, device="cuda") * 0.5)
+    a = env.privileged_state()
+    with torch.no_grad():
+        b = env.privileged_var()
+    assert a.shape == b.shape == (300, 14)
+    torch.testing.assert_close(a, b, rtol=2e-5, atol=2e-5)
