@@ -815,7 +815,9 @@ def run_c5(a):
     cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=N, episode_len=128)
     env = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
     env.reset(seed=1)
-    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0))
+    # whole updates replayed from a CUDA graph when single-rank (the eager
+    # update is host-bound: ~30 torch ops per policy step, autograd recording)
+    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0, cuda_graph=world == 1))
     for _ in range(a.warmup):
         tr.update()
     torch.cuda.synchronize()

@@ -847,10 +847,12 @@ class FlightTask:
     def _thrust(self, st: dyn.QuadState) -> torch.Tensor:
         """q/tasks.py:479-498."""
         name = self.config.dynamics
-        g = torch.as_tensor(self.base_params.g_vec, dtype=torch.float32, device=self.device)
         if name == "pm_continuous":
             return st.a_lat
         if name == "pm_discrete":
+            g = getattr(self, "_g_dev", None)
+            if g is None:  # cached: no host->device copy per call (CUDA-graph capture)
+                g = self._g_dev = torch.as_tensor(self.base_params.g_vec, dtype=torch.float32, device=self.device)
             return st.u_prev - g
         if name == "simplified":
             return st.R[:, :, 2] * 9.81

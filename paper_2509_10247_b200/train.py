@@ -59,6 +59,9 @@ class LearnerOptions:
     net_dtype: str = "bf16"
     # bf16 critic fit through the fused forward+backward kernel (nets.value_fit_grad)
     fused_critic: bool = True
+    # replay each whole update (rollout, BPTT backward, actor step, critic fit)
+    # from one CUDA graph (ShortHorizonTrainer; single-rank, no-sensor envs)
+    cuda_graph: bool = False
 
 
 def td_lambda_targets(r, values, bootstrap, done, gamma, lam):
@@ -204,11 +207,12 @@ class ShortHorizonTrainer:
         # same seed gives the reference's initial weights, on every rank
         self.policy, self.value = make_nets(env, opts, critic=opts.algo in ("shac", "sha2c", "ppo"))
         self.policy.to(dev)
-        self.actor_opt = torch.optim.Adam(self.policy.parameters(), lr=opts.actor_lr)
+        graph = opts.cuda_graph and dev.type == "cuda"
+        self.actor_opt = torch.optim.Adam(self.policy.parameters(), lr=opts.actor_lr, capturable=graph)
         self.needs_critic = self.value is not None
         if self.needs_critic:
             self.value.to(dev)
-            self.critic_opt = torch.optim.Adam(self.value.parameters(), lr=opts.critic_lr)
+            self.critic_opt = torch.optim.Adam(self.value.parameters(), lr=opts.critic_lr, capturable=graph)
         self.hidden = self.policy.initial_hidden(env.N, dev)
         self.update_count = 0
         self._gen = torch.Generator(device=dev)
@@ -217,10 +221,14 @@ class ShortHorizonTrainer:
         if opts.net_dtype not in ("bf16", "fp32"):
             raise ValueError("net_dtype must be 'bf16' or 'fp32'")
         self._amp = opts.net_dtype == "bf16" and dev.type == "cuda"
+        self._graph = None
+        self._graph_mode = graph
+        self._warm = 0
 
     def _nets(self):
-        """autocast scope for policy/critic evaluations (no-op for fp32 / CPU)."""
-        return torch.autocast("cuda", dtype=torch.bfloat16, enabled=self._amp)
+        """autocast scope for policy/critic evaluations (no-op for fp32 / CPU);
+        the cast cache is off under graph capture (torch's requirement)."""
+        return torch.autocast("cuda", dtype=torch.bfloat16, enabled=self._amp, cache_enabled=not self._graph_mode)
 
     def collect_window(self, record_privileged: bool):
         """q/learners.py:201-230."""
@@ -253,9 +261,10 @@ class ShortHorizonTrainer:
         return disc, torch.stack(r_ctrl), torch.stack(r_goal), torch.stack(dones), (
             torch.stack(priv) if record_privileged else None)
 
-    def update(self) -> dict:
+    def _update_tensors(self):
+        """One update with every result left on the device (no host sync):
+        (actor loss, pre-clip grad norm, critic loss or None)."""
         opts = self.opts
-        t0 = time.perf_counter()
         disc, r_ctrl, r_goal, dones, priv = self.collect_window(self.needs_critic)
         body = disc
         if self.needs_critic:
@@ -267,24 +276,88 @@ class ShortHorizonTrainer:
                 p.requires_grad_(True)
             body = body + v_term.mean() * (opts.gamma ** opts.horizon)
         loss = -body / opts.horizon
-        if not bool(torch.isfinite(loss)):
-            raise FloatingPointError("non-finite actor loss; check reward terms")
-        self.actor_opt.zero_grad(set_to_none=True)
+        self.actor_opt.zero_grad(set_to_none=not self._graph_mode)
         loss.backward()
-        torch.cuda.synchronize(self.env.device) if self.env.device.type == "cuda" else None
         t1 = time.perf_counter()
         allreduce_mean_(list(self.policy.parameters()), self.group)
-        t2 = time.perf_counter()
+        self.timing["allreduce_s"] += time.perf_counter() - t1
         gnorm = clip_grads_(list(self.policy.parameters()), opts.grad_clip)
         self.actor_opt.step()
-        out = {"loss": float(loss.detach()), "grad_norm": float(gnorm)}
+        closs = None
         if self.needs_critic:
-            out["critic_loss"] = self._critic_update(r_ctrl if opts.algo == "shac" else r_goal, dones, priv)
+            closs = self._critic_update(r_ctrl if opts.algo == "shac" else r_goal, dones, priv)
+        return loss.detach(), gnorm, closs
+
+    def update(self) -> dict:
+        opts = self.opts
+        t0 = time.perf_counter()
+        if self._graph_mode and self._graph is None and self._warm >= 3:
+            self._capture()  # records only: this call's update is the first replay
+        if self._graph is not None:
+            self._graph.replay()
+            loss, gnorm, closs = self._graph_out
+        elif self._graph_mode:  # the eager warm-up updates torch asks for, on a side stream
+            side = torch.cuda.Stream(self.env.device)
+            side.wait_stream(torch.cuda.current_stream(self.env.device))
+            with torch.cuda.stream(side):
+                loss, gnorm, closs = self._update_tensors()
+            torch.cuda.current_stream(self.env.device).wait_stream(side)
+            self._warm += 1
+        else:
+            loss, gnorm, closs = self._update_tensors()
+        out = {"loss": float(loss), "grad_norm": float(gnorm)}  # the update's one host sync
+        if not np.isfinite(out["loss"]):
+            raise FloatingPointError("non-finite actor loss; check reward terms")
+        if closs is not None:
+            out["critic_loss"] = float(closs)
         self.update_count += 1
-        self.timing["sim_fwd_bwd_s"] += t1 - t0
-        self.timing["allreduce_s"] += t2 - t1
+        self.timing["sim_fwd_bwd_s"] += time.perf_counter() - t0
         out["steps_per_sec"] = opts.horizon * self.env.N / (time.perf_counter() - t0)
         return out
+
+    def _capture(self):
+        """Record one whole update into a CUDA graph (torch's whole-network
+        capture: forward, autograd backward and capturable Adam).  The env's
+        functional state (S, goal, effort, randomisation) and the GRU hidden
+        state are carried through static buffers that the graph reads at its
+        start and rewrites at its end; counters, statistics and the error word
+        already live in device buffers updated in place.  update() runs three
+        eager updates on a side stream before capturing (lazy optimiser /
+        autograd state); capturing executes nothing."""
+        env = self.env
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
+            raise RuntimeError("cuda_graph: single-rank only (NCCL all-reduce stays eager)")
+        if env.strict or env.config.sensor != "none" or env.reset_source is not None or env._regen:
+            raise RuntimeError("cuda_graph needs strict=False, no sensor, in-kernel resets and no scene regen")
+        carry = {"S": env._S.detach().clone(), "goal": env._goal.clone(), "peff": env._peff.clone(),
+                 "dr": env._dr.clone() if env._dr is not None else None,
+                 "hidden": self.hidden.clone() if self.hidden is not None else None}
+
+        def bind():
+            env._S, env._goal, env._peff = carry["S"], carry["goal"], carry["peff"]
+            if carry["dr"] is not None:
+                env._dr = carry["dr"]
+            if carry["hidden"] is not None:
+                self.hidden = carry["hidden"]
+
+        def carry_back():
+            carry["S"].copy_(env._S.detach())
+            carry["goal"].copy_(env._goal)
+            carry["peff"].copy_(env._peff)
+            if carry["dr"] is not None:
+                carry["dr"].copy_(env._dr)
+            if carry["hidden"] is not None:
+                carry["hidden"].copy_(self.hidden)
+
+        g = torch.cuda.CUDAGraph()
+        g.register_generator_state(self._gen)
+        bind()
+        with torch.cuda.graph(g):
+            out = self._update_tensors()
+            carry_back()
+        bind()
+        self._graph, self._graph_out = g, out
+        self._carry = carry
 
     def _critic_update(self, r, dones, priv):
         """TD-lambda targets + full-batch MSE fit (q/learners.py:232-245, 286-292)."""
@@ -299,7 +372,7 @@ class ShortHorizonTrainer:
         y = targets.reshape(-1)
         fused = opts.fused_critic and self._amp and X.shape[1] <= 16 and tuple(opts.mlp) == (128, 128)
         for _ in range(opts.critic_iters):
-            self.critic_opt.zero_grad(set_to_none=True)
+            self.critic_opt.zero_grad(set_to_none=not self._graph_mode)
             if fused:  # one kernel: forward + backward of the whole batch, grads into .grad
                 loss = value_fit_grad(self.value, X, y)
             else:
@@ -310,7 +383,7 @@ class ShortHorizonTrainer:
             allreduce_mean_(list(self.value.parameters()), self.group)
             clip_grads_(list(self.value.parameters()), opts.grad_clip)
             self.critic_opt.step()
-        return float(loss.detach())  # the last iteration's loss; one host sync per fit
+        return loss.detach()  # the last iteration's loss (device scalar)
 
 
 class PPOTrainer:
