@@ -563,7 +563,36 @@ def bench_c1(dev):
         e1.record()
         torch.cuda.synchronize()
         ag_us = e0.elapsed_time(e1) / 5 * 1e3
+        # (iv) the same user loop (env.step + torch.autograd.grad) captured in a
+        # CUDA graph by the caller; the env's functional state is carried
+        # through static buffers, as ShortHorizonTrainer(cuda_graph=True) does
+        a_static = acts.clone().requires_grad_(True)
+        carry = [env._S.detach().clone(), env._goal.clone(), env._peff.clone()]
+
+        def graph_window():
+            env._S, env._goal, env._peff = carry
+            tot = 0.0
+            for t in range(32):
+                tot = tot + env.step(a_static[t]).r_ctrl.mean() * 0.99 ** t
+            (g,) = torch.autograd.grad(-tot / 32, a_static)
+            carry[0].copy_(env._S.detach())
+            carry[1].copy_(env._goal)
+            carry[2].copy_(env._peff)
+            return g
+
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                graph_window()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            graph_window()
+        env._S, env._goal, env._peff = carry
+        agg_us = time_graph(gr.replay, 50) * 1e3
         out[model] = {"env_step_fwd_us": step_us, "bptt_window_fwd_bwd_us": win_us,
+                      "bptt_window_autograd_graph_us": agg_us,
                       "bptt_window_autograd_us": ag_us}
     return out
 
