@@ -17,7 +17,8 @@
 //   G3  dZ1 = (dZ2 W1^T)(1 - H1^2)      (128x128 @ 128x128)
 //   G4  dW1 += H1^T dZ2                 (warp w owns dW1 rows 16w..: 16x128, K = 128 rows)
 //   G5  dW0 += X^T dZ1                  (warp w owns dW0 cols 16w..: 16x16)
-// and the bias / w2 gradients as column sums.  Operands are bf16 in shared
+// The bias gradients are column sums taken by the same MMAs with an all-ones
+// A operand, and the w2 gradient dpred^T H2 by one more MMA per k-step.  Operands are bf16 in shared
 // memory (row stride padded by 8 elements: conflict-free ldmatrix); the
 // accumulators, biases and all gradients are fp32.
 #include <cuda_bf16.h>
@@ -40,8 +41,9 @@ struct MlpSmem {
   __nv_bfloat16 H1[TILE][LDH];
   __nv_bfloat16 D2[TILE][LDH];
   __nv_bfloat16 D1[TILE][LDH];
+  __nv_bfloat16 H2[TILE][LDH];
   float b0[HID], b1[HID], w2[HID];
-  float gb0[HID], gb1[HID], gw2[HID];
+  float dp[TILE];  // dL/dpred of the tile's rows
   float red[4];  // gb2, loss
 };
 
@@ -124,16 +126,24 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     S.b0[i] = b0[i];
     S.b1[i] = b1[i];
     S.w2[i] = w2[i];
-    S.gb0[i] = S.gb1[i] = S.gw2[i] = 0.f;
   }
   if (tid < 4) S.red[tid] = 0.f;
   const float bias2 = b2[0];
   float acc4[16][4];  // dW1 rows 16w.. x 128 cols, persistent over tiles
   float acc5[2][4];   // dW0 16 rows x cols 16w..16w+15
+  float accb1[2][4];  // db1, db0 for cols 16w..16w+15 (every row of the tile holds the sums)
+  float accb0[2][4];
+  float accw2[2][4];  // dw2 for cols 16w..16w+15
+  const uint32_t kOnes[4] = {0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u};  // bf16 1.0 pairs
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc4[j][0] = acc4[j][1] = acc4[j][2] = acc4[j][3] = 0.f;
 #pragma unroll
-  for (int j = 0; j < 2; ++j) acc5[j][0] = acc5[j][1] = acc5[j][2] = acc5[j][3] = 0.f;
+  for (int j = 0; j < 2; ++j) {
+    acc5[j][0] = acc5[j][1] = acc5[j][2] = acc5[j][3] = 0.f;
+    accb1[j][0] = accb1[j][1] = accb1[j][2] = accb1[j][3] = 0.f;
+    accb0[j][0] = accb0[j][1] = accb0[j][2] = accb0[j][3] = 0.f;
+    accw2[j][0] = accw2[j][1] = accw2[j][2] = accw2[j][3] = 0.f;
+  }
   __syncthreads();
   const int r0 = warp * 16;  // this warp's rows within a tile
   const int64_t ntiles = (M + TILE - 1) / TILE;
@@ -207,31 +217,22 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     const float e1 = rb < M ? p1 + bias2 - y[rb] : 0.f;
     const float d0 = 2.f * inv_m * e0, d1 = 2.f * inv_m * e1;  // dL/dpred
     float lsum = t4 == 0 ? e0 * e0 + e1 * e1 : 0.f, gb2s = t4 == 0 ? d0 + d1 : 0.f;
-    // dw2, db1 column partials over this thread's two rows; dZ2 -> D2
+    if (t4 == 0) {
+      S.dp[r0 + g] = d0;
+      S.dp[r0 + g + 8] = d1;
+    }
+    // H2 -> smem (for dw2 = H2^T dpred in G4); dZ2 -> D2
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       const int c = j * 8 + 2 * t4;
-      float gw_a = acc[j][0] * d0 + acc[j][2] * d1, gw_b = acc[j][1] * d0 + acc[j][3] * d1;
+      *reinterpret_cast<uint32_t*>(&S.H2[r0 + g][c]) = pack_bf16(acc[j][0], acc[j][1]);
+      *reinterpret_cast<uint32_t*>(&S.H2[r0 + g + 8][c]) = pack_bf16(acc[j][2], acc[j][3]);
       const float z00 = d0 * S.w2[c] * (1.f - acc[j][0] * acc[j][0]);
       const float z01 = d0 * S.w2[c + 1] * (1.f - acc[j][1] * acc[j][1]);
       const float z10 = d1 * S.w2[c] * (1.f - acc[j][2] * acc[j][2]);
       const float z11 = d1 * S.w2[c + 1] * (1.f - acc[j][3] * acc[j][3]);
       *reinterpret_cast<uint32_t*>(&S.D2[r0 + g][c]) = pack_bf16(z00, z01);
       *reinterpret_cast<uint32_t*>(&S.D2[r0 + g + 8][c]) = pack_bf16(z10, z11);
-      float gbs_a = z00 + z10, gbs_b = z01 + z11;
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {  // sum over the 8 row groups (lanes with the same t4)
-        gw_a += __shfl_xor_sync(0xffffffffu, gw_a, o);
-        gw_b += __shfl_xor_sync(0xffffffffu, gw_b, o);
-        gbs_a += __shfl_xor_sync(0xffffffffu, gbs_a, o);
-        gbs_b += __shfl_xor_sync(0xffffffffu, gbs_b, o);
-      }
-      if (g == 0) {
-        atomicAdd(&S.gw2[c], gw_a);
-        atomicAdd(&S.gw2[c + 1], gw_b);
-        atomicAdd(&S.gb1[c], gbs_a);
-        atomicAdd(&S.gb1[c + 1], gbs_b);
-      }
     }
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -267,16 +268,6 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       const float z10 = acc[j][2] * (1.f - h1.x * h1.x), z11 = acc[j][3] * (1.f - h1.y * h1.y);
       *reinterpret_cast<uint32_t*>(&S.D1[r0 + g][c]) = pack_bf16(z00, z01);
       *reinterpret_cast<uint32_t*>(&S.D1[r0 + g + 8][c]) = pack_bf16(z10, z11);
-      float ga = z00 + z10, gb = z01 + z11;
-#pragma unroll
-      for (int o = 4; o < 32; o <<= 1) {
-        ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        gb += __shfl_xor_sync(0xffffffffu, gb, o);
-      }
-      if (g == 0) {
-        atomicAdd(&S.gb0[c], ga);
-        atomicAdd(&S.gb0[c + 1], gb);
-      }
     }
     __syncthreads();  // H1, D2, D1, X of every row are in shared memory
     // ---- G4: dW1[16w.., :] += H1^T dZ2 (K = the tile's 128 rows)
@@ -290,7 +281,20 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
         ldsm4t(b, bt_addr<LDH>(&S.D2[0][0], k0, j * 8, lane));
         mma(acc4[j], a, b[0], b[1]);
         mma(acc4[j + 1], a, b[2], b[3]);
+        if (j == 2 * warp) {  // db1 = 1^T dZ2: an all-ones A on the same fragments
+          mma(accb1[0], kOnes, b[0], b[1]);
+          mma(accb1[1], kOnes, b[2], b[3]);
+        }
       }
+      // dw2 = dpred^T H2 for this warp's columns: A rows all = dpred (k = rows)
+      uint32_t ad[4], bh[4];
+      const uint32_t lo = pack_bf16(S.dp[k0 + 2 * t4], S.dp[k0 + 2 * t4 + 1]);
+      const uint32_t hi = pack_bf16(S.dp[k0 + 8 + 2 * t4], S.dp[k0 + 9 + 2 * t4]);
+      ad[0] = ad[1] = lo;
+      ad[2] = ad[3] = hi;
+      ldsm4t(bh, bt_addr<LDH>(&S.H2[0][0], k0, r0, lane));
+      mma(accw2[0], ad, bh[0], bh[1]);
+      mma(accw2[1], ad, bh[2], bh[3]);
     }
     // ---- G5: dW0[:, 16w..16w+15] += X^T dZ1
 #pragma unroll
@@ -300,6 +304,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       ldsm4t(b, bt_addr<LDH>(&S.D1[0][0], k0, r0, lane));
       mma(acc5[0], a, b[0], b[1]);
       mma(acc5[1], a, b[2], b[3]);
+      mma(accb0[0], kOnes, b[0], b[1]);  // db0 = 1^T dZ1 on the same fragments
+      mma(accb0[1], kOnes, b[2], b[3]);
     }
     __syncthreads();  // the next tile overwrites X, H1, D2, D1
   }
@@ -324,12 +330,19 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       atomicAdd(&gW0[(g + 8) * HID + c + 1], acc5[j][3]);
     }
   }
-  __syncthreads();
-  for (int i = tid; i < HID; i += blockDim.x) {
-    atomicAdd(&gb0[i], S.gb0[i]);
-    atomicAdd(&gb1[i], S.gb1[i]);
-    atomicAdd(&gw2[i], S.gw2[i]);
+  if (g == 0) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int c = r0 + j * 8 + 2 * t4;
+      atomicAdd(&gb1[c], accb1[j][0]);
+      atomicAdd(&gb1[c + 1], accb1[j][1]);
+      atomicAdd(&gb0[c], accb0[j][0]);
+      atomicAdd(&gb0[c + 1], accb0[j][1]);
+      atomicAdd(&gw2[c], accw2[j][0]);
+      atomicAdd(&gw2[c + 1], accw2[j][1]);
+    }
   }
+  __syncthreads();
   if (tid == 0) {
     atomicAdd(gb2, S.red[0]);
     atomicAdd(loss, S.red[1] * inv_m);
