@@ -41,6 +41,37 @@ def _xavier(rng, n_in, n_out, scale=1.0):  # q/nets.py:64-66
     return rng.normal(scale=s, size=(n_in, n_out))
 
 
+class _LinearFn(torch.autograd.Function):
+    """x W + b whose bias gradient is a (1 x M) @ (M x n) GEMM.  torch's own
+    addmm backward reduces the bias gradient with a generic column-reduction
+    kernel that runs at ~0.2 TB/s on the learners' tall (131,072 x 128) bf16
+    gradients -- a quarter of a C5 update's GPU time (profiles/README.md)."""
+
+    @staticmethod
+    def forward(ctx, x, W, b):
+        ctx.save_for_backward(x, W)
+        return torch.addmm(b, x, W)
+
+    @staticmethod
+    def backward(ctx, g):
+        x, W = ctx.saved_tensors
+        g = g.contiguous()
+        gx = g @ W.t() if ctx.needs_input_grad[0] else None
+        gW = x.t() @ g if ctx.needs_input_grad[1] else None
+        gb = None
+        if ctx.needs_input_grad[2]:
+            gb = (torch.ones(1, g.shape[0], dtype=g.dtype, device=g.device) @ g)[0]
+        return gx, gW, gb
+
+
+def _linear(x, W, b):
+    if torch.is_autocast_enabled(x.device.type) and x.is_cuda:
+        dt = torch.get_autocast_dtype("cuda")
+        with torch.autocast("cuda", enabled=False):
+            return _LinearFn.apply(x.to(dt), W.to(dt), b.to(dt))
+    return _LinearFn.apply(x, W.to(x.dtype), b.to(x.dtype))
+
+
 class Linear(torch.nn.Module):
     """y = x W + b with W (n_in, n_out) (q/nets.py:73-82); ``tag`` is the
     container's activation tag."""
@@ -53,7 +84,7 @@ class Linear(torch.nn.Module):
         self.tag = tag
 
     def forward(self, x):
-        return torch.addmm(self.b.to(x.dtype), x, self.W.to(x.dtype)) if x.dim() == 2 else x @ self.W + self.b
+        return _linear(x, self.W, self.b) if x.dim() == 2 else x @ self.W + self.b
 
 
 class MLP(torch.nn.Module):
@@ -92,10 +123,18 @@ class GRUCell(torch.nn.Module):
         self.n_hidden = H
 
     def forward(self, x, h):
-        # torch's fused GRU cell takes (3H, n_in) weights with the same gate order
-        if x.is_cuda or x.dtype == torch.float32:
-            return torch._VF.gru_cell(x, h, self.Wi.t().to(x.dtype), self.Wh.t().to(x.dtype),
-                                      self.bi.to(x.dtype), self.bh.to(x.dtype))
+        if x.is_cuda:
+            # gate GEMMs through _linear (input padded to a multiple of 16
+            # features: cuBLAS picks slow legacy kernels for K = 9), then torch's
+            # fused gate kernel, which has the same (r, z, n) equations
+            pad = (-x.shape[1]) % 16
+            xp = torch.nn.functional.pad(x, (0, pad)) if pad else x
+            Wi = torch.nn.functional.pad(self.Wi, (0, 0, 0, pad)) if pad else self.Wi
+            gi = _linear(xp, Wi, self.bi)
+            gh = _linear(h.to(gi.dtype) if gi.dtype != h.dtype else h, self.Wh, self.bh)
+            return torch.ops.aten._thnn_fused_gru_cell(gi, gh, h.to(gi.dtype))[0]
+        if x.dtype == torch.float32:
+            return torch._VF.gru_cell(x, h, self.Wi.t(), self.Wh.t(), self.bi, self.bh)
         H = self.n_hidden
         gi = x @ self.Wi + self.bi
         gh = h @ self.Wh + self.bh
