@@ -240,7 +240,18 @@ class PolicyNet(torch.nn.Module):
             h = self.gru(x, h.to(x.dtype)).float() if x.dtype != torch.float64 else self.gru(x, h)
             x = h.to(x.dtype)
         z = torch.tanh(self.trunk(x))
-        mu, ls = self.mu(z), self.sig(z)
+        if z.is_cuda and z.dim() == 2:
+            # both heads as ONE GEMM, widened to a multiple of 8 outputs (the
+            # narrow N = A GEMMs, and their weight-gradient GEMMs with N = A,
+            # fall to slow unaligned kernels)
+            A = self.arch.action_dim
+            pad = (-2 * A) % 8
+            W = torch.nn.functional.pad(torch.cat([self.mu.W, self.sig.W], 1), (0, pad))
+            b = torch.nn.functional.pad(torch.cat([self.mu.b, self.sig.b]), (0, pad))
+            y = _linear(z, W, b)
+            mu, ls = y[:, :A], y[:, A:2 * A]
+        else:
+            mu, ls = self.mu(z), self.sig(z)
         out_t = torch.float64 if z.dtype == torch.float64 else torch.float32
         return mu.to(out_t), torch.clamp(ls.to(out_t), LOG_SIGMA_MIN, self.arch.log_sigma_max), h
 

@@ -214,3 +214,36 @@ def test_cuda_graph_updates_match_eager():
     same_clock = (trs[0].env._meta[:, :3] == trs[1].env._meta[:, :3]).all(-1).float().mean()
     assert float(same_clock) > 0.99  # episode step / episode index / tick per env
     assert trs[1]._graph is not None and trs[1].update_count == 7
+
+
+def test_policy_cuda_path_matches_reference_forward():
+    """The CUDA forward (GRU gate GEMMs on padded inputs + fused gate kernel,
+    both heads as one widened GEMM, conv encoder) reproduces the reference's
+    forward from its container, in fp32 without autocast, and its gradients
+    match the CPU fp64 path."""
+    import os
+
+    from golden_utils import GOLDEN, load
+    from paper_2509_10247_b200 import nets
+
+    z = load("nets_ppo")
+    sets, _ = nets.read_container(os.path.join(GOLDEN, "nets_container"))
+    arch = nets.PolicyArch(proprio_dim=9, action_dim=3,
+                           visual={"kind": "depth", "height": 12, "width": 16, "max_range": 10.0},
+                           recurrent=True, hidden=16, mlp=(32, 32), conv_feat=8,
+                           input_scale=tuple(np.linspace(0.2, 1.0, 9)))
+    pol = nets.PolicyNet(arch).cuda()
+    nets.load_into(pol, sets["policy"])
+    t = lambda k: torch.as_tensor(z[k], dtype=torch.float32, device="cuda")  # noqa: E731
+    mu, ls, h1 = pol(t("d_pro"), t("d_img"), t("d_h0"))
+    np.testing.assert_allclose(mu.detach().cpu().numpy(), z["d_mu"], rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(ls.detach().cpu().numpy(), z["d_ls"], rtol=1e-4, atol=1e-5)
+    np.testing.assert_allclose(h1.detach().cpu().numpy(), z["d_h1"], rtol=1e-4, atol=1e-5)
+    (mu.sum() + ls.sum() + h1.sum()).backward()
+    ref = nets.PolicyNet(arch).double()
+    nets.load_into(ref, sets["policy"])
+    d = lambda k: torch.as_tensor(z[k])  # noqa: E731
+    mu2, ls2, h2 = ref(d("d_pro"), d("d_img"), d("d_h0"))
+    (mu2.sum() + ls2.sum() + h2.sum()).backward()
+    for (name, (p, _)), (_, (q, _)) in zip(nets.ref_params(pol).items(), nets.ref_params(ref).items()):
+        np.testing.assert_allclose(p.grad.cpu().numpy(), q.grad.numpy(), rtol=2e-3, atol=2e-5, err_msg=name)
