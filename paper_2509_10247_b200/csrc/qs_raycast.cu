@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
       if (i < sv.ns) {
         float4 sp = ld4(sv.sph, i);
         V3 c = xyz(sp);
-        keep = !(rc.cull & 1) || keep_ball(rc, o, c, sp.w);
+        keep = !(rc.cull & 1) || (KIND == 0 ? keep_camera(rc, cs, o, c, sp.w) : keep_ball(rc, o, c, sp.w));
         q0 = f4(o - c, sp.w * sp.w);
         q1 = make_float4(0.f, 0.f, 0.f, 0.f);
         bs = bsphere(c - o, sp.w, ee);
@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
         int j = i - sv.ns;
         float4 c = ld4(sv.box, 2 * j), h = ld4(sv.box, 2 * j + 1);
         float rad = norm3(xyz(h));
-        keep = !(rc.cull & 1) || keep_ball(rc, o, xyz(c), rad);
+        keep = !(rc.cull & 1) || (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
         q0 = f4(xyz(c) - xyz(h) - o, 0.f);
         q1 = f4(xyz(c) + xyz(h) - o, 0.f);
         bs = bsphere(xyz(c) - o, rad, ee);
@@ -561,7 +561,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
         float4 c = ld4(sv.cyl, 2 * j);
         float hh = __ldg(sv.cyl + 8 * j + 4);
         float rad = sqrtf(c.w * c.w + hh * hh);
-        keep = !(rc.cull & 1) || keep_ball(rc, o, xyz(c), rad);
+        keep = !(rc.cull & 1) || (KIND == 0 ? keep_camera(rc, cs, o, xyz(c), rad) : keep_ball(rc, o, xyz(c), rad));
         q0 = make_float4(o.x - c.x, o.y - c.y, o.z - c.z, c.w * c.w);
         q1 = make_float4(hh, hh - (o.z - c.z), -hh - (o.z - c.z), 0.f);  // cap planes relative to o
         bs = bsphere(xyz(c) - o, rad, ee);
