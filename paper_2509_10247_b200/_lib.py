@@ -180,6 +180,12 @@ def check(status: int, what: str):
         raise QuadsimLibraryError(f"{what} failed with status {status}")
 
 
+def tensor_device(x):
+    """The device of a torch tensor, None otherwise (numpy >= 2 arrays carry a
+    ``.device`` of their own, "cpu", which must not pick the device)."""
+    return x.device if isinstance(x, torch.Tensor) else None
+
+
 def require_cuda(device) -> torch.device:
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device()) \
         if torch.cuda.is_available() else None

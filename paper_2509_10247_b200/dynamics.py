@@ -430,3 +430,48 @@ def rollout_grad(model: DynamicsModel, state0: QuadState, raw_actions, t1: int, 
     if g is None:
         return RolloutGrad(torch.zeros_like(leaves[t1]), True)
     return RolloutGrad(g, False)
+
+
+# ---------------------------------------------------------------------------
+# the reference's functional step API (q/dynamics.py:155-274): thin wrappers
+# over the same kernels as DynamicsModel.step; commands are already squashed
+
+
+def _functional_step(name, state, act, params):
+    dev = act.device if isinstance(act, torch.Tensor) else None
+    return make_model(name, params, device=dev).step(state, act)
+
+
+def step_full(state: QuadState, thrust, w_cmd, params: QuadParams) -> QuadState:
+    """q/dynamics.py:155-186: collective thrust (B,) and body-rate command (B,3)."""
+    th = torch.as_tensor(thrust, dtype=torch.float32).reshape(-1, 1)
+    w = torch.as_tensor(w_cmd, dtype=torch.float32).reshape(-1, 3)
+    return _functional_step("full", state, torch.cat([th.to(w.device), w], -1), params)
+
+
+def step_simplified(state: QuadState, thrust, w, params: QuadParams) -> QuadState:
+    """q/dynamics.py:203-234."""
+    th = torch.as_tensor(thrust, dtype=torch.float32).reshape(-1, 1)
+    w = torch.as_tensor(w, dtype=torch.float32).reshape(-1, 3)
+    return _functional_step("simplified", state, torch.cat([th.to(w.device), w], -1), params)
+
+
+def step_pm_continuous(state: QuadState, u, params: QuadParams) -> QuadState:
+    """q/dynamics.py:237-258 (u: world-frame commanded acceleration (B,3))."""
+    return _functional_step("pm_continuous", state, u, params)
+
+
+def step_pm_discrete(state: QuadState, u, params: QuadParams) -> QuadState:
+    """q/dynamics.py:261-274."""
+    return _functional_step("pm_discrete", state, u, params)
+
+
+def quat_to_matrix_np(q: np.ndarray) -> np.ndarray:
+    """q/dynamics.py:448-460: (w, x, y, z) unit quaternions (B,4) -> (B,3,3) (host helper)."""
+    q = np.asarray(q, dtype=np.float64)
+    w, x, y, z = q[..., 0], q[..., 1], q[..., 2], q[..., 3]
+    return np.stack([
+        np.stack([1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)], -1),
+        np.stack([2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)], -1),
+        np.stack([2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], -1),
+    ], -2)

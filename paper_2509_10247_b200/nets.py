@@ -395,6 +395,9 @@ def read_container(dirpath: str):
     return sets, manifest
 
 
+load_container = read_container  # q/nets.py:348 name; arrays in place of ParamSets
+
+
 def load_into(module: torch.nn.Module, arrays: dict) -> None:
     """Copy one container set into a PolicyNet / ValueNet (names and shapes
     must match the module's architecture)."""

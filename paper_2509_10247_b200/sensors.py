@@ -405,7 +405,7 @@ TILE_WIDTH = int(os.environ.get("QS_TILE_WIDTH", "0"))
 
 def raycast(prims, origins, dirs, max_range: float, chunk_elems: int = 0, device=None):
     """Nearest-hit distance (B,R) for unit rays, clamped (q/sensors.py:245-269)."""
-    dev = L.require_cuda(device if device is not None else getattr(origins, "device", None))
+    dev = L.require_cuda(device if device is not None else L.tensor_device(origins))
     sc = as_device_scene(prims, dev)
     o = _pos4(_t(origins, dev).reshape(-1, 3))
     d = _t(dirs, dev)
@@ -421,7 +421,7 @@ def raycast(prims, origins, dirs, max_range: float, chunk_elems: int = 0, device
 
 
 def _render(prims, body_pos, body_R, sensor, kind, cull, device):
-    dev = L.require_cuda(device if device is not None else getattr(body_pos, "device", None))
+    dev = L.require_cuda(device if device is not None else L.tensor_device(body_pos))
     sc = as_device_scene(prims, dev)
     pos = _pos4(_t(body_pos, dev).reshape(-1, 3))
     R = _t(body_R, dev)
@@ -451,7 +451,7 @@ def render_lidar(prims, body_pos, body_R, pattern: LidarPattern, device=None):
 
 def fov_cull(prims, cam_pos, cam_R, intrinsics: CameraIntrinsics):
     """Conservative frustum keep-masks (q/sensors.py:338-374), on device."""
-    dev = L.require_cuda(getattr(cam_pos, "device", None))
+    dev = L.require_cuda(L.tensor_device(cam_pos))
     th = np.tan(intrinsics.fov_h / 2)
     tv = np.tan(intrinsics.fov_v / 2)
     n = np.array([[th, -1.0, 0.0], [th, 1.0, 0.0], [tv, 0.0, -1.0], [tv, 0.0, 1.0], [1.0, 0.0, 0.0]])
@@ -534,7 +534,7 @@ def _sdf_launch(sc: DeviceScene, p: torch.Tensor, n_agents: int, grad: bool):
 
 def sdf_np(points, prims, n_agents: int = 1, device=None):
     """Signed distance (B,) to the nearest surface; FAR when the scene is empty."""
-    dev = L.require_cuda(device if device is not None else getattr(points, "device", None))
+    dev = L.require_cuda(device if device is not None else L.tensor_device(points))
     sc = as_device_scene(prims, dev)
     out, _ = _sdf_launch(sc, _t(points, dev).reshape(-1, 3), n_agents, False)
     return out
@@ -634,7 +634,7 @@ def ema_update(v_ema, v, alpha: float):
 
 def reconstruct_attitude(a_thrust, v_ema, device=None):
     """(B,3,3) attitude with columns (x_b, y_b, z_b) (q/sensors.py:569-606)."""
-    dev = L.require_cuda(device if device is not None else getattr(a_thrust, "device", None))
+    dev = L.require_cuda(device if device is not None else L.tensor_device(a_thrust))
     a = _pos4(_t(a_thrust, dev).reshape(-1, 3))
     ve = _pos4(_t(v_ema, dev).reshape(-1, 3))
     B = a.shape[0]
@@ -680,3 +680,24 @@ def read_depth_dump(path):
     if data.size != w * h:
         raise SensorContractError(f"truncated depth dump: {path}")
     return data.reshape(h, w), idx
+
+
+def ray_primitive(origin, direction, prim):
+    """q/sensors.py:219-242: smallest t >= 0 of one unit ray against one
+    primitive ("sphere", (4,)) | ("box", (6,)) | ("cylinder", (5,)) | ("ground", z),
+    or None -- through the same ray-cast kernel as every sensor."""
+    direction = np.asarray(direction, dtype=np.float64)
+    if abs(np.linalg.norm(direction) - 1.0) > 1e-9:
+        raise SensorContractError("ray direction must be unit-norm")
+    kind, data = prim
+    if kind not in ("sphere", "box", "cylinder", "ground"):
+        raise SensorContractError(f"unknown primitive kind '{kind}'")
+    ps = PrimitiveSet(spheres=data if kind == "sphere" else np.zeros((0, 4)),
+                      boxes=data if kind == "box" else np.zeros((0, 6)),
+                      cylinders=data if kind == "cylinder" else np.zeros((0, 5)),
+                      ground_z=float(data) if kind == "ground" else None)
+    big = 1e30
+    t = raycast(pack_primitives([ps]), np.asarray(origin, dtype=np.float64)[None, :],
+                direction[None, None, :], big, device=L.require_cuda(None))
+    v = float(t.reshape(-1)[0])
+    return None if v >= big else v

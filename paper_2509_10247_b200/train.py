@@ -511,3 +511,57 @@ def make_learner(env, opts: LearnerOptions, group=None):
     if opts.algo == "ppo":
         return PPOTrainer(env, opts, group)
     raise ValueError(f"unknown algorithm '{opts.algo}'; choose from ('bptt', 'shac', 'sha2c', 'ppo')")
+
+
+# ---------------------------------------------------------------------------
+# the reference's learner names (q/learners.py:63-71, 248-324, 494-527)
+
+ALGOS = ("bptt", "shac", "sha2c", "ppo")
+
+
+def _preset(algo):
+    class _Learner(ShortHorizonTrainer):
+        def __init__(self, env, opts: LearnerOptions = LearnerOptions(), group=None):
+            from dataclasses import replace
+
+            super().__init__(env, replace(opts, algo=algo), group)
+
+    _Learner.__name__ = _Learner.__qualname__ = algo.upper()
+    return _Learner
+
+
+BPTT, SHAC, SHA2C = _preset("bptt"), _preset("shac"), _preset("sha2c")
+PPO = PPOTrainer
+
+
+def wilson_interval(successes: int, n: int, z: float = 1.96):
+    """q/learners.py:494-501."""
+    if n == 0:
+        return (0.0, 1.0)
+    p = successes / n
+    denom = 1 + z * z / n
+    center = (p + z * z / (2 * n)) / denom
+    spread = z * np.sqrt(p * (1 - p) / n + z * z / (4 * n * n)) / denom
+    return (max(0.0, center - spread), min(1.0, center + spread))
+
+
+@torch.no_grad()
+def evaluate(env, policy, n_episodes: int, seed: int, max_steps: int | None = None) -> dict:
+    """Greedy (mean-action) rollouts until n_episodes finish (q/learners.py:504-527)."""
+    out = env.reset(seed)
+    env.reset_stats()
+    hidden = policy.initial_hidden(env.N, env.device)
+    obs = out.obs
+    cap = max_steps or (env.config.episode_len * (n_episodes // env.n_envs + 2) * 2)
+    steps = 0
+    while env.finished_episodes < n_episodes and steps < cap:
+        mu, _s, h2 = policy(obs.proprio, obs.visual, hidden)
+        res = env.step(mu)
+        if hidden is not None:
+            hidden = torch.where(res.done[:, None], torch.zeros_like(h2), h2.float())
+        obs = res.obs
+        steps += 1
+    lo, hi = wilson_interval(env.successful_episodes, env.finished_episodes)
+    return {"episodes": env.finished_episodes, "success_rate": env.success_rate,
+            "collision_rate": env.collision_rate, "mean_episode_reward": env.mean_episode_return,
+            "success_ci95": (lo, hi), "steps": steps}

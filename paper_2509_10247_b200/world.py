@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 from paper_2509_10247_b200 import _lib as L
-from paper_2509_10247_b200.sensors import DeviceScene, PrimitiveSet
+from paper_2509_10247_b200.sensors import DeviceScene, PrimitiveSet, pack_primitives  # noqa: F401
 
 SCENE_FORMAT_VERSION = 1
 SPHERE_R = (0.3, 1.0)  # q/world.py:21-24
@@ -263,3 +263,20 @@ def scenes_to_device(scenes: list, device, n_gates: int = 0) -> DeviceScene:
                 gt[e, k, 4:7], gt[e, k, 7] = g.normal, g.frame_width
         sc.gates.copy_(torch.as_tensor(gt, dtype=torch.float32))
     return sc
+
+
+def sdf_np_all(points, prims):
+    """q/world.py:182-196: signed distance of many points to ONE packed scene
+    (every point is a row of that scene's single env)."""
+    from paper_2509_10247_b200 import sensors as sn
+
+    pts = np.atleast_2d(np.asarray(points, dtype=np.float64)) if not isinstance(points, torch.Tensor) else points
+    n = pts.shape[0]
+    if getattr(prims, "batch", 1) != 1:
+        raise GenerationError("sdf_np_all expects a single-scene pack")
+    return sn.sdf_np(pts, prims, n_agents=n)
+
+
+def scene_sdf(scene: "Scene", points):
+    """q/world.py:199-200."""
+    return sdf_np_all(points, pack_primitives([scene.prims]))

@@ -143,3 +143,12 @@ def test_c5_policy_has_the_reference_parameter_count():
     # privileged state: 14 features (q/tasks.py:465-545)
     val = nets.ValueNet(14, rng)
     assert val.n_params() == 18561
+
+
+def test_quat_to_matrix_np_matches_oracle():
+    from oracle import quadsim_oracle as O
+    from paper_2509_10247_b200 import dynamics as dyn
+
+    q = np.random.default_rng(1).normal(size=(16, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    np.testing.assert_allclose(dyn.quat_to_matrix_np(q), O.quat_to_matrix(q), rtol=1e-14, atol=1e-14)
