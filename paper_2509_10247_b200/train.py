@@ -291,9 +291,12 @@ class ShortHorizonTrainer:
     def update(self) -> dict:
         opts = self.opts
         t0 = time.perf_counter()
+        if self._graph is not None and any(a is not b for a, b in zip(self._env_bufs, self._env_buffers())):
+            self._graph = None  # env.reset() re-allocated the buffers the graph points at
         if self._graph_mode and self._graph is None and self._warm >= 3:
             self._capture()  # records only: this call's update is the first replay
         if self._graph is not None:
+            self._sync_carry()
             self._graph.replay()
             loss, gnorm, closs = self._graph_out
         elif self._graph_mode:  # the eager warm-up updates torch asks for, on a side stream
@@ -314,6 +317,31 @@ class ShortHorizonTrainer:
         self.timing["sim_fwd_bwd_s"] += time.perf_counter() - t0
         out["steps_per_sec"] = opts.horizon * self.env.N / (time.perf_counter() - t0)
         return out
+
+    def _env_buffers(self):
+        """The env objects a captured update holds pointers to (reset() replaces them)."""
+        e = self.env
+        return (e._meta, e._ep_ret, e._stats, e._err, e._imu_bias, e._scene, e._cfg)
+
+    def _sync_carry(self):
+        """The env was reset or stepped outside the graph since the last replay
+        (e.g. by evaluate()): load its current state into the graph's carry
+        buffers and rebind."""
+        env, c = self.env, self._carry
+        if env._S is c["S"] and (c["hidden"] is None or self.hidden is c["hidden"]):
+            return
+        c["S"].copy_(env._S.detach())
+        c["goal"].copy_(env._goal)
+        c["peff"].copy_(env._peff)
+        if c["dr"] is not None:
+            c["dr"].copy_(env._dr)
+        if c["hidden"] is not None and self.hidden is not c["hidden"]:
+            c["hidden"].copy_(self.hidden)
+        env._S, env._goal, env._peff = c["S"], c["goal"], c["peff"]
+        if c["dr"] is not None:
+            env._dr = c["dr"]
+        if c["hidden"] is not None:
+            self.hidden = c["hidden"]
 
     def _capture(self):
         """Record one whole update into a CUDA graph (torch's whole-network
@@ -358,6 +386,7 @@ class ShortHorizonTrainer:
         bind()
         self._graph, self._graph_out = g, out
         self._carry = carry
+        self._env_bufs = self._env_buffers()
 
     def _critic_update(self, r, dones, priv):
         """TD-lambda targets + full-batch MSE fit (q/learners.py:232-245, 286-292)."""
