@@ -153,12 +153,26 @@ class BpttWindow:
         for dst, src in zip(live, snap):
             dst.copy_(src)
         self.graph = g
+        self._env_bufs = self._env_buffers()
         return self
+
+    def _env_buffers(self):
+        """The env objects a captured window points at; env.reset() replaces them."""
+        e = self.env
+        return (e._meta, e._ep_ret, e._stats, e._err, e._imu_bias, e._scene, e._cfg)
+
+    def _stale(self) -> bool:
+        return any(a is not b for a, b in zip(getattr(self, "_env_bufs", ()), self._env_buffers()))
 
     def run(self, actions: torch.Tensor | None = None):
         """One window (fwd + bwd).  Returns (loss tensor, dL/d actions (T,N,A))."""
         if actions is not None:
             self.actions.copy_(actions, non_blocking=True)
+        if self.graph is not None and self._stale():  # the env was reset since the capture
+            self._load_env_state()
+            self.graph = None
+            self._pipe = None
+            self.capture()
         if self.graph is not None:
             self.graph.replay()
         else:

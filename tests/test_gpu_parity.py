@@ -454,3 +454,30 @@ def test_window_ragged_batch_matches_autograd_path(qs, n_envs):
     win.sync_env()
     assert torch.allclose(e1._S, e2._S.detach(), rtol=1e-6, atol=1e-6)
     assert torch.equal(e1._meta, e2._meta)
+
+
+def test_window_graph_survives_env_reset(qs):
+    """A captured BpttWindow whose env is reset re-loads the env's state and
+    re-captures instead of replaying stale pointers; the result equals a fresh
+    window on the reset env."""
+    from paper_2509_10247_b200.window import BpttWindow
+
+    cfg = qs.TaskConfig(task="position", dynamics="full", n_envs=1024, episode_len=20,
+                        imu=qs.ImuSpec(0.1, 0.01, 0.01, 0.001))
+    env = qs.make_task(cfg, strict=False)
+    env.reset(seed=3)
+    acts = torch.randn(8, env.N, 4, generator=torch.Generator().manual_seed(1)).cuda() * 0.3
+    win = BpttWindow(env, 8)
+    win.actions.copy_(acts)
+    win.capture()
+    win.run()
+    env.reset(seed=4)
+    loss_a, g_a = win.run()
+    loss_a, g_a = float(loss_a), g_a.clone()
+    env2 = qs.make_task(cfg, strict=False)
+    env2.reset(seed=4)
+    win2 = BpttWindow(env2, 8)
+    win2.actions.copy_(acts)
+    loss_b, g_b = win2.run()
+    assert abs(loss_a - float(loss_b)) < 1e-9 * abs(float(loss_b))
+    assert torch.equal(g_a, g_b)
