@@ -412,6 +412,36 @@ def bench_c3_env(dev, steps=20):
             "n_envs": E, "api": "FlightTask.step (no grad): fused step kernel + depth render per step"}
 
 
+def bench_scene_gen(dev):
+    """Obstacle-course generation (resets / re-randomisation):
+    16,384 courses of the C3 distribution per launch, each with its
+    feasibility BFS on the 0.25 m occupancy grid, outdoor and indoor (the
+    reference: 52 / 31 scenes/s).  Timed on the device."""
+    import torch
+
+    from paper_2509_10247_b200 import world as wd
+
+    E = 16384
+    out = {}
+    for style in ("outdoor", "indoor"):
+        def gen(seed=[100]):
+            seed[0] += 1
+            return wd.gen_obstacle_courses(seed[0], E, [0.0, 0.0, 1.2], [8.0, 0.0, 1.5], 32 / 48.0, style=style,
+                                           device=dev, check=False)
+
+        gen()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            gen()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        out[style] = {"ms_per_batch": ms, "scenes_per_s": E / (ms * 1e-3), "n_envs": E}
+    return out
+
+
 def measure_fp32_peak(dev):
     """FFMA and FFMA2 throughput on this GPU (qs_probe_fp32): the measured FP32
     denominator BASELINE.md §3 asks for.  Full occupancy (8 x 256 threads per
@@ -757,6 +787,7 @@ def run_ours(a):
     c1 = bench_c1(dev) if rank == 0 and not a.no_depth else None
     c4 = bench_c4(dev) if rank == 0 and not a.no_depth else None
     c3_env = bench_c3_env(dev) if rank == 0 and not a.no_depth else None
+    scene_gen = bench_scene_gen(dev) if rank == 0 and not a.no_depth else None
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -796,6 +827,7 @@ def run_ours(a):
         "c1_latency": c1,
         "c4": c4,
         "c3_env": c3_env,
+        "scene_gen": scene_gen,
         "loss": loss,
     }
     print(json.dumps(line))
