@@ -76,6 +76,21 @@ QS_D uint32_t bits_at(const uint32_t* a, long nbits, long pos) {
   return out;
 }
 
+// bits of the cell range [a, b] within the 32 cells [i0, i0 + 31]
+QS_D uint32_t span_mask(long a, long b, long i0) {
+  const long lo = a > i0 ? a : i0, hi = b < i0 + 31 ? b : i0 + 31;
+  if (lo > hi) return 0u;
+  const int s = (int)(lo - i0), t = (int)(hi - i0);
+  const uint32_t upto = t == 31 ? 0xffffffffu : ((1u << (t + 1)) - 1u);
+  return upto & ~((1u << s) - 1u);
+}
+// bits b of the word at i0 whose cell i = i0 + b has (i mod period) in [r0, r1]
+QS_D uint32_t periodic_mask(long i0, long period, long r0, long r1) {
+  uint32_t m = 0u;
+  for (long k = (i0 / period) * period; k <= i0 + 31; k += period) m |= span_mask(k + r0, k + r1, i0);
+  return m;
+}
+
 __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_envs, float* bounds,
                                                    float* spawn_goal, float* spheres, float* boxes,
                                                    float* cylinders, int32_t* counts, float* ground_z,
@@ -180,25 +195,66 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
     }
     __syncthreads();
     const int ns = s_cnt[0], nb = s_cnt[1], nc = s_cnt[2];
-    // ---- occupancy: free iff sdf(cell centre) > r_quad + 0.05 (ground at z=0)
+    // ---- occupancy: free iff sdf(cell centre) > r_quad + 0.05 (ground at z=0).
+    // The ground rule fills the bitmap; then every obstacle blocks the cells of
+    // its thr-inflated bounding box whose centre lies within thr of it.  Blocked
+    // iff some distance <= thr is exactly "min over all distances <= thr" (each
+    // distance is the same fp32 value as in a full min), at ~1% of the work.
     const float thr = cfg.r_quad + 0.05f;
+    auto centre = [&](int ix, int iy, int iz) {
+      return v3(F.lo.x + (ix + 0.5f) * (F.hi.x - F.lo.x) / F.dims[0],
+                F.lo.y + (iy + 0.5f) * (F.hi.y - F.lo.y) / F.dims[1],
+                F.lo.z + (iz + 0.5f) * (F.hi.z - F.lo.z) / F.dims[2]);
+    };
     for (long wi = threadIdx.x; wi < nw; wi += blockDim.x) {
       uint32_t word = 0;
       for (int b = 0; b < 32; ++b) {
         long i = wi * 32 + b;
         if (i >= cells) break;
-        int iz = (int)(i % nz), iy = (int)((i / nz) % ny), ix = (int)(i / ((long)nz * ny));
-        V3 p = v3(F.lo.x + (ix + 0.5f) * (F.hi.x - F.lo.x) / F.dims[0],
-                  F.lo.y + (iy + 0.5f) * (F.hi.y - F.lo.y) / F.dims[1],
-                  F.lo.z + (iz + 0.5f) * (F.hi.z - F.lo.z) / F.dims[2]);
-        float best = p.z;  // ground z = 0
-        for (int q = 0; q < ns; ++q) best = fminf(best, norm3(p - xyz(s_sph[q])) - s_sph[q].w);
-        for (int q = 0; q < nb; ++q) best = fminf(best, sdf_box(p, s_box[2 * q], s_box[2 * q + 1]));
-        for (int q = 0; q < nc; ++q) best = fminf(best, sdf_cyl(p, s_cyl[q], s_cyl_hh[q]));
-        if (best > thr) word |= 1u << b;
+        const int iz = (int)(i % nz);
+        if (F.lo.z + (iz + 0.5f) * (F.hi.z - F.lo.z) / F.dims[2] > thr) word |= 1u << b;
       }
       freeb[wi] = word;
       vis[wi] = 0u;
+    }
+    __syncthreads();
+    const int n_obs = ns + nb + nc;
+    for (int q = 0; q < n_obs; ++q) {
+      V3 c, ext;  // centre and thr-inflated half-extent of the obstacle's box
+      if (q < ns) {
+        c = xyz(s_sph[q]);
+        ext = v3(s_sph[q].w, s_sph[q].w, s_sph[q].w);
+      } else if (q < ns + nb) {
+        c = xyz(s_box[2 * (q - ns)]);
+        ext = xyz(s_box[2 * (q - ns) + 1]);
+      } else {
+        c = xyz(s_cyl[q - ns - nb]);
+        ext = v3(s_cyl[q - ns - nb].w, s_cyl[q - ns - nb].w, s_cyl_hh[q - ns - nb]);
+      }
+      int lo_i[3], n_i[3];
+      const float clo[3] = {F.lo.x, F.lo.y, F.lo.z}, chi[3] = {F.hi.x, F.hi.y, F.hi.z};
+      const float cc[3] = {c.x, c.y, c.z}, ee[3] = {ext.x + thr, ext.y + thr, ext.z + thr};
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {  // cell index range, one cell of slack each side
+        const float inv = F.dims[a] / (chi[a] - clo[a]);
+        const int i0 = max(0, (int)floorf((cc[a] - ee[a] - clo[a]) * inv - 0.5f) - 1);
+        const int i1 = min(F.dims[a] - 1, (int)ceilf((cc[a] + ee[a] - clo[a]) * inv - 0.5f) + 1);
+        lo_i[a] = i0;
+        n_i[a] = max(0, i1 - i0 + 1);
+      }
+      const int tot = n_i[0] * n_i[1] * n_i[2];
+      for (int k = threadIdx.x; k < tot; k += blockDim.x) {
+        const int iz = lo_i[2] + k % n_i[2], iy = lo_i[1] + (k / n_i[2]) % n_i[1], ix = lo_i[0] + k / (n_i[2] * n_i[1]);
+        const V3 p = centre(ix, iy, iz);
+        float d;
+        if (q < ns) d = norm3(p - xyz(s_sph[q])) - s_sph[q].w;
+        else if (q < ns + nb) d = sdf_box(p, s_box[2 * (q - ns)], s_box[2 * (q - ns) + 1]);
+        else d = sdf_cyl(p, s_cyl[q - ns - nb], s_cyl_hh[q - ns - nb]);
+        if (!(d > thr)) {
+          const long i = ((long)ix * ny + iy) * nz + iz;
+          atomicAnd(&freeb[i >> 5], ~(1u << (i & 31)));
+        }
+      }
     }
     __syncthreads();
     auto cell_of = [&](V3 p) -> long {
@@ -225,17 +281,12 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
           uint32_t ym = bits_at(vis, cells, wi * 32 - nz), yp = bits_at(vis, cells, wi * 32 + nz);
           uint32_t xm = bits_at(vis, cells, wi * 32 - (long)ny * nz);
           uint32_t xp = bits_at(vis, cells, wi * 32 + (long)ny * nz);
-          // boundary masks: receive from iz-1 only if iz>0, etc.
-          uint32_t mzlo = 0, mzhi = 0, mylo = 0, myhi = 0;
-          for (int b = 0; b < 32; ++b) {
-            long i = wi * 32 + b;
-            if (i >= cells) break;
-            int iz = (int)(i % nz), iy = (int)((i / nz) % ny);
-            if (iz > 0) mzlo |= 1u << b;
-            if (iz < nz - 1) mzhi |= 1u << b;
-            if (iy > 0) mylo |= 1u << b;
-            if (iy < ny - 1) myhi |= 1u << b;
-          }
+          // boundary masks: receive from iz-1 only if iz>0, etc. (bits past
+          // `cells` are masked by freeb below)
+          const long i0 = wi * 32;
+          const uint32_t mzlo = ~periodic_mask(i0, nz, 0, 0), mzhi = ~periodic_mask(i0, nz, nz - 1, nz - 1);
+          const uint32_t mylo = ~periodic_mask(i0, (long)ny * nz, 0, nz - 1);
+          const uint32_t myhi = ~periodic_mask(i0, (long)ny * nz, (long)(ny - 1) * nz, (long)ny * nz - 1);
           g |= (zm & mzlo) | (zp & mzhi) | (ym & mylo) | (yp & myhi) | xm | xp;
           g &= freeb[wi];
           nxt[wi] = g;
