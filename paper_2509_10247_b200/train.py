@@ -60,7 +60,9 @@ class LearnerOptions:
     # bf16 critic fit through the fused forward+backward kernel (nets.value_fit_grad)
     fused_critic: bool = True
     # replay each whole update (rollout, BPTT backward, actor step, critic fit)
-    # from one CUDA graph (ShortHorizonTrainer; single-rank, no-sensor envs)
+    # from one CUDA graph (ShortHorizonTrainer; single-rank, no-sensor envs).
+    # The env's kernel configuration is frozen into the graph at capture; an
+    # env.reset() (new buffers) triggers a re-capture, other changes need one
     cuda_graph: bool = False
 
 
