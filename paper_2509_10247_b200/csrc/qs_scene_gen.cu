@@ -76,18 +76,19 @@ QS_D uint32_t bits_at(const uint32_t* a, long nbits, long pos) {
   return out;
 }
 
-// bits of the cell range [a, b] within the 32 cells [i0, i0 + 31]
-QS_D uint32_t span_mask(long a, long b, long i0) {
-  const long lo = a > i0 ? a : i0, hi = b < i0 + 31 ? b : i0 + 31;
-  if (lo > hi) return 0u;
-  const int s = (int)(lo - i0), t = (int)(hi - i0);
-  const uint32_t upto = t == 31 ? 0xffffffffu : ((1u << (t + 1)) - 1u);
-  return upto & ~((1u << s) - 1u);
+// bits [a, b] of a 32-bit word, clamped to [0, 31]
+QS_D uint32_t span32(int a, int b) {
+  a = a > 0 ? a : 0;
+  b = b < 31 ? b : 31;
+  if (a > b) return 0u;
+  const uint32_t upto = b == 31 ? 0xffffffffu : ((1u << (b + 1)) - 1u);
+  return upto & ~((1u << a) - 1u);
 }
-// bits b of the word at i0 whose cell i = i0 + b has (i mod period) in [r0, r1]
-QS_D uint32_t periodic_mask(long i0, long period, long r0, long r1) {
+// bits b of a word whose first cell has residue r (mod period) such that the
+// cell's residue (r + b) mod period lies in [r0, r1]
+QS_D uint32_t residue_mask(int r, int period, int r0, int r1) {
   uint32_t m = 0u;
-  for (long k = (i0 / period) * period; k <= i0 + 31; k += period) m |= span_mask(k + r0, k + r1, i0);
+  for (int s = -r; s < 32; s += period) m |= span32(s + r0, s + r1);
   return m;
 }
 
@@ -113,6 +114,9 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
   uint32_t* vis = smem + nw;
   uint32_t* nxt = smem + 2 * nw;
   const int nz = F.dims[2], ny = F.dims[1];
+  const int P = ny * nz;  // cells per x slab
+  // residue steps of a thread's word start i0 = 32 wi between its words
+  const int dz32 = (int)((blockDim.x * 32L) % nz), dy32 = (int)((blockDim.x * 32L) % P);
   const int n_total = (int)rintf(cfg.density * F.dist * 2.f * cfg.corridor_halfwidth);
   const int n_cyl = (int)rintf(0.4f * n_total), n_sph = (int)rintf(0.3f * n_total);
   const int n_box = n_total - n_cyl - n_sph;
@@ -206,16 +210,22 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
                 F.lo.y + (iy + 0.5f) * (F.hi.y - F.lo.y) / F.dims[1],
                 F.lo.z + (iz + 0.5f) * (F.hi.z - F.lo.z) / F.dims[2]);
     };
-    for (long wi = threadIdx.x; wi < nw; wi += blockDim.x) {
-      uint32_t word = 0;
-      for (int b = 0; b < 32; ++b) {
-        long i = wi * 32 + b;
-        if (i >= cells) break;
-        const int iz = (int)(i % nz);
-        if (F.lo.z + (iz + 0.5f) * (F.hi.z - F.lo.z) / F.dims[2] > thr) word |= 1u << b;
+    int izmin = nz;  // the ground rule: free iff the centre's z > thr, monotone in iz
+    for (int iz = 0; iz < nz; ++iz)
+      if (F.lo.z + (iz + 0.5f) * (F.hi.z - F.lo.z) / F.dims[2] > thr) {
+        izmin = iz;
+        break;
       }
-      freeb[wi] = word;
-      vis[wi] = 0u;
+    {
+      int rz = (int)((threadIdx.x * 32L) % nz);
+      for (long wi = threadIdx.x; wi < nw; wi += blockDim.x) {
+        uint32_t word = residue_mask(rz, nz, izmin, nz - 1);
+        if (wi * 32 + 32 > cells) word &= span32(0, (int)(cells - wi * 32) - 1);  // no cells past the grid
+        freeb[wi] = word;
+        vis[wi] = 0u;
+        rz += dz32;
+        if (rz >= nz) rz -= nz;
+      }
     }
     __syncthreads();
     const int n_obs = ns + nb + nc;
@@ -273,6 +283,7 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
       // ---- bit-parallel BFS: grown = (v | 6 shifted copies) & free
       for (int it = 0; it < (int)cells; ++it) {
         int changed = 0;
+        int rz = (int)((threadIdx.x * 32L) % nz), ry = (int)((threadIdx.x * 32L) % P);  // residues of i0
         for (long wi = threadIdx.x; wi < nw; wi += blockDim.x) {
           uint32_t v = vis[wi];
           uint32_t g = v;
@@ -283,10 +294,12 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
           uint32_t xp = bits_at(vis, cells, wi * 32 + (long)ny * nz);
           // boundary masks: receive from iz-1 only if iz>0, etc. (bits past
           // `cells` are masked by freeb below)
-          const long i0 = wi * 32;
-          const uint32_t mzlo = ~periodic_mask(i0, nz, 0, 0), mzhi = ~periodic_mask(i0, nz, nz - 1, nz - 1);
-          const uint32_t mylo = ~periodic_mask(i0, (long)ny * nz, 0, nz - 1);
-          const uint32_t myhi = ~periodic_mask(i0, (long)ny * nz, (long)(ny - 1) * nz, (long)ny * nz - 1);
+          const uint32_t mzlo = ~residue_mask(rz, nz, 0, 0), mzhi = ~residue_mask(rz, nz, nz - 1, nz - 1);
+          const uint32_t mylo = ~residue_mask(ry, P, 0, nz - 1), myhi = ~residue_mask(ry, P, P - nz, P - 1);
+          rz += dz32;
+          if (rz >= nz) rz -= nz;
+          ry += dy32;
+          if (ry >= P) ry -= P;
           g |= (zm & mzlo) | (zp & mzhi) | (ym & mylo) | (yp & myhi) | xm | xp;
           g &= freeb[wi];
           nxt[wi] = g;
