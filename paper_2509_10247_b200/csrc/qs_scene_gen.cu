@@ -11,7 +11,10 @@
 
 namespace {
 
-constexpr int GEN_BLOCK = 256;
+#ifndef QS_GEN_BLOCK
+#define QS_GEN_BLOCK 256
+#endif
+constexpr int GEN_BLOCK = QS_GEN_BLOCK;
 
 struct Frame {
   V3 spawn, goal, fwd, left, lo, hi;
