@@ -7,6 +7,8 @@
 // on the ground, indoor shell).  Feasibility is the reference's 6-connected
 // BFS over the 0.25 m occupancy grid with obstacles inflated by r_quad+0.05,
 // run as bit-parallel dilation over a shared-memory bitmap.
+#include <climits>
+
 #include "qs_geom.cuh"
 
 namespace {
@@ -106,6 +108,7 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
   __shared__ float s_cyl_hh[64];
   __shared__ int s_cnt[3];
   __shared__ int s_done;
+  __shared__ int s_vlo, s_vhi;  // visited word range of the BFS
   const long e = blockIdx.x;
   if (e >= n_envs) return;
   if (cfg.env_mask && !cfg.env_mask[e]) return;  // re-randomise only the masked envs
@@ -281,13 +284,22 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
     const bool t_ok = (freeb[target >> 5] >> (target & 31)) & 1u;
     bool ok = false;
     if (s_ok && t_ok) {
-      if (threadIdx.x == 0) vis[start >> 5] |= 1u << (start & 31);
+      if (threadIdx.x == 0) {
+        vis[start >> 5] |= 1u << (start & 31);
+        s_vlo = s_vhi = (int)(start >> 5);
+      }
       __syncthreads();
-      // ---- bit-parallel BFS: grown = (v | 6 shifted copies) & free
+      // ---- bit-parallel BFS: grown = (v | 6 shifted copies) & free, over the
+      // window of words within one x-slab (P bits) of the visited words --
+      // nothing outside it can change this iteration
+      const int margin = P / 32 + 2;
       for (int it = 0; it < (int)cells; ++it) {
         int changed = 0;
-        int rz = (int)((threadIdx.x * 32L) % nz), ry = (int)((threadIdx.x * 32L) % P);  // residues of i0
-        for (long wi = threadIdx.x; wi < nw; wi += blockDim.x) {
+        const long wlo = max(0, s_vlo - margin), whi = min((long)nw - 1, (long)s_vhi + margin);
+        int my_lo = INT_MAX, my_hi = -1;
+        long w0 = wlo + threadIdx.x;
+        int rz = (int)((w0 * 32) % nz), ry = (int)((w0 * 32) % P);  // residues of i0 = 32 wi
+        for (long wi = w0; wi <= whi; wi += blockDim.x) {
           uint32_t v = vis[wi];
           uint32_t g = v;
           // neighbour bit i-1 / i+1 (z), i-nz / i+nz (y), i-ny*nz / i+ny*nz (x)
@@ -307,9 +319,17 @@ __global__ void __launch_bounds__(GEN_BLOCK) k_gen(const qs_gen_cfg cfg, int n_e
           g &= freeb[wi];
           nxt[wi] = g;
           changed |= (g != v);
+          if (g) {
+            my_lo = min(my_lo, (int)wi);
+            my_hi = max(my_hi, (int)wi);
+          }
         }
-        changed = __syncthreads_or(changed);
-        for (long wi = threadIdx.x; wi < nw; wi += blockDim.x) vis[wi] = nxt[wi];
+        changed = __syncthreads_or(changed);  // every thread has read this iteration's window
+        if (my_hi >= 0) {
+          atomicMin(&s_vlo, my_lo);
+          atomicMax(&s_vhi, my_hi);
+        }
+        for (long wi = wlo + threadIdx.x; wi <= whi; wi += blockDim.x) vis[wi] = nxt[wi];
         __syncthreads();
         if ((vis[target >> 5] >> (target & 31)) & 1u) {
           ok = true;
