@@ -146,7 +146,7 @@ def test_adam_matches_hand_computed_sequence():  # :146-154 (oracles.adam_ref)
         m = 0.9 * m + 0.1 * g
         v = 0.999 * v + 0.001 * g * g
         e -= 0.01 * (m / (1 - 0.9 ** t)) / (math.sqrt(v / (1 - 0.999 ** t)) + 1e-8)
-    assert float(x) == pytest.approx(e, rel=1e-14)
+    assert float(x.detach()) == pytest.approx(e, rel=1e-14)
 
 
 def test_adam_grad_clip():  # :157-169
