@@ -210,7 +210,7 @@ def test_cuda_graph_updates_match_eager():
         torch.testing.assert_close(pa, pb, rtol=1e-3, atol=1e-4)
     # the carried env state: the two trainers' fp32 round-off (capturable Adam,
     # bf16 GEMMs) moves a few rows slightly after 56 closed-loop steps
-    d = (trs[0].env._S - trs[1].env._S).abs()
+    d = (trs[0].env._S - trs[1].env._S).detach().abs()
     assert float(d.max()) < 0.05, float(d.max())  # a stale carry would be off by O(1)
     same_clock = (trs[0].env._meta[:, :3] == trs[1].env._meta[:, :3]).all(-1).float().mean()
     assert float(same_clock) > 0.99  # episode step / episode index / tick per env
