@@ -1515,12 +1515,15 @@ def reward_ctrl_vjp(w: Weights, off, v, eff, deff, g):
     return g_off, g_v, g_eff
 
 
-def window_value_and_grad(env: OracleTask, actions, gamma=0.99):
+def window_value_and_grad(env: OracleTask, actions, gamma=0.99, before_step=None):
     """Position-task BPTT window: L and dL/d(raw actions) by the reverse pass.
 
     Forward runs env.step (resets included); the backward replays the
     recorded checkpoints in reverse with the tape's semantics: yaw frame and
     prev_effort constant, gradient cut at resets (q/tasks.py:712-721).
+    ``before_step(env, t)`` (tests) may overwrite the carried state before
+    step t is recorded (teacher forcing): the reverse pass then evaluates the
+    chain rule along the forced trajectory.
     """
     cfg = env.cfg
     assert cfg.task == "position" and env.n_agents == 1
@@ -1528,6 +1531,8 @@ def window_value_and_grad(env: OracleTask, actions, gamma=0.99):
     recs = []
     loss = 0.0
     for t in range(T):
+        if before_step is not None:
+            before_step(env, t)
         st = {k: v.copy() for k, v in env.state.items()}
         yaw = env.yaw() if env.model.startswith("pm") else None
         lo, hi = env.act_lo.copy(), env.act_hi.copy()

@@ -19,7 +19,11 @@ from paper_2509_10247_b200.tasks import FlightTask
 
 class BpttWindow:
     def __init__(self, env: FlightTask, horizon: int, gamma: float = 0.99, want_obs: bool = True,
-                 fused: bool = True):
+                 fused: bool = True, imu_noise: torch.Tensor | None = None):
+        """``imu_noise``: optional (T, 4, N, 3) normals injected into the IMU
+        (bias walk accel, bias walk gyro, white accel, white gyro -- the
+        reference's draw order, q/sensors.py:544-554) instead of the in-kernel
+        Philox draws; for exact parity checks."""
         if env.reset_source is not None:
             raise ValueError("BpttWindow needs in-kernel (Philox) resets; reset_source forces host syncs")
         if env._cfg.reset_mode != 0:
@@ -40,6 +44,12 @@ class BpttWindow:
         self.trunc = torch.zeros(T, N, dtype=torch.bool, device=dev)
         self.imu = torch.zeros(T, N, 6, **f) if env._imu_bias is not None else None
         self.actions = torch.zeros(T, N, A, **f)
+        self.imu_noise = None
+        if imu_noise is not None:
+            if self.imu is None:
+                raise ValueError("imu_noise needs an env built with TaskConfig.imu")
+            self.imu_noise = torch.as_tensor(imu_noise, dtype=torch.float32, device=dev).reshape(T, 4, N, 3)
+            self.imu_noise = self.imu_noise.contiguous()
         self.g_actions = torch.zeros(T, N, A, **f)
         self.gS = torch.zeros(2, NP, N, 4, **f)
         # dL/dr_ctrl_t = -gamma^t / (T N)
@@ -79,6 +89,7 @@ class BpttWindow:
         w.actions = L.ptr(self.actions)
         w.meta, w.ep_return, w.imu_bias = L.ptr(e._meta), L.ptr(e._ep_ret), L.ptr(e._imu_bias)
         w.imu_out = L.ptr(self.imu)
+        w.imu_noise = L.ptr(self.imu_noise)
         w.obs = L.ptr(self.obs) if self.want_obs else None
         w.r, w.terminated, w.truncated, w.flags = L.ptr(self.r), L.ptr(self.term), L.ptr(self.trunc), L.ptr(self.flags)
         w.stats, w.err = L.ptr(e._stats), L.ptr(e._err)
@@ -110,6 +121,7 @@ class BpttWindow:
                 io.dr_in, io.dr_out = L.ptr(self.dr[t]), L.ptr(self.dr[t + 1])
             if self.imu is not None:
                 io.imu_out = L.ptr(self.imu[t])
+                io.imu_noise = L.ptr(self.imu_noise[t]) if self.imu_noise is not None else None
             io.obs = L.ptr(self.obs[t if self.want_obs else 0])
             io.r_ctrl, io.r_goal, io.r_rl = L.ptr(self.r[t, 0]), L.ptr(self.r[t, 1]), L.ptr(self.r[t, 2])
             io.terminated, io.truncated, io.flags = L.ptr(self.term[t]), L.ptr(self.trunc[t]), L.ptr(self.flags[t])

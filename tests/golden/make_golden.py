@@ -507,10 +507,60 @@ def gen_nets_ppo():
     save("io_inputs", **io_rec)
 
 
+# ---------------------------------------------------------------------------
+# C1 at its exact shape: pm position task, 1,024 envs, reset(seed=1),
+# raw = default_rng(0).normal(size=(32,1024,3))*0.3, episode_len 1e6,
+# L = -(1/32) sum_t 0.99^t mean(r_ctrl_t) and dL/d(raw) through the tape.
+# Per-step rewards and the gradient are stored as float32 (the GPU bars are
+# 1e-5 / 1e-4, far above fp32 storage round-off), loss and states as fp64.
+
+
+def gen_c1():
+    raw = np.random.default_rng(0).normal(size=(32, 1024, 3)) * 0.3
+    for name, short in (("pm_continuous", "pmc"), ("pm_discrete", "pmd")):
+        cfg = tk.TaskConfig(task="position", dynamics=name, n_envs=1024, episode_len=10 ** 6)
+        env = tk.make_task(cfg)
+        env.reset(seed=1)
+        rec = {}
+        for k, v in _state_arrays(env).items():
+            rec[f"s0_{k}"] = v
+        rec["goals0"] = env.goals.copy()
+        tape = Tape()
+        leaves = [tape.leaf(raw[t].copy()) for t in range(32)]
+        env.detach_states()
+        disc = None
+        r_ctrl, r_rl, term = [], [], []
+        for t in range(32):
+            out = env.step(leaves[t])
+            term_ = ad.mul(ad.vmean(out.r_ctrl), 0.99 ** t)
+            disc = term_ if disc is None else ad.add(disc, term_)
+            r_ctrl.append(out.r_ctrl.value.copy())
+            r_rl.append(out.r_rl.copy())
+            term.append(out.terminated.copy())
+            if t == 15:
+                for k, v in _state_arrays(env).items():
+                    rec[f"s16_{k}"] = v
+        loss = ad.neg(ad.mul(disc, 1.0 / 32))
+        grads = tape.backward(loss)
+        for k, v in _state_arrays(env).items():
+            rec[f"s32_{k}"] = v
+        rec["goals32"] = env.goals.copy()
+        rec["loss"] = np.array(loss.value)
+        rec["grad"] = np.stack([grads[l] for l in leaves]).astype(np.float32)
+        rec["r_ctrl"] = np.stack(r_ctrl).astype(np.float32)
+        rec["r_rl"] = np.stack(r_rl).astype(np.float32)
+        rec["term"] = np.stack(term)
+        rec["stats"] = np.array([env.finished_episodes, env.successful_episodes, env.collision_episodes,
+                                 env.finished_return])
+        save(f"c1_{short}", **rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners", "nets_ppo"]
+    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners", "nets_ppo", "c1"]
     if "nets_ppo" in which:
         gen_nets_ppo()
+    if "c1" in which:
+        gen_c1()
     if "learners" in which:
         gen_learners()
     if "dynamics" in which:

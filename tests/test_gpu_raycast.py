@@ -119,28 +119,121 @@ def test_tiled_degenerate_rays_and_origins():
                 assert float(a[1, 0]) == 0.5  # inside the box: the exit face
 
 
-def test_depth_matches_oracle_on_generated_scenes():
-    import paper_2509_10247_b200 as qs
+# ---------------------------------------------------------------------------
+# exactness against the fp64 oracle at the C3 / C4 shapes.  The north star asks
+# for depth within 1e-4 m and EXACT hit/miss masks.  fp32 can only promise that
+# for rays whose fp64 answer is itself stable under fp32-sized input noise, so
+# every deviating ray is listed with its fp64 margin and must lie inside the
+# documented epsilon-band: moving the ray's origin by
+# PROBE_DELTA = 5 um along any axis changes the fp64 reference's own hit/miss
+# or depth by more than the 1e-4 m bar (grazing tangents, edges and corners,
+# t within 5 um of max_range).  Any deviation outside that band fails.
+
+PROBE_DELTA = 5e-6
+
+
+def _oracle_chunk(args):
+    from oracle import quadsim_oracle as O
+
+    prims, pos, R, kind, shape, max_range = args
+    if kind == "depth":
+        return O.render_depth(prims, pos, R, shape[0], shape[1], max_range).reshape(len(pos), -1)
+    return O.render_lidar(prims, pos, R, shape[0], shape[1], max_range)
+
+
+def _oracle_frames(prims, pos, R, kind, shape, max_range, chunk=32):
+    import multiprocessing as mp
+    import os
+
+    from oracle import quadsim_oracle as O
+
+    E = len(pos)
+    jobs = [(O.prims_take(prims, slice(s, s + chunk)), pos[s:s + chunk], R[s:s + chunk], kind, shape, max_range)
+            for s in range(0, E, chunk)]
+    n = max(1, min(len(jobs), len(os.sched_getaffinity(0))))
+    with mp.get_context("fork").Pool(n) as pool:
+        return np.concatenate(pool.map(_oracle_chunk, jobs))
+
+
+def _probe_margin(prims, env, origin, dirs, max_range):
+    """fp64 depth of each listed ray and its largest change when the origin
+    moves by +-PROBE_DELTA along x, y, z (uncull: the reference's cull is a
+    conservative superset filter and never changes a ray)."""
+    from oracle import quadsim_oracle as O
+
+    pe = O.prims_take(prims, env)
+    base = O.raycast(pe, origin, dirs[:, None, :], max_range)[:, 0]
+    dev = np.zeros_like(base)
+    flip = np.zeros(base.shape, bool)
+    for ax in range(3):
+        for sgn in (-1.0, 1.0):
+            o2 = origin.copy()
+            o2[:, ax] += sgn * PROBE_DELTA
+            t = O.raycast(pe, o2, dirs[:, None, :], max_range)[:, 0]
+            dev = np.maximum(dev, np.abs(t - base))
+            flip |= (t < max_range) != (base < max_range)
+    return base, dev, flip
+
+
+def _check_against_oracle(qs, E, seed, kind, style):
     from oracle import quadsim_oracle as O
 
     sn = qs.sensors
-    E = 256
-    sc, pos, cs, yaw = _scene_and_poses(qs, E, 9)
-    cam = sn.CameraIntrinsics(width=64, height=48, max_range=10.0)
-    d, hit, _ = sn.cast_rays(sc, pos, 4, cs, cam, 0, True, want_hit=True)
+    sc, pos, cs, _ = _scene_and_poses(qs, E, seed, style=style)
+    if kind == "depth":
+        sensor = sn.CameraIntrinsics(width=64, height=48, max_range=10.0)
+        shape, k = (64, 48), 0
+        body_dirs = O.pixel_dirs(64, 48)
+    else:
+        sensor = sn.LidarPattern(n_azimuth=360, n_elevation=16, max_range=20.0)
+        shape, k = (360, 16), 1
+        body_dirs = O.lidar_dirs(360, 16)
+    d, hit, _ = sn.cast_rays(sc, pos, 4, cs, sensor, k, True, want_hit=True)
+    d, hit = d.double().cpu().numpy(), hit.cpu().numpy().astype(bool)
     scenes = qs.world.device_scene_to_scenes(sc)
     prims = O.pack_primitives([{"spheres": s.prims.spheres, "boxes": s.prims.boxes,
                                 "cylinders": s.prims.cylinders, "ground_z": s.prims.ground_z} for s in scenes])
     # the oracle sees the fp32 scene and poses the kernel saw
-    ref = O.render_depth(prims, pos[:, :3].double().cpu().numpy(), O.rotz(np.arctan2(cs[:, 1].cpu().numpy(),
-                         cs[:, 0].cpu().numpy())), 64, 48, 10.0).reshape(E, -1)
-    err = np.abs(d.cpu().numpy() - ref)
-    # north-star bar: 1e-4 m; allow a handful of grazing rays (reported)
-    bad = err > 1e-4
-    assert bad.mean() < 1e-4, (bad.sum(), err.max())
-    mask_ref = ref < 10.0
-    flips = (hit.cpu().numpy().astype(bool) != mask_ref)
-    assert flips.mean() < 1e-4, flips.sum()
+    p64 = pos[:, :3].double().cpu().numpy()
+    csn = cs.double().cpu().numpy()
+    R = O.rotz(np.arctan2(csn[:, 1], csn[:, 0]))
+    mr = sensor.max_range
+    ref = _oracle_frames(prims, p64, R, kind, shape, mr)
+    err = np.abs(d - ref)
+    bad_depth = err > 1e-4
+    flips = hit != (ref < mr)
+    dev_mask = bad_depth | flips
+    env_i, ray_i = np.nonzero(dev_mask)
+    dirs = np.einsum("bij,rj->bri", R, body_dirs)
+    ok = True
+    lines = []
+    if len(env_i):
+        base, dev, pflip = _probe_margin(prims, env_i, p64[env_i], dirs[env_i, ray_i], mr)
+        assert np.allclose(base, ref[env_i, ray_i], rtol=0, atol=1e-12)
+        in_band = (dev > 1e-4) | pflip
+        for j in range(len(env_i)):
+            lines.append(f"  env {env_i[j]} ray {ray_i[j]}: gpu {d[env_i[j], ray_i[j]]:.6f} ref {base[j]:.6f} "
+                         f"flip {bool(flips[env_i[j], ray_i[j]])} fp64 probe dev {dev[j]:.3e} "
+                         f"probe flip {bool(pflip[j])} {'in band' if in_band[j] else 'OUT OF BAND'}")
+        ok = bool(in_band.all())
+    print(f"\n{kind}/{style} {E} envs x {d.shape[1]} rays: max err {err[~dev_mask].max() if (~dev_mask).any() else 0:.2e} "
+          f"on {int((~dev_mask).sum())} rays; {int(bad_depth.sum())} depth and {int(flips.sum())} hit-mask "
+          f"deviations, all listed:")
+    print("\n".join(lines))
+    assert ok, "deviation outside the documented epsilon-band"
+    assert dev_mask.mean() < 1e-4
+    return err
+
+
+@pytest.mark.parametrize("kind,style,E", [("depth", "outdoor", 1024), ("depth", "indoor", 512),
+                                          ("lidar", "indoor", 256)])
+def test_render_matches_oracle_exact_masks(kind, style, E):
+    """C3 (64x48 depth, 32 solids + ground) and C4 (LiDAR 360x16, indoor shell
+    with ceiling) against the fp64 oracle: depth within 1e-4 m and hit masks
+    equal on every ray outside the epsilon-band; the band's rays listed."""
+    import paper_2509_10247_b200 as qs
+
+    _check_against_oracle(qs, E, 9, kind, style)
 
 
 @pytest.mark.parametrize("kind,style", [("depth", "outdoor"), ("depth", "indoor"), ("lidar", "outdoor")])

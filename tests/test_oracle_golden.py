@@ -201,3 +201,36 @@ def test_oracle_reverse_pass_matches_reference_tape(name):
     g_ref = z["grad_unaliased"] if "grad_unaliased" in z else z["grad"]
     assert abs(loss - float(z["loss"])) < 1e-12
     assert np.abs(g - g_ref).max() / np.abs(g_ref).max() < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# C1 at its exact shape (1,024 envs x 32 steps, reset(seed=1), default_rng(0)
+# actions): the oracle's forward, resets and reverse pass against the
+# reference's own run (tests/golden/make_golden.py:gen_c1)
+
+
+@pytest.mark.parametrize("short,model", [("pmc", "pm_continuous"), ("pmd", "pm_discrete")])
+def test_c1_exact_shape_oracle_matches_reference(short, model):
+    z = load(f"c1_{short}")
+    env = O.OracleTask(O.Config(task="position", dynamics=model, n_envs=1024, episode_len=10 ** 6))
+    env.reset(1)
+    for k in STATE_KEYS[model]:
+        close(env.state[k], z[f"s0_{k}"], 1e-12)
+    raw = np.random.default_rng(0).normal(size=(32, 1024, 3)) * 0.3
+    snap = env.snapshot()
+    r_ctrl, term = [], []
+    for t in range(32):
+        out = env.step(raw[t])
+        r_ctrl.append(out["r_ctrl"])
+        term.append(out["terminated"])
+        if t == 15:
+            for k in STATE_KEYS[model]:
+                close(env.state[k], z[f"s16_{k}"], 1e-10)
+    for k in STATE_KEYS[model]:
+        close(env.state[k], z[f"s32_{k}"], 1e-10)
+    assert np.array_equal(np.stack(term), z["term"])
+    np.testing.assert_allclose(np.stack(r_ctrl), z["r_ctrl"], rtol=1e-6, atol=1e-6)  # f32 storage
+    env.restore(snap)
+    loss, g = O.window_value_and_grad(env, raw)
+    assert abs(loss - float(z["loss"])) < 1e-10
+    assert np.abs(g - z["grad"]).max() / np.abs(z["grad"]).max() < 1e-6  # f32 storage
