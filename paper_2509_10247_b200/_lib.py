@@ -164,14 +164,18 @@ def ptr(t):
 
 def stream_handle(device=None):
     """The raw cudaStream_t of the current stream on ``device`` (fast path: no
-    Stream object is built on every kernel launch)."""
+    Stream object is built on every kernel launch).  Kernels launch on the
+    calling thread's current device, so a call for another device makes that
+    device current first (FlightTask(device="cuda:1") without set_device)."""
+    cur = torch.cuda.current_device()
     if device is None:
-        idx = torch.cuda.current_device()
+        idx = cur
     elif isinstance(device, int):
         idx = device
     else:
-        idx = device.index if isinstance(device, torch.device) and device.index is not None \
-            else torch.cuda.current_device()
+        idx = device.index if isinstance(device, torch.device) and device.index is not None else cur
+    if idx != cur:
+        torch.cuda.set_device(idx)
     return torch._C._cuda_getCurrentRawStream(idx)
 
 

@@ -390,10 +390,15 @@ extern "C" int qs_gen_obstacle_course(const qs_gen_cfg* cfg, int32_t n_envs, flo
   long cells = (long)(ceilf(ext / 0.25f) + 1) * (long)(ceilf(ext / 0.25f) + 1) * 17;
   size_t smem = (size_t)3 * ((cells + 31) / 32) * 4;
   if (smem > 200 * 1024) return QS_ERR_BAD_ARGUMENT;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
+  // the dynamic shared memory opt-in is per device: cache it per device id
+  // and check it (a second device launching without it would fail)
+  static bool attr[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return QS_ERR_LAUNCH;
+  if (!attr[dev]) {
+    if (cudaFuncSetAttribute(k_gen, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024) != cudaSuccess)
+      return QS_ERR_LAUNCH;
+    attr[dev] = true;
   }
   k_gen<<<n_envs, GEN_BLOCK, smem, (cudaStream_t)stream>>>(*cfg, n_envs, bounds, spawn_goal, spheres,
                                                            boxes, cylinders, counts, ground_z, err);

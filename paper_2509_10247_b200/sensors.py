@@ -153,6 +153,15 @@ class DeviceScene:
         sc.counts.copy_(torch.stack([ns, nb, nc, has_g.to(torch.int32)], dim=-1))
         return sc
 
+    def clone(self) -> "DeviceScene":
+        """Deep copy (copy-on-write regeneration: autograd nodes recorded
+        against this scene keep seeing it unchanged)."""
+        sc = DeviceScene.__new__(DeviceScene)
+        sc.device, sc.n_envs, sc.ext_cull, sc._struct = self.device, self.n_envs, self.ext_cull, None
+        for k in ("spheres", "boxes", "cylinders", "counts", "ground_z", "bounds", "spawn_goal", "gates"):
+            setattr(sc, k, getattr(self, k).clone())
+        return sc
+
     def set_rows(self, e_slice, other: "DeviceScene"):
         for k in ("spheres", "boxes", "cylinders", "counts", "ground_z", "bounds", "spawn_goal", "gates"):
             getattr(self, k)[e_slice] = getattr(other, k)

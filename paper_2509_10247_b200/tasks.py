@@ -218,10 +218,14 @@ class _TaskStepFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, S_in, raw, env):
         ctx.set_materialize_grads(False)
-        b = env._launch_step(S_in, raw)
+        # the scene this step's SDF penalty was evaluated against: a course
+        # regenerated during the step (regen_scene_on_reset) is written into a
+        # copy, so this node's backward keeps the pre-regeneration course
+        scene = env._scene
+        b = env._launch_step(S_in, raw, cow_scene=bool(ctx.needs_input_grad[0] or ctx.needs_input_grad[1]))
         ctx.save_for_backward(S_in, raw)
         ctx.env_cfg = env._cfg
-        ctx.scene = env._scene
+        ctx.scene = scene
         ctx.rec = (b.goal_in, b.peff_in, b.dr_in, b.flags)
         ctx.P = b.obs.shape[1]
         env._pending = b
@@ -750,7 +754,7 @@ class FlightTask:
             raise wd.GenerationError(f"could not sample a reset (row {row})", self.seed)
         raise L.QuadsimLibraryError(f"device error code {code} at row {row}")
 
-    def _launch_step(self, S_in, raw) -> _StepBufs:
+    def _launch_step(self, S_in, raw, cow_scene: bool = False) -> _StepBufs:
         dev, N = self.device, self.N
         f = dict(device=dev, dtype=torch.float32)
         b = _StepBufs()
@@ -789,27 +793,33 @@ class FlightTask:
                 if done_env.any():
                     ids = np.flatnonzero(done_env)
                     tab, keep = self._reset_table(ids)
-                    self._regen_scenes(keep["mask"])
+                    self._regen_scenes(keep["mask"], cow_scene)
                     L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, tab.env_mask, tab,
                                                   stream), "qs_task_spawn")
                     self._episode_counter += 1
                     del keep
             else:  # device-only: done mask -> new course -> Philox spawn, no host sync
                 mask = (b.flags.view(self.n_envs, self.n_agents)[:, 0] & 1).to(torch.uint8)
-                self._regen_scenes(mask)
+                self._regen_scenes(mask, cow_scene)
                 L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, L.ptr(mask), None, stream),
                         "qs_task_spawn")
             L.check(L.lib().qs_task_observe(self._cfg, self._scene.struct(), io, stream), "qs_task_observe")
             self._frame_cache = None
         return b
 
-    def _regen_scenes(self, mask):
+    def _regen_scenes(self, mask, cow: bool = False):
         """Re-randomise the obstacle course of every env in ``mask`` (uint8, device),
         keyed by (seed, env, episode) — ``meta[:, 1]`` already holds the new
         episode index.  The reference declares ``regen_scene_on_reset`` without
-        wiring it (q/tasks.py:98); the course distribution is q/world.py:207-340."""
+        wiring it (q/tasks.py:98); the course distribution is q/world.py:207-340.
+
+        ``cow``: the current scene is referenced by recorded autograd nodes,
+        whose backward re-evaluates the SDF at the primitive the forward chose;
+        regenerate into a copy so those nodes keep their course."""
         if not self._regen:
             return
+        if cow:
+            self._scene = self._scene.clone()
         wd.gen_obstacle_courses(self.seed, self.n_envs, check=False, out=self._scene, env_mask=mask,
                                 episode=self._meta[:, 1], episode_stride=4, err=self._err, **self._gen_args)
 

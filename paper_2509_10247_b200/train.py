@@ -29,10 +29,11 @@ from paper_2509_10247_b200.nets import LOG_SIGMA_MIN, PolicyArch, PolicyNet, Val
 class LearnerOptions:
     """q/learners.py:34-58 (actor/critic subset)."""
 
-    algo: str = "shac"  # bptt | shac | sha2c
+    algo: str = "sha2c"  # bptt | shac | sha2c (the reference's default, q/learners.py:31)
     horizon: int = 16
     gamma: float = 0.99
     td_lambda: float = 0.95
+    k_steps: int | None = None  # critic k-step return window; None -> horizon (q/learners.py:38)
     actor_lr: float = 2e-3
     critic_lr: float = 2e-3
     critic_iters: int = 8
@@ -66,17 +67,43 @@ class LearnerOptions:
     cuda_graph: bool = False
 
 
-def td_lambda_targets(r, values, bootstrap, done, gamma, lam):
-    """TD(lambda) targets with termination cuts (q/learners.py:78-94), (T,N)."""
+def td_lambda_targets(r, values, bootstrap, done, gamma, lam, k=None):
+    """TD(lambda) targets with termination cuts (q/learners.py:78-113), (T,N).
+
+    ``k`` limits the return window (SHA2C's k-step critic target,
+    q/learners.py:95-113): G_t mixes the n-step returns n = 1..min(k, T-t)
+    with weights (1-lam) lam^(n-1), the last one taking the remaining
+    lam^(steps-1).  The n loop runs over all t at once (k vector steps)."""
     T = r.shape[0]
     cont = 1.0 - done.to(r.dtype)
-    G = torch.empty_like(r)
-    nxt = bootstrap
-    for t in reversed(range(T)):
-        v_next = values[t + 1] if t + 1 < T else bootstrap
-        G[t] = r[t] + gamma * cont[t] * ((1.0 - lam) * v_next + lam * nxt)
-        nxt = G[t]
-    return G
+    if k is None or k >= T:
+        G = torch.empty_like(r)
+        nxt = bootstrap
+        for t in reversed(range(T)):
+            v_next = values[t + 1] if t + 1 < T else bootstrap
+            G[t] = r[t] + gamma * cont[t] * ((1.0 - lam) * v_next + lam * nxt)
+            nxt = G[t]
+        return G
+    dev = r.device
+    v_ext = torch.cat([values, bootstrap[None]], 0)  # V(s_t), t = 0..T
+    ts = torch.arange(T, device=dev)
+    steps = torch.clamp(T - ts, max=k)  # (T,)
+    running = torch.zeros_like(r)
+    alive = torch.ones_like(r)
+    mix = torch.zeros_like(r)
+    disc = 1.0
+    for n in range(1, k + 1):
+        idx = torch.clamp(ts + n - 1, max=T - 1)  # r/cont index t+n-1 (clamped where n > steps: weight 0)
+        r_n, c_n = r[idx], cont[idx]
+        running = running + disc * alive * r_n
+        g_n = running + gamma * disc * alive * c_n * v_ext[torch.clamp(ts + n, max=T)]
+        full_w = torch.full((T,), (1.0 - lam) * lam ** (n - 1), dtype=r.dtype, device=dev)
+        last_w = torch.full((T,), lam ** (n - 1), dtype=r.dtype, device=dev)
+        w = torch.where(n < steps, full_w, torch.where(n == steps, last_w, torch.zeros_like(last_w)))
+        mix = mix + w[:, None] * g_n
+        alive = alive * c_n
+        disc *= gamma
+    return mix
 
 
 def gae_advantages(r, values, bootstrap, done, gamma, lam):
@@ -398,7 +425,7 @@ class ShortHorizonTrainer:
             with self._nets():
                 values = self.value(priv.reshape(T * N, K)).reshape(T, N)
                 boot = self.value(self.env.privileged_state())
-            targets = td_lambda_targets(r, values, boot, dones, opts.gamma, opts.td_lambda)
+            targets = td_lambda_targets(r, values, boot, dones, opts.gamma, opts.td_lambda, opts.k_steps)
         X = priv.reshape(-1, priv.shape[-1])
         y = targets.reshape(-1)
         fused = opts.fused_critic and self._amp and X.shape[1] <= 16 and tuple(opts.mlp) == (128, 128)

@@ -63,6 +63,7 @@ class BpttWindow:
         self.graph = None
         self.launches_per_window = 2 if fused else 2 * T
         self._load_env_state()
+        self._bound = self._env_buffers()
 
     def _load_env_state(self):
         e = self.env
@@ -165,26 +166,38 @@ class BpttWindow:
         for dst, src in zip(live, snap):
             dst.copy_(src)
         self.graph = g
-        self._env_bufs = self._env_buffers()
+        self._bound = self._env_buffers()
         return self
 
     def _env_buffers(self):
-        """The env objects a captured window points at; env.reset() replaces them."""
+        """The env objects a window (captured or eager) points at; env.reset()
+        replaces them."""
         e = self.env
         return (e._meta, e._ep_ret, e._stats, e._err, e._imu_bias, e._scene, e._cfg)
 
     def _stale(self) -> bool:
-        return any(a is not b for a, b in zip(getattr(self, "_env_bufs", ()), self._env_buffers()))
+        return any(a is not b for a, b in zip(self._bound, self._env_buffers()))
+
+    def _refresh(self):
+        """After env.reset(): reload the carried state from the env (graph,
+        pipeline and eager paths alike) and re-capture what was captured."""
+        if not self._stale():
+            return
+        self._load_env_state()
+        had_graph, had_pipe = self.graph is not None, getattr(self, "_pipe", None) is not None
+        if had_pipe:
+            self.actions = self._pipe["bufs"][0]
+        self.graph = None
+        self._pipe = None
+        self._bound = self._env_buffers()
+        if had_graph and not had_pipe:
+            self.capture()
 
     def run(self, actions: torch.Tensor | None = None):
         """One window (fwd + bwd).  Returns (loss tensor, dL/d actions (T,N,A))."""
+        self._refresh()
         if actions is not None:
             self.actions.copy_(actions, non_blocking=True)
-        if self.graph is not None and self._stale():  # the env was reset since the capture
-            self._load_env_state()
-            self.graph = None
-            self._pipe = None
-            self.capture()
         if self.graph is not None:
             self.graph.replay()
         else:
@@ -219,6 +232,7 @@ class BpttWindow:
         """Run one window per pinned host action batch (T,N,A); returns the
         host losses.  H2D of batch k+1 runs on a copy stream while window k
         computes; each window's loss is read back with an async D2H copy."""
+        self._refresh()
         self._ensure_pipeline()
         P = self._pipe
         comp = torch.cuda.current_stream(self.env.device)

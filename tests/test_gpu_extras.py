@@ -159,3 +159,34 @@ def test_every_kernel_family_at_small_odd_sizes():
     mod = importlib.util.module_from_spec(spec)
     spec.loader.exec_module(mod)
     mod.main()
+
+
+def test_regen_scene_gradient_uses_pre_regeneration_course():
+    """with regen_scene_on_reset, a step whose env resets
+    regenerates that env's course inside the step; the step's backward must
+    still evaluate the obstacle penalty's SDF against the course the forward
+    used.  Episodes of 4 steps: the loss over steps 0..3 must have the same
+    gradient whether courses are regenerated at step 3 (and again at step 7,
+    run but not in the loss) or never."""
+    import paper_2509_10247_b200 as qs
+
+    grads = []
+    for regen, T in ((False, 4), (True, 4), (True, 8)):
+        cfg = qs.TaskConfig(task="avoidance", dynamics="pm_continuous", n_envs=64, episode_len=4, density=0.25,
+                            regen_scene_on_reset=regen)
+        env = qs.make_task(cfg, strict=False)
+        env.reset(seed=5)
+        g = torch.Generator().manual_seed(9)
+        acts = (torch.randn(T, env.N, 3, generator=g) * 0.4).cuda().requires_grad_(True)
+        env.detach_states()
+        loss = 0.0
+        for t in range(T):
+            out = env.step(acts[t])
+            if t < 4:
+                loss = loss + out.r_ctrl.mean() * 0.99 ** t
+        (gr,) = torch.autograd.grad(-loss / 4, acts)
+        grads.append(gr[:4].cpu())
+        assert float(out.r_ctrl.abs().sum()) > 0
+    assert float(grads[0].abs().max()) > 0
+    assert torch.equal(grads[0], grads[1])
+    assert torch.equal(grads[0], grads[2])

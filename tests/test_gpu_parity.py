@@ -547,3 +547,37 @@ def test_window_graph_survives_env_reset(qs):
     loss_b, g_b = win2.run()
     assert abs(loss_a - float(loss_b)) < 1e-9 * abs(float(loss_b))
     assert torch.equal(g_a, g_b)
+
+
+@pytest.mark.parametrize("mode", ["pipelined", "eager"])
+def test_window_survives_env_reset_pipelined_and_eager(qs, mode):
+    """run_pipelined() and the eager (uncaptured) window
+    also reload the env's state after env.reset() instead of replaying the
+    pre-reset carry and stale env buffers."""
+    from paper_2509_10247_b200.window import BpttWindow
+
+    cfg = qs.TaskConfig(task="position", dynamics="full", n_envs=1024, episode_len=20,
+                        imu=qs.ImuSpec(0.1, 0.01, 0.01, 0.001))
+    acts = torch.randn(8, 1024, 4, generator=torch.Generator().manual_seed(1)) * 0.3
+    host = acts.pin_memory()
+
+    def go(win):
+        if mode == "pipelined":
+            return win.run_pipelined([host, host])[-1], win.g_actions.clone()
+        win.run(acts.cuda())
+        loss, g = win.run(acts.cuda())
+        return float(loss), g.clone()
+
+    env = qs.make_task(cfg, strict=False)
+    env.reset(seed=3)
+    win = BpttWindow(env, 8)
+    go(win)
+    env.reset(seed=4)
+    la, ga = go(win)
+    steps_a = env._meta.clone()
+    env2 = qs.make_task(cfg, strict=False)
+    env2.reset(seed=4)
+    lb, gb = go(BpttWindow(env2, 8))
+    assert la == lb
+    assert torch.equal(ga, gb)
+    assert torch.equal(steps_a, env2._meta)  # the window advanced the reset env's counters

@@ -102,3 +102,33 @@ def test_return_scaler_sharded_two_ranks_gloo():
     for rank, lo, hi, outs in res:
         for u in range(3):
             np.testing.assert_allclose(outs[u], z[f"s_scaled{u}"][:, lo:hi], rtol=1e-10, atol=1e-12)
+
+
+def test_td_lambda_k_steps_matches_reference():
+    """SHA2C's k-step critic window (q/learners.py:95-113): the reference's own
+    k=4 output (golden), its k=2 hand mixture (pkg/tests/test_learners.py:79-92)
+    and the recorded-rollout N=2, T=4, k=4 case (:62-76)."""
+    from paper_2509_10247_b200.train import LearnerOptions, td_lambda_targets
+
+    z = load("learners")
+    G = td_lambda_targets(torch.as_tensor(z["r"]), torch.as_tensor(z["values"]), torch.as_tensor(z["boot"]),
+                          torch.as_tensor(z["done"]), 0.99, 0.95, 4)
+    np.testing.assert_allclose(G.numpy(), z["td_k4"], rtol=1e-12, atol=1e-12)
+    rng = np.random.default_rng(3)
+    T, N = 6, 3
+    r, values, boot = rng.normal(size=(T, N)), rng.normal(size=(T, N)), rng.normal(size=N)
+    done = np.zeros((T, N), dtype=bool)
+    lam, gamma = 0.9, 0.98
+    got = td_lambda_targets(torch.as_tensor(r), torch.as_tensor(values), torch.as_tensor(boot),
+                            torch.as_tensor(done), gamma, lam, 2).numpy()
+    for t in range(T - 2):
+        g1 = r[t] + gamma * values[t + 1]
+        g2 = r[t] + gamma * r[t + 1] + gamma ** 2 * values[t + 2]
+        np.testing.assert_allclose(got[t], (1 - lam) * g1 + lam * g2, rtol=1e-12)
+    # k >= T is the full recursive mixture
+    full = td_lambda_targets(torch.as_tensor(r), torch.as_tensor(values), torch.as_tensor(boot),
+                             torch.as_tensor(done), gamma, lam)
+    k6 = td_lambda_targets(torch.as_tensor(r), torch.as_tensor(values), torch.as_tensor(boot),
+                           torch.as_tensor(done), gamma, lam, 6)
+    assert torch.equal(full, k6)
+    assert LearnerOptions().algo == "sha2c" and LearnerOptions(k_steps=4).k_steps == 4
