@@ -219,6 +219,23 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
+def spawn_ranks(n: int):
+    """``bench.py --gpus N`` without a launcher: re-exec this command under
+    torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous),
+    exactly as the driver launches it."""
+    import socket
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
+
+
+DIST = {"backend": None, "shared_gpu": False}
+
+
 def dist_init():
     import torch
     import torch.distributed as dist
@@ -226,13 +243,18 @@ def dist_init():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one GPU per rank; BENCH_DIST_BACKEND=gloo lets the multi-rank control
-    # flow be exercised with several ranks on fewer GPUs (no NCCL)
-    local = local % max(1, torch.cuda.device_count())
+    # one GPU per rank.  With fewer GPUs than ranks (a 1-GPU box running
+    # --gpus 2) the ranks share GPUs over gloo: the multi-rank control flow
+    # runs, but such a line's throughput is not a scaling measurement
+    # ("shared_gpu": true in the JSON line).  BENCH_DIST_BACKEND overrides.
+    ndev = max(1, torch.cuda.device_count())
+    DIST["shared_gpu"] = world > ndev
+    local = local % ndev
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        backend = os.environ.get("BENCH_DIST_BACKEND", "gloo" if DIST["shared_gpu"] else "nccl")
+        DIST["backend"] = backend
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -731,17 +753,24 @@ def run_ours(a):
         loss_t, _ = win.run(host)
         float(loss_t.item())
     serial_s = max_over_ranks((time.perf_counter() - t0) / e2e_iters, world)
-    # streamed: the next window's H2D overlaps this window's kernels
-    win.run_pipelined([host] * 2)  # warm-up: captures the second buffer's graph
+    # streamed: the next window's H2D overlaps this window's kernels, and each
+    # window's product -- dL/d(actions), (T,N,A) fp32 -- is downloaded to
+    # pinned host memory on a third stream (full-duplex PCIe), with its loss
+    grads_host = [torch.empty_like(host).pin_memory() for _ in range(2)]
+    win.run_pipelined([host] * 2, grad_out=grads_host)  # warm-up: captures the second buffer's graph
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    win.run_pipelined([host] * e2e_iters)
+    win.run_pipelined([host] * e2e_iters, grad_out=[grads_host[k % 2] for k in range(e2e_iters)])
     e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_iters, world)
+    assert bool(torch.isfinite(grads_host[0]).all())
     e2e = {"value": world * N * T / e2e_s, "unit": UNIT, "h2d_bytes_per_step": host.numel() * 4,
-           "d2h_bytes_per_step": 8,
-           "api": "paper_2509_10247_b200.window.BpttWindow.run_pipelined(pinned host action batches)",
+           "d2h_bytes_per_step": grads_host[0].numel() * 4 + 8,
+           "api": "paper_2509_10247_b200.window.BpttWindow.run_pipelined(pinned host action batches, "
+                  "grad_out=pinned host gradient buffers)",
+           "timed": "host wall clock around the whole stream of windows (H2D actions, fwd+bwd, D2H dL/d(actions) "
+                    "and loss), max over ranks",
            "serial_value": world * N * T / serial_s,
-           "serial_api": "BpttWindow.run(host actions) + loss.item() per window"}
+           "serial_api": "BpttWindow.run(host actions) + loss.item() per window (gradient left on the device)"}
 
     # eager public API (env.step + torch.autograd) for reference, 1 window
     eager = None
@@ -819,6 +848,9 @@ def run_ours(a):
         "per_step_kernels": {"ms_per_window": ms_per_step_path,
                              "env_steps_per_s": world * N * T / (ms_per_step_path * 1e-3),
                              "note": "same window through the per-step kernels behind FlightTask.step"},
+        "dist": {"backend": DIST["backend"], "shared_gpu": DIST["shared_gpu"],
+                 "note": "ranks share GPUs (control flow only, not a scaling number)" if DIST["shared_gpu"]
+                 else "one GPU per rank"},
         "e2e": e2e, "e2e_eager": eager,
         "gpu_launches": a.steps * win.launches_per_window,
         "clocks": getattr(clk, "result", None),
@@ -864,8 +896,12 @@ def run_c5(a):
     """C5: SHAC-style differentiable training, pm_continuous position task,
     131,072 envs per GPU, horizon 16, GRU-64 + MLP-128^2 policy, privileged
     critic; policy/critic gradients averaged by NCCL all-reduce across ranks.
-    Reports training env-steps/s and the all-reduce time separately."""
+    Whole updates replay from one CUDA graph per rank (with NCCL the
+    all-reduces are captured inside it).  Reports training env-steps/s
+    (CUDA-event time, max over ranks) and the all-reduce device time
+    separately (the same collectives timed standalone with CUDA events)."""
     import torch
+    import torch.distributed as dist
 
     world, rank, local = dist_init()
     dev = torch.device("cuda", local if world > 1 else 0)
@@ -876,32 +912,60 @@ def run_c5(a):
     cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=N, episode_len=128)
     env = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
     env.reset(seed=1)
-    # whole updates replayed from a CUDA graph when single-rank (the eager
-    # update is host-bound: ~30 torch ops per policy step, autograd recording)
-    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0, cuda_graph=world == 1))
-    for _ in range(a.warmup):
+    graph = world == 1 or DIST["backend"] == "nccl"
+    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0, cuda_graph=graph))
+    for _ in range(max(a.warmup, 4 if graph else 1)):
         tr.update()
     torch.cuda.synchronize()
-    barrier(world)
-    tr.timing = {"sim_fwd_bwd_s": 0.0, "allreduce_s": 0.0}
-    t0 = time.perf_counter()
-    for _ in range(a.steps):
-        out = tr.update()
-    torch.cuda.synchronize()
-    el = max_over_ranks(time.perf_counter() - t0, world)
-    ar = max_over_ranks(tr.timing["allreduce_s"], world)
+    tr.allreduce_ms()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        barrier(world)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            out = tr.update()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier(world)
+    ms = max_over_ranks(e0.elapsed_time(e1) / a.steps, world)
+    ar_inline = max_over_ranks(tr.allreduce_ms() / a.steps, world)
+    # the update's collectives timed standalone: one policy all-reduce and
+    # critic_iters critic all-reduces per update, NCCL on the current stream
+    ar = {"policy_floats": sum(p.numel() for p in tr.policy.parameters()),
+          "critic_floats": sum(p.numel() for p in tr.value.parameters())}
+    if world > 1:
+        for key in ("policy_floats", "critic_floats"):
+            buf = torch.zeros(ar[key], device=dev if DIST["backend"] == "nccl" else "cpu")
+            for _ in range(5):
+                dist.all_reduce(buf)
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record()
+            for _ in range(50):
+                dist.all_reduce(buf)
+            f1.record()
+            torch.cuda.synchronize()
+            ar[key.replace("floats", "allreduce_ms")] = max_over_ranks(f0.elapsed_time(f1) / 50, world)
+        ar["per_update_ms"] = ar["policy_allreduce_ms"] + tr.opts.critic_iters * ar["critic_allreduce_ms"]
     if rank == 0:
         print(json.dumps({
-            "metric": "env-steps/s (SHAC train: policy + sim fwd+bwd + critic)", "value": world * N * 16 * a.steps / el,
-            "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": el / a.steps * 1e3,
+            "metric": "env-steps/s (SHAC train: policy + sim fwd+bwd + critic)", "value": world * N * 16 / (ms * 1e-3),
+            "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "dtype": "f32 sim, bf16 policy/critic matmuls",
+            "data": "synthetic (in-kernel Philox resets)",
             "config": {"workload": f"C5: SHAC, pm_continuous position, {N} envs/GPU x {world}, horizon 16",
-                       "parallelism": f"env-sharded x{world}; NCCL all-reduce of policy+critic grads"},
-            "allreduce_ms_per_update": ar / a.steps * 1e3, "last": out}))
+                       "parallelism": f"env-sharded x{world}; NCCL all-reduce of policy+critic grads",
+                       "cuda_graph": graph},
+            "dist": {"backend": DIST["backend"], "shared_gpu": DIST["shared_gpu"]},
+            "allreduce": ar, "allreduce_ms_per_update_eager": ar_inline if not graph else None,
+            "clocks": getattr(clk, "result", None), "last": out}))
 
 
 if __name__ == "__main__":
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)
     if args.impl == "reference":
         run_reference(args)
     elif args.workload == "c5":

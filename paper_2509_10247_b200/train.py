@@ -253,6 +253,22 @@ class ShortHorizonTrainer:
         self._graph = None
         self._graph_mode = graph
         self._warm = 0
+        self._capturing = False
+        self._ar_events = []
+
+    def _distributed(self) -> bool:
+        return dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1
+
+    def allreduce_ms(self) -> float:
+        """Device time (CUDA events, ms) of the policy-gradient all-reduces of
+        the eager updates since the last call (syncs).  Captured updates run
+        the collective inside the graph; bench.py times it standalone."""
+        if not self._ar_events:
+            return 0.0
+        self._ar_events[-1][1].synchronize()
+        ms = sum(a.elapsed_time(b) for a, b in self._ar_events)
+        self._ar_events = []
+        return ms
 
     def _nets(self):
         """autocast scope for policy/critic evaluations (no-op for fp32 / CPU);
@@ -307,9 +323,14 @@ class ShortHorizonTrainer:
         loss = -body / opts.horizon
         self.actor_opt.zero_grad(set_to_none=not self._graph_mode)
         loss.backward()
-        t1 = time.perf_counter()
+        timed = self._distributed() and not self._capturing
+        if timed:  # device time of the collective: events on the stream that waits for it
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         allreduce_mean_(list(self.policy.parameters()), self.group)
-        self.timing["allreduce_s"] += time.perf_counter() - t1
+        if timed:
+            e1.record()
+            self._ar_events.append((e0, e1))
         gnorm = clip_grads_(list(self.policy.parameters()), opts.grad_clip)
         self.actor_opt.step()
         closs = None
@@ -382,8 +403,9 @@ class ShortHorizonTrainer:
         eager updates on a side stream before capturing (lazy optimiser /
         autograd state); capturing executes nothing."""
         env = self.env
-        if dist.is_available() and dist.is_initialized() and dist.get_world_size(self.group) > 1:
-            raise RuntimeError("cuda_graph: single-rank only (NCCL all-reduce stays eager)")
+        if self._distributed() and dist.get_backend(self.group) != "nccl":
+            raise RuntimeError("cuda_graph with several ranks needs the NCCL backend (the all-reduce is "
+                               "captured into the graph; gloo collectives run on the host)")
         if env.strict or env.config.sensor != "none" or env.reset_source is not None or env._regen:
             raise RuntimeError("cuda_graph needs strict=False, no sensor, in-kernel resets and no scene regen")
         carry = {"S": env._S.detach().clone(), "goal": env._goal.clone(), "peff": env._peff.clone(),
@@ -409,9 +431,13 @@ class ShortHorizonTrainer:
         g = torch.cuda.CUDAGraph()
         g.register_generator_state(self._gen)
         bind()
-        with torch.cuda.graph(g):
-            out = self._update_tensors()
-            carry_back()
+        self._capturing = True
+        try:
+            with torch.cuda.graph(g):
+                out = self._update_tensors()
+                carry_back()
+        finally:
+            self._capturing = False
         bind()
         self._graph, self._graph_out = g, out
         self._carry = carry

@@ -215,31 +215,42 @@ class BpttWindow:
         if getattr(self, "_pipe", None) is not None:
             return
         dev = self.env.device
+        # two device action buffers and two gradient buffers, one graph each:
+        # window k reads actions[k%2] and writes dL/d actions into grads[k%2]
         bufs = [self.actions, torch.zeros_like(self.actions)]
+        gbufs = [self.g_actions, torch.zeros_like(self.g_actions)]
         graphs = []
-        keep = self.actions
-        for b in bufs:
-            self.actions = b
+        keep, gkeep = self.actions, self.g_actions
+        for b, gb in zip(bufs, gbufs):
+            self.actions, self.g_actions = b, gb
             self.graph = None
             self.capture()
             graphs.append(self.graph)
-        self.actions = keep
+        self.actions, self.g_actions = keep, gkeep
         self.graph = graphs[0]
-        self._pipe = {"bufs": bufs, "graphs": graphs, "copy": torch.cuda.Stream(dev),
-                      "loss_host": torch.zeros(2, dtype=torch.float64).pin_memory()}
+        self._pipe = {"bufs": bufs, "gbufs": gbufs, "graphs": graphs, "copy": torch.cuda.Stream(dev),
+                      "d2h": torch.cuda.Stream(dev)}
 
-    def run_pipelined(self, host_batches):
+    def run_pipelined(self, host_batches, grad_out=None):
         """Run one window per pinned host action batch (T,N,A); returns the
         host losses.  H2D of batch k+1 runs on a copy stream while window k
-        computes; each window's loss is read back with an async D2H copy."""
+        computes; each window's loss is read back with an async D2H copy.
+
+        ``grad_out``: optional list (one per batch) of pinned host (T,N,A)
+        tensors receiving each window's dL/d(actions) -- the product of a
+        BPTT window (q/learners.py:251-265).  The gradient download of window
+        k runs on a third stream, overlapped with window k+1's compute and
+        upload (PCIe is full duplex); all copies have landed on return."""
         self._refresh()
         self._ensure_pipeline()
         P = self._pipe
         comp = torch.cuda.current_stream(self.env.device)
-        cp = P["copy"]
+        cp, d2h = P["copy"], P["d2h"]
         free = [torch.cuda.Event(), torch.cuda.Event()]
         ready = [torch.cuda.Event(), torch.cuda.Event()]
-        for e in free:
+        computed = [torch.cuda.Event(), torch.cuda.Event()]
+        drained = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in free + drained:
             e.record(comp)
         losses = torch.zeros(len(host_batches), dtype=torch.float64).pin_memory()
 
@@ -257,8 +268,17 @@ class BpttWindow:
             if k + 1 < len(host_batches):
                 upload(k + 1)
             comp.wait_event(ready[b])
+            comp.wait_event(drained[b])  # window k-2's gradient has left grads[b]
             P["graphs"][b].replay()
             free[b].record(comp)
             losses[k].copy_(self.loss64, non_blocking=True)
+            if grad_out is not None:
+                computed[b].record(comp)
+                with torch.cuda.stream(d2h):
+                    d2h.wait_event(computed[b])
+                    grad_out[k].copy_(P["gbufs"][b], non_blocking=True)
+                    drained[b].record(d2h)
         comp.synchronize()
+        if grad_out is not None:
+            d2h.synchronize()
         return losses.tolist()

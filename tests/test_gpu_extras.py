@@ -190,3 +190,78 @@ def test_regen_scene_gradient_uses_pre_regeneration_course():
     assert float(grads[0].abs().max()) > 0
     assert torch.equal(grads[0], grads[1])
     assert torch.equal(grads[0], grads[2])
+
+
+@pytest.mark.parametrize("case", ["full_imu_window", "pm_dr_window", "avoid_regen_steps"])
+def test_sharding_invariance(case):
+    """Multi-GPU readiness: N envs in one env equal two
+    env_offset shards of N/2 bit for bit -- Philox spawns, DR draws, IMU noise
+    and (regenerated) obstacle courses are keyed by global env id, so results
+    do not depend on how envs are split over ranks."""
+    import paper_2509_10247_b200 as qs
+    from paper_2509_10247_b200.window import BpttWindow
+
+    if case == "avoid_regen_steps":
+        N, T = 512, 12
+        kw = dict(task="avoidance", dynamics="pm_continuous", episode_len=4, density=0.2,
+                  regen_scene_on_reset=True)
+    elif case == "pm_dr_window":
+        N, T = 2048, 16
+        kw = dict(task="position", dynamics="pm_continuous", episode_len=5,
+                  randomization=qs.world.RandomizationSpec(action_scale=(0.7, 1.0)))
+    else:
+        N, T = 2048, 16
+        kw = dict(task="position", dynamics="full", episode_len=5, imu=qs.ImuSpec(0.1, 0.01, 0.01, 0.001))
+    g = torch.Generator().manual_seed(4)
+    A = 4 if kw["dynamics"] == "full" else 3
+    acts = (torch.randn(T, N, A, generator=g) * 0.5).cuda()
+
+    def run(n, off):
+        env = qs.make_task(qs.TaskConfig(n_envs=n, **kw), strict=False, env_offset=off)
+        env.reset(seed=7)
+        a = acts[:, off:off + n]
+        if case == "avoid_regen_steps":
+            sph0 = env._scene.spheres.clone()
+            recs = []
+            with torch.no_grad():
+                for t in range(T):
+                    out = env.step(a[t])
+                    recs.append((env._S.clone(), out.r_rl.clone(), out.terminated.clone(), out.obs.proprio.clone()))
+            sc = env._scene
+            assert not torch.equal(sph0, sc.spheres)  # the courses were regenerated at the resets
+            return recs, (sc.spheres.clone(), sc.boxes.clone(), sc.cylinders.clone(), sc.counts.clone())
+        win = BpttWindow(env, T)
+        win.actions.copy_(a)
+        _, ga = win.run()
+        out = [win.S[1:].clone(), win.r.clone(), win.term.clone(), ga.clone()]
+        if win.imu is not None:
+            out.append(win.imu.clone())
+        if win.dr is not None:
+            out.append(win.dr[1:].clone())
+        return out, None
+
+    full, sc_full = run(N, 0)
+    h0, sc0 = run(N // 2, 0)
+    h1, sc1 = run(N // 2, N // 2)
+    if case == "avoid_regen_steps":
+        for (Sf, rf, tf, of), (S0, r0, t0, o0), (S1, r1, t1, o1) in zip(full, h0, h1):
+            assert torch.equal(Sf, torch.cat([S0, S1], 1))
+            assert torch.equal(rf, torch.cat([r0, r1])) and torch.equal(tf, torch.cat([t0, t1]))
+            assert torch.equal(of, torch.cat([o0, o1]))
+        for a, b, c in zip(sc_full, sc0, sc1):
+            k = min(a.shape[1], b.shape[1]) if a.dim() > 2 else None
+            assert torch.equal(a[:N // 2, :k] if k else a[:N // 2], b[:, :k] if k else b)
+            assert torch.equal(a[N // 2:, :k] if k else a[N // 2:], c[:, :k] if k else c)
+        return
+    # dL/d(actions) carries the loss's 1/(T N) factor: the halves' gradients
+    # are exactly twice the full batch's (a power-of-two scale commutes with
+    # every rounding of the linear VJP chain)
+    full[3] = full[3] * 2
+    # window buffers: rows are the last axis before the per-row payload
+    for f, a, b in zip(full, h0, h1):
+        if f.dim() == 4:  # S (T, NP, N, 4)
+            assert torch.equal(f, torch.cat([a, b], 2))
+        elif f.shape[1] == 3 and f.dim() == 3:  # r (T, 3, N)
+            assert torch.equal(f, torch.cat([a, b], 2))
+        else:  # (T, N, ...)
+            assert torch.equal(f, torch.cat([a, b], 1))

@@ -320,16 +320,20 @@ def test_pipelined_windows_match_sequential(qs):
     e1 = qs.make_task(cfg, strict=False)
     e1.reset(seed=2)
     w1 = BpttWindow(e1, 16).capture()
-    seq = []
+    seq, seq_g = [], []
     for b in batches:
-        loss, _ = w1.run(b)
+        loss, g1 = w1.run(b)
         seq.append(float(loss))
+        seq_g.append(g1.cpu())
     e2 = qs.make_task(cfg, strict=False)
     e2.reset(seed=2)
     w2 = BpttWindow(e2, 16)
-    pip = w2.run_pipelined(batches)
+    grads = [torch.empty_like(b).pin_memory() for b in batches]
+    pip = w2.run_pipelined(batches, grad_out=grads)
     np.testing.assert_allclose(pip, seq, rtol=1e-9)
     assert torch.equal(w1.S[0], w2.S[0])
+    for a, b in zip(grads, seq_g):  # every window's downloaded gradient
+        assert torch.equal(a, b)
 
 
 def test_philox_resets_are_valid_and_deterministic(qs):
