@@ -319,6 +319,25 @@ int qs_gen_obstacle_course(const qs_gen_cfg* cfg, int32_t n_envs, float* bounds,
                            float* spheres, float* boxes, float* cylinders, int32_t* counts,
                            float* ground_z, int32_t* err, void* stream);
 
+/* In-kernel race-track generation (replaces the reference's per-env host
+ * loop gen_race_track, q/world.py:347-379): gates chained along an open loop,
+ * spacing U(4, spread), heading turns U(-pi/6, pi/6) after the first gate,
+ * gate heights U(1, 2.5); Philox keyed by (seed, global env id, episode).
+ * Writes bounds (E,2,4), spawn_goal (E,2,4), gates (E,G,8) = centre, inner
+ * radius 0.8, normal, frame width 0.3; counts (E,4) = (0,0,0,1), ground_z 0.
+ * env_mask / episode as in qs_gen_cfg (regeneration on reset). */
+typedef struct qs_track_cfg {
+  int32_t n_gates;
+  float spread;
+  uint64_t seed;
+  int64_t env_offset;
+  const uint8_t* env_mask;
+  const int32_t* episode;
+  int32_t episode_stride;
+} qs_track_cfg;
+int qs_gen_race_track(const qs_track_cfg* cfg, int32_t n_envs, float* bounds, float* spawn_goal, float* gates,
+                      int32_t* counts, float* ground_z, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -101,6 +101,11 @@ class QsGenCfg(C.Structure):
                 ("env_offset", i64), ("env_mask", vp), ("episode", vp), ("episode_stride", i32)]
 
 
+class QsTrackCfg(C.Structure):
+    _fields_ = [("n_gates", i32), ("spread", f32), ("seed", u64), ("env_offset", i64), ("env_mask", vp),
+                ("episode", vp), ("episode_stride", i32)]
+
+
 P = C.POINTER
 _SIGS = {
     "qs_abi_version": ([], i32),
@@ -126,6 +131,7 @@ _SIGS = {
     "qs_philox4x32_10": ([i32, vp, vp, vp], i32),
     "qs_probe_fp32": ([i32, i32, i32, vp, vp], i32),
     "qs_gen_obstacle_course": ([P(QsGenCfg), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+    "qs_gen_race_track": ([P(QsTrackCfg), i32, vp, vp, vp, vp, vp, vp], i32),
 }
 
 _lib = None

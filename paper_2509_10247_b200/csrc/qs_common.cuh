@@ -243,6 +243,7 @@ enum : uint32_t {
   RNG_DR = 2u,
   RNG_IMU = 3u,
   RNG_SCENE = 4u,
+  RNG_TRACK = 5u,
 };
 
 struct Rng {

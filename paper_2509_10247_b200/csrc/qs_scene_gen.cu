@@ -404,3 +404,58 @@ extern "C" int qs_gen_obstacle_course(const qs_gen_cfg* cfg, int32_t n_envs, flo
                                                            boxes, cylinders, counts, ground_z, err);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
+
+// ---------------------------------------------------------------------------
+// race tracks (q/world.py:347-379), one thread per env: gate k sits
+// spacing_k along the running heading from gate k-1 (from the spawn for
+// k = 0), the heading turning by U(-pi/6, pi/6) before every gate but the
+// first, at height U(1, 2.5).  One Philox block per gate: (spacing, turn,
+// height).  Bounds: the gates' and spawn's extent +-5 m, floor 0, ceiling
+// max(top + 5, 4).
+
+namespace {
+__global__ void __launch_bounds__(128) k_track(const qs_track_cfg cfg, int n_envs, float* bounds, float* spawn_goal,
+                                               float* gates, int32_t* counts, float* ground_z) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n_envs) return;
+  if (cfg.env_mask && !cfg.env_mask[e]) return;
+  const uint32_t episode = cfg.episode ? (uint32_t)cfg.episode[(long)e * cfg.episode_stride] : 0u;
+  Rng rng(cfg.seed, (uint64_t)(e + cfg.env_offset), episode, RNG_TRACK);
+  const V3 spawn = v3(0.f, 0.f, 1.5f);
+  V3 pos = spawn, lo = spawn, hi = spawn;
+  float heading = 0.f;
+  const int G = cfg.n_gates;
+  for (int k = 0; k < G; ++k) {
+    const float4 u = rng.uniform4();
+    const float spacing = 4.f + (cfg.spread - 4.f) * u.x;
+    if (k) heading += (u.y * 2.f - 1.f) * 0.52359877559829887f;
+    float s, c;
+    sincosf(heading, &s, &c);
+    const V3 d = v3(c, s, 0.f);
+    pos = pos + d * spacing;
+    const V3 ctr = v3(pos.x, pos.y, 1.f + 1.5f * u.z);
+    float* g = gates + ((long)e * G + k) * 8;
+    reinterpret_cast<float4*>(g)[0] = make_float4(ctr.x, ctr.y, ctr.z, 0.8f);
+    reinterpret_cast<float4*>(g)[1] = make_float4(d.x, d.y, d.z, 0.3f);
+    lo = v3(fminf(lo.x, ctr.x), fminf(lo.y, ctr.y), fminf(lo.z, ctr.z));
+    hi = v3(fmaxf(hi.x, ctr.x), fmaxf(hi.y, ctr.y), fmaxf(hi.z, ctr.z));
+    if (k == G - 1) reinterpret_cast<float4*>(spawn_goal)[2 * e + 1] = make_float4(ctr.x, ctr.y, ctr.z, 0.f);
+  }
+  reinterpret_cast<float4*>(spawn_goal)[2 * e] = make_float4(spawn.x, spawn.y, spawn.z, 0.f);
+  reinterpret_cast<float4*>(bounds)[2 * e] = make_float4(lo.x - 5.f, lo.y - 5.f, 0.f, 0.f);
+  reinterpret_cast<float4*>(bounds)[2 * e + 1] = make_float4(hi.x + 5.f, hi.y + 5.f, fmaxf(hi.z + 5.f, 4.f), 0.f);
+  reinterpret_cast<int4*>(counts)[e] = make_int4(0, 0, 0, 1);
+  ground_z[e] = 0.f;
+}
+}  // namespace
+
+extern "C" int qs_gen_race_track(const qs_track_cfg* cfg, int32_t n_envs, float* bounds, float* spawn_goal,
+                                 float* gates, int32_t* counts, float* ground_z, void* stream) {
+  if (!cfg || n_envs < 0 || cfg->n_gates < 1 || cfg->n_gates > QS_MAX_GATES || !(cfg->spread >= 4.f))
+    return QS_ERR_BAD_ARGUMENT;
+  if (n_envs == 0) return QS_OK;
+  if (!bounds || !spawn_goal || !gates || !counts || !ground_z) return QS_ERR_BAD_ARGUMENT;
+  k_track<<<(n_envs + 127) / 128, 128, 0, (cudaStream_t)stream>>>(*cfg, n_envs, bounds, spawn_goal, gates, counts,
+                                                                 ground_z);
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}

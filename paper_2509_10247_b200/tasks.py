@@ -461,10 +461,12 @@ class FlightTask:
                                   style=c.style, r_quad=c.collision_radius, env_offset=self.env_offset)
             self._scene = wd.gen_obstacle_courses(self.seed, E, device=dev, check=self.strict, **self._gen_args)
             self.scenes = None
-        else:
-            self.scenes = [wd.gen_race_track((self.seed * 99_991 + e + self.env_offset) & 0x7FFFFFFF,
-                                             c.n_gates, c.gate_spread) for e in range(E)]
-            self._scene = wd.scenes_to_device(self.scenes, dev, n_gates=c.n_gates)
+        else:  # racing: device-generated tracks (q/world.py:347-379; reference tracks via scene_source)
+            if c.n_gates > L.MAX_GATES:
+                raise TaskContractError(f"n_gates must be <= {L.MAX_GATES}")
+            self._track_args = dict(n_gates=c.n_gates, spread=c.gate_spread, env_offset=self.env_offset)
+            self._scene = wd.gen_race_tracks(self.seed, E, device=dev, **self._track_args)
+            self.scenes = None
         if c.task == "racing" and self.n_agents != 1:
             raise TaskContractError("racing is single-agent")
         if c.task == "racing" and c.n_gates > L.MAX_GATES:
@@ -494,9 +496,9 @@ class FlightTask:
         self._steps_total = 0
         self._frame_cache = None
         c = self.config
-        if c.regen_scene_on_reset and (c.task != "avoidance" or self.scene_source is not None):
-            raise TaskContractError("regen_scene_on_reset needs the avoidance task with generated scenes "
-                                    "(no scene_source)")
+        if c.regen_scene_on_reset and (c.task == "position" or self.scene_source is not None):
+            raise TaskContractError("regen_scene_on_reset needs the avoidance or racing task with generated "
+                                    "scenes (no scene_source)")
         self._regen = bool(c.regen_scene_on_reset)
         self._build_scenes()
         self._alloc_persistent()
@@ -820,6 +822,10 @@ class FlightTask:
             return
         if cow:
             self._scene = self._scene.clone()
+        if self.config.task == "racing":
+            wd.gen_race_tracks(self.seed, self.n_envs, out=self._scene, env_mask=mask, episode=self._meta[:, 1],
+                               episode_stride=4, **self._track_args)
+            return
         wd.gen_obstacle_courses(self.seed, self.n_envs, check=False, out=self._scene, env_mask=mask,
                                 episode=self._meta[:, 1], episode_stride=4, err=self._err, **self._gen_args)
 

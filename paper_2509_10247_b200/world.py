@@ -2,9 +2,9 @@
 
 ``gen_obstacle_courses`` generates a whole batch of feasible obstacle courses
 in-kernel (``qs_gen_obstacle_course``: Philox sampling + grid-BFS
-feasibility, one CTA per env).  Race tracks are O(n_gates) host draws with
-the reference's own numpy PCG64 stream (``gen_race_track``) -- identical to
-the reference -- and ``randomize_params`` is the reference's host draw used by
+feasibility, one CTA per env); ``gen_race_tracks`` does the same for race
+tracks (``qs_gen_race_track``, one thread per env).  ``randomize_params`` is
+the reference's host draw used by
 reference-compatible reset providers; per-episode randomisation inside the
 rollout is drawn in-kernel (``qs_task_step_fwd``).
 """
@@ -202,42 +202,59 @@ def device_scene_to_scenes(sc: DeviceScene, style="outdoor", seed=0) -> list:
     bd = sc.bounds.double().cpu().numpy()
     sg = sc.spawn_goal.double().cpu().numpy()
     gz = sc.ground_z.double().cpu().numpy()
+    gt = sc.gates.double().cpu().numpy() if style == "racing" else None
     out = []
     for e in range(sc.n_envs):
         ns, nb, nc, hg = cnt[e]
         prims = PrimitiveSet(spheres=sph[e, :ns], boxes=np.concatenate([box[e, :nb, 0:3], box[e, :nb, 4:7]], -1),
                              cylinders=cyl[e, :nc, 0:5], ground_z=float(gz[e]) if hg else None)
+        gates = [] if gt is None else [Gate(center=g[0:3], normal=g[4:7], inner_radius=float(g[3]),
+                                            frame_width=float(g[7]), order=k) for k, g in enumerate(gt[e])]
         out.append(Scene(prims=prims, bounds_lo=bd[e, 0, :3], bounds_hi=bd[e, 1, :3], spawn=sg[e, 0, :3],
-                         goal=sg[e, 1, :3], seed=seed, style=style))
+                         goal=sg[e, 1, :3], gates=gates, seed=seed, style=style))
     return out
 
 
-def gen_race_track(seed: int, n_gates: int, spread: float = 10.0) -> Scene:
-    """q/world.py:347-379 (O(n_gates) host draws with the reference's PCG64 stream)."""
+def gen_race_tracks(seed: int, n_envs: int, n_gates: int, spread: float = 10.0, device=None, env_offset: int = 0,
+                    out: DeviceScene | None = None, env_mask=None, episode=None,
+                    episode_stride: int = 1) -> DeviceScene:
+    """Batch of race tracks generated on the GPU (q/world.py:347-379), one
+    thread per env, Philox keyed by (seed, global env id, episode): gates
+    chained along an open loop (spacing U(4, spread), heading turns
+    U(-pi/6, pi/6) after the first gate, heights U(1, 2.5)), goal at the last
+    gate, bounds the track's extent +-5 m with floor 0 and ceiling >= 4.
+
+    The reference draws each env's track with its own PCG64 stream on the host
+    (seeded ``(seed*99991 + e) & 0x7FFFFFFF``); those exact tracks can be
+    injected through ``FlightTask(scene_source=...)``.  With ``out`` /
+    ``env_mask`` / ``episode`` only the masked envs are regenerated, in place
+    and without a host sync (re-randomisation on reset)."""
     if n_gates < 1:
         raise GenerationError("need at least one gate", seed)
+    if n_gates > L.MAX_GATES:
+        raise GenerationError(f"n_gates must be <= {L.MAX_GATES}", seed)
     if spread < 4.0:
         raise GenerationError("spread must be >= 4 m", seed)
-    rng = np.random.default_rng(seed & 0x7FFFFFFF)
-    spawn = np.array([0.0, 0.0, 1.5])
-    heading = 0.0
-    pos = spawn.copy()
-    gates = []
-    for k in range(n_gates):
-        spacing = rng.uniform(4.0, spread)
-        heading += rng.uniform(-np.pi / 6, np.pi / 6) if k else 0.0
-        d = np.array([np.cos(heading), np.sin(heading), 0.0])
-        pos = pos + d * spacing
-        center = pos.copy()
-        center[2] = rng.uniform(1.0, 2.5)
-        gates.append(Gate(center=center, normal=d.copy(), order=k))
-    pts = np.array([g.center for g in gates] + [spawn])
-    lo = pts.min(axis=0) - 5.0
-    hi = pts.max(axis=0) + 5.0
-    lo[2] = 0.0
-    hi[2] = max(hi[2], 4.0)
-    return Scene(prims=PrimitiveSet(ground_z=0.0), bounds_lo=lo, bounds_hi=hi, spawn=spawn,
-                 goal=gates[-1].center.copy(), gates=gates, seed=seed, style="racing")
+    dev = L.require_cuda(device if out is None else out.device)
+    sc = out if out is not None else DeviceScene(n_envs, dev, n_gates=n_gates)
+    if sc.gates.shape[1] != n_gates:
+        raise GenerationError("scene gate table does not match n_gates", seed)
+    cfg = L.QsTrackCfg()
+    cfg.n_gates, cfg.spread = int(n_gates), float(spread)
+    cfg.seed = int(seed) & 0xFFFFFFFFFFFFFFFF
+    cfg.env_offset = int(env_offset)
+    cfg.env_mask, cfg.episode, cfg.episode_stride = L.ptr(env_mask), L.ptr(episode), int(episode_stride)
+    L.check(L.lib().qs_gen_race_track(cfg, n_envs, L.ptr(sc.bounds), L.ptr(sc.spawn_goal), L.ptr(sc.gates),
+                                      L.ptr(sc.counts), L.ptr(sc.ground_z), L.stream_handle(dev)),
+            "qs_gen_race_track")
+    return sc
+
+
+def gen_race_track(seed: int, n_gates: int, spread: float = 10.0, device=None) -> Scene:
+    """Single-track convenience wrapper (q/world.py:347 name) returning a host
+    ``Scene`` with its gates, generated by the device kernel."""
+    sc = gen_race_tracks(seed, 1, n_gates, spread, device)
+    return device_scene_to_scenes(sc, style="racing", seed=seed)[0]
 
 
 def scenes_to_device(scenes: list, device, n_gates: int = 0) -> DeviceScene:

@@ -555,12 +555,38 @@ def gen_c1():
         save(f"c1_{short}", **rec)
 
 
+# ---------------------------------------------------------------------------
+# wire / disk formats written by the reference: Scene JSON v1
+# (q/world.py:72-111) for an outdoor course, an indoor course and a race
+# track, and DAIM depth / LiDAR dumps (q/sensors.py:614-642)
+
+
+def gen_formats():
+    import json
+
+    scenes = [wd.gen_obstacle_course(41, np.array([0.0, 0.0, 1.2]), np.array([8.0, 0.0, 1.5]), 0.12),
+              wd.gen_obstacle_course(42, np.array([0.0, 0.0, 1.2]), np.array([8.0, 0.0, 1.5]), 0.1, style="indoor"),
+              wd.gen_race_track(43, 5, 10.0)]
+    with open(os.path.join(OUT, "scenes_v1.json"), "w") as f:
+        json.dump([s.to_json() for s in scenes], f)
+    prims = sn.pack_primitives([scenes[0].prims])
+    R = np.eye(3)[None]
+    depth = sn.render_depth(prims, np.array([[0.5, 0.2, 1.2]]), R, sn.CameraIntrinsics(width=64, height=48))
+    sn.write_depth_dump(os.path.join(OUT, "depth_64x48.daim"), depth[0], frame_index=7)
+    lidar = sn.render_lidar(prims, np.array([[0.5, 0.2, 1.2]]), R, sn.LidarPattern(n_azimuth=36, n_elevation=4))
+    sn.write_depth_dump(os.path.join(OUT, "lidar_36x4.daim"), lidar[0], frame_index=3)
+    np.savez_compressed(os.path.join(OUT, "formats.npz"), depth=depth[0], lidar=lidar[0])
+    print("wrote scenes_v1.json, depth_64x48.daim, lidar_36x4.daim, formats.npz")
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners", "nets_ppo", "c1"]
+    which = sys.argv[1:] or ["dynamics", "sensors", "imu", "world", "tasks", "learners", "nets_ppo", "c1", "formats"]
     if "nets_ppo" in which:
         gen_nets_ppo()
     if "c1" in which:
         gen_c1()
+    if "formats" in which:
+        gen_formats()
     if "learners" in which:
         gen_learners()
     if "dynamics" in which:

@@ -265,3 +265,82 @@ def test_sharding_invariance(case):
             assert torch.equal(f, torch.cat([a, b], 2))
         else:  # (T, N, ...)
             assert torch.equal(f, torch.cat([a, b], 1))
+
+
+def test_device_race_tracks_follow_reference_distribution():
+    """qs_gen_race_track (q/world.py:347-379 on the GPU, Philox): the track
+    geometry the reference generates -- consecutive gate spacing in [4, spread]
+    along the running heading, heading turns within +-pi/6 after the first
+    gate, heights U(1, 2.5), normals = travel direction, spawn (0,0,1.5), goal
+    at the last gate, bounds = extent +-5 m with floor 0 and ceiling >= 4 --
+    with the reference's first moments; deterministic and keyed by global env
+    id; 16,384 tracks per launch."""
+    import paper_2509_10247_b200 as qs
+    from oracle import quadsim_oracle as O
+
+    E, G, spread = 16384, 5, 10.0
+    sc = qs.world.gen_race_tracks(3, E, G, spread)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5):
+        qs.world.gen_race_tracks(4, E, G, spread, out=sc)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    print(f"\n16,384 race tracks: {ms * 1e3:.1f} us per batch")
+    assert ms < 10.0
+    sc = qs.world.gen_race_tracks(3, E, G, spread)
+    gt = sc.gates.double().cpu().numpy()
+    c, n = gt[..., 0:3], gt[..., 4:7]
+    prev = np.concatenate([np.tile([[[0.0, 0.0, 1.5]]], (E, 1, 1)), c[:, :-1]], 1)
+    step = c[..., :2] - prev[..., :2]
+    spacing = np.linalg.norm(step, axis=-1)
+    assert spacing.min() >= 4.0 - 1e-4 and spacing.max() <= spread + 1e-4
+    np.testing.assert_allclose(step / spacing[..., None], n[..., :2], atol=1e-4)  # normal = travel direction
+    assert np.abs(n[..., 2]).max() == 0.0 and np.allclose(n[:, 0], [1.0, 0.0, 0.0], atol=1e-6)
+    head = np.arctan2(n[..., 1], n[..., 0])
+    turn = np.angle(np.exp(1j * np.diff(head, axis=1)))
+    assert np.abs(turn).max() <= np.pi / 6 + 1e-5
+    assert c[..., 2].min() >= 1.0 and c[..., 2].max() <= 2.5
+    assert np.all(gt[..., 3] == np.float32(0.8)) and np.all(gt[..., 7] == np.float32(0.3))
+    # first moments against the reference generator (the oracle restates it)
+    ref = [O.gen_race_track(s, G, spread) for s in range(2000)]
+    rc = np.stack([[g[0] for g in t.gates] for t in ref])
+    rprev = np.concatenate([np.tile([[[0.0, 0.0, 1.5]]], (2000, 1, 1)), rc[:, :-1]], 1)
+    rsp = np.linalg.norm(rc[..., :2] - rprev[..., :2], axis=-1)
+    assert abs(spacing.mean() - rsp.mean()) < 0.1 and abs(spacing.std() - rsp.std()) < 0.1
+    assert abs(c[..., 2].mean() - rc[..., 2].mean()) < 0.03
+    bd = sc.bounds.double().cpu().numpy()
+    sg = sc.spawn_goal.double().cpu().numpy()
+    pts = np.concatenate([c, np.tile([[[0.0, 0.0, 1.5]]], (E, 1, 1))], 1)
+    np.testing.assert_allclose(bd[:, 0, :2], pts[..., :2].min(1) - 5.0, atol=1e-4)
+    np.testing.assert_allclose(bd[:, 1, :2], pts[..., :2].max(1) + 5.0, atol=1e-4)
+    assert np.all(bd[:, 0, 2] == 0.0) and np.all(bd[:, 1, 2] >= 4.0)
+    np.testing.assert_allclose(sg[:, 1, :3], c[:, -1], atol=0)
+    assert np.all(sg[:, 0, :3] == [0.0, 0.0, 1.5])
+    # deterministic, and keyed by global env id (sharding-invariant)
+    again = qs.world.gen_race_tracks(3, E, G, spread)
+    half = qs.world.gen_race_tracks(3, E // 2, G, spread, env_offset=E // 2)
+    assert torch.equal(again.gates, sc.gates) and torch.equal(half.gates, sc.gates[E // 2:])
+
+
+def test_racing_env_regenerates_tracks_on_reset():
+    """regen_scene_on_reset for racing: a done env gets a new device-generated
+    track keyed by its new episode; envs that did not reset keep theirs."""
+    import paper_2509_10247_b200 as qs
+
+    cfg = qs.TaskConfig(task="racing", dynamics="pm_continuous", n_envs=256, episode_len=3, n_gates=4,
+                        regen_scene_on_reset=True)
+    env = qs.make_task(cfg, strict=False)
+    env.reset(seed=12)
+    g0 = env.gate_centers.clone()
+    with torch.no_grad():
+        for _ in range(3):
+            out = env.step(torch.zeros(256, 3, device="cuda"))
+    done = out.done.cpu().numpy()
+    assert done.all()  # truncation at episode_len
+    g1 = env.gate_centers
+    changed = (g1 != g0).flatten(1).any(1).cpu().numpy()
+    assert changed.all()
+    assert torch.equal(env.goals, g1[:, 0])  # respawned toward the new first gate

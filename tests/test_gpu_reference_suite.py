@@ -407,7 +407,7 @@ def _through_gate(qs, env, offset):
 def test_racing_gate_arrays_and_initial_goal(qs):  # :864-867, 887-891
     env = qs.make_task(race_cfg(qs))
     env.reset(seed=31)
-    g = env.scenes[0].gates
+    g = qs.world.device_scene_to_scenes(env._scene, style="racing")[0].gates
     assert env.gate_centers.shape == (1, 3, 3)
     np.testing.assert_allclose(np_(env.gate_centers[0]), np.stack([x.center for x in g]), atol=1e-6)
     np.testing.assert_allclose(np_(env.gate_normals[0]), np.stack([x.normal for x in g]), atol=1e-6)
