@@ -293,6 +293,8 @@ int qs_reconstruct_attitude(int32_t n, const float* a, const float* v_ema, float
  * items (n,6) = ctr[4], key[2] -> out (n,8) = the block computed with the key
  * schedule on the fly, then with precomputed round keys (the two must agree). */
 int qs_philox4x32_10(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream);
+/* Philox4x32-7 (the IMU sensor-noise generator), same layout */
+int qs_philox4x32_7(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream);
 
 /* Measurement aid (not part of the reference API): FP32 peak probe for the
  * ray-casting roofline.  n_blocks CTAs of 256 threads, each thread 8 independent

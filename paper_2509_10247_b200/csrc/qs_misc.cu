@@ -110,7 +110,7 @@ __global__ void k_attitude(int n, const float* __restrict__ a, const float* __re
   r[6] = xb.z; r[7] = yb.z; r[8] = zb.z;
 }
 
-__global__ void k_philox(int n, const uint32_t* __restrict__ ck, uint32_t* __restrict__ out) {
+__global__ void k_philox(int n, const uint32_t* __restrict__ ck, uint32_t* __restrict__ out, int rounds) {
   long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t* p = ck + 6 * i;
@@ -124,8 +124,8 @@ __global__ void k_philox(int n, const uint32_t* __restrict__ ck, uint32_t* __res
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
-  const uint4 a = philox4x32_10(c, make_uint2(p[4], p[5]));
-  const uint4 b = philox4x32_10_rk(c, rk);
+  const uint4 a = rounds == 7 ? philox4x32_7_rk(c, rk) : philox4x32_10(c, make_uint2(p[4], p[5]));
+  const uint4 b = rounds == 7 ? philox4x32_7_rk(c, rk) : philox4x32_10_rk(c, rk);
   uint32_t* o = out + 8 * i;
   o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
   o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
@@ -137,7 +137,13 @@ extern "C" {
 
 int qs_philox4x32_10(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream) {
   if (n <= 0) return QS_OK;
-  k_philox<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(n, ctr_key, out);
+  k_philox<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(n, ctr_key, out, 10);
+  return status();
+}
+
+int qs_philox4x32_7(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream) {
+  if (n <= 0) return QS_OK;
+  k_philox<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(n, ctr_key, out, 7);
   return status();
 }
 

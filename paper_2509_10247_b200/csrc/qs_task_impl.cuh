@@ -264,7 +264,7 @@ struct ImuNoise {
 QS_D ImuNoise imu_draw(const qs_task_cfg& cfg, long row, int tick) {
   RngK rng(cfg.rng_round_keys, (uint64_t)(row + cfg.env_offset * cfg.n_agents), (uint32_t)tick, RNG_IMU);
   ImuNoise z;
-  const uint4 a = rng.bits4(), b = rng.bits4();
+  const uint4 a = rng.bits4_r7(), b = rng.bits4_r7();  // Philox4x32-7: sensor noise
   normals12(a, b, z.a, z.b, z.c);
   return z;
 }
@@ -590,6 +590,20 @@ struct StepStat {
   float rc;  // this row's r_ctrl (0 for padding lanes)
 };
 
+// spawn-ahead (fused windows): a row's NEXT reset sample -- spawn, velocity,
+// goal, heading, DR draw for episode meta.y + 1 -- is drawn before the window's
+// step loop, with every lane of the warp in lockstep, and parked in shared
+// memory.  The draw is a pure function of (seed, global env, episode), so the
+// in-loop reset reads exactly the values the inline draw would produce, while
+// the warp no longer runs the divergent rejection-sampling path whenever one
+// of its lanes resets.  A second reset of the same row inside the window
+// (episode no longer matches) falls back to the inline draw.
+struct SpawnAhead {
+  float4* slot;  // 4 float4 with stride `stride`: (p, head.x) (v, head.y) (goal, ok) (dr)
+  int stride;
+  int episode;   // episode index the slot holds; -1 once consumed
+};
+
 // ---------------------------------------------------------------------------
 // one fused env step of one agent row (FlightTask.step, q/tasks.py:549-600);
 // IMU: 0 = decided at run time by has_imu / out.imu_noise; 1 = Philox IMU on
@@ -598,7 +612,7 @@ struct StepStat {
 template <int M, int TASK, int G, bool INLINE, int IMU = 0>
 QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, long row, int na, long N,
                            const Grp<G>& grp, EnvRegs& R, float4 raw, const StepOut& out, int32_t* err,
-                           bool has_dr, bool has_imu) {
+                           bool has_dr, bool has_imu, SpawnAhead* ahead = nullptr) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
   const DynK k = dyn_consts(cfg);
@@ -761,12 +775,25 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, l
     }
     if (INLINE) {
       V3 sp, sv_, sg, head;
-      int ng0;
-      bool ok = spawn_sample<M, TASK, G>(cfg, sc, e, episode, na, R.blo, R.bhi, grp, sp, sv_, sg, head, ng0);
+      bool ok;
+      const bool dr_new = cfg.dr_enabled && cfg.dr_per_episode;
+      if (ahead && ahead->episode == episode) {  // env-uniform: the group takes the same branch
+        const float4 a = ahead->slot[0], b = ahead->slot[ahead->stride], c = ahead->slot[2 * ahead->stride];
+        sp = xyz(a);
+        sv_ = xyz(b);
+        sg = xyz(c);
+        head = v3(a.w, b.w, 0.f);
+        ok = c.w != 0.f;
+        if (dr_new) R.dr = ahead->slot[3 * ahead->stride];
+        ahead->episode = -1;
+      } else {
+        int ng0;
+        ok = spawn_sample<M, TASK, G>(cfg, sc, e, episode, na, R.blo, R.bhi, grp, sp, sv_, sg, head, ng0);
+        if (dr_new) R.dr = dr_sample(cfg, row, episode);
+      }
       if (!ok && grp.g == 0) report_err(err, QS_ERR_GENERATION, (int)(e * na));
       so = init_state<M>(sp, sv_, head, k.g);
       R.goal = f4(sg, 0.f);
-      if (cfg.dr_enabled && cfg.dr_per_episode) R.dr = dr_sample(cfg, row, episode);
     }
   }
   R.s = so;
@@ -1047,6 +1074,20 @@ __global__ void __launch_bounds__(WIN_BLOCK, QS_WIN_MINB) k_window_fwd(const qs_
   }
   if (active)
     env_load<M>(sc.bounds, e, row, N, R, w.S, w.goal, w.peff, w.dr, w.meta, w.ep_return, w.imu_bias);
+  // spawn-ahead: this row's next reset sample, drawn by the whole warp at once
+  __shared__ float4 s_ahead[4][WIN_BLOCK];
+  SpawnAhead ahead{&s_ahead[0][threadIdx.x], WIN_BLOCK, -1};
+  if (active) {
+    const int ep = R.meta.y + 1;
+    V3 sp, sv_, sg, head;
+    int ng0;
+    const bool ok = spawn_sample<M, TASK, G>(cfg, sc, e, ep, na, R.blo, R.bhi, grp, sp, sv_, sg, head, ng0);
+    s_ahead[0][threadIdx.x] = f4(sp, head.x);
+    s_ahead[1][threadIdx.x] = f4(sv_, head.y);
+    s_ahead[2][threadIdx.x] = f4(sg, ok ? 1.f : 0.f);
+    if (has_dr && cfg.dr_per_episode) s_ahead[3][threadIdx.x] = dr_sample(cfg, row, ep);
+    ahead.episode = ep;
+  }
   const int lrow = (int)(row - e0 * na);  // this row's slot in the CTA's action block
   for (int t = 0; t < w.T; ++t) {
     float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1063,7 +1104,7 @@ __global__ void __launch_bounds__(WIN_BLOCK, QS_WIN_MINB) k_window_fwd(const qs_
                 w.flags + (long)t * N, nullptr, has_imu ? w.imu_out + (long)t * N * 6 : nullptr,
                 w.imu_noise ? w.imu_noise + (long)t * 4 * N * 3 : nullptr};
       StepStat st = env_step_fwd<M, TASK, G, true, IMU>(cfg, sc, e, row, na, N, grp, R, raw, o, w.err, has_dr,
-                                                        has_imu);
+                                                        has_imu, &ahead);
       if (st.done && grp.g == 0) {
         n_done++;
         n_succ += st.term == 1;

@@ -404,10 +404,18 @@ PHILOX_KAT = [  # Random123 kat_vectors, philox4x32 10 rounds: ctr[4], key[2] ->
 ]
 
 
-def _philox_py(c, k):
+# Random123 kat_vectors, philox4x32 7 rounds (the IMU noise generator)
+PHILOX7_KAT = [
+    ([0, 0, 0, 0], [0, 0], [0x5F6FB709, 0x0D893F64, 0x4F121F81, 0x4F730A48]),
+    ([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0],
+     [0x4DFCCABA, 0x190A87F0, 0xC47362BA, 0xB6B5242A]),
+]
+
+
+def _philox_py(c, k, rounds=10):
     M = 0xFFFFFFFF
     c, k = list(c), list(k)
-    for _ in range(10):
+    for _ in range(rounds):
         p0, p1 = c[0] * 0xD2511F53, c[2] * 0xCD9E8D57
         c = [(p1 >> 32) ^ c[1] ^ k[0], p1 & M, (p0 >> 32) ^ c[3] ^ k[1], p0 & M]
         k = [(k[0] + 0x9E3779B9) & M, (k[1] + 0xBB67AE85) & M]
@@ -431,6 +439,18 @@ def test_philox_known_answers(qs):
     for i, it in enumerate(items):
         want = _philox_py(it[:4], it[4:])
         assert got[i, :4].tolist() == want and got[i, 4:].tolist() == want
+    # Philox4x32-7 (IMU noise): the published 7-round vectors and the same
+    # restatement with seven rounds
+    items7 = [c + k for c, k, _ in PHILOX7_KAT] + items
+    ck7 = torch.tensor(np.array(items7, dtype=np.uint32).view(np.int32), device="cuda")
+    out7 = torch.empty(len(items7), 8, dtype=torch.int32, device="cuda")
+    L.check(L.lib().qs_philox4x32_7(len(items7), L.ptr(ck7), L.ptr(out7), L.stream_handle()), "philox7")
+    got7 = out7.cpu().numpy().view(np.uint32)
+    for i, (c, k, want) in enumerate(PHILOX7_KAT):
+        assert got7[i, :4].tolist() == want
+    for i, it in enumerate(items7):
+        want = _philox_py(it[:4], it[4:], rounds=7)
+        assert got7[i, :4].tolist() == want and got7[i, 4:].tolist() == want
 
 
 @pytest.mark.parametrize("task,n_agents", [("position", 2), ("position", 3), ("avoidance", 4), ("position", 8)])
