@@ -250,7 +250,7 @@ QS_D DynK dyn_consts(const qs_task_cfg& c) {
 QS_D State step_full(const State& s, float4 cmd, const DynK& k) {
   const float dt = k.dt;
   const Q4 q = s.q;
-  V3 zb = qrot(q, v3(0.f, 0.f, 1.f));
+  V3 zb = qaxis_z(q);
   V3 vdot = k.g + zb * cmd.x;
   if (k.has_drag) {
     V3 vb = qrot(qconj(q), s.v);
@@ -304,9 +304,9 @@ QS_D void step_full_vjp(const State& s, float4 cmd, const DynK& k, const State& 
   V3 gvdot = gs.v * dt;
   gi.p = gs.p;
   gi.v = gs.v + gs.p * dt;
-  V3 zb = qrot(q, v3(0.f, 0.f, 1.f));
+  V3 zb = qaxis_z(q);
   float gcx = dot(gvdot, zb);
-  Q4 gzq = qrot_vjp_q(q, v3(0.f, 0.f, 1.f), gvdot * cmd.x);
+  Q4 gzq = qaxis_z_vjp(q, gvdot * cmd.x);
   gq_tot = q4(gq_tot.w + gzq.w, gq_tot.x + gzq.x, gq_tot.y + gzq.y, gq_tot.z + gzq.z);
   if (k.has_drag) {
     // drag = rot(q, D (.) rot(conj q, v)); vdot -= drag

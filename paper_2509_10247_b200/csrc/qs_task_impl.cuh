@@ -70,7 +70,7 @@ QS_D int observe_row(const qs_task_cfg& cfg, const State& s, float2 cs, V3 goal,
     o[8] = zl.z;
     k = 9;
   } else if (M == QS_MODEL_FULL) {
-    V3 zl = unrotz(cs, qrot(s.q, v3(0.f, 0.f, 1.f)));
+    V3 zl = unrotz(cs, qaxis_z(s.q));
     o[6] = zl.x;
     o[7] = zl.y;
     o[8] = zl.z;
@@ -877,7 +877,7 @@ QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, long 
       g.r2 += rotz(cs2, v3(go[6], go[7], go[8]));
     } else if (M == QS_MODEL_FULL) {
       V3 gz = rotz(cs2, v3(go[6], go[7], go[8]));
-      Q4 gq = qrot_vjp_q(n.q, v3(0.f, 0.f, 1.f), gz);
+      Q4 gq = qaxis_z_vjp(n.q, gz);
       g.q = q4(g.q.w + gq.w, g.q.x + gq.x, g.q.y + gq.y, g.q.z + gq.z);
       g.w += v3(go[9], go[10], go[11]);
     } else {
@@ -939,7 +939,7 @@ QS_D void env_step_bwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, long 
     float* gout = g_raw_t + row * A;
 #pragma unroll
     for (int kk = 0; kk < A; ++kk) {
-      float t = tanh_fast(f4get(raw, kk));
+      const float t = f4get(q.t, kk);  // tanh(raw), from the squash above
       gout[kk] = f4get(gsq, kk) * rp.half[kk] * (1.f - t * t);
     }
   }
