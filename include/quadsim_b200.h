@@ -86,6 +86,8 @@ typedef struct qs_task_cfg {
   float imu_sqrt_dt;                 /* sqrt(dt) */
   uint32_t rng_round_keys[20];       /* Philox round keys of `seed`: written by the library
                                         on its private copy, ignored on input */
+  int32_t guard;  /* step forward: skip the whole launch when err[2] != INT32_MAX (set by
+                     qs_task_validate), so a rejected step mutates nothing */
 } qs_task_cfg;
 
 /* Per-env scene data (read-only during a rollout).  Obstacles are packed
@@ -184,6 +186,15 @@ int qs_state_planes(int32_t model);
  * EMA -> rewards -> termination -> auto-reset -> observe, fused per env. */
 int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
                      void* stream);
+/* Contract check of FlightTask.step's inputs before anything is mutated
+ * (q/tasks.py:551-558, q/dynamics.py:130-133): every row's raw action and
+ * model state must be finite.  Writes atomicMin(err[2], code << 27 | row) --
+ * the reference's precedence: the lowest non-finite action row
+ * (QS_ERR_NONFINITE_ACTION), else the lowest non-finite state row
+ * (QS_ERR_NONFINITE_STATE).  err must hold 3 ints, err[2] = INT32_MAX when
+ * clean.  Paired with qs_task_cfg.guard = 1 on the step launched after it,
+ * one host read of err[2] gives raise-before-mutate semantics. */
+int qs_task_validate(const qs_task_cfg* cfg, const qs_step_io* io, void* stream);
 /* Analytic VJP of qs_task_step_fwd (replaces the tape backward of the ops
  * recorded by FlightTask.step; subgradients per q/autodiff.py). */
 int qs_task_step_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_grad* g,

@@ -54,7 +54,7 @@ class QsTaskCfg(C.Structure):
         ("imu_gyro_rw", f32),
         ("reset_mode", i32), ("want_cam", i32),
         ("act_center", f32 * 4), ("act_half", f32 * 4), ("imu_sqrt_dt", f32),
-        ("rng_round_keys", C.c_uint32 * 20),
+        ("rng_round_keys", C.c_uint32 * 20), ("guard", i32),
     ]
 
 
@@ -112,6 +112,7 @@ _SIGS = {
     "qs_proprio_dim": ([i32, i32], i32),
     "qs_state_planes": ([i32], i32),
     "qs_task_step_fwd": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp], i32),
+    "qs_task_validate": ([P(QsTaskCfg), P(QsStepIo), vp], i32),
     "qs_task_step_bwd": ([P(QsTaskCfg), P(QsScene), P(QsStepGrad), vp], i32),
     "qs_task_spawn": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp, P(QsResetTable), vp], i32),
     "qs_task_observe": ([P(QsTaskCfg), P(QsScene), P(QsStepIo), vp], i32),
@@ -136,10 +137,60 @@ _SIGS = {
 }
 
 _lib = None
+_ops = None
+OPS_PATH = os.path.join(_PKG, "_qs_torch_ops.so")
 
 
 class QuadsimLibraryError(RuntimeError):
     pass
+
+
+def ops():
+    """``torch.ops.quadsim``: the torch custom-op layer over the C ABI
+    (``csrc/qs_torch_ops.cpp``; raises when it is missing: no fallback)."""
+    global _ops
+    if _ops is None:
+        lib()
+        if not os.path.exists(OPS_PATH):
+            raise QuadsimLibraryError(
+                f"{OPS_PATH} is missing; build it with `python -m paper_2509_10247_b200.build`")
+        torch.ops.load_library(OPS_PATH)
+        _register_fakes()
+        _ops = torch.ops.quadsim
+    return _ops
+
+
+def _register_fakes():
+    """Shape (fake) implementation of quadsim::task_step for FakeTensor /
+    torch.compile tracing: the outputs' shapes follow from S_in, the
+    action-free flags and proprio_dim (the cfg bytes stay on the host)."""
+
+    @torch.library.register_fake("quadsim::task_step")
+    def _task_step_fake(cfg, scene, S_in, raw, bufs, imu_noise, want_cam, strict, proprio_dim):
+        N = S_in.shape[1]
+        f = dict(dtype=torch.float32, device=S_in.device)
+        has_dr, has_imu = bufs[2].numel() > 0, bufs[5].numel() > 0
+        return [torch.empty_like(S_in), S_in.new_empty((N, proprio_dim)), S_in.new_empty(N), S_in.new_empty(N),
+                S_in.new_empty(N), torch.empty(N, dtype=torch.int8, device=S_in.device),
+                torch.empty(N, dtype=torch.bool, device=S_in.device),
+                torch.empty(N, dtype=torch.int32, device=S_in.device), torch.empty(N, 4, **f),
+                torch.empty(N, 4, **f), torch.empty(N if has_dr else 0, 4, **f),
+                torch.empty(N if want_cam else 0, 2, **f), torch.empty(N if has_imu else 0, 6, **f)]
+
+
+_fast = None
+
+
+def fast_ops():
+    """The op library's direct Python entry points (same kernels and C++
+    autograd node as torch.ops.quadsim, without the generic boxing)."""
+    global _fast
+    if _fast is None:
+        ops()
+        import importlib
+
+        _fast = importlib.import_module("paper_2509_10247_b200._qs_torch_ops")
+    return _fast
 
 
 def lib():

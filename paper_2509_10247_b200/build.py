@@ -50,6 +50,41 @@ def _compile(src: str, obj: str) -> tuple[str, str]:
     return src, r.stderr
 
 
+TORCH_OPS_SRC = os.path.join(CSRC, "qs_torch_ops.cpp")
+TORCH_OPS_LIB = os.path.join(PKG, "_qs_torch_ops.so")
+
+
+def build_torch_ops(force: bool = False, verbose: bool = False) -> str:
+    """The torch custom-op layer (``quadsim::task_step``): one C++ file
+    compiled against torch's headers, linked to ``libquadsim_b200.so``
+    (rpath $ORIGIN) and loaded with ``torch.ops.load_library``."""
+    deps = [TORCH_OPS_SRC, LIB, os.path.join(INCLUDE, "quadsim_b200.h")]
+    if not force and os.path.exists(TORCH_OPS_LIB) and \
+            os.path.getmtime(TORCH_OPS_LIB) >= max(os.path.getmtime(d) for d in deps):
+        return TORCH_OPS_LIB
+    import torch
+    from torch.utils import cpp_extension as ce
+
+    import sysconfig
+
+    incs = ce.include_paths(device_type="cuda") + [sysconfig.get_paths()["include"]]
+    libs = ce.library_paths(device_type="cuda")
+    abi = int(torch._C._GLIBCXX_USE_CXX11_ABI)
+    cxx = os.environ.get("CXX") or shutil.which("g++") or "g++"
+    cmd = [cxx, "-O2", "-std=c++17", "-fPIC", "-shared", f"-D_GLIBCXX_USE_CXX11_ABI={abi}", TORCH_OPS_SRC,
+           "-o", TORCH_OPS_LIB + ".tmp"] + [f"-I{i}" for i in incs] + [f"-L{d}" for d in libs] + [
+           "-DTORCH_EXTENSION_NAME=_qs_torch_ops", "-DTORCH_API_INCLUDE_EXTENSION_H",
+           "-ltorch", "-ltorch_cpu", "-ltorch_cuda", "-ltorch_python", "-lc10", "-lc10_cuda", "-lcudart",
+           f"-L{PKG}", "-lquadsim_b200", "-Wl,-rpath,$ORIGIN"] + [f"-Wl,-rpath,{d}" for d in libs]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"torch op layer build failed:\n{r.stderr[-4000:]}")
+    os.replace(TORCH_OPS_LIB + ".tmp", TORCH_OPS_LIB)
+    if verbose:
+        print("compiled qs_torch_ops.cpp", file=sys.stderr)
+    return TORCH_OPS_LIB
+
+
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
@@ -74,6 +109,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
         os.replace(tmp, LIB)
+    build_torch_ops(force=force, verbose=verbose)
     return LIB
 
 

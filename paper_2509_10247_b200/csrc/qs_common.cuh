@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <climits>
+
 #include "../../include/quadsim_b200.h"
 
 #define QS_HD __host__ __device__ __forceinline__

@@ -1,4 +1,6 @@
 // C ABI for the fused task step (include/quadsim_b200.h).
+#include <climits>
+
 #include "qs_dynamics.cuh"
 
 namespace qs {
@@ -19,6 +21,29 @@ int task_dispatch(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void
 }
 
 namespace {
+// q/tasks.py:551-558 then q/dynamics.py:130-133: key = code << 27 | row, so
+// atomicMin picks the lowest action row, else the lowest state row
+template <int M>
+__global__ void __launch_bounds__(256) k_task_validate(const qs_task_cfg cfg, const qs_step_io io) {
+  constexpr int A = ModelTraits<M>::A;
+  const long N = (long)cfg.n_envs * cfg.n_agents;
+  const long row = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  int key = INT_MAX;
+  if (row < N) {
+    bool act_ok = true;
+#pragma unroll
+    for (int k = 0; k < A; ++k) act_ok = act_ok && isfinite(__ldg(io.raw + row * A + k));
+    const State s = load_state<M>(io.S_in, N, row);
+    if (!act_ok)
+      key = (QS_ERR_NONFINITE_ACTION << 27) | (int)row;
+    else if (!state_finite<M>(s))
+      key = (QS_ERR_NONFINITE_STATE << 27) | (int)row;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+  if ((threadIdx.x & 31) == 0 && key != INT_MAX) atomicMin(io.err + 2, key);
+}
+
 int task_call(int op, const qs_task_cfg* cfg, const qs_scene* sc, const void* p,
               const uint8_t* mask, const qs_reset_table* tab, void* stream) {
   if (!cfg || !sc || !p) return QS_ERR_BAD_ARGUMENT;
@@ -53,6 +78,23 @@ int qs_state_planes(int32_t model) {
 int qs_task_step_fwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_io* io,
                      void* stream) {
   return task_call(0, cfg, scene, io, nullptr, nullptr, stream);
+}
+
+int qs_task_validate(const qs_task_cfg* cfg, const qs_step_io* io, void* stream) {
+  if (!cfg || !io || !io->raw || !io->S_in || !io->err) return QS_ERR_BAD_ARGUMENT;
+  const long N = (long)cfg->n_envs * cfg->n_agents;
+  if (N <= 0) return QS_OK;
+  if (N >= (1L << 27)) return QS_ERR_BAD_ARGUMENT;
+  const int grid = (int)((N + 255) / 256);
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (cfg->model) {
+    case QS_MODEL_FULL: k_task_validate<QS_MODEL_FULL><<<grid, 256, 0, s>>>(*cfg, *io); break;
+    case QS_MODEL_PM_CONTINUOUS: k_task_validate<QS_MODEL_PM_CONTINUOUS><<<grid, 256, 0, s>>>(*cfg, *io); break;
+    case QS_MODEL_PM_DISCRETE: k_task_validate<QS_MODEL_PM_DISCRETE><<<grid, 256, 0, s>>>(*cfg, *io); break;
+    case QS_MODEL_SIMPLIFIED: k_task_validate<QS_MODEL_SIMPLIFIED><<<grid, 256, 0, s>>>(*cfg, *io); break;
+    default: return QS_ERR_BAD_ARGUMENT;
+  }
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 
 int qs_task_step_bwd(const qs_task_cfg* cfg, const qs_scene* scene, const qs_step_grad* g,

@@ -973,6 +973,7 @@ __global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const q
   const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
   const Grp<G> grp = Grp<G>::make(na);
   const long N = (long)cfg.n_envs * na;
+  if (cfg.guard && io.err && io.err[2] != INT_MAX) return;  // rejected by qs_task_validate: mutate nothing
   StepStat st{false, 0, 0.f, 0.f};
   if (rm.active) {
     EnvRegs R;

@@ -166,6 +166,11 @@ class DeviceScene:
         for k in ("spheres", "boxes", "cylinders", "counts", "ground_z", "bounds", "spawn_goal", "gates"):
             getattr(self, k)[e_slice] = getattr(other, k)
 
+    def tensors(self) -> list:
+        """The scene as the op layer takes it (quadsim::task_step's ``scene``)."""
+        return [self.bounds, self.spawn_goal, self.spheres, self.boxes, self.cylinders, self.counts,
+                self.ground_z, self.gates]
+
     def struct(self) -> L.QsScene:
         s = L.QsScene()
         s.bounds = self.bounds.data_ptr()

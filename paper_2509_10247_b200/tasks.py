@@ -4,10 +4,11 @@ Mirrors ``q/tasks.py`` (TaskConfig, make_task, FlightTask.reset/step/observe/
 detach_states, StepOutput, the TERM_* codes and contract errors) on torch CUDA
 tensors.  ``FlightTask.step`` is ONE fused sm_100a kernel per env
 (``qs_task_step_fwd``: squash -> yaw frame -> dynamics -> EMA -> rewards ->
-termination -> auto-reset -> observation [-> IMU]) wrapped in a
-``torch.autograd.Function`` whose backward is the analytic VJP kernel
-(``qs_task_step_bwd``).  It saves only the step's checkpoint (state, raw
-action, goal, previous effort, per-row params, a 4-byte flag record).
+termination -> auto-reset -> observation [-> IMU]) behind the torch custom op
+``quadsim::task_step`` (``csrc/qs_torch_ops.cpp``), whose C++ autograd node
+runs the analytic VJP kernel (``qs_task_step_bwd``) as its backward.  It saves
+only the step's checkpoint (state, raw action, goal, previous effort, per-row
+params, a 4-byte flag record).
 
 Batch layout is env-major: row = env * n_agents + agent.
 """
@@ -207,51 +208,6 @@ def _fill_weights(dst: L.QsWeights, w: RewardWeights):
         setattr(dst, name, float(getattr(w, name)))
 
 
-class _StepBufs:
-    __slots__ = ("S_in", "raw", "goal_in", "peff_in", "dr_in", "S_out", "goal_out", "peff_out", "dr_out",
-                 "obs", "r_ctrl", "r_goal", "r_rl", "term", "trunc", "flags", "cam", "imu_out", "imu_noise")
-
-
-class _TaskStepFn(torch.autograd.Function):
-    """Autograd node of one fused env step (forward + analytic VJP kernels)."""
-
-    @staticmethod
-    def forward(ctx, S_in, raw, env):
-        ctx.set_materialize_grads(False)
-        # the scene this step's SDF penalty was evaluated against: a course
-        # regenerated during the step (regen_scene_on_reset) is written into a
-        # copy, so this node's backward keeps the pre-regeneration course
-        scene = env._scene
-        b = env._launch_step(S_in, raw, cow_scene=bool(ctx.needs_input_grad[0] or ctx.needs_input_grad[1]))
-        ctx.save_for_backward(S_in, raw)
-        ctx.env_cfg = env._cfg
-        ctx.scene = scene
-        ctx.rec = (b.goal_in, b.peff_in, b.dr_in, b.flags)
-        ctx.P = b.obs.shape[1]
-        env._pending = b
-        return b.S_out, b.obs, b.r_ctrl
-
-    @staticmethod
-    def backward(ctx, gS, gobs, gr):
-        if gS is None and gobs is None and gr is None:
-            return None, None, None
-        S_in, raw = ctx.saved_tensors
-        goal_in, peff_in, dr_in, flags = ctx.rec
-        gS_in = torch.empty_like(S_in)
-        g_raw = torch.empty_like(raw)
-        gs = L.QsStepGrad()
-        gs.S_in, gs.raw, gs.goal_in, gs.peff_in = L.ptr(S_in), L.ptr(raw), L.ptr(goal_in), L.ptr(peff_in)
-        gs.dr_in, gs.flags = L.ptr(dr_in), L.ptr(flags)
-        gS = gS.contiguous() if gS is not None else None
-        gobs = gobs.contiguous() if gobs is not None else None
-        gr = gr.contiguous() if gr is not None else None
-        gs.g_S_out, gs.g_obs, gs.g_rctrl = L.ptr(gS), L.ptr(gobs), L.ptr(gr)
-        gs.g_S_in, gs.g_raw = L.ptr(gS_in), L.ptr(g_raw)
-        L.check(L.lib().qs_task_step_bwd(ctx.env_cfg, ctx.scene.struct(), gs,
-                                         L.stream_handle(S_in.device)), "qs_task_step_bwd")
-        return gS_in, g_raw, None
-
-
 class FlightTask:
     """Batched environment (q/tasks.py:198-655) on one CUDA device.
 
@@ -297,7 +253,6 @@ class FlightTask:
         self._episode_counter = 0
         self._regen = False
         self._S = None
-        self._pending = None
 
     # -- spec of the policy-visible observation (q/tasks.py:225-297)
 
@@ -480,7 +435,10 @@ class FlightTask:
         self._meta = torch.zeros(E, 4, dtype=torch.int32, device=dev)
         self._ep_ret = torch.zeros(E, **f)
         self._stats = torch.zeros(4, dtype=torch.float64, device=dev)
-        self._err = torch.tensor([0, _INT_MAX], dtype=torch.int32, device=dev)
+        # {code, first row} of kernel-reported errors; [2]: qs_task_validate's
+        # code << 27 | row key (strict steps)
+        self._err = torch.tensor([0, _INT_MAX, _INT_MAX], dtype=torch.int32, device=dev)
+        self._empty = torch.empty(0, dtype=torch.float32, device=dev)
         self._imu_bias = torch.zeros(N, 8, **f) if self.config.imu is not None else None
 
     def _new_io(self):
@@ -503,6 +461,8 @@ class FlightTask:
         self._build_scenes()
         self._alloc_persistent()
         self._cfg = self._build_cfg()
+        self._cfg_blob = torch.frombuffer(bytearray(bytes(self._cfg)), dtype=torch.uint8)  # quadsim::task_step
+        self._ops = L.fast_ops()
         dev, N = self.device, self.N
         NP = L.lib().qs_state_planes(L.MODEL_IDS[self.config.dynamics])
         f = dict(device=dev, dtype=torch.float32)
@@ -730,24 +690,22 @@ class FlightTask:
     def _check_inputs(self, raw: torch.Tensor):
         if tuple(raw.shape) != (self.N, self.action_dim):
             raise TaskContractError(f"action shape {tuple(raw.shape)} != {(self.N, self.action_dim)}")
-        if self.strict:
-            finite = torch.isfinite(raw).all(dim=-1)
-            if not bool(finite.all()):
-                bad = int(torch.argmin(finite.to(torch.int8)))
-                raise TaskContractError(f"non-finite action for env row {bad}")
-            for name, v in self.state.fields().items():
-                if not bool(torch.isfinite(v).all()):
-                    raise dyn.ContractError(f"non-finite state field '{name}'")
 
     def check_errors(self):
         """Raise the contract error recorded by the kernels (syncs)."""
         self._raise_errors()
 
     def _raise_errors(self):
-        code, row = self._err.tolist()
+        code, row, key = self._err.tolist()  # the one host read of a strict step
+        if key != _INT_MAX:  # qs_task_validate: the step was rejected before anything changed
+            code, row = key >> 27, key & ((1 << 27) - 1)
+            self._err[2] = _INT_MAX
+            if code == L.QS_ERR_NONFINITE_ACTION:
+                raise TaskContractError(f"non-finite action for env row {row}")
+            raise dyn.ContractError(f"non-finite state (row {row})")
         if code == 0:
             return
-        self._err.copy_(torch.tensor([0, _INT_MAX], dtype=torch.int32))
+        self._err.copy_(torch.tensor([0, _INT_MAX, _INT_MAX], dtype=torch.int32))
         if code == L.QS_ERR_NONFINITE_ACTION:
             raise TaskContractError(f"non-finite action for env row {row}")
         if code == L.QS_ERR_NONFINITE_STATE:
@@ -756,58 +714,35 @@ class FlightTask:
             raise wd.GenerationError(f"could not sample a reset (row {row})", self.seed)
         raise L.QuadsimLibraryError(f"device error code {code} at row {row}")
 
-    def _launch_step(self, S_in, raw, cow_scene: bool = False) -> _StepBufs:
-        dev, N = self.device, self.N
-        f = dict(device=dev, dtype=torch.float32)
-        b = _StepBufs()
-        b.S_in, b.raw = S_in, raw
-        b.goal_in, b.peff_in, b.dr_in = self._goal, self._peff, self._dr
-        b.S_out = torch.empty_like(S_in)
-        b.goal_out = torch.empty_like(self._goal)
-        b.peff_out = torch.empty_like(self._peff)
-        b.dr_out = torch.empty_like(self._dr) if self._dr is not None else None
-        b.obs = torch.empty(N, self.proprio_dim, **f)
-        b.r_ctrl = torch.empty(N, **f)
-        b.r_goal = torch.empty(N, **f)
-        b.r_rl = torch.empty(N, **f)
-        b.term = torch.empty(N, dtype=torch.int8, device=dev)
-        b.trunc = torch.empty(N, dtype=torch.bool, device=dev)
-        b.flags = torch.empty(N, dtype=torch.int32, device=dev)
-        b.cam = torch.empty(N, 2, **f) if self.config.sensor != "none" else None
-        b.imu_out = torch.empty(N, 6, **f) if self._imu_bias is not None else None
-        b.imu_noise = None
-        if self._imu_bias is not None and self.imu_noise_source is not None:
-            b.imu_noise = torch.as_tensor(np.asarray(self.imu_noise_source(self._steps_total)),
-                                          dtype=torch.float32, device=dev).reshape(4, N, 3).contiguous()
+    def _deferred_resets(self, out, cow_scene: bool):
+        """reset_mode 1 (injected reset draws, or scene regeneration that must
+        precede the spawn): the step kernel left the done rows un-reset; spawn
+        them now and re-observe (q/tasks.py:583-594)."""
+        S_out, obs, flags, goal_out, peff_out, dr_out, cam, imu_out = (out[0], out[1], out[7], out[8], out[9],
+                                                                        out[10], out[11], out[12])
         io = self._new_io()
-        io.S_in, io.S_out, io.raw = L.ptr(S_in), L.ptr(b.S_out), L.ptr(raw)
-        io.goal_in, io.goal_out = L.ptr(b.goal_in), L.ptr(b.goal_out)
-        io.peff_in, io.peff_out = L.ptr(b.peff_in), L.ptr(b.peff_out)
-        io.dr_in, io.dr_out = L.ptr(b.dr_in), L.ptr(b.dr_out)
-        io.imu_noise, io.imu_out = L.ptr(b.imu_noise), L.ptr(b.imu_out)
-        io.obs, io.r_ctrl, io.r_goal, io.r_rl = L.ptr(b.obs), L.ptr(b.r_ctrl), L.ptr(b.r_goal), L.ptr(b.r_rl)
-        io.terminated, io.truncated, io.flags, io.cam = L.ptr(b.term), L.ptr(b.trunc), L.ptr(b.flags), L.ptr(b.cam)
-        stream = L.stream_handle(dev)
-        L.check(L.lib().qs_task_step_fwd(self._cfg, self._scene.struct(), io, stream), "qs_task_step_fwd")
-        if self._cfg.reset_mode == 1:  # deferred resets
-            if self.reset_source is not None:  # host-injected draws (syncs on the done mask)
-                done_env = (b.flags.view(self.n_envs, self.n_agents)[:, 0] & 1).cpu().numpy().astype(bool)
-                if done_env.any():
-                    ids = np.flatnonzero(done_env)
-                    tab, keep = self._reset_table(ids)
-                    self._regen_scenes(keep["mask"], cow_scene)
-                    L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, tab.env_mask, tab,
-                                                  stream), "qs_task_spawn")
-                    self._episode_counter += 1
-                    del keep
-            else:  # device-only: done mask -> new course -> Philox spawn, no host sync
-                mask = (b.flags.view(self.n_envs, self.n_agents)[:, 0] & 1).to(torch.uint8)
-                self._regen_scenes(mask, cow_scene)
-                L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, L.ptr(mask), None, stream),
+        io.S_out, io.goal_out, io.peff_out = L.ptr(S_out), L.ptr(goal_out), L.ptr(peff_out)
+        io.dr_out = L.ptr(dr_out) if dr_out.numel() else None
+        io.obs, io.flags = L.ptr(obs), L.ptr(flags)
+        io.cam = L.ptr(cam) if cam.numel() else None
+        stream = L.stream_handle(self.device)
+        if self.reset_source is not None:  # host-injected draws (syncs on the done mask)
+            done_env = (flags.view(self.n_envs, self.n_agents)[:, 0] & 1).cpu().numpy().astype(bool)
+            if done_env.any():
+                ids = np.flatnonzero(done_env)
+                tab, keep = self._reset_table(ids)
+                self._regen_scenes(keep["mask"], cow_scene)
+                L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, tab.env_mask, tab, stream),
                         "qs_task_spawn")
-            L.check(L.lib().qs_task_observe(self._cfg, self._scene.struct(), io, stream), "qs_task_observe")
-            self._frame_cache = None
-        return b
+                self._episode_counter += 1
+                del keep
+        else:  # device-only: done mask -> new course -> Philox spawn, no host sync
+            mask = (flags.view(self.n_envs, self.n_agents)[:, 0] & 1).to(torch.uint8)
+            self._regen_scenes(mask, cow_scene)
+            L.check(L.lib().qs_task_spawn(self._cfg, self._scene.struct(), io, L.ptr(mask), None, stream),
+                    "qs_task_spawn")
+        L.check(L.lib().qs_task_observe(self._cfg, self._scene.struct(), io, stream), "qs_task_observe")
+        self._frame_cache = None
 
     def _regen_scenes(self, mask, cow: bool = False):
         """Re-randomise the obstacle course of every env in ``mask`` (uint8, device),
@@ -834,20 +769,31 @@ class FlightTask:
         raw = raw.to(device=self.device, dtype=torch.float32)
         self._check_inputs(raw)
         raw = raw.contiguous()
-        S_out, obs, r_ctrl = _TaskStepFn.apply(self._S, raw, self)
-        b = self._pending
-        self._pending = None
-        self._S, self._goal, self._peff = S_out, b.goal_out, b.peff_out
-        if b.dr_out is not None:
-            self._dr = b.dr_out
-        self._steps_total += 1
-        self._last_flags = b.flags
-        visual = self._render(S_out, b.cam) if self.config.sensor != "none" else None
-        imu = (b.imu_out[:, 0:3], b.imu_out[:, 3:6]) if b.imu_out is not None else None
-        if self.strict:
+        noise = None
+        if self._imu_bias is not None and self.imu_noise_source is not None:
+            noise = torch.as_tensor(np.asarray(self.imu_noise_source(self._steps_total)), dtype=torch.float32,
+                                    device=self.device).reshape(4, self.N, 3).contiguous()
+        E = self._empty
+        bufs = [self._goal, self._peff, self._dr if self._dr is not None else E, self._meta, self._ep_ret,
+                self._imu_bias if self._imu_bias is not None else E, self._stats, self._err]
+        # one dispatcher call: the fused step kernel (quadsim::task_step); with
+        # strict=True a validation kernel runs first and guards the step
+        out = self._ops.task_step(self._cfg_blob, self._scene.tensors(), self._S, raw, bufs, noise,
+                                  self.config.sensor != "none", self.strict, self._cfg.proprio_dim)
+        if self.strict:  # raise-before-mutate: a rejected step changed nothing
             self._raise_errors()
-        return StepOutput(obs=Obs(proprio=obs, visual=visual, imu=imu), r_ctrl=r_ctrl, r_goal=b.r_goal,
-                          r_rl=b.r_rl, terminated=b.term, truncated=b.trunc)
+        if self._cfg.reset_mode == 1:
+            self._deferred_resets(out, cow_scene=bool(self._S.requires_grad or raw.requires_grad))
+        S_out, obs, r_ctrl, r_goal, r_rl, term, trunc, flags, goal_out, peff_out, dr_out, cam, imu_out = out
+        self._S, self._goal, self._peff = S_out, goal_out, peff_out
+        if self._dr is not None:
+            self._dr = dr_out
+        self._steps_total += 1
+        self._last_flags = flags
+        visual = self._render(S_out, cam) if self.config.sensor != "none" else None
+        imu = (imu_out[:, 0:3], imu_out[:, 3:6]) if self._imu_bias is not None else None
+        return StepOutput(obs=Obs(proprio=obs, visual=visual, imu=imu), r_ctrl=r_ctrl, r_goal=r_goal,
+                          r_rl=r_rl, terminated=term, truncated=trunc)
 
     def state_records(self):
         return {k: v.detach().cpu().tolist() for k, v in self.state.fields().items()}
