@@ -304,6 +304,9 @@ int qs_reconstruct_attitude(int32_t n, const float* a, const float* v_ema, float
  * items (n,6) = ctr[4], key[2] -> out (n,8) = the block computed with the key
  * schedule on the fly, then with precomputed round keys (the two must agree). */
 int qs_philox4x32_10(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream);
+/* tcgen05 self-test: D (128x128 fp32) = A (128x128) @ B (128x128), bf16 operands
+ * staged K-major or MN-major (mode bit 0: A, bit 1: B) in shared memory */
+int qs_probe_umma(int32_t mode, const float* A, const float* B, float* D, void* stream);
 /* Philox4x32-7 (the IMU sensor-noise generator), same layout */
 int qs_philox4x32_7(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream);
 

@@ -132,6 +132,7 @@ _SIGS = {
     "qs_philox4x32_10": ([i32, vp, vp, vp], i32),
     "qs_philox4x32_7": ([i32, vp, vp, vp], i32),
     "qs_probe_fp32": ([i32, i32, i32, vp, vp], i32),
+    "qs_probe_umma": ([i32, vp, vp, vp, vp], i32),
     "qs_gen_obstacle_course": ([P(QsGenCfg), i32, vp, vp, vp, vp, vp, vp, vp, vp, vp], i32),
     "qs_gen_race_track": ([P(QsTrackCfg), i32, vp, vp, vp, vp, vp, vp], i32),
 }
