@@ -275,6 +275,13 @@ int qs_mlp3_fit_grad(int64_t m, int32_t k, const float* x, const float* scale, c
                      const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
                      float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
                      int32_t n_sm, void* stream);
+/* The same fit step on the 5th-generation tensor cores (tcgen05.mma, TMEM
+ * accumulators, one persistent 128-thread CTA per SM): k <= 14 (the two spare
+ * input columns carry the bias and w2 gradients through the MMAs). */
+int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
+                        const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
+                        float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
+                        int32_t n_sm, void* stream);
 
 /* sdf_np / sdf_var (q/sensors.py:417-501): points (N,4); out (N,); grad (N,4) | NULL */
 int qs_sdf(const qs_scene* scene, int32_t n_rows, int32_t n_agents, const float* pts, float* out,

@@ -23,7 +23,7 @@
 // accumulators, biases and all gradients are fp32.
 #include <cuda_bf16.h>
 
-#include "qs_common.cuh"
+#include "qs_umma.cuh"
 
 namespace {
 
@@ -349,9 +349,302 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// The same fit step on the 5th-generation tensor cores (tcgen05).  One
+// persistent 128-thread CTA per SM walks 128-row tiles; thread t owns row t of
+// a tile and TMEM lane t.  Operands live in shared memory in the blocked
+// no-swizzle layout of qs_umma.cuh, so every activation tile is written once
+// and read by the MMAs both as a K-major operand (next layer) and as an
+// MN-major one (weight gradients, K = the tile's rows).  Accumulators live in
+// TMEM (512 columns):
+//   [0,128)   G1 / G2 / G3 results of the current tile (reused in turn)
+//   [128,256) dW1 = sum over tiles of H1^T dZ2          (lane = hid1 row)
+//   [256,272) dW0^T | db0 = dZ1^T X                     (lane = hid1; col 15 = db0)
+//   [272,288) db1 = dZ2^T X, column 15                  (lane = hid2)
+//   [288,304) dw2 = H2^T X, column 14 (X col 14 holds dL/dpred) (lane = hid2)
+// X's padding columns carry the bias / w2 gradients through the same MMAs:
+// column 15 is all ones (column sums), column 14 receives dL/dpred after the
+// forward.  Hence K <= 14 input features (the privileged state has 14).
+// Per tile, one thread issues: G1 (X W0), G2 (H1 W1), then G3 (dZ2 W1^T), G4
+// (H1^T dZ2), db1, dw2, then G5 (dZ1^T X); tcgen05.commit -> mbarrier hands each
+// group to the 128 epilogue threads (TMEM -> registers -> bias / tanh / chain
+// rule -> bf16 -> shared memory).
+
+constexpr int TC_THREADS = 128;
+constexpr int TC_KMAX = 14;
+
+struct TcSmem {
+  __nv_bfloat16 X[TILE * KIN];     // [rows][16]   blocked
+  __nv_bfloat16 W0T[HID * KIN];    // [hid1][16]   blocked (K-major B of G1)
+  __nv_bfloat16 W1T[HID * HID];    // [hid2][hid1] blocked (K-major B of G2, MN-major B of G3)
+  __nv_bfloat16 H1[TILE * HID];    // [rows][hid1]
+  __nv_bfloat16 D2[TILE * HID];    // [rows][hid2]  dZ2
+  __nv_bfloat16 H2[TILE * HID];    // [rows][hid2]
+  __nv_bfloat16 D1[TILE * HID];    // [rows][hid1]  dZ1
+  float b0[HID], b1[HID], w2[HID];
+  float red[2];                    // db2, loss
+  uint64_t bar;
+  uint32_t tbase;
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_mlp3_fit_grad_tc(int64_t M, int K, float inv_m, const float* __restrict__ x, const float* __restrict__ scale,
+                       const float* __restrict__ y, const float* __restrict__ W0, const float* __restrict__ b0,
+                       const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ w2,
+                       const float* __restrict__ b2, float* __restrict__ gW0, float* __restrict__ gb0,
+                       float* __restrict__ gW1, float* __restrict__ gb1, float* __restrict__ gw2,
+                       float* __restrict__ gb2, float* __restrict__ loss) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
+  using umma::blk_off;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // ---- parameters -> shared memory (bf16 operands, fp32 vectors)
+  for (int i = tid; i < HID * KIN; i += TC_THREADS) {
+    const int n = i / KIN, k = i % KIN;  // W0T[n][k] = W0[k][n]
+    S.W0T[blk_off(n, k, KIN)] = __float2bfloat16_rn(k < K ? W0[k * HID + n] : 0.f);
+  }
+  for (int i = tid; i < HID * HID; i += TC_THREADS) {
+    const int k = i / HID, n = i % HID;  // W1[k][n] -> W1T[n][k]
+    S.W1T[blk_off(n, k, HID)] = __float2bfloat16_rn(W1[i]);
+  }
+  for (int i = tid; i < HID; i += TC_THREADS) {
+    S.b0[i] = b0[i];
+    S.b1[i] = b1[i];
+    S.w2[i] = w2[i];
+  }
+  if (tid < 2) S.red[tid] = 0.f;
+  if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
+  if (tid == 0) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t T0 = S.tbase;
+  const uint32_t T_G = T0, T_W1 = T0 + 128, T_W0 = T0 + 256, T_B1 = T0 + 272, T_W2 = T0 + 288;
+  const uint32_t id_128 = umma::idesc_bf16(128, 128, false, false);
+  const uint32_t id_128_bmn = umma::idesc_bf16(128, 128, false, true);
+  const uint32_t id_128_mn = umma::idesc_bf16(128, 128, true, true);
+  const uint32_t id_16_mn = umma::idesc_bf16(128, 16, true, true);
+  const uint32_t my = umma::taddr(0, 32 * warp, 0);  // this warp's TMEM lanes
+  const float bias2 = b2[0];
+  uint32_t phase = 0;
+  bool first = true;
+  float gb2_acc = 0.f, loss_acc = 0.f;
+  auto sync_to_mma = [&]() {  // epilogue writes -> visible to the tensor cores, then hand over
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  };
+  auto wait_mma = [&]() {
+    umma::mbar_wait_parity(&S.bar, phase);
+    phase ^= 1u;
+    umma::fence_after();
+  };
+  const int64_t ntiles = (M + TILE - 1) / TILE;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row = tile * TILE + tid;
+    const bool valid = row < M;
+    // ---- X tile: row tid, scaled features, col 14 <- dL/dpred later, col 15 = 1
+    {
+      float v[KIN];
+#pragma unroll
+      for (int c = 0; c < KIN; ++c) v[c] = 0.f;
+      if (valid) {
+#pragma unroll
+        for (int c = 0; c < TC_KMAX; ++c)
+          if (c < K) v[c] = __ldg(x + row * K + c) * __ldg(scale + c);
+      }
+      v[KIN - 1] = 1.f;
+#pragma unroll
+      for (int c = 0; c < KIN; c += 8) {
+        uint4 pk;
+        pk.x = pack_bf16(v[c], v[c + 1]);
+        pk.y = pack_bf16(v[c + 2], v[c + 3]);
+        pk.z = pack_bf16(v[c + 4], v[c + 5]);
+        pk.w = pack_bf16(v[c + 6], v[c + 7]);
+        *reinterpret_cast<uint4*>(&S.X[blk_off(tid, c, KIN)]) = pk;
+      }
+    }
+    sync_to_mma();
+    // ---- G1: X W0 -> T_G
+    if (tid == 0) {
+      umma::mma_bf16(T_G, umma::desc_kmajor(S.X, KIN), umma::desc_kmajor(S.W0T, KIN), id_128, false);
+      umma::commit(&S.bar);
+    }
+    wait_mma();
+    // ---- epilogue 1: H1 = tanh(. + b0) -> smem
+#pragma unroll 1
+    for (int c0 = 0; c0 < HID; c0 += 16) {
+      float v[16];
+      umma::tmem_ld16(T_G + my + c0, v);
+      uint4 pk[2];
+      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2)
+        pw[j / 2] = pack_bf16(tanh_mufu(v[j] + S.b0[c0 + j]), tanh_mufu(v[j + 1] + S.b0[c0 + j + 1]));
+      *reinterpret_cast<uint4*>(&S.H1[blk_off(tid, c0, HID)]) = pk[0];
+      *reinterpret_cast<uint4*>(&S.H1[blk_off(tid, c0 + 8, HID)]) = pk[1];
+    }
+    sync_to_mma();
+    // ---- G2: H1 W1 -> T_G
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < HID / 16; ++ks)
+        umma::mma_bf16(T_G, umma::desc_kmajor(S.H1 + ks * 128, HID), umma::desc_kmajor(S.W1T + ks * 128, HID),
+                       id_128, ks > 0);
+      umma::commit(&S.bar);
+    }
+    wait_mma();
+    // ---- epilogue 2: H2 = tanh(. + b1), pred, dL/dpred, dZ2 = dpred w2 (1 - H2^2)
+    float pred = bias2;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HID; c0 += 16) {
+      float v[16];
+      umma::tmem_ld16(T_G + my + c0, v);
+      uint4 pk[2];
+      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const float h0 = tanh_mufu(v[j] + S.b1[c0 + j]), h1 = tanh_mufu(v[j + 1] + S.b1[c0 + j + 1]);
+        pred = fmaf(h0, S.w2[c0 + j], fmaf(h1, S.w2[c0 + j + 1], pred));
+        pw[j / 2] = pack_bf16(h0, h1);
+      }
+      *reinterpret_cast<uint4*>(&S.H2[blk_off(tid, c0, HID)]) = pk[0];
+      *reinterpret_cast<uint4*>(&S.H2[blk_off(tid, c0 + 8, HID)]) = pk[1];
+    }
+    const float e = valid ? pred - __ldg(y + row) : 0.f;
+    const float dp = 2.f * inv_m * e;
+    loss_acc += e * e;
+    gb2_acc += dp;
+#pragma unroll 1
+    for (int c0 = 0; c0 < HID; c0 += 16) {  // the fp32 H2 again (TMEM is cheap to re-read)
+      float v[16];
+      umma::tmem_ld16(T_G + my + c0, v);
+      uint4 pk[2];
+      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const float h0 = tanh_mufu(v[j] + S.b1[c0 + j]), h1 = tanh_mufu(v[j + 1] + S.b1[c0 + j + 1]);
+        pw[j / 2] = pack_bf16(dp * S.w2[c0 + j] * (1.f - h0 * h0), dp * S.w2[c0 + j + 1] * (1.f - h1 * h1));
+      }
+      *reinterpret_cast<uint4*>(&S.D2[blk_off(tid, c0, HID)]) = pk[0];
+      *reinterpret_cast<uint4*>(&S.D2[blk_off(tid, c0 + 8, HID)]) = pk[1];
+    }
+    S.X[blk_off(tid, KIN - 2, KIN)] = __float2bfloat16_rn(dp);  // X col 14 <- dL/dpred (for dw2)
+    sync_to_mma();
+    // ---- G3: dZ2 W1^T -> T_G;  G4: dW1 += H1^T dZ2;  db1 += dZ2^T 1;  dw2 += H2^T dpred
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < HID / 16; ++ks)
+        umma::mma_bf16(T_G, umma::desc_kmajor(S.D2 + ks * 128, HID), umma::desc_mnmajor(S.W1T + ks * 2048, HID),
+                       id_128_bmn, ks > 0);
+#pragma unroll
+      for (int ks = 0; ks < TILE / 16; ++ks) {
+        const bool acc = !first || ks > 0;
+        umma::mma_bf16(T_W1, umma::desc_mnmajor(S.H1 + ks * 2048, HID), umma::desc_mnmajor(S.D2 + ks * 2048, HID),
+                       id_128_mn, acc);
+        umma::mma_bf16(T_B1, umma::desc_mnmajor(S.D2 + ks * 2048, HID), umma::desc_mnmajor(S.X + ks * 256, KIN),
+                       id_16_mn, acc);
+        umma::mma_bf16(T_W2, umma::desc_mnmajor(S.H2 + ks * 2048, HID), umma::desc_mnmajor(S.X + ks * 256, KIN),
+                       id_16_mn, acc);
+      }
+      umma::commit(&S.bar);
+    }
+    wait_mma();
+    // ---- epilogue 3: dZ1 = (dZ2 W1^T)(1 - H1^2) -> smem
+#pragma unroll 1
+    for (int c0 = 0; c0 < HID; c0 += 16) {
+      float v[16];
+      umma::tmem_ld16(T_G + my + c0, v);
+      const uint4 ha = *reinterpret_cast<const uint4*>(&S.H1[blk_off(tid, c0, HID)]);
+      const uint4 hb = *reinterpret_cast<const uint4*>(&S.H1[blk_off(tid, c0 + 8, HID)]);
+      const uint32_t hw[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
+      uint4 pk[2];
+      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const float2 h = unpack_bf16(hw[j / 2]);
+        pw[j / 2] = pack_bf16(v[j] * (1.f - h.x * h.x), v[j + 1] * (1.f - h.y * h.y));
+      }
+      *reinterpret_cast<uint4*>(&S.D1[blk_off(tid, c0, HID)]) = pk[0];
+      *reinterpret_cast<uint4*>(&S.D1[blk_off(tid, c0 + 8, HID)]) = pk[1];
+    }
+    sync_to_mma();
+    // ---- G5: dW0^T | db0 += dZ1^T X
+    if (tid == 0) {
+#pragma unroll
+      for (int ks = 0; ks < TILE / 16; ++ks)
+        umma::mma_bf16(T_W0, umma::desc_mnmajor(S.D1 + ks * 2048, HID), umma::desc_mnmajor(S.X + ks * 256, KIN),
+                       id_16_mn, !first || ks > 0);
+      umma::commit(&S.bar);
+    }
+    wait_mma();  // the next tile overwrites X, H1, D2, H2, D1
+    first = false;
+  }
+  // ---- flush the TMEM accumulators into the global fp32 gradients
+  if (!first) {
+    const int r = tid;  // TMEM lane = hid row
+#pragma unroll 1
+    for (int c0 = 0; c0 < HID; c0 += 16) {
+      float v[16];
+      umma::tmem_ld16(T_W1 + my + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) atomicAdd(&gW1[r * HID + c0 + j], v[j]);
+    }
+    float v[16];
+    umma::tmem_ld16(T_W0 + my, v);
+#pragma unroll
+    for (int k = 0; k < TC_KMAX; ++k)
+      if (k < K) atomicAdd(&gW0[k * HID + r], v[k]);
+    atomicAdd(&gb0[r], v[KIN - 1]);
+    umma::tmem_ld16(T_B1 + my, v);
+    atomicAdd(&gb1[r], v[KIN - 1]);
+    umma::tmem_ld16(T_W2 + my, v);
+    atomicAdd(&gw2[r], v[KIN - 2]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    gb2_acc += __shfl_xor_sync(0xffffffffu, gb2_acc, o);
+    loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
+  }
+  if (lane == 0) {
+    atomicAdd(&S.red[0], gb2_acc);
+    atomicAdd(&S.red[1], loss_acc);
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free(T0, 512);
+  if (tid == 0) {
+    atomicAdd(gb2, S.red[0]);
+    atomicAdd(loss, S.red[1] * inv_m);
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
+                        const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
+                        float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
+                        int32_t n_sm, void* stream) {
+  if (m <= 0) return QS_OK;
+  if (k < 1 || k > TC_KMAX || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
+  const size_t smem = sizeof(TcSmem);
+  static_assert(sizeof(TcSmem) <= 227 * 1024, "shared memory");
+  if (cudaFuncSetAttribute(k_mlp3_fit_grad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return QS_ERR_LAUNCH;
+  const int64_t ntiles = (m + TILE - 1) / TILE;
+  const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
+  k_mlp3_fit_grad_tc<<<grid, TC_THREADS, smem, (cudaStream_t)stream>>>(m, k, 1.f / (float)m, x, scale, y, W0, b0,
+                                                                       W1, b1, w2, b2, gW0, gb0, gW1, gb1, gw2,
+                                                                       gb2, loss);
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
 
 int qs_mlp3_fit_grad(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
                      const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,

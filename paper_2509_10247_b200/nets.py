@@ -306,10 +306,14 @@ def value_fit_grad(value: "ValueNet", x: torch.Tensor, y: torch.Tensor) -> torch
     scale = value.input_scale.to(device=dev, dtype=torch.float32).contiguous()
     w = [p.detach().float().contiguous() for p in params]
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    L.check(L.lib().qs_mlp3_fit_grad(M, K, L.ptr(x), L.ptr(scale), L.ptr(y), L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]),
-                                     L.ptr(w[3]), L.ptr(w[4]), L.ptr(w[5]), L.ptr(grads[0]), L.ptr(grads[1]),
-                                     L.ptr(grads[2]), L.ptr(grads[3]), L.ptr(grads[4]), L.ptr(grads[5]),
-                                     L.ptr(loss), n_sm, L.stream_handle(dev)), "qs_mlp3_fit_grad")
+    # tcgen05 kernel (TMEM accumulators) for <= 14 inputs -- the privileged
+    # state's 14; the mma.sync kernel otherwise (QS_CRITIC_KERNEL=mma forces it)
+    tc = K <= 14 and os.environ.get("QS_CRITIC_KERNEL", "tc") != "mma"
+    fn = L.lib().qs_mlp3_fit_grad_tc if tc else L.lib().qs_mlp3_fit_grad
+    L.check(fn(M, K, L.ptr(x), L.ptr(scale), L.ptr(y), L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]), L.ptr(w[3]),
+               L.ptr(w[4]), L.ptr(w[5]), L.ptr(grads[0]), L.ptr(grads[1]), L.ptr(grads[2]), L.ptr(grads[3]),
+               L.ptr(grads[4]), L.ptr(grads[5]), L.ptr(loss), n_sm, L.stream_handle(dev)),
+            "qs_mlp3_fit_grad_tc" if tc else "qs_mlp3_fit_grad")
     for p, gr in zip(params, grads):
         p.grad = gr
     return loss[0]

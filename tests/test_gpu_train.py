@@ -129,12 +129,16 @@ def test_ppo_with_visual_encoders(task):
     assert enc and all(not torch.equal(before[k], dict(lr.policy.named_parameters())[k]) for k in enc)
 
 
+@pytest.mark.parametrize("kernel", ["tc", "mma"])
 @pytest.mark.parametrize("M", [5000, 128 * 148 * 3 + 77])
-def test_fused_critic_gradient_matches_autograd(M):
-    """qs_mlp3_fit_grad (forward + backward of the value MLP in one tensor-core
-    kernel, bf16 operands) against torch autograd in fp32 on the same weights:
-    loss and every parameter gradient to bf16 accuracy."""
+def test_fused_critic_gradient_matches_autograd(M, kernel, monkeypatch):
+    """qs_mlp3_fit_grad_tc (tcgen05, TMEM accumulators) and qs_mlp3_fit_grad
+    (mma.sync): forward + backward of the value MLP in one tensor-core kernel,
+    bf16 operands, against torch autograd in fp32 on the same weights: loss
+    and every parameter gradient to bf16 accuracy."""
     from paper_2509_10247_b200 import nets
+
+    monkeypatch.setenv("QS_CRITIC_KERNEL", kernel)
 
     torch.manual_seed(0)
     rng = np.random.default_rng(4)
