@@ -351,41 +351,65 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
 
 // ---------------------------------------------------------------------------
 // The same fit step on the 5th-generation tensor cores (tcgen05).  One
-// persistent 128-thread CTA per SM walks 128-row tiles; thread t owns row t of
-// a tile and TMEM lane t.  Operands live in shared memory in the blocked
+// persistent 512-thread CTA per SM walks 128-row tiles; thread (warp w, lane
+// l) owns row 32 (w % 4) + l of a tile -- its TMEM lane -- and columns
+// 32 (w / 4) .. + 31 of every 128-wide activation.  Operands live in shared memory in the blocked
 // no-swizzle layout of qs_umma.cuh, so every activation tile is written once
 // and read by the MMAs both as a K-major operand (next layer) and as an
 // MN-major one (weight gradients, K = the tile's rows).  Accumulators live in
 // TMEM (512 columns):
-//   [0,128)   G1 / G2 / G3 results of the current tile (reused in turn)
-//   [128,256) dW1 = sum over tiles of H1^T dZ2          (lane = hid1 row)
-//   [256,272) dW0^T | db0 = dZ1^T X                     (lane = hid1; col 15 = db0)
-//   [272,288) db1 = dZ2^T X, column 15                  (lane = hid2)
-//   [288,304) dw2 = H2^T X, column 14 (X col 14 holds dL/dpred) (lane = hid2)
-// X's padding columns carry the bias / w2 gradients through the same MMAs:
-// column 15 is all ones (column sums), column 14 receives dL/dpred after the
-// forward.  Hence K <= 14 input features (the privileged state has 14).
+//   [0,256)   G1 / G2 / G3 results of the tiles in slots 0 and 1 (reused in turn)
+//   [256,384) dW1 = sum over tiles of H1^T dZ2          (lane = hid1 row)
+//   [384,400) dW0^T | db0 = dZ1^T X                     (lane = hid1; col 15 = db0)
+//   [400,416) db1 = dZ2^T X, column 15                  (lane = hid2)
+// Tiles run in pairs through two operand slots: while the epilogue threads
+// work on one slot's tile, the tensor cores run the other slot's GEMMs.
+// X's padding column 15 is all ones, so the bias gradients are column sums
+// taken by the same MMAs; dw2 = dpred^T H2 is accumulated in fp32 registers
+// by the epilogue threads (each owns 32 columns).  K <= 14 input features
+// (the privileged state has 14).
 // Per tile, one thread issues: G1 (X W0), G2 (H1 W1), then G3 (dZ2 W1^T), G4
-// (H1^T dZ2), db1, dw2, then G5 (dZ1^T X); tcgen05.commit -> mbarrier hands each
+// (H1^T dZ2), db1, then G5 (dZ1^T X); tcgen05.commit -> mbarrier hands each
 // group to the 128 epilogue threads (TMEM -> registers -> bias / tanh / chain
 // rule -> bf16 -> shared memory).
 
-constexpr int TC_THREADS = 128;
+constexpr int TC_THREADS = 512;  // 16 warps: warp w reads TMEM lanes 32 (w % 4).., columns 32 (w / 4)..
 constexpr int TC_KMAX = 14;
+constexpr int TC_QC = HID / 4;   // columns per thread (a quarter of a row)
 
-struct TcSmem {
+// one tile's operands; two slots let the tensor cores run one tile's GEMMs
+// while the epilogue threads work on the other's
+struct TcSlot {
   __nv_bfloat16 X[TILE * KIN];     // [rows][16]   blocked
+  __nv_bfloat16 H1[TILE * HID];    // [rows][hid1]  H1, then dZ1 in place (epilogue 3)
+  __nv_bfloat16 D2[TILE * HID];    // [rows][hid2]  dZ2
+  float predq[4][TILE];            // per-quarter partial dot products H2 . w2
+};
+struct TcSmem {
+  TcSlot slot[2];
   __nv_bfloat16 W0T[HID * KIN];    // [hid1][16]   blocked (K-major B of G1)
   __nv_bfloat16 W1T[HID * HID];    // [hid2][hid1] blocked (K-major B of G2, MN-major B of G3)
-  __nv_bfloat16 H1[TILE * HID];    // [rows][hid1]
-  __nv_bfloat16 D2[TILE * HID];    // [rows][hid2]  dZ2
-  __nv_bfloat16 H2[TILE * HID];    // [rows][hid2]
-  __nv_bfloat16 D1[TILE * HID];    // [rows][hid1]  dZ1
   float b0[HID], b1[HID], w2[HID];
   float red[2];                    // db2, loss
-  uint64_t bar;
+  uint64_t bar[2];
   uint32_t tbase;
 };
+
+// 32 consecutive columns of this thread's TMEM lane
+QS_D void tmem_ld32(uint32_t t, float (&v)[32]) {
+  float a[16], b[16];
+  umma::tmem_ld16(t, a);
+  umma::tmem_ld16(t + 16, b);
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    v[j] = a[j];
+    v[16 + j] = b[j];
+  }
+}
+// 8 bf16 pairs -> one 16-byte store at (row, c0) of a blocked [rows][HID] buffer
+QS_D void st_row8(__nv_bfloat16* buf, int row, int c0, const uint32_t* w) {
+  *reinterpret_cast<uint4*>(&buf[umma::blk_off(row, c0, HID)]) = make_uint4(w[0], w[1], w[2], w[3]);
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_mlp3_fit_grad_tc(int64_t M, int K, float inv_m, const float* __restrict__ x, const float* __restrict__ scale,
@@ -398,6 +422,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
   using umma::blk_off;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = 32 * (warp & 3) + lane;  // this thread's tile row == TMEM lane
+  const int q = warp >> 2;               // its column quarter
+  const int cq = q * TC_QC;
   // ---- parameters -> shared memory (bf16 operands, fp32 vectors)
   for (int i = tid; i < HID * KIN; i += TC_THREADS) {
     const int n = i / KIN, k = i % KIN;  // W0T[n][k] = W0[k][n]
@@ -415,202 +442,236 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (tid < 2) S.red[tid] = 0.f;
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
-    mbar_init(&S.bar, 1);
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
     fence_barrier_init();
   }
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
   const uint32_t T0 = S.tbase;
-  const uint32_t T_G = T0, T_W1 = T0 + 128, T_W0 = T0 + 256, T_B1 = T0 + 272, T_W2 = T0 + 288;
+  // TMEM: G accumulator per slot [0,128) [128,256); dW1 [256,384); dW0^T|db0 [384,400); db1 [400,416)
+  const uint32_t T_W1 = T0 + 256, T_W0 = T0 + 384, T_B1 = T0 + 400;
   const uint32_t id_128 = umma::idesc_bf16(128, 128, false, false);
   const uint32_t id_128_bmn = umma::idesc_bf16(128, 128, false, true);
   const uint32_t id_128_mn = umma::idesc_bf16(128, 128, true, true);
   const uint32_t id_16_mn = umma::idesc_bf16(128, 16, true, true);
-  const uint32_t my = umma::taddr(0, 32 * warp, 0);  // this warp's TMEM lanes
+  const uint32_t my = umma::taddr(0, 32 * (warp & 3), cq);  // this thread's lanes / columns
   const float bias2 = b2[0];
-  uint32_t phase = 0;
-  bool first = true;
+  uint32_t phase[2] = {0u, 0u};
+  bool first = true;   // no dW1 / db1 MMA issued yet (the first one overwrites TMEM)
+  bool first5 = true;  // no dW0 / db0 MMA issued yet
   float gb2_acc = 0.f, loss_acc = 0.f;
+  float gw2p[32];  // this thread's columns of dw2, summed over its rows
+#pragma unroll
+  for (int j = 0; j < 32; ++j) gw2p[j] = 0.f;
   auto sync_to_mma = [&]() {  // epilogue writes -> visible to the tensor cores, then hand over
     umma::fence_async_smem();
     umma::fence_before();
     __syncthreads();
     umma::fence_after();
   };
-  auto wait_mma = [&]() {
-    umma::mbar_wait_parity(&S.bar, phase);
-    phase ^= 1u;
+  auto wait_mma = [&](int sl) {
+    umma::mbar_wait_parity(&S.bar[sl], phase[sl]);
+    phase[sl] ^= 1u;
     umma::fence_after();
   };
-  const int64_t ntiles = (M + TILE - 1) / TILE;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t row = tile * TILE + tid;
-    const bool valid = row < M;
-    // ---- X tile: row tid, scaled features, col 14 <- dL/dpred later, col 15 = 1
-    {
-      float v[KIN];
+  // ---- the phases of one tile in slot sl
+  auto stage_x = [&](int sl, int64_t tile) {
+    if (q != 0) return;
+    const int64_t row = tile * TILE + r;
+    float v[KIN];
 #pragma unroll
-      for (int c = 0; c < KIN; ++c) v[c] = 0.f;
-      if (valid) {
+    for (int c = 0; c < KIN; ++c) v[c] = 0.f;
+    if (row < M) {
 #pragma unroll
-        for (int c = 0; c < TC_KMAX; ++c)
-          if (c < K) v[c] = __ldg(x + row * K + c) * __ldg(scale + c);
-      }
-      v[KIN - 1] = 1.f;
-#pragma unroll
-      for (int c = 0; c < KIN; c += 8) {
-        uint4 pk;
-        pk.x = pack_bf16(v[c], v[c + 1]);
-        pk.y = pack_bf16(v[c + 2], v[c + 3]);
-        pk.z = pack_bf16(v[c + 4], v[c + 5]);
-        pk.w = pack_bf16(v[c + 6], v[c + 7]);
-        *reinterpret_cast<uint4*>(&S.X[blk_off(tid, c, KIN)]) = pk;
-      }
+      for (int c = 0; c < TC_KMAX; ++c)
+        if (c < K) v[c] = __ldg(x + row * K + c) * __ldg(scale + c);
     }
-    sync_to_mma();
-    // ---- G1: X W0 -> T_G
-    if (tid == 0) {
-      umma::mma_bf16(T_G, umma::desc_kmajor(S.X, KIN), umma::desc_kmajor(S.W0T, KIN), id_128, false);
-      umma::commit(&S.bar);
-    }
-    wait_mma();
-    // ---- epilogue 1: H1 = tanh(. + b0) -> smem
-#pragma unroll 1
-    for (int c0 = 0; c0 < HID; c0 += 16) {
-      float v[16];
-      umma::tmem_ld16(T_G + my + c0, v);
-      uint4 pk[2];
-      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+    v[KIN - 1] = 1.f;  // bias-gradient column
 #pragma unroll
-      for (int j = 0; j < 16; j += 2)
-        pw[j / 2] = pack_bf16(tanh_mufu(v[j] + S.b0[c0 + j]), tanh_mufu(v[j + 1] + S.b0[c0 + j + 1]));
-      *reinterpret_cast<uint4*>(&S.H1[blk_off(tid, c0, HID)]) = pk[0];
-      *reinterpret_cast<uint4*>(&S.H1[blk_off(tid, c0 + 8, HID)]) = pk[1];
-    }
-    sync_to_mma();
-    // ---- G2: H1 W1 -> T_G
-    if (tid == 0) {
+    for (int c = 0; c < KIN; c += 8)
+      *reinterpret_cast<uint4*>(&S.slot[sl].X[blk_off(r, c, KIN)]) =
+          make_uint4(pack_bf16(v[c], v[c + 1]), pack_bf16(v[c + 2], v[c + 3]), pack_bf16(v[c + 4], v[c + 5]),
+                     pack_bf16(v[c + 6], v[c + 7]));
+  };
+  auto issue_g1 = [&](int sl) {  // X W0
+    TcSlot& T = S.slot[sl];
+    umma::mma_bf16(T0 + 128 * sl, umma::desc_kmajor(T.X, KIN), umma::desc_kmajor(S.W0T, KIN), id_128, false);
+    umma::commit(&S.bar[sl]);
+  };
+  auto issue_g2 = [&](int sl) {  // H1 W1
+    TcSlot& T = S.slot[sl];
 #pragma unroll
-      for (int ks = 0; ks < HID / 16; ++ks)
-        umma::mma_bf16(T_G, umma::desc_kmajor(S.H1 + ks * 128, HID), umma::desc_kmajor(S.W1T + ks * 128, HID),
-                       id_128, ks > 0);
-      umma::commit(&S.bar);
-    }
-    wait_mma();
-    // ---- epilogue 2: H2 = tanh(. + b1), pred, dL/dpred, dZ2 = dpred w2 (1 - H2^2)
-    float pred = bias2;
-#pragma unroll 1
-    for (int c0 = 0; c0 < HID; c0 += 16) {
-      float v[16];
-      umma::tmem_ld16(T_G + my + c0, v);
-      uint4 pk[2];
-      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+    for (int ks = 0; ks < HID / 16; ++ks)
+      umma::mma_bf16(T0 + 128 * sl, umma::desc_kmajor(T.H1 + ks * 128, HID), umma::desc_kmajor(S.W1T + ks * 128, HID),
+                     id_128, ks > 0);
+    umma::commit(&S.bar[sl]);
+  };
+  auto issue_g34 = [&](int sl) {  // dZ2 W1^T;  dW1 += H1^T dZ2;  db1 += dZ2^T 1
+    TcSlot& T = S.slot[sl];
 #pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const float h0 = tanh_mufu(v[j] + S.b1[c0 + j]), h1 = tanh_mufu(v[j + 1] + S.b1[c0 + j + 1]);
-        pred = fmaf(h0, S.w2[c0 + j], fmaf(h1, S.w2[c0 + j + 1], pred));
-        pw[j / 2] = pack_bf16(h0, h1);
-      }
-      *reinterpret_cast<uint4*>(&S.H2[blk_off(tid, c0, HID)]) = pk[0];
-      *reinterpret_cast<uint4*>(&S.H2[blk_off(tid, c0 + 8, HID)]) = pk[1];
+    for (int ks = 0; ks < HID / 16; ++ks)
+      umma::mma_bf16(T0 + 128 * sl, umma::desc_kmajor(T.D2 + ks * 128, HID),
+                     umma::desc_mnmajor(S.W1T + ks * 2048, HID), id_128_bmn, ks > 0);
+#pragma unroll
+    for (int ks = 0; ks < TILE / 16; ++ks) {
+      const bool acc = !first || ks > 0;
+      umma::mma_bf16(T_W1, umma::desc_mnmajor(T.H1 + ks * 2048, HID), umma::desc_mnmajor(T.D2 + ks * 2048, HID),
+                     id_128_mn, acc);
+      umma::mma_bf16(T_B1, umma::desc_mnmajor(T.D2 + ks * 2048, HID), umma::desc_mnmajor(T.X + ks * 256, KIN),
+                     id_16_mn, acc);
     }
-    const float e = valid ? pred - __ldg(y + row) : 0.f;
+    umma::commit(&S.bar[sl]);
+  };
+  auto issue_g5 = [&](int sl) {  // dW0^T | db0 += dZ1^T X
+    TcSlot& T = S.slot[sl];
+#pragma unroll
+    for (int ks = 0; ks < TILE / 16; ++ks)
+      umma::mma_bf16(T_W0, umma::desc_mnmajor(T.H1 + ks * 2048, HID), umma::desc_mnmajor(T.X + ks * 256, KIN),
+                     id_16_mn, !first5 || ks > 0);
+    umma::commit(&S.bar[sl]);
+  };
+  auto epi1 = [&](int sl) {  // H1 = tanh(. + b0)
+    float v[32];
+    tmem_ld32(T0 + 128 * sl + my, v);
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2)
+      w[j / 2] = pack_bf16(tanh_mufu(v[j] + S.b0[cq + j]), tanh_mufu(v[j + 1] + S.b0[cq + j + 1]));
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_row8(S.slot[sl].H1, r, cq + 8 * j, w + 4 * j);
+  };
+  auto epi2 = [&](int sl, int64_t tile) {  // H2, pred, dL/dpred, dZ2 = dpred w2 (1 - H2^2), dw2
+    TcSlot& T = S.slot[sl];
+    float h[32];
+    tmem_ld32(T0 + 128 * sl + my, h);
+    float part = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      h[j] = tanh_mufu(h[j] + S.b1[cq + j]);
+      h[j + 1] = tanh_mufu(h[j + 1] + S.b1[cq + j + 1]);
+      part = fmaf(h[j], S.w2[cq + j], fmaf(h[j + 1], S.w2[cq + j + 1], part));
+    }
+    T.predq[q][r] = part;
+    __syncthreads();
+    const int64_t row = tile * TILE + r;
+    const float pred = bias2 + T.predq[0][r] + T.predq[1][r] + T.predq[2][r] + T.predq[3][r];
+    const float e = row < M ? pred - __ldg(y + row) : 0.f;
     const float dp = 2.f * inv_m * e;
-    loss_acc += e * e;
-    gb2_acc += dp;
-#pragma unroll 1
-    for (int c0 = 0; c0 < HID; c0 += 16) {  // the fp32 H2 again (TMEM is cheap to re-read)
-      float v[16];
-      umma::tmem_ld16(T_G + my + c0, v);
-      uint4 pk[2];
-      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const float h0 = tanh_mufu(v[j] + S.b1[c0 + j]), h1 = tanh_mufu(v[j + 1] + S.b1[c0 + j + 1]);
-        pw[j / 2] = pack_bf16(dp * S.w2[c0 + j] * (1.f - h0 * h0), dp * S.w2[c0 + j + 1] * (1.f - h1 * h1));
-      }
-      *reinterpret_cast<uint4*>(&S.D2[blk_off(tid, c0, HID)]) = pk[0];
-      *reinterpret_cast<uint4*>(&S.D2[blk_off(tid, c0 + 8, HID)]) = pk[1];
+    if (q == 0) {
+      loss_acc += e * e;
+      gb2_acc += dp;
     }
-    S.X[blk_off(tid, KIN - 2, KIN)] = __float2bfloat16_rn(dp);  // X col 14 <- dL/dpred (for dw2)
+    uint32_t w[16];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      gw2p[j] = fmaf(dp, h[j], gw2p[j]);  // dw2 = dpred^T H2, fp32 in registers
+      gw2p[j + 1] = fmaf(dp, h[j + 1], gw2p[j + 1]);
+      w[j / 2] = pack_bf16(dp * S.w2[cq + j] * (1.f - h[j] * h[j]), dp * S.w2[cq + j + 1] * (1.f - h[j + 1] * h[j + 1]));
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_row8(T.D2, r, cq + 8 * j, w + 4 * j);
+  };
+  auto epi3 = [&](int sl) {  // dZ1 = (dZ2 W1^T)(1 - H1^2), in place over H1
+    TcSlot& T = S.slot[sl];
+    float v[32];
+    tmem_ld32(T0 + 128 * sl + my, v);
+    uint32_t w[16];
+#pragma unroll
+    for (int j8 = 0; j8 < 32; j8 += 8) {
+      const uint4 hh = *reinterpret_cast<const uint4*>(&T.H1[blk_off(r, cq + j8, HID)]);
+      const uint32_t hw[4] = {hh.x, hh.y, hh.z, hh.w};
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const float2 hv = unpack_bf16(hw[j / 2]);
+        w[(j8 + j) / 2] = pack_bf16(v[j8 + j] * (1.f - hv.x * hv.x), v[j8 + j + 1] * (1.f - hv.y * hv.y));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) st_row8(T.H1, r, cq + 8 * j, w + 4 * j);
+  };
+  // ---- tiles in pairs (slot 0, slot 1): each epilogue overlaps the other
+  //      slot's GEMMs on the tensor cores
+  const int64_t ntiles = (M + TILE - 1) / TILE;
+  for (int64_t ta = blockIdx.x; ta < ntiles; ta += 2 * (int64_t)gridDim.x) {
+    const int64_t tb = ta + gridDim.x;
+    const bool two = tb < ntiles;
+    stage_x(0, ta);
+    if (two) stage_x(1, tb);
     sync_to_mma();
-    // ---- G3: dZ2 W1^T -> T_G;  G4: dW1 += H1^T dZ2;  db1 += dZ2^T 1;  dw2 += H2^T dpred
     if (tid == 0) {
-#pragma unroll
-      for (int ks = 0; ks < HID / 16; ++ks)
-        umma::mma_bf16(T_G, umma::desc_kmajor(S.D2 + ks * 128, HID), umma::desc_mnmajor(S.W1T + ks * 2048, HID),
-                       id_128_bmn, ks > 0);
-#pragma unroll
-      for (int ks = 0; ks < TILE / 16; ++ks) {
-        const bool acc = !first || ks > 0;
-        umma::mma_bf16(T_W1, umma::desc_mnmajor(S.H1 + ks * 2048, HID), umma::desc_mnmajor(S.D2 + ks * 2048, HID),
-                       id_128_mn, acc);
-        umma::mma_bf16(T_B1, umma::desc_mnmajor(S.D2 + ks * 2048, HID), umma::desc_mnmajor(S.X + ks * 256, KIN),
-                       id_16_mn, acc);
-        umma::mma_bf16(T_W2, umma::desc_mnmajor(S.H2 + ks * 2048, HID), umma::desc_mnmajor(S.X + ks * 256, KIN),
-                       id_16_mn, acc);
-      }
-      umma::commit(&S.bar);
+      issue_g1(0);
+      if (two) issue_g1(1);
     }
-    wait_mma();
-    // ---- epilogue 3: dZ1 = (dZ2 W1^T)(1 - H1^2) -> smem
-#pragma unroll 1
-    for (int c0 = 0; c0 < HID; c0 += 16) {
-      float v[16];
-      umma::tmem_ld16(T_G + my + c0, v);
-      const uint4 ha = *reinterpret_cast<const uint4*>(&S.H1[blk_off(tid, c0, HID)]);
-      const uint4 hb = *reinterpret_cast<const uint4*>(&S.H1[blk_off(tid, c0 + 8, HID)]);
-      const uint32_t hw[8] = {ha.x, ha.y, ha.z, ha.w, hb.x, hb.y, hb.z, hb.w};
-      uint4 pk[2];
-      uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
-#pragma unroll
-      for (int j = 0; j < 16; j += 2) {
-        const float2 h = unpack_bf16(hw[j / 2]);
-        pw[j / 2] = pack_bf16(v[j] * (1.f - h.x * h.x), v[j + 1] * (1.f - h.y * h.y));
-      }
-      *reinterpret_cast<uint4*>(&S.D1[blk_off(tid, c0, HID)]) = pk[0];
-      *reinterpret_cast<uint4*>(&S.D1[blk_off(tid, c0 + 8, HID)]) = pk[1];
-    }
+    wait_mma(0);
+    epi1(0);
     sync_to_mma();
-    // ---- G5: dW0^T | db0 += dZ1^T X
-    if (tid == 0) {
-#pragma unroll
-      for (int ks = 0; ks < TILE / 16; ++ks)
-        umma::mma_bf16(T_W0, umma::desc_mnmajor(S.D1 + ks * 2048, HID), umma::desc_mnmajor(S.X + ks * 256, KIN),
-                       id_16_mn, !first || ks > 0);
-      umma::commit(&S.bar);
+    if (tid == 0) issue_g2(0);
+    if (two) {
+      wait_mma(1);
+      epi1(1);
+      sync_to_mma();
+      if (tid == 0) issue_g2(1);
     }
-    wait_mma();  // the next tile overwrites X, H1, D2, H2, D1
+    wait_mma(0);
+    epi2(0, ta);
+    sync_to_mma();
+    if (tid == 0) issue_g34(0);
     first = false;
-  }
-  // ---- flush the TMEM accumulators into the global fp32 gradients
-  if (!first) {
-    const int r = tid;  // TMEM lane = hid row
-#pragma unroll 1
-    for (int c0 = 0; c0 < HID; c0 += 16) {
-      float v[16];
-      umma::tmem_ld16(T_W1 + my + c0, v);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) atomicAdd(&gW1[r * HID + c0 + j], v[j]);
+    if (two) {
+      wait_mma(1);
+      epi2(1, tb);
+      sync_to_mma();
+      if (tid == 0) issue_g34(1);
     }
-    float v[16];
-    umma::tmem_ld16(T_W0 + my, v);
+    wait_mma(0);
+    epi3(0);
+    sync_to_mma();
+    if (tid == 0) issue_g5(0);
+    first5 = false;
+    if (two) {
+      wait_mma(1);
+      epi3(1);
+      sync_to_mma();
+      if (tid == 0) issue_g5(1);
+    }
+    wait_mma(0);  // both slots' buffers are free for the next pair
+    if (two) wait_mma(1);
+  }
+  // ---- flush the TMEM accumulators into the global fp32 gradients (lane = hid row)
+  if (!first) {
+    float v[32];
+    tmem_ld32(T_W1 + my, v);
 #pragma unroll
-    for (int k = 0; k < TC_KMAX; ++k)
-      if (k < K) atomicAdd(&gW0[k * HID + r], v[k]);
-    atomicAdd(&gb0[r], v[KIN - 1]);
-    umma::tmem_ld16(T_B1 + my, v);
-    atomicAdd(&gb1[r], v[KIN - 1]);
-    umma::tmem_ld16(T_W2 + my, v);
-    atomicAdd(&gw2[r], v[KIN - 2]);
+    for (int j = 0; j < 32; ++j) atomicAdd(&gW1[r * HID + cq + j], v[j]);
+    if (q == 0) {
+      float u[16];
+      umma::tmem_ld16(umma::taddr(T_W0, 32 * (warp & 3), 0), u);
+#pragma unroll
+      for (int k = 0; k < TC_KMAX; ++k)
+        if (k < K) atomicAdd(&gW0[k * HID + r], u[k]);
+      atomicAdd(&gb0[r], u[KIN - 1]);
+    } else if (q == 1) {
+      float u[16];
+      umma::tmem_ld16(umma::taddr(T_B1, 32 * (warp & 3), 0), u);
+      atomicAdd(&gb1[r], u[KIN - 1]);
+    }
+  }
+  // dw2: reduce each column over the warp's 32 rows, one atomic per (warp, column)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    float v = gw2p[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == j) atomicAdd(&gw2[cq + j], v);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     gb2_acc += __shfl_xor_sync(0xffffffffu, gb2_acc, o);
     loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
   }
-  if (lane == 0) {
+  if (lane == 0 && q == 0) {
     atomicAdd(&S.red[0], gb2_acc);
     atomicAdd(&S.red[1], loss_acc);
   }
