@@ -363,7 +363,8 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
 //   [384,400) dW0^T | db0 = dZ1^T X                     (lane = hid1; col 15 = db0)
 //   [400,416) db1 = dZ2^T X, column 15                  (lane = hid2)
 // Tiles run in pairs through two operand slots: while the epilogue threads
-// work on one slot's tile, the tensor cores run the other slot's GEMMs.
+// work on one slot's tile, the tensor cores run the other slot's GEMMs; the
+// next pair's x / y rows stream into the slots with cp.async meanwhile.
 // X's padding column 15 is all ones, so the bias gradients are column sums
 // taken by the same MMAs; dw2 = dpred^T H2 is accumulated in fp32 registers
 // by the epilogue threads (each owns 32 columns).  K <= 14 input features
@@ -384,6 +385,10 @@ struct TcSlot {
   __nv_bfloat16 H1[TILE * HID];    // [rows][hid1]  H1, then dZ1 in place (epilogue 3)
   __nv_bfloat16 D2[TILE * HID];    // [rows][hid2]  dZ2
   float predq[4][TILE];            // per-quarter partial dot products H2 . w2
+  // raw fp32 rows of the NEXT pair's tile for this slot, prefetched with
+  // cp.async while the current pair computes (x: 128 rows x K floats, y)
+  float xraw[TILE * TC_KMAX];
+  float yraw[TILE];
 };
 struct TcSmem {
   TcSlot slot[2];
@@ -477,6 +482,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     umma::fence_after();
   };
   // ---- the phases of one tile in slot sl
+  // the tile's raw x / y rows -> slot staging (contiguous blocks, 16-byte
+  // cp.async chunks; the tail tile's bytes past row M are zero-filled)
+  auto prefetch = [&](int sl, int64_t tile) {
+    if (tile >= (M + TILE - 1) / TILE) return;
+    const int64_t r0 = tile * TILE;
+    const int64_t nrows = M - r0 < TILE ? M - r0 : TILE;
+    const char* xs = reinterpret_cast<const char*>(x + r0 * K);
+    char* xd = reinterpret_cast<char*>(S.slot[sl].xraw);
+    const int xbytes = (int)(nrows * K * 4), xcap = TILE * K * 4;
+    for (int b = tid * 16; b < xcap; b += TC_THREADS * 16) {
+      const int n = xbytes - b >= 16 ? 16 : (xbytes > b ? xbytes - b : 0);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(xd + b)), "l"(xs + (n ? b : 0)),
+                   "r"(n)
+                   : "memory");
+    }
+    const char* ys = reinterpret_cast<const char*>(y + r0);
+    char* yd = reinterpret_cast<char*>(S.slot[sl].yraw);
+    const int ybytes = (int)(nrows * 4);
+    if (tid * 16 < TILE * 4) {
+      const int b = tid * 16, n = ybytes - b >= 16 ? 16 : (ybytes > b ? ybytes - b : 0);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(yd + b)), "l"(ys + (n ? b : 0)),
+                   "r"(n)
+                   : "memory");
+    }
+  };
   auto stage_x = [&](int sl, int64_t tile) {
     if (q != 0) return;
     const int64_t row = tile * TILE + r;
@@ -486,7 +516,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (row < M) {
 #pragma unroll
       for (int c = 0; c < TC_KMAX; ++c)
-        if (c < K) v[c] = __ldg(x + row * K + c) * __ldg(scale + c);
+        if (c < K) v[c] = S.slot[sl].xraw[r * K + c] * __ldg(scale + c);
     }
     v[KIN - 1] = 1.f;  // bias-gradient column
 #pragma unroll
@@ -557,7 +587,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     const int64_t row = tile * TILE + r;
     const float pred = bias2 + T.predq[0][r] + T.predq[1][r] + T.predq[2][r] + T.predq[3][r];
-    const float e = row < M ? pred - __ldg(y + row) : 0.f;
+    const float e = row < M ? pred - T.yraw[r] : 0.f;
     const float dp = 2.f * inv_m * e;
     if (q == 0) {
       loss_acc += e * e;
@@ -594,9 +624,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // ---- tiles in pairs (slot 0, slot 1): each epilogue overlaps the other
   //      slot's GEMMs on the tensor cores
   const int64_t ntiles = (M + TILE - 1) / TILE;
+  prefetch(0, blockIdx.x);
+  prefetch(1, blockIdx.x + gridDim.x);
+  cp_async_commit();
   for (int64_t ta = blockIdx.x; ta < ntiles; ta += 2 * (int64_t)gridDim.x) {
     const int64_t tb = ta + gridDim.x;
     const bool two = tb < ntiles;
+    cp_async_wait<0>();
+    __syncthreads();  // this pair's raw rows have landed
     stage_x(0, ta);
     if (two) stage_x(1, tb);
     sync_to_mma();
@@ -616,7 +651,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     wait_mma(0);
     epi2(0, ta);
-    sync_to_mma();
+    sync_to_mma();  // (also: every thread is past its reads of this pair's xraw / yraw)
     if (tid == 0) issue_g34(0);
     first = false;
     if (two) {
@@ -625,6 +660,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       sync_to_mma();
       if (tid == 0) issue_g34(1);
     }
+    prefetch(0, ta + 2 * (int64_t)gridDim.x);  // the next pair's rows, behind this pair's GEMMs
+    prefetch(1, tb + 2 * (int64_t)gridDim.x);
+    cp_async_commit();
     wait_mma(0);
     epi3(0);
     sync_to_mma();
@@ -639,6 +677,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     wait_mma(0);  // both slots' buffers are free for the next pair
     if (two) wait_mma(1);
   }
+  cp_async_wait<0>();
   // ---- flush the TMEM accumulators into the global fp32 gradients (lane = hid row)
   if (!first) {
     float v[32];
