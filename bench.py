@@ -95,6 +95,75 @@ def _cpu_worker(args):
             return done_steps, el
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")  # the reference package (pip --target)
+
+
+def have_ref_pkg() -> bool:
+    return os.path.isdir(os.path.join(REF_PKG, "quadsim"))
+
+
+def _ref_worker(args):
+    """The REFERENCE's own code on the C2 workload: quadsim's position task with
+    the full quadrotor (FlightTask.step recorded on its Tape), the discounted
+    BPTT loss and Tape.backward (q/learners.py:201-265), plus one
+    ImuModel.read per step with C2's noise (q/sensors.py:508-555; the
+    reference's tasks do not wire the IMU, so the window calls it after each
+    step on the post-step state)."""
+    n_envs, T, seconds, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    from quadsim import autodiff as ad
+    from quadsim import dynamics as rdyn
+    from quadsim import sensors as rsn
+    from quadsim import tasks as rtk
+    from quadsim.autodiff import Tape
+
+    env = rtk.make_task(rtk.TaskConfig(task="position", dynamics="full", n_envs=n_envs, episode_len=128))
+    env.reset(seed=seed)
+    imu = rsn.ImuModel(n_envs, seed=seed, **IMU)
+    g = env.params.g_vec
+    dt = env.config.dt
+    rng = np.random.default_rng(seed)
+    done_steps = 0
+    t0 = time.perf_counter()
+    while True:
+        raw = rng.normal(size=(T, n_envs, 4)) * 0.3
+        tape = Tape()
+        leaves = [tape.leaf(raw[t].copy()) for t in range(T)]
+        env.detach_states()
+        disc = None
+        for t in range(T):
+            out = env.step(leaves[t])
+            term = ad.mul(ad.vmean(out.r_ctrl), 0.99 ** t)
+            disc = term if disc is None else ad.add(disc, term)
+            st = env.state
+            imu.read(rdyn.quat_to_matrix_np(st.q.value), st.w.value, env.last_v_dot, g, dt)
+            if out.done.any():
+                imu.reset(out.done)
+        tape.backward(ad.neg(ad.mul(disc, 1.0 / T)))
+        done_steps += n_envs * T
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return done_steps, el
+
+
+def reference_continuity():
+    """BASELINE.md §4 continuity points: the reference's own `quadsim bench`
+    harness (q/cli.py:202-256, median of 5 after 3 warm-ups, 1 process),
+    unchanged: raw full-model stepping at 8,192 envs and 64x64 depth frames."""
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    from quadsim import cli as rcli
+
+    n = 8192
+    phys = rcli.bench_physics("full", n, max(2, min(50, 40_000 // n)), 5, 3)
+    depth = rcli.bench_depth(64, 1, 5, 3)  # 1 frame per trial (the harness's 10 take 80 s here)
+    return {"bench_physics_full_8192_steps_per_s": phys, "bench_depth_64x64_64envs_images_per_s": depth,
+            "rays_per_s": depth * 64 * 64, "harness": "quadsim.cli.bench_physics / bench_depth (q/cli.py:202-256)",
+            "cores": 1}
+
+
 def _cpu_depth_worker(args):
     """C3 depth on the host: the oracle's render_depth (the reference's
     algorithm: fov cull, then every kept solid per ray, fp64) over a few
@@ -122,6 +191,18 @@ def cpu_baseline(seconds: float, model: str, T: int, n_sample: int = 4096, extra
     cores = len(os.sched_getaffinity(0))
     per = max(1, n_sample // cores)
     ctx = mp.get_context("fork")
+    if have_ref_pkg() and model == "full":  # the reference package itself
+        with ctx.Pool(cores) as pool:
+            res = pool.map(_ref_worker, [(per, T, seconds, 1000 + i) for i in range(cores)])
+        steps = sum(r[0] for r in res)
+        wall = max(r[1] for r in res)
+        out = {"value": steps / wall, "unit": UNIT, "cores": cores, "kind": "reference",
+               "sample": f"{cores} procs x {per} envs: the reference package (quadsim, baseline/_ref) position "
+                         f"task, full quadrotor, T={T} windows of FlightTask.step on its Tape + Tape.backward + "
+                         f"ImuModel.read per step, fp64, for {wall:.1f}s"}
+        if extras:
+            out["continuity"] = reference_continuity()
+        return out
     with ctx.Pool(cores) as pool:
         res = pool.map(_cpu_worker, [(per, T, model, seconds, 1000 + i) for i in range(cores)])
         # depth (the metric's second half): 16 courses per process, 64x48
@@ -882,12 +963,15 @@ def run_reference(a):
     ms = a.envs * a.horizon / v * 1e3
     last["value"] = v
     last["host"] = cpu_model()
+    if last.get("kind") == "reference":
+        last["continuity"] = reference_continuity()
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "config": {
             "workload": f"C2: {a.model} quadrotor + IMU, position task, BPTT window T={a.horizon} fwd+bwd; "
-                        f"CPU oracle port on a bounded env sample"},
+                        + ("the reference package (baseline/_ref)" if last.get("kind") == "reference"
+                           else "CPU oracle port") + " on a bounded env sample"},
         "cpu_baseline": last, "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
