@@ -282,6 +282,11 @@ int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale
                         const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
                         float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
                         int32_t n_sm, void* stream);
+/* The value MLP's forward only (the TD-lambda targets' values and bootstrap,
+ * q/learners.py:286-292) on the same tcgen05 path: pred (m,) fp32, k <= 14. */
+int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* W0, const float* b0,
+                       const float* W1, const float* b1, const float* w2, const float* b2, float* pred,
+                       int32_t n_sm, void* stream);
 
 /* sdf_np / sdf_var (q/sensors.py:417-501): points (N,4); out (N,); grad (N,4) | NULL */
 int qs_sdf(const qs_scene* scene, int32_t n_rows, int32_t n_agents, const float* pts, float* out,

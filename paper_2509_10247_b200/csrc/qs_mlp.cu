@@ -416,13 +416,16 @@ QS_D void st_row8(__nv_bfloat16* buf, int row, int c0, const uint32_t* w) {
   *reinterpret_cast<uint4*>(&buf[umma::blk_off(row, c0, HID)]) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+// FWD: forward only -- pred (the value) of every row into `pred_out`, no
+// backward GEMMs (the TD-lambda targets' values and bootstrap, q/learners.py:286-292)
+template <bool FWD>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_mlp3_fit_grad_tc(int64_t M, int K, float inv_m, const float* __restrict__ x, const float* __restrict__ scale,
                        const float* __restrict__ y, const float* __restrict__ W0, const float* __restrict__ b0,
                        const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ w2,
                        const float* __restrict__ b2, float* __restrict__ gW0, float* __restrict__ gb0,
                        float* __restrict__ gW1, float* __restrict__ gb1, float* __restrict__ gw2,
-                       float* __restrict__ gb2, float* __restrict__ loss) {
+                       float* __restrict__ gb2, float* __restrict__ loss, float* __restrict__ pred_out) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
   using umma::blk_off;
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const char* ys = reinterpret_cast<const char*>(y + r0);
     char* yd = reinterpret_cast<char*>(S.slot[sl].yraw);
     const int ybytes = (int)(nrows * 4);
-    if (tid * 16 < TILE * 4) {
+    if (!FWD && tid * 16 < TILE * 4) {
       const int b = tid * 16, n = ybytes - b >= 16 ? 16 : (ybytes > b ? ybytes - b : 0);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(yd + b)), "l"(ys + (n ? b : 0)),
                    "r"(n)
@@ -587,6 +590,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     const int64_t row = tile * TILE + r;
     const float pred = bias2 + T.predq[0][r] + T.predq[1][r] + T.predq[2][r] + T.predq[3][r];
+    if constexpr (FWD) {
+      if (q == 0 && row < M) pred_out[row] = pred;
+      return;
+    }
     const float e = row < M ? pred - T.yraw[r] : 0.f;
     const float dp = 2.f * inv_m * e;
     if (q == 0) {
@@ -649,6 +656,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       sync_to_mma();
       if (tid == 0) issue_g2(1);
     }
+    if constexpr (FWD) {
+      wait_mma(0);
+      epi2(0, ta);
+      if (two) {
+        wait_mma(1);
+        epi2(1, tb);
+      }
+      __syncthreads();  // every thread is past this pair's slot reads
+      prefetch(0, ta + 2 * (int64_t)gridDim.x);
+      prefetch(1, tb + 2 * (int64_t)gridDim.x);
+      cp_async_commit();
+      continue;
+    }
     wait_mma(0);
     epi2(0, ta);
     sync_to_mma();  // (also: every thread is past its reads of this pair's xraw / yraw)
@@ -678,6 +698,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (two) wait_mma(1);
   }
   cp_async_wait<0>();
+  if constexpr (FWD) {
+    umma::fence_before();
+    __syncthreads();
+    if (warp == 0) umma::tmem_free(T0, 512);
+    return;
+  }
   // ---- flush the TMEM accumulators into the global fp32 gradients (lane = hid row)
   if (!first) {
     float v[32];
@@ -735,14 +761,30 @@ int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale
   if (k < 1 || k > TC_KMAX || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
   const size_t smem = sizeof(TcSmem);
   static_assert(sizeof(TcSmem) <= 227 * 1024, "shared memory");
-  if (cudaFuncSetAttribute(k_mlp3_fit_grad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(k_mlp3_fit_grad_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (m + TILE - 1) / TILE;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_mlp3_fit_grad_tc<<<grid, TC_THREADS, smem, (cudaStream_t)stream>>>(m, k, 1.f / (float)m, x, scale, y, W0, b0,
-                                                                       W1, b1, w2, b2, gW0, gb0, gW1, gb1, gw2,
-                                                                       gb2, loss);
+  k_mlp3_fit_grad_tc<false><<<grid, TC_THREADS, smem, (cudaStream_t)stream>>>(
+      m, k, 1.f / (float)m, x, scale, y, W0, b0, W1, b1, w2, b2, gW0, gb0, gW1, gb1, gw2, gb2, loss, nullptr);
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
+
+int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* W0, const float* b0,
+                       const float* W1, const float* b1, const float* w2, const float* b2, float* pred,
+                       int32_t n_sm, void* stream) {
+  if (m <= 0) return QS_OK;
+  if (k < 1 || k > TC_KMAX || n_sm < 1 || !pred) return QS_ERR_BAD_ARGUMENT;
+  const size_t smem = sizeof(TcSmem);
+  if (cudaFuncSetAttribute(k_mlp3_fit_grad_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return QS_ERR_LAUNCH;
+  const int64_t ntiles = (m + TILE - 1) / TILE;
+  const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
+  k_mlp3_fit_grad_tc<true><<<grid, TC_THREADS, smem, (cudaStream_t)stream>>>(
+      m, k, 1.f, x, scale, nullptr, W0, b0, W1, b1, w2, b2, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+      nullptr, pred);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 

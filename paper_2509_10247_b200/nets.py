@@ -319,6 +319,31 @@ def value_fit_grad(value: "ValueNet", x: torch.Tensor, y: torch.Tensor) -> torch
     return loss[0]
 
 
+def value_forward(value: "ValueNet", x: torch.Tensor) -> torch.Tensor:
+    """value(x) for the reference critic shape (two tanh layers of width 128,
+    <= 14 inputs) by one tcgen05 kernel (``qs_mlp3_forward_tc``; bf16 operands,
+    fp32 accumulation in TMEM, as torch's bf16 autocast computes it), no
+    autograd: the TD-lambda targets' values and bootstrap (q/learners.py:286-292)."""
+    from paper_2509_10247_b200 import _lib as L
+
+    layers = value.value.layers
+    if len(layers) != 3 or layers[0].W.shape[1] != 128 or layers[1].W.shape != (128, 128) or \
+            layers[2].W.shape != (128, 1) or x.shape[1] > 14:
+        raise ValueError("value_forward: needs the (128, 128) critic with <= 14 inputs")
+    dev = x.device
+    x = x.contiguous().float()
+    M, K = x.shape
+    w = [p.detach().float().contiguous() for p in (layers[0].W, layers[0].b, layers[1].W, layers[1].b,
+                                                   layers[2].W, layers[2].b)]
+    scale = value.input_scale.to(device=dev, dtype=torch.float32).contiguous()
+    out = torch.empty(M, dtype=torch.float32, device=dev)
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    L.check(L.lib().qs_mlp3_forward_tc(M, K, L.ptr(x), L.ptr(scale), L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]),
+                                       L.ptr(w[3]), L.ptr(w[4]), L.ptr(w[5]), L.ptr(out), n_sm,
+                                       L.stream_handle(dev)), "qs_mlp3_forward_tc")
+    return out
+
+
 # ---------------------------------------------------------------------------
 # the reference's parameter names <-> module parameters
 

@@ -22,7 +22,8 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from paper_2509_10247_b200.nets import LOG_SIGMA_MIN, PolicyArch, PolicyNet, ValueNet, value_fit_grad  # noqa: F401
+from paper_2509_10247_b200.nets import (LOG_SIGMA_MIN, PolicyArch, PolicyNet, ValueNet, value_fit_grad,  # noqa: F401
+                                        value_forward)
 
 
 @dataclass
@@ -448,9 +449,14 @@ class ShortHorizonTrainer:
         opts = self.opts
         with torch.no_grad():
             T, N, K = priv.shape
-            with self._nets():
-                values = self.value(priv.reshape(T * N, K)).reshape(T, N)
-                boot = self.value(self.env.privileged_state())
+            if self._amp and K <= 14 and tuple(opts.mlp) == (128, 128) and opts.fused_critic:
+                # the critic's values for the targets on the tcgen05 path (one kernel each)
+                values = value_forward(self.value, priv.reshape(T * N, K)).reshape(T, N)
+                boot = value_forward(self.value, self.env.privileged_state())
+            else:
+                with self._nets():
+                    values = self.value(priv.reshape(T * N, K)).reshape(T, N)
+                    boot = self.value(self.env.privileged_state())
             targets = td_lambda_targets(r, values, boot, dones, opts.gamma, opts.td_lambda, opts.k_steps)
         X = priv.reshape(-1, priv.shape[-1])
         y = targets.reshape(-1)

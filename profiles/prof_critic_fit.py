@@ -47,7 +47,12 @@ def fwd():
         val(X)
 
 
-res = {"fused_grad_ms": timed(fused), "torch_autocast_grad_ms": timed(torch_ag), "torch_fwd_ms": timed(fwd)}
+def fwd_tc():
+    nets.value_forward(val, X)
+
+
+res = {"fused_grad_ms": timed(fused), "torch_autocast_grad_ms": timed(torch_ag), "torch_fwd_ms": timed(fwd),
+       "tcgen05_fwd_ms": timed(fwd_tc)}
 flops = M * 2 * (16 * 128 + 3 * 128 * 128 + 16 * 128)
 res["fused_tflops"] = flops / (res["fused_grad_ms"] * 1e-3) / 1e12
 print(res)

@@ -161,6 +161,24 @@ def test_fused_critic_gradient_matches_autograd(M, kernel, monkeypatch):
         assert err < 3e-2, err
 
 
+def test_tcgen05_value_forward_matches_torch():
+    """qs_mlp3_forward_tc (the critic's forward on tcgen05, bf16 operands,
+    fp32 TMEM accumulation) against torch in fp32, ragged row count."""
+    from paper_2509_10247_b200 import nets
+
+    rng = np.random.default_rng(6)
+    val = nets.ValueNet(14, rng, input_scale=tuple(np.linspace(0.2, 1.0, 14))).cuda()
+    with torch.no_grad():
+        for p in val.parameters():
+            p.add_(torch.randn_like(p) * 0.05)
+    X = torch.randn(128 * 148 * 2 + 333, 14, device="cuda")
+    got = nets.value_forward(val, X)
+    with torch.no_grad():
+        ref = val(X)
+    err = float((got - ref).abs().max()) / float(ref.abs().max())
+    assert err < 2e-2, err
+
+
 def test_shac_with_fused_critic_fits_values():
     import paper_2509_10247_b200 as qs
     from paper_2509_10247_b200.train import LearnerOptions, ShortHorizonTrainer
