@@ -288,6 +288,21 @@ int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale,
                        const float* W1, const float* b1, const float* w2, const float* b2, float* pred,
                        int32_t n_sm, void* stream);
 
+/* The policy's MLP trunk + Gaussian heads (q/nets.py:198-256; PolicyArch with
+ * hidden 64, mlp (128, 128)) on tcgen05: y = tanh(tanh(tanh(h W0 + b0) W1 + b1)
+ * W2 + b2) Wh + bh for h (n, 64) fp32; W0 (64,128), W1, W2 (128,128), Wh
+ * (128, n_out) row-major fp32, n_out <= 8 (mu | log sigma). */
+int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W0, const float* b0, const float* W1,
+                        const float* b1, const float* W2, const float* b2, const float* Wh, const float* bh, float* y,
+                        int32_t n_sm, void* stream);
+/* Its backward: given dL/dy (n, n_out), recomputes the forward per tile,
+ * writes dL/dh (n, 64) and ACCUMULATES every weight / bias gradient (same
+ * shapes as the parameters, caller-zeroed). */
+int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
+                        const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
+                        float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
+                        float* gWh, float* gbh, int32_t n_sm, void* stream);
+
 /* sdf_np / sdf_var (q/sensors.py:417-501): points (N,4); out (N,); grad (N,4) | NULL */
 int qs_sdf(const qs_scene* scene, int32_t n_rows, int32_t n_agents, const float* pts, float* out,
            float* grad, void* stream);

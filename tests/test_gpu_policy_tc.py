@@ -1,0 +1,52 @@
+"""The policy trunk + Gaussian heads on tcgen05 (qs_policy_trunk_fwd/_bwd,
+q/nets.py:198-256) against torch autograd in fp32 on the same weights: the
+forward y, dL/dh and every parameter gradient to bf16-operand accuracy."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ptrs(*ts):
+    from paper_2509_10247_b200 import _lib as L
+
+    return [L.ptr(t) for t in ts]
+
+
+@pytest.mark.parametrize("n_out,N", [(6, 128 * 148 + 77), (8, 1000)])
+def test_policy_trunk_fwd_bwd_match_autograd(n_out, N):
+    from paper_2509_10247_b200 import _lib as L
+
+    g = torch.Generator().manual_seed(n_out)
+    r = lambda *s, sc=1.0: (torch.randn(*s, generator=g) * sc).cuda()  # noqa: E731
+    W0, b0 = r(64, 128, sc=0.15), r(128, sc=0.1)
+    W1, b1 = r(128, 128, sc=0.1), r(128, sc=0.1)
+    W2, b2 = r(128, 128, sc=0.1), r(128, sc=0.1)
+    Wh, bh = r(128, n_out, sc=0.1), r(n_out, sc=0.1)
+    h = r(N, 64, sc=0.8)
+    dy = r(N, n_out)
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    y = torch.empty(N, n_out, device="cuda")
+    L.check(L.lib().qs_policy_trunk_fwd(N, n_out, *_ptrs(h, W0, b0, W1, b1, W2, b2, Wh, bh, y), n_sm,
+                                        L.stream_handle()), "fwd")
+    params = [W0, b0, W1, b1, W2, b2, Wh, bh]
+    grads = [torch.zeros_like(p) for p in params]
+    dh = torch.empty_like(h)
+    L.check(L.lib().qs_policy_trunk_bwd(N, n_out, *_ptrs(h, dy, W0, b0, W1, b1, W2, b2, Wh, dh, grads[0], grads[1],
+                                                           grads[2], grads[3], grads[4], grads[5], grads[6],
+                                                           grads[7]), n_sm, L.stream_handle()), "bwd")
+    leaves = [p.clone().requires_grad_(True) for p in params]
+    hl = h.clone().requires_grad_(True)
+    w0, c0, w1, c1, w2, c2, wh, ch = leaves
+    z = torch.tanh(torch.tanh(torch.tanh(hl @ w0 + c0) @ w1 + c1) @ w2 + c2)
+    y_ref = z @ wh + ch
+    (y_ref * dy).sum().backward()
+
+    def rel(a, b):
+        return float((a - b).abs().max()) / (float(b.abs().max()) + 1e-12)
+
+    assert rel(y, y_ref.detach()) < 2e-2, rel(y, y_ref.detach())
+    assert rel(dh, hl.grad) < 3e-2, rel(dh, hl.grad)
+    for name, a, b in zip(["W0", "b0", "W1", "b1", "W2", "b2", "Wh", "bh"], grads, [p.grad for p in leaves]):
+        assert rel(a, b) < 3e-2, (name, rel(a, b))
