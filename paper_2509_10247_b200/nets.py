@@ -180,6 +180,50 @@ class ConvEncoder(torch.nn.Module):
         return torch.tanh(self.out(feat))
 
 
+# the trunk + heads of the reference policy shape on the tcgen05 kernels
+# (qs_policy_trunk_fwd/_bwd) under bf16 autocast; QS_POLICY_TRUNK=torch keeps
+# torch's GEMMs
+FUSED_TRUNK = os.environ.get("QS_POLICY_TRUNK", "tc") != "torch"
+
+
+class _TrunkFn(torch.autograd.Function):
+    """y = tanh(tanh(tanh(h W0 + b0) W1 + b1) W2 + b2) Wh + bh (q/nets.py:241-256)
+    as two tcgen05 kernels: the forward, and a backward that recomputes the
+    forward per 128-row tile and returns dL/dh with every parameter gradient
+    (bf16 operands, fp32 accumulation -- torch's bf16 autocast arithmetic)."""
+
+    @staticmethod
+    def forward(ctx, h, W0, b0, W1, b1, W2, b2, Wh, bh):
+        from paper_2509_10247_b200 import _lib as L
+
+        h = h.contiguous()
+        ws = [t.detach().float().contiguous() for t in (W0, b0, W1, b1, W2, b2, Wh, bh)]
+        N, n_out = h.shape[0], ws[6].shape[1]
+        y = torch.empty(N, n_out, dtype=torch.float32, device=h.device)
+        n_sm = torch.cuda.get_device_properties(h.device).multi_processor_count
+        L.check(L.lib().qs_policy_trunk_fwd(N, n_out, L.ptr(h), *[L.ptr(t) for t in ws], L.ptr(y), n_sm,
+                                            L.stream_handle(h.device)), "qs_policy_trunk_fwd")
+        ctx.save_for_backward(h, *ws[:7])
+        ctx.n_sm = n_sm
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        from paper_2509_10247_b200 import _lib as L
+
+        h, W0, b0, W1, b1, W2, b2, Wh = ctx.saved_tensors
+        gy = gy.contiguous().float()
+        N, n_out = gy.shape
+        dh = torch.empty_like(h)
+        grads = [torch.zeros_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
+        gbh = torch.zeros(n_out, dtype=torch.float32, device=h.device)
+        L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h), L.ptr(gy), *[L.ptr(t) for t in
+                                                                              (W0, b0, W1, b1, W2, b2, Wh)],
+                                            L.ptr(dh), *[L.ptr(t) for t in grads], L.ptr(gbh), ctx.n_sm,
+                                            L.stream_handle(h.device)), "qs_policy_trunk_bwd")
+        return (dh, *grads, gbh)
+
+
 @dataclass
 class PolicyArch:
     """q/nets.py:183-195."""
@@ -239,12 +283,20 @@ class PolicyNet(torch.nn.Module):
                 h = torch.zeros(x.shape[0], self.hidden, device=x.device, dtype=x.dtype)
             h = self.gru(x, h.to(x.dtype)).float() if x.dtype != torch.float64 else self.gru(x, h)
             x = h.to(x.dtype)
+        A = self.arch.action_dim
+        layers = self.trunk.layers
+        if (FUSED_TRUNK and x.is_cuda and x.dim() == 2 and x.dtype == torch.float32 and torch.is_autocast_enabled()
+                and x.shape[1] == 64 and len(layers) == 3 and tuple(l.W.shape for l in layers) ==
+                ((64, 128), (128, 128), (128, 128)) and 2 * A <= 8):
+            # bf16 policy mode: trunk and both heads in two tcgen05 kernels
+            y = _TrunkFn.apply(x, layers[0].W, layers[0].b, layers[1].W, layers[1].b, layers[2].W, layers[2].b,
+                               torch.cat([self.mu.W, self.sig.W], 1), torch.cat([self.mu.b, self.sig.b]))
+            return y[:, :A], torch.clamp(y[:, A:2 * A], LOG_SIGMA_MIN, self.arch.log_sigma_max), h
         z = torch.tanh(self.trunk(x))
         if z.is_cuda and z.dim() == 2:
             # both heads as ONE GEMM, widened to a multiple of 8 outputs (the
             # narrow N = A GEMMs, and their weight-gradient GEMMs with N = A,
             # fall to slow unaligned kernels)
-            A = self.arch.action_dim
             pad = (-2 * A) % 8
             W = torch.nn.functional.pad(torch.cat([self.mu.W, self.sig.W], 1), (0, pad))
             b = torch.nn.functional.pad(torch.cat([self.mu.b, self.sig.b]), (0, pad))

@@ -50,3 +50,37 @@ def test_policy_trunk_fwd_bwd_match_autograd(n_out, N):
     assert rel(dh, hl.grad) < 3e-2, rel(dh, hl.grad)
     for name, a, b in zip(["W0", "b0", "W1", "b1", "W2", "b2", "Wh", "bh"], grads, [p.grad for p in leaves]):
         assert rel(a, b) < 3e-2, (name, rel(a, b))
+
+
+def test_policynet_autocast_uses_trunk_kernels_and_matches_torch_path():
+    """PolicyNet under bf16 autocast routes the trunk + heads through
+    _TrunkFn; its outputs and parameter gradients agree with the torch bf16
+    path (QS_POLICY_TRUNK=torch) of the same module."""
+    import numpy as np
+
+    from paper_2509_10247_b200 import nets
+
+    arch = nets.PolicyArch(proprio_dim=10, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128))
+    pol = nets.PolicyNet(arch, np.random.default_rng(3)).cuda()
+    x = torch.randn(3000, 10, device="cuda")
+    h0 = torch.randn(3000, 64, device="cuda") * 0.5
+
+    def run(fused):
+        old = nets.FUSED_TRUNK
+        nets.FUSED_TRUNK = fused
+        try:
+            pol.zero_grad(set_to_none=True)
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                mu, ls, h = pol(x, h=h0)
+            (mu.square().sum() + (ls * 0.3).sum() + h.square().sum()).backward()
+            return mu.detach(), ls.detach(), {k: p.grad.clone() for k, p in pol.named_parameters()}
+        finally:
+            nets.FUSED_TRUNK = old
+
+    mu_f, ls_f, g_f = run(True)
+    mu_t, ls_t, g_t = run(False)
+    assert float((mu_f - mu_t).abs().max()) < 2e-2 * float(mu_t.abs().max()) + 1e-4
+    assert float((ls_f - ls_t).abs().max()) < 2e-2 * float(ls_t.abs().max()) + 1e-4
+    for k in g_t:
+        d = float((g_f[k] - g_t[k]).abs().max())
+        assert d < 5e-2 * float(g_t[k].abs().max()) + 1e-6, (k, d)
