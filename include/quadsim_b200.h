@@ -276,12 +276,16 @@ int qs_mlp3_fit_grad(int64_t m, int32_t k, const float* x, const float* scale, c
                      float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
                      int32_t n_sm, void* stream);
 /* The same fit step on the 5th-generation tensor cores (tcgen05.mma, TMEM
- * accumulators, one persistent 128-thread CTA per SM): k <= 14 (the two spare
- * input columns carry the bias and w2 gradients through the MMAs). */
+ * accumulators, one persistent 512-thread CTA per SM): k <= 14 (the two spare
+ * input columns carry the bias gradients through the MMAs).  `work` holds
+ * qs_mlp3_work_floats(n_sm) floats of scratch: each CTA writes its partial
+ * gradients there and a second kernel sums them in CTA order, so the
+ * gradients and the loss are bitwise reproducible (no float atomics). */
 int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
                         const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
                         float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
-                        int32_t n_sm, void* stream);
+                        float* work, int64_t work_floats, int32_t n_sm, void* stream);
+int64_t qs_mlp3_work_floats(int32_t n_sm);
 /* The value MLP's forward only (the TD-lambda targets' values and bootstrap,
  * q/learners.py:286-292) on the same tcgen05 path: pred (m,) fp32, k <= 14. */
 int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* W0, const float* b0,
@@ -301,7 +305,26 @@ int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W
 int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
                         const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
-                        float* gWh, float* gbh, int32_t n_sm, void* stream);
+                        float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream);
+/* The GRU cell (q/nets.py:107-132; Wi (n_in, 192), Wh_g (64, 192), gates
+ * r|z|n) fused in front of the trunk: h_out (n, 64) = GRU(x (n, n_in), h),
+ * y = trunk + heads of h_out.  n_in <= 16. */
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, const float* h, const float* Wi,
+                      const float* bi, const float* Wh_g, const float* bh_g, const float* W0, const float* b0,
+                      const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
+                      const float* bh, float* h_out, float* y, int32_t n_sm, void* stream);
+/* The GRU cell's backward for dL/dh_out = dh_out_a + dh_out_b (b may be
+ * NULL): writes dx (n, n_in) and dh (n, 64); ACCUMULATES into gWi, gbi,
+ * gWh_g, gbh_g (zero them first). */
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const float* dh_out_a,
+                      const float* dh_out_b, const float* Wi, const float* bi, const float* Wh_g, const float* bh_g,
+                      float* dx, float* dh, float* gWi, float* gbi, float* gWh_g, float* gbh_g, float* work,
+                      int64_t work_floats, int32_t n_sm, void* stream);
+/* Scratch the gradient kernels above need (floats): which 0 = trunk backward,
+ * 1 = GRU backward; each CTA writes its partial gradients there and a second
+ * kernel sums them in CTA order, so the gradients are bitwise reproducible
+ * (no float atomics).  -1 for a bad argument. */
+int64_t qs_policy_work_floats(int32_t which, int32_t n_sm);
 
 /* sdf_np / sdf_var (q/sensors.py:417-501): points (N,4); out (N,); grad (N,4) | NULL */
 int qs_sdf(const qs_scene* scene, int32_t n_rows, int32_t n_agents, const float* pts, float* out,

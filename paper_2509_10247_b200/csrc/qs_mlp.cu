@@ -23,6 +23,7 @@
 // accumulators, biases and all gradients are fp32.
 #include <cuda_bf16.h>
 
+#include "qs_reduce.cuh"
 #include "qs_umma.cuh"
 
 namespace {
@@ -396,9 +397,15 @@ struct TcSmem {
   __nv_bfloat16 W1T[HID * HID];    // [hid2][hid1] blocked (K-major B of G2, MN-major B of G3)
   float b0[HID], b1[HID], w2[HID];
   float red[2];                    // db2, loss
+  float w2p[4][HID];               // dw2 per row quarter (warp % 4)
+  float redp[4][2];                // db2, loss per row quarter
   uint64_t bar[2];
   uint32_t tbase;
 };
+// per-CTA gradient partials of the tcgen05 fit (qs_reduce.cuh)
+constexpr int64_t CK_W1 = 0, CK_W0 = CK_W1 + HID * HID, CK_B0 = CK_W0 + 16 * HID, CK_B1 = CK_B0 + HID,
+                  CK_W2 = CK_B1 + HID, CK_B2 = CK_W2 + HID, CK_L = CK_B2 + 1,
+                  CK_P = (CK_L + 1 + 31) / 32 * 32;  // rows 128-byte aligned (float4 stores)
 
 // 32 consecutive columns of this thread's TMEM lane
 QS_D void tmem_ld32(uint32_t t, float (&v)[32]) {
@@ -425,7 +432,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                        const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ w2,
                        const float* __restrict__ b2, float* __restrict__ gW0, float* __restrict__ gb0,
                        float* __restrict__ gW1, float* __restrict__ gb1, float* __restrict__ gw2,
-                       float* __restrict__ gb2, float* __restrict__ loss, float* __restrict__ pred_out) {
+                       float* __restrict__ gb2, float* __restrict__ loss, float* __restrict__ pred_out,
+                       float* __restrict__ work) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
   using umma::blk_off;
@@ -704,32 +712,45 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 0) umma::tmem_free(T0, 512);
     return;
   }
-  // ---- flush the TMEM accumulators into the global fp32 gradients (lane = hid row)
-  if (!first) {
+  // ---- this CTA's partial gradients (TMEM lane = hid row) -> work; summed
+  // over the CTAs in a fixed order by red::sum_partials
+  float* wk = work + (int64_t)blockIdx.x * CK_P;
+  {
     float v[32];
-    tmem_ld32(T_W1 + my, v);
+    if (!first) {
+      tmem_ld32(T_W1 + my, v);
+    } else {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) atomicAdd(&gW1[r * HID + cq + j], v[j]);
-    if (q == 0) {
-      float u[16];
-      umma::tmem_ld16(umma::taddr(T_W0, 32 * (warp & 3), 0), u);
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    }
 #pragma unroll
-      for (int k = 0; k < TC_KMAX; ++k)
-        if (k < K) atomicAdd(&gW0[k * HID + r], u[k]);
-      atomicAdd(&gb0[r], u[KIN - 1]);
-    } else if (q == 1) {
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(wk + CK_W1 + r * HID + cq + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    if (q < 2) {
       float u[16];
-      umma::tmem_ld16(umma::taddr(T_B1, 32 * (warp & 3), 0), u);
-      atomicAdd(&gb1[r], u[KIN - 1]);
+      if (!first) {
+        umma::tmem_ld16(umma::taddr(q == 0 ? T_W0 : T_B1, 32 * (warp & 3), 0), u);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) u[j] = 0.f;
+      }
+      if (q == 0) {
+#pragma unroll
+        for (int k = 0; k < TC_KMAX; ++k)
+          if (k < K) wk[CK_W0 + k * HID + r] = u[k];
+        wk[CK_B0 + r] = u[KIN - 1];
+      } else {
+        wk[CK_B1 + r] = u[KIN - 1];
+      }
     }
   }
-  // dw2: reduce each column over the warp's 32 rows, one atomic per (warp, column)
+  // dw2: each column reduced over the warp's 32 rows, then over the 4 row quarters in order
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     float v = gw2p[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == j) atomicAdd(&gw2[cq + j], v);
+    if (lane == j) S.w2p[warp & 3][cq + j] = v;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -737,15 +758,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     loss_acc += __shfl_xor_sync(0xffffffffu, loss_acc, o);
   }
   if (lane == 0 && q == 0) {
-    atomicAdd(&S.red[0], gb2_acc);
-    atomicAdd(&S.red[1], loss_acc);
+    S.redp[warp & 3][0] = gb2_acc;
+    S.redp[warp & 3][1] = loss_acc;
   }
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free(T0, 512);
+  if (tid < HID) wk[CK_W2 + tid] = (S.w2p[0][tid] + S.w2p[1][tid]) + (S.w2p[2][tid] + S.w2p[3][tid]);
   if (tid == 0) {
-    atomicAdd(gb2, S.red[0]);
-    atomicAdd(loss, S.red[1] * inv_m);
+    wk[CK_B2] = (S.redp[0][0] + S.redp[1][0]) + (S.redp[2][0] + S.redp[3][0]);
+    wk[CK_L] = ((S.redp[0][1] + S.redp[1][1]) + (S.redp[2][1] + S.redp[3][1])) * inv_m;
   }
 }
 
@@ -753,12 +775,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
 extern "C" {
 
+int64_t qs_mlp3_work_floats(int32_t n_sm) { return n_sm < 1 ? -1 : (int64_t)n_sm * CK_P; }
+
 int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* y, const float* W0,
                         const float* b0, const float* W1, const float* b1, const float* w2, const float* b2,
                         float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
-                        int32_t n_sm, void* stream) {
+                        float* work, int64_t work_floats, int32_t n_sm, void* stream) {
   if (m <= 0) return QS_OK;
   if (k < 1 || k > TC_KMAX || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
+  if (!work || work_floats < (int64_t)n_sm * CK_P) return QS_ERR_BAD_ARGUMENT;
   const size_t smem = sizeof(TcSmem);
   static_assert(sizeof(TcSmem) <= 227 * 1024, "shared memory");
   if (cudaFuncSetAttribute(k_mlp3_fit_grad_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
@@ -767,8 +792,13 @@ int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale
   const int64_t ntiles = (m + TILE - 1) / TILE;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
   k_mlp3_fit_grad_tc<false><<<grid, TC_THREADS, smem, (cudaStream_t)stream>>>(
-      m, k, 1.f / (float)m, x, scale, y, W0, b0, W1, b1, w2, b2, gW0, gb0, gW1, gb1, gw2, gb2, loss, nullptr);
-  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+      m, k, 1.f / (float)m, x, scale, y, W0, b0, W1, b1, w2, b2, gW0, gb0, gW1, gb1, gw2, gb2, loss, nullptr, work);
+  if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
+  red::Segs sg{{gW1, gW0, gb0, gb1, gw2, gb2, loss},
+               {CK_W1, CK_W0, CK_B0, CK_B1, CK_W2, CK_B2, CK_L},
+               {HID * HID, (int64_t)k * HID, HID, HID, HID, 1, 1},
+               7};
+  return red::sum_partials(work, grid, CK_P, sg, (cudaStream_t)stream);
 }
 
 int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* W0, const float* b0,
@@ -784,7 +814,7 @@ int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale,
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
   k_mlp3_fit_grad_tc<true><<<grid, TC_THREADS, smem, (cudaStream_t)stream>>>(
       m, k, 1.f, x, scale, nullptr, W0, b0, W1, b1, w2, b2, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-      nullptr, pred);
+      nullptr, pred, nullptr);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 

@@ -10,12 +10,18 @@
 //   qs_policy_trunk_bwd  given dL/dy, recompute the forward per tile and
 //                        return dL/dh (for the GRU's backward) while
 //                        accumulating every weight and bias gradient in TMEM.
+//   qs_policy_gru_fwd    the GRU cell (q/nets.py:107-132, gates r, z, n) fused
+//                        in front of the trunk: h' and y from (x, h) in one pass
+//   qs_policy_gru_bwd    the GRU cell's backward: recompute the gates, return
+//                        dL/dx and dL/dh for dL/dh' (trunk + carried), and
+//                        accumulate dWi, dWh, dbi, dbh in TMEM.
 // Same machinery as the critic fit (qs_mlp.cu / qs_umma.cuh): one persistent
 // 512-thread CTA per SM; thread (warp w, lane l) owns tile row 32 (w % 4) + l
 // -- its TMEM lane -- and a quarter of the 128 columns; one elected thread
 // issues tcgen05.mma (bf16 operands in the blocked no-swizzle layout, fp32
 // accumulators in TMEM) and commits to an mbarrier; every weight matrix is
 // staged once and serves as a K-major operand one way and MN-major the other.
+#include "qs_reduce.cuh"
 #include "qs_umma.cuh"
 
 namespace {
@@ -25,6 +31,16 @@ constexpr int TR = 128;     // rows per tile
 constexpr int HI = 64;      // GRU width (trunk input)
 constexpr int HW = 128;     // trunk width
 constexpr int HY = 16;      // head outputs, padded (mu | log sigma | 0 | ones column for bias sums)
+constexpr int XI = 16;      // GRU input width, padded (proprio features)
+constexpr int G3 = 3 * HI;  // GRU gate columns (r | z | n)
+QS_D float sigm_f(float x) { return 1.f / (1.f + __expf(-x)); }
+// per-CTA gradient partials (qs_reduce.cuh): the trunk backward's layout
+constexpr int64_t TK_W0 = 0, TK_B0 = TK_W0 + HI * HW, TK_W1 = TK_B0 + HW, TK_B1 = TK_W1 + HW * HW,
+                  TK_W2 = TK_B1 + HW, TK_B2 = TK_W2 + HW * HW, TK_WH = TK_B2 + HW, TK_BH = TK_WH + HW * 8,
+                  TK_P = (TK_BH + 8 + 31) / 32 * 32;
+// ... and the GRU backward's
+constexpr int64_t GK_WI = 0, GK_BI = GK_WI + XI * G3, GK_WG = GK_BI + G3, GK_BG = GK_WG + HI * G3,
+                  GK_P = (GK_BG + G3 + 31) / 32 * 32;
 
 QS_D float tanh_f(float x) {
   float y;
@@ -75,23 +91,34 @@ struct PolSmem {
   __nv_bfloat16 H[TR * HI];    // [rows][64]  the tile's GRU output
   __nv_bfloat16 A1[TR * HW];   // A1, then dL/dA1-pre in place
   __nv_bfloat16 A2[TR * HW];   // A2, then dL/dA2-pre in place
-  __nv_bfloat16 Z[TR * HW];    // z, then dL/dz-pre in place
+  // backward: z, then dL/dz-pre in place.  Forward: z lives in A1 (dead once
+  // A2 is computed) and this space holds the GRU weights Wi [16][192] and
+  // Wh [64][192] (blocked); the tile's x [128][16] and h [128][64] sit in A2
+  // until the gate GEMMs completed.
+  __nv_bfloat16 Z[TR * HW];
   __nv_bfloat16 DY[TR * HY];   // dL/dy (8 columns), column 15 = 1
   float b0[HW], b1[HW], b2[HW], bh[HY];
-  float dbh[HY];
+  float bg[4 * HI];            // GRU: bi + bh (r, z), bi (n), bh (n)
+  float dbh[4][HY];             // per-warp dL/dbh sums (warps 0-3)
   uint64_t bar;
   uint32_t tbase;
 };
 
-template <bool BWD>
+static_assert(XI * G3 + HI * G3 <= TR * HW && TR * XI + TR * HI <= TR * HW, "GRU staging aliases");
+
+struct GruArgs {  // the forward's GRU cell (GRU = true)
+  int n_in;
+  const float *x, *hp, *Wi, *bi, *Wg, *bg;
+  float* h_out;
+};
+
+template <bool BWD, bool GRU = false>
 __global__ void __launch_bounds__(PT, 1)
-    k_policy_trunk(int64_t N, int n_out, const float* __restrict__ h, const float* __restrict__ dy,
+    k_policy_trunk(int64_t N, int n_out, GruArgs ga, const float* __restrict__ h, const float* __restrict__ dy,
                    const float* __restrict__ W0, const float* __restrict__ b0, const float* __restrict__ W1,
                    const float* __restrict__ b1, const float* __restrict__ W2, const float* __restrict__ b2,
                    const float* __restrict__ Wh, const float* __restrict__ bh, float* __restrict__ y,
-                   float* __restrict__ dh, float* __restrict__ gW0, float* __restrict__ gb0,
-                   float* __restrict__ gW1, float* __restrict__ gb1, float* __restrict__ gW2,
-                   float* __restrict__ gb2, float* __restrict__ gWh, float* __restrict__ gbh) {
+                   float* __restrict__ dh, float* __restrict__ work) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   PolSmem& S = *reinterpret_cast<PolSmem*>(smem_raw);
   using umma::blk_off;
@@ -112,9 +139,19 @@ __global__ void __launch_bounds__(PT, 1)
     S.b1[i] = b1[i];
     S.b2[i] = b2[i];
   }
-  if (tid < HY) {
-    S.bh[tid] = (bh && tid < n_out) ? bh[tid] : 0.f;  // (the backward takes no bh)
-    S.dbh[tid] = 0.f;
+  if (tid < HY) S.bh[tid] = (bh && tid < n_out) ? bh[tid] : 0.f;  // (the backward takes no bh)
+  __nv_bfloat16* const WI = S.Z;             // GRU (forward only)
+  __nv_bfloat16* const WG = S.Z + XI * G3;
+  __nv_bfloat16* const XS = S.A2;
+  __nv_bfloat16* const HS = S.A2 + TR * XI;
+  if constexpr (GRU) {
+    for (int i = tid; i < XI * G3; i += PT) {
+      const int k = i / G3, n = i % G3;
+      WI[blk_off(k, n, G3)] = __float2bfloat16_rn(k < ga.n_in ? ga.Wi[k * G3 + n] : 0.f);
+    }
+    for (int i = tid; i < HI * G3; i += PT) WG[blk_off(i / G3, i % G3, G3)] = __float2bfloat16_rn(ga.Wg[i]);
+    for (int i = tid; i < 4 * HI; i += PT)
+      S.bg[i] = i < 2 * HI ? ga.bi[i] + ga.bg[i] : i < 3 * HI ? ga.bi[i] : ga.bg[i - HI];
   }
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
@@ -152,6 +189,10 @@ __global__ void __launch_bounds__(PT, 1)
   auto mK = [](const __nv_bfloat16* b, int cols, int ks) {
     return umma::desc_mnmajor(b + ks * 2 * (cols / 8) * 64, cols);
   };
+  // the same from MN column c0 (a multiple of 8)
+  auto mKc = [](const __nv_bfloat16* b, int cols, int ks, int c0) {
+    return umma::desc_mnmajor(b + ks * 2 * (cols / 8) * 64 + (c0 / 8) * 64, cols);
+  };
   // epilogue: TMEM columns [cq, cq+32) of this row + bias -> tanh -> bf16 row of dst
   auto epi_tanh = [&](const float* bias, __nv_bfloat16* dst) {
     float v[32];
@@ -182,8 +223,70 @@ __global__ void __launch_bounds__(PT, 1)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = tile * TR + r;
     const bool valid = row < N;
-    // ---- stage h (quarter q: columns 16q..16q+15) and, backward, dL/dy
-    {
+    if constexpr (GRU) {
+      // ---- the GRU cell: gates from x and the carried h; TMEM [128,256)
+      // r|z pre-activations (x Wi + h Wh summed), [256,320) x Wi_n, [320,384) h Wh_n
+      float hp[16];
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(ga.hp + row * HI + 16 * q + j))
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+        hp[j] = t.x;
+        hp[j + 1] = t.y;
+        hp[j + 2] = t.z;
+        hp[j + 3] = t.w;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 8)
+        *reinterpret_cast<uint4*>(&HS[blk_off(r, 16 * q + j, HI)]) = make_uint4(
+            pk(hp[j], hp[j + 1]), pk(hp[j + 2], hp[j + 3]), pk(hp[j + 4], hp[j + 5]), pk(hp[j + 6], hp[j + 7]));
+      if (q == 0) {
+        float xv[XI];
+#pragma unroll
+        for (int j = 0; j < XI; ++j) xv[j] = (valid && j < ga.n_in) ? __ldg(ga.x + row * ga.n_in + j) : 0.f;
+#pragma unroll
+        for (int j = 0; j < XI; j += 8)
+          *reinterpret_cast<uint4*>(&XS[blk_off(r, j, XI)]) = make_uint4(
+              pk(xv[j], xv[j + 1]), pk(xv[j + 2], xv[j + 3]), pk(xv[j + 4], xv[j + 5]), pk(xv[j + 6], xv[j + 7]));
+      }
+      to_mma();
+      if (tid == 0) {
+        const uint32_t id128 = umma::idesc_bf16(128, 128, false, true), id64 = umma::idesc_bf16(128, 64, false, true);
+        umma::mma_bf16(T0 + 128, aK(XS, XI, 0), mKc(WI, G3, 0, 0), id128, false);
+#pragma unroll
+        for (int ks = 0; ks < HI / 16; ++ks) umma::mma_bf16(T0 + 128, aK(HS, HI, ks), mKc(WG, G3, ks, 0), id128, true);
+        umma::mma_bf16(T0 + 256, aK(XS, XI, 0), mKc(WI, G3, 0, 2 * HI), id64, false);
+#pragma unroll
+        for (int ks = 0; ks < HI / 16; ++ks)
+          umma::mma_bf16(T0 + 320, aK(HS, HI, ks), mKc(WG, G3, ks, 2 * HI), id64, ks > 0);
+        umma::commit(&S.bar);
+      }
+      wait();
+      {  // h' = (1 - z) n + z h for units 16q..16q+15 of this row
+        float gr[16], gz[16], gn[16], hn[16];
+        umma::tmem_ld16(T0 + 128 + lanes + 16 * q, gr);
+        umma::tmem_ld16(T0 + 128 + lanes + HI + 16 * q, gz);
+        umma::tmem_ld16(T0 + 256 + lanes + 16 * q, gn);
+        umma::tmem_ld16(T0 + 320 + lanes + 16 * q, hn);
+        float o[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int u = 16 * q + j;
+          const float rr = sigm_f(gr[j] + S.bg[u]), zz = sigm_f(gz[j] + S.bg[HI + u]);
+          const float nn = tanh_f(gn[j] + S.bg[2 * HI + u] + rr * (hn[j] + S.bg[3 * HI + u]));
+          o[j] = nn + zz * (hp[j] - nn);
+        }
+        if (valid) {
+          float4* dst = reinterpret_cast<float4*>(ga.h_out + row * HI + 16 * q);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j += 8)
+          *reinterpret_cast<uint4*>(&S.H[blk_off(r, 16 * q + j, HI)]) =
+              make_uint4(pk(o[j], o[j + 1]), pk(o[j + 2], o[j + 3]), pk(o[j + 4], o[j + 5]), pk(o[j + 6], o[j + 7]));
+      }
+    } else {  // ---- stage h (quarter q: columns 16q..16q+15)
       float v[16];
 #pragma unroll
       for (int j = 0; j < 16; j += 4) {
@@ -199,7 +302,7 @@ __global__ void __launch_bounds__(PT, 1)
         *reinterpret_cast<uint4*>(&S.H[blk_off(r, 16 * q + j, HI)]) =
             make_uint4(pk(v[j], v[j + 1]), pk(v[j + 2], v[j + 3]), pk(v[j + 4], v[j + 5]), pk(v[j + 6], v[j + 7]));
     }
-    if (BWD && q == 0) {
+    if (BWD && q == 0) {  // dL/dy
       float g[HY];
 #pragma unroll
       for (int j = 0; j < HY; ++j) g[j] = 0.f;
@@ -240,14 +343,15 @@ __global__ void __launch_bounds__(PT, 1)
       umma::commit(&S.bar);
     }
     wait();
-    epi_tanh(S.b2, S.Z);
+    __nv_bfloat16* const ZB = BWD ? S.Z : S.A1;  // forward: z over the dead A1 (Z holds the GRU weights)
+    epi_tanh(S.b2, ZB);
     to_mma();
     if constexpr (!BWD) {
       // ---- heads: y = z Wh + bh (N = 16, the first n_out columns written)
       if (tid == 0) {
 #pragma unroll
         for (int ks = 0; ks < HW / 16; ++ks)
-          umma::mma_bf16(TG, aK(S.Z, HW, ks), mK(S.WH, HY, ks), id_k_mn16, ks > 0);
+          umma::mma_bf16(TG, aK(ZB, HW, ks), mK(S.WH, HY, ks), id_k_mn16, ks > 0);
         umma::commit(&S.bar);
       }
       wait();
@@ -330,87 +434,405 @@ __global__ void __launch_bounds__(PT, 1)
     umma::fence_after();
   }
   if constexpr (BWD) {
-    if (!first) {  // flush the TMEM accumulators (lane = the gradient's row index)
-      float v[32];
-      ld32(TW2 + lanes + cq, v);
+    // this CTA's partial gradients (lane = the gradient's row index) -> work;
+    // summed over the CTAs in a fixed order by red::sum_partials
+    float* wk = work + (int64_t)blockIdx.x * TK_P;
+    auto ld32z = [&](uint32_t t, float (&v)[32]) {
+      if (!first) {
+        ld32(t, v);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) atomicAdd(&gW2[r * HW + cq + j], v[j]);
-      ld32(TW1 + lanes + cq, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) atomicAdd(&gW1[r * HW + cq + j], v[j]);
-      float u[16];
-      umma::tmem_ld16(TW0 + lanes + 16 * q, u);  // dW0^T: lane = trunk unit, column = input
-#pragma unroll
-      for (int j = 0; j < 16; ++j) atomicAdd(&gW0[(16 * q + j) * HW + r], u[j]);
-      if (q == 0) {
-        umma::tmem_ld16(TWH + lanes, u);
-#pragma unroll
-        for (int j = 0; j < HY / 2; ++j)
-          if (j < n_out) atomicAdd(&gWh[r * n_out + j], u[j]);
-        umma::tmem_ld16(TB2 + lanes, u);
-        atomicAdd(&gb2[r], u[HY - 1]);
-      } else if (q == 1) {
-        umma::tmem_ld16(TB1 + lanes, u);
-        atomicAdd(&gb1[r], u[HY - 1]);
-      } else if (q == 2) {
-        umma::tmem_ld16(TB0 + lanes, u);
-        atomicAdd(&gb0[r], u[HY - 1]);
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
-    }
-    if (q == 0) {  // dbh: per-row sums of dL/dy, reduced over the warp then the CTA
+    };
+    auto ld16z = [&](uint32_t t, float (&v)[16]) {
+      if (!first) {
+        umma::tmem_ld16(t, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+      }
+    };
+    float v[32];
+    ld32z(TW2 + lanes + cq, v);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(wk + TK_W2 + r * HW + cq + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    ld32z(TW1 + lanes + cq, v);
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(wk + TK_W1 + r * HW + cq + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    float u[16];
+    ld16z(TW0 + lanes + 16 * q, u);  // dW0^T: lane = trunk unit, column = input
+#pragma unroll
+    for (int j = 0; j < 16; ++j) wk[TK_W0 + (16 * q + j) * HW + r] = u[j];
+    if (q == 0) {
+      ld16z(TWH + lanes, u);
+#pragma unroll
+      for (int j = 0; j < HY / 2; ++j)
+        if (j < n_out) wk[TK_WH + r * n_out + j] = u[j];
+      ld16z(TB2 + lanes, u);
+      wk[TK_B2 + r] = u[HY - 1];
+      // dbh: per-row sums of dL/dy over the tiles, reduced over the warp
 #pragma unroll
       for (int j = 0; j < HY / 2; ++j) {
-        float v = dbh_acc[j];
+        float t = dbh_acc[j];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) atomicAdd(&S.dbh[j], v);
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) S.dbh[warp][j] = t;
+      }
+    } else if (q == 1) {
+      ld16z(TB1 + lanes, u);
+      wk[TK_B1 + r] = u[HY - 1];
+    } else if (q == 2) {
+      ld16z(TB0 + lanes, u);
+      wk[TK_B0 + r] = u[HY - 1];
+    }
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free(T0, 512);
+  if (BWD && tid < n_out)
+    work[(int64_t)blockIdx.x * TK_P + TK_BH + tid] = (S.dbh[0][tid] + S.dbh[1][tid]) + (S.dbh[2][tid] + S.dbh[3][tid]);
+}
+
+// ---- the GRU cell's backward (q/nets.py:107-132 differentiated):
+//   r = s(ar), z = s(az), n = tanh(an), an = xWi_n + bi_n + r (hWh_n + bh_n),
+//   h' = n + z (h - n);  for g = dL/dh':
+//   dn = g (1 - z), dz = g (h - n), dan = dn (1 - n^2), dr = dan (hWh_n + bh_n)
+//   dar = dr r (1 - r), daz = dz z (1 - z)
+//   dgi = [dar | daz | dan], dgh = [dar | daz | dan r]
+//   dx = dgi Wi^T, dh = g z + dgh Wh^T, dWi = x^T dgi, dWh = h^T dgh
+// Weight gradients as (gate units) x [x | h | 1]: two M = 128 GEMMs per tile
+// over B = [x | h | 1] (96 columns) -- rows r|z of dgi^T (= dgh^T), and
+// [dan | dan r]^T (rows 0-63 give dWi_n, dbi_n; rows 64-127 dWh_n, dbh_n).
+struct GruSmem {
+  __nv_bfloat16 WI[XI * G3];   // [16][192]  MN-major B of x Wi, K-major B of dgi Wi^T
+  __nv_bfloat16 WG[HI * G3];   // [64][192]
+  __nv_bfloat16 B[TR * 96];    // [rows][x 0-15 | h 16-79 | 1 80 | 0]
+  __nv_bfloat16 GRZ[TR * HW];  // [rows][dar | daz]
+  __nv_bfloat16 GN[TR * HW];   // [rows][dan | dan r]
+  float bg[4 * HI];
+  uint64_t bar;
+  uint32_t tbase;
+};
+
+__global__ void __launch_bounds__(PT, 1)
+    k_gru_bwd(int64_t N, int n_in, const float* __restrict__ x, const float* __restrict__ hp,
+              const float* __restrict__ dha, const float* __restrict__ dhb, const float* __restrict__ Wi,
+              const float* __restrict__ bi, const float* __restrict__ Wg, const float* __restrict__ bgv,
+              float* __restrict__ dx, float* __restrict__ dhp, float* __restrict__ work) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  GruSmem& S = *reinterpret_cast<GruSmem*>(smem_raw);
+  using umma::blk_off;
+  constexpr int BC = 96;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = 32 * (warp & 3) + lane, q = warp >> 2;
+  for (int i = tid; i < XI * G3; i += PT) {
+    const int k = i / G3, n = i % G3;
+    S.WI[blk_off(k, n, G3)] = __float2bfloat16_rn(k < n_in ? Wi[k * G3 + n] : 0.f);
+  }
+  for (int i = tid; i < HI * G3; i += PT) S.WG[blk_off(i / G3, i % G3, G3)] = __float2bfloat16_rn(Wg[i]);
+  for (int i = tid; i < 4 * HI; i += PT) S.bg[i] = i < 2 * HI ? bi[i] + bgv[i] : i < 3 * HI ? bi[i] : bgv[i - HI];
+  if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
+  if (tid == 0) {
+    mbar_init(&S.bar, 1);
+    fence_barrier_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  const uint32_t T0 = S.tbase;
+  // TMEM: r|z [0,128), x Wi_n [128,192), h Wh_n [192,256) -- then dx [0,16),
+  // dgh Wh^T [64,128); dW r|z [256,352); dW n [352,448)
+  const uint32_t TRZ = T0, TGN = T0 + 128, THN = T0 + 192, TDX = T0, TDH = T0 + 64, TWR = T0 + 256,
+                 TWN = T0 + 352;
+  const uint32_t lanes = umma::taddr(0, 32 * (warp & 3), 0);
+  uint32_t phase = 0;
+  bool first = true;
+  auto to_mma = [&]() {
+    umma::fence_async_smem();
+    umma::fence_before();
+    __syncthreads();
+    umma::fence_after();
+  };
+  auto wait = [&]() {
+    umma::mbar_wait_parity(&S.bar, phase);
+    phase ^= 1u;
+    umma::fence_after();
+  };
+  auto aK = [](const __nv_bfloat16* b, int cols, int ks) { return umma::desc_kmajor(b + ks * 128, cols); };
+  auto mKc = [](const __nv_bfloat16* b, int cols, int ks, int c0) {
+    return umma::desc_mnmajor(b + ks * 2 * (cols / 8) * 64 + (c0 / 8) * 64, cols);
+  };
+  const int64_t ntiles = (N + TR - 1) / TR;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row = tile * TR + r;
+    const bool valid = row < N;
+    float h0[16];  // h, units 16q..16q+15
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(hp + row * HI + 16 * q + j))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      h0[j] = t.x;
+      h0[j + 1] = t.y;
+      h0[j + 2] = t.z;
+      h0[j + 3] = t.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 16; j += 8)
+      *reinterpret_cast<uint4*>(&S.B[blk_off(r, 16 + 16 * q + j, BC)]) =
+          make_uint4(pk(h0[j], h0[j + 1]), pk(h0[j + 2], h0[j + 3]), pk(h0[j + 4], h0[j + 5]), pk(h0[j + 6], h0[j + 7]));
+    if (q == 0) {
+      float xv[XI];
+#pragma unroll
+      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < n_in) ? __ldg(x + row * n_in + j) : 0.f;
+#pragma unroll
+      for (int j = 0; j < XI; j += 8)
+        *reinterpret_cast<uint4*>(&S.B[blk_off(r, j, BC)]) = make_uint4(
+            pk(xv[j], xv[j + 1]), pk(xv[j + 2], xv[j + 3]), pk(xv[j + 4], xv[j + 5]), pk(xv[j + 6], xv[j + 7]));
+    } else if (q == 1) {
+      const uint32_t one = pk(valid ? 1.f : 0.f, 0.f), zero = pk(0.f, 0.f);
+      *reinterpret_cast<uint4*>(&S.B[blk_off(r, 80, BC)]) = make_uint4(one, zero, zero, zero);
+      *reinterpret_cast<uint4*>(&S.B[blk_off(r, 88, BC)]) = make_uint4(zero, zero, zero, zero);
+    }
+    to_mma();
+    if (tid == 0) {  // recompute the gate pre-activations
+      const uint32_t id128 = umma::idesc_bf16(128, 128, false, true), id64 = umma::idesc_bf16(128, 64, false, true);
+      umma::mma_bf16(TRZ, aK(S.B, BC, 0), mKc(S.WI, G3, 0, 0), id128, false);
+#pragma unroll
+      for (int ks = 0; ks < HI / 16; ++ks) umma::mma_bf16(TRZ, aK(S.B, BC, 1 + ks), mKc(S.WG, G3, ks, 0), id128, true);
+      umma::mma_bf16(TGN, aK(S.B, BC, 0), mKc(S.WI, G3, 0, 2 * HI), id64, false);
+#pragma unroll
+      for (int ks = 0; ks < HI / 16; ++ks)
+        umma::mma_bf16(THN, aK(S.B, BC, 1 + ks), mKc(S.WG, G3, ks, 2 * HI), id64, ks > 0);
+      umma::commit(&S.bar);
+    }
+    wait();
+    float dd[16];  // g z: the direct part of dL/dh
+    {
+      float gr[16], gz[16], gn[16], hn[16], g[16];
+      umma::tmem_ld16(TRZ + lanes + 16 * q, gr);
+      umma::tmem_ld16(TRZ + lanes + HI + 16 * q, gz);
+      umma::tmem_ld16(TGN + lanes + 16 * q, gn);
+      umma::tmem_ld16(THN + lanes + 16 * q, hn);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+        if (valid) {
+          a = __ldg(reinterpret_cast<const float4*>(dha + row * HI + 16 * q + j));
+          if (dhb) b = __ldg(reinterpret_cast<const float4*>(dhb + row * HI + 16 * q + j));
+        }
+        g[j] = a.x + b.x;
+        g[j + 1] = a.y + b.y;
+        g[j + 2] = a.z + b.z;
+        g[j + 3] = a.w + b.w;
+      }
+      uint32_t wr[8], wz[8], wn[8], wnr[8];
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        float ar[2], az[2], an[2], anr[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int u = 16 * q + j + e;
+          const float rr = sigm_f(gr[j + e] + S.bg[u]), zz = sigm_f(gz[j + e] + S.bg[HI + u]);
+          const float hb = hn[j + e] + S.bg[3 * HI + u];
+          const float nn = tanh_f(gn[j + e] + S.bg[2 * HI + u] + rr * hb);
+          const float gg = g[j + e];
+          dd[j + e] = gg * zz;
+          const float dan = gg * (1.f - zz) * (1.f - nn * nn);
+          ar[e] = dan * hb * rr * (1.f - rr);
+          az[e] = gg * (h0[j + e] - nn) * zz * (1.f - zz);
+          an[e] = dan;
+          anr[e] = dan * rr;
+        }
+        wr[j / 2] = pk(ar[0], ar[1]);
+        wz[j / 2] = pk(az[0], az[1]);
+        wn[j / 2] = pk(an[0], an[1]);
+        wnr[j / 2] = pk(anr[0], anr[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        *reinterpret_cast<uint4*>(&S.GRZ[blk_off(r, 16 * q + 8 * j, HW)]) =
+            make_uint4(wr[4 * j], wr[4 * j + 1], wr[4 * j + 2], wr[4 * j + 3]);
+        *reinterpret_cast<uint4*>(&S.GRZ[blk_off(r, HI + 16 * q + 8 * j, HW)]) =
+            make_uint4(wz[4 * j], wz[4 * j + 1], wz[4 * j + 2], wz[4 * j + 3]);
+        *reinterpret_cast<uint4*>(&S.GN[blk_off(r, 16 * q + 8 * j, HW)]) =
+            make_uint4(wn[4 * j], wn[4 * j + 1], wn[4 * j + 2], wn[4 * j + 3]);
+        *reinterpret_cast<uint4*>(&S.GN[blk_off(r, HI + 16 * q + 8 * j, HW)]) =
+            make_uint4(wnr[4 * j], wnr[4 * j + 1], wnr[4 * j + 2], wnr[4 * j + 3]);
+      }
+    }
+    to_mma();
+    if (tid == 0) {
+      const uint32_t id16 = umma::idesc_bf16(128, 16, false, false), id64 = umma::idesc_bf16(128, 64, false, false);
+      const uint32_t idw = umma::idesc_bf16(128, BC, true, true);
+      // dx = [dar | daz | dan] Wi^T; dh = [dar | daz | dan r] Wh^T
+#pragma unroll
+      for (int ks = 0; ks < HW / 16; ++ks) {
+        umma::mma_bf16(TDX, aK(S.GRZ, HW, ks), aK(S.WI, G3, ks), id16, ks > 0);
+        umma::mma_bf16(TDH, aK(S.GRZ, HW, ks), aK(S.WG, G3, ks), id64, ks > 0);
+      }
+#pragma unroll
+      for (int ks = 0; ks < HI / 16; ++ks) {
+        umma::mma_bf16(TDX, aK(S.GN, HW, ks), aK(S.WI, G3, 8 + ks), id16, true);
+        umma::mma_bf16(TDH, aK(S.GN, HW, 4 + ks), aK(S.WG, G3, 8 + ks), id64, true);
+      }
+      // weight gradients: (gate units) x [x | h | 1], summed over the tile rows
+#pragma unroll
+      for (int ks = 0; ks < TR / 16; ++ks) {
+        umma::mma_bf16(TWR, mKc(S.GRZ, HW, ks, 0), mKc(S.B, BC, ks, 0), idw, !first || ks > 0);
+        umma::mma_bf16(TWN, mKc(S.GN, HW, ks, 0), mKc(S.B, BC, ks, 0), idw, !first || ks > 0);
+      }
+      umma::commit(&S.bar);
+    }
+    wait();
+    first = false;
+    {
+      float v[16];
+      umma::tmem_ld16(TDH + lanes + 16 * q, v);
+      if (valid) {
+        float4* dst = reinterpret_cast<float4*>(dhp + row * HI + 16 * q);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          dst[j] = make_float4(v[4 * j] + dd[4 * j], v[4 * j + 1] + dd[4 * j + 1], v[4 * j + 2] + dd[4 * j + 2],
+                               v[4 * j + 3] + dd[4 * j + 3]);
+      }
+      if (q == 0) {
+        umma::tmem_ld16(TDX + lanes, v);
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < XI; ++j)
+            if (j < n_in) dx[row * n_in + j] = v[j];
+        }
+      }
+    }
+    umma::fence_before();
+    __syncthreads();  // the next tile overwrites B, GRZ, GN and the gate columns
+    umma::fence_after();
+  }
+  {  // this CTA's partials -> work (TMEM lane = gate unit; columns [x 0-15 | h 16-79 | 1 80])
+    float* wk = work + (int64_t)blockIdx.x * GK_P;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int chunk = q + 4 * c;  // 16-column chunks 0..5 of each 96-column accumulator
+      if (chunk >= 6) continue;
+      float a[16], b[16];
+      if (!first) {
+        umma::tmem_ld16(TWR + lanes + 16 * chunk, a);
+        umma::tmem_ld16(TWN + lanes + 16 * chunk, b);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a[j] = b[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = 16 * chunk + j;
+        if (col < XI) {
+          if (col < n_in) {
+            wk[GK_WI + col * G3 + r] = a[j];
+            if (r < HI) wk[GK_WI + col * G3 + 2 * HI + r] = b[j];
+          }
+        } else if (col < XI + HI) {
+          wk[GK_WG + (col - XI) * G3 + r] = a[j];
+          if (r >= HI) wk[GK_WG + (col - XI) * G3 + HI + r] = b[j];
+        } else if (col == XI + HI) {
+          wk[GK_BI + r] = a[j];
+          wk[GK_BG + r] = a[j];
+          if (r < HI)
+            wk[GK_BI + 2 * HI + r] = b[j];
+          else
+            wk[GK_BG + HI + r] = b[j];
+        }
       }
     }
   }
   umma::fence_before();
   __syncthreads();
   if (warp == 0) umma::tmem_free(T0, 512);
-  if (BWD && tid < n_out) atomicAdd(&gbh[tid], S.dbh[tid]);
 }
 
-template <bool BWD>
-int launch_trunk(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
+template <bool BWD, bool GRU = false>
+int launch_trunk(int64_t n, int32_t n_out, GruArgs ga, const float* h, const float* dy, const float* W0, const float* b0,
                  const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                  const float* bh, float* y, float* dh, float* gW0, float* gb0, float* gW1, float* gb1,
-                 float* gW2, float* gb2, float* gWh, float* gbh, int32_t n_sm, void* stream) {
+                 float* gW2, float* gb2, float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm,
+                 void* stream) {
   if (n <= 0) return QS_OK;
   if (n_out < 1 || n_out > 8 || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
+  if (BWD && (!work || work_floats < (int64_t)n_sm * TK_P)) return QS_ERR_BAD_ARGUMENT;
   const size_t smem = sizeof(PolSmem);
   static_assert(sizeof(PolSmem) <= 227 * 1024, "shared memory");
-  if (cudaFuncSetAttribute(k_policy_trunk<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(k_policy_trunk<BWD, GRU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_policy_trunk<BWD><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
-                                                                dh, gW0, gb0, gW1, gb1, gW2, gb2, gWh, gbh);
-  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+  k_policy_trunk<BWD, GRU><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, ga, h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
+                                                                     dh, work);
+  if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
+  if (!BWD) return QS_OK;
+  red::Segs sg{{gW0, gb0, gW1, gb1, gW2, gb2, gWh, gbh},
+               {TK_W0, TK_B0, TK_W1, TK_B1, TK_W2, TK_B2, TK_WH, TK_BH},
+               {HI * HW, HW, HW * HW, HW, HW * HW, HW, (int64_t)HW * n_out, n_out},
+               8};
+  return red::sum_partials(work, grid, TK_P, sg, (cudaStream_t)stream);
 }
 
 }  // namespace
 
 extern "C" {
 
+int64_t qs_policy_work_floats(int32_t which, int32_t n_sm) {
+  if (n_sm < 1) return -1;
+  return which == 0 ? (int64_t)n_sm * TK_P : which == 1 ? (int64_t)n_sm * GK_P : -1;
+}
+
 int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W0, const float* b0, const float* W1,
                         const float* b1, const float* W2, const float* b2, const float* Wh, const float* bh, float* y,
                         int32_t n_sm, void* stream) {
-  if (!y) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<false>(n, n_out, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr, nullptr,
-                             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, n_sm, stream);
+  if (!y || !h) return QS_ERR_BAD_ARGUMENT;
+  return launch_trunk<false>(n, n_out, GruArgs{}, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
+                             nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, n_sm, stream);
 }
 
 int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
                         const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
-                        float* gWh, float* gbh, int32_t n_sm, void* stream) {
-  if (!dy || !dh) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<true>(n, n_out, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0, gW1, gb1,
-                            gW2, gb2, gWh, gbh, n_sm, stream);
+                        float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream) {
+  if (!h || !dy || !dh) return QS_ERR_BAD_ARGUMENT;
+  return launch_trunk<true>(n, n_out, GruArgs{}, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
+                            gW1, gb1, gW2, gb2, gWh, gbh, work, work_floats, n_sm, stream);
+}
+
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, const float* h, const float* Wi,
+                      const float* bi, const float* Wh_g, const float* bh_g, const float* W0, const float* b0,
+                      const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
+                      const float* bh, float* h_out, float* y, int32_t n_sm, void* stream) {
+  if (!y || !h_out || !x || !h || n_in < 1 || n_in > XI) return QS_ERR_BAD_ARGUMENT;
+  const GruArgs ga{n_in, x, h, Wi, bi, Wh_g, bh_g, h_out};
+  return launch_trunk<false, true>(n, n_out, ga, nullptr, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr,
+                                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+                                   n_sm, stream);
+}
+
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const float* dh_out_a,
+                      const float* dh_out_b, const float* Wi, const float* bi, const float* Wh_g, const float* bh_g,
+                      float* dx, float* dh, float* gWi, float* gbi, float* gWh_g, float* gbh_g, float* work,
+                      int64_t work_floats, int32_t n_sm, void* stream) {
+  if (n <= 0) return QS_OK;
+  if (!x || !h || !dh_out_a || !dx || !dh || n_in < 1 || n_in > XI || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
+  if (!work || work_floats < (int64_t)n_sm * GK_P) return QS_ERR_BAD_ARGUMENT;
+  const size_t smem = sizeof(GruSmem);
+  if (cudaFuncSetAttribute(k_gru_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return QS_ERR_LAUNCH;
+  const int64_t ntiles = (n + TR - 1) / TR;
+  const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
+  k_gru_bwd<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_in, x, h, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
+                                                      work);
+  if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
+  red::Segs sg{{gWi, gbi, gWh_g, gbh_g}, {GK_WI, GK_BI, GK_WG, GK_BG}, {(int64_t)n_in * G3, G3, HI * G3, G3}, 4};
+  return red::sum_partials(work, grid, GK_P, sg, (cudaStream_t)stream);
 }
 
 }  // extern "C"

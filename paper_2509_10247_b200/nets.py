@@ -180,10 +180,17 @@ class ConvEncoder(torch.nn.Module):
         return torch.tanh(self.out(feat))
 
 
-# the trunk + heads of the reference policy shape on the tcgen05 kernels
-# (qs_policy_trunk_fwd/_bwd) under bf16 autocast; QS_POLICY_TRUNK=torch keeps
-# torch's GEMMs
+# the GRU cell, trunk and heads of the reference policy shape on the tcgen05
+# kernels (qs_policy_gru_fwd/_bwd, qs_policy_trunk_fwd/_bwd) under bf16
+# autocast; QS_POLICY_TRUNK=torch keeps torch's GEMMs
 FUSED_TRUNK = os.environ.get("QS_POLICY_TRUNK", "tc") != "torch"
+
+
+def _work(which, n_sm, dev):
+    """Scratch for a policy gradient kernel's per-CTA partials (0 trunk, 1 GRU)."""
+    from paper_2509_10247_b200 import _lib as L
+
+    return torch.empty(L.lib().qs_policy_work_floats(which, n_sm), dtype=torch.float32, device=dev)
 
 
 class _TrunkFn(torch.autograd.Function):
@@ -217,11 +224,63 @@ class _TrunkFn(torch.autograd.Function):
         dh = torch.empty_like(h)
         grads = [torch.zeros_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
         gbh = torch.zeros(n_out, dtype=torch.float32, device=h.device)
+        work = _work(0, ctx.n_sm, h.device)
         L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h), L.ptr(gy), *[L.ptr(t) for t in
                                                                               (W0, b0, W1, b1, W2, b2, Wh)],
-                                            L.ptr(dh), *[L.ptr(t) for t in grads], L.ptr(gbh), ctx.n_sm,
+                                            L.ptr(dh), *[L.ptr(t) for t in grads], L.ptr(gbh), L.ptr(work),
+                                            work.numel(), ctx.n_sm,
                                             L.stream_handle(h.device)), "qs_policy_trunk_bwd")
         return (dh, *grads, gbh)
+
+
+class _PolicyStepFn(torch.autograd.Function):
+    """(h', y) = (GRU(x, h), trunk + heads of h') (q/nets.py:107-132, 241-256)
+    in one tcgen05 kernel (qs_policy_gru_fwd); the backward is the trunk's
+    (qs_policy_trunk_bwd, dL/dy -> dL/dh') then the GRU cell's
+    (qs_policy_gru_bwd, dL/dh' from the trunk plus the carried one)."""
+
+    @staticmethod
+    def forward(ctx, x, h, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh):
+        from paper_2509_10247_b200 import _lib as L
+
+        ctx.set_materialize_grads(False)
+        x, h = x.contiguous(), h.contiguous()
+        ws = [t.detach().float().contiguous() for t in (Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh)]
+        N, n_in, n_out = x.shape[0], x.shape[1], ws[10].shape[1]
+        h_out = torch.empty(N, h.shape[1], dtype=torch.float32, device=x.device)
+        y = torch.empty(N, n_out, dtype=torch.float32, device=x.device)
+        n_sm = torch.cuda.get_device_properties(x.device).multi_processor_count
+        L.check(L.lib().qs_policy_gru_fwd(N, n_in, n_out, L.ptr(x), L.ptr(h), *[L.ptr(t) for t in ws], L.ptr(h_out),
+                                          L.ptr(y), n_sm, L.stream_handle(x.device)), "qs_policy_gru_fwd")
+        ctx.save_for_backward(x, h, h_out, *ws[:11])
+        ctx.n_sm = n_sm
+        return h_out, y
+
+    @staticmethod
+    def backward(ctx, g_h, g_y):
+        from paper_2509_10247_b200 import _lib as L
+
+        x, h, h_out, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh = ctx.saved_tensors
+        N, n_out = x.shape[0], Wh.shape[1]
+        dev, st = x.device, L.stream_handle(x.device)
+        g_y = torch.zeros(N, n_out, device=dev) if g_y is None else g_y.contiguous().float()
+        g_h = None if g_h is None else g_h.contiguous().float()
+        dh_t = torch.empty_like(h_out)
+        tg = [torch.zeros_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
+        gbh = torch.zeros(n_out, dtype=torch.float32, device=dev)
+        work = _work(0, ctx.n_sm, dev)
+        L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h_out), L.ptr(g_y),
+                                            *[L.ptr(t) for t in (W0, b0, W1, b1, W2, b2, Wh)], L.ptr(dh_t),
+                                            *[L.ptr(t) for t in tg], L.ptr(gbh), L.ptr(work), work.numel(), ctx.n_sm,
+                                            st), "qs_policy_trunk_bwd")
+        dx, dh = torch.empty_like(x), torch.empty_like(h)
+        gg = [torch.zeros_like(t) for t in (Wi, bi, Wg, bg)]
+        work = _work(1, ctx.n_sm, dev)
+        L.check(L.lib().qs_policy_gru_bwd(N, x.shape[1], L.ptr(x), L.ptr(h), L.ptr(dh_t), L.ptr(g_h),
+                                          *[L.ptr(t) for t in (Wi, bi, Wg, bg)], L.ptr(dx), L.ptr(dh),
+                                          *[L.ptr(t) for t in gg], L.ptr(work), work.numel(), ctx.n_sm, st),
+                "qs_policy_gru_bwd")
+        return (dx, dh, *gg, *tg, gbh)
 
 
 @dataclass
@@ -278,16 +337,26 @@ class PolicyNet(torch.nn.Module):
             img = visual.to(x.dtype) * (1.0 / float(self.arch.visual.get("max_range", 1.0)))
             f = self.enc(img) if self.arch.visual["kind"] == "depth" else torch.tanh(self.enc(img))
             x = torch.cat([x, f.to(x.dtype)], -1)
+        A = self.arch.action_dim
+        layers = self.trunk.layers
+        trunk_ok = (FUSED_TRUNK and x.is_cuda and x.dim() == 2 and x.dtype == torch.float32 and
+                    torch.is_autocast_enabled() and len(layers) == 3 and
+                    tuple(l.W.shape for l in layers) == ((64, 128), (128, 128), (128, 128)) and 2 * A <= 8)
+        if trunk_ok and self.gru is not None and self.hidden == 64 and x.shape[1] <= 16:
+            # bf16 policy mode: GRU cell, trunk and both heads in one tcgen05 kernel
+            if h is None:
+                h = torch.zeros(x.shape[0], self.hidden, device=x.device)
+            g = self.gru
+            h, y = _PolicyStepFn.apply(x, h.float(), g.Wi, g.bi, g.Wh, g.bh, layers[0].W, layers[0].b, layers[1].W,
+                                       layers[1].b, layers[2].W, layers[2].b, torch.cat([self.mu.W, self.sig.W], 1),
+                                       torch.cat([self.mu.b, self.sig.b]))
+            return y[:, :A], torch.clamp(y[:, A:2 * A], LOG_SIGMA_MIN, self.arch.log_sigma_max), h
         if self.gru is not None:
             if h is None:
                 h = torch.zeros(x.shape[0], self.hidden, device=x.device, dtype=x.dtype)
             h = self.gru(x, h.to(x.dtype)).float() if x.dtype != torch.float64 else self.gru(x, h)
             x = h.to(x.dtype)
-        A = self.arch.action_dim
-        layers = self.trunk.layers
-        if (FUSED_TRUNK and x.is_cuda and x.dim() == 2 and x.dtype == torch.float32 and torch.is_autocast_enabled()
-                and x.shape[1] == 64 and len(layers) == 3 and tuple(l.W.shape for l in layers) ==
-                ((64, 128), (128, 128), (128, 128)) and 2 * A <= 8):
+        if trunk_ok and x.shape[1] == 64:
             # bf16 policy mode: trunk and both heads in two tcgen05 kernels
             y = _TrunkFn.apply(x, layers[0].W, layers[0].b, layers[1].W, layers[1].b, layers[2].W, layers[2].b,
                                torch.cat([self.mu.W, self.sig.W], 1), torch.cat([self.mu.b, self.sig.b]))
@@ -361,11 +430,16 @@ def value_fit_grad(value: "ValueNet", x: torch.Tensor, y: torch.Tensor) -> torch
     # tcgen05 kernel (TMEM accumulators) for <= 14 inputs -- the privileged
     # state's 14; the mma.sync kernel otherwise (QS_CRITIC_KERNEL=mma forces it)
     tc = K <= 14 and os.environ.get("QS_CRITIC_KERNEL", "tc") != "mma"
-    fn = L.lib().qs_mlp3_fit_grad_tc if tc else L.lib().qs_mlp3_fit_grad
-    L.check(fn(M, K, L.ptr(x), L.ptr(scale), L.ptr(y), L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]), L.ptr(w[3]),
-               L.ptr(w[4]), L.ptr(w[5]), L.ptr(grads[0]), L.ptr(grads[1]), L.ptr(grads[2]), L.ptr(grads[3]),
-               L.ptr(grads[4]), L.ptr(grads[5]), L.ptr(loss), n_sm, L.stream_handle(dev)),
-            "qs_mlp3_fit_grad_tc" if tc else "qs_mlp3_fit_grad")
+    args = [M, K, L.ptr(x), L.ptr(scale), L.ptr(y), L.ptr(w[0]), L.ptr(w[1]), L.ptr(w[2]), L.ptr(w[3]),
+            L.ptr(w[4]), L.ptr(w[5]), L.ptr(grads[0]), L.ptr(grads[1]), L.ptr(grads[2]), L.ptr(grads[3]),
+            L.ptr(grads[4]), L.ptr(grads[5]), L.ptr(loss)]
+    if tc:  # per-CTA partials summed in a fixed order: reproducible gradients
+        n_work = L.lib().qs_mlp3_work_floats(n_sm)
+        work = torch.empty(n_work, dtype=torch.float32, device=dev)
+        L.check(L.lib().qs_mlp3_fit_grad_tc(*args, L.ptr(work), n_work, n_sm, L.stream_handle(dev)),
+                "qs_mlp3_fit_grad_tc")
+    else:
+        L.check(L.lib().qs_mlp3_fit_grad(*args, n_sm, L.stream_handle(dev)), "qs_mlp3_fit_grad")
     for p, gr in zip(params, grads):
         p.grad = gr
     return loss[0]

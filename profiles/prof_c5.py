@@ -1,19 +1,36 @@
-import sys, time, torch
-sys.path.insert(0, '/root/repo')
-import paper_2509_10247_b200 as qs
-from paper_2509_10247_b200.train import LearnerOptions, ShortHorizonTrainer
-dev = torch.device('cuda', 0)
-cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=131072, episode_len=128)
-env = qs.make_task(cfg, device=dev, strict=False)
+"""Per-kernel device time of one C5 SHAC update (131,072 envs, horizon 16),
+eager (no CUDA graph) under torch.profiler: which kernels the update spends
+its time in.  Run on the GPU box; prints a table sorted by device time."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2509_10247_b200 as qs  # noqa: E402
+from paper_2509_10247_b200.train import LearnerOptions, ShortHorizonTrainer  # noqa: E402
+
+N = 131072
+cfg = qs.TaskConfig(task="position", dynamics="pm_continuous", n_envs=N, episode_len=128)
+env = qs.make_task(cfg, device="cuda", strict=False)
 env.reset(seed=1)
-tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0))
-for _ in range(3): tr.update()
+tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0, cuda_graph=False))
+for _ in range(4):
+    tr.update()
 torch.cuda.synchronize()
-t0=time.perf_counter()
-for _ in range(3): tr.update()
-torch.cuda.synchronize(); print('per update ms', (time.perf_counter()-t0)/3*1e3)
-# split timing
-import torch.profiler as P
-with P.profile(activities=[P.ProfilerActivity.CPU, P.ProfilerActivity.CUDA]) as prof:
-    tr.update(); torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
+n = 3
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+    for _ in range(n):
+        tr.update()
+    torch.cuda.synchronize()
+tot = 0.0
+rows = {}
+for e in prof.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        k = e.name[:90]
+        t, c = rows.get(k, (0.0, 0))
+        rows[k] = (t + e.device_time / n, c + 1)
+        tot += e.device_time / n
+print(f"total device us per update: {tot:.1f}")
+for k, (t, c) in sorted(rows.items(), key=lambda kv: -kv[1][0])[:40]:
+    print(f"{t:9.1f} us {100 * t / tot:5.1f}%  x{c // n:4d}  {k}")

@@ -11,7 +11,7 @@ HEADER = os.path.join(ROOT, "include", "quadsim_b200.h")
 
 def declared_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^int\s+(qs_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t)\s+(qs_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_boundary():

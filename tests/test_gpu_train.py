@@ -150,6 +150,9 @@ def test_fused_critic_gradient_matches_autograd(M, kernel, monkeypatch):
     y = torch.randn(M, device="cuda") * 0.5
     loss_k = nets.value_fit_grad(val, X, y)
     gk = [p.grad.clone() for p in val.parameters()]
+    if kernel == "tc":  # per-CTA partials summed in CTA order: the same bits every call
+        loss_2 = nets.value_fit_grad(val, X, y)
+        assert torch.equal(loss_2, loss_k) and all(torch.equal(a, p.grad) for a, p in zip(gk, val.parameters()))
     for p in val.parameters():
         p.grad = None
     loss_t = ((val(X) - y) ** 2).mean()
@@ -228,8 +231,13 @@ def test_cuda_graph_updates_match_eager():
     for a, b in zip(*hist):
         assert abs(a["loss"] - b["loss"]) <= 1e-3 * max(1.0, abs(a["loss"])), (a, b)
         assert abs(a["critic_loss"] - b["critic_loss"]) <= 1e-2 * max(1.0, abs(a["critic_loss"])), (a, b)
+    # Adam normalises each element's gradient: where a weight's gradient is at
+    # round-off level (an input feature that is ~0), the capturable (graph)
+    # and foreach (eager) Adam arithmetic move it by different fractions of
+    # the learning rate -- bounded by lr per update, well below a stale carry
+    lr = trs[0].opts.actor_lr
     for pa, pb in zip(trs[0].policy.parameters(), trs[1].policy.parameters()):
-        torch.testing.assert_close(pa, pb, rtol=1e-3, atol=1e-4)
+        torch.testing.assert_close(pa, pb, rtol=1e-3, atol=0.25 * lr)
     # the carried env state: the two trainers' fp32 round-off (capturable Adam,
     # bf16 GEMMs) moves a few rows slightly after 56 closed-loop steps
     d = (trs[0].env._S - trs[1].env._S).detach().abs()
