@@ -797,7 +797,8 @@ int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale
   red::Segs sg{{gW1, gW0, gb0, gb1, gw2, gb2, loss},
                {CK_W1, CK_W0, CK_B0, CK_B1, CK_W2, CK_B2, CK_L},
                {HID * HID, (int64_t)k * HID, HID, HID, HID, 1, 1},
-               7};
+               7,
+               true};
   return red::sum_partials(work, grid, CK_P, sg, (cudaStream_t)stream);
 }
 

@@ -109,6 +109,7 @@ static_assert(XI * G3 + HI * G3 <= TR * HW && TR * XI + TR * HI <= TR * HW, "GRU
 struct GruArgs {  // the forward's GRU cell (GRU = true)
   int n_in;
   const float *x, *hp, *Wi, *bi, *Wg, *bg;
+  const uint8_t* reset;  // rows whose carried h restarts at 0 (episode reset), or null
   float* h_out;
 };
 
@@ -227,9 +228,10 @@ __global__ void __launch_bounds__(PT, 1)
       // ---- the GRU cell: gates from x and the carried h; TMEM [128,256)
       // r|z pre-activations (x Wi + h Wh summed), [256,320) x Wi_n, [320,384) h Wh_n
       float hp[16];
+      const bool live = valid && !(ga.reset && ga.reset[row]);
 #pragma unroll
       for (int j = 0; j < 16; j += 4) {
-        const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(ga.hp + row * HI + 16 * q + j))
+        const float4 t = live ? __ldg(reinterpret_cast<const float4*>(ga.hp + row * HI + 16 * q + j))
                                : make_float4(0.f, 0.f, 0.f, 0.f);
         hp[j] = t.x;
         hp[j + 1] = t.y;
@@ -519,7 +521,7 @@ struct GruSmem {
 
 __global__ void __launch_bounds__(PT, 1)
     k_gru_bwd(int64_t N, int n_in, const float* __restrict__ x, const float* __restrict__ hp,
-              const float* __restrict__ dha, const float* __restrict__ dhb, const float* __restrict__ Wi,
+              const uint8_t* __restrict__ rst, const float* __restrict__ dha, const float* __restrict__ dhb, const float* __restrict__ Wi,
               const float* __restrict__ bi, const float* __restrict__ Wg, const float* __restrict__ bgv,
               float* __restrict__ dx, float* __restrict__ dhp, float* __restrict__ work) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -569,10 +571,11 @@ __global__ void __launch_bounds__(PT, 1)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = tile * TR + r;
     const bool valid = row < N;
-    float h0[16];  // h, units 16q..16q+15
+    float h0[16];  // h, units 16q..16q+15 (0 on a reset row)
+    const bool live = valid && !(rst && rst[row]);
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
-      const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(hp + row * HI + 16 * q + j))
+      const float4 t = live ? __ldg(reinterpret_cast<const float4*>(hp + row * HI + 16 * q + j))
                              : make_float4(0.f, 0.f, 0.f, 0.f);
       h0[j] = t.x;
       h0[j + 1] = t.y;
@@ -691,12 +694,13 @@ __global__ void __launch_bounds__(PT, 1)
     {
       float v[16];
       umma::tmem_ld16(TDH + lanes + 16 * q, v);
-      if (valid) {
+      if (valid) {  // a reset row's carried h was replaced by 0: no gradient reaches it
         float4* dst = reinterpret_cast<float4*>(dhp + row * HI + 16 * q);
+        const float m = live ? 1.f : 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          dst[j] = make_float4(v[4 * j] + dd[4 * j], v[4 * j + 1] + dd[4 * j + 1], v[4 * j + 2] + dd[4 * j + 2],
-                               v[4 * j + 3] + dd[4 * j + 3]);
+          dst[j] = make_float4(m * (v[4 * j] + dd[4 * j]), m * (v[4 * j + 1] + dd[4 * j + 1]),
+                               m * (v[4 * j + 2] + dd[4 * j + 2]), m * (v[4 * j + 3] + dd[4 * j + 3]));
       }
       if (q == 0) {
         umma::tmem_ld16(TDX + lanes, v);
@@ -775,7 +779,8 @@ int launch_trunk(int64_t n, int32_t n_out, GruArgs ga, const float* h, const flo
   red::Segs sg{{gW0, gb0, gW1, gb1, gW2, gb2, gWh, gbh},
                {TK_W0, TK_B0, TK_W1, TK_B1, TK_W2, TK_B2, TK_WH, TK_BH},
                {HI * HW, HW, HW * HW, HW, HW * HW, HW, (int64_t)HW * n_out, n_out},
-               8};
+               8,
+               false};
   return red::sum_partials(work, grid, TK_P, sg, (cudaStream_t)stream);
 }
 
@@ -805,18 +810,19 @@ int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* d
                             gW1, gb1, gW2, gb2, gWh, gbh, work, work_floats, n_sm, stream);
 }
 
-int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, const float* h, const float* Wi,
-                      const float* bi, const float* Wh_g, const float* bh_g, const float* W0, const float* b0,
-                      const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
-                      const float* bh, float* h_out, float* y, int32_t n_sm, void* stream) {
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, const float* h, const uint8_t* h_reset,
+                      const float* Wi, const float* bi, const float* Wh_g, const float* bh_g, const float* W0,
+                      const float* b0, const float* W1, const float* b1, const float* W2, const float* b2,
+                      const float* Wh, const float* bh, float* h_out, float* y, int32_t n_sm, void* stream) {
   if (!y || !h_out || !x || !h || n_in < 1 || n_in > XI) return QS_ERR_BAD_ARGUMENT;
-  const GruArgs ga{n_in, x, h, Wi, bi, Wh_g, bh_g, h_out};
+  const GruArgs ga{n_in, x, h, Wi, bi, Wh_g, bh_g, h_reset, h_out};
   return launch_trunk<false, true>(n, n_out, ga, nullptr, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr,
                                    nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
                                    n_sm, stream);
 }
 
-int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const float* dh_out_a,
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const uint8_t* h_reset,
+                      const float* dh_out_a,
                       const float* dh_out_b, const float* Wi, const float* bi, const float* Wh_g, const float* bh_g,
                       float* dx, float* dh, float* gWi, float* gbi, float* gWh_g, float* gbh_g, float* work,
                       int64_t work_floats, int32_t n_sm, void* stream) {
@@ -828,10 +834,10 @@ int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, c
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_gru_bwd<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_in, x, h, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
+  k_gru_bwd<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_in, x, h, h_reset, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
                                                       work);
   if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
-  red::Segs sg{{gWi, gbi, gWh_g, gbh_g}, {GK_WI, GK_BI, GK_WG, GK_BG}, {(int64_t)n_in * G3, G3, HI * G3, G3}, 4};
+  red::Segs sg{{gWi, gbi, gWh_g, gbh_g}, {GK_WI, GK_BI, GK_WG, GK_BG}, {(int64_t)n_in * G3, G3, HI * G3, G3}, 4, false};
   return red::sum_partials(work, grid, GK_P, sg, (cudaStream_t)stream);
 }
 

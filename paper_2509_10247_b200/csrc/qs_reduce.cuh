@@ -10,11 +10,12 @@
 namespace red {
 
 constexpr int MAXSEG = 8;
-struct Segs {  // out[s][i] += sum_b work[b * P + off[s] + i], i < len[s]
+struct Segs {  // out[s][i] (+)= sum_b work[b * P + off[s] + i], i < len[s]
   float* out[MAXSEG];
   int64_t off[MAXSEG];
   int64_t len[MAXSEG];
   int n;
+  bool accumulate;  // add to out (else overwrite)
 };
 
 static __global__ void k_sum_partials(const float* __restrict__ work, int nblk, int64_t P, Segs s) {
@@ -32,12 +33,14 @@ static __global__ void k_sum_partials(const float* __restrict__ work, int nblk, 
     a3 += __ldg(p + (int64_t)(b + 3) * P);
   }
   for (; b < nblk; ++b) a0 += __ldg(p + (int64_t)b * P);
-  s.out[k][i] += (a0 + a1) + (a2 + a3);
+  const float sum = (a0 + a1) + (a2 + a3);
+  s.out[k][i] = s.accumulate ? s.out[k][i] + sum : sum;
 }
 
 // launch the sum over `nblk` partials of width P for the non-null segments
 static int sum_partials(const float* work, int nblk, int64_t P, const Segs& segs, cudaStream_t st) {
   Segs s{};
+  s.accumulate = segs.accumulate;
   int64_t total = 0;
   for (int k = 0; k < segs.n; ++k) {
     if (!segs.out[k] || segs.len[k] <= 0) continue;

@@ -222,8 +222,8 @@ class _TrunkFn(torch.autograd.Function):
         gy = gy.contiguous().float()
         N, n_out = gy.shape
         dh = torch.empty_like(h)
-        grads = [torch.zeros_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
-        gbh = torch.zeros(n_out, dtype=torch.float32, device=h.device)
+        grads = [torch.empty_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
+        gbh = torch.empty(n_out, dtype=torch.float32, device=h.device)
         work = _work(0, ctx.n_sm, h.device)
         L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h), L.ptr(gy), *[L.ptr(t) for t in
                                                                               (W0, b0, W1, b1, W2, b2, Wh)],
@@ -234,53 +234,60 @@ class _TrunkFn(torch.autograd.Function):
 
 
 class _PolicyStepFn(torch.autograd.Function):
-    """(h', y) = (GRU(x, h), trunk + heads of h') (q/nets.py:107-132, 241-256)
-    in one tcgen05 kernel (qs_policy_gru_fwd); the backward is the trunk's
-    (qs_policy_trunk_bwd, dL/dy -> dL/dh') then the GRU cell's
-    (qs_policy_gru_bwd, dL/dh' from the trunk plus the carried one)."""
+    """(h', y) = (GRU(x, h masked by reset), trunk + heads of h')
+    (q/nets.py:107-132, 241-256) in one tcgen05 kernel (qs_policy_gru_fwd);
+    the backward is the trunk's (qs_policy_trunk_bwd, dL/dy -> dL/dh') then the
+    GRU cell's (qs_policy_gru_bwd, dL/dh' from the trunk plus the carried one).
+    The two heads enter as separate parameters (Wh = [W_mu | W_sigma] is
+    assembled here, outside autograd, and its gradient split back)."""
 
     @staticmethod
-    def forward(ctx, x, h, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh):
+    def forward(ctx, x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wmu, bmu, Wsig, bsig):
         from paper_2509_10247_b200 import _lib as L
 
         ctx.set_materialize_grads(False)
         x, h = x.contiguous(), h.contiguous()
-        ws = [t.detach().float().contiguous() for t in (Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh)]
-        N, n_in, n_out = x.shape[0], x.shape[1], ws[10].shape[1]
+        rs = reset.contiguous().view(torch.uint8) if reset is not None else None
+        ws = [t.detach().float().contiguous() for t in (Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2)]
+        Wh = torch.cat([Wmu.detach(), Wsig.detach()], 1).float().contiguous()
+        bh = torch.cat([bmu.detach(), bsig.detach()]).float().contiguous()
+        N, n_in, n_out = x.shape[0], x.shape[1], Wh.shape[1]
         h_out = torch.empty(N, h.shape[1], dtype=torch.float32, device=x.device)
         y = torch.empty(N, n_out, dtype=torch.float32, device=x.device)
         n_sm = torch.cuda.get_device_properties(x.device).multi_processor_count
-        L.check(L.lib().qs_policy_gru_fwd(N, n_in, n_out, L.ptr(x), L.ptr(h), *[L.ptr(t) for t in ws], L.ptr(h_out),
-                                          L.ptr(y), n_sm, L.stream_handle(x.device)), "qs_policy_gru_fwd")
-        ctx.save_for_backward(x, h, h_out, *ws[:11])
-        ctx.n_sm = n_sm
+        L.check(L.lib().qs_policy_gru_fwd(N, n_in, n_out, L.ptr(x), L.ptr(h), L.ptr(rs), *[L.ptr(t) for t in ws],
+                                          L.ptr(Wh), L.ptr(bh), L.ptr(h_out), L.ptr(y), n_sm,
+                                          L.stream_handle(x.device)), "qs_policy_gru_fwd")
+        ctx.save_for_backward(x, h, rs, h_out, *ws, Wh)
+        ctx.n_sm, ctx.A = n_sm, Wmu.shape[1]
         return h_out, y
 
     @staticmethod
     def backward(ctx, g_h, g_y):
         from paper_2509_10247_b200 import _lib as L
 
-        x, h, h_out, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh = ctx.saved_tensors
-        N, n_out = x.shape[0], Wh.shape[1]
+        x, h, rs, h_out, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh = ctx.saved_tensors
+        N, n_out, A = x.shape[0], Wh.shape[1], ctx.A
         dev, st = x.device, L.stream_handle(x.device)
         g_y = torch.zeros(N, n_out, device=dev) if g_y is None else g_y.contiguous().float()
         g_h = None if g_h is None else g_h.contiguous().float()
         dh_t = torch.empty_like(h_out)
-        tg = [torch.zeros_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
-        gbh = torch.zeros(n_out, dtype=torch.float32, device=dev)
+        tg = [torch.empty_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
+        gbh = torch.empty(n_out, dtype=torch.float32, device=dev)
         work = _work(0, ctx.n_sm, dev)
         L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h_out), L.ptr(g_y),
                                             *[L.ptr(t) for t in (W0, b0, W1, b1, W2, b2, Wh)], L.ptr(dh_t),
                                             *[L.ptr(t) for t in tg], L.ptr(gbh), L.ptr(work), work.numel(), ctx.n_sm,
                                             st), "qs_policy_trunk_bwd")
         dx, dh = torch.empty_like(x), torch.empty_like(h)
-        gg = [torch.zeros_like(t) for t in (Wi, bi, Wg, bg)]
+        gg = [torch.empty_like(t) for t in (Wi, bi, Wg, bg)]
         work = _work(1, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_gru_bwd(N, x.shape[1], L.ptr(x), L.ptr(h), L.ptr(dh_t), L.ptr(g_h),
+        L.check(L.lib().qs_policy_gru_bwd(N, x.shape[1], L.ptr(x), L.ptr(h), L.ptr(rs), L.ptr(dh_t), L.ptr(g_h),
                                           *[L.ptr(t) for t in (Wi, bi, Wg, bg)], L.ptr(dx), L.ptr(dh),
                                           *[L.ptr(t) for t in gg], L.ptr(work), work.numel(), ctx.n_sm, st),
                 "qs_policy_gru_bwd")
-        return (dx, dh, *gg, *tg, gbh)
+        gWh = tg.pop()
+        return (dx, dh, None, *gg, *tg, gWh[:, :A], gbh[:A], gWh[:, A:], gbh[A:])
 
 
 @dataclass
@@ -329,7 +336,10 @@ class PolicyNet(torch.nn.Module):
     def initial_hidden(self, batch, device=None):
         return torch.zeros(batch, self.hidden, device=device) if self.gru is not None else None
 
-    def forward(self, proprio, visual=None, h=None):
+    def forward(self, proprio, visual=None, h=None, h_reset=None):
+        """h_reset (bool (N,), optional): rows whose carried hidden state
+        restarts at zero before this step (the trainer's episode resets,
+        q/learners.py:215-217), folded into the fused kernel when it runs."""
         x = proprio * self.input_scale.to(proprio.dtype)
         if self.enc is not None:
             if visual is None:
@@ -347,13 +357,15 @@ class PolicyNet(torch.nn.Module):
             if h is None:
                 h = torch.zeros(x.shape[0], self.hidden, device=x.device)
             g = self.gru
-            h, y = _PolicyStepFn.apply(x, h.float(), g.Wi, g.bi, g.Wh, g.bh, layers[0].W, layers[0].b, layers[1].W,
-                                       layers[1].b, layers[2].W, layers[2].b, torch.cat([self.mu.W, self.sig.W], 1),
-                                       torch.cat([self.mu.b, self.sig.b]))
+            h, y = _PolicyStepFn.apply(x, h.float(), h_reset, g.Wi, g.bi, g.Wh, g.bh, layers[0].W, layers[0].b,
+                                       layers[1].W, layers[1].b, layers[2].W, layers[2].b, self.mu.W, self.mu.b,
+                                       self.sig.W, self.sig.b)
             return y[:, :A], torch.clamp(y[:, A:2 * A], LOG_SIGMA_MIN, self.arch.log_sigma_max), h
         if self.gru is not None:
             if h is None:
                 h = torch.zeros(x.shape[0], self.hidden, device=x.device, dtype=x.dtype)
+            elif h_reset is not None:
+                h = torch.where(h_reset[:, None], torch.zeros_like(h), h)
             h = self.gru(x, h.to(x.dtype)).float() if x.dtype != torch.float64 else self.gru(x, h)
             x = h.to(x.dtype)
         if trunk_ok and x.shape[1] == 64:

@@ -238,11 +238,16 @@ class ShortHorizonTrainer:
         self.policy, self.value = make_nets(env, opts, critic=opts.algo in ("shac", "sha2c", "ppo"))
         self.policy.to(dev)
         graph = opts.cuda_graph and dev.type == "cuda"
-        self.actor_opt = torch.optim.Adam(self.policy.parameters(), lr=opts.actor_lr, capturable=graph)
+        # fused Adam: one kernel per step for all parameters (device-side step
+        # counter, so it captures into the update's CUDA graph)
+        fused = dev.type == "cuda"
+        self.actor_opt = torch.optim.Adam(self.policy.parameters(), lr=opts.actor_lr, capturable=graph,
+                                          fused=fused)
         self.needs_critic = self.value is not None
         if self.needs_critic:
             self.value.to(dev)
-            self.critic_opt = torch.optim.Adam(self.value.parameters(), lr=opts.critic_lr, capturable=graph)
+            self.critic_opt = torch.optim.Adam(self.value.parameters(), lr=opts.critic_lr, capturable=graph,
+                                               fused=fused)
         self.hidden = self.policy.initial_hidden(env.N, dev)
         self.update_count = 0
         self._gen = torch.Generator(device=dev)
@@ -285,25 +290,25 @@ class ShortHorizonTrainer:
         h = self.hidden.detach() if self.hidden is not None else None
         disc = 0.0
         r_ctrl, r_goal, dones, priv = [], [], [], []
+        reset = None  # rows whose episode ended last step: their hidden state restarts at 0
         for t in range(T):
             if record_privileged:
                 priv.append(env.privileged_state())
             with self._nets():
-                mu, log_sigma, h = self.policy(obs.proprio, obs.visual, h)
+                mu, log_sigma, h = self.policy(obs.proprio, obs.visual, h, h_reset=reset)
             a = mu
             if opts.explore:
                 eps = torch.randn(mu.shape, generator=self._gen, device=mu.device)
                 a = mu + torch.exp(log_sigma) * eps
             out = env.step(a)
-            if h is not None:
-                h = torch.where(out.done[:, None], torch.zeros_like(h), h)
+            reset = out.done if h is not None else None
             disc = disc + out.r_ctrl.mean() * (opts.gamma ** t)
             r_ctrl.append(out.r_ctrl.detach())
             r_goal.append(out.r_goal)
             dones.append(out.done)
             obs = out.obs
         if h is not None:
-            self.hidden = h.detach()
+            self.hidden = torch.where(reset[:, None], torch.zeros_like(h), h).detach()
         return disc, torch.stack(r_ctrl), torch.stack(r_goal), torch.stack(dones), (
             torch.stack(priv) if record_privileged else None)
 

@@ -34,3 +34,11 @@ for e in prof.events():
 print(f"total device us per update: {tot:.1f}")
 for k, (t, c) in sorted(rows.items(), key=lambda kv: -kv[1][0])[:40]:
     print(f"{t:9.1f} us {100 * t / tot:5.1f}%  x{c // n:4d}  {k}")
+
+# the same, attributed to the torch operators that launched them
+with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CPU,
+                                        torch.profiler.ProfilerActivity.CUDA]) as prof2:
+    for _ in range(n):
+        tr.update()
+    torch.cuda.synchronize()
+print(prof2.key_averages().table(sort_by="self_cuda_time_total", row_limit=30, max_name_column_width=60))

@@ -31,7 +31,7 @@ def test_policy_trunk_fwd_bwd_match_autograd(n_out, N):
     L.check(L.lib().qs_policy_trunk_fwd(N, n_out, *_ptrs(h, W0, b0, W1, b1, W2, b2, Wh, bh, y), n_sm,
                                         L.stream_handle()), "fwd")
     params = [W0, b0, W1, b1, W2, b2, Wh, bh]
-    grads = [torch.zeros_like(p) for p in params]
+    grads = [torch.full_like(p, 7.0) for p in params]  # overwritten, not accumulated
     dh = torch.empty_like(h)
     work = torch.empty(L.lib().qs_policy_work_floats(0, n_sm), device="cuda")
     L.check(L.lib().qs_policy_trunk_bwd(N, n_out, *_ptrs(h, dy, W0, b0, W1, b1, W2, b2, Wh, dh, grads[0], grads[1],
@@ -66,6 +66,7 @@ def test_policynet_autocast_uses_trunk_kernels_and_matches_torch_path():
     pol = nets.PolicyNet(arch, np.random.default_rng(3)).cuda()
     x = torch.randn(3000, 10, device="cuda")
     h0 = torch.randn(3000, 64, device="cuda") * 0.5
+    reset = torch.rand(3000, device="cuda") < 0.2
 
     def run(fused):
         old = nets.FUSED_TRUNK
@@ -73,7 +74,7 @@ def test_policynet_autocast_uses_trunk_kernels_and_matches_torch_path():
         try:
             pol.zero_grad(set_to_none=True)
             with torch.autocast("cuda", dtype=torch.bfloat16):
-                mu, ls, h = pol(x, h=h0)
+                mu, ls, h = pol(x, h=h0, h_reset=reset)
             (mu.square().sum() + (ls * 0.3).sum() + h.square().sum()).backward()
             return mu.detach(), ls.detach(), {k: p.grad.clone() for k, p in pol.named_parameters()}
         finally:
@@ -101,27 +102,29 @@ def test_policy_gru_fwd_bwd_match_autograd(n_in, N):
     W2, b2, Wh, bh = r(128, 128, sc=0.1), r(128, sc=0.1), r(128, 6, sc=0.1), r(6, sc=0.1)
     x, h = r(N, n_in), r(N, 64, sc=0.6)
     gh = r(N, 64, sc=0.5)
+    reset = (torch.rand(N, generator=g) < 0.1).cuda()  # rows whose carried h restarts at 0
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     h_out, y = torch.empty(N, 64, device="cuda"), torch.empty(N, 6, device="cuda")
-    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, *_ptrs(x, h, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh, h_out,
-                                                          y), n_sm, L.stream_handle()), "gru fwd")
+    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, *_ptrs(x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh,
+                                                          h_out, y), n_sm, L.stream_handle()), "gru fwd")
     dx, dh = torch.empty_like(x), torch.empty_like(h)
-    gr = [torch.zeros_like(t) for t in (Wi, bi, Wg, bg)]
+    gr = [torch.full_like(t, 7.0) for t in (Wi, bi, Wg, bg)]  # overwritten, not accumulated
     work = torch.empty(L.lib().qs_policy_work_floats(1, n_sm), device="cuda")
-    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(x, h, gh, None, Wi, bi, Wg, bg, dx, dh, *gr, work),
+    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr, work),
                                       work.numel(), n_sm, L.stream_handle()), "gru bwd")
     # reproducible: a second pass gives the same bits (per-CTA partials, fixed-order sum)
     gr2 = [torch.zeros_like(t) for t in (Wi, bi, Wg, bg)]
-    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(x, h, gh, None, Wi, bi, Wg, bg, dx, dh, *gr2, work),
+    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr2, work),
                                       work.numel(), n_sm, L.stream_handle()), "gru bwd")
     assert all(torch.equal(a, b) for a, b in zip(gr, gr2))
     leaves = [t.clone().requires_grad_(True) for t in (x, h, Wi, bi, Wg, bg)]
     xl, hl, wi, ci, wg, cg = leaves
-    gi, gg = xl @ wi + ci, hl @ wg + cg
+    hm = torch.where(reset[:, None], torch.zeros_like(hl), hl)
+    gi, gg = xl @ wi + ci, hm @ wg + cg
     rr = torch.sigmoid(gi[:, :64] + gg[:, :64])
     zz = torch.sigmoid(gi[:, 64:128] + gg[:, 64:128])
     nn = torch.tanh(gi[:, 128:] + rr * gg[:, 128:])
-    h_ref = nn + zz * (hl - nn)
+    h_ref = nn + zz * (hm - nn)
     z = torch.tanh(torch.tanh(torch.tanh(h_ref @ W0 + b0) @ W1 + b1) @ W2 + b2)
     y_ref = z @ Wh + bh
     (h_ref * gh).sum().backward()
