@@ -83,6 +83,30 @@ QS_D void ld32s(const __nv_bfloat16* buf, int r, int c0, int cols, float (&v)[32
   }
 }
 
+// fp32 row-major [rows][COLS] (rows >= valid read as 0) -> bf16 blocked [rows][COLS]:
+// 16-byte loads, four in flight per thread before any conversion
+template <int COLS>
+QS_D void stage_w(const float* __restrict__ src, int rows, int valid, __nv_bfloat16* dst, int tid) {
+  constexpr int C4 = COLS / 4;
+  const int total = rows * C4;
+  for (int i0 = tid; i0 < total; i0 += 4 * PT) {
+    float4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * PT, rr = i / C4;
+      v[u] = (i < total && rr < valid) ? __ldg(reinterpret_cast<const float4*>(src) + i)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * PT;
+      if (i < total)
+        *reinterpret_cast<uint2*>(&dst[umma::blk_off(i / C4, (i % C4) * 4, COLS)]) =
+            make_uint2(pk(v[u].x, v[u].y), pk(v[u].z, v[u].w));
+    }
+  }
+}
+
 struct PolSmem {
   __nv_bfloat16 W0[HI * HW];   // [64][128]   B of h W0 (MN-major) and of gA1 W0^T (K-major)
   __nv_bfloat16 W1[HW * HW];   // [128][128]  B of A1 W1 (MN) and gA2 W1^T (K)
@@ -126,11 +150,9 @@ __global__ void __launch_bounds__(PT, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 32 * (warp & 3) + lane, q = warp >> 2, cq = 32 * q;
   // ---- weights (bf16, blocked) and biases
-  for (int i = tid; i < HI * HW; i += PT) S.W0[blk_off(i / HW, i % HW, HW)] = __float2bfloat16_rn(W0[i]);
-  for (int i = tid; i < HW * HW; i += PT) {
-    S.W1[blk_off(i / HW, i % HW, HW)] = __float2bfloat16_rn(W1[i]);
-    S.W2[blk_off(i / HW, i % HW, HW)] = __float2bfloat16_rn(W2[i]);
-  }
+  stage_w<HW>(W0, HI, HI, S.W0, tid);
+  stage_w<HW>(W1, HW, HW, S.W1, tid);
+  stage_w<HW>(W2, HW, HW, S.W2, tid);
   for (int i = tid; i < HW * HY; i += PT) {
     const int k = i / HY, n = i % HY;  // Wh (128, n_out) row-major, zero-padded to 16 columns
     S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
@@ -146,11 +168,8 @@ __global__ void __launch_bounds__(PT, 1)
   __nv_bfloat16* const XS = S.A2;
   __nv_bfloat16* const HS = S.A2 + TR * XI;
   if constexpr (GRU) {
-    for (int i = tid; i < XI * G3; i += PT) {
-      const int k = i / G3, n = i % G3;
-      WI[blk_off(k, n, G3)] = __float2bfloat16_rn(k < ga.n_in ? ga.Wi[k * G3 + n] : 0.f);
-    }
-    for (int i = tid; i < HI * G3; i += PT) WG[blk_off(i / G3, i % G3, G3)] = __float2bfloat16_rn(ga.Wg[i]);
+    stage_w<G3>(ga.Wi, XI, ga.n_in, WI, tid);
+    stage_w<G3>(ga.Wg, HI, HI, WG, tid);
     for (int i = tid; i < 4 * HI; i += PT)
       S.bg[i] = i < 2 * HI ? ga.bi[i] + ga.bg[i] : i < 3 * HI ? ga.bi[i] : ga.bg[i - HI];
   }
@@ -221,31 +240,67 @@ __global__ void __launch_bounds__(PT, 1)
   const uint32_t id_mm16 = umma::idesc_bf16(128, 16, true, true);
   const uint32_t id_k_mn16 = umma::idesc_bf16(128, 16, false, true);
   const int64_t ntiles = (N + TR - 1) / TR;
+  // the next tile's h row quarter and dL/dy, loaded one tile ahead (registers)
+  float hv_n[16], gy_n[HY / 2], xv_n[GRU ? XI : 1];
+  auto fetch = [&](int64_t t) {
+    const int64_t rw = t * TR + r;
+    const bool vd = t < ntiles && rw < N;
+    if constexpr (GRU) {  // the carried h (0 on a reset row) and, quarter 0, the input row
+      const bool lv = vd && !(ga.reset && ga.reset[rw]);
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 u = lv ? __ldg(reinterpret_cast<const float4*>(ga.hp + rw * HI + 16 * q + j))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        hv_n[j] = u.x;
+        hv_n[j + 1] = u.y;
+        hv_n[j + 2] = u.z;
+        hv_n[j + 3] = u.w;
+      }
+      if (q == 0) {
+#pragma unroll
+        for (int j = 0; j < XI; ++j) xv_n[j] = (vd && j < ga.n_in) ? __ldg(ga.x + rw * ga.n_in + j) : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        const float4 u = vd ? __ldg(reinterpret_cast<const float4*>(h + rw * HI + 16 * q + j))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        hv_n[j] = u.x;
+        hv_n[j + 1] = u.y;
+        hv_n[j + 2] = u.z;
+        hv_n[j + 3] = u.w;
+      }
+    }
+    if constexpr (BWD) {
+      if (q == 0) {
+#pragma unroll
+        for (int j = 0; j < HY / 2; ++j) gy_n[j] = (vd && j < n_out) ? __ldg(dy + rw * n_out + j) : 0.f;
+      }
+    }
+  };
+  fetch(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = tile * TR + r;
     const bool valid = row < N;
+    float v[16], gyc[HY / 2], xv[GRU ? XI : 1];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = hv_n[j];
+    if constexpr (GRU) {
+#pragma unroll
+      for (int j = 0; j < XI; ++j) xv[j] = xv_n[j];
+    }
+#pragma unroll
+    for (int j = 0; j < HY / 2; ++j) gyc[j] = gy_n[j];
+    fetch(tile + gridDim.x);
     if constexpr (GRU) {
       // ---- the GRU cell: gates from x and the carried h; TMEM [128,256)
       // r|z pre-activations (x Wi + h Wh summed), [256,320) x Wi_n, [320,384) h Wh_n
-      float hp[16];
-      const bool live = valid && !(ga.reset && ga.reset[row]);
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const float4 t = live ? __ldg(reinterpret_cast<const float4*>(ga.hp + row * HI + 16 * q + j))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-        hp[j] = t.x;
-        hp[j + 1] = t.y;
-        hp[j + 2] = t.z;
-        hp[j + 3] = t.w;
-      }
+      float (&hp)[16] = v;
 #pragma unroll
       for (int j = 0; j < 16; j += 8)
         *reinterpret_cast<uint4*>(&HS[blk_off(r, 16 * q + j, HI)]) = make_uint4(
             pk(hp[j], hp[j + 1]), pk(hp[j + 2], hp[j + 3]), pk(hp[j + 4], hp[j + 5]), pk(hp[j + 6], hp[j + 7]));
       if (q == 0) {
-        float xv[XI];
-#pragma unroll
-        for (int j = 0; j < XI; ++j) xv[j] = (valid && j < ga.n_in) ? __ldg(ga.x + row * ga.n_in + j) : 0.f;
 #pragma unroll
         for (int j = 0; j < XI; j += 8)
           *reinterpret_cast<uint4*>(&XS[blk_off(r, j, XI)]) = make_uint4(
@@ -289,16 +344,6 @@ __global__ void __launch_bounds__(PT, 1)
               make_uint4(pk(o[j], o[j + 1]), pk(o[j + 2], o[j + 3]), pk(o[j + 4], o[j + 5]), pk(o[j + 6], o[j + 7]));
       }
     } else {  // ---- stage h (quarter q: columns 16q..16q+15)
-      float v[16];
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const float4 t = valid ? __ldg(reinterpret_cast<const float4*>(h + row * HI + 16 * q + j))
-                               : make_float4(0.f, 0.f, 0.f, 0.f);
-        v[j] = t.x;
-        v[j + 1] = t.y;
-        v[j + 2] = t.z;
-        v[j + 3] = t.w;
-      }
 #pragma unroll
       for (int j = 0; j < 16; j += 8)
         *reinterpret_cast<uint4*>(&S.H[blk_off(r, 16 * q + j, HI)]) =
@@ -307,12 +352,7 @@ __global__ void __launch_bounds__(PT, 1)
     if (BWD && q == 0) {  // dL/dy
       float g[HY];
 #pragma unroll
-      for (int j = 0; j < HY; ++j) g[j] = 0.f;
-      if (valid) {
-#pragma unroll
-        for (int j = 0; j < HY / 2; ++j)
-          if (j < n_out) g[j] = __ldg(dy + row * n_out + j);
-      }
+      for (int j = 0; j < HY; ++j) g[j] = j < HY / 2 ? gyc[j] : 0.f;
 #pragma unroll
       for (int j = 0; j < HY / 2; ++j) dbh_acc[j] += g[j];
       g[HY - 1] = 1.f;  // ones column: the bias gradients' column sums
@@ -530,11 +570,8 @@ __global__ void __launch_bounds__(PT, 1)
   constexpr int BC = 96;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 32 * (warp & 3) + lane, q = warp >> 2;
-  for (int i = tid; i < XI * G3; i += PT) {
-    const int k = i / G3, n = i % G3;
-    S.WI[blk_off(k, n, G3)] = __float2bfloat16_rn(k < n_in ? Wi[k * G3 + n] : 0.f);
-  }
-  for (int i = tid; i < HI * G3; i += PT) S.WG[blk_off(i / G3, i % G3, G3)] = __float2bfloat16_rn(Wg[i]);
+  stage_w<G3>(Wi, XI, n_in, S.WI, tid);
+  stage_w<G3>(Wg, HI, HI, S.WG, tid);
   for (int i = tid; i < 4 * HI; i += PT) S.bg[i] = i < 2 * HI ? bi[i] + bgv[i] : i < 3 * HI ? bi[i] : bgv[i - HI];
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
@@ -611,26 +648,27 @@ __global__ void __launch_bounds__(PT, 1)
         umma::mma_bf16(THN, aK(S.B, BC, 1 + ks), mKc(S.WG, G3, ks, 2 * HI), id64, ks > 0);
       umma::commit(&S.bar);
     }
+    float g[16];  // dL/dh', loaded while the gate GEMMs run
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
+      if (valid) {
+        a = __ldg(reinterpret_cast<const float4*>(dha + row * HI + 16 * q + j));
+        if (dhb) b = __ldg(reinterpret_cast<const float4*>(dhb + row * HI + 16 * q + j));
+      }
+      g[j] = a.x + b.x;
+      g[j + 1] = a.y + b.y;
+      g[j + 2] = a.z + b.z;
+      g[j + 3] = a.w + b.w;
+    }
     wait();
     float dd[16];  // g z: the direct part of dL/dh
     {
-      float gr[16], gz[16], gn[16], hn[16], g[16];
+      float gr[16], gz[16], gn[16], hn[16];
       umma::tmem_ld16(TRZ + lanes + 16 * q, gr);
       umma::tmem_ld16(TRZ + lanes + HI + 16 * q, gz);
       umma::tmem_ld16(TGN + lanes + 16 * q, gn);
       umma::tmem_ld16(THN + lanes + 16 * q, hn);
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-        if (valid) {
-          a = __ldg(reinterpret_cast<const float4*>(dha + row * HI + 16 * q + j));
-          if (dhb) b = __ldg(reinterpret_cast<const float4*>(dhb + row * HI + 16 * q + j));
-        }
-        g[j] = a.x + b.x;
-        g[j + 1] = a.y + b.y;
-        g[j + 2] = a.z + b.z;
-        g[j + 3] = a.w + b.w;
-      }
       uint32_t wr[8], wz[8], wn[8], wnr[8];
 #pragma unroll
       for (int j = 0; j < 16; j += 2) {

@@ -18,23 +18,27 @@ struct Segs {  // out[s][i] (+)= sum_b work[b * P + off[s] + i], i < len[s]
   bool accumulate;  // add to out (else overwrite)
 };
 
-static __global__ void k_sum_partials(const float* __restrict__ work, int nblk, int64_t P, Segs s) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+constexpr int RED_E = 32, RED_S = 8;  // a block: 32 consecutive entries x 8 CTA slices
+
+static __global__ void __launch_bounds__(RED_E * RED_S)
+    k_sum_partials(const float* __restrict__ work, int nblk, int64_t P, Segs s) {
+  __shared__ float part[RED_S][RED_E];
+  const int e = threadIdx.x % RED_E, sl = threadIdx.x / RED_E;
+  int64_t i = (int64_t)blockIdx.x * RED_E + e;
   int k = 0;
   while (k < s.n && i >= s.len[k]) i -= s.len[k++];
-  if (k >= s.n) return;
-  const float* p = work + s.off[k] + i;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;  // fixed association: ((b%4 classes) in order) then combined
-  int b = 0;
-  for (; b + 4 <= nblk; b += 4) {
-    a0 += __ldg(p + (int64_t)b * P);
-    a1 += __ldg(p + (int64_t)(b + 1) * P);
-    a2 += __ldg(p + (int64_t)(b + 2) * P);
-    a3 += __ldg(p + (int64_t)(b + 3) * P);
+  float a = 0.f;
+  if (k < s.n) {  // slice sl: CTAs sl, sl + 8, sl + 16, ... in order
+    const float* p = work + s.off[k] + i;
+    for (int b = sl; b < nblk; b += RED_S) a += __ldg(p + (int64_t)b * P);
   }
-  for (; b < nblk; ++b) a0 += __ldg(p + (int64_t)b * P);
-  const float sum = (a0 + a1) + (a2 + a3);
-  s.out[k][i] = s.accumulate ? s.out[k][i] + sum : sum;
+  part[sl][e] = a;
+  __syncthreads();
+  if (sl == 0 && k < s.n) {
+    const float sum = ((part[0][e] + part[1][e]) + (part[2][e] + part[3][e])) +
+                      ((part[4][e] + part[5][e]) + (part[6][e] + part[7][e]));
+    s.out[k][i] = s.accumulate ? s.out[k][i] + sum : sum;
+  }
 }
 
 // launch the sum over `nblk` partials of width P for the non-null segments
@@ -51,8 +55,7 @@ static int sum_partials(const float* work, int nblk, int64_t P, const Segs& segs
     ++s.n;
   }
   if (total == 0) return QS_OK;
-  const int threads = 128;
-  k_sum_partials<<<(unsigned)((total + threads - 1) / threads), threads, 0, st>>>(work, nblk, P, s);
+  k_sum_partials<<<(unsigned)((total + RED_E - 1) / RED_E), RED_E * RED_S, 0, st>>>(work, nblk, P, s);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 
