@@ -408,15 +408,13 @@ constexpr int64_t CK_W1 = 0, CK_W0 = CK_W1 + HID * HID, CK_B0 = CK_W0 + 16 * HID
                   CK_P = (CK_L + 1 + 31) / 32 * 32;  // rows 128-byte aligned (float4 stores)
 
 // 32 consecutive columns of this thread's TMEM lane
-QS_D void tmem_ld32(uint32_t t, float (&v)[32]) {
-  float a[16], b[16];
-  umma::tmem_ld16(t, a);
-  umma::tmem_ld16(t + 16, b);
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    v[j] = a[j];
-    v[16 + j] = b[j];
-  }
+QS_D void tmem_ld32(uint32_t t, float (&v)[32]) { umma::tmem_ld32(t, v); }
+// tanh of a bf16 pair (MUFU, one op for two values): torch's bf16 autocast
+// rounds the linear layer's output to bf16 before its tanh, so does this
+QS_D uint32_t tanh_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
 }
 // 8 bf16 pairs -> one 16-byte store at (row, c0) of a blocked [rows][HID] buffer
 QS_D void st_row8(__nv_bfloat16* buf, int row, int c0, const uint32_t* w) {
@@ -443,8 +441,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int cq = q * TC_QC;
   // ---- parameters -> shared memory (bf16 operands, fp32 vectors)
   for (int i = tid; i < HID * KIN; i += TC_THREADS) {
-    const int n = i / KIN, k = i % KIN;  // W0T[n][k] = W0[k][n]
-    S.W0T[blk_off(n, k, KIN)] = __float2bfloat16_rn(k < K ? W0[k * HID + n] : 0.f);
+    const int n = i / KIN, k = i % KIN;  // W0T[n][k] = W0[k][n]; column 15 = b0 (X's ones column adds it)
+    S.W0T[blk_off(n, k, KIN)] = __float2bfloat16_rn(k < K ? W0[k * HID + n] : k == KIN - 1 ? b0[n] : 0.f);
   }
   for (int i = tid; i < HID * HID; i += TC_THREADS) {
     const int k = i / HID, n = i % HID;  // W1[k][n] -> W1T[n][k]
@@ -573,13 +571,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      id_16_mn, !first5 || ks > 0);
     umma::commit(&S.bar[sl]);
   };
-  auto epi1 = [&](int sl) {  // H1 = tanh(. + b0)
+  auto epi1 = [&](int sl) {  // H1 = tanh(X W0 + b0) (b0 entered through X's ones column)
     float v[32];
     tmem_ld32(T0 + 128 * sl + my, v);
     uint32_t w[16];
 #pragma unroll
-    for (int j = 0; j < 32; j += 2)
-      w[j / 2] = pack_bf16(tanh_mufu(v[j] + S.b0[cq + j]), tanh_mufu(v[j + 1] + S.b0[cq + j + 1]));
+    for (int j = 0; j < 32; j += 2) w[j / 2] = tanh_bf16x2(pack_bf16(v[j], v[j + 1]));
 #pragma unroll
     for (int j = 0; j < 4; ++j) st_row8(S.slot[sl].H1, r, cq + 8 * j, w + 4 * j);
   };
@@ -590,8 +587,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float part = 0.f;
 #pragma unroll
     for (int j = 0; j < 32; j += 2) {
-      h[j] = tanh_mufu(h[j] + S.b1[cq + j]);
-      h[j + 1] = tanh_mufu(h[j + 1] + S.b1[cq + j + 1]);
+      const float2 t = unpack_bf16(tanh_bf16x2(pack_bf16(h[j] + S.b1[cq + j], h[j + 1] + S.b1[cq + j + 1])));
+      h[j] = t.x;
+      h[j + 1] = t.y;
       part = fmaf(h[j], S.w2[cq + j], fmaf(h[j + 1], S.w2[cq + j + 1], part));
     }
     T.predq[q][r] = part;
