@@ -238,56 +238,81 @@ class _PolicyStepFn(torch.autograd.Function):
     (q/nets.py:107-132, 241-256) in one tcgen05 kernel (qs_policy_gru_fwd);
     the backward is the trunk's (qs_policy_trunk_bwd, dL/dy -> dL/dh') then the
     GRU cell's (qs_policy_gru_bwd, dL/dh' from the trunk plus the carried one).
-    The two heads enter as separate parameters (Wh = [W_mu | W_sigma] is
-    assembled here, outside autograd, and its gradient split back)."""
+    The parameters enter as ONE flat tensor (``PolicyNet.pack_weights``, layout
+    ``PolicyNet._fused_params``): a rollout packs them once, and the 16 steps'
+    gradients accumulate into one buffer instead of 14 per step."""
 
     @staticmethod
-    def forward(ctx, x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wmu, bmu, Wsig, bsig):
+    def forward(ctx, x, h, reset, wp, n_in, A):
         from paper_2509_10247_b200 import _lib as L
 
         ctx.set_materialize_grads(False)
         x, h = x.contiguous(), h.contiguous()
         rs = reset.contiguous().view(torch.uint8) if reset is not None else None
-        ws = [t.detach().float().contiguous() for t in (Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2)]
-        Wh = torch.cat([Wmu.detach(), Wsig.detach()], 1).float().contiguous()
-        bh = torch.cat([bmu.detach(), bsig.detach()]).float().contiguous()
-        N, n_in, n_out = x.shape[0], x.shape[1], Wh.shape[1]
+        wp = wp.detach()
+        offs = _pack_offsets(n_in, A)
+        v = {k: wp[o:o + n] for k, (o, n) in offs.items()}
+        Wh = torch.cat([v["Wmu"].view(128, A), v["Wsig"].view(128, A)], 1).contiguous()
+        bh = torch.cat([v["bmu"], v["bsig"]])
+        N = x.shape[0]
         h_out = torch.empty(N, h.shape[1], dtype=torch.float32, device=x.device)
-        y = torch.empty(N, n_out, dtype=torch.float32, device=x.device)
+        y = torch.empty(N, 2 * A, dtype=torch.float32, device=x.device)
         n_sm = torch.cuda.get_device_properties(x.device).multi_processor_count
-        L.check(L.lib().qs_policy_gru_fwd(N, n_in, n_out, L.ptr(x), L.ptr(h), L.ptr(rs), *[L.ptr(t) for t in ws],
+        L.check(L.lib().qs_policy_gru_fwd(N, n_in, 2 * A, L.ptr(x), L.ptr(h), L.ptr(rs),
+                                          *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg", "W0", "b0", "W1", "b1", "W2",
+                                                                  "b2")],
                                           L.ptr(Wh), L.ptr(bh), L.ptr(h_out), L.ptr(y), n_sm,
                                           L.stream_handle(x.device)), "qs_policy_gru_fwd")
-        ctx.save_for_backward(x, h, rs, h_out, *ws, Wh)
-        ctx.n_sm, ctx.A = n_sm, Wmu.shape[1]
+        ctx.save_for_backward(x, h, rs, h_out, wp, Wh)
+        ctx.n_sm, ctx.A, ctx.n_in = n_sm, A, n_in
         return h_out, y
 
     @staticmethod
     def backward(ctx, g_h, g_y):
         from paper_2509_10247_b200 import _lib as L
 
-        x, h, rs, h_out, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh = ctx.saved_tensors
-        N, n_out, A = x.shape[0], Wh.shape[1], ctx.A
+        x, h, rs, h_out, wp, Wh = ctx.saved_tensors
+        N, A, n_in = x.shape[0], ctx.A, ctx.n_in
         dev, st = x.device, L.stream_handle(x.device)
-        g_y = torch.zeros(N, n_out, device=dev) if g_y is None else g_y.contiguous().float()
+        offs = _pack_offsets(n_in, A)
+        v = {k: wp[o:o + n] for k, (o, n) in offs.items()}
+        gw = torch.empty_like(wp)  # every slice is written below
+        gv = {k: gw[o:o + n] for k, (o, n) in offs.items()}
+        g_y = torch.zeros(N, 2 * A, device=dev) if g_y is None else g_y.contiguous().float()
         g_h = None if g_h is None else g_h.contiguous().float()
         dh_t = torch.empty_like(h_out)
-        tg = [torch.empty_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
-        gbh = torch.empty(n_out, dtype=torch.float32, device=dev)
+        gWh = torch.empty(128, 2 * A, dtype=torch.float32, device=dev)
+        gbh = torch.empty(2 * A, dtype=torch.float32, device=dev)
         work = _work(0, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h_out), L.ptr(g_y),
-                                            *[L.ptr(t) for t in (W0, b0, W1, b1, W2, b2, Wh)], L.ptr(dh_t),
-                                            *[L.ptr(t) for t in tg], L.ptr(gbh), L.ptr(work), work.numel(), ctx.n_sm,
-                                            st), "qs_policy_trunk_bwd")
+        L.check(L.lib().qs_policy_trunk_bwd(N, 2 * A, L.ptr(h_out), L.ptr(g_y),
+                                            *[L.ptr(v[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2")], L.ptr(Wh),
+                                            L.ptr(dh_t), *[L.ptr(gv[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2")],
+                                            L.ptr(gWh), L.ptr(gbh), L.ptr(work), work.numel(), ctx.n_sm, st),
+                "qs_policy_trunk_bwd")
         dx, dh = torch.empty_like(x), torch.empty_like(h)
-        gg = [torch.empty_like(t) for t in (Wi, bi, Wg, bg)]
         work = _work(1, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_gru_bwd(N, x.shape[1], L.ptr(x), L.ptr(h), L.ptr(rs), L.ptr(dh_t), L.ptr(g_h),
-                                          *[L.ptr(t) for t in (Wi, bi, Wg, bg)], L.ptr(dx), L.ptr(dh),
-                                          *[L.ptr(t) for t in gg], L.ptr(work), work.numel(), ctx.n_sm, st),
-                "qs_policy_gru_bwd")
-        gWh = tg.pop()
-        return (dx, dh, None, *gg, *tg, gWh[:, :A], gbh[:A], gWh[:, A:], gbh[A:])
+        L.check(L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(x), L.ptr(h), L.ptr(rs), L.ptr(dh_t), L.ptr(g_h),
+                                          *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg")], L.ptr(dx), L.ptr(dh),
+                                          *[L.ptr(gv[k]) for k in ("Wi", "bi", "Wg", "bg")], L.ptr(work),
+                                          work.numel(), ctx.n_sm, st), "qs_policy_gru_bwd")
+        gv["Wmu"].view(128, A).copy_(gWh[:, :A])
+        gv["Wsig"].view(128, A).copy_(gWh[:, A:])
+        gv["bmu"].copy_(gbh[:A])
+        gv["bsig"].copy_(gbh[A:])
+        return dx, dh, None, gw, None, None
+
+
+def _pack_offsets(n_in, A, H=64, W=128):
+    """Flat layout of the fused policy-step parameters (every matrix starts on
+    a 16-byte boundary: the kernels stage them with 16-byte loads)."""
+    sizes = [("Wi", n_in * 3 * H), ("bi", 3 * H), ("Wg", H * 3 * H), ("bg", 3 * H), ("W0", H * W), ("b0", W),
+             ("W1", W * W), ("b1", W), ("W2", W * W), ("b2", W), ("Wmu", W * A), ("bmu", A), ("Wsig", W * A),
+             ("bsig", A)]
+    out, o = {}, 0
+    for k, n in sizes:
+        out[k] = (o, n)
+        o += n
+    return out
 
 
 @dataclass
@@ -333,13 +358,30 @@ class PolicyNet(torch.nn.Module):
             self.sig.b.fill_(arch.log_sigma_init)
         self.hidden = arch.hidden
 
+    def _fused_params(self):
+        """The parameters of the fused policy step, in ``_pack_offsets`` order."""
+        g, L = self.gru, self.trunk.layers
+        return [g.Wi, g.bi, g.Wh, g.bh, L[0].W, L[0].b, L[1].W, L[1].b, L[2].W, L[2].b, self.mu.W, self.mu.b,
+                self.sig.W, self.sig.b]
+
+    def pack_weights(self):
+        """One flat, differentiable copy of the fused step's parameters; pass
+        it to every step of a rollout (``forward(..., packed=...)``) so their
+        gradients accumulate in one buffer.  None when the fused step does
+        not apply to this architecture."""
+        if self.gru is None or self.hidden != 64 or tuple(self.arch.mlp) != (128, 128) or \
+                2 * self.arch.action_dim > 8:
+            return None
+        return torch.cat([p.reshape(-1) for p in self._fused_params()])
+
     def initial_hidden(self, batch, device=None):
         return torch.zeros(batch, self.hidden, device=device) if self.gru is not None else None
 
-    def forward(self, proprio, visual=None, h=None, h_reset=None):
+    def forward(self, proprio, visual=None, h=None, h_reset=None, packed=None):
         """h_reset (bool (N,), optional): rows whose carried hidden state
         restarts at zero before this step (the trainer's episode resets,
-        q/learners.py:215-217), folded into the fused kernel when it runs."""
+        q/learners.py:215-217), folded into the fused kernel when it runs.
+        packed: ``pack_weights()`` of this module, reused across a rollout."""
         x = proprio * self.input_scale.to(proprio.dtype)
         if self.enc is not None:
             if visual is None:
@@ -356,10 +398,8 @@ class PolicyNet(torch.nn.Module):
             # bf16 policy mode: GRU cell, trunk and both heads in one tcgen05 kernel
             if h is None:
                 h = torch.zeros(x.shape[0], self.hidden, device=x.device)
-            g = self.gru
-            h, y = _PolicyStepFn.apply(x, h.float(), h_reset, g.Wi, g.bi, g.Wh, g.bh, layers[0].W, layers[0].b,
-                                       layers[1].W, layers[1].b, layers[2].W, layers[2].b, self.mu.W, self.mu.b,
-                                       self.sig.W, self.sig.b)
+            wp = packed if packed is not None else self.pack_weights()
+            h, y = _PolicyStepFn.apply(x, h.float(), h_reset, wp, x.shape[1], A)
             return y[:, :A], torch.clamp(y[:, A:2 * A], LOG_SIGMA_MIN, self.arch.log_sigma_max), h
         if self.gru is not None:
             if h is None:

@@ -291,11 +291,13 @@ class ShortHorizonTrainer:
         disc = 0.0
         r_ctrl, r_goal, dones, priv = [], [], [], []
         reset = None  # rows whose episode ended last step: their hidden state restarts at 0
+        # the fused policy step's parameters packed once for the window (bf16 mode)
+        packed = self.policy.pack_weights() if self._amp else None
         for t in range(T):
             if record_privileged:
                 priv.append(env.privileged_state())
             with self._nets():
-                mu, log_sigma, h = self.policy(obs.proprio, obs.visual, h, h_reset=reset)
+                mu, log_sigma, h = self.policy(obs.proprio, obs.visual, h, h_reset=reset, packed=packed)
             a = mu
             if opts.explore:
                 eps = torch.randn(mu.shape, generator=self._gen, device=mu.device)
