@@ -253,6 +253,10 @@ class BpttWindow:
         for e in free + drained:
             e.record(comp)
         losses = torch.zeros(len(host_batches), dtype=torch.float64).pin_memory()
+        # each window's loss is parked on the device by a kernel on the compute
+        # stream and read back once at the end: a per-window 8-byte D2H on the
+        # compute stream would queue behind the 33.5 MB gradient downloads
+        loss_dev = torch.zeros(len(host_batches), dtype=torch.float64, device=self.env.device)
 
         def upload(k):
             b = k % 2
@@ -271,13 +275,14 @@ class BpttWindow:
             comp.wait_event(drained[b])  # window k-2's gradient has left grads[b]
             P["graphs"][b].replay()
             free[b].record(comp)
-            losses[k].copy_(self.loss64, non_blocking=True)
+            loss_dev[k:k + 1].add_(self.loss64)
             if grad_out is not None:
                 computed[b].record(comp)
                 with torch.cuda.stream(d2h):
                     d2h.wait_event(computed[b])
                     grad_out[k].copy_(P["gbufs"][b], non_blocking=True)
                     drained[b].record(d2h)
+        losses.copy_(loss_dev, non_blocking=True)
         comp.synchronize()
         if grad_out is not None:
             d2h.synchronize()
