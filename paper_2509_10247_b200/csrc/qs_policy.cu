@@ -33,7 +33,18 @@ constexpr int HW = 128;     // trunk width
 constexpr int HY = 16;      // head outputs, padded (mu | log sigma | 0 | ones column for bias sums)
 constexpr int XI = 16;      // GRU input width, padded (proprio features)
 constexpr int G3 = 3 * HI;  // GRU gate columns (r | z | n)
-QS_D float sigm_f(float x) { return 1.f / (1.f + __expf(-x)); }
+// logistic sigmoid as 0.5 tanh(x / 2) + 0.5: one MUFU op (an IEEE 1 / (1 + e^-x)
+// is a multi-instruction software divide: it was a third of the policy
+// kernels' instructions)
+QS_D float tanh_f(float x);
+QS_D float sigm_f(float x) { return fmaf(0.5f, tanh_f(0.5f * x), 0.5f); }
+// tanh of a bf16 pair in one MUFU op; the trunk's activations are bf16 (and
+// torch's bf16 autocast rounds the linear output to bf16 before its tanh)
+QS_D uint32_t tanh_bf16x2(uint32_t x) {
+  uint32_t y;
+  asm("tanh.approx.bf16x2 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
 // per-CTA gradient partials (qs_reduce.cuh): the trunk backward's layout
 constexpr int64_t TK_W0 = 0, TK_B0 = TK_W0 + HI * HW, TK_W1 = TK_B0 + HW, TK_B1 = TK_W1 + HW * HW,
                   TK_W2 = TK_B1 + HW, TK_B2 = TK_W2 + HW * HW, TK_WH = TK_B2 + HW, TK_BH = TK_WH + HW * 8,
@@ -115,31 +126,24 @@ struct PolSmem {
   __nv_bfloat16 H[TR * HI];    // [rows][64]  the tile's GRU output
   __nv_bfloat16 A1[TR * HW];   // A1, then dL/dA1-pre in place
   __nv_bfloat16 A2[TR * HW];   // A2, then dL/dA2-pre in place
-  // backward: z, then dL/dz-pre in place.  Forward: z lives in A1 (dead once
-  // A2 is computed) and this space holds the GRU weights Wi [16][192] and
-  // Wh [64][192] (blocked); the tile's x [128][16] and h [128][64] sit in A2
-  // until the gate GEMMs completed.
-  __nv_bfloat16 Z[TR * HW];
+  __nv_bfloat16 Z[TR * HW];    // z, then (backward) dL/dz-pre in place
   __nv_bfloat16 DY[TR * HY];   // dL/dy (8 columns), column 15 = 1
   float b0[HW], b1[HW], b2[HW], bh[HY];
-  float bg[4 * HI];            // GRU: bi + bh (r, z), bi (n), bh (n)
   float dbh[4][HY];             // per-warp dL/dbh sums (warps 0-3)
   uint64_t bar;
   uint32_t tbase;
 };
 
-static_assert(XI * G3 + HI * G3 <= TR * HW && TR * XI + TR * HI <= TR * HW, "GRU staging aliases");
-
-struct GruArgs {  // the forward's GRU cell (GRU = true)
+struct GruArgs {  // the GRU cell of the forward (k_policy_fwd2)
   int n_in;
   const float *x, *hp, *Wi, *bi, *Wg, *bg;
   const uint8_t* reset;  // rows whose carried h restarts at 0 (episode reset), or null
   float* h_out;
 };
 
-template <bool BWD, bool GRU = false>
+template <bool BWD>
 __global__ void __launch_bounds__(PT, 1)
-    k_policy_trunk(int64_t N, int n_out, GruArgs ga, const float* __restrict__ h, const float* __restrict__ dy,
+    k_policy_trunk(int64_t N, int n_out, const float* __restrict__ h, const float* __restrict__ dy,
                    const float* __restrict__ W0, const float* __restrict__ b0, const float* __restrict__ W1,
                    const float* __restrict__ b1, const float* __restrict__ W2, const float* __restrict__ b2,
                    const float* __restrict__ Wh, const float* __restrict__ bh, float* __restrict__ y,
@@ -163,16 +167,6 @@ __global__ void __launch_bounds__(PT, 1)
     S.b2[i] = b2[i];
   }
   if (tid < HY) S.bh[tid] = (bh && tid < n_out) ? bh[tid] : 0.f;  // (the backward takes no bh)
-  __nv_bfloat16* const WI = S.Z;             // GRU (forward only)
-  __nv_bfloat16* const WG = S.Z + XI * G3;
-  __nv_bfloat16* const XS = S.A2;
-  __nv_bfloat16* const HS = S.A2 + TR * XI;
-  if constexpr (GRU) {
-    stage_w<G3>(ga.Wi, XI, ga.n_in, WI, tid);
-    stage_w<G3>(ga.Wg, HI, HI, WG, tid);
-    for (int i = tid; i < 4 * HI; i += PT)
-      S.bg[i] = i < 2 * HI ? ga.bi[i] + ga.bg[i] : i < 3 * HI ? ga.bi[i] : ga.bg[i - HI];
-  }
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
     mbar_init(&S.bar, 1);
@@ -219,7 +213,7 @@ __global__ void __launch_bounds__(PT, 1)
     ld32(TG + lanes + cq, v);
     uint32_t w[16];
 #pragma unroll
-    for (int j = 0; j < 32; j += 2) w[j / 2] = pk(tanh_f(v[j] + bias[cq + j]), tanh_f(v[j + 1] + bias[cq + j + 1]));
+    for (int j = 0; j < 32; j += 2) w[j / 2] = tanh_bf16x2(pk(v[j] + bias[cq + j], v[j + 1] + bias[cq + j + 1]));
     st32(dst, r, cq, HW, w);
   };
   // epilogue: TMEM columns * (1 - act^2) (act = the bf16 activation row) -> in place over act
@@ -241,35 +235,18 @@ __global__ void __launch_bounds__(PT, 1)
   const uint32_t id_k_mn16 = umma::idesc_bf16(128, 16, false, true);
   const int64_t ntiles = (N + TR - 1) / TR;
   // the next tile's h row quarter and dL/dy, loaded one tile ahead (registers)
-  float hv_n[16], gy_n[HY / 2], xv_n[GRU ? XI : 1];
+  float hv_n[16], gy_n[HY / 2];
   auto fetch = [&](int64_t t) {
     const int64_t rw = t * TR + r;
     const bool vd = t < ntiles && rw < N;
-    if constexpr (GRU) {  // the carried h (0 on a reset row) and, quarter 0, the input row
-      const bool lv = vd && !(ga.reset && ga.reset[rw]);
 #pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const float4 u = lv ? __ldg(reinterpret_cast<const float4*>(ga.hp + rw * HI + 16 * q + j))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-        hv_n[j] = u.x;
-        hv_n[j + 1] = u.y;
-        hv_n[j + 2] = u.z;
-        hv_n[j + 3] = u.w;
-      }
-      if (q == 0) {
-#pragma unroll
-        for (int j = 0; j < XI; ++j) xv_n[j] = (vd && j < ga.n_in) ? __ldg(ga.x + rw * ga.n_in + j) : 0.f;
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; j += 4) {
-        const float4 u = vd ? __ldg(reinterpret_cast<const float4*>(h + rw * HI + 16 * q + j))
-                            : make_float4(0.f, 0.f, 0.f, 0.f);
-        hv_n[j] = u.x;
-        hv_n[j + 1] = u.y;
-        hv_n[j + 2] = u.z;
-        hv_n[j + 3] = u.w;
-      }
+    for (int j = 0; j < 16; j += 4) {
+      const float4 u = vd ? __ldg(reinterpret_cast<const float4*>(h + rw * HI + 16 * q + j))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      hv_n[j] = u.x;
+      hv_n[j + 1] = u.y;
+      hv_n[j + 2] = u.z;
+      hv_n[j + 3] = u.w;
     }
     if constexpr (BWD) {
       if (q == 0) {
@@ -282,68 +259,13 @@ __global__ void __launch_bounds__(PT, 1)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = tile * TR + r;
     const bool valid = row < N;
-    float v[16], gyc[HY / 2], xv[GRU ? XI : 1];
+    float v[16], gyc[HY / 2];
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = hv_n[j];
-    if constexpr (GRU) {
-#pragma unroll
-      for (int j = 0; j < XI; ++j) xv[j] = xv_n[j];
-    }
 #pragma unroll
     for (int j = 0; j < HY / 2; ++j) gyc[j] = gy_n[j];
     fetch(tile + gridDim.x);
-    if constexpr (GRU) {
-      // ---- the GRU cell: gates from x and the carried h; TMEM [128,256)
-      // r|z pre-activations (x Wi + h Wh summed), [256,320) x Wi_n, [320,384) h Wh_n
-      float (&hp)[16] = v;
-#pragma unroll
-      for (int j = 0; j < 16; j += 8)
-        *reinterpret_cast<uint4*>(&HS[blk_off(r, 16 * q + j, HI)]) = make_uint4(
-            pk(hp[j], hp[j + 1]), pk(hp[j + 2], hp[j + 3]), pk(hp[j + 4], hp[j + 5]), pk(hp[j + 6], hp[j + 7]));
-      if (q == 0) {
-#pragma unroll
-        for (int j = 0; j < XI; j += 8)
-          *reinterpret_cast<uint4*>(&XS[blk_off(r, j, XI)]) = make_uint4(
-              pk(xv[j], xv[j + 1]), pk(xv[j + 2], xv[j + 3]), pk(xv[j + 4], xv[j + 5]), pk(xv[j + 6], xv[j + 7]));
-      }
-      to_mma();
-      if (tid == 0) {
-        const uint32_t id128 = umma::idesc_bf16(128, 128, false, true), id64 = umma::idesc_bf16(128, 64, false, true);
-        umma::mma_bf16(T0 + 128, aK(XS, XI, 0), mKc(WI, G3, 0, 0), id128, false);
-#pragma unroll
-        for (int ks = 0; ks < HI / 16; ++ks) umma::mma_bf16(T0 + 128, aK(HS, HI, ks), mKc(WG, G3, ks, 0), id128, true);
-        umma::mma_bf16(T0 + 256, aK(XS, XI, 0), mKc(WI, G3, 0, 2 * HI), id64, false);
-#pragma unroll
-        for (int ks = 0; ks < HI / 16; ++ks)
-          umma::mma_bf16(T0 + 320, aK(HS, HI, ks), mKc(WG, G3, ks, 2 * HI), id64, ks > 0);
-        umma::commit(&S.bar);
-      }
-      wait();
-      {  // h' = (1 - z) n + z h for units 16q..16q+15 of this row
-        float gr[16], gz[16], gn[16], hn[16];
-        umma::tmem_ld16(T0 + 128 + lanes + 16 * q, gr);
-        umma::tmem_ld16(T0 + 128 + lanes + HI + 16 * q, gz);
-        umma::tmem_ld16(T0 + 256 + lanes + 16 * q, gn);
-        umma::tmem_ld16(T0 + 320 + lanes + 16 * q, hn);
-        float o[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int u = 16 * q + j;
-          const float rr = sigm_f(gr[j] + S.bg[u]), zz = sigm_f(gz[j] + S.bg[HI + u]);
-          const float nn = tanh_f(gn[j] + S.bg[2 * HI + u] + rr * (hn[j] + S.bg[3 * HI + u]));
-          o[j] = nn + zz * (hp[j] - nn);
-        }
-        if (valid) {
-          float4* dst = reinterpret_cast<float4*>(ga.h_out + row * HI + 16 * q);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
-        }
-#pragma unroll
-        for (int j = 0; j < 16; j += 8)
-          *reinterpret_cast<uint4*>(&S.H[blk_off(r, 16 * q + j, HI)]) =
-              make_uint4(pk(o[j], o[j + 1]), pk(o[j + 2], o[j + 3]), pk(o[j + 4], o[j + 5]), pk(o[j + 6], o[j + 7]));
-      }
-    } else {  // ---- stage h (quarter q: columns 16q..16q+15)
+    {  // ---- stage h (quarter q: columns 16q..16q+15)
 #pragma unroll
       for (int j = 0; j < 16; j += 8)
         *reinterpret_cast<uint4*>(&S.H[blk_off(r, 16 * q + j, HI)]) =
@@ -385,7 +307,7 @@ __global__ void __launch_bounds__(PT, 1)
       umma::commit(&S.bar);
     }
     wait();
-    __nv_bfloat16* const ZB = BWD ? S.Z : S.A1;  // forward: z over the dead A1 (Z holds the GRU weights)
+    __nv_bfloat16* const ZB = S.Z;
     epi_tanh(S.b2, ZB);
     to_mma();
     if constexpr (!BWD) {
@@ -536,6 +458,217 @@ __global__ void __launch_bounds__(PT, 1)
   if (warp == 0) umma::tmem_free(T0, 512);
   if (BWD && tid < n_out)
     work[(int64_t)blockIdx.x * TK_P + TK_BH + tid] = (S.dbh[0][tid] + S.dbh[1][tid]) + (S.dbh[2][tid] + S.dbh[3][tid]);
+}
+
+// ---- the policy step's forward with two tiles in flight (qs_policy_gru_fwd).
+// The forward keeps no activation after the next layer's GEMM read it, so a
+// tile needs ONE 32 KB activation buffer, overwritten layer by layer (h, then
+// A1, A2, z in place: each epilogue runs after the GEMM that read the previous
+// activation completed).  That leaves room for two tiles next to the 114 KB of
+// weights: the CTA's 16 warps form two independent groups of 8 (256 threads,
+// thread = TMEM lane x column half), each with its own tile, TMEM half
+// (256 columns), mbarrier and named barrier -- one group's epilogues fill the
+// other's GEMM and memory latencies.
+struct Fwd2Smem {
+  __nv_bfloat16 W0[HI * HW], W1[HW * HW], W2[HW * HW], WH[HW * HY];
+  __nv_bfloat16 WI[XI * G3], WG[HI * G3];
+  __nv_bfloat16 ACT[2][TR * HW];  // per group: h (prev, bf16) -> h' -> A1 -> A2 -> z
+  __nv_bfloat16 XS[2][TR * XI];   // per group: the input rows
+  float b0[HW], b1[HW], b2[HW], bh[HY], bg[4 * HI];
+  uint64_t bar[2];
+  uint32_t tbase;
+};
+
+QS_D void group_sync(int g) { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); }
+
+__global__ void __launch_bounds__(PT, 1)
+    k_policy_fwd2(int64_t N, int n_out, GruArgs ga, const float* __restrict__ W0, const float* __restrict__ b0,
+                  const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ W2,
+                  const float* __restrict__ b2, const float* __restrict__ Wh, const float* __restrict__ bh,
+                  float* __restrict__ y) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Fwd2Smem& S = *reinterpret_cast<Fwd2Smem*>(smem_raw);
+  using umma::blk_off;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = warp >> 3, gw = warp & 7;          // group, warp within the group
+  const int r = 32 * (gw & 3) + lane, hh = gw >> 2;  // tile row (TMEM lane), column half
+  stage_w<HW>(W0, HI, HI, S.W0, tid);
+  stage_w<HW>(W1, HW, HW, S.W1, tid);
+  stage_w<HW>(W2, HW, HW, S.W2, tid);
+  stage_w<G3>(ga.Wi, XI, ga.n_in, S.WI, tid);
+  stage_w<G3>(ga.Wg, HI, HI, S.WG, tid);
+  for (int i = tid; i < HW * HY; i += PT) {
+    const int k = i / HY, n = i % HY;
+    S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+  }
+  for (int i = tid; i < HW; i += PT) {
+    S.b0[i] = b0[i];
+    S.b1[i] = b1[i];
+    S.b2[i] = b2[i];
+  }
+  for (int i = tid; i < 4 * HI; i += PT)
+    S.bg[i] = i < 2 * HI ? ga.bi[i] + ga.bg[i] : i < 3 * HI ? ga.bi[i] : ga.bg[i - HI];
+  if (tid < HY) S.bh[tid] = tid < n_out ? bh[tid] : 0.f;
+  if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
+  if (tid == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    fence_barrier_init();
+  }
+  umma::fence_before();
+  __syncthreads();
+  umma::fence_after();
+  // this group's TMEM: r|z [0,128) (then the trunk accumulator), x Wi_n [128,192), h Wh_n [192,256)
+  const uint32_t TB = S.tbase + 256 * g, TRZ = TB, TGN = TB + 128, THN = TB + 192;
+  const uint32_t lanes = umma::taddr(0, 32 * (gw & 3), 0);
+  __nv_bfloat16* const ACT = S.ACT[g];
+  __nv_bfloat16* const XS = S.XS[g];
+  const bool issuer = (tid & 255) == 0;
+  uint32_t phase = 0;
+  auto to_mma = [&]() {
+    umma::fence_async_smem();
+    umma::fence_before();
+    group_sync(g);
+    umma::fence_after();
+  };
+  auto wait = [&]() {
+    umma::mbar_wait_parity(&S.bar[g], phase);
+    phase ^= 1u;
+    umma::fence_after();
+  };
+  auto aK = [](const __nv_bfloat16* b, int cols, int ks) { return umma::desc_kmajor(b + ks * 128, cols); };
+  auto mKc = [](const __nv_bfloat16* b, int cols, int ks, int c0) {
+    return umma::desc_mnmajor(b + ks * 2 * (cols / 8) * 64 + (c0 / 8) * 64, cols);
+  };
+  const uint32_t id128 = umma::idesc_bf16(128, 128, false, true), id64 = umma::idesc_bf16(128, 64, false, true),
+                 id16 = umma::idesc_bf16(128, 16, false, true);
+  // trunk layer epilogue: TMEM columns [64 hh, 64 hh + 64) + bias -> tanh -> ACT (in place)
+  auto epi_tanh = [&](const float* bias) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int c0 = 64 * hh + 32 * c;
+      float v[32];
+      umma::tmem_ld32(TRZ + lanes + c0, v);
+      uint32_t w[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) w[j / 2] = tanh_bf16x2(pk(v[j] + bias[c0 + j], v[j + 1] + bias[c0 + j + 1]));
+      st32(ACT, r, c0, HW, w);
+    }
+  };
+  const int64_t ntiles = (N + TR - 1) / TR;
+  for (int64_t tile = 2 * (int64_t)blockIdx.x + g; tile < ntiles; tile += 2 * (int64_t)gridDim.x) {
+    const int64_t row = tile * TR + r;
+    const bool valid = row < N;
+    const bool live = valid && !(ga.reset && ga.reset[row]);
+    // ---- stage the carried h (units 32 hh .. 32 hh + 31; 0 on a reset row) and the input row
+    float hp[32];
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      const float4 t = live ? __ldg(reinterpret_cast<const float4*>(ga.hp + row * HI + 32 * hh + j))
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+      hp[j] = t.x;
+      hp[j + 1] = t.y;
+      hp[j + 2] = t.z;
+      hp[j + 3] = t.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; j += 8)
+      *reinterpret_cast<uint4*>(&ACT[blk_off(r, 32 * hh + j, HI)]) =
+          make_uint4(pk(hp[j], hp[j + 1]), pk(hp[j + 2], hp[j + 3]), pk(hp[j + 4], hp[j + 5]), pk(hp[j + 6], hp[j + 7]));
+    if (hh == 0) {
+      float xv[XI];
+#pragma unroll
+      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < ga.n_in) ? __ldg(ga.x + row * ga.n_in + j) : 0.f;
+#pragma unroll
+      for (int j = 0; j < XI; j += 8)
+        *reinterpret_cast<uint4*>(&XS[blk_off(r, j, XI)]) = make_uint4(
+            pk(xv[j], xv[j + 1]), pk(xv[j + 2], xv[j + 3]), pk(xv[j + 4], xv[j + 5]), pk(xv[j + 6], xv[j + 7]));
+    }
+    to_mma();
+    if (issuer) {  // gate pre-activations: r|z (x Wi + h Wh), x Wi_n, h Wh_n
+      umma::mma_bf16(TRZ, aK(XS, XI, 0), mKc(S.WI, G3, 0, 0), id128, false);
+#pragma unroll
+      for (int ks = 0; ks < HI / 16; ++ks) umma::mma_bf16(TRZ, aK(ACT, HI, ks), mKc(S.WG, G3, ks, 0), id128, true);
+      umma::mma_bf16(TGN, aK(XS, XI, 0), mKc(S.WI, G3, 0, 2 * HI), id64, false);
+#pragma unroll
+      for (int ks = 0; ks < HI / 16; ++ks)
+        umma::mma_bf16(THN, aK(ACT, HI, ks), mKc(S.WG, G3, ks, 2 * HI), id64, ks > 0);
+      umma::commit(&S.bar[g]);
+    }
+    wait();
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {  // h' = n + z (h - n), units 32 hh + 16 c .. + 15
+      const int u0 = 32 * hh + 16 * c;
+      float gr[16], gz[16], gn[16], hn[16];
+      umma::tmem_ld16(TRZ + lanes + u0, gr);
+      umma::tmem_ld16(TRZ + lanes + HI + u0, gz);
+      umma::tmem_ld16(TGN + lanes + u0, gn);
+      umma::tmem_ld16(THN + lanes + u0, hn);
+      float o[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int u = u0 + j;
+        const float rr = sigm_f(gr[j] + S.bg[u]), zz = sigm_f(gz[j] + S.bg[HI + u]);
+        const float nn = tanh_f(gn[j] + S.bg[2 * HI + u] + rr * (hn[j] + S.bg[3 * HI + u]));
+        o[j] = nn + zz * (hp[16 * c + j] - nn);
+      }
+      if (valid) {
+        float4* dst = reinterpret_cast<float4*>(ga.h_out + row * HI + u0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dst[j] = make_float4(o[4 * j], o[4 * j + 1], o[4 * j + 2], o[4 * j + 3]);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; j += 8)
+        *reinterpret_cast<uint4*>(&ACT[blk_off(r, u0 + j, HI)]) =
+            make_uint4(pk(o[j], o[j + 1]), pk(o[j + 2], o[j + 3]), pk(o[j + 4], o[j + 5]), pk(o[j + 6], o[j + 7]));
+    }
+    to_mma();
+    if (issuer) {  // A1 = tanh(h' W0 + b0)
+#pragma unroll
+      for (int ks = 0; ks < HI / 16; ++ks) umma::mma_bf16(TRZ, aK(ACT, HI, ks), mKc(S.W0, HW, ks, 0), id128, ks > 0);
+      umma::commit(&S.bar[g]);
+    }
+    wait();
+    epi_tanh(S.b0);
+    to_mma();
+    if (issuer) {
+#pragma unroll
+      for (int ks = 0; ks < HW / 16; ++ks) umma::mma_bf16(TRZ, aK(ACT, HW, ks), mKc(S.W1, HW, ks, 0), id128, ks > 0);
+      umma::commit(&S.bar[g]);
+    }
+    wait();
+    epi_tanh(S.b1);
+    to_mma();
+    if (issuer) {
+#pragma unroll
+      for (int ks = 0; ks < HW / 16; ++ks) umma::mma_bf16(TRZ, aK(ACT, HW, ks), mKc(S.W2, HW, ks, 0), id128, ks > 0);
+      umma::commit(&S.bar[g]);
+    }
+    wait();
+    epi_tanh(S.b2);
+    to_mma();
+    if (issuer) {  // heads: y = z Wh + bh (N = 16)
+#pragma unroll
+      for (int ks = 0; ks < HW / 16; ++ks) umma::mma_bf16(TRZ, aK(ACT, HW, ks), mKc(S.WH, HY, ks, 0), id16, ks > 0);
+      umma::commit(&S.bar[g]);
+    }
+    wait();
+    if (hh == 0) {
+      float v[16];
+      umma::tmem_ld16(TRZ + lanes, v);
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < HY / 2; ++j)
+          if (j < n_out) y[row * n_out + j] = v[j] + S.bh[j];
+      }
+    }
+    umma::fence_before();
+    group_sync(g);  // the next tile overwrites ACT / XS and the accumulators
+    umma::fence_after();
+  }
+  umma::fence_before();
+  __syncthreads();
+  if (warp == 0) umma::tmem_free(S.tbase, 512);
 }
 
 // ---- the GRU cell's backward (q/nets.py:107-132 differentiated):
@@ -794,8 +927,8 @@ __global__ void __launch_bounds__(PT, 1)
   if (warp == 0) umma::tmem_free(T0, 512);
 }
 
-template <bool BWD, bool GRU = false>
-int launch_trunk(int64_t n, int32_t n_out, GruArgs ga, const float* h, const float* dy, const float* W0, const float* b0,
+template <bool BWD>
+int launch_trunk(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
                  const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                  const float* bh, float* y, float* dh, float* gW0, float* gb0, float* gW1, float* gb1,
                  float* gW2, float* gb2, float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm,
@@ -805,12 +938,12 @@ int launch_trunk(int64_t n, int32_t n_out, GruArgs ga, const float* h, const flo
   if (BWD && (!work || work_floats < (int64_t)n_sm * TK_P)) return QS_ERR_BAD_ARGUMENT;
   const size_t smem = sizeof(PolSmem);
   static_assert(sizeof(PolSmem) <= 227 * 1024, "shared memory");
-  if (cudaFuncSetAttribute(k_policy_trunk<BWD, GRU>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(k_policy_trunk<BWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_policy_trunk<BWD, GRU><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, ga, h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
+  k_policy_trunk<BWD><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
                                                                      dh, work);
   if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
   if (!BWD) return QS_OK;
@@ -835,7 +968,7 @@ int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W
                         const float* b1, const float* W2, const float* b2, const float* Wh, const float* bh, float* y,
                         int32_t n_sm, void* stream) {
   if (!y || !h) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<false>(n, n_out, GruArgs{}, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
+  return launch_trunk<false>(n, n_out, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, n_sm, stream);
 }
 
@@ -844,7 +977,7 @@ int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* d
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
                         float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream) {
   if (!h || !dy || !dh) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<true>(n, n_out, GruArgs{}, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
+  return launch_trunk<true>(n, n_out, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
                             gW1, gb1, gW2, gb2, gWh, gbh, work, work_floats, n_sm, stream);
 }
 
@@ -853,10 +986,17 @@ int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, co
                       const float* b0, const float* W1, const float* b1, const float* W2, const float* b2,
                       const float* Wh, const float* bh, float* h_out, float* y, int32_t n_sm, void* stream) {
   if (!y || !h_out || !x || !h || n_in < 1 || n_in > XI) return QS_ERR_BAD_ARGUMENT;
+  if (n <= 0) return QS_OK;
+  if (n_out < 1 || n_out > 8 || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
   const GruArgs ga{n_in, x, h, Wi, bi, Wh_g, bh_g, h_reset, h_out};
-  return launch_trunk<false, true>(n, n_out, ga, nullptr, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr,
-                                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
-                                   n_sm, stream);
+  const size_t smem = sizeof(Fwd2Smem);
+  static_assert(sizeof(Fwd2Smem) <= 227 * 1024, "shared memory");
+  if (cudaFuncSetAttribute(k_policy_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return QS_ERR_LAUNCH;
+  const int64_t npairs = ((n + TR - 1) / TR + 1) / 2;
+  const int grid = (int)(npairs < n_sm ? npairs : n_sm);
+  k_policy_fwd2<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, ga, W0, b0, W1, b1, W2, b2, Wh, bh, y);
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 
 int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const uint8_t* h_reset,
