@@ -299,10 +299,19 @@ int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale,
 int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W0, const float* b0, const float* W1,
                         const float* b1, const float* W2, const float* b2, const float* Wh, const float* bh, float* y,
                         int32_t n_sm, void* stream);
+/* The bf16 weight image the kernels below can stage with bulk copies instead
+ * of converting the fp32 weights in every CTA: W0 | W1 | W2 | Wh | Wi | Wh_g in
+ * the kernels' blocked operand layout, qs_policy_image_bytes() bytes, 16-byte
+ * aligned.  Build it once per set of weights (e.g. per rollout). */
+int64_t qs_policy_image_bytes(void);
+int qs_policy_pack_image(int32_t n_in, int32_t n_out, const float* Wi, const float* Wh_g, const float* W0,
+                         const float* W1, const float* W2, const float* Wh, void* w_image, void* stream);
 /* Its backward: given dL/dy (n, n_out), recomputes the forward per tile,
  * writes dL/dh (n, 64) and every weight / bias gradient (same shapes as the
- * parameters; overwritten, not accumulated). */
-int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
+ * parameters; overwritten, not accumulated).  w_image: NULL, or the image of
+ * the same weights. */
+int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const void* w_image, const float* h, const float* dy,
+                        const float* W0, const float* b0,
                         const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
                         float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream);
@@ -310,14 +319,16 @@ int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* d
  * r|z|n) fused in front of the trunk: h_out (n, 64) = GRU(x (n, n_in), h'),
  * y = trunk + heads of h_out, where h' = h with the rows h_reset[i] != 0
  * zeroed (the trainer's episode-reset mask; h_reset may be NULL).  n_in <= 16. */
-int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, const float* h, const uint8_t* h_reset,
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const void* w_image, const float* x, const float* h,
+                      const uint8_t* h_reset,
                       const float* Wi, const float* bi, const float* Wh_g, const float* bh_g, const float* W0,
                       const float* b0, const float* W1, const float* b1, const float* W2, const float* b2,
                       const float* Wh, const float* bh, float* h_out, float* y, int32_t n_sm, void* stream);
 /* The GRU cell's backward for dL/dh_out = dh_out_a + dh_out_b (b may be
  * NULL): writes dx (n, n_in), dh (n, 64; 0 on h_reset rows) and gWi, gbi,
  * gWh_g, gbh_g (overwritten). */
-int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const uint8_t* h_reset,
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float* x, const float* h,
+                      const uint8_t* h_reset,
                       const float* dh_out_a, const float* dh_out_b, const float* Wi, const float* bi,
                       const float* Wh_g, const float* bh_g, float* dx, float* dh, float* gWi, float* gbi,
                       float* gWh_g, float* gbh_g, float* work, int64_t work_floats, int32_t n_sm, void* stream);

@@ -349,6 +349,19 @@ QS_D void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint
       : "memory");
 }
 
+// several bulk copies completing on one barrier: arm once with the total
+QS_D void tma_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+QS_D void tma_copy_1d(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // per-thread asynchronous global -> shared copies (LDGSTS): no register is held
 // while the data is in flight; completion is tracked per thread by groups
 QS_D void cp_async16(void* dst_smem, const void* src) {

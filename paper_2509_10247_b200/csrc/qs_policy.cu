@@ -52,6 +52,20 @@ constexpr int64_t TK_W0 = 0, TK_B0 = TK_W0 + HI * HW, TK_W1 = TK_B0 + HW, TK_B1 
 // ... and the GRU backward's
 constexpr int64_t GK_WI = 0, GK_BI = GK_WI + XI * G3, GK_WG = GK_BI + G3, GK_BG = GK_WG + HI * G3,
                   GK_P = (GK_BG + G3 + 31) / 32 * 32;
+// the bf16 weight image (qs_policy_pack_image): W0 | W1 | W2 | WH | WI | WG, each
+// in the blocked operand layout -- byte for byte the kernels' shared-memory
+// weight section, so a CTA stages it with bulk copies instead of converting
+constexpr int IMG_W0 = 0, IMG_W1 = IMG_W0 + HI * HW, IMG_W2 = IMG_W1 + HW * HW, IMG_WH = IMG_W2 + HW * HW,
+              IMG_WI = IMG_WH + HW * HY, IMG_WG = IMG_WI + XI * G3, IMG_N = IMG_WG + HI * G3;  // bf16 elements
+// one thread: bulk-copy `bytes` of the image (from element `off`) to smem, in <= 32 KB pieces
+QS_D void load_image(void* dst, const __nv_bfloat16* img, int off, int elems, uint64_t* bar) {
+  const uint32_t bytes = (uint32_t)elems * 2u;
+  tma_expect(bar, bytes);
+  const char* src = reinterpret_cast<const char*>(img + off);
+  char* d = reinterpret_cast<char*>(dst);
+  for (uint32_t o = 0; o < bytes; o += 32768u)
+    tma_copy_1d(d + o, src + o, bytes - o < 32768u ? bytes - o : 32768u, bar);
+}
 
 QS_D float tanh_f(float x) {
   float y;
@@ -130,7 +144,7 @@ struct PolSmem {
   __nv_bfloat16 DY[TR * HY];   // dL/dy (8 columns), column 15 = 1
   float b0[HW], b1[HW], b2[HW], bh[HY];
   float dbh[4][HY];             // per-warp dL/dbh sums (warps 0-3)
-  uint64_t bar;
+  uint64_t bar, wbar;
   uint32_t tbase;
 };
 
@@ -143,7 +157,8 @@ struct GruArgs {  // the GRU cell of the forward (k_policy_fwd2)
 
 template <bool BWD>
 __global__ void __launch_bounds__(PT, 1)
-    k_policy_trunk(int64_t N, int n_out, const float* __restrict__ h, const float* __restrict__ dy,
+    k_policy_trunk(int64_t N, int n_out, const __nv_bfloat16* __restrict__ img, const float* __restrict__ h,
+                   const float* __restrict__ dy,
                    const float* __restrict__ W0, const float* __restrict__ b0, const float* __restrict__ W1,
                    const float* __restrict__ b1, const float* __restrict__ W2, const float* __restrict__ b2,
                    const float* __restrict__ Wh, const float* __restrict__ bh, float* __restrict__ y,
@@ -154,12 +169,20 @@ __global__ void __launch_bounds__(PT, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 32 * (warp & 3) + lane, q = warp >> 2, cq = 32 * q;
   // ---- weights (bf16, blocked) and biases
-  stage_w<HW>(W0, HI, HI, S.W0, tid);
-  stage_w<HW>(W1, HW, HW, S.W1, tid);
-  stage_w<HW>(W2, HW, HW, S.W2, tid);
-  for (int i = tid; i < HW * HY; i += PT) {
-    const int k = i / HY, n = i % HY;  // Wh (128, n_out) row-major, zero-padded to 16 columns
-    S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+  if (img) {  // pre-converted image: W0 | W1 | W2 | WH are the first members of PolSmem
+    if (tid == 0) {
+      mbar_init(&S.wbar, 1);
+      fence_barrier_init();
+      load_image(S.W0, img, IMG_W0, IMG_WI - IMG_W0, &S.wbar);
+    }
+  } else {
+    stage_w<HW>(W0, HI, HI, S.W0, tid);
+    stage_w<HW>(W1, HW, HW, S.W1, tid);
+    stage_w<HW>(W2, HW, HW, S.W2, tid);
+    for (int i = tid; i < HW * HY; i += PT) {
+      const int k = i / HY, n = i % HY;  // Wh (128, n_out) row-major, zero-padded to 16 columns
+      S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+    }
   }
   for (int i = tid; i < HW; i += PT) {
     S.b0[i] = b0[i];
@@ -175,6 +198,7 @@ __global__ void __launch_bounds__(PT, 1)
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+  if (img) mbar_wait(&S.wbar, 0);  // (initialised before the barrier above)
   const uint32_t T0 = S.tbase;
   // TMEM: tile GEMM [0,128); dW2 [128,256); dW1 [256,384); dW0^T [384,448);
   // dWh [448,464); db2 [464,480); db1 [480,496); db0 [496,512)
@@ -475,14 +499,15 @@ struct Fwd2Smem {
   __nv_bfloat16 ACT[2][TR * HW];  // per group: h (prev, bf16) -> h' -> A1 -> A2 -> z
   __nv_bfloat16 XS[2][TR * XI];   // per group: the input rows
   float b0[HW], b1[HW], b2[HW], bh[HY], bg[4 * HI];
-  uint64_t bar[2];
+  uint64_t bar[2], wbar;
   uint32_t tbase;
 };
 
 QS_D void group_sync(int g) { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); }
 
 __global__ void __launch_bounds__(PT, 1)
-    k_policy_fwd2(int64_t N, int n_out, GruArgs ga, const float* __restrict__ W0, const float* __restrict__ b0,
+    k_policy_fwd2(int64_t N, int n_out, const __nv_bfloat16* __restrict__ img, GruArgs ga,
+                  const float* __restrict__ W0, const float* __restrict__ b0,
                   const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ W2,
                   const float* __restrict__ b2, const float* __restrict__ Wh, const float* __restrict__ bh,
                   float* __restrict__ y) {
@@ -492,14 +517,22 @@ __global__ void __launch_bounds__(PT, 1)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = warp >> 3, gw = warp & 7;          // group, warp within the group
   const int r = 32 * (gw & 3) + lane, hh = gw >> 2;  // tile row (TMEM lane), column half
-  stage_w<HW>(W0, HI, HI, S.W0, tid);
-  stage_w<HW>(W1, HW, HW, S.W1, tid);
-  stage_w<HW>(W2, HW, HW, S.W2, tid);
-  stage_w<G3>(ga.Wi, XI, ga.n_in, S.WI, tid);
-  stage_w<G3>(ga.Wg, HI, HI, S.WG, tid);
-  for (int i = tid; i < HW * HY; i += PT) {
-    const int k = i / HY, n = i % HY;
-    S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+  if (img) {  // pre-converted image == the weight section of Fwd2Smem
+    if (tid == 0) {
+      mbar_init(&S.wbar, 1);
+      fence_barrier_init();
+      load_image(S.W0, img, 0, IMG_N, &S.wbar);
+    }
+  } else {
+    stage_w<HW>(W0, HI, HI, S.W0, tid);
+    stage_w<HW>(W1, HW, HW, S.W1, tid);
+    stage_w<HW>(W2, HW, HW, S.W2, tid);
+    stage_w<G3>(ga.Wi, XI, ga.n_in, S.WI, tid);
+    stage_w<G3>(ga.Wg, HI, HI, S.WG, tid);
+    for (int i = tid; i < HW * HY; i += PT) {
+      const int k = i / HY, n = i % HY;
+      S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+    }
   }
   for (int i = tid; i < HW; i += PT) {
     S.b0[i] = b0[i];
@@ -518,6 +551,7 @@ __global__ void __launch_bounds__(PT, 1)
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+  if (img) mbar_wait(&S.wbar, 0);
   // this group's TMEM: r|z [0,128) (then the trunk accumulator), x Wi_n [128,192), h Wh_n [192,256)
   const uint32_t TB = S.tbase + 256 * g, TRZ = TB, TGN = TB + 128, THN = TB + 192;
   const uint32_t lanes = umma::taddr(0, 32 * (gw & 3), 0);
@@ -688,12 +722,12 @@ struct GruSmem {
   __nv_bfloat16 GRZ[TR * HW];  // [rows][dar | daz]
   __nv_bfloat16 GN[TR * HW];   // [rows][dan | dan r]
   float bg[4 * HI];
-  uint64_t bar;
+  uint64_t bar, wbar;
   uint32_t tbase;
 };
 
 __global__ void __launch_bounds__(PT, 1)
-    k_gru_bwd(int64_t N, int n_in, const float* __restrict__ x, const float* __restrict__ hp,
+    k_gru_bwd(int64_t N, int n_in, const __nv_bfloat16* __restrict__ img, const float* __restrict__ x, const float* __restrict__ hp,
               const uint8_t* __restrict__ rst, const float* __restrict__ dha, const float* __restrict__ dhb, const float* __restrict__ Wi,
               const float* __restrict__ bi, const float* __restrict__ Wg, const float* __restrict__ bgv,
               float* __restrict__ dx, float* __restrict__ dhp, float* __restrict__ work) {
@@ -703,8 +737,16 @@ __global__ void __launch_bounds__(PT, 1)
   constexpr int BC = 96;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = 32 * (warp & 3) + lane, q = warp >> 2;
-  stage_w<G3>(Wi, XI, n_in, S.WI, tid);
-  stage_w<G3>(Wg, HI, HI, S.WG, tid);
+  if (img) {  // WI | WG: the image's tail, the first members of GruSmem
+    if (tid == 0) {
+      mbar_init(&S.wbar, 1);
+      fence_barrier_init();
+      load_image(S.WI, img, IMG_WI, IMG_N - IMG_WI, &S.wbar);
+    }
+  } else {
+    stage_w<G3>(Wi, XI, n_in, S.WI, tid);
+    stage_w<G3>(Wg, HI, HI, S.WG, tid);
+  }
   for (int i = tid; i < 4 * HI; i += PT) S.bg[i] = i < 2 * HI ? bi[i] + bgv[i] : i < 3 * HI ? bi[i] : bgv[i - HI];
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
@@ -714,6 +756,7 @@ __global__ void __launch_bounds__(PT, 1)
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+  if (img) mbar_wait(&S.wbar, 0);
   const uint32_t T0 = S.tbase;
   // TMEM: r|z [0,128), x Wi_n [128,192), h Wh_n [192,256) -- then dx [0,16),
   // dgh Wh^T [64,128); dW r|z [256,352); dW n [352,448)
@@ -928,7 +971,7 @@ __global__ void __launch_bounds__(PT, 1)
 }
 
 template <bool BWD>
-int launch_trunk(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
+int launch_trunk(int64_t n, int32_t n_out, const void* img, const float* h, const float* dy, const float* W0, const float* b0,
                  const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                  const float* bh, float* y, float* dh, float* gW0, float* gb0, float* gW1, float* gb1,
                  float* gW2, float* gb2, float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm,
@@ -943,7 +986,8 @@ int launch_trunk(int64_t n, int32_t n_out, const float* h, const float* dy, cons
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_policy_trunk<BWD><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
+  k_policy_trunk<BWD><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out,
+                                                                reinterpret_cast<const __nv_bfloat16*>(img), h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
                                                                      dh, work);
   if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
   if (!BWD) return QS_OK;
@@ -955,9 +999,51 @@ int launch_trunk(int64_t n, int32_t n_out, const float* h, const float* dy, cons
   return red::sum_partials(work, grid, TK_P, sg, (cudaStream_t)stream);
 }
 
+__global__ void k_pack_image(int n_in, int n_out, const float* __restrict__ Wi, const float* __restrict__ Wg,
+                             const float* __restrict__ W0, const float* __restrict__ W1, const float* __restrict__ W2,
+                             const float* __restrict__ Wh, __nv_bfloat16* __restrict__ img) {
+  using umma::blk_off;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < IMG_N; i += gridDim.x * blockDim.x) {
+    float v;
+    if (i < IMG_W1) {
+      const int e = i - IMG_W0;  // element e of the blocked W0: find (k, n) by inverting blk_off
+      const int k = e / HW, n = e % HW;
+      v = W0[k * HW + n];
+      img[IMG_W0 + blk_off(k, n, HW)] = __float2bfloat16_rn(v);
+    } else if (i < IMG_W2) {
+      const int e = i - IMG_W1, k = e / HW, n = e % HW;
+      img[IMG_W1 + blk_off(k, n, HW)] = __float2bfloat16_rn(W1[e]);
+    } else if (i < IMG_WH) {
+      const int e = i - IMG_W2, k = e / HW, n = e % HW;
+      img[IMG_W2 + blk_off(k, n, HW)] = __float2bfloat16_rn(W2[e]);
+    } else if (i < IMG_WI) {
+      const int e = i - IMG_WH, k = e / HY, n = e % HY;
+      img[IMG_WH + blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+    } else if (i < IMG_WG) {
+      const int e = i - IMG_WI, k = e / G3, n = e % G3;
+      img[IMG_WI + blk_off(k, n, G3)] = __float2bfloat16_rn(k < n_in ? Wi[k * G3 + n] : 0.f);
+    } else {
+      const int e = i - IMG_WG, k = e / G3, n = e % G3;
+      img[IMG_WG + blk_off(k, n, G3)] = __float2bfloat16_rn(Wg[e]);
+    }
+  }
+}
+
 }  // namespace
 
 extern "C" {
+
+int64_t qs_policy_image_bytes(void) { return (int64_t)IMG_N * 2; }
+
+int qs_policy_pack_image(int32_t n_in, int32_t n_out, const float* Wi, const float* Wh_g, const float* W0,
+                         const float* W1, const float* W2, const float* Wh, void* w_image, void* stream) {
+  if (!Wi || !Wh_g || !W0 || !W1 || !W2 || !Wh || !w_image || n_in < 1 || n_in > XI || n_out < 1 || n_out > 8)
+    return QS_ERR_BAD_ARGUMENT;
+  if (reinterpret_cast<uintptr_t>(w_image) % 16) return QS_ERR_BAD_ARGUMENT;
+  k_pack_image<<<(IMG_N + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n_in, n_out, Wi, Wh_g, W0, W1, W2, Wh,
+                                                                     reinterpret_cast<__nv_bfloat16*>(w_image));
+  return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
+}
 
 int64_t qs_policy_work_floats(int32_t which, int32_t n_sm) {
   if (n_sm < 1) return -1;
@@ -968,20 +1054,22 @@ int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W
                         const float* b1, const float* W2, const float* b2, const float* Wh, const float* bh, float* y,
                         int32_t n_sm, void* stream) {
   if (!y || !h) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<false>(n, n_out, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
+  return launch_trunk<false>(n, n_out, nullptr, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, n_sm, stream);
 }
 
-int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const float* h, const float* dy, const float* W0, const float* b0,
+int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const void* w_image, const float* h, const float* dy,
+                        const float* W0, const float* b0,
                         const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
                         float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream) {
   if (!h || !dy || !dh) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<true>(n, n_out, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
+  return launch_trunk<true>(n, n_out, w_image, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
                             gW1, gb1, gW2, gb2, gWh, gbh, work, work_floats, n_sm, stream);
 }
 
-int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, const float* h, const uint8_t* h_reset,
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const void* w_image, const float* x, const float* h,
+                      const uint8_t* h_reset,
                       const float* Wi, const float* bi, const float* Wh_g, const float* bh_g, const float* W0,
                       const float* b0, const float* W1, const float* b1, const float* W2, const float* b2,
                       const float* Wh, const float* bh, float* h_out, float* y, int32_t n_sm, void* stream) {
@@ -995,11 +1083,13 @@ int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const float* x, co
     return QS_ERR_LAUNCH;
   const int64_t npairs = ((n + TR - 1) / TR + 1) / 2;
   const int grid = (int)(npairs < n_sm ? npairs : n_sm);
-  k_policy_fwd2<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, ga, W0, b0, W1, b1, W2, b2, Wh, bh, y);
+  k_policy_fwd2<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, reinterpret_cast<const __nv_bfloat16*>(w_image),
+                                                          ga, W0, b0, W1, b1, W2, b2, Wh, bh, y);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 
-int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, const uint8_t* h_reset,
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float* x, const float* h,
+                      const uint8_t* h_reset,
                       const float* dh_out_a,
                       const float* dh_out_b, const float* Wi, const float* bi, const float* Wh_g, const float* bh_g,
                       float* dx, float* dh, float* gWi, float* gbi, float* gWh_g, float* gbh_g, float* work,
@@ -1012,7 +1102,8 @@ int qs_policy_gru_bwd(int64_t n, int32_t n_in, const float* x, const float* h, c
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_gru_bwd<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_in, x, h, h_reset, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
+  k_gru_bwd<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_in, reinterpret_cast<const __nv_bfloat16*>(w_image), x,
+                                                      h, h_reset, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
                                                       work);
   if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
   red::Segs sg{{gWi, gbi, gWh_g, gbh_g}, {GK_WI, GK_BI, GK_WG, GK_BG}, {(int64_t)n_in * G3, G3, HI * G3, G3}, 4, false};

@@ -225,7 +225,7 @@ class _TrunkFn(torch.autograd.Function):
         grads = [torch.empty_like(t) for t in (W0, b0, W1, b1, W2, b2, Wh)]
         gbh = torch.empty(n_out, dtype=torch.float32, device=h.device)
         work = _work(0, ctx.n_sm, h.device)
-        L.check(L.lib().qs_policy_trunk_bwd(N, n_out, L.ptr(h), L.ptr(gy), *[L.ptr(t) for t in
+        L.check(L.lib().qs_policy_trunk_bwd(N, n_out, None, L.ptr(h), L.ptr(gy), *[L.ptr(t) for t in
                                                                               (W0, b0, W1, b1, W2, b2, Wh)],
                                             L.ptr(dh), *[L.ptr(t) for t in grads], L.ptr(gbh), L.ptr(work),
                                             work.numel(), ctx.n_sm,
@@ -255,15 +255,18 @@ class _PolicyStepFn(torch.autograd.Function):
         Wh = torch.cat([v["Wmu"].view(128, A), v["Wsig"].view(128, A)], 1).contiguous()
         bh = torch.cat([v["bmu"], v["bsig"]])
         N = x.shape[0]
+        img = getattr(wp, "_qs_image", None)  # bf16 weight image built with the pack (once per rollout)
+        if img is None:
+            img = _policy_image(v, n_in, A, Wh)
         h_out = torch.empty(N, h.shape[1], dtype=torch.float32, device=x.device)
         y = torch.empty(N, 2 * A, dtype=torch.float32, device=x.device)
         n_sm = torch.cuda.get_device_properties(x.device).multi_processor_count
-        L.check(L.lib().qs_policy_gru_fwd(N, n_in, 2 * A, L.ptr(x), L.ptr(h), L.ptr(rs),
+        L.check(L.lib().qs_policy_gru_fwd(N, n_in, 2 * A, L.ptr(img), L.ptr(x), L.ptr(h), L.ptr(rs),
                                           *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg", "W0", "b0", "W1", "b1", "W2",
                                                                   "b2")],
                                           L.ptr(Wh), L.ptr(bh), L.ptr(h_out), L.ptr(y), n_sm,
                                           L.stream_handle(x.device)), "qs_policy_gru_fwd")
-        ctx.save_for_backward(x, h, rs, h_out, wp, Wh)
+        ctx.save_for_backward(x, h, rs, h_out, wp, Wh, img)
         ctx.n_sm, ctx.A, ctx.n_in = n_sm, A, n_in
         return h_out, y
 
@@ -271,7 +274,7 @@ class _PolicyStepFn(torch.autograd.Function):
     def backward(ctx, g_h, g_y):
         from paper_2509_10247_b200 import _lib as L
 
-        x, h, rs, h_out, wp, Wh = ctx.saved_tensors
+        x, h, rs, h_out, wp, Wh, img = ctx.saved_tensors
         N, A, n_in = x.shape[0], ctx.A, ctx.n_in
         dev, st = x.device, L.stream_handle(x.device)
         offs = _pack_offsets(n_in, A)
@@ -284,14 +287,14 @@ class _PolicyStepFn(torch.autograd.Function):
         gWh = torch.empty(128, 2 * A, dtype=torch.float32, device=dev)
         gbh = torch.empty(2 * A, dtype=torch.float32, device=dev)
         work = _work(0, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_trunk_bwd(N, 2 * A, L.ptr(h_out), L.ptr(g_y),
+        L.check(L.lib().qs_policy_trunk_bwd(N, 2 * A, L.ptr(img), L.ptr(h_out), L.ptr(g_y),
                                             *[L.ptr(v[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2")], L.ptr(Wh),
                                             L.ptr(dh_t), *[L.ptr(gv[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2")],
                                             L.ptr(gWh), L.ptr(gbh), L.ptr(work), work.numel(), ctx.n_sm, st),
                 "qs_policy_trunk_bwd")
         dx, dh = torch.empty_like(x), torch.empty_like(h)
         work = _work(1, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(x), L.ptr(h), L.ptr(rs), L.ptr(dh_t), L.ptr(g_h),
+        L.check(L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(img), L.ptr(x), L.ptr(h), L.ptr(rs), L.ptr(dh_t), L.ptr(g_h),
                                           *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg")], L.ptr(dx), L.ptr(dh),
                                           *[L.ptr(gv[k]) for k in ("Wi", "bi", "Wg", "bg")], L.ptr(work),
                                           work.numel(), ctx.n_sm, st), "qs_policy_gru_bwd")
@@ -300,6 +303,18 @@ class _PolicyStepFn(torch.autograd.Function):
         gv["bmu"].copy_(gbh[:A])
         gv["bsig"].copy_(gbh[A:])
         return dx, dh, None, gw, None, None
+
+
+def _policy_image(v, n_in, A, Wh):
+    """The kernels' bf16 weight image (qs_policy_pack_image) of the packed slices v."""
+    from paper_2509_10247_b200 import _lib as L
+
+    dev = Wh.device
+    img = torch.empty(L.lib().qs_policy_image_bytes() // 2, dtype=torch.bfloat16, device=dev)
+    L.check(L.lib().qs_policy_pack_image(n_in, 2 * A, L.ptr(v["Wi"]), L.ptr(v["Wg"]), L.ptr(v["W0"]),
+                                         L.ptr(v["W1"]), L.ptr(v["W2"]), L.ptr(Wh), L.ptr(img),
+                                         L.stream_handle(dev)), "qs_policy_pack_image")
+    return img
 
 
 def _pack_offsets(n_in, A, H=64, W=128):
@@ -372,7 +387,14 @@ class PolicyNet(torch.nn.Module):
         if self.gru is None or self.hidden != 64 or tuple(self.arch.mlp) != (128, 128) or \
                 2 * self.arch.action_dim > 8:
             return None
-        return torch.cat([p.reshape(-1) for p in self._fused_params()])
+        wp = torch.cat([p.reshape(-1) for p in self._fused_params()])
+        if wp.is_cuda:  # the kernels' bf16 weight image, built once with the pack
+            with torch.no_grad():
+                A = self.arch.action_dim
+                v = {k: wp[o:o + n] for k, (o, n) in _pack_offsets(self.gru.Wi.shape[0], A).items()}
+                Wh = torch.cat([v["Wmu"].view(128, A), v["Wsig"].view(128, A)], 1).contiguous()
+                wp._qs_image = _policy_image(v, self.gru.Wi.shape[0], A, Wh)
+        return wp
 
     def initial_hidden(self, batch, device=None):
         return torch.zeros(batch, self.hidden, device=device) if self.gru is not None else None

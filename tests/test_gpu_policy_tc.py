@@ -34,7 +34,7 @@ def test_policy_trunk_fwd_bwd_match_autograd(n_out, N):
     grads = [torch.full_like(p, 7.0) for p in params]  # overwritten, not accumulated
     dh = torch.empty_like(h)
     work = torch.empty(L.lib().qs_policy_work_floats(0, n_sm), device="cuda")
-    L.check(L.lib().qs_policy_trunk_bwd(N, n_out, *_ptrs(h, dy, W0, b0, W1, b1, W2, b2, Wh, dh, grads[0], grads[1],
+    L.check(L.lib().qs_policy_trunk_bwd(N, n_out, None, *_ptrs(h, dy, W0, b0, W1, b1, W2, b2, Wh, dh, grads[0], grads[1],
                                                            grads[2], grads[3], grads[4], grads[5], grads[6],
                                                            grads[7], work), work.numel(), n_sm, L.stream_handle()),
             "bwd")
@@ -105,16 +105,23 @@ def test_policy_gru_fwd_bwd_match_autograd(n_in, N):
     reset = (torch.rand(N, generator=g) < 0.1).cuda()  # rows whose carried h restarts at 0
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     h_out, y = torch.empty(N, 64, device="cuda"), torch.empty(N, 6, device="cuda")
-    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, *_ptrs(x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2, Wh, bh,
-                                                          h_out, y), n_sm, L.stream_handle()), "gru fwd")
+    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, None, *_ptrs(x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2,
+                                                                Wh, bh, h_out, y), n_sm, L.stream_handle()), "gru fwd")
+    # the same from the pre-converted bf16 weight image (bulk-copied by every CTA): same bits
+    img = torch.empty(L.lib().qs_policy_image_bytes() // 2, dtype=torch.bfloat16, device="cuda")
+    L.check(L.lib().qs_policy_pack_image(n_in, 6, *_ptrs(Wi, Wg, W0, W1, W2, Wh, img), L.stream_handle()), "image")
+    h_out2, y2 = torch.empty_like(h_out), torch.empty_like(y)
+    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, *_ptrs(img, x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2,
+                                                          Wh, bh, h_out2, y2), n_sm, L.stream_handle()), "gru fwd img")
+    assert torch.equal(h_out, h_out2) and torch.equal(y, y2)
     dx, dh = torch.empty_like(x), torch.empty_like(h)
     gr = [torch.full_like(t, 7.0) for t in (Wi, bi, Wg, bg)]  # overwritten, not accumulated
     work = torch.empty(L.lib().qs_policy_work_floats(1, n_sm), device="cuda")
-    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr, work),
+    L.check(L.lib().qs_policy_gru_bwd(N, n_in, None, *_ptrs(x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr, work),
                                       work.numel(), n_sm, L.stream_handle()), "gru bwd")
-    # reproducible: a second pass gives the same bits (per-CTA partials, fixed-order sum)
+    # reproducible: a second pass (from the weight image) gives the same bits
     gr2 = [torch.zeros_like(t) for t in (Wi, bi, Wg, bg)]
-    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr2, work),
+    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(img, x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr2, work),
                                       work.numel(), n_sm, L.stream_handle()), "gru bwd")
     assert all(torch.equal(a, b) for a, b in zip(gr, gr2))
     leaves = [t.clone().requires_grad_(True) for t in (x, h, Wi, bi, Wg, bg)]
