@@ -605,6 +605,10 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
   uint8_t* hitm_row = hitm && !GRAD ? hitm + row * rc.n_rays : nullptr;
   const float* g_row = GRAD ? g_depth + row * rc.n_rays : nullptr;
   V3 gacc = v3(0.f, 0.f, 0.f);  // GRAD: this lane's share of d loss / d origin
+  // vector stores of a lane's consecutive rays need rows that keep their alignment
+  const bool vec_ok = RPL > 1 && !GRAD && (rc.n_rays % RPL) == 0 &&
+                      (reinterpret_cast<uintptr_t>(out) % (4 * RPL)) == 0 &&
+                      (!hitm || (reinterpret_cast<uintptr_t>(hitm) % RPL) == 0);
   for (int tile = t0 + warp; tile < t1; tile += nwarps) {
     // tile record (12 floats): cone axis xyz, cos, sin | azimuth centre xy, cos, sin of the sector
     const float4 c0 = ld4(tile_cones, 3 * tile), c1 = ld4(tile_cones, 3 * tile + 1);
@@ -758,13 +762,40 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
       }
       continue;
     }
+    float tk[RPL];
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
       if (ground) best[k] = min(best[k], fbits(pos0(gdz * inv[k].z)));  // +inf / NaN / t < 0 drop out
-      if (ray[k] >= 0) {
-        const float t = __uint_as_float(best[k]);
-        out_row[ray[k]] = fminf(t, rc.max_range);
-        if (hitm) hitm_row[ray[k]] = t < rc.max_range ? 1 : 0;
+      tk[k] = __uint_as_float(best[k]);
+    }
+    // the host table gives a lane consecutive rays (sensors._tile_table): one
+    // vector store of the depths and one of the hit bytes
+    bool vec = vec_ok && ray[0] >= 0 && (ray[0] % RPL) == 0;
+#pragma unroll
+    for (int k = 1; k < RPL; ++k) vec = vec && ray[k] == ray[0] + k;
+    if (vec) {
+      if constexpr (RPL == 2) {
+        *reinterpret_cast<float2*>(out_row + ray[0]) =
+            make_float2(fminf(tk[0], rc.max_range), fminf(tk[1], rc.max_range));
+        if (hitm)
+          *reinterpret_cast<uint16_t*>(hitm_row + ray[0]) =
+              (uint16_t)((tk[0] < rc.max_range ? 1u : 0u) | (tk[1] < rc.max_range ? 0x100u : 0u));
+      } else if constexpr (RPL == 4) {
+        *reinterpret_cast<float4*>(out_row + ray[0]) =
+            make_float4(fminf(tk[0], rc.max_range), fminf(tk[1], rc.max_range), fminf(tk[2], rc.max_range),
+                        fminf(tk[3], rc.max_range));
+        if (hitm)
+          *reinterpret_cast<uint32_t*>(hitm_row + ray[0]) =
+              (tk[0] < rc.max_range ? 1u : 0u) | (tk[1] < rc.max_range ? 0x100u : 0u) |
+              (tk[2] < rc.max_range ? 0x10000u : 0u) | (tk[3] < rc.max_range ? 0x1000000u : 0u);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) {
+        if (ray[k] >= 0) {
+          out_row[ray[k]] = fminf(tk[k], rc.max_range);
+          if (hitm) hitm_row[ray[k]] = tk[k] < rc.max_range ? 1 : 0;
+        }
       }
     }
   }

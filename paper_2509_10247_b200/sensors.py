@@ -307,6 +307,13 @@ def _tile_table(sensor, device, width=None):
     else:
         d = sensor.ray_dirs()
         tiles = [list(range(s, min(len(d), s + width))) for s in range(0, len(d), width)]
+    # lane j of the kernel's warp owns slots j, j + 32, ...: order each full
+    # tile so that a lane's rays are consecutive in the image (horizontally
+    # adjacent pixels / consecutive LiDAR rays), so it stores them with one
+    # vector store.  The tile's ray SET (and so its cone) is unchanged.
+    rpl = width // 32
+    if rpl > 1 and LANE_CONSECUTIVE:
+        tiles = [[t[(p % 32) * rpl + p // 32] for p in range(width)] if len(t) == width else t for t in tiles]
     rays = np.full((len(tiles), width), -1, dtype=np.int32)
     # axis xyz, cos/sin(half-angle) | sector centre xy, cos/sin(sector half-width) | pad
     cones = np.zeros((len(tiles), 12))
@@ -415,6 +422,8 @@ TILED = True  # per-warp cone culling (k_raycast_tiled); False selects the until
 # pixel blocks for cameras, 8 azimuths x 16 elevations for LiDARs, the fastest
 # measured, profiles/README.md); QS_TILE_WIDTH overrides it for A/B runs
 TILE_WIDTH = int(os.environ.get("QS_TILE_WIDTH", "0"))
+# give each lane consecutive rays within a tile (vector stores); 0 for A/B runs
+LANE_CONSECUTIVE = os.environ.get("QS_TILE_LANE_ORDER", "1") != "0"
 
 
 def raycast(prims, origins, dirs, max_range: float, chunk_elems: int = 0, device=None):
