@@ -659,6 +659,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
     }
     for (int base = 0; base < tot; base += 32) {
       const int j = base + lane;
+      const uint2 km = kmask[base >> 5];  // (loaded ahead of the cone test that hides its latency)
       bool keep = false;
       if (j < tot) {
         const float4 bj = b_all[j], fj = f_all[j];
@@ -675,8 +676,56 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
       // warp-uniform candidate masks, split by kind (the list is kind-sorted:
       // spheres, boxes, cylinders), so each loop runs one test with no dispatch
       const unsigned m = __ballot_sync(0xffffffffu, keep);
-      const uint2 km = kmask[base >> 5];
       unsigned ms = m & km.x, mb = m & km.y & ~km.x, mc = m & ~km.y;
+      if constexpr (!GRAD && NP > 0) {
+        // software-pipelined candidate loops: the next candidate's record is
+        // read from shared memory while the current one is tested
+        if (ms) {
+          int i = base + __ffs(ms) - 1;
+          ms &= ms - 1;
+          float4 q = r0[i];
+          for (;;) {
+            const int i2 = ms ? base + __ffs(ms) - 1 : i;
+            const float4 qn = r0[i2];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) hit_sphere_p(best[2 * p], best[2 * p + 1], q, rp[p]);
+            if (!ms) break;
+            ms &= ms - 1;
+            q = qn;
+          }
+        }
+        if (mb) {
+          int i = base + __ffs(mb) - 1;
+          mb &= mb - 1;
+          float4 lo = r0[i], hi = r1[i];
+          for (;;) {
+            const int i2 = mb ? base + __ffs(mb) - 1 : i;
+            const float4 lon = r0[i2], hin = r1[i2];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) hit_box_p(best[2 * p], best[2 * p + 1], lo, hi, rp[p]);
+            if (!mb) break;
+            mb &= mb - 1;
+            lo = lon;
+            hi = hin;
+          }
+        }
+        if (mc) {
+          int i = base + __ffs(mc) - 1;
+          mc &= mc - 1;
+          float4 q = r0[i], h = r1[i];
+          for (;;) {
+            const int i2 = mc ? base + __ffs(mc) - 1 : i;
+            const float4 qn = r0[i2], hn = r1[i2];
+#pragma unroll
+            for (int p = 0; p < NP; ++p) hit_cyl_p(best[2 * p], best[2 * p + 1], q, h, rp[p]);
+            if (!mc) break;
+            mc &= mc - 1;
+            q = qn;
+            h = hn;
+          }
+        }
+        continue;
+      }
       while (ms) {
         const int i = base + __ffs(ms) - 1;
         ms &= ms - 1;
