@@ -172,9 +172,19 @@ struct TaskStepFn : public torch::autograd::Function<TaskStepFn> {
   static variable_list forward(AutogradContext* ctx, const at::Tensor& S_in, const at::Tensor& raw,
                                const at::Tensor& cfg_blob, std::vector<at::Tensor> scene,
                                std::vector<at::Tensor> bufs, std::optional<at::Tensor> imu_noise, bool want_cam,
-                               bool strict, int64_t proprio_dim) {
-    // redispatch below autograd: the CUDA kernel for real tensors, the Meta
-    // kernel under FakeTensor tracing
+                               bool strict, int64_t proprio_dim, bool direct) {
+    // direct (the pybind entry, real CUDA tensors): call the CUDA kernel
+    // without a dispatcher round trip; otherwise redispatch below autograd --
+    // the CUDA kernel for real tensors, the fake kernel under tracing
+    if (direct) {
+      auto out = task_step_cuda(cfg_blob, scene, S_in, raw, bufs, imu_noise, want_cam, strict, proprio_dim);
+      ctx->save_for_backward({S_in, raw, bufs[0], bufs[1], bufs[2], out[7]});
+      ctx->saved_data["cfg"] = cfg_blob;
+      ctx->saved_data["scene"] = scene;
+      ctx->mark_non_differentiable(variable_list(out.begin() + 3, out.end()));
+      ctx->set_materialize_grads(false);
+      return out;
+    }
     static auto op = c10::Dispatcher::singleton()
                          .findSchemaOrThrow("quadsim::task_step", "")
                          .typed<std::vector<at::Tensor>(const at::Tensor&, at::TensorList, const at::Tensor&,
@@ -198,7 +208,7 @@ struct TaskStepFn : public torch::autograd::Function<TaskStepFn> {
     const at::Tensor gS = go[0].defined() ? go[0].contiguous() : at::Tensor();
     const at::Tensor gobs = go[1].defined() ? go[1].contiguous() : at::Tensor();
     const at::Tensor gr = go[2].defined() ? go[2].contiguous() : at::Tensor();
-    variable_list grads(9);
+    variable_list grads(10);
     if (!gS.defined() && !gobs.defined() && !gr.defined()) return grads;
     const c10::cuda::CUDAGuard guard(S_in.device());
     const qs_task_cfg& c = cfg_of(ctx->saved_data["cfg"].toTensor());
@@ -230,7 +240,7 @@ std::vector<at::Tensor> task_step_autograd(const at::Tensor& cfg_blob, at::Tenso
                                            const std::optional<at::Tensor>& imu_noise, bool want_cam, bool strict,
                                            int64_t proprio_dim) {
   return TaskStepFn::apply(S_in, raw, cfg_blob, scene.vec(), bufs.vec(), imu_noise, want_cam, strict,
-                           proprio_dim);
+                           proprio_dim, false);
 }
 
 }  // namespace
@@ -254,7 +264,14 @@ PYBIND11_MODULE(_qs_torch_ops, m) {
       [](const at::Tensor& cfg_blob, const std::vector<at::Tensor>& scene, const at::Tensor& S_in,
          const at::Tensor& raw, const std::vector<at::Tensor>& bufs, const std::optional<at::Tensor>& imu_noise,
          bool want_cam, bool strict, int64_t proprio_dim) {
-        return task_step_autograd(cfg_blob, scene, S_in, raw, bufs, imu_noise, want_cam, strict, proprio_dim);
+        // no autograd node when nothing needs a gradient; else the node with a
+        // direct kernel call (no dispatcher round trip either way)
+        if (!(at::GradMode::is_enabled() && (S_in.requires_grad() || raw.requires_grad()))) {
+          at::AutoDispatchBelowADInplaceOrView g;
+          return task_step_cuda(cfg_blob, scene, S_in, raw, bufs, imu_noise, want_cam, strict, proprio_dim);
+        }
+        return TaskStepFn::apply(S_in, raw, cfg_blob, scene, bufs, imu_noise, want_cam, strict, proprio_dim,
+                                 true);
       },
       "quadsim::task_step (autograd path)");
 }

@@ -765,10 +765,13 @@ class FlightTask:
                                 episode=self._meta[:, 1], episode_stride=4, err=self._err, **self._gen_args)
 
     def step(self, raw_action) -> StepOutput:
-        raw = raw_action if isinstance(raw_action, torch.Tensor) else torch.as_tensor(np.asarray(raw_action))
-        raw = raw.to(device=self.device, dtype=torch.float32)
+        raw = raw_action
+        if not (type(raw) is torch.Tensor and raw.dtype is torch.float32 and raw.device == self.device):
+            raw = raw if isinstance(raw, torch.Tensor) else torch.as_tensor(np.asarray(raw))
+            raw = raw.to(device=self.device, dtype=torch.float32)
         self._check_inputs(raw)
-        raw = raw.contiguous()
+        if not raw.is_contiguous():
+            raw = raw.contiguous()
         noise = None
         if self._imu_bias is not None and self.imu_noise_source is not None:
             noise = torch.as_tensor(np.asarray(self.imu_noise_source(self._steps_total)), dtype=torch.float32,
