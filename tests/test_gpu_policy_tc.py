@@ -143,3 +143,42 @@ def test_policy_gru_fwd_bwd_match_autograd(n_in, N):
     assert rel(y, y_ref.detach()) < 2e-2, rel(y, y_ref.detach())
     for name, a, b in zip(["dx", "dh", "Wi", "bi", "Wg", "bg"], [dx, dh, *gr], [t.grad for t in leaves]):
         assert rel(a, b) < 3e-2, (name, rel(a, b))
+
+
+def test_policynet_recurrent_rollout_gradients_match_torch_path():
+    """Four recurrent steps with the hidden state carried (reset mask mid-way,
+    parameters packed once as the trainer does): the fused kernels' rollout
+    loss and every parameter gradient against the torch bf16 path."""
+    import numpy as np
+
+    from paper_2509_10247_b200 import nets
+
+    arch = nets.PolicyArch(proprio_dim=9, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128))
+    pol = nets.PolicyNet(arch, np.random.default_rng(11)).cuda()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    xs = [torch.randn(2048, 9, device="cuda", generator=g) for _ in range(4)]
+    resets = [None, torch.rand(2048, device="cuda", generator=g) < 0.3, None,
+              torch.rand(2048, device="cuda", generator=g) < 0.3]
+
+    def rollout(fused):
+        old = nets.FUSED_TRUNK
+        nets.FUSED_TRUNK = fused
+        try:
+            pol.zero_grad(set_to_none=True)
+            packed = pol.pack_weights() if fused else None
+            h, loss = None, 0.0
+            with torch.autocast("cuda", dtype=torch.bfloat16):
+                for x, rs in zip(xs, resets):
+                    mu, ls, h = pol(x, h=h, h_reset=rs, packed=packed)
+                    loss = loss + (mu - 0.1).square().mean() + 0.2 * ls.mean() + 0.05 * h.square().mean()
+            loss.backward()
+            return float(loss.detach()), {k: p.grad.clone() for k, p in pol.named_parameters()}
+        finally:
+            nets.FUSED_TRUNK = old
+
+    lf, gf = rollout(True)
+    lt, gt = rollout(False)
+    assert abs(lf - lt) < 2e-2 * abs(lt) + 1e-4, (lf, lt)
+    for k in gt:
+        d = float((gf[k] - gt[k]).abs().max())
+        assert d < 6e-2 * float(gt[k].abs().max()) + 1e-6, (k, d, float(gt[k].abs().max()))
