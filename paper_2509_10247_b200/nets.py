@@ -249,13 +249,15 @@ class _PolicyStepFn(torch.autograd.Function):
         ctx.set_materialize_grads(False)
         x, h = x.contiguous(), h.contiguous()
         rs = reset.contiguous().view(torch.uint8) if reset is not None else None
+        img = getattr(wp, "_qs_image", None)  # bf16 weight image built with the pack (once per rollout)
         wp = wp.detach()
         offs = _pack_offsets(n_in, A)
+        if wp.numel() != sum(n for _, n in offs.values()):
+            raise ValueError("packed policy weights do not match this policy's shapes")
         v = {k: wp[o:o + n] for k, (o, n) in offs.items()}
         Wh = torch.cat([v["Wmu"].view(128, A), v["Wsig"].view(128, A)], 1).contiguous()
         bh = torch.cat([v["bmu"], v["bsig"]])
         N = x.shape[0]
-        img = getattr(wp, "_qs_image", None)  # bf16 weight image built with the pack (once per rollout)
         if img is None:
             img = _policy_image(v, n_in, A, Wh)
         h_out = torch.empty(N, h.shape[1], dtype=torch.float32, device=x.device)
