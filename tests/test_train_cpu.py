@@ -132,3 +132,32 @@ def test_td_lambda_k_steps_matches_reference():
                            torch.as_tensor(done), gamma, lam, 6)
     assert torch.equal(full, k6)
     assert LearnerOptions().algo == "sha2c" and LearnerOptions(k_steps=4).k_steps == 4
+
+
+def test_policy_pack_layout():
+    """The fused policy step's flat parameter layout (nets._pack_offsets):
+    it covers every parameter of PolicyNet._fused_params once, in order, and
+    every matrix the kernels stage with 16-byte loads starts on a 4-float
+    boundary; pack_weights is differentiable back to each parameter."""
+    from paper_2509_10247_b200 import nets
+
+    for n_in in (3, 9, 10, 16):
+        arch = nets.PolicyArch(proprio_dim=n_in, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128))
+        pol = nets.PolicyNet(arch, np.random.default_rng(0))
+        offs = nets._pack_offsets(n_in, 3)
+        params = pol._fused_params()
+        assert [n for _, n in offs.values()] == [p.numel() for p in params]
+        o = 0
+        for k, (off, n) in offs.items():
+            assert off == o
+            o += n
+            if k in ("Wi", "Wg", "W0", "W1", "W2"):
+                assert off % 4 == 0, k
+        wp = pol.pack_weights()
+        assert wp.numel() == o and not hasattr(wp, "_qs_image")  # CPU: no kernel image
+        (wp * torch.arange(o, dtype=wp.dtype)).sum().backward()
+        for (k, (off, n)), p in zip(offs.items(), params):
+            assert torch.equal(p.grad.reshape(-1), torch.arange(off, off + n, dtype=wp.dtype)), k
+    # shapes the fused step does not cover: no pack
+    arch = nets.PolicyArch(proprio_dim=9, action_dim=3, recurrent=True, hidden=32, mlp=(64, 64))
+    assert nets.PolicyNet(arch, np.random.default_rng(0)).pack_weights() is None
