@@ -871,13 +871,19 @@ def run_ours(a):
             loss_e.backward()
             return float(loss_e.item())
 
-        eager_window()  # warm-up (allocator, autograd)
+        for _ in range(2):
+            eager_window()  # warm-up (allocator, autograd)
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(3):
+        times = []
+        for _ in range(5):
+            t0 = time.perf_counter()
             eager_window()
-        eager = {"value": N * T / ((time.perf_counter() - t0) / 3), "unit": UNIT,
-                 "api": "FlightTask.step + torch.autograd backward, per window (host sync per window)"}
+            times.append(time.perf_counter() - t0)
+        times.sort()
+        eager = {"value": N * T / times[len(times) // 2], "unit": UNIT,
+                 "api": "FlightTask.step + torch.autograd backward, per window (host sync per window)",
+                 "timed": "median of 5 windows (host-bound: Python step loop + autograd)",
+                 "window_ms": [round(1e3 * t, 3) for t in times]}
         del env2
 
     depth = None
