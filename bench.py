@@ -865,8 +865,10 @@ def run_ours(a):
             acts = host.to(dev, non_blocking=True).requires_grad_(True)
             env2.detach_states()
             tot = 0.0
-            for t in range(T):
-                tot = tot + env2.step(acts[t]).r_ctrl.mean() * 0.99 ** t
+            # unbind: one stack in the backward, not the full-size zero tensor
+            # select's backward builds per step for acts[t]
+            for t, a_t in enumerate(acts.unbind(0)):
+                tot = tot + env2.step(a_t).r_ctrl.mean() * 0.99 ** t
             loss_e = -tot / T
             loss_e.backward()
             return float(loss_e.item())
