@@ -516,23 +516,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                    : "memory");
     }
   };
-  auto stage_x = [&](int sl, int64_t tile) {
-    if (q != 0) return;
+  auto stage_x = [&](int sl, int64_t tile) {  // quarter q stages columns 4q..4q+3 of its row
     const int64_t row = tile * TILE + r;
-    float v[KIN];
+    float v[4];
 #pragma unroll
-    for (int c = 0; c < KIN; ++c) v[c] = 0.f;
-    if (row < M) {
-#pragma unroll
-      for (int c = 0; c < TC_KMAX; ++c)
-        if (c < K) v[c] = S.slot[sl].xraw[r * K + c] * __ldg(scale + c);
-    }
-    v[KIN - 1] = 1.f;  // bias-gradient column
-#pragma unroll
-    for (int c = 0; c < KIN; c += 8)
-      *reinterpret_cast<uint4*>(&S.slot[sl].X[blk_off(r, c, KIN)]) =
-          make_uint4(pack_bf16(v[c], v[c + 1]), pack_bf16(v[c + 2], v[c + 3]), pack_bf16(v[c + 4], v[c + 5]),
-                     pack_bf16(v[c + 6], v[c + 7]));
+    for (int j = 0; j < 4; ++j) {
+      const int c = 4 * q + j;
+      v[j] = (row < M && c < K) ? S.slot[sl].xraw[r * K + c] * __ldg(scale + c) : (c == KIN - 1 ? 1.f : 0.f);
+    }  // column 15: ones (the bias / bias-gradient column)
+    *reinterpret_cast<uint2*>(&S.slot[sl].X[blk_off(r, 4 * q, KIN)]) =
+        make_uint2(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]));
   };
   auto issue_g1 = [&](int sl) {  // X W0
     TcSlot& T = S.slot[sl];
@@ -593,7 +586,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       part = fmaf(h[j], S.w2[cq + j], fmaf(h[j + 1], S.w2[cq + j + 1], part));
     }
     T.predq[q][r] = part;
-    __syncthreads();
+    // only the four warps sharing these rows (warp % 4) exchange partials
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + (warp & 3)) : "memory");
     const int64_t row = tile * TILE + r;
     const float pred = bias2 + T.predq[0][r] + T.predq[1][r] + T.predq[2][r] + T.predq[3][r];
     if constexpr (FWD) {
