@@ -935,7 +935,13 @@ def run_ours(a):
                          "bytes_per_env_step": {"fwd": FWD_BYTES_FUSED, "bwd": BWD_BYTES_FUSED},
                          "gbs": {"fwd": FWD_BYTES_FUSED * N * T / (ms_fwd * 1e-3) / 1e9,
                                  "bwd": BWD_BYTES_FUSED * N * T / (ms_bwd * 1e-3) / 1e9},
-                         "note": "bytes the fused-window kernels must move; they are issue-bound (profiles/README.md)"}},
+                         "note": "bytes the fused-window kernels must move; they are issue-bound (profiles/README.md)"},
+                     # the bytes the forward really moves (ncu dram read+write of one launch,
+                     # profiles/traffic.json) over this run's launch time
+                     "dram_measured": ({"gbs": traffic / (ms_fwd * 1e-3) / 1e9,
+                                        "frac_of_peak": traffic / (ms_fwd * 1e-3) / 1e9 / peak,
+                                        "source": "ncu dram__bytes_read+write of k_window_fwd (profiles/traffic.json)"}
+                                       if traffic else None)},
         "per_step_kernels": {"ms_per_window": ms_per_step_path,
                              "env_steps_per_s": world * N * T / (ms_per_step_path * 1e-3),
                              "note": "same window through the per-step kernels behind FlightTask.step"},
