@@ -56,3 +56,19 @@ def test_product_refuses_to_run_without_cuda():
 
     with pytest.raises(qs._lib.QuadsimLibraryError):
         qs.make_task(qs.TaskConfig(n_envs=4))
+
+
+def test_header_is_plain_c(tmp_path):
+    """The boundary header compiles as C99 (no torch / C++ types): a C, cgo or
+    FFI caller can include it as is."""
+    import shutil
+    import subprocess
+
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    src = tmp_path / "h.c"
+    src.write_text('#include "quadsim_b200.h"\nint main(void) { return 0; }\n')
+    r = subprocess.run([cc, "-std=c99", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I", os.path.dirname(HEADER),
+                        "-c", str(src), "-o", str(tmp_path / "h.o")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
