@@ -35,3 +35,30 @@ for kind in ("h2d", "d2h", "both"):
     for ch in (1, 4):
         run(kind, 5, ch)
         print(kind, "chunks", ch, run(kind, 40, ch))
+
+# the same bidirectional copies while an HBM-heavy kernel stream runs beside
+# them (the e2e leg's situation: window kernels at ~4 TB/s between the copies)
+big = torch.empty(256 * 1024 * 1024 // 4, device="cuda")
+s3 = torch.cuda.Stream()
+
+
+def run_loaded(reps=40):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with torch.cuda.stream(s3):
+        for _ in range(reps * 4):
+            big.mul_(1.0000001)  # 2 x 256 MB per launch, ~0.08 ms
+    for k in range(reps):
+        with torch.cuda.stream(s1):
+            d[k % 2].copy_(h_in[k % 2], non_blocking=True)
+        with torch.cuda.stream(s2):
+            h_out[k % 2].copy_(d[2 + k % 2], non_blocking=True)
+    s1.synchronize()
+    s2.synchronize()
+    dt = (time.perf_counter() - t0) / reps
+    torch.cuda.synchronize()
+    return {"ms_per_window": dt * 1e3, "GBps_per_direction": NB / dt / 1e9}
+
+
+run_loaded(5)
+print("both + HBM load", run_loaded(40))
