@@ -80,11 +80,11 @@ std::vector<at::Tensor> alloc_outputs(const qs_task_cfg& c, const at::Tensor& S_
   const int64_t nS = NP * N * 4, nO = N * P, nD = has_dr ? 4 * N : 0, nC = want_cam ? 2 * N : 0,
                 nI = has_imu ? 6 * N : 0;
   auto up = [](int64_t n) { return (n + 31) & ~int64_t(31); };
-  const at::Tensor fbuf =
-      at::empty({up(nS) + up(nO) + 3 * up(N) + 2 * up(4 * N) + up(nD) + up(nC) + up(nI)}, S_in.options());
-  // int32 words: flags | terminated (int8) + truncated (bool) bytes, 4-byte aligned
+  const int64_t nf = up(nS) + up(nO) + 3 * up(N) + 2 * up(4 * N) + up(nD) + up(nC) + up(nI);
+  // int32 words after the fp32 ones: flags | terminated (int8) + truncated (bool) bytes
   const int64_t nb = (2 * N + 3) / 4;
-  const at::Tensor ibuf = at::empty({N + nb}, S_in.options().dtype(at::kInt));
+  // ONE allocation for every output (fp32 words, then the int32 words)
+  const at::Tensor fbuf = at::empty({nf + N + nb}, S_in.options());
   // the pieces are tensors over the buffers' storage built directly (no
   // dispatcher round trip per narrow/view: ~1 us each, a third of a step)
   auto carve = [](const at::Tensor& base, int64_t byte_off, std::initializer_list<int64_t> sizes,
@@ -108,9 +108,9 @@ std::vector<at::Tensor> alloc_outputs(const qs_task_cfg& c, const at::Tensor& S_
   at::Tensor dr = has_dr ? take(nD, {N, 4}) : take(0, {0});
   at::Tensor cam = want_cam ? take(nC, {N, 2}) : take(0, {0});
   at::Tensor imu = has_imu ? take(nI, {N, 6}) : take(0, {0});
-  at::Tensor flags = carve(ibuf, 0, {N}, at::kInt);
-  at::Tensor term = carve(ibuf, 4 * N, {N}, at::kChar);
-  at::Tensor trunc = carve(ibuf, 4 * N + N, {N}, at::kBool);
+  at::Tensor flags = carve(fbuf, 4 * nf, {N}, at::kInt);
+  at::Tensor term = carve(fbuf, 4 * (nf + N), {N}, at::kChar);
+  at::Tensor trunc = carve(fbuf, 4 * (nf + N) + N, {N}, at::kBool);
   return {S_out, obs, rc, rg, rl, term, trunc, flags, goal, peff, dr, cam, imu};
 }
 

@@ -1,3 +1,4 @@
+"""Host cost of the pieces of one FlightTask.step at C1 (pm_continuous, 1,024 envs)."""
 import time, torch, sys
 sys.path.insert(0, '/root/repo')
 import paper_2509_10247_b200 as qs
