@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-imu", action="store_true", help="diagnostic: full model without the IMU")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no cpu/clock sampling)")
+    ap.add_argument("--net-dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="C5: the policy / critic arithmetic (bf16 tensor-core kernels, or torch fp32)")
     ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
                     help="c2: headline BPTT windows; c5: SHAC training with NCCL gradient all-reduce")
     return ap.parse_args()
@@ -1013,7 +1015,8 @@ def run_c5(a):
     env = qs.make_task(cfg, device=dev, strict=False, env_offset=rank * N)
     env.reset(seed=1)
     graph = world == 1 or DIST["backend"] == "nccl"
-    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0, cuda_graph=graph))
+    tr = ShortHorizonTrainer(env, LearnerOptions(algo="shac", horizon=16, seed=0, cuda_graph=graph,
+                                                 net_dtype=a.net_dtype))
     for _ in range(max(a.warmup, 4 if graph else 1)):
         tr.update()
     torch.cuda.synchronize()
@@ -1052,7 +1055,8 @@ def run_c5(a):
         print(json.dumps({
             "metric": "env-steps/s (SHAC train: policy + sim fwd+bwd + critic)", "value": world * N * 16 / (ms * 1e-3),
             "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "dtype": "f32 sim, bf16 policy/critic matmuls",
+            "higher_is_better": True, "scaling": "weak",
+            "dtype": "f32 sim, " + ("bf16 policy/critic matmuls" if a.net_dtype == "bf16" else "fp32 policy/critic"),
             "data": "synthetic (in-kernel Philox resets)",
             "config": {"workload": f"C5: SHAC, pm_continuous position, {N} envs/GPU x {world}, horizon 16",
                        "parallelism": f"env-sharded x{world}; NCCL all-reduce of policy+critic grads",
