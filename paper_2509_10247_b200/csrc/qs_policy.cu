@@ -721,10 +721,16 @@ struct GruSmem {
   __nv_bfloat16 B[TR * 96];    // [rows][x 0-15 | h 16-79 | 1 80 | 0]
   __nv_bfloat16 GRZ[TR * HW];  // [rows][dar | daz]
   __nv_bfloat16 GN[TR * HW];   // [rows][dan | dan r]
+  // the next tile's raw rows, streamed in by cp.async while this tile computes:
+  // h, dL/dh' (a, b) as 16-byte chunks XOR-swizzled by row (conflict-free row reads)
+  float HR[TR * HI], AR[TR * HI], BR[TR * HI];
+  float XR[TR * XI];           // x rows (n_in floats each, contiguous)
+  uint8_t RR[TR];              // reset bytes
   float bg[4 * HI];
   uint64_t bar, wbar;
   uint32_t tbase;
 };
+static_assert(sizeof(GruSmem) <= 227 * 1024, "GRU backward shared memory");
 
 __global__ void __launch_bounds__(PT, 1)
     k_gru_bwd(int64_t N, int n_in, const __nv_bfloat16* __restrict__ img, const float* __restrict__ x, const float* __restrict__ hp,
@@ -781,19 +787,60 @@ __global__ void __launch_bounds__(PT, 1)
     return umma::desc_mnmajor(b + ks * 2 * (cols / 8) * 64 + (c0 / 8) * 64, cols);
   };
   const int64_t ntiles = (N + TR - 1) / TR;
+  const bool rst_bulk = rst && (reinterpret_cast<uintptr_t>(rst) & 15) == 0;
+  auto cp16 = [](void* dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+                 : "memory");
+  };
+  auto prefetch = [&](int64_t t) {  // all threads: tile t's raw rows -> HR / AR / BR / XR / RR
+    if (t >= ntiles) return;
+    const int64_t r0 = t * TR;
+    const int nrows = (int)(N - r0 < TR ? N - r0 : TR);
+    for (int i = tid; i < TR * 16; i += PT) {
+      const int rr = i >> 4, c = i & 15, ok = rr < nrows;
+      const int dst = rr * HI + ((c ^ (rr & 15)) << 2);
+      const int64_t src = ok ? (r0 + rr) * HI + 4 * c : 0;
+      cp16(&S.HR[dst], hp + src, ok ? 16 : 0);
+      cp16(&S.AR[dst], dha + src, ok ? 16 : 0);
+      if (dhb) cp16(&S.BR[dst], dhb + src, ok ? 16 : 0);
+    }
+    const int xbytes = nrows * n_in * 4;
+    const char* xs = reinterpret_cast<const char*>(x + r0 * n_in);
+    for (int b = tid * 16; b < TR * n_in * 4; b += PT * 16) {
+      const int nb = xbytes - b >= 16 ? 16 : (xbytes > b ? xbytes - b : 0);
+      cp16(reinterpret_cast<char*>(S.XR) + b, xs + (nb ? b : 0), nb);
+    }
+    if (rst_bulk && tid < TR / 16) {
+      const int nb = nrows - 16 * tid >= 16 ? 16 : (nrows > 16 * tid ? nrows - 16 * tid : 0);
+      cp16(&S.RR[16 * tid], rst + r0 + (nb ? 16 * tid : 0), nb);
+    }
+    cp_async_commit();
+  };
+  prefetch(blockIdx.x);
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t row = tile * TR + r;
     const bool valid = row < N;
-    float h0[16];  // h, units 16q..16q+15 (0 on a reset row)
-    const bool live = valid && !(rst && rst[row]);
+    cp_async_wait<0>();
+    __syncthreads();  // this tile's raw rows have landed
+    float h0[16], g[16];  // h (0 on a reset row) and dL/dh', units 16q..16q+15
+    const bool live = valid && !(rst && (rst_bulk ? S.RR[r] : rst[row]));
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
-      const float4 t = live ? __ldg(reinterpret_cast<const float4*>(hp + row * HI + 16 * q + j))
-                             : make_float4(0.f, 0.f, 0.f, 0.f);
+      const int off = r * HI + (((4 * q + j / 4) ^ (r & 15)) << 2);
+      const float4 t = live ? *reinterpret_cast<const float4*>(&S.HR[off]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 a = valid ? *reinterpret_cast<const float4*>(&S.AR[off]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (valid && dhb) {
+        const float4 b = *reinterpret_cast<const float4*>(&S.BR[off]);
+        a = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+      }
       h0[j] = t.x;
       h0[j + 1] = t.y;
       h0[j + 2] = t.z;
       h0[j + 3] = t.w;
+      g[j] = a.x;
+      g[j + 1] = a.y;
+      g[j + 2] = a.z;
+      g[j + 3] = a.w;
     }
 #pragma unroll
     for (int j = 0; j < 16; j += 8)
@@ -802,7 +849,7 @@ __global__ void __launch_bounds__(PT, 1)
     if (q == 0) {
       float xv[XI];
 #pragma unroll
-      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < n_in) ? __ldg(x + row * n_in + j) : 0.f;
+      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < n_in) ? S.XR[r * n_in + j] : 0.f;
 #pragma unroll
       for (int j = 0; j < XI; j += 8)
         *reinterpret_cast<uint4*>(&S.B[blk_off(r, j, BC)]) = make_uint4(
@@ -812,7 +859,8 @@ __global__ void __launch_bounds__(PT, 1)
       *reinterpret_cast<uint4*>(&S.B[blk_off(r, 80, BC)]) = make_uint4(one, zero, zero, zero);
       *reinterpret_cast<uint4*>(&S.B[blk_off(r, 88, BC)]) = make_uint4(zero, zero, zero, zero);
     }
-    to_mma();
+    to_mma();                         // (every thread is past its raw reads)
+    prefetch(tile + gridDim.x);       // the next tile's rows stream in behind this one
     if (tid == 0) {  // recompute the gate pre-activations
       const uint32_t id128 = umma::idesc_bf16(128, 128, false, true), id64 = umma::idesc_bf16(128, 64, false, true);
       umma::mma_bf16(TRZ, aK(S.B, BC, 0), mKc(S.WI, G3, 0, 0), id128, false);
@@ -823,19 +871,6 @@ __global__ void __launch_bounds__(PT, 1)
       for (int ks = 0; ks < HI / 16; ++ks)
         umma::mma_bf16(THN, aK(S.B, BC, 1 + ks), mKc(S.WG, G3, ks, 2 * HI), id64, ks > 0);
       umma::commit(&S.bar);
-    }
-    float g[16];  // dL/dh', loaded while the gate GEMMs run
-#pragma unroll
-    for (int j = 0; j < 16; j += 4) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a;
-      if (valid) {
-        a = __ldg(reinterpret_cast<const float4*>(dha + row * HI + 16 * q + j));
-        if (dhb) b = __ldg(reinterpret_cast<const float4*>(dhb + row * HI + 16 * q + j));
-      }
-      g[j] = a.x + b.x;
-      g[j + 1] = a.y + b.y;
-      g[j + 2] = a.z + b.z;
-      g[j + 3] = a.w + b.w;
     }
     wait();
     float dd[16];  // g z: the direct part of dL/dh
