@@ -305,30 +305,37 @@ int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W
  * aligned.  Build it once per set of weights (e.g. per rollout). */
 int64_t qs_policy_image_bytes(void);
 int qs_policy_pack_image(int32_t n_in, int32_t n_out, const float* Wi, const float* Wh_g, const float* W0,
-                         const float* W1, const float* W2, const float* Wh, void* w_image, void* stream);
+                         const float* W1, const float* W2, const float* Wh, int32_t wh_planar, void* w_image,
+                         void* stream);
 /* Its backward: given dL/dy (n, n_out), recomputes the forward per tile,
  * writes dL/dh (n, 64) and every weight / bias gradient (same shapes as the
  * parameters; overwritten, not accumulated).  w_image: NULL, or the image of
- * the same weights. */
+ * the same weights.  Planar mode (dy_planar != 0): dy is (2, n, n_out / 2) --
+ * the mu block, then the log-sigma block -- and the heads Wh / gWh are
+ * (2, 128, n_out / 2) likewise ([W_mu | W_sigma] as two blocks). */
 int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const void* w_image, const float* h, const float* dy,
-                        const float* W0, const float* b0,
+                        int32_t dy_planar, const float* W0, const float* b0,
                         const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
                         float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream);
 /* The GRU cell (q/nets.py:107-132; Wi (n_in, 192), Wh_g (64, 192), gates
- * r|z|n) fused in front of the trunk: h_out (n, 64) = GRU(x (n, n_in), h'),
- * y = trunk + heads of h_out, where h' = h with the rows h_reset[i] != 0
- * zeroed (the trainer's episode-reset mask; h_reset may be NULL).  n_in <= 16. */
-int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const void* w_image, const float* x, const float* h,
-                      const uint8_t* h_reset,
+ * r|z|n) fused in front of the trunk: h_out (n, 64) = GRU(x' , h'),
+ * y = trunk + heads of h_out, where x' = x (n, n_in) times the per-feature
+ * x_scale (the policy's input scale, q/nets.py:241; NULL = 1) and h' = h with
+ * the rows h_reset[i] != 0 zeroed (the trainer's episode-reset mask; may be
+ * NULL).  y: (n, n_out), or with y_planar != 0 (2, n, n_out / 2) -- mu block,
+ * then log-sigma block, and Wh is (2, 128, n_out / 2) likewise.  n_in <= 16. */
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const void* w_image, const float* x,
+                      const float* x_scale, const float* h, const uint8_t* h_reset,
                       const float* Wi, const float* bi, const float* Wh_g, const float* bh_g, const float* W0,
                       const float* b0, const float* W1, const float* b1, const float* W2, const float* b2,
-                      const float* Wh, const float* bh, float* h_out, float* y, int32_t n_sm, void* stream);
+                      const float* Wh, const float* bh, float* h_out, float* y, int32_t y_planar, int32_t n_sm,
+                      void* stream);
 /* The GRU cell's backward for dL/dh_out = dh_out_a + dh_out_b (b may be
- * NULL): writes dx (n, n_in), dh (n, 64; 0 on h_reset rows) and gWi, gbi,
- * gWh_g, gbh_g (overwritten). */
-int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float* x, const float* h,
-                      const uint8_t* h_reset,
+ * NULL): writes dx (n, n_in; dL/dx through x_scale), dh (n, 64; 0 on h_reset
+ * rows) and gWi, gbi, gWh_g, gbh_g (overwritten). */
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float* x, const float* x_scale,
+                      const float* h, const uint8_t* h_reset,
                       const float* dh_out_a, const float* dh_out_b, const float* Wi, const float* bi,
                       const float* Wh_g, const float* bh_g, float* dx, float* dh, float* gWi, float* gbi,
                       float* gWh_g, float* gbh_g, float* work, int64_t work_floats, int32_t n_sm, void* stream);

@@ -124,10 +124,10 @@ _SIGS = {
     "qs_mlp3_work_floats": ([i32], i64),
     "qs_mlp3_forward_tc": ([i64, i32] + [vp] * 9 + [i32, vp], i32),
     "qs_policy_trunk_fwd": ([i64, i32] + [vp] * 10 + [i32, vp], i32),
-    "qs_policy_trunk_bwd": ([i64, i32] + [vp] * 20 + [i64, i32, vp], i32),
-    "qs_policy_gru_fwd": ([i64, i32, i32] + [vp] * 18 + [i32, vp], i32),
-    "qs_policy_gru_bwd": ([i64, i32] + [vp] * 17 + [i64, i32, vp], i32),
-    "qs_policy_pack_image": ([i32, i32] + [vp] * 8, i32),
+    "qs_policy_trunk_bwd": ([i64, i32, vp, vp, vp, i32] + [vp] * 17 + [i64, i32, vp], i32),
+    "qs_policy_gru_fwd": ([i64, i32, i32] + [vp] * 19 + [i32, i32, vp], i32),
+    "qs_policy_gru_bwd": ([i64, i32] + [vp] * 18 + [i64, i32, vp], i32),
+    "qs_policy_pack_image": ([i32, i32] + [vp] * 6 + [i32, vp, vp], i32),
     "qs_policy_image_bytes": ([], i64),
     "qs_policy_work_floats": ([i32, i32], i64),
     "qs_raycast": ([P(QsRayCfg), P(QsScene), i32, vp, i32, vp, vp, vp, vp, vp, vp, vp], i32),

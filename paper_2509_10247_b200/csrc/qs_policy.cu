@@ -148,17 +148,28 @@ struct PolSmem {
   uint32_t tbase;
 };
 
+// head output j of row `row` in y: row-major (n, n_out), or planar (2, n, n_out / 2)
+// -- the mu block then the log-sigma block, each contiguous
+QS_D int wh_at(int k, int n, int n_out, int planar) {  // Wh (128, n_out), or planar (2, 128, n_out / 2)
+  const int half = n_out >> 1;
+  return planar ? (n >= half ? 128 * half : 0) + k * half + (n >= half ? n - half : n) : k * n_out + n;
+}
+QS_D int64_t y_at(int64_t row, int j, int64_t N, int n_out, int planar) {
+  const int half = n_out >> 1;
+  return planar ? (j >= half ? N * half : 0) + row * half + (j >= half ? j - half : j) : row * n_out + j;
+}
+
 struct GruArgs {  // the GRU cell of the forward (k_policy_fwd2)
   int n_in;
-  const float *x, *hp, *Wi, *bi, *Wg, *bg;
+  const float *x, *xs, *hp, *Wi, *bi, *Wg, *bg;  // xs: per-feature input scale, or null
   const uint8_t* reset;  // rows whose carried h restarts at 0 (episode reset), or null
   float* h_out;
 };
 
 template <bool BWD>
 __global__ void __launch_bounds__(PT, 1)
-    k_policy_trunk(int64_t N, int n_out, const __nv_bfloat16* __restrict__ img, const float* __restrict__ h,
-                   const float* __restrict__ dy,
+    k_policy_trunk(int64_t N, int n_out, int planar, const __nv_bfloat16* __restrict__ img,
+                   const float* __restrict__ h, const float* __restrict__ dy,
                    const float* __restrict__ W0, const float* __restrict__ b0, const float* __restrict__ W1,
                    const float* __restrict__ b1, const float* __restrict__ W2, const float* __restrict__ b2,
                    const float* __restrict__ Wh, const float* __restrict__ bh, float* __restrict__ y,
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(PT, 1)
     stage_w<HW>(W2, HW, HW, S.W2, tid);
     for (int i = tid; i < HW * HY; i += PT) {
       const int k = i / HY, n = i % HY;  // Wh (128, n_out) row-major, zero-padded to 16 columns
-      S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+      S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[wh_at(k, n, n_out, planar)] : 0.f);
     }
   }
   for (int i = tid; i < HW; i += PT) {
@@ -275,7 +286,7 @@ __global__ void __launch_bounds__(PT, 1)
     if constexpr (BWD) {
       if (q == 0) {
 #pragma unroll
-        for (int j = 0; j < HY / 2; ++j) gy_n[j] = (vd && j < n_out) ? __ldg(dy + rw * n_out + j) : 0.f;
+        for (int j = 0; j < HY / 2; ++j) gy_n[j] = (vd && j < n_out) ? __ldg(dy + y_at(rw, j, N, n_out, planar)) : 0.f;
       }
     }
   };
@@ -349,7 +360,7 @@ __global__ void __launch_bounds__(PT, 1)
         if (valid) {
 #pragma unroll
           for (int j = 0; j < HY / 2; ++j)
-            if (j < n_out) y[row * n_out + j] = v[j] + S.bh[j];
+            if (j < n_out) y[y_at(row, j, N, n_out, planar)] = v[j] + S.bh[j];
         }
       }
       umma::fence_before();
@@ -458,7 +469,7 @@ __global__ void __launch_bounds__(PT, 1)
       ld16z(TWH + lanes, u);
 #pragma unroll
       for (int j = 0; j < HY / 2; ++j)
-        if (j < n_out) wk[TK_WH + r * n_out + j] = u[j];
+        if (j < n_out) wk[TK_WH + wh_at(r, j, n_out, planar)] = u[j];
       ld16z(TB2 + lanes, u);
       wk[TK_B2 + r] = u[HY - 1];
       // dbh: per-row sums of dL/dy over the tiles, reduced over the warp
@@ -499,6 +510,7 @@ struct Fwd2Smem {
   __nv_bfloat16 ACT[2][TR * HW];  // per group: h (prev, bf16) -> h' -> A1 -> A2 -> z
   __nv_bfloat16 XS[2][TR * XI];   // per group: the input rows
   float b0[HW], b1[HW], b2[HW], bh[HY], bg[4 * HI];
+  float xs[XI];  // the input scale (1 past n_in / when absent)
   uint64_t bar[2], wbar;
   uint32_t tbase;
 };
@@ -506,7 +518,7 @@ struct Fwd2Smem {
 QS_D void group_sync(int g) { asm volatile("bar.sync %0, 256;" ::"r"(1 + g) : "memory"); }
 
 __global__ void __launch_bounds__(PT, 1)
-    k_policy_fwd2(int64_t N, int n_out, const __nv_bfloat16* __restrict__ img, GruArgs ga,
+    k_policy_fwd2(int64_t N, int n_out, int planar, const __nv_bfloat16* __restrict__ img, GruArgs ga,
                   const float* __restrict__ W0, const float* __restrict__ b0,
                   const float* __restrict__ W1, const float* __restrict__ b1, const float* __restrict__ W2,
                   const float* __restrict__ b2, const float* __restrict__ Wh, const float* __restrict__ bh,
@@ -531,7 +543,7 @@ __global__ void __launch_bounds__(PT, 1)
     stage_w<G3>(ga.Wg, HI, HI, S.WG, tid);
     for (int i = tid; i < HW * HY; i += PT) {
       const int k = i / HY, n = i % HY;
-      S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+      S.WH[blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[wh_at(k, n, n_out, planar)] : 0.f);
     }
   }
   for (int i = tid; i < HW; i += PT) {
@@ -542,6 +554,7 @@ __global__ void __launch_bounds__(PT, 1)
   for (int i = tid; i < 4 * HI; i += PT)
     S.bg[i] = i < 2 * HI ? ga.bi[i] + ga.bg[i] : i < 3 * HI ? ga.bi[i] : ga.bg[i - HI];
   if (tid < HY) S.bh[tid] = tid < n_out ? bh[tid] : 0.f;
+  if (tid < XI) S.xs[tid] = (ga.xs && tid < ga.n_in) ? ga.xs[tid] : 1.f;
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
     mbar_init(&S.bar[0], 1);
@@ -612,7 +625,8 @@ __global__ void __launch_bounds__(PT, 1)
     if (hh == 0) {
       float xv[XI];
 #pragma unroll
-      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < ga.n_in) ? __ldg(ga.x + row * ga.n_in + j) : 0.f;
+      for (int j = 0; j < XI; ++j)
+        xv[j] = (valid && j < ga.n_in) ? __ldg(ga.x + row * ga.n_in + j) * S.xs[j] : 0.f;
 #pragma unroll
       for (int j = 0; j < XI; j += 8)
         *reinterpret_cast<uint4*>(&XS[blk_off(r, j, XI)]) = make_uint4(
@@ -693,7 +707,7 @@ __global__ void __launch_bounds__(PT, 1)
       if (valid) {
 #pragma unroll
         for (int j = 0; j < HY / 2; ++j)
-          if (j < n_out) y[row * n_out + j] = v[j] + S.bh[j];
+          if (j < n_out) y[y_at(row, j, N, n_out, planar)] = v[j] + S.bh[j];
       }
     }
     umma::fence_before();
@@ -726,6 +740,7 @@ struct GruSmem {
   float HR[TR * HI], AR[TR * HI], BR[TR * HI];
   float XR[TR * XI];           // x rows (n_in floats each, contiguous)
   uint8_t RR[TR];              // reset bytes
+  float xs[XI];                // the input scale (1 past n_in / when absent)
   float bg[4 * HI];
   uint64_t bar, wbar;
   uint32_t tbase;
@@ -733,7 +748,8 @@ struct GruSmem {
 static_assert(sizeof(GruSmem) <= 227 * 1024, "GRU backward shared memory");
 
 __global__ void __launch_bounds__(PT, 1)
-    k_gru_bwd(int64_t N, int n_in, const __nv_bfloat16* __restrict__ img, const float* __restrict__ x, const float* __restrict__ hp,
+    k_gru_bwd(int64_t N, int n_in, const __nv_bfloat16* __restrict__ img, const float* __restrict__ x,
+              const float* __restrict__ xs, const float* __restrict__ hp,
               const uint8_t* __restrict__ rst, const float* __restrict__ dha, const float* __restrict__ dhb, const float* __restrict__ Wi,
               const float* __restrict__ bi, const float* __restrict__ Wg, const float* __restrict__ bgv,
               float* __restrict__ dx, float* __restrict__ dhp, float* __restrict__ work) {
@@ -754,6 +770,7 @@ __global__ void __launch_bounds__(PT, 1)
     stage_w<G3>(Wg, HI, HI, S.WG, tid);
   }
   for (int i = tid; i < 4 * HI; i += PT) S.bg[i] = i < 2 * HI ? bi[i] + bgv[i] : i < 3 * HI ? bi[i] : bgv[i - HI];
+  if (tid < XI) S.xs[tid] = (xs && tid < n_in) ? xs[tid] : 1.f;
   if (warp == 0) umma::tmem_alloc(&S.tbase, 512);
   if (tid == 0) {
     mbar_init(&S.bar, 1);
@@ -849,7 +866,7 @@ __global__ void __launch_bounds__(PT, 1)
     if (q == 0) {
       float xv[XI];
 #pragma unroll
-      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < n_in) ? S.XR[r * n_in + j] : 0.f;
+      for (int j = 0; j < XI; ++j) xv[j] = (valid && j < n_in) ? S.XR[r * n_in + j] * S.xs[j] : 0.f;
 #pragma unroll
       for (int j = 0; j < XI; j += 8)
         *reinterpret_cast<uint4*>(&S.B[blk_off(r, j, BC)]) = make_uint4(
@@ -956,7 +973,7 @@ __global__ void __launch_bounds__(PT, 1)
         if (valid) {
 #pragma unroll
           for (int j = 0; j < XI; ++j)
-            if (j < n_in) dx[row * n_in + j] = v[j];
+            if (j < n_in) dx[row * n_in + j] = v[j] * S.xs[j];  // d/dx = d/d(x * xs) * xs
         }
       }
     }
@@ -1006,13 +1023,14 @@ __global__ void __launch_bounds__(PT, 1)
 }
 
 template <bool BWD>
-int launch_trunk(int64_t n, int32_t n_out, const void* img, const float* h, const float* dy, const float* W0, const float* b0,
+int launch_trunk(int64_t n, int32_t n_out, int32_t planar, const void* img, const float* h, const float* dy,
+                 const float* W0, const float* b0,
                  const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                  const float* bh, float* y, float* dh, float* gW0, float* gb0, float* gW1, float* gb1,
                  float* gW2, float* gb2, float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm,
                  void* stream) {
   if (n <= 0) return QS_OK;
-  if (n_out < 1 || n_out > 8 || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
+  if (n_out < 1 || n_out > 8 || n_sm < 1 || (planar && (n_out & 1))) return QS_ERR_BAD_ARGUMENT;
   if (BWD && (!work || work_floats < (int64_t)n_sm * TK_P)) return QS_ERR_BAD_ARGUMENT;
   const size_t smem = sizeof(PolSmem);
   static_assert(sizeof(PolSmem) <= 227 * 1024, "shared memory");
@@ -1021,7 +1039,7 @@ int launch_trunk(int64_t n, int32_t n_out, const void* img, const float* h, cons
     return QS_ERR_LAUNCH;
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
-  k_policy_trunk<BWD><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out,
+  k_policy_trunk<BWD><<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, planar,
                                                                 reinterpret_cast<const __nv_bfloat16*>(img), h, dy, W0, b0, W1, b1, W2, b2, Wh, bh, y,
                                                                      dh, work);
   if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
@@ -1034,7 +1052,7 @@ int launch_trunk(int64_t n, int32_t n_out, const void* img, const float* h, cons
   return red::sum_partials(work, grid, TK_P, sg, (cudaStream_t)stream);
 }
 
-__global__ void k_pack_image(int n_in, int n_out, const float* __restrict__ Wi, const float* __restrict__ Wg,
+__global__ void k_pack_image(int n_in, int n_out, int planar, const float* __restrict__ Wi, const float* __restrict__ Wg,
                              const float* __restrict__ W0, const float* __restrict__ W1, const float* __restrict__ W2,
                              const float* __restrict__ Wh, __nv_bfloat16* __restrict__ img) {
   using umma::blk_off;
@@ -1053,7 +1071,7 @@ __global__ void k_pack_image(int n_in, int n_out, const float* __restrict__ Wi, 
       img[IMG_W2 + blk_off(k, n, HW)] = __float2bfloat16_rn(W2[e]);
     } else if (i < IMG_WI) {
       const int e = i - IMG_WH, k = e / HY, n = e % HY;
-      img[IMG_WH + blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[k * n_out + n] : 0.f);
+      img[IMG_WH + blk_off(k, n, HY)] = __float2bfloat16_rn(n < n_out ? Wh[wh_at(k, n, n_out, planar)] : 0.f);
     } else if (i < IMG_WG) {
       const int e = i - IMG_WI, k = e / G3, n = e % G3;
       img[IMG_WI + blk_off(k, n, G3)] = __float2bfloat16_rn(k < n_in ? Wi[k * G3 + n] : 0.f);
@@ -1071,11 +1089,13 @@ extern "C" {
 int64_t qs_policy_image_bytes(void) { return (int64_t)IMG_N * 2; }
 
 int qs_policy_pack_image(int32_t n_in, int32_t n_out, const float* Wi, const float* Wh_g, const float* W0,
-                         const float* W1, const float* W2, const float* Wh, void* w_image, void* stream) {
-  if (!Wi || !Wh_g || !W0 || !W1 || !W2 || !Wh || !w_image || n_in < 1 || n_in > XI || n_out < 1 || n_out > 8)
+                         const float* W1, const float* W2, const float* Wh, int32_t wh_planar, void* w_image,
+                         void* stream) {
+  if (!Wi || !Wh_g || !W0 || !W1 || !W2 || !Wh || !w_image || n_in < 1 || n_in > XI || n_out < 1 || n_out > 8 ||
+      (wh_planar && (n_out & 1)))
     return QS_ERR_BAD_ARGUMENT;
   if (reinterpret_cast<uintptr_t>(w_image) % 16) return QS_ERR_BAD_ARGUMENT;
-  k_pack_image<<<(IMG_N + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n_in, n_out, Wi, Wh_g, W0, W1, W2, Wh,
+  k_pack_image<<<(IMG_N + 255) / 256, 256, 0, (cudaStream_t)stream>>>(n_in, n_out, wh_planar, Wi, Wh_g, W0, W1, W2, Wh,
                                                                      reinterpret_cast<__nv_bfloat16*>(w_image));
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
@@ -1089,42 +1109,44 @@ int qs_policy_trunk_fwd(int64_t n, int32_t n_out, const float* h, const float* W
                         const float* b1, const float* W2, const float* b2, const float* Wh, const float* bh, float* y,
                         int32_t n_sm, void* stream) {
   if (!y || !h) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<false>(n, n_out, nullptr, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
+  return launch_trunk<false>(n, n_out, 0, nullptr, h, nullptr, W0, b0, W1, b1, W2, b2, Wh, bh, y, nullptr, nullptr,
                              nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, n_sm, stream);
 }
 
 int qs_policy_trunk_bwd(int64_t n, int32_t n_out, const void* w_image, const float* h, const float* dy,
-                        const float* W0, const float* b0,
+                        int32_t dy_planar, const float* W0, const float* b0,
                         const float* W1, const float* b1, const float* W2, const float* b2, const float* Wh,
                         float* dh, float* gW0, float* gb0, float* gW1, float* gb1, float* gW2, float* gb2,
                         float* gWh, float* gbh, float* work, int64_t work_floats, int32_t n_sm, void* stream) {
   if (!h || !dy || !dh) return QS_ERR_BAD_ARGUMENT;
-  return launch_trunk<true>(n, n_out, w_image, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
+  return launch_trunk<true>(n, n_out, dy_planar, w_image, h, dy, W0, b0, W1, b1, W2, b2, Wh, nullptr, nullptr, dh, gW0, gb0,
                             gW1, gb1, gW2, gb2, gWh, gbh, work, work_floats, n_sm, stream);
 }
 
-int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const void* w_image, const float* x, const float* h,
-                      const uint8_t* h_reset,
+int qs_policy_gru_fwd(int64_t n, int32_t n_in, int32_t n_out, const void* w_image, const float* x,
+                      const float* x_scale, const float* h, const uint8_t* h_reset,
                       const float* Wi, const float* bi, const float* Wh_g, const float* bh_g, const float* W0,
                       const float* b0, const float* W1, const float* b1, const float* W2, const float* b2,
-                      const float* Wh, const float* bh, float* h_out, float* y, int32_t n_sm, void* stream) {
+                      const float* Wh, const float* bh, float* h_out, float* y, int32_t y_planar, int32_t n_sm,
+                      void* stream) {
   if (!y || !h_out || !x || !h || n_in < 1 || n_in > XI) return QS_ERR_BAD_ARGUMENT;
   if (n <= 0) return QS_OK;
-  if (n_out < 1 || n_out > 8 || n_sm < 1) return QS_ERR_BAD_ARGUMENT;
-  const GruArgs ga{n_in, x, h, Wi, bi, Wh_g, bh_g, h_reset, h_out};
+  if (n_out < 1 || n_out > 8 || n_sm < 1 || (y_planar && (n_out & 1))) return QS_ERR_BAD_ARGUMENT;
+  const GruArgs ga{n_in, x, x_scale, h, Wi, bi, Wh_g, bh_g, h_reset, h_out};
   const size_t smem = sizeof(Fwd2Smem);
   static_assert(sizeof(Fwd2Smem) <= 227 * 1024, "shared memory");
   if (cudaFuncSetAttribute(k_policy_fwd2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return QS_ERR_LAUNCH;
   const int64_t npairs = ((n + TR - 1) / TR + 1) / 2;
   const int grid = (int)(npairs < n_sm ? npairs : n_sm);
-  k_policy_fwd2<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, reinterpret_cast<const __nv_bfloat16*>(w_image),
+  k_policy_fwd2<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_out, y_planar,
+                                                          reinterpret_cast<const __nv_bfloat16*>(w_image),
                                                           ga, W0, b0, W1, b1, W2, b2, Wh, bh, y);
   return cudaGetLastError() == cudaSuccess ? QS_OK : QS_ERR_LAUNCH;
 }
 
-int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float* x, const float* h,
-                      const uint8_t* h_reset,
+int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float* x, const float* x_scale,
+                      const float* h, const uint8_t* h_reset,
                       const float* dh_out_a,
                       const float* dh_out_b, const float* Wi, const float* bi, const float* Wh_g, const float* bh_g,
                       float* dx, float* dh, float* gWi, float* gbi, float* gWh_g, float* gbh_g, float* work,
@@ -1138,7 +1160,7 @@ int qs_policy_gru_bwd(int64_t n, int32_t n_in, const void* w_image, const float*
   const int64_t ntiles = (n + TR - 1) / TR;
   const int grid = (int)(ntiles < n_sm ? ntiles : n_sm);
   k_gru_bwd<<<grid, PT, smem, (cudaStream_t)stream>>>(n, n_in, reinterpret_cast<const __nv_bfloat16*>(w_image), x,
-                                                      h, h_reset, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
+                                                      x_scale, h, h_reset, dh_out_a, dh_out_b, Wi, bi, Wh_g, bh_g, dx, dh,
                                                       work);
   if (cudaGetLastError() != cudaSuccess) return QS_ERR_LAUNCH;
   red::Segs sg{{gWi, gbi, gWh_g, gbh_g}, {GK_WI, GK_BI, GK_WG, GK_BG}, {(int64_t)n_in * G3, G3, HI * G3, G3}, 4, false};

@@ -234,16 +234,19 @@ class _TrunkFn(torch.autograd.Function):
 
 
 class _PolicyStepFn(torch.autograd.Function):
-    """(h', y) = (GRU(x, h masked by reset), trunk + heads of h')
+    """(h', y) = (GRU(x * scale, h masked by reset), trunk + heads of h')
     (q/nets.py:107-132, 241-256) in one tcgen05 kernel (qs_policy_gru_fwd);
     the backward is the trunk's (qs_policy_trunk_bwd, dL/dy -> dL/dh') then the
     GRU cell's (qs_policy_gru_bwd, dL/dh' from the trunk plus the carried one).
     The parameters enter as ONE flat tensor (``PolicyNet.pack_weights``, layout
-    ``PolicyNet._fused_params``): a rollout packs them once, and the 16 steps'
-    gradients accumulate into one buffer instead of 14 per step."""
+    ``_pack_offsets``): a rollout packs them once, and the 16 steps' gradients
+    accumulate into one buffer instead of 14 per step.  The kernels run in
+    planar mode: y is (2, N, A) -- mu, then log-sigma, each contiguous -- and
+    the heads [W_mu | W_sigma], [b_mu | b_sigma] are read and their gradients
+    written as the flat buffer's own slices (no concatenation or split)."""
 
     @staticmethod
-    def forward(ctx, x, h, reset, wp, n_in, A):
+    def forward(ctx, x, scale, h, reset, wp, n_in, A):
         from paper_2509_10247_b200 import _lib as L
 
         ctx.set_materialize_grads(False)
@@ -255,20 +258,18 @@ class _PolicyStepFn(torch.autograd.Function):
         if wp.numel() != sum(n for _, n in offs.values()):
             raise ValueError("packed policy weights do not match this policy's shapes")
         v = {k: wp[o:o + n] for k, (o, n) in offs.items()}
-        Wh = torch.cat([v["Wmu"].view(128, A), v["Wsig"].view(128, A)], 1).contiguous()
-        bh = torch.cat([v["bmu"], v["bsig"]])
         N = x.shape[0]
         if img is None:
-            img = _policy_image(v, n_in, A, Wh)
+            img = _policy_image(v, n_in, A)
         h_out = torch.empty(N, h.shape[1], dtype=torch.float32, device=x.device)
-        y = torch.empty(N, 2 * A, dtype=torch.float32, device=x.device)
+        y = torch.empty(2, N, A, dtype=torch.float32, device=x.device)
         n_sm = torch.cuda.get_device_properties(x.device).multi_processor_count
-        L.check(L.lib().qs_policy_gru_fwd(N, n_in, 2 * A, L.ptr(img), L.ptr(x), L.ptr(h), L.ptr(rs),
+        L.check(L.lib().qs_policy_gru_fwd(N, n_in, 2 * A, L.ptr(img), L.ptr(x), L.ptr(scale), L.ptr(h), L.ptr(rs),
                                           *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg", "W0", "b0", "W1", "b1", "W2",
-                                                                  "b2")],
-                                          L.ptr(Wh), L.ptr(bh), L.ptr(h_out), L.ptr(y), n_sm,
-                                          L.stream_handle(x.device)), "qs_policy_gru_fwd")
-        ctx.save_for_backward(x, h, rs, h_out, wp, Wh, img)
+                                                                  "b2", "Wh", "bh")],
+                                          L.ptr(h_out), L.ptr(y), 1, n_sm, L.stream_handle(x.device)),
+                "qs_policy_gru_fwd")
+        ctx.save_for_backward(x, scale, h, rs, h_out, wp, img)
         ctx.n_sm, ctx.A, ctx.n_in = n_sm, A, n_in
         return h_out, y
 
@@ -276,55 +277,50 @@ class _PolicyStepFn(torch.autograd.Function):
     def backward(ctx, g_h, g_y):
         from paper_2509_10247_b200 import _lib as L
 
-        x, h, rs, h_out, wp, Wh, img = ctx.saved_tensors
+        x, scale, h, rs, h_out, wp, img = ctx.saved_tensors
         N, A, n_in = x.shape[0], ctx.A, ctx.n_in
         dev, st = x.device, L.stream_handle(x.device)
         offs = _pack_offsets(n_in, A)
         v = {k: wp[o:o + n] for k, (o, n) in offs.items()}
-        gw = torch.empty_like(wp)  # every slice is written below
+        gw = torch.empty_like(wp)  # every slice is written by the two kernels
         gv = {k: gw[o:o + n] for k, (o, n) in offs.items()}
-        g_y = torch.zeros(N, 2 * A, device=dev) if g_y is None else g_y.contiguous().float()
+        g_y = torch.zeros(2, N, A, device=dev) if g_y is None else g_y.contiguous().float()
         g_h = None if g_h is None else g_h.contiguous().float()
         dh_t = torch.empty_like(h_out)
-        gWh = torch.empty(128, 2 * A, dtype=torch.float32, device=dev)
-        gbh = torch.empty(2 * A, dtype=torch.float32, device=dev)
         work = _work(0, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_trunk_bwd(N, 2 * A, L.ptr(img), L.ptr(h_out), L.ptr(g_y),
-                                            *[L.ptr(v[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2")], L.ptr(Wh),
-                                            L.ptr(dh_t), *[L.ptr(gv[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2")],
-                                            L.ptr(gWh), L.ptr(gbh), L.ptr(work), work.numel(), ctx.n_sm, st),
-                "qs_policy_trunk_bwd")
+        L.check(L.lib().qs_policy_trunk_bwd(N, 2 * A, L.ptr(img), L.ptr(h_out), L.ptr(g_y), 1,
+                                            *[L.ptr(v[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2", "Wh")],
+                                            L.ptr(dh_t),
+                                            *[L.ptr(gv[k]) for k in ("W0", "b0", "W1", "b1", "W2", "b2", "Wh", "bh")],
+                                            L.ptr(work), work.numel(), ctx.n_sm, st), "qs_policy_trunk_bwd")
         dx, dh = torch.empty_like(x), torch.empty_like(h)
         work = _work(1, ctx.n_sm, dev)
-        L.check(L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(img), L.ptr(x), L.ptr(h), L.ptr(rs), L.ptr(dh_t), L.ptr(g_h),
-                                          *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg")], L.ptr(dx), L.ptr(dh),
-                                          *[L.ptr(gv[k]) for k in ("Wi", "bi", "Wg", "bg")], L.ptr(work),
-                                          work.numel(), ctx.n_sm, st), "qs_policy_gru_bwd")
-        gv["Wmu"].view(128, A).copy_(gWh[:, :A])
-        gv["Wsig"].view(128, A).copy_(gWh[:, A:])
-        gv["bmu"].copy_(gbh[:A])
-        gv["bsig"].copy_(gbh[A:])
-        return dx, dh, None, gw, None, None
+        L.check(L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(img), L.ptr(x), L.ptr(scale), L.ptr(h), L.ptr(rs),
+                                          L.ptr(dh_t), L.ptr(g_h), *[L.ptr(v[k]) for k in ("Wi", "bi", "Wg", "bg")],
+                                          L.ptr(dx), L.ptr(dh), *[L.ptr(gv[k]) for k in ("Wi", "bi", "Wg", "bg")],
+                                          L.ptr(work), work.numel(), ctx.n_sm, st), "qs_policy_gru_bwd")
+        return dx, None, dh, None, gw, None, None
 
 
-def _policy_image(v, n_in, A, Wh):
+def _policy_image(v, n_in, A):
     """The kernels' bf16 weight image (qs_policy_pack_image) of the packed slices v."""
     from paper_2509_10247_b200 import _lib as L
 
-    dev = Wh.device
+    dev = v["W0"].device
     img = torch.empty(L.lib().qs_policy_image_bytes() // 2, dtype=torch.bfloat16, device=dev)
     L.check(L.lib().qs_policy_pack_image(n_in, 2 * A, L.ptr(v["Wi"]), L.ptr(v["Wg"]), L.ptr(v["W0"]),
-                                         L.ptr(v["W1"]), L.ptr(v["W2"]), L.ptr(Wh), L.ptr(img),
+                                         L.ptr(v["W1"]), L.ptr(v["W2"]), L.ptr(v["Wh"]), 1, L.ptr(img),
                                          L.stream_handle(dev)), "qs_policy_pack_image")
     return img
 
 
 def _pack_offsets(n_in, A, H=64, W=128):
-    """Flat layout of the fused policy-step parameters (every matrix starts on
-    a 16-byte boundary: the kernels stage them with 16-byte loads)."""
+    """Flat layout of the fused policy-step parameters: the order of
+    ``PolicyNet._fused_params``, with the two heads as the planar blocks the
+    kernels read -- Wh = [W_mu | W_sigma] as (2, 128, A), bh = [b_mu | b_sigma].
+    Every matrix starts on a 16-byte boundary (16-byte staging loads)."""
     sizes = [("Wi", n_in * 3 * H), ("bi", 3 * H), ("Wg", H * 3 * H), ("bg", 3 * H), ("W0", H * W), ("b0", W),
-             ("W1", W * W), ("b1", W), ("W2", W * W), ("b2", W), ("Wmu", W * A), ("bmu", A), ("Wsig", W * A),
-             ("bsig", A)]
+             ("W1", W * W), ("b1", W), ("W2", W * W), ("b2", W), ("Wh", 2 * W * A), ("bh", 2 * A)]
     out, o = {}, 0
     for k, n in sizes:
         out[k] = (o, n)
@@ -378,8 +374,17 @@ class PolicyNet(torch.nn.Module):
     def _fused_params(self):
         """The parameters of the fused policy step, in ``_pack_offsets`` order."""
         g, L = self.gru, self.trunk.layers
-        return [g.Wi, g.bi, g.Wh, g.bh, L[0].W, L[0].b, L[1].W, L[1].b, L[2].W, L[2].b, self.mu.W, self.mu.b,
-                self.sig.W, self.sig.b]
+        return [g.Wi, g.bi, g.Wh, g.bh, L[0].W, L[0].b, L[1].W, L[1].b, L[2].W, L[2].b, self.mu.W,
+                self.sig.W, self.mu.b, self.sig.b]
+
+    def _scale_f32(self):
+        """The input scale as fp32 on the module's device (cached; the buffer is fp64)."""
+        sc = self.input_scale
+        key = (sc.device, sc.data_ptr(), sc._version)
+        if getattr(self, "_scale_key", None) != key:
+            self._scale_cache = sc.to(torch.float32).contiguous()
+            self._scale_key = key
+        return self._scale_cache
 
     def pack_weights(self):
         """One flat, differentiable copy of the fused step's parameters; pass
@@ -392,10 +397,9 @@ class PolicyNet(torch.nn.Module):
         wp = torch.cat([p.reshape(-1) for p in self._fused_params()])
         if wp.is_cuda:  # the kernels' bf16 weight image, built once with the pack
             with torch.no_grad():
-                A = self.arch.action_dim
-                v = {k: wp[o:o + n] for k, (o, n) in _pack_offsets(self.gru.Wi.shape[0], A).items()}
-                Wh = torch.cat([v["Wmu"].view(128, A), v["Wsig"].view(128, A)], 1).contiguous()
-                wp._qs_image = _policy_image(v, self.gru.Wi.shape[0], A, Wh)
+                n_in = self.gru.Wi.shape[0]
+                v = {k: wp[o:o + n] for k, (o, n) in _pack_offsets(n_in, self.arch.action_dim).items()}
+                wp._qs_image = _policy_image(v, n_in, self.arch.action_dim)
         return wp
 
     def initial_hidden(self, batch, device=None):
@@ -406,6 +410,21 @@ class PolicyNet(torch.nn.Module):
         restarts at zero before this step (the trainer's episode resets,
         q/learners.py:215-217), folded into the fused kernel when it runs.
         packed: ``pack_weights()`` of this module, reused across a rollout."""
+        A = self.arch.action_dim
+        layers = self.trunk.layers
+        trunk_ok = (FUSED_TRUNK and proprio.is_cuda and proprio.dim() == 2 and proprio.dtype == torch.float32 and
+                    torch.is_autocast_enabled() and len(layers) == 3 and
+                    tuple(l.W.shape for l in layers) == ((64, 128), (128, 128), (128, 128)) and 2 * A <= 8)
+        if (trunk_ok and self.enc is None and self.gru is not None and self.hidden == 64 and
+                proprio.shape[1] <= 16):
+            # bf16 policy mode: input scale, GRU cell, trunk and both heads in one
+            # tcgen05 kernel; mu and log-sigma come out as two contiguous planes
+            if h is None:
+                h = torch.zeros(proprio.shape[0], self.hidden, device=proprio.device)
+            wp = packed if packed is not None else self.pack_weights()
+            h, y = _PolicyStepFn.apply(proprio, self._scale_f32(), h.float(), h_reset, wp, proprio.shape[1], A)
+            mu, ls = y.unbind(0)
+            return mu, torch.clamp(ls, LOG_SIGMA_MIN, self.arch.log_sigma_max), h
         x = proprio * self.input_scale.to(proprio.dtype)
         if self.enc is not None:
             if visual is None:
@@ -413,18 +432,7 @@ class PolicyNet(torch.nn.Module):
             img = visual.to(x.dtype) * (1.0 / float(self.arch.visual.get("max_range", 1.0)))
             f = self.enc(img) if self.arch.visual["kind"] == "depth" else torch.tanh(self.enc(img))
             x = torch.cat([x, f.to(x.dtype)], -1)
-        A = self.arch.action_dim
-        layers = self.trunk.layers
-        trunk_ok = (FUSED_TRUNK and x.is_cuda and x.dim() == 2 and x.dtype == torch.float32 and
-                    torch.is_autocast_enabled() and len(layers) == 3 and
-                    tuple(l.W.shape for l in layers) == ((64, 128), (128, 128), (128, 128)) and 2 * A <= 8)
-        if trunk_ok and self.gru is not None and self.hidden == 64 and x.shape[1] <= 16:
-            # bf16 policy mode: GRU cell, trunk and both heads in one tcgen05 kernel
-            if h is None:
-                h = torch.zeros(x.shape[0], self.hidden, device=x.device)
-            wp = packed if packed is not None else self.pack_weights()
-            h, y = _PolicyStepFn.apply(x, h.float(), h_reset, wp, x.shape[1], A)
-            return y[:, :A], torch.clamp(y[:, A:2 * A], LOG_SIGMA_MIN, self.arch.log_sigma_max), h
+        trunk_ok = trunk_ok and x.dtype == torch.float32
         if self.gru is not None:
             if h is None:
                 h = torch.zeros(x.shape[0], self.hidden, device=x.device, dtype=x.dtype)

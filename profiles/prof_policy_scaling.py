@@ -42,12 +42,12 @@ for tiles_per_sm in (1, 2, 4, 7, 14, 28):
     w1 = torch.empty(L.lib().qs_policy_work_floats(1, n_sm), device="cuda")
     dx = torch.empty_like(x)
     img = torch.empty(L.lib().qs_policy_image_bytes() // 2, dtype=torch.bfloat16, device="cuda")
-    L.lib().qs_policy_pack_image(n_in, 6, *P(Wi, Wg, W0, W1, W2, Wh, img), st)
-    fwd = ev_time(lambda: L.lib().qs_policy_gru_fwd(N, n_in, 6, L.ptr(img), *P(x, h), None, *P(Wi, bi, Wg, bg, W0, b0, W1, b1, W2,
-                                                                                  b2, Wh, bh, ho, y), n_sm, st))
-    tb = ev_time(lambda: L.lib().qs_policy_trunk_bwd(N, 6, L.ptr(img), *P(ho, dy, W0, b0, W1, b1, W2, b2, Wh, dh, *gr, w0),
+    L.lib().qs_policy_pack_image(n_in, 6, *P(Wi, Wg, W0, W1, W2, Wh), 0, L.ptr(img), st)
+    fwd = ev_time(lambda: L.lib().qs_policy_gru_fwd(N, n_in, 6, L.ptr(img), L.ptr(x), None, L.ptr(h), None, *P(Wi, bi, Wg, bg, W0, b0, W1, b1, W2,
+                                                                                  b2, Wh, bh, ho, y), 0, n_sm, st))
+    tb = ev_time(lambda: L.lib().qs_policy_trunk_bwd(N, 6, L.ptr(img), *P(ho, dy), 0, *P(W0, b0, W1, b1, W2, b2, Wh, dh, *gr, w0),
                                                      w0.numel(), n_sm, st))
-    gb = ev_time(lambda: L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(img), *P(x, h), None, *P(dh), None, *P(Wi, bi, Wg, bg, dx, dh,
+    gb = ev_time(lambda: L.lib().qs_policy_gru_bwd(N, n_in, L.ptr(img), L.ptr(x), None, L.ptr(h), None, *P(dh), None, *P(Wi, bi, Wg, bg, dx, dh,
                                                                                             *gg, w1), w1.numel(), n_sm,
                                                    st))
     print(f"tiles/SM {tiles_per_sm:3d}  N {N:8d}  fwd {fwd:7.1f} us  trunk_bwd {tb:7.1f} us  gru_bwd {gb:7.1f} us")

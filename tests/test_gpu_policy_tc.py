@@ -34,10 +34,10 @@ def test_policy_trunk_fwd_bwd_match_autograd(n_out, N):
     grads = [torch.full_like(p, 7.0) for p in params]  # overwritten, not accumulated
     dh = torch.empty_like(h)
     work = torch.empty(L.lib().qs_policy_work_floats(0, n_sm), device="cuda")
-    L.check(L.lib().qs_policy_trunk_bwd(N, n_out, None, *_ptrs(h, dy, W0, b0, W1, b1, W2, b2, Wh, dh, grads[0], grads[1],
-                                                           grads[2], grads[3], grads[4], grads[5], grads[6],
-                                                           grads[7], work), work.numel(), n_sm, L.stream_handle()),
-            "bwd")
+    L.check(L.lib().qs_policy_trunk_bwd(N, n_out, None, *_ptrs(h, dy), 0,
+                                        *_ptrs(W0, b0, W1, b1, W2, b2, Wh, dh, grads[0], grads[1], grads[2], grads[3],
+                                               grads[4], grads[5], grads[6], grads[7], work), work.numel(), n_sm,
+                                        L.stream_handle()), "bwd")
     leaves = [p.clone().requires_grad_(True) for p in params]
     hl = h.clone().requires_grad_(True)
     w0, c0, w1, c1, w2, c2, wh, ch = leaves
@@ -62,7 +62,8 @@ def test_policynet_autocast_uses_trunk_kernels_and_matches_torch_path():
 
     from paper_2509_10247_b200 import nets
 
-    arch = nets.PolicyArch(proprio_dim=10, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128))
+    arch = nets.PolicyArch(proprio_dim=10, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128),
+                           input_scale=tuple(np.linspace(0.3, 1.5, 10)))
     pol = nets.PolicyNet(arch, np.random.default_rng(3)).cuda()
     x = torch.randn(3000, 10, device="cuda")
     h0 = torch.randn(3000, 64, device="cuda") * 0.5
@@ -105,23 +106,28 @@ def test_policy_gru_fwd_bwd_match_autograd(n_in, N):
     reset = (torch.rand(N, generator=g) < 0.1).cuda()  # rows whose carried h restarts at 0
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
     h_out, y = torch.empty(N, 64, device="cuda"), torch.empty(N, 6, device="cuda")
-    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, None, *_ptrs(x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2,
-                                                                Wh, bh, h_out, y), n_sm, L.stream_handle()), "gru fwd")
+    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, None, *_ptrs(x, None, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2,
+                                                                b2, Wh, bh, h_out, y), 0, n_sm, L.stream_handle()),
+            "gru fwd")
     # the same from the pre-converted bf16 weight image (bulk-copied by every CTA): same bits
     img = torch.empty(L.lib().qs_policy_image_bytes() // 2, dtype=torch.bfloat16, device="cuda")
-    L.check(L.lib().qs_policy_pack_image(n_in, 6, *_ptrs(Wi, Wg, W0, W1, W2, Wh, img), L.stream_handle()), "image")
+    L.check(L.lib().qs_policy_pack_image(n_in, 6, *_ptrs(Wi, Wg, W0, W1, W2, Wh), 0, L.ptr(img), L.stream_handle()),
+            "image")
     h_out2, y2 = torch.empty_like(h_out), torch.empty_like(y)
-    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, *_ptrs(img, x, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2, b2,
-                                                          Wh, bh, h_out2, y2), n_sm, L.stream_handle()), "gru fwd img")
+    L.check(L.lib().qs_policy_gru_fwd(N, n_in, 6, *_ptrs(img, x, None, h, reset, Wi, bi, Wg, bg, W0, b0, W1, b1, W2,
+                                                          b2, Wh, bh, h_out2, y2), 0, n_sm, L.stream_handle()),
+            "gru fwd img")
     assert torch.equal(h_out, h_out2) and torch.equal(y, y2)
     dx, dh = torch.empty_like(x), torch.empty_like(h)
     gr = [torch.full_like(t, 7.0) for t in (Wi, bi, Wg, bg)]  # overwritten, not accumulated
     work = torch.empty(L.lib().qs_policy_work_floats(1, n_sm), device="cuda")
-    L.check(L.lib().qs_policy_gru_bwd(N, n_in, None, *_ptrs(x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr, work),
+    L.check(L.lib().qs_policy_gru_bwd(N, n_in, None, *_ptrs(x, None, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr,
+                                                            work),
                                       work.numel(), n_sm, L.stream_handle()), "gru bwd")
     # reproducible: a second pass (from the weight image) gives the same bits
     gr2 = [torch.zeros_like(t) for t in (Wi, bi, Wg, bg)]
-    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(img, x, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr2, work),
+    L.check(L.lib().qs_policy_gru_bwd(N, n_in, *_ptrs(img, x, None, h, reset, gh, None, Wi, bi, Wg, bg, dx, dh, *gr2,
+                                                      work),
                                       work.numel(), n_sm, L.stream_handle()), "gru bwd")
     assert all(torch.equal(a, b) for a, b in zip(gr, gr2))
     leaves = [t.clone().requires_grad_(True) for t in (x, h, Wi, bi, Wg, bg)]
@@ -153,7 +159,8 @@ def test_policynet_recurrent_rollout_gradients_match_torch_path():
 
     from paper_2509_10247_b200 import nets
 
-    arch = nets.PolicyArch(proprio_dim=9, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128))
+    arch = nets.PolicyArch(proprio_dim=9, action_dim=3, recurrent=True, hidden=64, mlp=(128, 128),
+                           input_scale=tuple(np.linspace(0.2, 2.0, 9)))
     pol = nets.PolicyNet(arch, np.random.default_rng(11)).cuda()
     g = torch.Generator(device="cuda").manual_seed(5)
     xs = [torch.randn(2048, 9, device="cuda", generator=g) for _ in range(4)]

@@ -135,10 +135,11 @@ def test_td_lambda_k_steps_matches_reference():
 
 
 def test_policy_pack_layout():
-    """The fused policy step's flat parameter layout (nets._pack_offsets):
-    it covers every parameter of PolicyNet._fused_params once, in order, and
-    every matrix the kernels stage with 16-byte loads starts on a 4-float
-    boundary; pack_weights is differentiable back to each parameter."""
+    """The fused policy step's flat parameter layout (nets._pack_offsets): the
+    parameters of PolicyNet._fused_params back to back (the two heads as the
+    planar blocks [W_mu | W_sigma], [b_mu | b_sigma] the kernels read), every
+    matrix the kernels stage with 16-byte loads on a 4-float boundary, and
+    pack_weights differentiable back to each parameter."""
     from paper_2509_10247_b200 import nets
 
     for n_in in (3, 9, 10, 16):
@@ -146,18 +147,24 @@ def test_policy_pack_layout():
         pol = nets.PolicyNet(arch, np.random.default_rng(0))
         offs = nets._pack_offsets(n_in, 3)
         params = pol._fused_params()
-        assert [n for _, n in offs.values()] == [p.numel() for p in params]
+        total = sum(p.numel() for p in params)
         o = 0
         for k, (off, n) in offs.items():
             assert off == o
             o += n
-            if k in ("Wi", "Wg", "W0", "W1", "W2"):
+            if k in ("Wi", "Wg", "W0", "W1", "W2", "Wh"):
                 assert off % 4 == 0, k
+        assert o == total
+        assert offs["Wh"][1] == pol.mu.W.numel() + pol.sig.W.numel() and offs["bh"][1] == 6
         wp = pol.pack_weights()
-        assert wp.numel() == o and not hasattr(wp, "_qs_image")  # CPU: no kernel image
-        (wp * torch.arange(o, dtype=wp.dtype)).sum().backward()
-        for (k, (off, n)), p in zip(offs.items(), params):
-            assert torch.equal(p.grad.reshape(-1), torch.arange(off, off + n, dtype=wp.dtype)), k
+        assert wp.numel() == total and not hasattr(wp, "_qs_image")  # CPU: no kernel image
+        # the planar head block: W_mu (128, 3) row-major, then W_sigma
+        assert torch.equal(wp[offs["Wh"][0]:offs["Wh"][0] + 384].view(128, 3), pol.mu.W.detach())
+        (wp * torch.arange(total, dtype=wp.dtype)).sum().backward()
+        po = 0
+        for p in params:
+            assert torch.equal(p.grad.reshape(-1), torch.arange(po, po + p.numel(), dtype=wp.dtype))
+            po += p.numel()
     # shapes the fused step does not cover: no pack
     arch = nets.PolicyArch(proprio_dim=9, action_dim=3, recurrent=True, hidden=32, mlp=(64, 64))
     assert nets.PolicyNet(arch, np.random.default_rng(0)).pack_weights() is None
