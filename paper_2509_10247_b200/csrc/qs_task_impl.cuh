@@ -1313,11 +1313,17 @@ __global__ void __launch_bounds__(128) k_task_observe(const qs_task_cfg cfg, con
 template <int M, int TASK, int G>
 __global__ void __launch_bounds__(128) k_task_privileged(const qs_task_cfg cfg, const qs_scene sc,
                                                          const qs_step_io io) {
+  // the CTA's rows are consecutive: their 14 features go out through shared
+  // memory as one contiguous, coalesced block (per-thread 56-byte rows of scalar
+  // stores touched 8x the sectors they wrote)
+  __shared__ float s_out[128 * 14];
   const int na = G == 1 ? 1 : cfg.n_agents;
   const RowMap<G> rm = RowMap<G>::make((long)blockIdx.x * blockDim.x + threadIdx.x, cfg.n_envs, na);
   const Grp<G> grp = Grp<G>::make(na);
-  if (!rm.active || !grp.real) return;
+  const bool contiguous = G == 1;  // one row per thread, rows = global thread ids
+  if (!contiguous && (!rm.active || !grp.real)) return;
   const long e = rm.e, row = rm.row;
+  if (rm.active) {  // (contiguous: every thread reaches the one barrier below)
   const long N = (long)cfg.n_envs * na;
   const DynK k = dyn_consts(cfg);
   const State s = load_state<M>(io.S_out, N, row);
@@ -1337,13 +1343,22 @@ __global__ void __launch_bounds__(128) k_task_privileged(const qs_task_cfg cfg, 
   const float sd = sdf_eval(sv, s.p, code);
   const V3 gd = code ? sdf_grad(sv, s.p, code) : v3(0.f, 0.f, 0.f);
   const V3 a = unrotz(cs, off), b = unrotz(cs, s.v), c = unrotz(cs, th), d = unrotz(cs, gd);
-  float* o = io.obs + row * 14;
+  float* o = contiguous ? s_out + threadIdx.x * 14 : io.obs + row * 14;
   o[0] = a.x; o[1] = a.y; o[2] = a.z;
   o[3] = b.x; o[4] = b.y; o[5] = b.z;
   o[6] = c.x; o[7] = c.y; o[8] = c.z;
   o[9] = clampf(sd, -5.f, 5.f);
   o[10] = d.x; o[11] = d.y; o[12] = d.z;
   o[13] = sqrtf(dot(off, off));
+  }
+  if (!contiguous) return;
+  __syncthreads();
+  {
+    const long NR = (long)cfg.n_envs * na, r0 = (long)blockIdx.x * blockDim.x;
+    const long nrows = NR - r0 < (long)blockDim.x ? NR - r0 : (long)blockDim.x;
+    float* dst = io.obs + r0 * 14;
+    for (int i = threadIdx.x; i < nrows * 14; i += blockDim.x) dst[i] = s_out[i];
+  }
 }
 
 // ---------------------------------------------------------------------------
