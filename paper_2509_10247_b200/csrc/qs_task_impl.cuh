@@ -612,7 +612,7 @@ struct SpawnAhead {
 template <int M, int TASK, int G, bool INLINE, int IMU = 0>
 QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, long row, int na, long N,
                            const Grp<G>& grp, EnvRegs& R, float4 raw, const StepOut& out, int32_t* err,
-                           bool has_dr, bool has_imu, SpawnAhead* ahead = nullptr) {
+                           bool has_dr, bool has_imu, SpawnAhead* ahead = nullptr, float* obs_stage = nullptr) {
   constexpr int A = ModelTraits<M>::A;
   constexpr int P = TaskTraits<M, TASK>::P;
   const DynK k = dyn_consts(cfg);
@@ -814,6 +814,21 @@ QS_D StepStat env_step_fwd(const qs_task_cfg& cfg, const qs_scene& sc, long e, l
         float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
         for (int kk = 0; kk < P / 4; ++kk) d4[kk] = make_float4(o[4 * kk], o[4 * kk + 1], o[4 * kk + 2], o[4 * kk + 3]);
+      } else if (G == 1 && obs_stage) {
+        // rows of P (not a multiple of 4) floats: through this warp's shared
+        // staging buffer, so the warp's consecutive rows leave as one coalesced
+        // run (per-lane scalar rows touched ~8x the sectors they wrote)
+        // the lanes stepping rows are the prefix of the warp with row < N
+        const int lane = threadIdx.x & 31;
+        const long left = N - (row - lane);
+        const unsigned m = left >= 32 ? 0xffffffffu : ((1u << left) - 1u);
+#pragma unroll
+        for (int kk = 0; kk < P; ++kk) obs_stage[lane * P + kk] = o[kk];
+        __syncwarp(m);
+        float* base = out.obs + (row - lane) * P;
+        const int nl = __popc(m), nv = nl * P;  // only the nl stepping lanes copy
+        for (int i = lane; i < nv; i += nl) base[i] = obs_stage[i];
+        __syncwarp(m);  // the buffer is reused by the next step
       } else {
 #pragma unroll
         for (int kk = 0; kk < P; ++kk) dst[kk] = o[kk];
@@ -975,6 +990,8 @@ __global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const q
   const long N = (long)cfg.n_envs * na;
   if (cfg.guard && io.err && io.err[2] != INT_MAX) return;  // rejected by qs_task_validate: mutate nothing
   StepStat st{false, 0, 0.f, 0.f};
+  constexpr int P = TaskTraits<M, TASK>::P;
+  __shared__ float s_obs[4][32 * P];  // per-warp observation staging (128-thread CTA)
   if (rm.active) {
     EnvRegs R;
     const float4 raw = load_act<ModelTraits<M>::A>(io.raw, rm.row);
@@ -983,7 +1000,8 @@ __global__ void __launch_bounds__(128) k_task_fwd(const qs_task_cfg cfg, const q
     StepOut o{io.obs, io.r_ctrl, io.r_goal, io.r_rl, io.terminated, io.truncated, io.flags, io.cam,
               io.imu_out, io.imu_noise};
     st = env_step_fwd<M, TASK, G, INLINE>(cfg, sc, rm.e, rm.row, na, N, grp, R, raw, o, io.err,
-                                          io.dr_in != nullptr, io.imu_out != nullptr);
+                                          io.dr_in != nullptr, io.imu_out != nullptr, nullptr,
+                                          s_obs[threadIdx.x >> 5]);
     if (grp.real) {
       env_store_ckpt<M>(rm.row, N, R, io.S_out, io.goal_out, io.peff_out, io.dr_out);
       env_store_inplace(rm.e, rm.row, grp.g == 0, R, io.meta, io.ep_return, io.imu_out ? io.imu_bias : nullptr);
@@ -1104,6 +1122,8 @@ __global__ void __launch_bounds__(WIN_BLOCK, QS_WIN_MINB) k_window_fwd(const qs_
                 w.r + (long)t * 3 * N + 2 * N, w.terminated + (long)t * N, w.truncated + (long)t * N,
                 w.flags + (long)t * N, nullptr, has_imu ? w.imu_out + (long)t * N * 6 : nullptr,
                 w.imu_noise ? w.imu_noise + (long)t * 4 * N * 3 : nullptr};
+      // (no observation staging here: at C1's 1,024 rows the window is latency-bound
+      // and the staging's warp syncs cost more than the coalescing saves, measured)
       StepStat st = env_step_fwd<M, TASK, G, true, IMU>(cfg, sc, e, row, na, N, grp, R, raw, o, w.err, has_dr,
                                                         has_imu, &ahead);
       if (st.done && grp.g == 0) {
