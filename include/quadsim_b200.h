@@ -286,6 +286,11 @@ int qs_mlp3_fit_grad_tc(int64_t m, int32_t k, const float* x, const float* scale
                         float* gW0, float* gb0, float* gW1, float* gb1, float* gw2, float* gb2, float* loss,
                         float* work, int64_t work_floats, int32_t n_sm, void* stream);
 int64_t qs_mlp3_work_floats(int32_t n_sm);
+/* TD(lambda) targets over a (T, n) window with termination cuts (q/learners.py:78-94):
+ * r, values, done (uint8) are (T, n) row-major, bootstrap (n,); targets (T, n).
+ * one_minus_lam: 1 - lam as the caller rounds it (torch: from double). */
+int qs_td_lambda(int32_t T, int64_t n, const float* r, const float* values, const float* bootstrap,
+                 const uint8_t* done, float gamma, float lam, float one_minus_lam, float* targets, void* stream);
 /* The value MLP's forward only (the TD-lambda targets' values and bootstrap,
  * q/learners.py:286-292) on the same tcgen05 path: pred (m,) fp32, k <= 14. */
 int qs_mlp3_forward_tc(int64_t m, int32_t k, const float* x, const float* scale, const float* W0, const float* b0,

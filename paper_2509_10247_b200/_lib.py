@@ -122,6 +122,7 @@ _SIGS = {
     "qs_mlp3_fit_grad": ([i64, i32] + [vp] * 16 + [i32, vp], i32),
     "qs_mlp3_fit_grad_tc": ([i64, i32] + [vp] * 17 + [i64, i32, vp], i32),
     "qs_mlp3_work_floats": ([i32], i64),
+    "qs_td_lambda": ([i32, i64] + [vp] * 4 + [f32, f32, f32, vp, vp], i32),
     "qs_mlp3_forward_tc": ([i64, i32] + [vp] * 9 + [i32, vp], i32),
     "qs_policy_trunk_fwd": ([i64, i32] + [vp] * 10 + [i32, vp], i32),
     "qs_policy_trunk_bwd": ([i64, i32, vp, vp, vp, i32] + [vp] * 17 + [i64, i32, vp], i32),

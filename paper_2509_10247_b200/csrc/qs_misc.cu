@@ -133,6 +133,30 @@ __global__ void k_philox(int n, const uint32_t* __restrict__ ck, uint32_t* __res
 
 }  // namespace
 
+// TD(lambda) targets with termination cuts (q/learners.py:78-94, the full
+// window): one thread per env walks the window backwards,
+//   G_t = r_t + (gamma cont_t) ((1 - lam) V_{t+1} + lam G_{t+1}),  G_T = V_T = bootstrap,
+// with every multiply / add rounded separately in the order torch evaluates
+// train.td_lambda_targets, and 1 - lam rounded from double as torch's scalar
+// is, so both give the same bits.
+__global__ void k_td_lambda(int T, int64_t N, const float* __restrict__ r, const float* __restrict__ v,
+                            const float* __restrict__ boot, const uint8_t* __restrict__ done, float gamma, float lam,
+                            float oml, float* __restrict__ G) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  const float b = boot[n];
+  float nxt = b;
+  for (int t = T - 1; t >= 0; --t) {
+    const int64_t i = (int64_t)t * N + n;
+    const float v_next = t + 1 < T ? v[i + N] : b;
+    const float cont = done[i] ? 0.f : 1.f;
+    const float mix = __fadd_rn(__fmul_rn(oml, v_next), __fmul_rn(lam, nxt));
+    const float g = __fadd_rn(r[i], __fmul_rn(__fmul_rn(gamma, cont), mix));
+    G[i] = g;
+    nxt = g;
+  }
+}
+
 extern "C" {
 
 int qs_philox4x32_10(int32_t n, const uint32_t* ctr_key, uint32_t* out, void* stream) {
@@ -201,6 +225,15 @@ int qs_dyn_step_bwd(int32_t model, int32_t n, const float* S_in, const float* ac
 int qs_reconstruct_attitude(int32_t n, const float* a, const float* v_ema, float* R, void* stream) {
   if (n <= 0) return QS_OK;
   k_attitude<<<grid_for(n, 128), 128, 0, (cudaStream_t)stream>>>(n, a, v_ema, R);
+  return status();
+}
+
+int qs_td_lambda(int32_t T, int64_t n, const float* r, const float* values, const float* bootstrap,
+                 const uint8_t* done, float gamma, float lam, float one_minus_lam, float* targets, void* stream) {
+  if (T <= 0 || n <= 0) return QS_OK;
+  if (!r || !values || !bootstrap || !done || !targets) return QS_ERR_BAD_ARGUMENT;
+  k_td_lambda<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(T, n, r, values, bootstrap, done, gamma,
+                                                                             lam, one_minus_lam, targets);
   return status();
 }
 

@@ -76,6 +76,20 @@ def td_lambda_targets(r, values, bootstrap, done, gamma, lam, k=None):
     with weights (1-lam) lam^(n-1), the last one taking the remaining
     lam^(steps-1).  The n loop runs over all t at once (k vector steps)."""
     T = r.shape[0]
+    if ((k is None or k >= T) and r.is_cuda and r.dim() == 2 and r.dtype == torch.float32 and
+            values.dtype == torch.float32 and bootstrap.dtype == torch.float32 and done.dtype == torch.bool and
+            not (torch.is_grad_enabled() and (r.requires_grad or values.requires_grad or bootstrap.requires_grad))):
+        # one CUDA kernel (qs_td_lambda): a thread per env walks the window
+        # backwards with the same rounding as the loop below
+        from paper_2509_10247_b200 import _lib as L
+
+        r_, v_, b_ = r.contiguous(), values.contiguous(), bootstrap.contiguous()
+        d_ = done.contiguous().view(torch.uint8)
+        G = torch.empty_like(r_)
+        L.check(L.lib().qs_td_lambda(T, r_.shape[1], L.ptr(r_), L.ptr(v_), L.ptr(b_), L.ptr(d_), float(gamma),
+                                     float(lam), 1.0 - float(lam), L.ptr(G), L.stream_handle(r_.device)),
+                "qs_td_lambda")
+        return G
     cont = 1.0 - done.to(r.dtype)
     if k is None or k >= T:
         G = torch.empty_like(r)

@@ -302,3 +302,21 @@ def test_cuda_graph_trainer_follows_external_resets():
     # (re-derive by stepping an eager twin is overkill; check the state moved on from it)
     assert not torch.equal(env._S, s_after_eval)
     assert np.isfinite(lr.update()["loss"]) and obs0.shape[0] == 1024
+
+
+def test_td_lambda_kernel_matches_torch_loop():
+    """qs_td_lambda (one CUDA kernel, a thread per env) against the torch loop
+    of train.td_lambda_targets on the same fp32 inputs (q/learners.py:78-94):
+    the same rounding order, so the same bits; episode cuts included."""
+    from paper_2509_10247_b200 import train
+
+    g = torch.Generator().manual_seed(3)
+    T, N = 16, 5003
+    r = torch.randn(T, N, generator=g)
+    v = torch.randn(T, N, generator=g)
+    b = torch.randn(N, generator=g)
+    d = torch.rand(T, N, generator=g) < 0.1
+    with torch.no_grad():
+        want = train.td_lambda_targets(r, v, b, d, 0.99, 0.95)  # CPU: the torch loop
+        got = train.td_lambda_targets(r.cuda(), v.cuda(), b.cuda(), d.cuda(), 0.99, 0.95)
+    assert torch.equal(got.cpu(), want), float((got.cpu() - want).abs().max())
