@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(TILED_BLOCK, QS_TILED_MINB) k_raycast_tiled(
 #pragma unroll
     for (int k = 0; k < RPL; ++k) {
       const float4 td = ld4(tile_dirs, (tile * RPL + k) * 32 + lane);
-      ray[k] = (int)td.w;
+      ray[k] = __float_as_int(td.w);  // the ray index's int32 bits (no conversion)
       d[k] = rotz_f(cs, xyz(td));
       best[k] = INF_BITS;
       bestf[k] = INF;

@@ -349,13 +349,12 @@ def _tile_table(sensor, device, width=None):
         cones[k, 9] = float(v[:, 2].min())  # vertical range of the tile's directions
         cones[k, 10] = float(v[:, 2].max())
     # tile-ordered direction table for the kernel: (dir xyz as the fp32 values
-    # of the sensor's ray table, ray index; -1 = empty slot)
+    # of the sensor's ray table, ray index as int32 bits; -1 = empty slot)
     dirs32 = d.astype(np.float32)
     td = np.zeros((len(tiles), width, 4), dtype=np.float32)
-    td[..., 3] = -1.0
     ok = rays >= 0
     td[ok, :3] = dirs32[rays[ok]]
-    td[ok, 3] = rays[ok]
+    td[..., 3] = rays.view(np.float32)  # the int32 ray index bit for bit (-1: empty slot)
     out = (torch.as_tensor(rays, device=device), torch.as_tensor(cones, dtype=torch.float32, device=device),
            torch.as_tensor(td, device=device))
     _TILE_CACHE[key] = out

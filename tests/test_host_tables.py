@@ -24,7 +24,7 @@ def test_tile_tables_bound_their_rays(kind, width):
     dir32 = sn._dir_table(sensor, torch.device("cpu")).numpy()
     ok = rays >= 0
     assert np.array_equal(tdirs[ok][:, :3], dir32[rays[ok], :3])
-    assert np.array_equal(tdirs[..., 3], rays.astype(np.float32))
+    assert np.array_equal(np.ascontiguousarray(tdirs[..., 3]).view(np.int32), rays)  # int32 bits
     got = np.sort(rays[rays >= 0])
     assert np.array_equal(got, np.arange(len(d)))  # a partition of the rays
     for t in range(len(rays)):
