@@ -630,12 +630,31 @@ def bench_c4(dev):
     e1.record()
     torch.cuda.synchronize()
     ms_win = e0.elapsed_time(e1) / 10
+    n_rows = env.N
+    del win, env
+    # closed loop through the env API: the racing task (gates, full quadrotor)
+    # at 16,384 envs, one LiDAR 360x16 sweep / one 64x48 depth frame per step
+    racing = {}
+    for sensor in ("lidar", "depth"):
+        kw = dict(lidar=lidar) if sensor == "lidar" else dict(depth_width=64, depth_height=48)
+        renv = qs.make_task(qs.TaskConfig(task="racing", dynamics="full", n_envs=E, sensor=sensor, **kw),
+                            device=dev, strict=False)
+        renv.reset(seed=3)
+        act = torch.zeros(E, renv.action_dim, device=dev)
+        for _ in range(3):
+            renv.step(act)
+        ms_step = time_graph(lambda: renv.step(act), 20)
+        racing[sensor] = {"ms_per_step": ms_step, "env_steps_per_s": E / (ms_step * 1e-3),
+                          "rays_per_env": renv.obs_spec()["visual"].get("rays") if sensor == "lidar" else 64 * 48}
+        del renv
     return {"indoor_lidar_plus_depth": {"ms_per_frame": ms, "rays_per_s": rays / (ms * 1e-3), "n_envs": E,
                                         "rays_per_env": lidar.n_rays + cam.n_rays},
+            "racing_env_step": {"task": "racing (5 gates), full quadrotor, FlightTask.step + sensor render",
+                                "n_envs": E, **{k: v for k, v in racing.items()}},
             "multi_agent_formation_window": {"task": "position", "envs": 4096, "agents": 4,
                                              "formation": "line, side 1 m", "horizon": 32,
                                              "ms_per_window": ms_win,
-                                             "row_steps_per_s": env.N * 32 / (ms_win * 1e-3)}}
+                                             "row_steps_per_s": n_rows * 32 / (ms_win * 1e-3)}}
 
 
 def bench_c1(dev):
