@@ -1,7 +1,8 @@
 // Deterministic cross-CTA gradient sums.  A persistent gradient kernel writes
 // its CTA's partial sums with plain stores to work[blockIdx.x * P + i]
 // (every CTA writes every entry of the segments below); k_sum_partials then
-// adds the partials to the outputs in CTA order 0, 1, ... -- the same bits
+// adds the partials to the outputs in a fixed order (16 strided slices of the
+// CTAs, combined by a fixed pairwise tree) -- the same bits
 // every run, eager or graph-replayed, unlike float atomics whose order
 // follows the schedule.
 #pragma once
@@ -18,7 +19,7 @@ struct Segs {  // out[s][i] (+)= sum_b work[b * P + off[s] + i], i < len[s]
   bool accumulate;  // add to out (else overwrite)
 };
 
-constexpr int RED_E = 32, RED_S = 8;  // a block: 32 consecutive entries x 8 CTA slices
+constexpr int RED_E = 32, RED_S = 16;  // a block: 32 consecutive entries x 16 CTA slices
 
 static __global__ void __launch_bounds__(RED_E * RED_S)
     k_sum_partials(const float* __restrict__ work, int nblk, int64_t P, Segs s) {
@@ -35,8 +36,15 @@ static __global__ void __launch_bounds__(RED_E * RED_S)
   part[sl][e] = a;
   __syncthreads();
   if (sl == 0 && k < s.n) {
-    const float sum = ((part[0][e] + part[1][e]) + (part[2][e] + part[3][e])) +
-                      ((part[4][e] + part[5][e]) + (part[6][e] + part[7][e]));
+    float q[RED_S];  // a fixed pairwise tree over the slices
+#pragma unroll
+    for (int j = 0; j < RED_S; ++j) q[j] = part[j][e];
+#pragma unroll
+    for (int w = RED_S / 2; w > 0; w >>= 1) {
+#pragma unroll
+      for (int j = 0; j < w; ++j) q[j] = q[2 * j] + q[2 * j + 1];
+    }
+    const float sum = q[0];
     s.out[k][i] = s.accumulate ? s.out[k][i] + sum : sum;
   }
 }
