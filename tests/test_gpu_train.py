@@ -316,7 +316,12 @@ def test_td_lambda_kernel_matches_torch_loop():
     v = torch.randn(T, N, generator=g)
     b = torch.randn(N, generator=g)
     d = torch.rand(T, N, generator=g) < 0.1
+    cases = [(r, v, b, d, 0.99, 0.95),
+             (r[:1], v[:1], b, d[:1], 0.99, 0.95),                        # T = 1: bootstrap only
+             (r, v, b, torch.ones_like(d), 0.97, 0.0),                   # every step cut, lambda = 0
+             (r, v, b, torch.zeros_like(d), 0.9, 1.0)]                   # no cut, lambda = 1
     with torch.no_grad():
-        want = train.td_lambda_targets(r, v, b, d, 0.99, 0.95)  # CPU: the torch loop
-        got = train.td_lambda_targets(r.cuda(), v.cuda(), b.cuda(), d.cuda(), 0.99, 0.95)
-    assert torch.equal(got.cpu(), want), float((got.cpu() - want).abs().max())
+        for rr, vv, bb, dd, gamma, lam in cases:
+            want = train.td_lambda_targets(rr, vv, bb, dd, gamma, lam)  # CPU: the torch loop
+            got = train.td_lambda_targets(rr.cuda(), vv.cuda(), bb.cuda(), dd.cuda(), gamma, lam)
+            assert torch.equal(got.cpu(), want), (gamma, lam, float((got.cpu() - want).abs().max()))
