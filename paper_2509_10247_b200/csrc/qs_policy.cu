@@ -12,15 +12,20 @@
 //                        accumulating every weight and bias gradient in TMEM.
 //   qs_policy_gru_fwd    the GRU cell (q/nets.py:107-132, gates r, z, n) fused
 //                        in front of the trunk: h' and y from (x, h) in one pass
+//                        (k_policy_fwd2: two 8-warp groups, two tiles in flight)
 //   qs_policy_gru_bwd    the GRU cell's backward: recompute the gates, return
 //                        dL/dx and dL/dh for dL/dh' (trunk + carried), and
 //                        accumulate dWi, dWh, dbi, dbh in TMEM.
+//   qs_policy_pack_image the weights as one bf16 operand image every CTA stages
+//                        with bulk copies.
 // Same machinery as the critic fit (qs_mlp.cu / qs_umma.cuh): one persistent
 // 512-thread CTA per SM; thread (warp w, lane l) owns tile row 32 (w % 4) + l
-// -- its TMEM lane -- and a quarter of the 128 columns; one elected thread
-// issues tcgen05.mma (bf16 operands in the blocked no-swizzle layout, fp32
+// -- its TMEM lane -- and a slice of the columns; one elected thread issues
+// tcgen05.mma (bf16 operands in the blocked no-swizzle layout, fp32
 // accumulators in TMEM) and commits to an mbarrier; every weight matrix is
 // staged once and serves as a K-major operand one way and MN-major the other.
+// Weight gradients leave as per-CTA partials summed in a fixed order
+// (qs_reduce.cuh): bitwise reproducible.
 #include "qs_reduce.cuh"
 #include "qs_umma.cuh"
 
